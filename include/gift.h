@@ -1,0 +1,222 @@
+/*
+ * gift.h — C ABI of the B200-native GIFT query path (libgift.so).
+ *
+ * The reference (`/root/reference/pkg`, package `shapesearch`) is pure Python +
+ * numpy and has no FFI layer of its own; its boundary is the Python API in
+ * `shapesearch/index.py` and the module functions it composes.  Every entry
+ * point below replaces one numpy call site of that path and names the
+ * reference function (file:line) whose semantics it reproduces.  The Python
+ * binding a maintainer would add is shown in INTEGRATION.md (ctypes).
+ *
+ * Conventions
+ *   - plain pointers and sizes only; all array pointers are DEVICE pointers
+ *     unless stated otherwise; all buffers are caller-allocated (the library
+ *     never allocates or frees caller memory);
+ *   - `stream` is a cudaStream_t passed as void*; every call is asynchronous
+ *     on that stream unless stated otherwise;
+ *   - every call returns GIFT_OK (0) or an error code; the message of the last
+ *     error on the calling thread is available from gift_last_error();
+ *   - dtype codes: GIFT_F32 = 0, GIFT_F16 = 1, GIFT_F64 = 2.
+ *   - entry points are reentrant given distinct outputs, workspaces and
+ *     streams; there is no hidden global mutable state besides the
+ *     thread-local error message.
+ */
+#ifndef GIFT_H_
+#define GIFT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (mapped onto shapesearch.errors by the Python shim) ---- */
+#define GIFT_OK 0
+#define GIFT_ERR_INVALID 1     /* ValueError                                  */
+#define GIFT_ERR_DIM 2         /* errors.DimensionMismatch  (errors.py:28)    */
+#define GIFT_ERR_EMPTY 3       /* errors.EmptySet           (errors.py:36)    */
+#define GIFT_ERR_CUDA 4        /* CUDA runtime failure                        */
+#define GIFT_ERR_CAPACITY 5    /* workspace too small (size reported)         */
+#define GIFT_ERR_UNSUPPORTED 6 /* shape outside the kernels' supported range  */
+
+#define GIFT_F32 0
+#define GIFT_F16 1
+#define GIFT_F64 2
+
+#define GIFT_SIM_COSINE 0   /* clip(q.p, 0, 1)          matching.py:158      */
+#define GIFT_SIM_GAUSSIAN 1 /* exp(-|q-p|^2 / sigma^2)   north_star (D1)      */
+
+/* Device-resident first inverted file of one shard (cell-major CSR).
+ * Replaces matching.FirstInvertedFile (matching.py:64-103).  Built by the
+ * gift_fif_* build calls below; all pointers are device pointers. */
+typedef struct gift_fif_view {
+  int32_t K;                 /* codebook size                                 */
+  int32_t d;                 /* feature dimension                             */
+  int32_t dtype;             /* storage dtype of feat: GIFT_F32 / GIFT_F16    */
+  int32_t pad0;
+  int64_t n_postings;        /* P                                             */
+  int64_t n_segments;        /* S: (cell, shape) runs                          */
+  int64_t n_tiles;           /* T: scan tiles (whole segments, <= tile_n)     */
+  int64_t n_local;           /* shapes owned by this shard                    */
+  int64_t ord_base;          /* first global ordinal of this shard            */
+  const int64_t* cell_off;   /* [K+1] posting offsets per cell                */
+  const int32_t* post_ord;   /* [P] global shape ordinal per posting          */
+  const void* feat;          /* [P, d] stored view features, cell-major       */
+  const float* pnorm2;       /* [P] |p|^2 (gaussian mode)                     */
+  const int64_t* seg_off;    /* [K+1] segment offsets per cell                */
+  const int32_t* seg_ord;    /* [S] shape ordinal of each segment             */
+  const int32_t* seg_pstart; /* [S+1] first posting of each segment           */
+  const int64_t* tile_off;   /* [K+1] tile offsets per cell                   */
+  const int32_t* tile_pstart;/* [T]                                           */
+  const int32_t* tile_pend;  /* [T]                                           */
+  const int32_t* tile_seg0;  /* [T] first segment overlapping the tile        */
+  const int32_t* tile_seg1;  /* [T] one past the last                         */
+  const float* centroids;    /* [K, d] f32 codebook (codebook.py:22-34)       */
+  const double* cnorm2;      /* [K] |c|^2 in f64                              */
+  double cmax_norm;          /* max_c |c|                                     */
+} gift_fif_view;
+
+/* ---- library ---- */
+int gift_version(void);
+int gift_last_error(char* buf, size_t len);
+int gift_fif_tile_n(void); /* posting-tile height of the scan kernel */
+
+/* ---- K1 quantize: replaces codebook.quantize (codebook.py:111-124) ----
+ * For each of n vectors X[i] (dtype f32/f16/f64, row-major [n, d]) writes the
+ * ma nearest centroids, ascending by the reference's f64 direct-difference
+ * squared distance (numpy pairwise summation order), ties to the lower index.
+ * Bit-exact with the reference.  If nz != NULL, rows with nz[i] == 0 get
+ * out_idx = -1 (query_fif skips zero views, matching.py:150-151); if
+ * zero_key >= 0 such rows get zero_key instead (F-IF build sort key).
+ * Workspace: at least gift_quantize_ws_bytes(128, d, K, xdtype); larger
+ * workspaces process more rows per pass. */
+size_t gift_quantize_ws_bytes(int64_t n, int32_t d, int32_t K, int32_t xdtype);
+int gift_quantize(const void* X, int32_t xdtype, int64_t n, int32_t d,
+                  const float* C, const double* cnorm2, int32_t K,
+                  double cmax_norm, int32_t ma, const uint8_t* nz,
+                  int32_t zero_key, int32_t* out_idx, void* ws,
+                  size_t ws_bytes, void* stream);
+
+/* Per-view non-zero flag and |x|^2 (f64 accumulate, stored f32).
+ * `row.any()` tests of matching.py:121 / :150. */
+int gift_view_prep(const void* X, int32_t xdtype, int64_t nviews, int32_t d,
+                   uint8_t* out_nz, float* out_norm2, void* stream);
+
+/* ---- K2 support: stable LSD radix sort of (u32 key, u32 value) pairs ----
+ * Sorted result is left in keys/vals.  Stable: equal keys keep input order
+ * (the reference appends postings in shape-major, view-minor order,
+ * matching.py:112-125, and activations in owner order, rerank.py:194-198). */
+size_t gift_radix_sort_ws_bytes(int64_t n);
+int gift_radix_sort_pairs(uint32_t* keys, uint32_t* vals, int64_t n,
+                          int32_t key_bits, uint32_t* keys_tmp,
+                          uint32_t* vals_tmp, void* ws, size_t ws_bytes,
+                          void* stream);
+/* out_off[b] = first position of key b in a sorted key array, b in [0, nb]. */
+int gift_offsets_from_sorted(const uint32_t* keys, int64_t n, int64_t nbuckets,
+                             int64_t* out_off, void* stream);
+
+/* ---- K2 F-IF build: replaces matching.build_fif (matching.py:106-133) ----
+ * gather: out_feat[p] = src[perm[p]] (rows of d), out_ord[p] = ord_base +
+ * perm[p] / V, out_pnorm2[p] = |src[perm[p]]|^2. */
+int gift_fif_gather(const void* src, int32_t dtype, int32_t d, int32_t V,
+                    const uint32_t* perm, int64_t P, int64_t ord_base,
+                    void* out_feat, int32_t* out_ord, float* out_pnorm2,
+                    void* stream);
+/* Segments = maximal runs of one shape inside one cell.  Two passes: with
+ * seg_ord == NULL only seg_off[K+1] is written (read seg_off[K] = S), then
+ * call again with seg_ord/seg_pstart allocated ([S], [S+1]). */
+size_t gift_fif_build_ws_bytes(int64_t P, int32_t K);
+int gift_fif_segments(const int64_t* cell_off, const int32_t* post_ord,
+                      int32_t K, int64_t P, int64_t* seg_off, int32_t* seg_ord,
+                      int32_t* seg_pstart, void* ws, size_t ws_bytes,
+                      void* stream);
+/* Scan tiles: greedy packing of whole segments into tiles of <= tile_n
+ * postings (segments longer than tile_n are split).  Two passes as above. */
+int gift_fif_tiles(const int64_t* cell_off, const int64_t* seg_off,
+                   const int32_t* seg_pstart, int32_t K, int32_t tile_n,
+                   int64_t* tile_off, int32_t* tile_pstart, int32_t* tile_pend,
+                   int32_t* tile_seg0, int32_t* tile_seg1, void* ws,
+                   size_t ws_bytes, void* stream);
+/* out[i] = src[idx[i]] widened to f32 (query_by_id's shape_matrix,
+ * matching.py:94-103, index.py:302-314). */
+int gift_gather_rows_f32(const void* src, int32_t dtype, int32_t d,
+                         const int64_t* idx, int64_t n, float* out,
+                         void* stream);
+
+/* ---- K3 F-IF score: replaces matching.query_fif (matching.py:136-161) ----
+ * Batched: Q is [B*V, d] f32 (B queries of V views).  Writes dense f64
+ * scores [B, n_local] for the shard's shapes: mean over the query's views of
+ * the best similarity among postings of the view's ma nearest cells; never
+ * visited shapes score exactly 0.  vq (nullable) overrides the per-query
+ * divisor (default V).  Workspace layout is internal; the first 64 bytes hold
+ * int64 status words: [0] work items, [1] compact outputs needed,
+ * [2] overflow flag (1 = workspace too small: grow to
+ * gift_fif_score_ws_bytes(.., needed) and rerun). */
+size_t gift_fif_score_ws_bytes(const gift_fif_view* f, int32_t B, int32_t V,
+                               int32_t ma, int64_t compact_capacity);
+int gift_fif_score(const gift_fif_view* f, const float* Q, int32_t B,
+                   int32_t V, const int32_t* vq, int32_t ma, int32_t mode,
+                   double sigma, double* out_scores, void* ws,
+                   size_t ws_bytes, void* stream);
+
+/* ---- K4 top-k: replaces the lexsort selections rerank.py:74, :86-87 and
+ * index.py:290-294.  Per row of a dense f64 score matrix [B, n], returns the
+ * k best by (score desc, tiebreak asc) where tiebreak(j) = 0 if
+ * j == self_local[b] else 1 + (idrank ? idrank[j] : ord_base + j).  Output
+ * global ordinals (ord_base + j); with positive_only, entries scoring <= 0
+ * are reported as -1.  k <= 2048. */
+int gift_topk_rows(const double* scores, int32_t B, int64_t n, int32_t k,
+                   const int32_t* idrank, const int32_t* self_local,
+                   int64_t ord_base, int32_t positive_only, int32_t* out_idx,
+                   double* out_val, void* stream);
+
+/* ---- K5 activations (fixed-capacity rows: idx[B,cap] asc, val, cnt, norm) */
+/* build_activation (rerank.py:64-75) from a top-k result: first k1 positive
+ * entries, re-sorted by ordinal, norm = sequential ascending sum. */
+int gift_act_from_topk(const int32_t* topk_idx, const double* topk_val,
+                       int32_t B, int32_t kk, int32_t k1, int32_t cap,
+                       int32_t* act_idx, double* act_val, int32_t* act_cnt,
+                       double* act_norm, void* stream);
+/* mean_activation (rerank.py:90-100): out[b] = mean of raw[nbr[b, t]] over
+ * the valid (>= 0) neighbours t, accumulated in neighbour order. */
+int gift_act_mean(const int32_t* raw_idx, const double* raw_val,
+                  const int32_t* raw_cnt, int32_t raw_cap, const int32_t* nbr,
+                  int32_t B, int32_t k2, int32_t cap, int32_t* out_idx,
+                  double* out_val, int32_t* out_cnt, double* out_norm,
+                  void* stream);
+/* aggregate (rerank.py:128-147): generalized mean over the union support. */
+int gift_act_aggregate(const int32_t* a_idx, const double* a_val,
+                       const int32_t* a_cnt, int32_t a_cap,
+                       const int32_t* b_idx, const double* b_val,
+                       const int32_t* b_cnt, int32_t b_cap, int32_t B,
+                       double alpha, int32_t cap, int32_t* out_idx,
+                       double* out_val, int32_t* out_cnt, double* out_norm,
+                       void* stream);
+
+/* ---- K5/K6 S-IF: replaces rerank.build_sif / query_sif (rerank.py:187-230)
+ * compact: rows [0, nrows) of an activation matrix -> (key = coordinate,
+ * value = position) pairs in row-major order plus owner/value per position;
+ * row_off[nrows+1] is written (exclusive scan of cnt). */
+int gift_act_compact(const int32_t* act_idx, const double* act_val,
+                     const int32_t* act_cnt, int32_t cap, int64_t nrows,
+                     int64_t* row_off, uint32_t* out_key, uint32_t* out_pos,
+                     int32_t* out_owner, double* out_val, void* ws,
+                     size_t ws_bytes, void* stream);
+/* permute: e_ord[q] = owner[pos[q]], e_val[q] = val[pos[q]]. */
+int gift_sif_permute(const uint32_t* pos, const int32_t* owner,
+                     const double* val, int64_t nnz, int32_t* e_ord,
+                     double* e_val, void* stream);
+/* Dense re-ranked scores [B, n_local]: acc_j accumulates min(Fq[i], F_j[i])
+ * over the query support in ascending i (f64, sequential per j), then
+ * S' = acc / ((|Fq|_1 + |F_j|_1) - acc) on touched shapes, 0 elsewhere. */
+int gift_sif_query(const int64_t* e_off, const int32_t* e_ord,
+                   const double* e_val, const double* norms, int64_t n_global,
+                   int64_t n_local, const int32_t* q_idx, const double* q_val,
+                   const int32_t* q_cnt, const double* q_norm, int32_t B,
+                   int32_t cap, double* out_scores, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GIFT_H_ */

@@ -1,0 +1,37 @@
+"""B200-native GIFT query path (arXiv 1604.01879): F-IF multi-view matching
+followed by S-IF context re-ranking, on hand-written sm_100a kernels
+(libgift.so, include/gift.h).
+
+Drop-in for the reference package `shapesearch` on that path: the public API
+(`__init__.py:9-29` of the reference) keeps its names and semantics.
+"""
+
+from .index import (
+    IndexBundle,
+    IndexConfig,
+    build_index,
+    build_index_from_views,
+    load_bundle,
+    query,
+    query_batch,
+    query_by_id,
+    query_many,
+    rerank_scores,
+    save_bundle,
+)
+
+__all__ = [
+    "IndexBundle",
+    "IndexConfig",
+    "build_index",
+    "build_index_from_views",
+    "load_bundle",
+    "query",
+    "query_batch",
+    "query_by_id",
+    "query_many",
+    "rerank_scores",
+    "save_bundle",
+]
+
+__version__ = "0.1.0"

@@ -1,0 +1,172 @@
+"""ctypes binding of libgift.so (include/gift.h) and torch plumbing helpers.
+
+The library is the product path: every numeric step of the GIFT query path
+runs in its sm_100a kernels.  There is no CPU fallback — if the library or a
+CUDA device is missing, `lib()` raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+from . import errors
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgift.so")
+
+GIFT_F32, GIFT_F16, GIFT_F64 = 0, 1, 2
+SIM_COSINE, SIM_GAUSSIAN = 0, 1
+
+_c_i32 = ctypes.c_int32
+_c_i64 = ctypes.c_int64
+_c_sz = ctypes.c_size_t
+_c_dbl = ctypes.c_double
+_c_p = ctypes.c_void_p
+
+
+class FifView(ctypes.Structure):
+    """Mirror of `gift_fif_view` (include/gift.h)."""
+    _fields_ = [
+        ("K", _c_i32), ("d", _c_i32), ("dtype", _c_i32), ("pad0", _c_i32),
+        ("n_postings", _c_i64), ("n_segments", _c_i64), ("n_tiles", _c_i64),
+        ("n_local", _c_i64), ("ord_base", _c_i64),
+        ("cell_off", _c_p), ("post_ord", _c_p), ("feat", _c_p), ("pnorm2", _c_p),
+        ("seg_off", _c_p), ("seg_ord", _c_p), ("seg_pstart", _c_p),
+        ("tile_off", _c_p), ("tile_pstart", _c_p), ("tile_pend", _c_p),
+        ("tile_seg0", _c_p), ("tile_seg1", _c_p),
+        ("centroids", _c_p), ("cnorm2", _c_p), ("cmax_norm", _c_dbl),
+    ]
+
+
+_SIGS = {
+    "gift_version": (_c_i32, []),
+    "gift_last_error": (_c_i32, [ctypes.c_char_p, _c_sz]),
+    "gift_fif_tile_n": (_c_i32, []),
+    "gift_quantize_ws_bytes": (_c_sz, [_c_i64, _c_i32, _c_i32, _c_i32]),
+    "gift_quantize": (_c_i32, [_c_p, _c_i32, _c_i64, _c_i32, _c_p, _c_p, _c_i32, _c_dbl, _c_i32,
+                               _c_p, _c_i32, _c_p, _c_p, _c_sz, _c_p]),
+    "gift_view_prep": (_c_i32, [_c_p, _c_i32, _c_i64, _c_i32, _c_p, _c_p, _c_p]),
+    "gift_radix_sort_ws_bytes": (_c_sz, [_c_i64]),
+    "gift_radix_sort_pairs": (_c_i32, [_c_p, _c_p, _c_i64, _c_i32, _c_p, _c_p, _c_p, _c_sz, _c_p]),
+    "gift_offsets_from_sorted": (_c_i32, [_c_p, _c_i64, _c_i64, _c_p, _c_p]),
+    "gift_fif_gather": (_c_i32, [_c_p, _c_i32, _c_i32, _c_i32, _c_p, _c_i64, _c_i64, _c_p, _c_p,
+                                 _c_p, _c_p]),
+    "gift_fif_build_ws_bytes": (_c_sz, [_c_i64, _c_i32]),
+    "gift_fif_segments": (_c_i32, [_c_p, _c_p, _c_i32, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_sz,
+                                   _c_p]),
+    "gift_fif_tiles": (_c_i32, [_c_p, _c_p, _c_p, _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_p,
+                                _c_p, _c_sz, _c_p]),
+    "gift_gather_rows_f32": (_c_i32, [_c_p, _c_i32, _c_i32, _c_p, _c_i64, _c_p, _c_p]),
+    "gift_fif_score_ws_bytes": (_c_sz, [ctypes.POINTER(FifView), _c_i32, _c_i32, _c_i32, _c_i64]),
+    "gift_fif_score": (_c_i32, [ctypes.POINTER(FifView), _c_p, _c_i32, _c_i32, _c_p, _c_i32,
+                                _c_i32, _c_dbl, _c_p, _c_p, _c_sz, _c_p]),
+    "gift_topk_rows": (_c_i32, [_c_p, _c_i32, _c_i64, _c_i32, _c_p, _c_p, _c_i64, _c_i32, _c_p,
+                                _c_p, _c_p]),
+    "gift_act_from_topk": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_p, _c_p,
+                                    _c_p, _c_p]),
+    "gift_act_mean": (_c_i32, [_c_p, _c_p, _c_p, _c_i32, _c_p, _c_i32, _c_i32, _c_i32, _c_p, _c_p,
+                               _c_p, _c_p, _c_p]),
+    "gift_act_aggregate": (_c_i32, [_c_p, _c_p, _c_p, _c_i32, _c_p, _c_p, _c_p, _c_i32, _c_i32,
+                                    _c_dbl, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_p]),
+    "gift_act_compact": (_c_i32, [_c_p, _c_p, _c_p, _c_i32, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p,
+                                  _c_p, _c_sz, _c_p]),
+    "gift_sif_permute": (_c_i32, [_c_p, _c_p, _c_p, _c_i64, _c_p, _c_p, _c_p]),
+    "gift_sif_query": (_c_i32, [_c_p, _c_p, _c_p, _c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p,
+                                _c_i32, _c_i32, _c_p, _c_p]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libgift.so and bind every entry point (no GPU needed)."""
+    if not os.path.exists(path):
+        raise errors.NativeUnavailable(
+            f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+def lib() -> ctypes.CDLL:
+    """The loaded library; requires a CUDA device (no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not torch.cuda.is_available():
+                    raise errors.NativeUnavailable(
+                        "no CUDA device: the GIFT path runs only on the sm_100a kernels")
+                _lib = load_library()
+    return _lib
+
+
+def last_error() -> str:
+    buf = ctypes.create_string_buffer(1024)
+    lib().gift_last_error(buf, 1024)
+    return buf.value.decode("utf-8", "replace")
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == 0:
+        return
+    msg = f"{what}: {last_error()}" if what else last_error()
+    raise errors.from_status(rc, msg)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(lib(), name)(*args), name)
+
+
+def ptr(t) -> int | None:
+    """Device (or host) address of a tensor, None for None."""
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def stream_ptr(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def device() -> torch.device:
+    lib()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+class Workspace:
+    """Grow-only per-stream scratch buffer (caller-owned memory for the ABI)."""
+
+    def __init__(self):
+        self._buf = None
+
+    def get(self, nbytes: int) -> torch.Tensor:
+        nbytes = max(int(nbytes), 256)
+        if self._buf is None or self._buf.numel() < nbytes:
+            self._buf = None
+            self._buf = torch.empty(nbytes, dtype=torch.uint8, device=device())
+        return self._buf
+
+
+_ws_local = threading.local()
+
+
+def workspace(slot: str = "default") -> Workspace:
+    d = getattr(_ws_local, "pool", None)
+    if d is None:
+        d = _ws_local.pool = {}
+    ws = d.get(slot)
+    if ws is None:
+        ws = d[slot] = Workspace()
+    return ws

@@ -1,0 +1,320 @@
+// K5/K6 — sparse neighbour activations and the second inverted file.
+// Replaces shapesearch.rerank (rerank.py:24-230).  Activations are kept in a
+// fixed-capacity row format: idx[B, cap] (strictly ascending, -1 padded),
+// val[B, cap] (f64 > 0), cnt[B], norm[B] (sequential ascending-coordinate f64
+// sum, rerank.py:24-31, so a self-query's S-IF accumulator is bit-equal to
+// the cached norm and scores exactly 1.0).
+#include "gift_common.cuh"
+
+namespace gift {
+
+constexpr int MAX_NBR = 64;
+
+__device__ __forceinline__ double seq_norm(const double* v, int n) {
+  double t = 0.0;
+  for (int i = 0; i < n; ++i) t = __dadd_rn(t, v[i]);
+  return t;
+}
+
+// build_activation (rerank.py:64-75) + make_activation (:51-61): the first k1
+// entries of a best-first top-k row that are present (idx >= 0, value > 0),
+// re-ordered by ascending ordinal.  One warp per row.
+__global__ void act_from_topk_kernel(const int32_t* __restrict__ tk_idx,
+                                     const double* __restrict__ tk_val, int B, int kk, int k1,
+                                     int cap, int32_t* __restrict__ a_idx,
+                                     double* __restrict__ a_val, int32_t* __restrict__ a_cnt,
+                                     double* __restrict__ a_norm) {
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (b >= B) return;
+  const int lim = min(k1, kk);
+  const int32_t* ti = tk_idx + b * kk;
+  const double* tv = tk_val + b * kk;
+  int n = 0;
+  for (int i = 0; i < lim; ++i) n += (ti[i] >= 0 && tv[i] > 0.0) ? 1 : 0;
+  int32_t* oi = a_idx + b * cap;
+  double* ov = a_val + b * cap;
+  for (int i = lane; i < cap; i += 32) {
+    oi[i] = -1;
+    ov[i] = 0.0;
+  }
+  __syncwarp();
+  for (int i = lane; i < lim; i += 32) {
+    const int32_t x = ti[i];
+    if (x < 0 || !(tv[i] > 0.0)) continue;
+    int rank = 0;
+    for (int m = 0; m < lim; ++m) {
+      const int32_t y = ti[m];
+      if (y >= 0 && tv[m] > 0.0 && y < x) ++rank;
+    }
+    oi[rank] = x;
+    ov[rank] = tv[i];
+  }
+  __syncwarp();
+  if (lane == 0) {
+    a_cnt[b] = n;
+    a_norm[b] = seq_norm(ov, n);
+  }
+}
+
+// mean_activation (rerank.py:90-100): dict accumulation in neighbour order,
+// coordinates sorted, divided by len(neighbor_list).  One thread per row.
+__global__ void act_mean_kernel(const int32_t* __restrict__ raw_idx,
+                                const double* __restrict__ raw_val,
+                                const int32_t* __restrict__ raw_cnt, int raw_cap,
+                                const int32_t* __restrict__ nbr, int B, int k2, int cap,
+                                int32_t* __restrict__ o_idx, double* __restrict__ o_val,
+                                int32_t* __restrict__ o_cnt, double* __restrict__ o_norm) {
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  int list[MAX_NBR];
+  int head[MAX_NBR];
+  int len[MAX_NBR];
+  int nl = 0;
+  for (int t = 0; t < k2; ++t) {
+    const int q = nbr[b * k2 + t];
+    if (q < 0) continue;
+    list[nl] = q;
+    head[nl] = 0;
+    len[nl] = raw_cnt[q];
+    ++nl;
+  }
+  int32_t* oi = o_idx + b * cap;
+  double* ov = o_val + b * cap;
+  int n = 0;
+  if (nl > 0) {
+    const double count = static_cast<double>(nl);
+    for (;;) {
+      int mn = 0x7fffffff;
+      for (int t = 0; t < nl; ++t)
+        if (head[t] < len[t]) mn = min(mn, raw_idx[static_cast<int64_t>(list[t]) * raw_cap + head[t]]);
+      if (mn == 0x7fffffff) break;
+      double acc = 0.0;
+      bool first = true;
+      for (int t = 0; t < nl; ++t) {
+        if (head[t] < len[t]) {
+          const int64_t at = static_cast<int64_t>(list[t]) * raw_cap + head[t];
+          if (raw_idx[at] == mn) {
+            acc = first ? __dadd_rn(0.0, raw_val[at]) : __dadd_rn(acc, raw_val[at]);
+            first = false;
+            ++head[t];
+          }
+        }
+      }
+      const double v = __ddiv_rn(acc, count);
+      if (v > 0.0 && n < cap) {
+        oi[n] = mn;
+        ov[n] = v;
+        ++n;
+      }
+    }
+  }
+  for (int i = n; i < cap; ++i) {
+    oi[i] = -1;
+    ov[i] = 0.0;
+  }
+  o_cnt[b] = n;
+  o_norm[b] = seq_norm(ov, n);
+}
+
+__device__ __forceinline__ double np_power_scalar(double v, double e) {
+  // numpy: np.power(v, a) (libm pow) and ndarray ** e (fast paths for
+  // e in {0.5, 1, 2}); the fast paths are exact/correctly rounded.
+  if (e == 1.0) return v;
+  if (e == 2.0) return __dmul_rn(v, v);
+  if (e == 0.5) return __dsqrt_rn(v);
+  return pow(v, e);
+}
+
+// aggregate (rerank.py:128-147): union support, equal values pass through.
+__global__ void act_aggregate_kernel(const int32_t* __restrict__ ai, const double* __restrict__ av,
+                                     const int32_t* __restrict__ ac, int acap,
+                                     const int32_t* __restrict__ bi, const double* __restrict__ bv,
+                                     const int32_t* __restrict__ bc, int bcap, int B, double alpha,
+                                     int cap, int32_t* __restrict__ oi, double* __restrict__ ov,
+                                     int32_t* __restrict__ oc, double* __restrict__ on) {
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int32_t* x = ai + b * acap;
+  const double* xv = av + b * acap;
+  const int32_t* y = bi + b * bcap;
+  const double* yv = bv + b * bcap;
+  const int nx = ac[b], ny = bc[b];
+  int32_t* o = oi + b * cap;
+  double* w = ov + b * cap;
+  const double inv = 1.0 / alpha;
+  int i = 0, j = 0, n = 0;
+  while (i < nx || j < ny) {
+    int idx;
+    double v1 = 0.0, v2 = 0.0;
+    if (j >= ny || (i < nx && x[i] < y[j])) {
+      idx = x[i];
+      v1 = xv[i++];
+    } else if (i >= nx || y[j] < x[i]) {
+      idx = y[j];
+      v2 = yv[j++];
+    } else {
+      idx = x[i];
+      v1 = xv[i++];
+      v2 = yv[j++];
+    }
+    double r;
+    if (v1 == v2) {
+      r = v1;
+    } else {
+      const double s = __dadd_rn(np_power_scalar(v1, alpha), np_power_scalar(v2, alpha));
+      r = np_power_scalar(__ddiv_rn(s, 2.0), inv);
+    }
+    if (r > 0.0 && n < cap) {
+      o[n] = idx;
+      w[n] = r;
+      ++n;
+    }
+  }
+  for (int k = n; k < cap; ++k) {
+    o[k] = -1;
+    w[k] = 0.0;
+  }
+  oc[b] = n;
+  on[b] = seq_norm(w, n);
+}
+
+__global__ void act_compact_kernel(const int32_t* __restrict__ idx, const double* __restrict__ val,
+                                   const int32_t* __restrict__ cnt, int cap, int64_t nrows,
+                                   const int64_t* __restrict__ row_off, uint32_t* __restrict__ key,
+                                   uint32_t* __restrict__ pos, int32_t* __restrict__ owner,
+                                   double* __restrict__ oval) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= nrows) return;
+  const int64_t base = row_off[r];
+  for (int e = 0; e < cnt[r]; ++e) {
+    key[base + e] = static_cast<uint32_t>(idx[r * cap + e]);
+    pos[base + e] = static_cast<uint32_t>(base + e);
+    owner[base + e] = static_cast<int32_t>(r);
+    oval[base + e] = val[r * cap + e];
+  }
+}
+
+__global__ void sif_permute_kernel(const uint32_t* __restrict__ pos, const int32_t* __restrict__ owner,
+                                   const double* __restrict__ val, int64_t nnz,
+                                   int32_t* __restrict__ e_ord, double* __restrict__ e_val) {
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= nnz) return;
+  const uint32_t p = pos[q];
+  e_ord[q] = owner[p];
+  e_val[q] = val[p];
+}
+
+// query_sif (rerank.py:211-230) for a batch: one CTA per query; the dense
+// output row doubles as the accumulator.  Entries are visited in ascending
+// coordinate order with a barrier between entries, so every acc[j] is the
+// same left-to-right f64 sum as the reference's acc[ords] += min(...).
+__global__ void __launch_bounds__(256)
+    sif_query_kernel(const int64_t* __restrict__ e_off, const int32_t* __restrict__ e_ord,
+                     const double* __restrict__ e_val, const double* __restrict__ norms,
+                     int64_t n_global, int64_t n_local, const int32_t* __restrict__ q_idx,
+                     const double* __restrict__ q_val, const int32_t* __restrict__ q_cnt,
+                     const double* __restrict__ q_norm, int cap, double* __restrict__ out) {
+  const int b = blockIdx.x;
+  double* row = out + static_cast<int64_t>(b) * n_local;
+  for (int64_t j = threadIdx.x; j < n_local; j += blockDim.x) row[j] = 0.0;
+  __syncthreads();
+  const int cnt = q_cnt[b];
+  for (int e = 0; e < cnt; ++e) {
+    const int64_t i = q_idx[static_cast<int64_t>(b) * cap + e];
+    if (i < 0 || i >= n_global) continue;
+    const double v = q_val[static_cast<int64_t>(b) * cap + e];
+    const int64_t p0 = e_off[i], p1 = e_off[i + 1];
+    for (int64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+      const int32_t j = e_ord[p];
+      row[j] = __dadd_rn(row[j], fmin(v, e_val[p]));
+    }
+    __syncthreads();
+  }
+  const double qn = q_norm[b];
+  for (int64_t j = threadIdx.x; j < n_local; j += blockDim.x) {
+    const double acc = row[j];
+    if (acc > 0.0) row[j] = __ddiv_rn(acc, __dsub_rn(__dadd_rn(qn, norms[j]), acc));
+  }
+}
+
+}  // namespace gift
+
+using namespace gift;
+
+extern "C" int gift_act_from_topk(const int32_t* topk_idx, const double* topk_val, int32_t B,
+                                  int32_t kk, int32_t k1, int32_t cap, int32_t* act_idx,
+                                  double* act_val, int32_t* act_cnt, double* act_norm,
+                                  void* stream) {
+  GIFT_REQUIRE(k1 >= 1, GIFT_ERR_INVALID, "k1 must be >= 1");
+  GIFT_REQUIRE(cap >= min(k1, kk), GIFT_ERR_CAPACITY, "activation capacity too small");
+  if (B <= 0) return GIFT_OK;
+  act_from_topk_kernel<<<static_cast<unsigned>(cdiv(B, 4)), 128, 0, as_stream(stream)>>>(
+      topk_idx, topk_val, B, kk, k1, cap, act_idx, act_val, act_cnt, act_norm);
+  GIFT_LAUNCH_CHECK();
+  return GIFT_OK;
+}
+
+extern "C" int gift_act_mean(const int32_t* raw_idx, const double* raw_val, const int32_t* raw_cnt,
+                             int32_t raw_cap, const int32_t* nbr, int32_t B, int32_t k2,
+                             int32_t cap, int32_t* out_idx, double* out_val, int32_t* out_cnt,
+                             double* out_norm, void* stream) {
+  GIFT_REQUIRE(k2 >= 0 && k2 <= MAX_NBR, GIFT_ERR_UNSUPPORTED, "k2 = %d > %d", k2, MAX_NBR);
+  GIFT_REQUIRE(cap >= raw_cap * k2, GIFT_ERR_CAPACITY, "activation capacity too small");
+  if (B <= 0) return GIFT_OK;
+  act_mean_kernel<<<static_cast<unsigned>(cdiv(B, 128)), 128, 0, as_stream(stream)>>>(
+      raw_idx, raw_val, raw_cnt, raw_cap, nbr, B, k2, cap, out_idx, out_val, out_cnt, out_norm);
+  GIFT_LAUNCH_CHECK();
+  return GIFT_OK;
+}
+
+extern "C" int gift_act_aggregate(const int32_t* a_idx, const double* a_val, const int32_t* a_cnt,
+                                  int32_t a_cap, const int32_t* b_idx, const double* b_val,
+                                  const int32_t* b_cnt, int32_t b_cap, int32_t B, double alpha,
+                                  int32_t cap, int32_t* out_idx, double* out_val, int32_t* out_cnt,
+                                  double* out_norm, void* stream) {
+  GIFT_REQUIRE(alpha > 0.0, GIFT_ERR_INVALID, "alpha must be > 0");
+  GIFT_REQUIRE(cap >= a_cap + b_cap, GIFT_ERR_CAPACITY, "aggregate capacity must be >= a_cap + b_cap");
+  if (B <= 0) return GIFT_OK;
+  act_aggregate_kernel<<<static_cast<unsigned>(cdiv(B, 128)), 128, 0, as_stream(stream)>>>(
+      a_idx, a_val, a_cnt, a_cap, b_idx, b_val, b_cnt, b_cap, B, alpha, cap, out_idx, out_val,
+      out_cnt, out_norm);
+  GIFT_LAUNCH_CHECK();
+  return GIFT_OK;
+}
+
+extern "C" int gift_act_compact(const int32_t* act_idx, const double* act_val,
+                                const int32_t* act_cnt, int32_t cap, int64_t nrows,
+                                int64_t* row_off, uint32_t* out_key, uint32_t* out_pos,
+                                int32_t* out_owner, double* out_val, void* ws, size_t ws_bytes,
+                                void* stream) {
+  cudaStream_t st = as_stream(stream);
+  int rc = scan_exclusive_i32_to_i64(act_cnt, row_off, nrows, true, ws, ws_bytes, st);
+  if (rc != GIFT_OK) return rc;
+  if (nrows <= 0 || out_key == nullptr) return GIFT_OK;
+  act_compact_kernel<<<static_cast<unsigned>(cdiv(nrows, 128)), 128, 0, st>>>(
+      act_idx, act_val, act_cnt, cap, nrows, row_off, out_key, out_pos, out_owner, out_val);
+  GIFT_LAUNCH_CHECK();
+  return GIFT_OK;
+}
+
+extern "C" int gift_sif_permute(const uint32_t* pos, const int32_t* owner, const double* val,
+                                int64_t nnz, int32_t* e_ord, double* e_val, void* stream) {
+  if (nnz <= 0) return GIFT_OK;
+  sif_permute_kernel<<<static_cast<unsigned>(cdiv(nnz, 256)), 256, 0, as_stream(stream)>>>(
+      pos, owner, val, nnz, e_ord, e_val);
+  GIFT_LAUNCH_CHECK();
+  return GIFT_OK;
+}
+
+extern "C" int gift_sif_query(const int64_t* e_off, const int32_t* e_ord, const double* e_val,
+                              const double* norms, int64_t n_global, int64_t n_local,
+                              const int32_t* q_idx, const double* q_val, const int32_t* q_cnt,
+                              const double* q_norm, int32_t B, int32_t cap, double* out_scores,
+                              void* stream) {
+  if (B <= 0 || n_local <= 0) return GIFT_OK;
+  sif_query_kernel<<<static_cast<unsigned>(B), 256, 0, as_stream(stream)>>>(
+      e_off, e_ord, e_val, norms, n_global, n_local, q_idx, q_val, q_cnt, q_norm, cap, out_scores);
+  GIFT_LAUNCH_CHECK();
+  return GIFT_OK;
+}

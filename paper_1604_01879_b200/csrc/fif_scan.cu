@@ -1,0 +1,493 @@
+// K3 F-IF score — replaces shapesearch.matching.query_fif (matching.py:136-161)
+// for a whole batch of queries at once.
+//
+// Reference (per query, per non-zero view q_i):
+//   view_best[p] = max over the postings of shape p stored in the ma nearest
+//                  cells of q_i of clip(q_i . f, 0, 1)            (:152-159)
+//   total += view_best ; score = total / Vq                       (:160-161)
+//
+// Batched, cell-major plan (one pass over each probed cell per batch):
+//   plan   : every (query view, ma slot) probe is bucketed by cell;
+//   scan   : persistent CTAs take work items (posting tile of a cell x tile of
+//            that cell's probes), compute the posting x probe dot tile on the
+//            CUDA-core mainloop, and reduce each (cell, shape) segment of the
+//            tile to its maximum similarity -> compact[cell][probe][segment];
+//   reduce : per (query, range of shapes): max over the ma slots of a view,
+//            f64 sum over the views in view order, / Vq  -> dense scores.
+// Deterministic: no floating-point atomics; the only atomics are integer
+// counters and atomicMax on non-negative float bits (order-independent).
+#include "simt_tile.cuh"
+
+namespace gift {
+
+constexpr int RED_RS = 4096;  // shapes per reduce CTA
+constexpr int RED_THREADS = 256;
+constexpr int PLAN_THREADS = 1024;
+
+enum Meta { M_ITEMS = 0, M_OUT_TOTAL = 1, M_OVERFLOW = 2, M_WORK = 3 };
+
+__global__ void probe_count_kernel(const int32_t* __restrict__ cells, int64_t nprobes,
+                                   int32_t* __restrict__ counts) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nprobes) return;
+  int c = cells[i];
+  if (c >= 0) atomicAdd(&counts[c], 1);
+}
+
+__global__ void __launch_bounds__(PLAN_THREADS)
+    probe_plan_kernel(const int32_t* __restrict__ counts, int K, const int64_t* __restrict__ seg_off,
+                      const int64_t* __restrict__ tile_off, int32_t* __restrict__ probe_off,
+                      int64_t* __restrict__ outbase, int64_t* __restrict__ item_off,
+                      int32_t* __restrict__ cursor, int64_t* __restrict__ meta, int64_t capacity) {
+  __shared__ int64_t sbuf[32];
+  const int per = (K + PLAN_THREADS - 1) / PLAN_THREADS;
+  const int c0 = threadIdx.x * per;
+  int64_t s_cnt = 0, s_out = 0, s_items = 0;
+  for (int c = c0; c < min(c0 + per, K); ++c) {
+    int64_t n = counts[c];
+    int64_t S = seg_off[c + 1] - seg_off[c];
+    int64_t T = tile_off[c + 1] - tile_off[c];
+    s_cnt += n;
+    s_out += n * S;
+    s_items += T * ((n + simt::TB - 1) / simt::TB);
+  }
+  int64_t tot_cnt, tot_out, tot_items;
+  int64_t p_cnt = block_exclusive_scan<int64_t>(s_cnt, &tot_cnt, sbuf);
+  int64_t p_out = block_exclusive_scan<int64_t>(s_out, &tot_out, sbuf);
+  int64_t p_items = block_exclusive_scan<int64_t>(s_items, &tot_items, sbuf);
+  for (int c = c0; c < min(c0 + per, K); ++c) {
+    int64_t n = counts[c];
+    int64_t S = seg_off[c + 1] - seg_off[c];
+    int64_t T = tile_off[c + 1] - tile_off[c];
+    probe_off[c] = static_cast<int32_t>(p_cnt);
+    outbase[c] = p_out;
+    item_off[c] = p_items;
+    cursor[c] = 0;
+    p_cnt += n;
+    p_out += n * S;
+    p_items += T * ((n + simt::TB - 1) / simt::TB);
+  }
+  if (threadIdx.x == 0) {
+    probe_off[K] = static_cast<int32_t>(tot_cnt);
+    outbase[K] = tot_out;
+    item_off[K] = tot_items;
+    meta[M_ITEMS] = tot_items;
+    meta[M_OUT_TOTAL] = tot_out;
+    meta[M_OVERFLOW] = tot_out > capacity ? 1 : 0;
+    meta[M_WORK] = 0;
+  }
+}
+
+__global__ void probe_scatter_kernel(const int32_t* __restrict__ cells, int64_t nprobes,
+                                     const int32_t* __restrict__ probe_off,
+                                     int32_t* __restrict__ cursor, int32_t* __restrict__ probe_list,
+                                     int32_t* __restrict__ probe_rank) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nprobes) return;
+  int c = cells[i];
+  if (c < 0) return;
+  int r = atomicAdd(&cursor[c], 1);
+  probe_list[probe_off[c] + r] = static_cast<int32_t>(i);
+  probe_rank[i] = r;
+}
+
+__global__ void compact_zero_kernel(float* __restrict__ out, const int64_t* __restrict__ meta) {
+  if (meta[M_OVERFLOW]) return;
+  const int64_t n = meta[M_OUT_TOTAL];
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (; i < n; i += stride) out[i] = 0.f;
+}
+
+struct ScanArgs {
+  gift_fif_view f;
+  const float* Q;
+  const float* qn2;
+  int ma;
+  int mode;
+  float inv_sigma2;
+  bool vec16;
+  const int32_t* counts;
+  const int32_t* probe_off;
+  const int32_t* probe_list;
+  const int64_t* outbase;
+  const int64_t* item_off;
+  float* out;
+  int64_t* meta;
+};
+
+template <bool A_HALF>
+__global__ void __launch_bounds__(simt::NTHR, 2) fif_scan_kernel(ScanArgs p) {
+  extern __shared__ __align__(128) char smem[];
+  __shared__ int64_t s_item;
+  __shared__ int64_t s_brow[simt::TB];
+  __shared__ float s_qn2[simt::TB];
+  __shared__ float s_pn2[simt::TA];
+  __shared__ int32_t s_sp[simt::TA + 2];
+  const int tid = threadIdx.x;
+  const gift_fif_view& f = p.f;
+  if (p.meta[M_OVERFLOW]) return;
+  const int64_t n_items = p.meta[M_ITEMS];
+  const int K = f.K, d = f.d;
+  for (;;) {
+    if (tid == 0) s_item = static_cast<int64_t>(atomicAdd(reinterpret_cast<unsigned long long*>(&p.meta[M_WORK]), 1ull));
+    __syncthreads();
+    const int64_t item = s_item;
+    if (item >= n_items) break;
+    // cell = largest c with item_off[c] <= item (item_off non-decreasing)
+    int lo = 0, hi = K - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (p.item_off[mid] <= item)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    const int c = lo;
+    const int64_t rem = item - p.item_off[c];
+    const int cnt = p.counts[c];
+    const int nm = (cnt + simt::TB - 1) / simt::TB;
+    const int64_t t = f.tile_off[c] + rem / nm;
+    const int mt = static_cast<int>(rem % nm);
+    const int p0 = f.tile_pstart[t], p1 = f.tile_pend[t];
+    const int seg0 = f.tile_seg0[t], seg1 = f.tile_seg1[t];
+    const int nb = min(simt::TB, cnt - mt * simt::TB);
+    const int pb0 = p.probe_off[c] + mt * simt::TB;
+    if (tid < simt::TB) {
+      if (tid < nb) {
+        int pr = p.probe_list[pb0 + tid];
+        int64_t view = pr / p.ma;
+        s_brow[tid] = view;
+        s_qn2[tid] = p.qn2[view];
+      } else {
+        s_brow[tid] = 0;
+        s_qn2[tid] = 0.f;
+      }
+    }
+    if (tid < simt::TA) s_pn2[tid] = (p0 + tid < p1) ? f.pnorm2[p0 + tid] : 0.f;
+    const int nseg = seg1 - seg0;
+    for (int i = tid; i <= nseg; i += simt::NTHR) s_sp[i] = f.seg_pstart[seg0 + i];
+    __syncthreads();
+
+    simt::TileRows tr;
+    tr.a_base = f.feat;
+    tr.b_base = p.Q;
+    tr.na = p1 - p0;
+    tr.nb = nb;
+    tr.d = d;
+    float acc[8][4];
+    simt::mainloop<A_HALF>(
+        smem, tr, [&](int r) -> int64_t { return static_cast<int64_t>(p0) + r; },
+        [&](int r) -> int64_t { return s_brow[r]; }, p.vec16, acc);
+
+    // epilogue 1: transformed dot tile -> smem
+    float* Ds = reinterpret_cast<float*>(smem);
+    const simt::Lanes L;
+    const bool gauss = p.mode == GIFT_SIM_GAUSSIAN;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = L.a_row(i);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int m = L.b_row(j);
+        float v = acc[i][j];
+        if (gauss) v = 2.0f * v - s_pn2[r];  // max_p(2q.p - |p|^2) <-> min_p |q-p|^2
+        Ds[r * simt::DS_STRIDE + m] = v;
+      }
+    }
+    __syncthreads();
+    // epilogue 2: max over each segment's rows, similarity, store
+    const int64_t S_c = f.seg_off[c + 1] - f.seg_off[c];
+    const int64_t seg_base = f.seg_off[c];
+    const int64_t obase = p.outbase[c];
+    for (int idx = tid; idx < nseg * nb; idx += simt::NTHR) {
+      const int m = idx / nseg;
+      const int sl = idx - m * nseg;
+      const int sp0 = s_sp[sl], sp1 = s_sp[sl + 1];
+      const int r0 = max(sp0, p0) - p0, r1 = min(sp1, p1) - p0;
+      float mx = -INFINITY;
+      for (int r = r0; r < r1; ++r) mx = fmaxf(mx, Ds[r * simt::DS_STRIDE + m]);
+      float sim;
+      if (gauss)
+        sim = expf(-fmaxf(s_qn2[m] - mx, 0.f) * p.inv_sigma2);
+      else
+        sim = fminf(fmaxf(mx, 0.f), 1.f);
+      const int64_t o = obase + static_cast<int64_t>(mt * simt::TB + m) * S_c + (seg0 + sl - seg_base);
+      if (sp0 < p0 || sp1 > p1)
+        atomicMax(reinterpret_cast<int*>(p.out + o), __float_as_int(sim));
+      else
+        p.out[o] = sim;
+    }
+    __syncthreads();
+  }
+}
+
+struct ReduceArgs {
+  const int32_t* cells;       // [B*V*ma]
+  const int32_t* probe_rank;  // [B*V*ma]
+  const int64_t* seg_off;
+  const int32_t* seg_ord;
+  const int64_t* outbase;
+  const float* out;
+  const int64_t* meta;
+  const int32_t* vq;
+  int V, ma;
+  int64_t n_local, ord_base;
+  double* scores;
+};
+
+__global__ void __launch_bounds__(RED_THREADS) fif_reduce_kernel(ReduceArgs a) {
+  extern __shared__ __align__(128) char smem[];
+  double* acc = reinterpret_cast<double*>(smem);
+  float* vb = reinterpret_cast<float*>(acc + RED_RS);
+  __shared__ int s_sa, s_sb;
+  __shared__ int64_t s_base;
+  if (a.meta[M_OVERFLOW]) return;
+  const int tid = threadIdx.x;
+  const int b = blockIdx.y;
+  const int64_t lo = static_cast<int64_t>(blockIdx.x) * RED_RS;
+  const int64_t hi = min64(lo + RED_RS, a.n_local);
+  const int n = static_cast<int>(hi - lo);
+  const int64_t glo = a.ord_base + lo, ghi = a.ord_base + hi;
+  for (int i = tid; i < n; i += RED_THREADS) {
+    acc[i] = 0.0;
+    vb[i] = 0.f;
+  }
+  __syncthreads();
+  for (int v = 0; v < a.V; ++v) {
+    const int64_t pbase = (static_cast<int64_t>(b) * a.V + v) * a.ma;
+    // pass 1: view_best = max over the ma slots (matching.py:153-159)
+    for (int s = 0; s < a.ma; ++s) {
+      if (tid == 0) {
+        const int c = a.cells[pbase + s];
+        int sa = 0, sb = 0;
+        int64_t base = 0;
+        if (c >= 0) {
+          const int64_t b0 = a.seg_off[c], b1 = a.seg_off[c + 1];
+          int64_t l = b0, h = b1;
+          while (l < h) {
+            int64_t mid = (l + h) >> 1;
+            if (a.seg_ord[mid] < glo) l = mid + 1; else h = mid;
+          }
+          int64_t l2 = l, h2 = b1;
+          while (l2 < h2) {
+            int64_t mid = (l2 + h2) >> 1;
+            if (a.seg_ord[mid] < ghi) l2 = mid + 1; else h2 = mid;
+          }
+          sa = static_cast<int>(l - b0);
+          sb = static_cast<int>(l2 - b0);
+          base = a.outbase[c] + static_cast<int64_t>(a.probe_rank[pbase + s]) * (b1 - b0);
+        }
+        s_sa = sa;
+        s_sb = sb;
+        s_base = base;
+      }
+      __syncthreads();
+      const int sa = s_sa, sb = s_sb;
+      if (sa < sb) {
+        const int c = a.cells[pbase + s];
+        const int64_t b0 = a.seg_off[c];
+        const int64_t base = s_base;
+        for (int k = sa + tid; k < sb; k += RED_THREADS) {
+          const int o = static_cast<int>(a.seg_ord[b0 + k] - glo);
+          const float val = a.out[base + k];
+          if (a.ma == 1)
+            acc[o] += static_cast<double>(val);
+          else
+            vb[o] = fmaxf(vb[o], val);
+        }
+      }
+      __syncthreads();
+    }
+    if (a.ma == 1) continue;
+    // pass 2: total += view_best (f64, view order), reset
+    for (int s = 0; s < a.ma; ++s) {
+      if (tid == 0) {
+        const int c = a.cells[pbase + s];
+        int sa = 0, sb = 0;
+        if (c >= 0) {
+          const int64_t b0 = a.seg_off[c], b1 = a.seg_off[c + 1];
+          int64_t l = b0, h = b1;
+          while (l < h) {
+            int64_t mid = (l + h) >> 1;
+            if (a.seg_ord[mid] < glo) l = mid + 1; else h = mid;
+          }
+          int64_t l2 = l, h2 = b1;
+          while (l2 < h2) {
+            int64_t mid = (l2 + h2) >> 1;
+            if (a.seg_ord[mid] < ghi) l2 = mid + 1; else h2 = mid;
+          }
+          sa = static_cast<int>(l - b0);
+          sb = static_cast<int>(l2 - b0);
+        }
+        s_sa = sa;
+        s_sb = sb;
+      }
+      __syncthreads();
+      const int sa = s_sa, sb = s_sb;
+      if (sa < sb) {
+        const int c = a.cells[pbase + s];
+        const int64_t b0 = a.seg_off[c];
+        for (int k = sa + tid; k < sb; k += RED_THREADS) {
+          const int o = static_cast<int>(a.seg_ord[b0 + k] - glo);
+          acc[o] += static_cast<double>(vb[o]);
+          vb[o] = 0.f;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  const double denom = static_cast<double>(a.vq ? a.vq[b] : a.V);
+  for (int i = tid; i < n; i += RED_THREADS)
+    a.scores[static_cast<int64_t>(b) * a.n_local + lo + i] = acc[i] / denom;
+}
+
+}  // namespace gift
+
+using namespace gift;
+
+namespace {
+struct ScoreWs {
+  int64_t* meta;
+  uint8_t* nz;
+  float* qn2;
+  int32_t* cells;
+  int32_t* counts;
+  int32_t* cursor;
+  int32_t* probe_off;
+  int64_t* outbase;
+  int64_t* item_off;
+  int32_t* probe_list;
+  int32_t* probe_rank;
+  void* qws;
+  size_t qws_bytes;
+  float* compact;
+  int64_t capacity;
+};
+
+bool carve(Arena& ar, const gift_fif_view* f, int64_t nviews, int ma, ScoreWs& w) {
+  const int K = f->K;
+  const int64_t nprobes = nviews * ma;
+  w.meta = ar.take<int64_t>(8);
+  w.nz = ar.take<uint8_t>(nviews);
+  w.qn2 = ar.take<float>(nviews);
+  w.cells = ar.take<int32_t>(nprobes);
+  w.counts = ar.take<int32_t>(K);
+  w.cursor = ar.take<int32_t>(K);
+  w.probe_off = ar.take<int32_t>(K + 1);
+  w.outbase = ar.take<int64_t>(K + 1);
+  w.item_off = ar.take<int64_t>(K + 1);
+  w.probe_list = ar.take<int32_t>(nprobes);
+  w.probe_rank = ar.take<int32_t>(nprobes);
+  w.qws_bytes = gift_quantize_ws_bytes(nviews, f->d, K, GIFT_F32);
+  w.qws = ar.take<char>(static_cast<int64_t>(w.qws_bytes));
+  if (!w.meta || !w.nz || !w.qn2 || !w.cells || !w.counts || !w.cursor || !w.probe_off ||
+      !w.outbase || !w.item_off || !w.probe_list || !w.probe_rank || !w.qws)
+    return false;
+  w.capacity = static_cast<int64_t>(ar.remaining() / sizeof(float));
+  w.compact = ar.take<float>(w.capacity);
+  return w.capacity > 0 && w.compact != nullptr;
+}
+}  // namespace
+
+extern "C" size_t gift_fif_score_ws_bytes(const gift_fif_view* f, int32_t B, int32_t V, int32_t ma,
+                                          int64_t compact_capacity) {
+  Arena ar(nullptr, SIZE_MAX / 2);
+  ScoreWs w;
+  carve(ar, f, static_cast<int64_t>(B) * V, ma, w);
+  return align_up(ar.used, 256) + static_cast<size_t>(compact_capacity) * sizeof(float) + 512;
+}
+
+extern "C" int gift_fif_score(const gift_fif_view* f, const float* Q, int32_t B, int32_t V,
+                              const int32_t* vq, int32_t ma, int32_t mode, double sigma,
+                              double* out_scores, void* ws, size_t ws_bytes, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  GIFT_REQUIRE(f != nullptr, GIFT_ERR_INVALID, "null index");
+  GIFT_REQUIRE(ma >= 1 && ma <= f->K, GIFT_ERR_INVALID, "ma must be in [1, %d]", f->K);
+  GIFT_REQUIRE(mode == GIFT_SIM_COSINE || mode == GIFT_SIM_GAUSSIAN, GIFT_ERR_INVALID, "bad mode");
+  GIFT_REQUIRE(mode != GIFT_SIM_GAUSSIAN || sigma > 0, GIFT_ERR_INVALID, "sigma must be > 0");
+  GIFT_REQUIRE(f->dtype == GIFT_F32 || f->dtype == GIFT_F16, GIFT_ERR_INVALID, "bad storage");
+  GIFT_REQUIRE(f->n_postings < (int64_t(1) << 31), GIFT_ERR_UNSUPPORTED, "too many postings");
+  if (B <= 0 || f->n_local <= 0) return GIFT_OK;
+  GIFT_REQUIRE(V >= 1, GIFT_ERR_EMPTY, "view set is empty");
+  const int64_t nviews = static_cast<int64_t>(B) * V;
+  const int64_t nprobes = nviews * ma;
+  Arena ar(ws, ws_bytes);
+  ScoreWs w;
+  GIFT_REQUIRE(carve(ar, f, nviews, ma, w), GIFT_ERR_CAPACITY, "score workspace too small");
+  const int K = f->K, d = f->d;
+
+  int rc = gift_view_prep(Q, GIFT_F32, nviews, d, w.nz, w.qn2, stream);
+  if (rc) return rc;
+  rc = gift_quantize(Q, GIFT_F32, nviews, d, f->centroids, f->cnorm2, K, f->cmax_norm, ma, w.nz, -1,
+                     w.cells, w.qws, w.qws_bytes, stream);
+  if (rc) return rc;
+  GIFT_CUDA_TRY(cudaMemsetAsync(w.counts, 0, sizeof(int32_t) * K, st));
+  probe_count_kernel<<<static_cast<unsigned>(cdiv(nprobes, 256)), 256, 0, st>>>(w.cells, nprobes,
+                                                                               w.counts);
+  GIFT_LAUNCH_CHECK();
+  probe_plan_kernel<<<1, PLAN_THREADS, 0, st>>>(w.counts, K, f->seg_off, f->tile_off, w.probe_off,
+                                                w.outbase, w.item_off, w.cursor, w.meta, w.capacity);
+  GIFT_LAUNCH_CHECK();
+  probe_scatter_kernel<<<static_cast<unsigned>(cdiv(nprobes, 256)), 256, 0, st>>>(
+      w.cells, nprobes, w.probe_off, w.cursor, w.probe_list, w.probe_rank);
+  GIFT_LAUNCH_CHECK();
+  compact_zero_kernel<<<sm_count() * 4, 256, 0, st>>>(w.compact, w.meta);
+  GIFT_LAUNCH_CHECK();
+
+  ScanArgs sa;
+  sa.f = *f;
+  sa.Q = Q;
+  sa.qn2 = w.qn2;
+  sa.ma = ma;
+  sa.mode = mode;
+  sa.inv_sigma2 = mode == GIFT_SIM_GAUSSIAN ? static_cast<float>(1.0 / (sigma * sigma)) : 0.f;
+  const bool a_half = f->dtype == GIFT_F16;
+  const bool aligned = reinterpret_cast<uintptr_t>(f->feat) % 16 == 0 &&
+                       reinterpret_cast<uintptr_t>(Q) % 16 == 0;
+  sa.vec16 = aligned && (a_half ? d % 8 == 0 : d % 4 == 0);
+  sa.counts = w.counts;
+  sa.probe_off = w.probe_off;
+  sa.probe_list = w.probe_list;
+  sa.outbase = w.outbase;
+  sa.item_off = w.item_off;
+  sa.out = w.compact;
+  sa.meta = w.meta;
+  const int nblk = sm_count() * 2;
+  if (a_half) {
+    GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_scan_kernel<true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       simt::Cfg<true>::SMEM));
+    fif_scan_kernel<true><<<nblk, simt::NTHR, simt::Cfg<true>::SMEM, st>>>(sa);
+  } else {
+    GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_scan_kernel<false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       simt::Cfg<false>::SMEM));
+    fif_scan_kernel<false><<<nblk, simt::NTHR, simt::Cfg<false>::SMEM, st>>>(sa);
+  }
+  GIFT_LAUNCH_CHECK();
+
+  ReduceArgs ra;
+  ra.cells = w.cells;
+  ra.probe_rank = w.probe_rank;
+  ra.seg_off = f->seg_off;
+  ra.seg_ord = f->seg_ord;
+  ra.outbase = w.outbase;
+  ra.out = w.compact;
+  ra.meta = w.meta;
+  ra.vq = vq;
+  ra.V = V;
+  ra.ma = ma;
+  ra.n_local = f->n_local;
+  ra.ord_base = f->ord_base;
+  ra.scores = out_scores;
+  const int red_smem = RED_RS * (8 + 4);
+  GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     red_smem));
+  dim3 rgrid(static_cast<unsigned>(cdiv(f->n_local, RED_RS)), static_cast<unsigned>(B));
+  fif_reduce_kernel<<<rgrid, RED_THREADS, red_smem, st>>>(ra);
+  GIFT_LAUNCH_CHECK();
+  return GIFT_OK;
+}
+
+extern "C" int gift_fif_tile_n(void) { return simt::TA; }

@@ -1,0 +1,403 @@
+// K1 quantize — replaces shapesearch.codebook.quantize (codebook.py:111-124).
+//
+// Reference semantics: d2[c] = sum_k (c_k(f64) - x_k(f64))^2 reduced with
+// numpy's pairwise summation (8 accumulators, 128-element leaves, halving
+// split rounded to multiples of 8), then argsort(kind="stable")[:ma] — ties
+// to the lower centroid index.
+//
+// Two stages:
+//   1. approx[v, c] = |c|^2 - 2 x.c in fp32 on the CUDA-core tile mainloop
+//      (simt_tile.cuh);
+//   2. per view: T = (ma-th smallest approx) + 2M, where M bounds
+//      |approx + |x|^2 - d2_numpy| (fp32 dot error gamma_d |x||c|, rounding of
+//      the inputs and of the f64 pairwise sum); every centroid of the true
+//      top-ma satisfies approx <= T, so only candidates under T are re-scored
+//      with the exact f64 pairwise-order arithmetic (__dsub_rn/__dmul_rn/
+//      __dadd_rn, no FMA contraction) and sorted by (d2, index).
+// The result is bit-identical to the reference's indices.
+#include "simt_tile.cuh"
+
+namespace gift {
+
+constexpr int QS_THREADS = 128;
+constexpr int QS_WARPS = QS_THREADS / 32;
+constexpr int MAX_LEAVES = 256;  // leaves are >= 64 elements -> d <= 16384
+constexpr int MAX_K = 8192;
+constexpr int MAX_D = 16384;
+
+template <bool A_HALF>
+__global__ void __launch_bounds__(simt::NTHR, 2)
+    quant_approx_kernel(const void* __restrict__ X, int64_t n, int d, const float* __restrict__ C,
+                        const double* __restrict__ cn2, int K, float* __restrict__ approx,
+                        bool vec16) {
+  extern __shared__ __align__(128) char smem[];
+  const int64_t v0 = static_cast<int64_t>(blockIdx.x) * simt::TA;
+  const int c0 = blockIdx.y * simt::TB;
+  simt::TileRows t;
+  t.a_base = X;
+  t.b_base = C;
+  t.na = static_cast<int>(min64(simt::TA, n - v0));
+  t.nb = min(simt::TB, K - c0);
+  t.d = d;
+  float acc[8][4];
+  simt::mainloop<A_HALF>(
+      smem, t, [&](int r) -> int64_t { return v0 + r; }, [&](int r) -> int64_t { return c0 + r; },
+      vec16, acc);
+  const simt::Lanes L;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    int r = L.a_row(i);
+    if (r >= t.na) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int c = L.b_row(j);
+      if (c >= t.nb) continue;
+      approx[(v0 + r) * K + c0 + c] = static_cast<float>(cn2[c0 + c]) - 2.0f * acc[i][j];
+    }
+  }
+}
+
+__global__ void f64_to_f32_kernel(const double* __restrict__ in, float* __restrict__ out,
+                                  int64_t n) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (; i < n; i += stride) out[i] = static_cast<float>(in[i]);
+}
+
+// --- numpy pairwise summation of (c - x)^2 over one leaf (n <= 128) ---------
+__device__ __forceinline__ double sq_term(const void* X, int xdtype, int64_t xoff,
+                                          const float* __restrict__ c, int k) {
+  double xv = load_as_f64(X, xdtype, xoff + k);
+  double t = __dsub_rn(static_cast<double>(c[k]), xv);
+  return __dmul_rn(t, t);
+}
+
+__device__ double leaf_sum(const void* X, int xdtype, int64_t xoff, const float* __restrict__ c,
+                           int off, int len) {
+  if (len < 8) {
+    double r = 0.0;
+    for (int i = 0; i < len; ++i) r = __dadd_rn(r, sq_term(X, xdtype, xoff, c, off + i));
+    return r;
+  }
+  double r0 = sq_term(X, xdtype, xoff, c, off + 0), r1 = sq_term(X, xdtype, xoff, c, off + 1),
+         r2 = sq_term(X, xdtype, xoff, c, off + 2), r3 = sq_term(X, xdtype, xoff, c, off + 3),
+         r4 = sq_term(X, xdtype, xoff, c, off + 4), r5 = sq_term(X, xdtype, xoff, c, off + 5),
+         r6 = sq_term(X, xdtype, xoff, c, off + 6), r7 = sq_term(X, xdtype, xoff, c, off + 7);
+  int i = 8;
+  const int lim = len - (len % 8);
+  for (; i < lim; i += 8) {
+    r0 = __dadd_rn(r0, sq_term(X, xdtype, xoff, c, off + i + 0));
+    r1 = __dadd_rn(r1, sq_term(X, xdtype, xoff, c, off + i + 1));
+    r2 = __dadd_rn(r2, sq_term(X, xdtype, xoff, c, off + i + 2));
+    r3 = __dadd_rn(r3, sq_term(X, xdtype, xoff, c, off + i + 3));
+    r4 = __dadd_rn(r4, sq_term(X, xdtype, xoff, c, off + i + 4));
+    r5 = __dadd_rn(r5, sq_term(X, xdtype, xoff, c, off + i + 5));
+    r6 = __dadd_rn(r6, sq_term(X, xdtype, xoff, c, off + i + 6));
+    r7 = __dadd_rn(r7, sq_term(X, xdtype, xoff, c, off + i + 7));
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3)),
+                         __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
+  for (; i < len; ++i) res = __dadd_rn(res, sq_term(X, xdtype, xoff, c, off + i));
+  return res;
+}
+
+struct PairwisePlan {
+  int n_leaves, n_ops;
+  int leaf_off[MAX_LEAVES];
+  int leaf_len[MAX_LEAVES];
+  unsigned char ops[2 * MAX_LEAVES];  // 0 = push next leaf, 1 = add top two
+};
+
+// Postfix program of numpy's pairwise recursion for a length-d reduction.
+__device__ void build_plan(PairwisePlan& p, int d) {
+  struct Frame {
+    int off, n, state;
+  };
+  Frame st[40];
+  int top = 0;
+  st[0] = {0, d, 0};
+  p.n_leaves = 0;
+  p.n_ops = 0;
+  while (top >= 0) {
+    Frame& f = st[top];
+    if (f.n <= 128) {
+      p.leaf_off[p.n_leaves] = f.off;
+      p.leaf_len[p.n_leaves] = f.n;
+      p.n_leaves++;
+      p.ops[p.n_ops++] = 0;
+      --top;
+      continue;
+    }
+    int n2 = f.n / 2;
+    n2 -= n2 % 8;
+    if (f.state == 0) {
+      f.state = 1;
+      st[top + 1] = {f.off, n2, 0};
+      ++top;
+    } else if (f.state == 1) {
+      f.state = 2;
+      st[top + 1] = {f.off + n2, f.n - n2, 0};
+      ++top;
+    } else {
+      p.ops[p.n_ops++] = 1;
+      --top;
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t float_order_key(float f) {
+  uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float float_from_order_key(uint32_t u) {
+  return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+
+__global__ void __launch_bounds__(QS_THREADS)
+    quant_select_kernel(const float* __restrict__ approx, int64_t n, int K, int ma,
+                        const void* __restrict__ X, int xdtype, int d, const float* __restrict__ C,
+                        double cmax, const uint8_t* __restrict__ nz, int zero_key, int p2k,
+                        int32_t* __restrict__ out) {
+  extern __shared__ __align__(128) char smem[];
+  float* a = reinterpret_cast<float*>(smem);
+  double* cd = reinterpret_cast<double*>(smem + ((K * 4 + 15) / 16) * 16);
+  int* ci = reinterpret_cast<int*>(cd + p2k);
+  __shared__ PairwisePlan plan;
+  __shared__ double lv[QS_WARPS][MAX_LEAVES];
+  __shared__ unsigned hist[256];
+  __shared__ double s_red[QS_WARPS];
+  __shared__ float s_redf[QS_WARPS];
+  __shared__ uint32_t s_prefix;
+  __shared__ int s_rank, s_nc;
+  __shared__ float s_kth;
+
+  const int64_t v = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (v >= n) return;
+  if (nz != nullptr && nz[v] == 0) {
+    for (int s = tid; s < ma; s += QS_THREADS) out[v * ma + s] = zero_key >= 0 ? zero_key : -1;
+    return;
+  }
+  const int64_t xoff = v * static_cast<int64_t>(d);
+  // |x| (f64) for the error margin
+  double xs = 0.0;
+  for (int k = tid; k < d; k += QS_THREADS) {
+    double xv = load_as_f64(X, xdtype, xoff + k);
+    xs += xv * xv;
+  }
+  for (int o = 16; o > 0; o >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
+  if (lane == 0) s_red[warp] = xs;
+  for (int c = tid; c < K; c += QS_THREADS) a[c] = approx[v * K + c];
+  if (tid == 0) {
+    build_plan(plan, d);
+    s_nc = 0;
+  }
+  __syncthreads();
+  double xn2 = 0.0;
+  for (int w = 0; w < QS_WARPS; ++w) xn2 += s_red[w];
+  const double xn = sqrt(xn2) * (1.0 + 1e-6) + 1e-300;
+
+  // ma-th smallest approx value
+  if (ma == 1) {
+    float m = INFINITY;
+    for (int c = tid; c < K; c += QS_THREADS) m = fminf(m, a[c]);
+    for (int o = 16; o > 0; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) s_redf[warp] = m;
+    __syncthreads();
+    if (tid == 0) {
+      float mm = INFINITY;
+      for (int w = 0; w < QS_WARPS; ++w) mm = fminf(mm, s_redf[w]);
+      s_kth = mm;
+    }
+    __syncthreads();
+  } else {
+    if (tid == 0) {
+      s_prefix = 0;
+      s_rank = ma - 1;
+    }
+    uint32_t mask = 0;
+    for (int pass = 3; pass >= 0; --pass) {
+      const int shift = 8 * pass;
+      for (int b = tid; b < 256; b += QS_THREADS) hist[b] = 0;
+      __syncthreads();
+      const uint32_t prefix = s_prefix;
+      for (int c = tid; c < K; c += QS_THREADS) {
+        uint32_t u = float_order_key(a[c]);
+        if ((u & mask) == prefix) atomicAdd(&hist[(u >> shift) & 255u], 1u);
+      }
+      __syncthreads();
+      if (tid == 0) {
+        int rank = s_rank;
+        unsigned cum = 0;
+        for (int b = 0; b < 256; ++b) {
+          if (cum + hist[b] > static_cast<unsigned>(rank)) {
+            s_prefix = prefix | (static_cast<uint32_t>(b) << shift);
+            s_rank = rank - static_cast<int>(cum);
+            break;
+          }
+          cum += hist[b];
+        }
+      }
+      mask |= 255u << shift;
+      __syncthreads();
+    }
+    if (tid == 0) s_kth = float_from_order_key(s_prefix);
+    __syncthreads();
+  }
+
+  // rigorous margin M >= |approx + |x|^2 - d2_numpy|
+  const double u32 = 5.9604644775390625e-08;  // 2^-24
+  const double u64 = 1.1102230246251565e-16;  // 2^-53
+  const double gd = (d + 2) * u32 / (1.0 - (d + 2) * u32);
+  const double M = 1.5 * (2.0 * (gd + 2.0 * u32) * xn * cmax + 3.0 * u32 * cmax * cmax +
+                          2.0 * u32 * xn * cmax + (d + 4) * u64 * (xn + cmax) * (xn + cmax)) +
+                   1e-30;
+  const double thresh = static_cast<double>(s_kth) + 2.0 * M;
+  for (int c = tid; c < K; c += QS_THREADS) {
+    if (static_cast<double>(a[c]) <= thresh) {
+      int pos = atomicAdd(&s_nc, 1);
+      ci[pos] = c;
+    }
+  }
+  __syncthreads();
+  const int nc = s_nc;
+  if (nc == ma && ma == 1) {
+    if (tid == 0) out[v * ma] = ci[0];
+    return;
+  }
+  // exact numpy-order d2 of every candidate (warp per candidate)
+  for (int q = warp; q < nc; q += QS_WARPS) {
+    const float* crow = C + static_cast<int64_t>(ci[q]) * d;
+    for (int l = lane; l < plan.n_leaves; l += 32)
+      lv[warp][l] = leaf_sum(X, xdtype, xoff, crow, plan.leaf_off[l], plan.leaf_len[l]);
+    __syncwarp();
+    if (lane == 0) {
+      double stk[24];
+      int sp = 0, li = 0;
+      for (int o = 0; o < plan.n_ops; ++o) {
+        if (plan.ops[o] == 0) {
+          stk[sp++] = lv[warp][li++];
+        } else {
+          double b = stk[--sp];
+          double aa = stk[--sp];
+          stk[sp++] = __dadd_rn(aa, b);
+        }
+      }
+      cd[q] = stk[0];
+    }
+    __syncwarp();
+  }
+  // sort candidates ascending by (d2, index): bitonic over the next power of 2
+  int p2 = 1;
+  while (p2 < nc) p2 <<= 1;
+  for (int i = nc + tid; i < p2; i += QS_THREADS) {
+    cd[i] = INFINITY;
+    ci[i] = 0x7fffffff;
+  }
+  __syncthreads();
+  for (int size = 2; size <= p2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = tid; i < (p2 >> 1); i += QS_THREADS) {
+        int lo = 2 * stride * (i / stride) + (i % stride);
+        int hi = lo + stride;
+        bool up = (lo & size) == 0;
+        double dl = cd[lo], dh = cd[hi];
+        int il = ci[lo], ih = ci[hi];
+        bool hi_first = (dh < dl) || (dh == dl && ih < il);
+        if (hi_first == up) {
+          cd[lo] = dh;
+          cd[hi] = dl;
+          ci[lo] = ih;
+          ci[hi] = il;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int s = tid; s < ma; s += QS_THREADS) out[v * ma + s] = ci[s];
+}
+
+}  // namespace gift
+
+using namespace gift;
+
+static int64_t quant_rows_for(size_t ws_bytes, int d, int K, int xdtype) {
+  size_t per_row = static_cast<size_t>(K) * 4 + (xdtype == GIFT_F64 ? static_cast<size_t>(d) * 4 : 0);
+  if (ws_bytes < 4096) return 0;
+  return static_cast<int64_t>((ws_bytes - 4096) / per_row);
+}
+
+extern "C" size_t gift_quantize_ws_bytes(int64_t n, int32_t d, int32_t K, int32_t xdtype) {
+  int64_t rows = n < 16384 ? (n < 128 ? 128 : n) : 16384;
+  size_t per_row = static_cast<size_t>(K) * 4 + (xdtype == GIFT_F64 ? static_cast<size_t>(d) * 4 : 0);
+  return per_row * rows + 4096 + 1024;
+}
+
+extern "C" int gift_quantize(const void* X, int32_t xdtype, int64_t n, int32_t d, const float* C,
+                             const double* cnorm2, int32_t K, double cmax_norm, int32_t ma,
+                             const uint8_t* nz, int32_t zero_key, int32_t* out_idx, void* ws,
+                             size_t ws_bytes, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  GIFT_REQUIRE(K >= 1 && d >= 1, GIFT_ERR_EMPTY, "empty codebook");
+  GIFT_REQUIRE(ma >= 1 && ma <= K, GIFT_ERR_INVALID, "ma must be in [1, %d]", K);
+  GIFT_REQUIRE(K <= MAX_K, GIFT_ERR_UNSUPPORTED, "codebook size %d > %d", K, MAX_K);
+  GIFT_REQUIRE(d <= MAX_D, GIFT_ERR_UNSUPPORTED, "dimension %d > %d", d, MAX_D);
+  GIFT_REQUIRE(xdtype == GIFT_F32 || xdtype == GIFT_F16 || xdtype == GIFT_F64, GIFT_ERR_INVALID,
+               "bad dtype");
+  if (n <= 0) return GIFT_OK;
+  int64_t rows = quant_rows_for(ws_bytes, d, K, xdtype);
+  if (rows >= n) rows = n;
+  else rows = rows / simt::TA * simt::TA;
+  GIFT_REQUIRE(rows >= 1, GIFT_ERR_CAPACITY, "quantize workspace too small");
+
+  int p2k = 1;
+  while (p2k < K) p2k <<= 1;
+  const size_t sel_smem = ((static_cast<size_t>(K) * 4 + 15) / 16) * 16 + static_cast<size_t>(p2k) * 12;
+  GIFT_CUDA_TRY(cudaFuncSetAttribute(quant_select_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(sel_smem)));
+  const bool a_half = xdtype == GIFT_F16;
+  const int approx_smem = a_half ? simt::Cfg<true>::SMEM : simt::Cfg<false>::SMEM;
+  if (a_half)
+    GIFT_CUDA_TRY(cudaFuncSetAttribute(quant_approx_kernel<true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, approx_smem));
+  else
+    GIFT_CUDA_TRY(cudaFuncSetAttribute(quant_approx_kernel<false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, approx_smem));
+
+  Arena ar(ws, ws_bytes);
+  float* approx = ar.take<float>(rows * K);
+  float* xconv = xdtype == GIFT_F64 ? ar.take<float>(rows * static_cast<int64_t>(d)) : nullptr;
+  GIFT_REQUIRE(approx != nullptr && (xdtype != GIFT_F64 || xconv != nullptr), GIFT_ERR_CAPACITY,
+               "quantize workspace too small");
+
+  const size_t esz = xdtype == GIFT_F16 ? 2 : (xdtype == GIFT_F64 ? 8 : 4);
+  for (int64_t r0 = 0; r0 < n; r0 += rows) {
+    const int64_t nr = min64(rows, n - r0);
+    const char* xs = static_cast<const char*>(X) + r0 * d * esz;
+    const void* a_src = xs;
+    if (xdtype == GIFT_F64) {
+      int64_t cnt = nr * d;
+      f64_to_f32_kernel<<<static_cast<unsigned>(min64(cdiv(cnt, 256), 4096)), 256, 0, st>>>(
+          reinterpret_cast<const double*>(xs), xconv, cnt);
+      GIFT_LAUNCH_CHECK();
+      a_src = xconv;
+    }
+    const bool aligned = (reinterpret_cast<uintptr_t>(a_src) % 16 == 0) &&
+                         (reinterpret_cast<uintptr_t>(C) % 16 == 0);
+    const bool vec16 = aligned && (a_half ? (d % 8 == 0) : (d % 4 == 0));
+    dim3 grid(static_cast<unsigned>(cdiv(nr, simt::TA)), static_cast<unsigned>(cdiv(K, simt::TB)));
+    if (a_half)
+      quant_approx_kernel<true><<<grid, simt::NTHR, approx_smem, st>>>(a_src, nr, d, C, cnorm2, K,
+                                                                      approx, vec16);
+    else
+      quant_approx_kernel<false><<<grid, simt::NTHR, approx_smem, st>>>(a_src, nr, d, C, cnorm2, K,
+                                                                       approx, vec16);
+    GIFT_LAUNCH_CHECK();
+    quant_select_kernel<<<static_cast<unsigned>(nr), QS_THREADS, sel_smem, st>>>(
+        approx, nr, K, ma, xs, xdtype, d, C, cmax_norm, nz ? nz + r0 : nullptr, zero_key, p2k,
+        out_idx + r0 * ma);
+    GIFT_LAUNCH_CHECK();
+  }
+  return GIFT_OK;
+}

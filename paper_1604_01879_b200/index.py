@@ -1,0 +1,507 @@
+"""Pipeline composition on the GPU: index build, batched query, persistence.
+
+Drop-in for `shapesearch.index` (index.py:38-414) on the F-IF + S-IF path:
+IndexConfig, IndexBundle, build_index, query, query_by_id, rerank_scores,
+save_bundle, load_bundle keep the reference's names, arguments, results and
+errors.  New: `build_index_from_views` (explicit feature
+tensors and codebooks, D3/D4), `query_batch` / `query_many` (batched and
+pipelined queries, D6), and IndexConfig fields `similarity`, `sigma`,
+`storage_dtype`, `batch_size` whose defaults reproduce the reference.
+"""
+
+from __future__ import annotations
+
+import json
+import logging
+import time
+from dataclasses import asdict, dataclass, field, fields, replace
+from pathlib import Path
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from . import codebook as cb
+from . import engine as eg
+from . import features as ft
+from . import matching as mt
+from . import rerank as rr
+from .errors import (AllShapesFailed, ChannelMismatch, EmptyIndex, EmptyManifest, FormatError,
+                     Unsupported)
+
+log = logging.getLogger(__name__)
+
+FORMAT_VERSION = "shapesearch-index-1"
+CHANNELS = ("A", "B")
+_REFERENCE_FIELDS = ("n_views", "resolution", "grid", "cells", "bins", "codebook_size", "ma",
+                     "k1", "k2", "alpha", "seed", "imported")
+
+
+@dataclass(frozen=True)
+class IndexConfig:
+    n_views: int = 64
+    resolution: int = 64
+    grid: int = 8
+    cells: int = 4
+    bins: int = 8
+    codebook_size: int = 256
+    ma: int = 2
+    k1: int = 10
+    k2: int = 4
+    alpha: float = 0.5
+    seed: int = 0
+    imported: bool = False
+    # new fields; defaults reproduce the reference
+    similarity: str = "cosine"      # or "gaussian" (north-star kernel, D1)
+    sigma: float = 0.5
+    storage_dtype: str = "float32"  # or "float16" (config 4, D5)
+    batch_size: int = 64            # queries per device batch
+
+    def __post_init__(self):
+        # index.py:58-64
+        if min(self.n_views, self.codebook_size, self.ma, self.k1, self.k2) < 1:
+            raise ValueError("all counts must be >= 1")
+        if self.alpha <= 0:
+            raise ValueError("alpha must be > 0")
+        if self.ma > self.codebook_size:
+            raise ValueError("ma must not exceed the codebook size")
+        if self.similarity not in ("cosine", "gaussian"):
+            raise ValueError("similarity must be 'cosine' or 'gaussian'")
+        if self.sigma <= 0:
+            raise ValueError("sigma must be > 0")
+        if self.storage_dtype not in ("float32", "float16"):
+            raise ValueError("storage_dtype must be 'float32' or 'float16'")
+        if self.batch_size < 1:
+            raise ValueError("batch_size must be >= 1")
+
+    @property
+    def torch_storage(self):
+        return torch.float16 if self.storage_dtype == "float16" else torch.float32
+
+
+@dataclass
+class IndexBundle:
+    config: IndexConfig
+    shape_ids: list
+    labels: dict
+    codebooks: dict
+    fifs: dict
+    raw_activations: dict
+    sif: rr.SecondInvertedFile
+    version: str = FORMAT_VERSION
+    _engine: object = field(default=None, repr=False, compare=False)
+
+    @property
+    def n_shapes(self) -> int:
+        return len(self.shape_ids)
+
+    def viewset_matrix(self, channel: str, ordinal: int) -> np.ndarray:
+        """Stored view features of one shape (index.py:80-84)."""
+        return self.fifs[channel].shape_matrix(ordinal)
+
+    @property
+    def engine(self) -> "QueryEngine":
+        if self._engine is None:
+            self._engine = QueryEngine(self)
+        return self._engine
+
+
+def read_manifest(path) -> list:
+    """`path<TAB>label` rows; relative paths resolve against the manifest
+    (index.py:87-103)."""
+    path = Path(path)
+    rows = []
+    for line in path.read_text(encoding="utf-8").splitlines():
+        line = line.strip()
+        if not line:
+            continue
+        rel, _, label = line.partition("\t")
+        rows.append((path.parent / rel, label.strip()))
+    if not rows:
+        raise EmptyManifest(f"manifest {path} lists no shapes")
+    return rows
+
+
+# ------------------------------------------------------------------ engine
+class QueryEngine:
+    """Batched device pipeline over one bundle (single GPU or one shard):
+    K1 quantize -> K3 F-IF score -> K4 top-k2 -> K5 mean activation
+    (-> aggregate) -> K6 S-IF -> K4 final top-k (index.py:230-299)."""
+
+    def __init__(self, bundle: IndexBundle):
+        self.b = bundle
+        cfg = bundle.config
+        self.cfg = cfg
+        self.fa = bundle.fifs["A"].dev
+        self.fb = bundle.fifs["B"].dev
+        self.dup = bundle.fifs["A"] is bundle.fifs["B"]
+        ra, rb = bundle.raw_activations["A"], bundle.raw_activations["B"]
+        self.raw_a = rr._rows(ra)
+        self.raw_b = self.raw_a if rb is ra else rr._rows(rb)
+        self.raw_dup = rb is ra
+        self.sif = bundle.sif.dev
+        self.n = bundle.n_shapes
+        order = sorted(range(self.n), key=lambda i: bundle.shape_ids[i])
+        rank = np.empty(self.n, dtype=np.int32)
+        rank[np.asarray(order, dtype=np.int64)] = np.arange(self.n, dtype=np.int32)
+        self.idrank = torch.from_numpy(rank).to(nat.device())
+        self.ord_of = {sid: i for i, sid in enumerate(bundle.shape_ids)}
+        self.runner = eg.ScoreRunner()
+        self.mode = mt.sim_mode(cfg.similarity)
+
+    def scores(self, Qa, Qb=None, vq=None, vqb=None, stream=None):
+        sa = self.runner.score(self.fa, Qa, self.cfg.ma, self.mode, self.cfg.sigma, vq=vq,
+                               stream=stream)
+        if Qb is None and self.dup:
+            return sa, sa
+        sb = self.runner.score(self.fb, Qa if Qb is None else Qb, self.cfg.ma, self.mode,
+                               self.cfg.sigma, vq=vq if vqb is None else vqb, stream=stream)
+        return sa, sb
+
+    def rerank(self, sa, sb, stream=None):
+        """index.py:249-258 for a batch of channel scores -> dense f64."""
+        k2 = min(self.cfg.k2, self.n)
+        na, _ = eg.topk_rows(sa, k2, positive_only=True, stream=stream)
+        nb = na if sb is sa else eg.topk_rows(sb, k2, positive_only=True, stream=stream)[0]
+        fa = eg.act_mean(self.raw_a, nb, stream=stream)
+        if sb is sa and self.raw_dup:
+            final = fa  # aggregate(f, f) == f exactly (rerank.py:142-146)
+        else:
+            fb = eg.act_mean(self.raw_b, na, stream=stream)
+            final = eg.act_aggregate(fa, fb, self.cfg.alpha, stream=stream)
+        return self.sif.query(final, stream=stream)
+
+    def run(self, Qa, Qb=None, top_k=10, rerank=True, self_local=None, vq=None, vqb=None,
+            stream=None):
+        """Device batch -> (idx [B, k] i32 global ordinals, val [B, k] f64)."""
+        sa, sb = self.scores(Qa, Qb, vq, vqb, stream)
+        if rerank:
+            final = self.rerank(sa, sb, stream)
+        elif sb is sa:
+            final = sa  # np.mean([s, s], axis=0) == s exactly
+        else:
+            final = (sa + sb) / 2.0
+        k = min(top_k, self.n)
+        return eg.topk_rows(final, k, idrank=self.idrank, self_local=self_local, stream=stream)
+
+    def results(self, idx_row, val_row):
+        ids, labels = self.b.shape_ids, self.b.labels
+        return [(ids[int(i)], float(v), labels.get(ids[int(i)], ""))
+                for i, v in zip(idx_row, val_row) if i >= 0]
+
+
+# ------------------------------------------------------------------ build
+def _to_device_views(views, dtype):
+    if torch.is_tensor(views):
+        t = views
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(views, dtype=np.float32))
+    if t.dim() != 3:
+        raise ValueError("views must be [n_shapes, n_views, d]")
+    return t.to(nat.device()).to(dtype).contiguous()
+
+
+def _self_join(fif: eg.DeviceFif, X: torch.Tensor, cfg: IndexConfig, runner: eg.ScoreRunner,
+               batch: int):
+    """index.py:196-210: every database shape queried against the F-IF ->
+    raw top-k1 activations and top-k2 neighbour lists (device)."""
+    n = X.shape[0]
+    k1 = min(cfg.k1, n)
+    kk = max(k1, min(cfg.k2, n))
+    raw = eg.ActRows.empty(n, max(k1, 1), X.device)
+    nbr = torch.full((n, max(min(cfg.k2, n), 1)), -1, dtype=torch.int32, device=X.device)
+    mode = mt.sim_mode(cfg.similarity)
+    for b0 in range(0, n, batch):
+        b1 = min(n, b0 + batch)
+        Q = X[b0:b1].float()
+        s = runner.score(fif, Q, cfg.ma, mode, cfg.sigma)
+        tidx, tval = eg.topk_rows(s, kk, positive_only=True)
+        eg.act_from_topk(tidx, tval, k1, out=raw.rows(b0, b1))
+        nbr[b0:b1] = tidx[:, : nbr.shape[1]]
+    return raw, nbr
+
+
+def build_index_from_views(views_a, shape_ids, config: IndexConfig = IndexConfig(), *,
+                           views_b=None, labels=None, codebooks=None,
+                           self_join_batch: int = 256) -> IndexBundle:
+    """Build the full index from feature tensors [N, V, d] (host array or
+    device tensor).  views_b=None feeds one feature set to both channels
+    (computed once).  `codebooks` = {"A": Codebook, "B": ...};
+    default: seeded sampled DB rows (D3)."""
+    shape_ids = list(shape_ids)
+    if not shape_ids:
+        raise EmptyManifest("no shapes listed")
+    Xa = _to_device_views(views_a, config.torch_storage)
+    if Xa.shape[0] != len(shape_ids):
+        raise ValueError("views and shape_ids disagree on the number of shapes")
+    Xb = None if views_b is None else _to_device_views(views_b, config.torch_storage)
+    if codebooks is None:
+        ca = cb.sample_codebook(Xa.float().cpu().numpy(), config.codebook_size, config.seed, "A")
+        cbb = (cb.Codebook(ca.centroids, "B", config.seed) if Xb is None else
+               cb.sample_codebook(Xb.float().cpu().numpy(), config.codebook_size, config.seed, "B"))
+        codebooks = {"A": ca, "B": cbb}
+    fa = mt.build_fif_from_tensor(Xa, codebooks["A"], shape_ids)
+    if Xb is None and np.array_equal(codebooks["A"].centroids, codebooks["B"].centroids):
+        fb = fa
+    else:
+        fb = mt.build_fif_from_tensor(Xa if Xb is None else Xb, codebooks["B"], shape_ids)
+    runner = eg.ScoreRunner()
+    raw_a, nbr_a = _self_join(fa.dev, Xa, config, runner, self_join_batch)
+    if fb is fa:
+        raw_b, nbr_b = raw_a, nbr_a
+    else:
+        raw_b, nbr_b = _self_join(fb.dev, Xa if Xb is None else Xb, config, runner,
+                                  self_join_batch)
+    # co-augment (rerank.py:114-125) + aggregate (index.py:214-217)
+    aug_a = eg.act_mean(raw_a, nbr_b)
+    if fb is fa:
+        final = aug_a
+    else:
+        aug_b = eg.act_mean(raw_b, nbr_a)
+        final = eg.act_aggregate(aug_a, aug_b, config.alpha)
+    sif = rr.SecondInvertedFile(shape_ids, eg.DeviceSif.build(final, len(shape_ids)))
+    acts_a = rr.ActivationList(raw_a, shape_ids)
+    acts_b = acts_a if raw_b is raw_a else rr.ActivationList(raw_b, shape_ids)
+    config = replace(config, n_views=max(1, Xa.shape[1]), codebook_size=codebooks["A"].k)
+    return IndexBundle(config=config, shape_ids=shape_ids,
+                       labels=dict(labels) if labels else {s: "" for s in shape_ids},
+                       codebooks=dict(codebooks), fifs={"A": fa, "B": fb},
+                       raw_activations={"A": acts_a, "B": acts_b}, sif=sif)
+
+
+def build_index(manifest, config: IndexConfig = IndexConfig(), jobs: int = 1,
+                feature_files: dict | None = None, codebooks=None) -> IndexBundle:
+    """index.py:146-227 from precomputed feature files ({"A": path, "B":
+    path}); mesh rendering (index.py:106-139) is outside the GPU path."""
+    if isinstance(manifest, (str, Path)):
+        rows = read_manifest(manifest)
+    else:
+        rows = [(Path(p), lab) for p, lab in manifest]
+    if not rows:
+        raise EmptyManifest("no shapes listed")
+    if not feature_files:
+        raise Unsupported("mesh rendering is outside the GPU path: pass feature_files "
+                          "or use build_index_from_views")
+    if set(feature_files) != set(CHANNELS):
+        raise ChannelMismatch(f"feature files required for channels {CHANNELS}")
+    config = replace(config, imported=True)
+    imported = {ch: ft.import_features(feature_files[ch], ch) for ch in CHANNELS}
+    mats = {ch: [] for ch in CHANNELS}
+    ids, labels = [], {}
+    for path, label in rows:
+        sid = Path(path).stem
+        if sid not in imported["A"] or sid not in imported["B"]:
+            log.warning("skipping shape %s: not present in feature files", sid)
+            continue
+        ids.append(sid)
+        labels[sid] = label
+        for ch in CHANNELS:
+            mats[ch].append(imported[ch][sid].matrix(ch))
+    if not ids:
+        raise AllShapesFailed("every shape in the manifest failed to build")
+    va, vb = np.stack(mats["A"]), np.stack(mats["B"])
+    same = va.shape == vb.shape and np.array_equal(va, vb)
+    return build_index_from_views(va, ids, config, views_b=None if same else vb, labels=labels,
+                                  codebooks=codebooks)
+
+
+# ------------------------------------------------------------------ query
+def _viewset_mats(bundle, target):
+    if isinstance(target, ft.ViewSet):
+        try:
+            ma_ = target.matrix("A")
+            mb_ = target.matrix("B")
+        except KeyError as exc:
+            raise ChannelMismatch(f"query lacks channel {exc.args[0]!r}") from exc
+        return ma_, mb_, target.shape_id
+    if isinstance(target, np.ndarray) or torch.is_tensor(target):
+        return target, target, ""
+    raise ChannelMismatch("queries must be view sets or feature matrices "
+                          "(mesh rendering is outside the GPU path)")
+
+
+def query(bundle: IndexBundle, target, top_k: int = 10, exact: bool = False,
+          rerank: bool = True):
+    """Rank database shapes for one query view set (index.py:261-299).
+    Returns ([(shape_id, score, label)], {"render": s, "match": s})."""
+    if bundle.n_shapes == 0:
+        raise EmptyIndex("index holds no shapes")
+    if exact:
+        raise Unsupported("exact Hausdorff ranking is outside the GPU path (SURVEY.md §8(f))")
+    eng = bundle.engine
+    ma_, mb_, sid = _viewset_mats(bundle, target)
+    t0 = time.perf_counter()
+    qa = mt._as_query_tensor(ma_, bundle.fifs["A"].dim)[None]
+    qb = None
+    if not (eng.dup and (mb_ is ma_ or np.array_equal(np.asarray(ma_), np.asarray(mb_)))):
+        qb = mt._as_query_tensor(mb_, bundle.fifs["B"].dim)[None]
+    self_local = torch.tensor([eng.ord_of.get(sid, -1)], dtype=torch.int32, device=qa.device)
+    idx, val = eng.run(qa, qb, top_k=top_k, rerank=rerank, self_local=self_local)
+    idx, val = idx.cpu().numpy(), val.cpu().numpy()
+    t1 = time.perf_counter()
+    return eng.results(idx[0], val[0]), {"render": 0.0, "match": t1 - t0}
+
+
+def query_by_id(bundle: IndexBundle, shape_id: str, top_k: int = 10, exact: bool = False,
+                rerank: bool = True):
+    """Query with a database shape's stored views, recovered cell-major with
+    zero views absent (index.py:302-314)."""
+    if shape_id not in bundle.engine.ord_of:
+        raise EmptyIndex(f"unknown shape id {shape_id!r}")
+    o = bundle.engine.ord_of[shape_id]
+    vs = ft.ViewSet(shape_id=shape_id)
+    for ch in CHANNELS:
+        mat = bundle.viewset_matrix(ch, o)
+        vs.descriptors[ch] = [ft.ViewDescriptor(values=row.astype(np.float32), channel=ch)
+                              for row in mat]
+    return query(bundle, vs, top_k=top_k, exact=exact, rerank=rerank)
+
+
+def rerank_scores(bundle: IndexBundle, channel_scores: dict) -> np.ndarray:
+    """Contextual re-ranked similarity from per-channel match scores
+    (index.py:249-258)."""
+    dev = nat.device()
+    sa = torch.from_numpy(np.asarray(channel_scores["A"], dtype=np.float64)[None].copy()).to(dev)
+    if np.array_equal(channel_scores["A"], channel_scores["B"]):
+        sb = sa
+    else:
+        sb = torch.from_numpy(np.asarray(channel_scores["B"], dtype=np.float64)[None].copy()).to(dev)
+    return bundle.engine.rerank(sa, sb)[0].cpu().numpy()
+
+
+def query_batch(bundle: IndexBundle, views, top_k: int = 10, rerank: bool = True,
+                self_ids=None, views_b=None):
+    """Batched `query` (new): views [B, V, d] (host or device) -> list of
+    result lists, identical to calling `query` on each view set."""
+    eng = bundle.engine
+    Qa = views if torch.is_tensor(views) else torch.from_numpy(np.ascontiguousarray(views, np.float32))
+    Qa = Qa.to(nat.device(), dtype=torch.float32)
+    Qb = None
+    if views_b is not None:
+        Qb = views_b if torch.is_tensor(views_b) else torch.from_numpy(
+            np.ascontiguousarray(views_b, np.float32))
+        Qb = Qb.to(nat.device(), dtype=torch.float32)
+    B = Qa.shape[0]
+    selfs = [eng.ord_of.get(s, -1) for s in (self_ids or [""] * B)]
+    self_local = torch.tensor(selfs, dtype=torch.int32, device=Qa.device)
+    out = []
+    bs = bundle.config.batch_size
+    for b0 in range(0, B, bs):
+        b1 = min(B, b0 + bs)
+        idx, val = eng.run(Qa[b0:b1], None if Qb is None else Qb[b0:b1], top_k=top_k,
+                           rerank=rerank, self_local=self_local[b0:b1])
+        idx, val = idx.cpu().numpy(), val.cpu().numpy()
+        out.extend(eng.results(i, v) for i, v in zip(idx, val))
+    return out
+
+
+def query_many(bundle: IndexBundle, views_host: torch.Tensor, top_k: int = 10,
+               rerank: bool = True, batch_size: int | None = None):
+    """Throughput API (new): queries from pinned host memory [Q, V, d] f32,
+    processed in device batches with the host->device copy of batch i+1
+    overlapped with the compute of batch i on a second stream.  Returns host
+    (idx [Q, k] int32 global ordinals, val [Q, k] f64)."""
+    eng = bundle.engine
+    bs = batch_size or bundle.config.batch_size
+    Qn, V, d = views_host.shape
+    k = min(top_k, eng.n)
+    dev = nat.device()
+    comp = torch.cuda.current_stream()
+    copy = torch.cuda.Stream()
+    bufs = [torch.empty((bs, V, d), dtype=torch.float32, device=dev) for _ in range(2)]
+    ready = [torch.cuda.Event() for _ in range(2)]
+    free = [torch.cuda.Event() for _ in range(2)]
+    out_idx = torch.empty((Qn, k), dtype=torch.int32, pin_memory=True)
+    out_val = torch.empty((Qn, k), dtype=torch.float64, pin_memory=True)
+    nb = (Qn + bs - 1) // bs
+
+    def issue(i):
+        s = i % 2
+        b0, b1 = i * bs, min(Qn, (i + 1) * bs)
+        with torch.cuda.stream(copy):
+            copy.wait_event(free[s])
+            bufs[s][: b1 - b0].copy_(views_host[b0:b1], non_blocking=True)
+            ready[s].record(copy)
+
+    free[0].record(comp)
+    free[1].record(comp)
+    if nb:
+        issue(0)
+    for i in range(nb):
+        s = i % 2
+        if i + 1 < nb:
+            issue(i + 1)
+        b0, b1 = i * bs, min(Qn, (i + 1) * bs)
+        comp.wait_event(ready[s])
+        idx, val = eng.run(bufs[s][: b1 - b0], top_k=k, rerank=rerank)
+        free[s].record(comp)
+        out_idx[b0:b1].copy_(idx, non_blocking=True)
+        out_val[b0:b1].copy_(val, non_blocking=True)
+    comp.synchronize()
+    return out_idx.numpy(), out_val.numpy()
+
+
+# ------------------------------------------------------------------ persistence
+def save_bundle(bundle: IndexBundle, out_dir) -> Path:
+    """Versioned directory with deterministic bytes (index.py:360-375)."""
+    out = Path(out_dir)
+    out.mkdir(parents=True, exist_ok=True)
+    cfg = asdict(bundle.config)
+    defaults = IndexConfig()
+    extra = {k: v for k, v in cfg.items()
+             if k not in _REFERENCE_FIELDS and getattr(defaults, k) != v}
+    meta = {"version": bundle.version,
+            "config": {k: cfg[k] for k in _REFERENCE_FIELDS} | extra}
+    with open(out / "config.json", "w", encoding="utf-8") as fh:
+        json.dump(meta, fh, indent=2, sort_keys=True)
+        fh.write("\n")
+    with open(out / "shapes.tsv", "w", encoding="utf-8", newline="\n") as fh:
+        for sid in bundle.shape_ids:
+            fh.write(f"{sid}\t{bundle.labels.get(sid, '')}\n")
+    for ch in CHANNELS:
+        cb.save_codebook(bundle.codebooks[ch], out / f"codebook_{ch}.bin")
+        mt.save_fif(bundle.fifs[ch], out / f"fif_{ch}.bin")
+        rr.save_activations(bundle.raw_activations[ch], out / f"activations_{ch}.bin")
+    rr.save_sif(bundle.sif, out / "sif.bin")
+    return out
+
+
+def load_bundle(index_dir) -> IndexBundle:
+    """index.py:378-414; identical channel files are loaded once."""
+    index_dir = Path(index_dir)
+    try:
+        with open(index_dir / "config.json", encoding="utf-8") as fh:
+            meta = json.load(fh)
+    except FileNotFoundError as exc:
+        raise FormatError(f"no index bundle at {index_dir}") from exc
+    if meta.get("version") != FORMAT_VERSION:
+        raise FormatError(f"unsupported index version {meta.get('version')!r}")
+    known = {f.name for f in fields(IndexConfig)}
+    config = IndexConfig(**{k: v for k, v in meta["config"].items() if k in known})
+    ids, labels = [], {}
+    for line in (index_dir / "shapes.tsv").read_text(encoding="utf-8").splitlines():
+        if not line:
+            continue
+        sid, _, label = line.partition("\t")
+        ids.append(sid)
+        labels[sid] = label
+    raw_bytes = {ch: (index_dir / f"fif_{ch}.bin").read_bytes() for ch in CHANNELS}
+    cbs, fifs, acts = {}, {}, {}
+    for ch in CHANNELS:
+        cbs[ch] = cb.load_codebook(index_dir / f"codebook_{ch}.bin")
+    same = (raw_bytes["A"] == raw_bytes["B"]
+            and np.array_equal(cbs["A"].centroids, cbs["B"].centroids))
+    fifs["A"] = mt.load_fif(index_dir / "fif_A.bin", cbs["A"], config.torch_storage)
+    fifs["B"] = fifs["A"] if same else mt.load_fif(index_dir / "fif_B.bin", cbs["B"],
+                                                   config.torch_storage)
+    act_bytes = {ch: (index_dir / f"activations_{ch}.bin").read_bytes() for ch in CHANNELS}
+    for ch in CHANNELS:
+        if ch == "B" and act_bytes["A"] == act_bytes["B"]:
+            acts["B"] = acts["A"]
+            continue
+        host = rr.load_activations(index_dir / f"activations_{ch}.bin")
+        cap = max([a.support for a in host] + [1])
+        acts[ch] = rr.ActivationList(eg.ActRows.from_host(host, cap), [a.owner for a in host])
+    sif = rr.load_sif(index_dir / "sif.bin")
+    return IndexBundle(config=config, shape_ids=ids, labels=labels, codebooks=cbs, fifs=fifs,
+                       raw_activations=acts, sif=sif, version=meta["version"])

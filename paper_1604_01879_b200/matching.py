@@ -1,0 +1,214 @@
+"""First inverted file: GPU build and batched scoring.
+
+Mirrors `shapesearch.matching` (matching.py:64-211): FirstInvertedFile,
+build_fif, query_fif, save_fif/load_fif.  The exact-Hausdorff helpers
+(matching.py:22-61) are outside the GPU path.
+"""
+
+from __future__ import annotations
+
+import struct
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from . import engine as eg
+from .codebook import Codebook
+from .errors import DimensionMismatch, EmptySet, FormatError
+
+DEFAULT_MA = 2
+_RUNNER = None
+
+
+def runner() -> eg.ScoreRunner:
+    global _RUNNER
+    if _RUNNER is None:
+        _RUNNER = eg.ScoreRunner()
+    return _RUNNER
+
+
+def sim_mode(similarity: str) -> int:
+    if similarity == "cosine":
+        return nat.SIM_COSINE
+    if similarity == "gaussian":
+        return nat.SIM_GAUSSIAN
+    raise ValueError(f"unknown similarity {similarity!r}")
+
+
+class FirstInvertedFile:
+    """Codeword-indexed postings of (shape ordinal, stored view feature),
+    resident on the GPU as a cell-major CSR (engine.DeviceFif).  The
+    reference's list attributes are materialized on demand."""
+
+    def __init__(self, codebook: Codebook, shape_ids, n_views: int, dev: eg.DeviceFif):
+        self.codebook = codebook
+        self.shape_ids = list(shape_ids)
+        self.n_views = n_views
+        self.dev = dev
+        self._host = None
+
+    @property
+    def k(self) -> int:
+        return self.codebook.k
+
+    @property
+    def dim(self) -> int:
+        return self.codebook.dim
+
+    @property
+    def n_shapes(self) -> int:
+        return len(self.shape_ids)
+
+    @property
+    def total_postings(self) -> int:
+        return self.dev.P
+
+    def _lists(self):
+        if self._host is None:
+            self._host = self.dev.host_lists()
+        return self._host
+
+    @property
+    def entry_ordinals(self):
+        return self._lists()[0]
+
+    @property
+    def entry_features(self):
+        return self._lists()[1]
+
+    def shape_matrix(self, ordinal: int) -> np.ndarray:
+        """Stored views of one shape, gathered cell-major (matching.py:94-103)."""
+        loc = ordinal - self.dev.ord_base
+        if not 0 <= loc < self.dev.n_local:
+            raise EmptySet(f"shape ordinal {ordinal} has no stored views")
+        lo, hi = (int(v) for v in self.dev.shape_off[loc:loc + 2].cpu())
+        if hi == lo:
+            raise EmptySet(f"shape ordinal {ordinal} has no stored views")
+        Q, _vq = self.dev.shape_views(torch.tensor([loc], device=self.dev.feat.device))
+        return Q[0].cpu().numpy()
+
+
+def _stack_views(viewsets, channel, dim):
+    mats = []
+    for vs in viewsets:
+        mat = vs.matrix(channel)
+        if mat.shape[1] != dim:
+            raise DimensionMismatch(f"shape {vs.shape_id!r} dim {mat.shape[1]} != codebook dim {dim}")
+        mats.append(np.asarray(mat, dtype=np.float32))
+    V = max(m.shape[0] for m in mats)
+    X = np.zeros((len(mats), V, dim), dtype=np.float32)
+    for i, m in enumerate(mats):
+        X[i, : m.shape[0]] = m
+    return X, V
+
+
+def build_fif(viewsets, codebook: Codebook, channel: str,
+              storage_dtype=torch.float32) -> FirstInvertedFile:
+    """Store each non-empty view once, under its nearest codeword
+    (matching.py:106-133) — K1 quantize + K2 device radix-sort layout."""
+    viewsets = list(viewsets)
+    X, V = _stack_views(viewsets, channel, codebook.dim)
+    dev = nat.device()
+    Xd = torch.from_numpy(X).to(dev).to(storage_dtype)
+    d = eg.DeviceFif.build(Xd, codebook.device())
+    return FirstInvertedFile(codebook, [vs.shape_id for vs in viewsets], V, d)
+
+
+def build_fif_from_tensor(X: torch.Tensor, codebook: Codebook, shape_ids,
+                          ord_base: int = 0) -> FirstInvertedFile:
+    """Build from a device tensor [n, V, d] (f32 or f16 storage)."""
+    d = eg.DeviceFif.build(X, codebook.device(), ord_base=ord_base)
+    return FirstInvertedFile(codebook, shape_ids, X.shape[1], d)
+
+
+def _as_query_tensor(query_views, dim):
+    if torch.is_tensor(query_views):
+        q = query_views
+    else:
+        arr = np.asarray(query_views, dtype=np.float64)
+        if arr.ndim != 2 or arr.shape[0] == 0:
+            raise EmptySet("view set is empty")
+        q = torch.from_numpy(arr.astype(np.float32))
+    if q.dim() != 2 or q.shape[0] == 0:
+        raise EmptySet("view set is empty")
+    if q.shape[1] != dim:
+        raise DimensionMismatch(f"query dim {q.shape[1]} != index dim {dim}")
+    return q.to(nat.device(), dtype=torch.float32)
+
+
+def query_fif(fif: FirstInvertedFile, query_views, ma: int = DEFAULT_MA,
+              similarity: str = "cosine", sigma: float = 0.5) -> np.ndarray:
+    """Approximate similarity of one query view set against every shape
+    (matching.py:136-161).  Query views are scored as f32 (stored features
+    are f32); scores are f64."""
+    q = _as_query_tensor(query_views, fif.dim)
+    s = runner().score(fif.dev, q[None], ma, sim_mode(similarity), sigma)
+    return s[0].cpu().numpy()
+
+
+def query_fif_batch(fif: FirstInvertedFile, Q, ma: int = DEFAULT_MA, similarity: str = "cosine",
+                    sigma: float = 0.5, vq=None) -> torch.Tensor:
+    """Batched scores: Q [B, V, d] -> device f64 [B, n_local] (new API)."""
+    if not torch.is_tensor(Q):
+        Q = torch.from_numpy(np.ascontiguousarray(Q, dtype=np.float32))
+    Q = Q.to(nat.device(), dtype=torch.float32)
+    return runner().score(fif.dev, Q, ma, sim_mode(similarity), sigma, vq=vq)
+
+
+def save_fif(fif: FirstInvertedFile, path) -> None:
+    """matching.py:164-175 byte layout."""
+    ords, feats = fif.entry_ordinals, fif.entry_features
+    with open(path, "wb") as fh:
+        fh.write(struct.pack("<III", fif.k, fif.dim, fif.n_views))
+        fh.write(struct.pack("<I", fif.n_shapes))
+        for sid in fif.shape_ids:
+            raw = sid.encode("utf-8")
+            fh.write(struct.pack("<H", len(raw)))
+            fh.write(raw)
+        for o, f in zip(ords, feats):
+            fh.write(struct.pack("<I", len(o)))
+            fh.write(np.asarray(o).astype("<u4").tobytes())
+            fh.write(np.asarray(f).astype("<f4").tobytes())
+
+
+def load_fif(path, codebook: Codebook, storage_dtype=torch.float32) -> FirstInvertedFile:
+    """matching.py:178-211: read the lists, rebuild the device layout."""
+    data = open(path, "rb").read()
+    off = 0
+
+    def take(fmt):
+        nonlocal off
+        size = struct.calcsize(fmt)
+        if off + size > len(data):
+            raise FormatError(f"truncated inverted file {path}")
+        out = struct.unpack_from(fmt, data, off)
+        off += size
+        return out
+
+    k, dim, n_views = take("<III")
+    if k != codebook.k or dim != codebook.dim:
+        raise DimensionMismatch(f"inverted file {path} does not match codebook")
+    (n_shapes,) = take("<I")
+    ids = []
+    for _ in range(n_shapes):
+        (n,) = take("<H")
+        ids.append(data[off:off + n].decode("utf-8"))
+        off += n
+    counts, ords, feats = [], [], []
+    for _ in range(k):
+        (cnt,) = take("<I")
+        if off + cnt * 4 * (1 + dim) > len(data):
+            raise FormatError(f"truncated inverted file {path}")
+        ords.append(np.frombuffer(data, dtype="<u4", count=cnt, offset=off).astype(np.int32))
+        off += cnt * 4
+        feats.append(np.frombuffer(data, dtype="<f4", count=cnt * dim, offset=off).reshape(cnt, dim))
+        off += cnt * dim * 4
+        counts.append(cnt)
+    dev = nat.device()
+    cell_off = torch.tensor(np.concatenate([[0], np.cumsum(counts)]), dtype=torch.int64, device=dev)
+    post_ord = torch.from_numpy(np.concatenate(ords) if ords else np.zeros(0, np.int32)).to(dev)
+    feat = torch.from_numpy(np.concatenate(feats) if feats else np.zeros((0, dim), np.float32))
+    d = eg.DeviceFif.from_arrays(codebook.device(), cell_off, post_ord,
+                                 feat.to(dev).to(storage_dtype), n_shapes, n_views)
+    return FirstInvertedFile(codebook, ids, n_views, d)

@@ -1,0 +1,62 @@
+"""Deterministic input builders shared by make_golden.py and the tests.
+
+Pure numpy (`default_rng` streams are machine-independent), so the GPU box
+regenerates exactly the inputs the committed golden outputs were computed on.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def unit_nonneg_rows(rng, n, d):
+    """Random unit-norm non-negative f32 rows (like the reference fixtures,
+    conftest.py:5-16)."""
+    v = rng.random((n, d))
+    v /= np.linalg.norm(v, axis=1, keepdims=True)
+    return v.astype(np.float32)
+
+
+def mixture_views(seed, n_shapes, n_views, dim, n_classes, sigma=0.3, mu0=0.0,
+                  zero_views=0, n_queries=0):
+    """Gaussian-mixture view sets (BASELINE.json config 1 generator, small):
+    class means ~ N(mu0, 1); each shape's views = normalize(relu(mean +
+    sigma * N(0, 1))); f32.  `zero_views` rows are zeroed at seeded spots.
+    The first n_shapes rows are the database, the next n_queries the queries
+    (same class means)."""
+    rng = np.random.default_rng(seed)
+    means = rng.standard_normal((n_classes, dim)) + mu0
+    n_shapes = n_shapes + n_queries
+    labels = rng.integers(0, n_classes, size=n_shapes)
+    x = means[labels][:, None, :] + sigma * rng.standard_normal((n_shapes, n_views, dim))
+    x = np.maximum(x, 0.0)
+    nrm = np.linalg.norm(x, axis=2, keepdims=True)
+    nrm[nrm == 0] = 1.0
+    x = (x / nrm).astype(np.float32)
+    if zero_views:
+        flat = rng.choice(n_shapes * n_views, size=zero_views, replace=False)
+        x.reshape(-1, dim)[flat] = 0.0
+    return x, labels
+
+
+def sampled_codebook(views, k, seed):
+    """K distinct non-zero DB view rows sampled without replacement (SURVEY.md
+    §8(d) 'Codebooks'; stands in for k-means, divergence D3)."""
+    rng = np.random.default_rng(seed)
+    flat = views.reshape(-1, views.shape[-1])
+    nz = np.flatnonzero(flat.any(axis=1))
+    pick = rng.choice(nz, size=k, replace=False)
+    return flat[np.sort(pick)].astype(np.float32)
+
+
+def shape_ids(n, prefix="s"):
+    width = max(4, len(str(n)))
+    return [f"{prefix}{i:0{width}d}" for i in range(n)]
+
+
+# End-to-end cases: (name, seed, N, V, d, classes, K, ma, k1, k2, n_queries, top_k, zero_views)
+E2E_CASES = [
+    ("tiny", 11, 24, 6, 16, 4, 5, 2, 4, 2, 6, 10, 3),
+    ("small", 12, 120, 8, 32, 8, 12, 2, 6, 3, 10, 20, 0),
+    ("c1like", 13, 400, 16, 64, 12, 16, 1, 10, 4, 12, 50, 0),
+]

@@ -1,0 +1,227 @@
+"""Generate the golden vectors under tests/golden/ by running the REFERENCE
+implementation (`shapesearch`, /root/reference/pkg/src) on seeded inputs.
+
+Run in the build container (the reference does not travel to the GPU box):
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+Only reference public functions are called; the index bundle is assembled
+from them the way index.build_index does (index.py:185-227) except that the
+codebook is a sampled one (SURVEY.md divergence D3) and the one feature set
+feeds both channels (D4).
+"""
+
+from __future__ import annotations
+
+import io
+import os
+import sys
+import tempfile
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from cases import E2E_CASES, mixture_views, sampled_codebook, shape_ids, unit_nonneg_rows  # noqa: E402
+from shapesearch import codebook as rcb  # noqa: E402
+from shapesearch import features as rft  # noqa: E402
+from shapesearch import index as rix  # noqa: E402
+from shapesearch import matching as rmt  # noqa: E402
+from shapesearch import rerank as rrr  # noqa: E402
+
+
+def as_viewset(sid, mat, channels=("A", "B")):
+    vs = rft.ViewSet(shape_id=sid)
+    for ch in channels:
+        for row in mat:
+            vs.add(ch, rft.ViewDescriptor(values=np.asarray(row, dtype=np.float32), channel=ch))
+    return vs
+
+
+def golden_quantize():
+    rng = np.random.default_rng(2024)
+    out = {}
+    cases = []
+    # 1. generic f64 inputs
+    C = rng.random((10, 8)).astype(np.float32)
+    X = rng.random((40, 8))
+    cases += [(C, X, 1), (C, X, 2), (C, X, 10)]
+    # 2. duplicated centroids (exact ties -> lower index) + exact centroid queries
+    C2 = rng.random((9, 6)).astype(np.float32)
+    C2[4] = C2[1]
+    C2[7] = C2[1]
+    X2 = np.concatenate([C2.astype(np.float64), rng.random((12, 6))])
+    cases += [(C2, X2, 1), (C2, X2, 3), (C2, X2, 9)]
+    # 3. odd dims / pairwise tree shapes
+    for d, k, ma in ((5, 7, 7), (129, 12, 2), (300, 20, 3), (1000, 16, 2)):
+        Cd = unit_nonneg_rows(rng, k, d)
+        Xd = unit_nonneg_rows(rng, 24, d).astype(np.float64)
+        cases.append((Cd, Xd, ma))
+    # 4. mixture rows at d = 4096 (config 2 dimension), f32 queries
+    views, _ = mixture_views(77, 40, 4, 4096, 6, mu0=-0.26)
+    Cm = sampled_codebook(views, 64, 5)
+    Xm = views.reshape(-1, 4096)[:96].astype(np.float64)
+    cases += [(Cm, Xm, 1), (Cm, Xm, 2)]
+    for i, (C, X, ma) in enumerate(cases):
+        cb = rcb.Codebook(centroids=C)
+        res = np.stack([rcb.quantize(cb, x, ma=ma) for x in X])
+        out[f"c{i}_C"] = C
+        out[f"c{i}_X"] = X
+        out[f"c{i}_ma"] = np.int64(ma)
+        out[f"c{i}_out"] = res.astype(np.int64)
+    out["n_cases"] = np.int64(len(cases))
+    np.savez_compressed(os.path.join(HERE, "quantize.npz"), **out)
+
+
+def golden_fif():
+    out = {}
+    views, _ = mixture_views(31, 12, 6, 16, 3, zero_views=3, n_queries=4)
+    db, qs = views[:12], views[12:]
+    ids = shape_ids(12)
+    for tag, k in (("k5", 5), ("k1", 1)):
+        C = sampled_codebook(db, k, 3)
+        cb = rcb.Codebook(centroids=C, channel="A")
+        vsets = [as_viewset(ids[i], db[i], ("A",)) for i in range(12)]
+        fif = rmt.build_fif(vsets, cb, "A")
+        with tempfile.TemporaryDirectory() as td:
+            path = os.path.join(td, "fif.bin")
+            rmt.save_fif(fif, path)
+            out[f"{tag}_fif_bytes"] = np.frombuffer(open(path, "rb").read(), dtype=np.uint8)
+        out[f"{tag}_C"] = C
+        lens = [len(o) for o in fif.entry_ordinals]
+        out[f"{tag}_entry_len"] = np.array(lens, dtype=np.int64)
+        out[f"{tag}_entry_ord"] = np.concatenate(fif.entry_ordinals).astype(np.int32)
+        out[f"{tag}_entry_feat"] = np.concatenate(fif.entry_features).astype(np.float32)
+        for ma in sorted({1, min(2, k), k}):
+            sc = np.stack([rmt.query_fif(fif, q, ma=ma) for q in list(qs) + list(db[:3])])
+            out[f"{tag}_scores_ma{ma}"] = sc
+        out[f"{tag}_shape_matrix_0"] = fif.shape_matrix(0)
+    out["db"] = db
+    out["queries"] = qs
+    np.savez_compressed(os.path.join(HERE, "fif.npz"), **out)
+
+
+def golden_rerank():
+    rng = np.random.default_rng(4242)
+    out = {}
+    # build_activation / top_neighbors on scores with ties and zeros
+    S = np.round(rng.random((6, 30)), 2)
+    S[:, rng.choice(30, 8, replace=False)] = 0.0
+    S[1] = 0.0
+    out["scores"] = S
+    for k in (1, 4, 10, 40):
+        acts = [rrr.build_activation(s, k) for s in S]
+        out[f"act_k{k}_idx"] = [a.indices for a in acts] and np.concatenate([a.indices for a in acts])
+        out[f"act_k{k}_len"] = np.array([a.support for a in acts])
+        out[f"act_k{k}_val"] = np.concatenate([a.values for a in acts])
+        out[f"act_k{k}_norm"] = np.array([a.norm for a in acts])
+        nb = [rrr.top_neighbors(s, k) for s in S]
+        out[f"nbr_k{k}_len"] = np.array([len(x) for x in nb])
+        out[f"nbr_k{k}"] = np.array(sum(nb, []), dtype=np.int64)
+    # co_augment over random activations / neighbourhoods
+    n = 16
+    def rand_act(owner):
+        sup = rng.choice(n, size=int(rng.integers(1, 6)), replace=False)
+        return rrr.make_activation(owner, sup, rng.random(len(sup)) * 0.9 + 0.1)
+    a1 = [rand_act(f"a{i}") for i in range(n)]
+    a2 = [rand_act(f"b{i}") for i in range(n)]
+    n1 = [list(rng.choice(n, size=int(rng.integers(0, 4)), replace=False)) for _ in range(n)]
+    n2 = [list(rng.choice(n, size=int(rng.integers(0, 4)), replace=False)) for _ in range(n)]
+    c1, c2 = rrr.co_augment(a1, a2, n1, n2)
+    def pack(prefix, acts):
+        out[f"{prefix}_len"] = np.array([a.support for a in acts])
+        out[f"{prefix}_idx"] = np.concatenate([a.indices for a in acts])
+        out[f"{prefix}_val"] = np.concatenate([a.values for a in acts])
+        out[f"{prefix}_norm"] = np.array([a.norm for a in acts])
+    pack("a1", a1)
+    pack("a2", a2)
+    out["n1_len"] = np.array([len(x) for x in n1])
+    out["n1"] = np.array(sum(n1, []), dtype=np.int64)
+    out["n2_len"] = np.array([len(x) for x in n2])
+    out["n2"] = np.array(sum(n2, []), dtype=np.int64)
+    pack("co1", c1)
+    pack("co2", c2)
+    for alpha in (0.25, 0.5, 1.0, 2.0):
+        pack(f"agg{alpha}", [rrr.aggregate(x, y, alpha) for x, y in zip(c1, c2)])
+    sif = rrr.build_sif(c1)
+    out["sif_len"] = np.array([len(o) for o in sif.entry_ordinals])
+    out["sif_ord"] = np.concatenate(sif.entry_ordinals)
+    out["sif_val"] = np.concatenate(sif.entry_values)
+    out["sif_norms"] = sif.norms
+    out["sif_scores"] = np.stack([rrr.query_sif(sif, q) for q in c1 + c2])
+    np.savez_compressed(os.path.join(HERE, "rerank.npz"), **out)
+
+
+def reference_bundle(db, ids, C, cfg):
+    """index.py:185-227 with a given codebook; channel B = channel A."""
+    vsets = [as_viewset(ids[i], db[i]) for i in range(len(ids))]
+    codebooks, fifs = {}, {}
+    for ch in rix.CHANNELS:
+        codebooks[ch] = rcb.Codebook(centroids=C, channel=ch, seed=cfg.seed)
+        fifs[ch] = rmt.build_fif(vsets, codebooks[ch], ch)
+    scores = {ch: [rmt.query_fif(fifs[ch], vs.matrix(ch), ma=cfg.ma) for vs in vsets]
+              for ch in rix.CHANNELS}
+    raw = {ch: [rrr.build_activation(scores[ch][i], cfg.k1, owner=ids[i]) for i in range(len(ids))]
+           for ch in rix.CHANNELS}
+    nbr = {ch: [rrr.top_neighbors(scores[ch][i], cfg.k2) for i in range(len(ids))]
+           for ch in rix.CHANNELS}
+    aa, ab = rrr.co_augment(raw["A"], raw["B"], nbr["A"], nbr["B"])
+    final = [rrr.aggregate(x, y, cfg.alpha) for x, y in zip(aa, ab)]
+    sif = rrr.build_sif(final, shape_ids=ids)
+    bundle = rix.IndexBundle(config=cfg, shape_ids=list(ids), labels={i: "" for i in ids},
+                             codebooks=codebooks, fifs=fifs, raw_activations=raw, sif=sif)
+    return bundle, scores, raw, nbr, final
+
+
+def golden_e2e():
+    for (name, seed, N, V, d, classes, K, ma, k1, k2, nq, top_k, zv) in E2E_CASES:
+        views, _ = mixture_views(seed, N, V, d, classes, zero_views=zv, n_queries=nq)
+        db, qs = views[:N], views[N:]
+        ids = shape_ids(N)
+        C = sampled_codebook(db, K, seed + 1)
+        cfg = rix.IndexConfig(n_views=V, codebook_size=K, ma=ma, k1=k1, k2=k2, imported=True)
+        bundle, scores, raw, nbr, final = reference_bundle(db, ids, C, cfg)
+        out = {"C": C}
+        out["db_scores"] = np.stack(scores["A"]) if N <= 200 else np.zeros(0)
+        out["raw_len"] = np.array([a.support for a in raw["A"]])
+        out["raw_idx"] = np.concatenate([a.indices for a in raw["A"]])
+        out["raw_val"] = np.concatenate([a.values for a in raw["A"]])
+        out["raw_norm"] = np.array([a.norm for a in raw["A"]])
+        out["nbr_len"] = np.array([len(x) for x in nbr["A"]])
+        out["nbr"] = np.array(sum(nbr["A"], []), dtype=np.int64)
+        out["final_len"] = np.array([a.support for a in final])
+        out["final_idx"] = np.concatenate([a.indices for a in final])
+        out["final_val"] = np.concatenate([a.values for a in final])
+        out["final_norm"] = np.array([a.norm for a in final])
+        for rerank in (True, False):
+            tag = "rr" if rerank else "nr"
+            rid, rsc = [], []
+            for q in qs:
+                res, _t = rix.query(bundle, as_viewset("query", q), top_k=top_k, rerank=rerank)
+                rid.append([ids.index(r[0]) for r in res])
+                rsc.append([r[1] for r in res])
+            out[f"q_{tag}_ids"] = np.array(rid, dtype=np.int64)
+            out[f"q_{tag}_scores"] = np.array(rsc)
+            bid, bsc = [], []
+            for i in range(0, N, max(1, N // 8)):
+                res, _t = rix.query_by_id(bundle, ids[i], top_k=top_k, rerank=rerank)
+                bid.append([ids.index(r[0]) for r in res])
+                bsc.append([r[1] for r in res])
+            out[f"id_{tag}_ids"] = np.array(bid, dtype=np.int64)
+            out[f"id_{tag}_scores"] = np.array(bsc)
+        out["q_fif_scores"] = np.stack([rmt.query_fif(bundle.fifs["A"], q, ma=ma) for q in qs])
+        out["q_rerank_scores"] = np.stack([
+            rix.rerank_scores(bundle, {"A": s, "B": s})
+            for s in out["q_fif_scores"]])
+        np.savez_compressed(os.path.join(HERE, f"e2e_{name}.npz"), **out)
+        print(name, "done")
+
+
+if __name__ == "__main__":
+    golden_quantize()
+    print("quantize done")
+    golden_fif()
+    print("fif done")
+    golden_rerank()
+    print("rerank done")
+    golden_e2e()

@@ -1,0 +1,341 @@
+"""GPU parity: the CUDA path (through libgift.so) against the reference's
+golden vectors and the CPU oracle on the same seeded inputs."""
+
+import io
+import os
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from cases import E2E_CASES, mixture_views, sampled_codebook, shape_ids, unit_nonneg_rows
+from conftest import load_golden
+from helpers import RTOL, assert_act_close, assert_ranking_close, unpack_acts, unpack_lists
+
+pytestmark = pytest.mark.gpu
+
+import paper_1604_01879_b200 as gift  # noqa: E402
+from paper_1604_01879_b200 import engine as eg  # noqa: E402
+from paper_1604_01879_b200 import matching as mt  # noqa: E402
+from paper_1604_01879_b200 import rerank as rr  # noqa: E402
+from paper_1604_01879_b200.codebook import Codebook, quantize, quantize_batch  # noqa: E402
+from paper_1604_01879_b200.errors import DimensionMismatch, EmptySet  # noqa: E402
+from paper_1604_01879_b200.features import ViewSet  # noqa: E402
+
+
+def dev():
+    return torch.device("cuda", 0)
+
+
+# ---------------------------------------------------------------- K1 quantize
+def test_quantize_bit_exact_golden():
+    g = load_golden("quantize.npz")
+    for i in range(int(g["n_cases"])):
+        C, X, ma, out = g[f"c{i}_C"], g[f"c{i}_X"], int(g[f"c{i}_ma"]), g[f"c{i}_out"]
+        cb = Codebook(C)
+        got = quantize_batch(cb, X, ma)  # f64 inputs
+        np.testing.assert_array_equal(got, out, err_msg=f"case {i}")
+        if np.array_equal(X.astype(np.float32).astype(np.float64), X):
+            np.testing.assert_array_equal(quantize_batch(cb, X.astype(np.float32), ma), out)
+        np.testing.assert_array_equal(quantize(cb, X[0], ma), out[0])
+
+
+@pytest.mark.parametrize("K,d,ma", [(256, 4096, 2), (1024, 4096, 2), (64, 256, 1), (4096, 1024, 1)])
+def test_quantize_bit_exact_vs_oracle_config_shapes(K, d, ma):
+    views, _ = mixture_views(K + d, 300, 8, d, 20, mu0=-0.26)
+    C = sampled_codebook(views, K, 1)
+    X = mixture_views(K + d + 1, 120, 8, d, 20, mu0=-0.26)[0].reshape(-1, d)
+    got = quantize_batch(Codebook(C), X, ma)
+    np.testing.assert_array_equal(got, oracle.quantize_many(C, X, ma))
+
+
+def test_quantize_fp16_rows_and_ties():
+    rng = np.random.default_rng(3)
+    C = unit_nonneg_rows(rng, 32, 1024).astype(np.float16).astype(np.float32)
+    C[5] = C[17]  # exact duplicate: lower index wins
+    X = np.concatenate([C[:8], unit_nonneg_rows(rng, 200, 1024)]).astype(np.float16)
+    got = quantize_batch(Codebook(C), torch.from_numpy(X), 3)
+    np.testing.assert_array_equal(got, oracle.quantize_many(C, X.astype(np.float64), 3))
+
+
+def test_quantize_errors():
+    cb = Codebook(np.eye(4, dtype=np.float32))
+    with pytest.raises(DimensionMismatch):
+        quantize(cb, np.zeros(5))
+    with pytest.raises(ValueError):
+        quantize(cb, np.zeros(4), ma=5)
+
+
+# ---------------------------------------------------------------- K2 build
+def _viewsets(db, ids, channels=("A", "B")):
+    return [ViewSet.from_matrix(s, m, channels) for s, m in zip(ids, db)]
+
+
+@pytest.mark.parametrize("tag", ["k5", "k1"])
+def test_build_fif_bit_exact_golden(tag):
+    g = load_golden("fif.npz")
+    db = g["db"]
+    ids = shape_ids(len(db))
+    fif = mt.build_fif(_viewsets(db, ids, ("A",)), Codebook(g[f"{tag}_C"], "A"), "A")
+    np.testing.assert_array_equal([len(o) for o in fif.entry_ordinals], g[f"{tag}_entry_len"])
+    np.testing.assert_array_equal(np.concatenate(fif.entry_ordinals), g[f"{tag}_entry_ord"])
+    np.testing.assert_array_equal(np.concatenate(fif.entry_features), g[f"{tag}_entry_feat"])
+    np.testing.assert_array_equal(fif.shape_matrix(0), g[f"{tag}_shape_matrix_0"])
+    with tempfile.TemporaryDirectory() as td:
+        p = os.path.join(td, "fif.bin")
+        mt.save_fif(fif, p)
+        assert open(p, "rb").read() == g[f"{tag}_fif_bytes"].tobytes()
+        loaded = mt.load_fif(p, Codebook(g[f"{tag}_C"], "A"))
+        q = g["queries"][0]
+        np.testing.assert_array_equal(mt.query_fif(loaded, q, 2 if tag == "k5" else 1),
+                                      mt.query_fif(fif, q, 2 if tag == "k5" else 1))
+    # K3 scores against the reference
+    K = len(g[f"{tag}_entry_len"])
+    queries = list(g["queries"]) + list(db[:3])
+    for ma in sorted({1, min(2, K), K}):
+        got = np.stack([mt.query_fif(fif, q, ma) for q in queries])
+        np.testing.assert_allclose(got, g[f"{tag}_scores_ma{ma}"], rtol=RTOL, atol=1e-7)
+        ref = g[f"{tag}_scores_ma{ma}"]
+        assert ((got == 0) == (ref == 0)).all()  # unvisited shapes score exactly 0
+
+
+def test_build_fif_large_bit_exact_vs_oracle():
+    """C2-shaped cells (d=4096, K=256) on 400 shapes: lists bit-exact."""
+    views, _ = mixture_views(99, 400, 16, 4096, 55, mu0=-0.26)
+    C = sampled_codebook(views, 256, 2)
+    assign = oracle.quantize_many(C, views.reshape(-1, 4096), 1).reshape(400, 16)
+    ref = oracle.build_fif(list(views), C, assign=assign)
+    fif = mt.build_fif_from_tensor(torch.from_numpy(views).to(dev()), Codebook(C), shape_ids(400))
+    for a, b in zip(fif.entry_ordinals, ref.entry_ordinals):
+        np.testing.assert_array_equal(a, b)
+    np.testing.assert_array_equal(np.concatenate(fif.entry_features),
+                                  np.concatenate(ref.entry_features))
+
+
+# ---------------------------------------------------------------- K3 score
+@pytest.mark.parametrize("similarity", ["cosine", "gaussian"])
+@pytest.mark.parametrize("ma", [1, 2])
+def test_query_fif_vs_oracle_c1_shapes(similarity, ma):
+    """Config-1 shapes (d=256, K=64) at N=300: scores within 1e-5 rel."""
+    views, _ = mixture_views(7, 300, 64, 256, 40, n_queries=6)
+    db, qs = views[:300], views[300:]
+    C = sampled_codebook(db, 64, 3)
+    assign = oracle.quantize_many(C, db.reshape(-1, 256), 1).reshape(300, 64)
+    ref = oracle.build_fif(list(db), C, assign=assign)
+    fif = mt.build_fif_from_tensor(torch.from_numpy(db).to(dev()), Codebook(C), shape_ids(300))
+    got = mt.query_fif_batch(fif, qs, ma, similarity).cpu().numpy()
+    for q, g in zip(qs, got):
+        cells = oracle.quantize_many(C, q.astype(np.float64), ma)
+        e = oracle.query_fif(ref, q, ma, similarity, cells=cells)
+        np.testing.assert_allclose(g, e, rtol=RTOL, atol=1e-9)
+        assert ((g == 0) == (e == 0)).all()
+
+
+def test_query_fif_degeneracy_and_bounds():
+    """K=1 and ma=K equal the exact mean-of-max similarity; scores
+    lower-bound it and grow with ma (test_matching.py:127-162)."""
+    rng = np.random.default_rng(5)
+    mats = np.stack([unit_nonneg_rows(rng, 6, 24) for _ in range(12)])
+    exact = np.array([[np.clip(q.astype(np.float64) @ p.astype(np.float64).T, 0, 1).max(1).mean()
+                       for p in mats] for q in mats])
+    C = sampled_codebook(mats, 5, 0)
+    for K in (1, 5):
+        fif = mt.build_fif_from_tensor(torch.from_numpy(mats).to(dev()), Codebook(C[:K]),
+                                       shape_ids(12))
+        prev = None
+        for ma in range(1, K + 1):
+            s = mt.query_fif_batch(fif, mats, ma).cpu().numpy()
+            assert (s <= exact + 1e-6).all()
+            if prev is not None:
+                assert (s >= prev - 1e-7).all()
+            prev = s
+        np.testing.assert_allclose(prev, exact, rtol=RTOL, atol=1e-7)
+        assert (prev.argmax(axis=1) == np.arange(12)).all()  # self-retrieval
+
+
+def test_zero_views_skipped_and_counted():
+    rng = np.random.default_rng(8)
+    mats = np.stack([unit_nonneg_rows(rng, 4, 16) for _ in range(5)])
+    mats[0, 1] = 0.0
+    C = sampled_codebook(mats, 3, 0)
+    fif = mt.build_fif_from_tensor(torch.from_numpy(mats).to(dev()), Codebook(C), shape_ids(5))
+    assert fif.total_postings == 5 * 4 - 1
+    q = mats[2].copy()
+    q[0] = 0.0
+    ref = oracle.build_fif(list(mats), C)
+    np.testing.assert_allclose(mt.query_fif(fif, q, 2), oracle.query_fif(ref, q, 2),
+                               rtol=RTOL, atol=1e-9)
+    with pytest.raises(EmptySet):
+        mt.query_fif(fif, np.zeros((0, 16)), 2)
+
+
+# ---------------------------------------------------------------- K4/K5/K6
+def test_rerank_kernels_golden():
+    g = load_golden("rerank.npz")
+    S = g["scores"]
+    for k in (1, 4, 10, 40):
+        for s, ref in zip(S, unpack_acts(g, f"act_k{k}")):
+            a = rr.build_activation(s, k)
+            np.testing.assert_array_equal(a.indices, ref[0])
+            np.testing.assert_array_equal(a.values, ref[1])
+            assert a.norm == ref[2]
+        for s, ref in zip(S, unpack_lists(g, f"nbr_k{k}", f"nbr_k{k}_len")):
+            assert rr.top_neighbors(s, k) == list(ref)
+    mk = lambda t: [rr.SparseActivation("x", i, v, n) for i, v, n in t]  # noqa: E731
+    a1, a2 = mk(unpack_acts(g, "a1")), mk(unpack_acts(g, "a2"))
+    n1 = [list(map(int, x)) for x in unpack_lists(g, "n1", "n1_len")]
+    n2 = [list(map(int, x)) for x in unpack_lists(g, "n2", "n2_len")]
+    c1, c2 = rr.co_augment(a1, a2, n1, n2)
+    for got, ref in zip(c1, unpack_acts(g, "co1")):  # same f64 op order: bit-exact
+        np.testing.assert_array_equal(got.indices, ref[0])
+        np.testing.assert_array_equal(got.values, ref[1])
+        assert got.norm == ref[2]
+    for got, ref in zip(c2, unpack_acts(g, "co2")):
+        np.testing.assert_array_equal(got.values, ref[1])
+    for alpha in (0.25, 0.5, 1.0, 2.0):
+        for x, y, ref in zip(c1, c2, unpack_acts(g, f"agg{alpha}")):
+            got = rr.aggregate(x, y, alpha)
+            np.testing.assert_array_equal(got.indices, ref[0])
+            np.testing.assert_allclose(got.values, ref[1], rtol=1e-13, atol=0)
+        for x in c1:  # idempotence is exact (rerank.py:142-146)
+            got = rr.aggregate(x, x, alpha)
+            np.testing.assert_array_equal(got.values, x.values)
+    sif = rr.build_sif(c1)
+    np.testing.assert_array_equal([len(o) for o in sif.entry_ordinals], g["sif_len"])
+    np.testing.assert_array_equal(np.concatenate(sif.entry_ordinals), g["sif_ord"])
+    np.testing.assert_array_equal(np.concatenate(sif.entry_values), g["sif_val"])
+    np.testing.assert_array_equal(sif.norms, g["sif_norms"])
+    got = np.stack([rr.query_sif(sif, q) for q in c1 + c2])
+    np.testing.assert_array_equal(got, g["sif_scores"])
+    for j, q in enumerate(c1):
+        if q.support:
+            assert rr.query_sif(sif, q)[j] == 1.0  # self-score exactly 1
+
+
+def test_rerank_kats():
+    a = rr.build_activation([1.0, 0.8, 0.3, 0.1], 2)
+    assert dict(a.items()) == {0: 1.0, 1: 0.8}
+    assert rr.build_activation([0.0, 0.0, 0.0], 2).support == 0
+    assert dict(rr.build_activation([1.0, 0.5, 0.5, 0.2], 2).items()) == {0: 1.0, 1: 0.5}
+    assert rr.top_neighbors([0.2, 1.0, 0.5, 0.5], 3) == [1, 2, 3]
+    assert rr.top_neighbors([0.0, 0.0], 2) == []
+    f = rr.aggregate(rr.make_activation("a", [0], [0.25]), rr.make_activation("a", [0], [0.81]), 0.5)
+    assert abs(f.values[0] - 0.49) <= 1e-12
+    with pytest.raises(ValueError):
+        rr.build_sif([rr.make_activation("a", [3], [0.5])])
+
+
+def test_topk_large_rows_vs_lexsort():
+    rng = np.random.default_rng(11)
+    S = np.round(rng.random((7, 50_000)), 3)
+    S[:, ::7] = 0.0
+    t = torch.from_numpy(S).to(dev())
+    for k in (1, 4, 10, 100, 700, 2048):
+        idx, val = eg.topk_rows(t, k)
+        for r in range(7):
+            ref = np.lexsort((np.arange(S.shape[1]), -S[r]))[:k]
+            np.testing.assert_array_equal(idx[r].cpu().numpy(), ref)
+
+
+# ---------------------------------------------------------------- end to end
+def _e2e_bundle(case, storage="float32", similarity="cosine"):
+    name, seed, N, V, d, classes, K, ma, k1, k2, nq, top_k, zv = case
+    views, _ = mixture_views(seed, N, V, d, classes, zero_views=zv, n_queries=nq)
+    db, qs = views[:N], views[N:]
+    ids = shape_ids(N)
+    C = sampled_codebook(db, K, seed + 1)
+    cfg = gift.IndexConfig(n_views=V, codebook_size=K, ma=ma, k1=k1, k2=k2, imported=True,
+                           storage_dtype=storage, similarity=similarity)
+    bundle = gift.build_index_from_views(db, ids, cfg,
+                                         codebooks={"A": Codebook(C, "A"), "B": Codebook(C, "B")})
+    return bundle, db, qs, ids, C
+
+
+@pytest.mark.parametrize("case", E2E_CASES, ids=[c[0] for c in E2E_CASES])
+def test_end_to_end_against_reference(case):
+    name, seed, N, V, d, classes, K, ma, k1, k2, nq, top_k, zv = case
+    g = load_golden(f"e2e_{name}.npz")
+    bundle, db, qs, ids, C = _e2e_bundle(case)
+    # stage-wise: raw activations and final (augmented) activations
+    raw = bundle.raw_activations["A"]
+    for i, ref in enumerate(unpack_acts(g, "raw")):
+        a = raw[i]
+        assert_act_close((a.indices, a.values, a.norm), ref)
+    # F-IF and re-rank scores of the queries
+    sc = mt.query_fif_batch(bundle.fifs["A"], qs, ma).cpu().numpy()
+    np.testing.assert_allclose(sc, g["q_fif_scores"], rtol=RTOL, atol=1e-9)
+    rs = np.stack([gift.rerank_scores(bundle, {"A": s, "B": s}) for s in g["q_fif_scores"]])
+    np.testing.assert_allclose(rs, g["q_rerank_scores"], rtol=RTOL, atol=1e-12)
+    for rerank, tag in ((True, "rr"), (False, "nr")):
+        batch = gift.query_batch(bundle, qs, top_k=top_k, rerank=rerank)
+        for qi, q in enumerate(qs):
+            res, tim = gift.query(bundle, ViewSet.from_matrix("query", q), top_k=top_k,
+                                  rerank=rerank)
+            assert set(tim) == {"render", "match"}
+            assert res == batch[qi]
+            assert_ranking_close([ids.index(r[0]) for r in res], [r[1] for r in res],
+                                 g[f"q_{tag}_ids"][qi], g[f"q_{tag}_scores"][qi])
+        for j, i in enumerate(range(0, N, max(1, N // 8))):
+            res, _ = gift.query_by_id(bundle, ids[i], top_k=top_k, rerank=rerank)
+            assert res[0][0] == ids[i]  # self-retrieval ranks first
+            assert_ranking_close([ids.index(r[0]) for r in res], [r[1] for r in res],
+                                 g[f"id_{tag}_ids"][j], g[f"id_{tag}_scores"][j])
+
+
+def test_persistence_round_trip_and_bytes():
+    bundle, db, qs, ids, C = _e2e_bundle(E2E_CASES[1])
+    with tempfile.TemporaryDirectory() as td:
+        d1 = gift.save_bundle(bundle, os.path.join(td, "a"))
+        d2 = gift.save_bundle(bundle, os.path.join(td, "b"))
+        for f in sorted(os.listdir(d1)):
+            assert open(os.path.join(d1, f), "rb").read() == open(os.path.join(d2, f), "rb").read()
+        loaded = gift.load_bundle(d1)
+        assert loaded.shape_ids == bundle.shape_ids and loaded.config == bundle.config
+        for sid in ids[:5]:
+            assert gift.query_by_id(loaded, sid, top_k=20)[0] == gift.query_by_id(bundle, sid, top_k=20)[0]
+
+
+def test_fp16_storage_matches_widened_oracle():
+    """Config 4 storage (D5): fp16 features, fp32 accumulation; the oracle
+    sees the same fp16 values widened to f32."""
+    views, _ = mixture_views(21, 200, 20, 1024, 16, n_queries=4)
+    v16 = views.astype(np.float16)
+    db, qs = v16[:200], v16[200:].astype(np.float32)
+    C = sampled_codebook(db.astype(np.float32), 32, 1)
+    fif = mt.build_fif_from_tensor(torch.from_numpy(db).to(dev()), Codebook(C), shape_ids(200))
+    dbw = db.astype(np.float32)
+    assign = oracle.quantize_many(C, dbw.reshape(-1, 1024), 1).reshape(200, 20)
+    ref = oracle.build_fif(list(dbw), C, assign=assign)
+    for a, b in zip(fif.entry_ordinals, ref.entry_ordinals):
+        np.testing.assert_array_equal(a, b)
+    got = mt.query_fif_batch(fif, qs, 1, "gaussian").cpu().numpy()
+    for q, gsc in zip(qs, got):
+        e = oracle.query_fif(ref, q, 1, "gaussian", cells=oracle.quantize_many(C, q.astype(np.float64), 1))
+        np.testing.assert_allclose(gsc, e, rtol=RTOL, atol=1e-9)
+
+
+def test_sif_self_score_exactly_one_at_scale():
+    """A DB shape's own final activation scores exactly 1.0 against itself
+    (test_rerank.py:249-253): sequential f64 accumulation == cached norm."""
+    bundle, db, qs, ids, C = _e2e_bundle(E2E_CASES[2])
+    cfg = bundle.config
+    s = mt.query_fif_batch(bundle.fifs["A"], db[:64], cfg.ma)  # the self-join's scores
+    nbr, _ = eg.topk_rows(s, cfg.k2, positive_only=True)
+    fa = eg.act_mean(bundle.raw_activations["A"].rows, nbr)
+    sc = bundle.sif.dev.query(fa).cpu().numpy()
+    cnt = fa.cnt.cpu().numpy()
+    assert cnt.min() > 0
+    for j in range(64):
+        assert sc[j, j] == 1.0
+
+
+def test_query_many_pipelined_equals_batch():
+    bundle, db, qs, ids, C = _e2e_bundle(E2E_CASES[2])
+    host = torch.from_numpy(np.concatenate([qs, db[:20]])).pin_memory()
+    idx, val = gift.query_many(bundle, host, top_k=30, batch_size=5)
+    ref = gift.query_batch(bundle, host.numpy(), top_k=30)
+    for r in range(len(ref)):
+        assert [ids[i] for i in idx[r]] == [x[0] for x in ref[r]]
+        np.testing.assert_array_equal(val[r], [x[1] for x in ref[r]])
