@@ -159,6 +159,13 @@ int gift_fif_score(const gift_fif_view* f, const float* Q, int32_t B,
                    int32_t V, const int32_t* vq, int32_t ma, int32_t mode,
                    double sigma, double* out_scores, void* ws,
                    size_t ws_bytes, void* stream);
+/* Same, recording the caller's cudaEvent_t handles (nullable) on `stream`
+ * immediately before and after the scan kernel (bench roofline timing). */
+int gift_fif_score_ex(const gift_fif_view* f, const float* Q, int32_t B,
+                      int32_t V, const int32_t* vq, int32_t ma, int32_t mode,
+                      double sigma, double* out_scores, void* ws,
+                      size_t ws_bytes, void* stream, void* ev_scan_begin,
+                      void* ev_scan_end);
 
 /* ---- K4 top-k: replaces the lexsort selections rerank.py:74, :86-87 and
  * index.py:290-294.  Per row of a dense f64 score matrix [B, n], returns the

@@ -64,6 +64,8 @@ _SIGS = {
     "gift_fif_score_ws_bytes": (_c_sz, [ctypes.POINTER(FifView), _c_i32, _c_i32, _c_i32, _c_i64]),
     "gift_fif_score": (_c_i32, [ctypes.POINTER(FifView), _c_p, _c_i32, _c_i32, _c_p, _c_i32,
                                 _c_i32, _c_dbl, _c_p, _c_p, _c_sz, _c_p]),
+    "gift_fif_score_ex": (_c_i32, [ctypes.POINTER(FifView), _c_p, _c_i32, _c_i32, _c_p, _c_i32,
+                                   _c_i32, _c_dbl, _c_p, _c_p, _c_sz, _c_p, _c_p, _c_p]),
     "gift_topk_rows": (_c_i32, [_c_p, _c_i32, _c_i64, _c_i32, _c_p, _c_p, _c_i64, _c_i32, _c_p,
                                 _c_p, _c_p]),
     "gift_act_from_topk": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_p, _c_p,

@@ -401,6 +401,14 @@ extern "C" size_t gift_fif_score_ws_bytes(const gift_fif_view* f, int32_t B, int
 extern "C" int gift_fif_score(const gift_fif_view* f, const float* Q, int32_t B, int32_t V,
                               const int32_t* vq, int32_t ma, int32_t mode, double sigma,
                               double* out_scores, void* ws, size_t ws_bytes, void* stream) {
+  return gift_fif_score_ex(f, Q, B, V, vq, ma, mode, sigma, out_scores, ws, ws_bytes, stream,
+                           nullptr, nullptr);
+}
+
+extern "C" int gift_fif_score_ex(const gift_fif_view* f, const float* Q, int32_t B, int32_t V,
+                                 const int32_t* vq, int32_t ma, int32_t mode, double sigma,
+                                 double* out_scores, void* ws, size_t ws_bytes, void* stream,
+                                 void* ev_scan_begin, void* ev_scan_end) {
   cudaStream_t st = as_stream(stream);
   GIFT_REQUIRE(f != nullptr, GIFT_ERR_INVALID, "null index");
   GIFT_REQUIRE(ma >= 1 && ma <= f->K, GIFT_ERR_INVALID, "ma must be in [1, %d]", f->K);
@@ -454,6 +462,7 @@ extern "C" int gift_fif_score(const gift_fif_view* f, const float* Q, int32_t B,
   sa.out = w.compact;
   sa.meta = w.meta;
   const int nblk = sm_count() * 2;
+  if (ev_scan_begin) GIFT_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(ev_scan_begin), st));
   if (a_half) {
     GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_scan_kernel<true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -466,6 +475,7 @@ extern "C" int gift_fif_score(const gift_fif_view* f, const float* Q, int32_t B,
     fif_scan_kernel<false><<<nblk, simt::NTHR, simt::Cfg<false>::SMEM, st>>>(sa);
   }
   GIFT_LAUNCH_CHECK();
+  if (ev_scan_end) GIFT_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(ev_scan_end), st));
 
   ReduceArgs ra;
   ra.cells = w.cells;

@@ -274,7 +274,7 @@ class ScoreRunner:
 
     def score(self, fif: DeviceFif, Q: torch.Tensor, ma: int, mode: int = nat.SIM_COSINE,
               sigma: float = 0.5, vq: torch.Tensor | None = None, out: torch.Tensor | None = None,
-              stream=None) -> torch.Tensor:
+              stream=None, scan_events=None) -> torch.Tensor:
         """Q: [B, V, d] f32 device -> f64 [B, n_local] (matching.py:136-161)."""
         if Q.dim() != 3:
             raise ValueError("queries must be [B, V, d]")
@@ -301,9 +301,13 @@ class ScoreRunner:
         for _attempt in range(8):
             wsb = lib.gift_fif_score_ws_bytes(ctypes.byref(view), B, V, ma, self.capacity)
             ws = self.ws.get(wsb)
-            nat.check(lib.gift_fif_score(ctypes.byref(view), nat.ptr(Q), B, V, nat.ptr(vq), ma, mode,
-                                         float(sigma), nat.ptr(out), nat.ptr(ws), ws.numel(),
-                                         _sp(stream)), "gift_fif_score")
+            ev0, ev1 = scan_events if scan_events is not None else (None, None)
+            nat.check(lib.gift_fif_score_ex(ctypes.byref(view), nat.ptr(Q), B, V, nat.ptr(vq), ma,
+                                            mode, float(sigma), nat.ptr(out), nat.ptr(ws),
+                                            ws.numel(), _sp(stream),
+                                            None if ev0 is None else ev0.cuda_event,
+                                            None if ev1 is None else ev1.cuda_event),
+                      "gift_fif_score")
             if not checked:
                 return out
             meta = ws[:64].view(torch.int64)

@@ -44,7 +44,7 @@ def test_quantize_bit_exact_golden():
 
 @pytest.mark.parametrize("K,d,ma", [(256, 4096, 2), (1024, 4096, 2), (64, 256, 1), (4096, 1024, 1)])
 def test_quantize_bit_exact_vs_oracle_config_shapes(K, d, ma):
-    views, _ = mixture_views(K + d, 300, 8, d, 20, mu0=-0.26)
+    views, _ = mixture_views(K + d, max(300, K // 4), 8, d, 20, mu0=-0.26)
     C = sampled_codebook(views, K, 1)
     X = mixture_views(K + d + 1, 120, 8, d, 20, mu0=-0.26)[0].reshape(-1, d)
     got = quantize_batch(Codebook(C), X, ma)
