@@ -1,0 +1,372 @@
+"""Benchmark of the GIFT F-IF + S-IF query path (BASELINE.json metric:
+queries/sec, F-IF match + S-IF re-rank; F-IF scan HBM GB/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl gift|reference]
+                    [--config c2]
+
+A step = one batch of queries (config 2: 64 queries x 64 views x d=4096)
+through quantize -> F-IF scan -> top-k2 -> query activation -> S-IF ->
+top-100, against a 10,000-shape database resident in HBM.  `value` is
+device-timed (CUDA events, inputs resident); `e2e` runs the public API
+`query_many` from pinned host memory (H2D of every batch and D2H of its
+results inside the timed region).  Under torchrun (N > 1) every rank serves
+an index replica and a disjoint query stream ("replicas": the 10 GB
+database of config 2 fits one GPU; sharding is for configs 3-5).
+
+--impl reference times the reference's CPU path (oracle/ numpy port of
+shapesearch's query_fif + rerank_scores, single-channel variant) on all host
+cores; its index lists come from the parity-verified GPU build (the CPU
+build of config 2 would take hours).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1604_01879_b200 import IndexConfig, build_index_from_views, query_many  # noqa: E402
+from paper_1604_01879_b200 import engine as eg  # noqa: E402
+from paper_1604_01879_b200 import synth  # noqa: E402
+from paper_1604_01879_b200.codebook import Codebook  # noqa: E402
+
+METRIC = "queries/sec (F-IF match + S-IF rerank)"
+UNIT = "queries/s"
+SEED = 20160407
+
+
+# ------------------------------------------------------------------ helpers
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def scan_work(eng, Q, w, top_k):
+    """Algorithmic bytes / flops of one scan launch:
+    bytes = sum_{c in U} |c| (d s_feat + 4 [+4 |p|^2]) + B V d 4 + B k 8,
+    flops = sum_c M_c |c| 2 d."""
+    fif = eng.fa
+    B, V, d = Q.shape
+    flat = Q.reshape(-1, d)
+    nz, _ = eg.view_prep(flat)
+    cells = eg.quantize_rows(fif.cb, flat, w.ma, nz=nz).reshape(-1)
+    cells = cells[cells >= 0].long()
+    counts = torch.bincount(cells, minlength=fif.cb.K).double()
+    sizes = (fif.cell_off[1:] - fif.cell_off[:-1]).double()
+    s_feat = 2 if w.storage == "float16" else 4
+    per_post = d * s_feat + 4 + (4 if eng.cfg.similarity == "gaussian" else 0)
+    used = counts > 0
+    nbytes = float((sizes[used] * per_post).sum()) + B * V * d * 4 + B * top_k * 8
+    flops = float((counts * sizes).sum()) * 2 * d
+    return nbytes, flops
+
+
+def load_traffic(config):
+    path = os.path.join(ROOT, "profiles", "scan_traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(config)
+    except (OSError, ValueError):
+        return None
+
+
+# ------------------------------------------------------------------ setup
+def build(w, device):
+    db, qs, _labels = synth.mixture(w, SEED, device)
+    C = synth.sample_centroids(db, w.K, SEED + 1).cpu().numpy()
+    cfg = IndexConfig(n_views=w.n_views, codebook_size=w.K, ma=w.ma, k1=w.k1, k2=w.k2,
+                      similarity="gaussian", sigma=w.sigma, storage_dtype=w.storage,
+                      batch_size=w.batch, imported=True)
+    ids = synth.shape_ids(w.n_shapes)
+    t0 = time.perf_counter()
+    bundle = build_index_from_views(db, ids, cfg, codebooks={"A": Codebook(C, "A"),
+                                                             "B": Codebook(C, "B")})
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    del db
+    torch.cuda.empty_cache()
+    return bundle, qs, build_s
+
+
+def host_oracle(bundle, w):
+    """oracle.OracleIndex over the (parity-verified) GPU-built lists."""
+    import oracle
+
+    fif = bundle.fifs["A"]
+    ords, feats = fif.entry_ordinals, fif.entry_features
+    raw = [oracle.Act(a.indices, a.values, a.norm) for a in bundle.raw_activations["A"]]
+    sif = oracle.Sif(norms=bundle.sif.norms, entry_ordinals=bundle.sif.entry_ordinals,
+                     entry_values=bundle.sif.entry_values)
+    orc = oracle.OracleIndex.from_parts(
+        bundle.shape_ids, fif.codebook.centroids, ords, feats, raw, sif, ma=w.ma, k1=w.k1,
+        k2=w.k2, alpha=0.5, similarity="gaussian_expanded", sigma=w.sigma)
+    for e in range(len(ords)):  # |p|^2 per cell, computed once before forking
+        orc.fifs["A"].pnorm2(e)
+    return orc
+
+
+_ORACLE = None
+_QUERIES = None
+
+
+def _cpu_query(i):
+    from threadpoolctl import threadpool_limits
+
+    with threadpool_limits(1):
+        res, _ = _ORACLE.query(_QUERIES[i], top_k=100, rerank=True)
+    return len(res)
+
+
+def cpu_sample(orc, queries_host, n_procs, n_queries):
+    """Wall time of n_queries oracle queries on n_procs forked workers."""
+    import multiprocessing as mp
+
+    global _ORACLE, _QUERIES
+    _ORACLE, _QUERIES = orc, queries_host
+    ctx = mp.get_context("fork")
+    with ctx.Pool(n_procs) as pool:
+        pool.map(_cpu_query, [0] * min(n_procs, 2))  # warm the forked workers
+        t0 = time.perf_counter()
+        pool.map(_cpu_query, [i % len(queries_host) for i in range(n_queries)], chunksize=1)
+        return time.perf_counter() - t0
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------------ arms
+def run_reference(args, w):
+    ws, rank, local = dist_env()
+    if ws > 1 and rank != 0:
+        return
+    torch.cuda.set_device(local)
+    bundle, qs, _ = build(w, torch.device("cuda", local))  # setup only (not timed)
+    orc = host_oracle(bundle, w)
+    qh = qs[: max(64, w.batch)].cpu().numpy()
+    del bundle
+    torch.cuda.empty_cache()
+    cores = host_cores()
+    per_step = cores  # one query per worker per step
+    for _ in range(args.warmup):
+        cpu_sample(orc, qh, cores, min(cores, 4))
+    times = [cpu_sample(orc, qh, cores, per_step) for _ in range(args.steps)]
+    qps = per_step * len(times) / sum(times)
+    sample = (f"{per_step} queries/step x {len(times)} steps of config {w.name} "
+              f"(single-channel oracle port of query_fif+rerank_scores, gaussian via GEMV)")
+    line = {"impl": "reference", "metric": METRIC, "value": qps, "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000 * sum(times) / len(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w.name, "n_shapes": w.n_shapes, "n_views": w.n_views,
+                       "dim": w.dim, "K": w.K, "ma": w.ma, "sigma": w.sigma, "top_k": w.top_k},
+            "cpu_baseline": {"value": qps, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": qps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_gift(args, w):
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=device)
+    bundle, qs, build_s = build(w, device)
+    eng = bundle.engine
+    B = w.batch
+    nb = max(1, qs.shape[0] // B)
+    order = [(rank + i * ws) % nb for i in range(args.steps + args.warmup)]
+    batches = [qs[j * B:(j + 1) * B].contiguous() for j in range(nb)]
+    for i in range(args.warmup):
+        eng.run(batches[order[i]], top_k=w.top_k, rerank=True)
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    scan_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev[0].record(stream)
+        for i in range(args.steps):
+            eng.run(batches[order[args.warmup + i]], top_k=w.top_k, rerank=True,
+                    scan_events=scan_ev[i])
+        ev[1].record(stream)
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+    ms = ev[0].elapsed_time(ev[1])
+    scan_ms = [a.elapsed_time(b) for a, b in scan_ev]
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    total_q = B * args.steps * ws
+    value = total_q / (ms_max / 1000.0)
+
+    # ---- e2e through the public API from pinned host memory
+    host = torch.empty((args.steps * B, w.n_views, w.dim), dtype=torch.float32, pin_memory=True)
+    for i in range(args.steps):
+        host[i * B:(i + 1) * B].copy_(batches[order[args.warmup + i]])
+    query_many(bundle, host[:B], top_k=w.top_k)  # warm
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    query_many(bundle, host, top_k=w.top_k)
+    e2e_s = time.perf_counter() - t0
+    t = torch.tensor([e2e_s], dtype=torch.float64, device=device)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_value = total_q / float(t.item())
+
+    # ---- roofline of the dominant kernel (F-IF scan)
+    work = [scan_work(eng, batches[order[args.warmup + i]], w, w.top_k) for i in range(args.steps)]
+    nbytes = sum(x[0] for x in work) / len(work)
+    flops = sum(x[1] for x in work) / len(work)
+    scan_avg_ms = sum(scan_ms) / len(scan_ms)
+    peak, peak_kind = measured_peaks()
+    achieved = nbytes / (scan_avg_ms / 1000.0) / 1e9
+    roofline = {"bound": "hbm", "kernel": "fif_scan_kernel", "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_kind,
+                "traffic": load_traffic(w.name), "alg_bytes_per_launch": nbytes,
+                "alg_flops_per_launch": flops, "scan_ms_avg": scan_avg_ms,
+                "scan_share_of_step": scan_avg_ms * args.steps / ms,
+                "achieved_tflops": flops / (scan_avg_ms / 1000.0) / 1e12}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        orc = host_oracle(bundle, w)
+        qh = batches[0].cpu().numpy()
+        cores = host_cores()
+        n = cores
+        wall = cpu_sample(orc, qh, cores, n)
+        cpu = {"value": n / wall, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{n} config-{w.name} queries on {cores} forked workers "
+                         f"(oracle port of query_fif+rerank_scores, single channel)"}
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic",
+                "config": {"workload": w.name, "n_shapes": w.n_shapes, "n_views": w.n_views,
+                           "dim": w.dim, "K": w.K, "ma": w.ma, "similarity": "gaussian",
+                           "sigma": w.sigma, "k1": w.k1, "k2": w.k2, "top_k": w.top_k,
+                           "batch": B, "parallelism": f"replicas{ws}",
+                           "l2": "inputs larger than L2 (database 10.5 GB)",
+                           "build_s": build_s},
+                "e2e": {"value": e2e_value, "unit": UNIT,
+                        "h2d_bytes_per_step": B * w.n_views * w.dim * 4,
+                        "d2h_bytes_per_step": B * w.top_k * 12},
+                "gpu_launches": eg.LAUNCHES_PER_BATCH * args.steps,
+                "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="gift", choices=["gift", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(synth.WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "gift" else args.warmup
+    w = synth.WORKLOADS[args.config]
+    if args.impl == "reference":
+        run_reference(args, w)
+    else:
+        run_gift(args, w)
+
+
+if __name__ == "__main__":
+    main()

@@ -146,6 +146,13 @@ class Fif:
     def total_postings(self) -> int:
         return int(sum(len(o) for o in self.entry_ordinals))
 
+    def pnorm2(self, e: int) -> np.ndarray:
+        cache = self.__dict__.setdefault("_pn", {})
+        if e not in cache:
+            F = self.entry_features[e].astype(np.float64)
+            cache[e] = (F * F).sum(axis=1)
+        return cache[e]
+
     def shape_matrix(self, ordinal: int) -> np.ndarray:
         """matching.py:94-103 — cell-major gather of one shape's views."""
         rows = [f[o == ordinal] for o, f in zip(self.entry_ordinals, self.entry_features)
@@ -215,6 +222,12 @@ def query_fif(fif: Fif, query_views, ma: int = 2, similarity: str = "cosine",
             F = fif.entry_features[int(e)]
             if similarity == "cosine":
                 sims = np.clip(F @ row, 0.0, 1.0)
+            elif similarity == "gaussian_expanded":
+                # same kernel via |q|^2 + |p|^2 - 2 q.p (one GEMV per cell, the
+                # reference's cost profile); used only for CPU-baseline timing
+                pn = fif.pnorm2(int(e))
+                d2 = np.maximum(row @ row + pn - 2.0 * (F @ row), 0.0)
+                sims = np.exp(-d2 * inv_s2)
             else:
                 diff = F.astype(np.float64) - row
                 sims = np.exp(-(diff * diff).sum(axis=1) * inv_s2)
@@ -400,6 +413,24 @@ class OracleIndex:
                                        assign_a if self.dup else assign_b)
         if build_sif_now:
             self.build_context()
+
+    @classmethod
+    def from_parts(cls, shape_ids, centroids, entry_ordinals, entry_features, raw, sif, *,
+                   ma, k1, k2, alpha=0.5, similarity="cosine", sigma=0.5):
+        """Assemble a single-channel (duplicated) oracle index from given
+        lists (e.g. parity-verified GPU-built lists; the CPU build of the
+        large configs takes hours)."""
+        self = cls.__new__(cls)
+        self.shape_ids = list(shape_ids)
+        self.ma, self.k1, self.k2, self.alpha = ma, k1, k2, alpha
+        self.similarity, self.sigma = similarity, sigma
+        self.dup = self.single = True
+        fif = Fif(centroids=np.asarray(centroids, dtype=np.float32), n_shapes=len(shape_ids),
+                  entry_ordinals=list(entry_ordinals), entry_features=list(entry_features))
+        self.fifs = {"A": fif, "B": fif}
+        self.raw = {"A": raw, "B": raw}
+        self.sif = sif
+        return self
 
     def channel_scores(self, views, ch):
         return query_fif(self.fifs[ch], views, self.ma, self.similarity, self.sigma)

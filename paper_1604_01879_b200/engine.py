@@ -30,6 +30,12 @@ _DTYPE_CODE = {torch.float32: nat.GIFT_F32, torch.float16: nat.GIFT_F16,
                torch.float64: nat.GIFT_F64}
 
 
+# libgift kernel launches of one QueryEngine.run batch (single channel, rerank):
+# view_prep, quantize approx + select, probe count, plan, scatter, compact
+# zero, scan, reduce (gift_fif_score) + top-k2, act_mean, sif_query, top-k.
+LAUNCHES_PER_BATCH = 13
+
+
 def _bits(n: int) -> int:
     return max(1, int(n).bit_length())
 
@@ -235,8 +241,8 @@ class DeviceFif:
         off = self.cell_off.cpu().numpy()
         ords = self.post_ord.cpu().numpy()
         feats = self.feat.float().cpu().numpy()
-        return ([ords[off[c]:off[c + 1]].copy() for c in range(self.cb.K)],
-                [feats[off[c]:off[c + 1]].copy() for c in range(self.cb.K)])
+        return ([ords[off[c]:off[c + 1]] for c in range(self.cb.K)],
+                [feats[off[c]:off[c + 1]] for c in range(self.cb.K)])
 
     def shape_views(self, local: torch.Tensor):
         """Stored views of shapes (local indices) recovered cell-major, f32,

@@ -149,9 +149,9 @@ class QueryEngine:
         self.runner = eg.ScoreRunner()
         self.mode = mt.sim_mode(cfg.similarity)
 
-    def scores(self, Qa, Qb=None, vq=None, vqb=None, stream=None):
+    def scores(self, Qa, Qb=None, vq=None, vqb=None, stream=None, scan_events=None):
         sa = self.runner.score(self.fa, Qa, self.cfg.ma, self.mode, self.cfg.sigma, vq=vq,
-                               stream=stream)
+                               stream=stream, scan_events=scan_events)
         if Qb is None and self.dup:
             return sa, sa
         sb = self.runner.score(self.fb, Qa if Qb is None else Qb, self.cfg.ma, self.mode,
@@ -172,9 +172,9 @@ class QueryEngine:
         return self.sif.query(final, stream=stream)
 
     def run(self, Qa, Qb=None, top_k=10, rerank=True, self_local=None, vq=None, vqb=None,
-            stream=None):
+            stream=None, scan_events=None):
         """Device batch -> (idx [B, k] i32 global ordinals, val [B, k] f64)."""
-        sa, sb = self.scores(Qa, Qb, vq, vqb, stream)
+        sa, sb = self.scores(Qa, Qb, vq, vqb, stream, scan_events)
         if rerank:
             final = self.rerank(sa, sb, stream)
         elif sb is sa:
