@@ -269,6 +269,9 @@ def run_gift(args, w):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     scan_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(args.steps)]
+    for a, b in scan_ev:  # torch creates the CUDA events lazily, on first record
+        a.record(stream)
+        b.record(stream)
     with ClockSampler(local) as clk:
         if ws > 1:
             dist.barrier()
