@@ -75,6 +75,9 @@ typedef struct gift_fif_view {
   const float* centroids;    /* [K, d] f32 codebook (codebook.py:22-34)       */
   const double* cnorm2;      /* [K] |c|^2 in f64                              */
   double cmax_norm;          /* max_c |c|                                     */
+  const void* feat_hi;       /* [P, d] fp16 plane h1 = rn(feat) (tensor-core  */
+  const void* feat_lo;       /* scan); feat_lo: rn((feat-h1) 2^11), NULL for   */
+                             /* fp16 storage (feat_hi == feat)                 */
 } gift_fif_view;
 
 /* ---- library ---- */
@@ -138,6 +141,10 @@ int gift_fif_tiles(const int64_t* cell_off, const int64_t* seg_off,
                    int64_t* tile_off, int32_t* tile_pstart, int32_t* tile_pend,
                    int32_t* tile_seg0, int32_t* tile_seg1, void* ws,
                    size_t ws_bytes, void* stream);
+/* Tensor-core operand planes of f32 rows: h1 = rn16(x), h2 = rn16((x - h1)
+ * 2^11), so x = h1 + 2^-11 h2 to 22 significant bits (fif_scan_tc.cu). */
+int gift_split_planes(const float* x, int64_t n, void* h1, void* h2,
+                      void* stream);
 /* out[i] = src[idx[i]] widened to f32 (query_by_id's shape_matrix,
  * matching.py:94-103, index.py:302-314). */
 int gift_gather_rows_f32(const void* src, int32_t dtype, int32_t d,

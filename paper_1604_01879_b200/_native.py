@@ -39,6 +39,7 @@ class FifView(ctypes.Structure):
         ("tile_off", _c_p), ("tile_pstart", _c_p), ("tile_pend", _c_p),
         ("tile_seg0", _c_p), ("tile_seg1", _c_p),
         ("centroids", _c_p), ("cnorm2", _c_p), ("cmax_norm", _c_dbl),
+        ("feat_hi", _c_p), ("feat_lo", _c_p),
     ]
 
 
@@ -60,6 +61,7 @@ _SIGS = {
                                    _c_p]),
     "gift_fif_tiles": (_c_i32, [_c_p, _c_p, _c_p, _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_p,
                                 _c_p, _c_sz, _c_p]),
+    "gift_split_planes": (_c_i32, [_c_p, _c_i64, _c_p, _c_p, _c_p]),
     "gift_gather_rows_f32": (_c_i32, [_c_p, _c_i32, _c_i32, _c_p, _c_i64, _c_p, _c_p]),
     "gift_fif_score_ws_bytes": (_c_sz, [ctypes.POINTER(FifView), _c_i32, _c_i32, _c_i32, _c_i64]),
     "gift_fif_score": (_c_i32, [ctypes.POINTER(FifView), _c_p, _c_i32, _c_i32, _c_p, _c_i32,

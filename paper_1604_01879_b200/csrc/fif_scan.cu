@@ -16,6 +16,9 @@
 //            f64 sum over the views in view order, / Vq  -> dense scores.
 // Deterministic: no floating-point atomics; the only atomics are integer
 // counters and atomicMax on non-negative float bits (order-independent).
+#include <stdlib.h>
+
+#include "fif_scan_tc.cuh"
 #include "simt_tile.cuh"
 
 namespace gift {
@@ -24,7 +27,6 @@ constexpr int RED_RS = 4096;  // shapes per reduce CTA
 constexpr int RED_THREADS = 256;
 constexpr int PLAN_THREADS = 1024;
 
-enum Meta { M_ITEMS = 0, M_OUT_TOTAL = 1, M_OVERFLOW = 2, M_WORK = 3 };
 
 __global__ void probe_count_kernel(const int32_t* __restrict__ cells, int64_t nprobes,
                                    int32_t* __restrict__ counts) {
@@ -363,7 +365,15 @@ struct ScoreWs {
   size_t qws_bytes;
   float* compact;
   int64_t capacity;
+  __half* g1;
+  __half* g2;
 };
+
+bool use_tc(const gift_fif_view* f) {
+  const char* e = getenv("GIFT_SCAN");
+  if (e != nullptr && e[0] == 's') return false;  // GIFT_SCAN=simt forces the CUDA-core scan
+  return tc_supported(f);
+}
 
 bool carve(Arena& ar, const gift_fif_view* f, int64_t nviews, int ma, ScoreWs& w) {
   const int K = f->K;
@@ -381,6 +391,12 @@ bool carve(Arena& ar, const gift_fif_view* f, int64_t nviews, int ma, ScoreWs& w
   w.probe_rank = ar.take<int32_t>(nprobes);
   w.qws_bytes = gift_quantize_ws_bytes(nviews, f->d, K, GIFT_F32);
   w.qws = ar.take<char>(static_cast<int64_t>(w.qws_bytes));
+  w.g1 = w.g2 = nullptr;
+  if (use_tc(f)) {
+    w.g1 = ar.take<__half>(nprobes * f->d + 512);
+    w.g2 = ar.take<__half>(nprobes * f->d + 512);
+    if (!w.g1 || !w.g2) return false;
+  }
   if (!w.meta || !w.nz || !w.qn2 || !w.cells || !w.counts || !w.cursor || !w.probe_off ||
       !w.outbase || !w.item_off || !w.probe_list || !w.probe_rank || !w.qws)
     return false;
@@ -443,39 +459,70 @@ extern "C" int gift_fif_score_ex(const gift_fif_view* f, const float* Q, int32_t
   compact_zero_kernel<<<sm_count() * 4, 256, 0, st>>>(w.compact, w.meta);
   GIFT_LAUNCH_CHECK();
 
-  ScanArgs sa;
-  sa.f = *f;
-  sa.Q = Q;
-  sa.qn2 = w.qn2;
-  sa.ma = ma;
-  sa.mode = mode;
-  sa.inv_sigma2 = mode == GIFT_SIM_GAUSSIAN ? static_cast<float>(1.0 / (sigma * sigma)) : 0.f;
-  const bool a_half = f->dtype == GIFT_F16;
-  const bool aligned = reinterpret_cast<uintptr_t>(f->feat) % 16 == 0 &&
-                       reinterpret_cast<uintptr_t>(Q) % 16 == 0;
-  sa.vec16 = aligned && (a_half ? d % 8 == 0 : d % 4 == 0);
-  sa.counts = w.counts;
-  sa.probe_off = w.probe_off;
-  sa.probe_list = w.probe_list;
-  sa.outbase = w.outbase;
-  sa.item_off = w.item_off;
-  sa.out = w.compact;
-  sa.meta = w.meta;
-  const int nblk = sm_count() * 2;
-  if (ev_scan_begin) GIFT_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(ev_scan_begin), st));
-  if (a_half) {
-    GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_scan_kernel<true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       simt::Cfg<true>::SMEM));
-    fif_scan_kernel<true><<<nblk, simt::NTHR, simt::Cfg<true>::SMEM, st>>>(sa);
+  if (use_tc(f)) {
+    TcArgs ta;
+    ta.item_off = w.item_off;
+    ta.counts = w.counts;
+    ta.probe_off = w.probe_off;
+    ta.probe_list = w.probe_list;
+    ta.outbase = w.outbase;
+    ta.out = w.compact;
+    ta.meta = w.meta;
+    ta.tile_off = f->tile_off;
+    ta.tile_pstart = f->tile_pstart;
+    ta.tile_pend = f->tile_pend;
+    ta.tile_seg0 = f->tile_seg0;
+    ta.tile_seg1 = f->tile_seg1;
+    ta.seg_off = f->seg_off;
+    ta.seg_pstart = f->seg_pstart;
+    ta.pnorm2 = f->pnorm2;
+    ta.qn2 = w.qn2;
+    ta.K = K;
+    ta.d = d;
+    ta.ma = ma;
+    ta.mode = mode;
+    ta.inv_sigma2 = mode == GIFT_SIM_GAUSSIAN ? static_cast<float>(1.0 / (sigma * sigma)) : 0.f;
+    ta.has_lo = 0;
+    const char* ck = getenv("GIFT_TC_CHUNK_KB");
+    ta.chunk_kb = ck ? atoi(ck) : 4;
+    if (ta.chunk_kb < 1) ta.chunk_kb = 1;
+    int rc2 = launch_scan_tc(f, Q, nprobes, ta, w.g1, w.g2, st, ev_scan_begin, ev_scan_end);
+    if (rc2) return rc2;
   } else {
-    GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_scan_kernel<false>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       simt::Cfg<false>::SMEM));
-    fif_scan_kernel<false><<<nblk, simt::NTHR, simt::Cfg<false>::SMEM, st>>>(sa);
+    ScanArgs sa;
+    sa.f = *f;
+    sa.Q = Q;
+    sa.qn2 = w.qn2;
+    sa.ma = ma;
+    sa.mode = mode;
+    sa.inv_sigma2 = mode == GIFT_SIM_GAUSSIAN ? static_cast<float>(1.0 / (sigma * sigma)) : 0.f;
+    const bool a_half = f->dtype == GIFT_F16;
+    const bool aligned = reinterpret_cast<uintptr_t>(f->feat) % 16 == 0 &&
+                         reinterpret_cast<uintptr_t>(Q) % 16 == 0;
+    sa.vec16 = aligned && (a_half ? d % 8 == 0 : d % 4 == 0);
+    sa.counts = w.counts;
+    sa.probe_off = w.probe_off;
+    sa.probe_list = w.probe_list;
+    sa.outbase = w.outbase;
+    sa.item_off = w.item_off;
+    sa.out = w.compact;
+    sa.meta = w.meta;
+    const int nblk = sm_count() * 2;
+    if (ev_scan_begin) GIFT_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(ev_scan_begin), st));
+    if (a_half) {
+      GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_scan_kernel<true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         simt::Cfg<true>::SMEM));
+      fif_scan_kernel<true><<<nblk, simt::NTHR, simt::Cfg<true>::SMEM, st>>>(sa);
+    } else {
+      GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_scan_kernel<false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         simt::Cfg<false>::SMEM));
+      fif_scan_kernel<false><<<nblk, simt::NTHR, simt::Cfg<false>::SMEM, st>>>(sa);
+    }
+    GIFT_LAUNCH_CHECK();
+    if (ev_scan_end) GIFT_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(ev_scan_end), st));
   }
-  GIFT_LAUNCH_CHECK();
-  if (ev_scan_end) GIFT_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(ev_scan_end), st));
 
   ReduceArgs ra;
   ra.cells = w.cells;

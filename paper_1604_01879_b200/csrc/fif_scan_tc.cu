@@ -1,0 +1,379 @@
+// K3 F-IF scan on the 5th-generation tensor cores (tcgen05 + TMA + TMEM).
+//
+// Same work items and outputs as the CUDA-core scan (fif_scan.cu): one item =
+// a posting tile (<= 128 postings of one cell, whole segments) x a tile of up
+// to 64 of that cell's probes; output = per (probe, segment) best similarity.
+//
+// Precision (north_star: scores within 1e-5 relative, gaussian amplifies dot
+// errors 8x at sigma = 0.5): every fp32 operand x is split into two fp16
+// planes x = h1 + 2^-11 h2 (h1 = rn(x), h2 = rn((x - h1) 2^11), 22 significant
+// bits); the dot is  D1 + 2^-11 D2,  D1 = sum a1 b1,  D2 = sum (a1 b2 + a2 b1),
+// three kind::f16 MMAs per k-step with fp32 accumulation in TMEM.  fp16
+// products are exact in fp32.  The accumulators are drained to registers every
+// `chunk_kb` k-blocks (and summed there in fp32, round-to-nearest) so the
+// tensor-core accumulation chains stay short.  Database planes are built once
+// (gift_split_planes); query planes per batch (gather_split kernel below).
+//
+// Warp roles (1 CTA / SM, persistent, static round-robin over items):
+//   warp 0      TMA producer: A1/A2 (postings, 128 x 64 fp16, 128B swizzle) and
+//               B1/B2 (probes, 64 x 64) per k-block into a 3-stage ring;
+//   warp 1      MMA issuer: 12 tcgen05.mma (M=128, N=64, K=16) per k-block into
+//               one of two TMEM accumulator pairs (D1 | D2), tcgen05.commit
+//               releases smem stages and hands full accumulators over;
+//   warps 2..5  epilogue: tcgen05.ld drains (row = TMEM lane), fp32 sums,
+//               similarity transform, per-segment max over rows, store.
+#include <cudaTypedefs.h>
+
+#include "fif_scan_tc.cuh"
+#include "tc_ptx.cuh"
+
+namespace gift {
+
+constexpr int TC_M = 128;
+constexpr int TC_N = 64;
+constexpr int TC_BK = 64;  // fp16 per k-block = 128-byte rows
+constexpr int TC_STAGES = 3;
+constexpr int A_TILE = TC_M * TC_BK * 2;  // 16 KB
+constexpr int B_TILE = TC_N * TC_BK * 2;  //  8 KB
+constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;
+constexpr int EPI_STRIDE = TC_N + 1;
+constexpr int EPI_BYTES = TC_M * EPI_STRIDE * 4;
+constexpr int TC_THREADS = 192;
+constexpr uint32_t TMEM_COLS = 256;  // 2 buffers x (D1[64] | D2[64])
+constexpr int SMEM_TC = TC_STAGES * STAGE_BYTES + EPI_BYTES + 256;
+constexpr float SPLIT_SCALE = 2048.0f;        // 2^11
+constexpr float SPLIT_INV = 1.0f / 2048.0f;
+
+struct ItemInfo {
+  int c, mt, p0, p1, seg0, seg1, nb, pb0;
+};
+
+__device__ __forceinline__ ItemInfo decode_item(const TcArgs& p, int64_t item) {
+  int lo = 0, hi = p.K - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (p.item_off[mid] <= item) lo = mid; else hi = mid - 1;
+  }
+  ItemInfo I;
+  I.c = lo;
+  const int64_t rem = item - p.item_off[lo];
+  const int cnt = p.counts[lo];
+  const int nm = (cnt + TC_N - 1) / TC_N;
+  const int64_t t = p.tile_off[lo] + rem / nm;
+  I.mt = static_cast<int>(rem % nm);
+  I.p0 = p.tile_pstart[t];
+  I.p1 = p.tile_pend[t];
+  I.seg0 = p.tile_seg0[t];
+  I.seg1 = p.tile_seg1[t];
+  I.nb = min(TC_N, cnt - I.mt * TC_N);
+  I.pb0 = p.probe_off[lo] + I.mt * TC_N;
+  return I;
+}
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    fif_scan_tc_kernel(const __grid_constant__ CUtensorMap tmA1,
+                       const __grid_constant__ CUtensorMap tmA2,
+                       const __grid_constant__ CUtensorMap tmB1,
+                       const __grid_constant__ CUtensorMap tmB2, const TcArgs p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ int32_t s_sp[TC_M + 2];
+  __shared__ float s_qn2[TC_N];
+  float* Ds = reinterpret_cast<float*>(smem + TC_STAGES * STAGE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TC_STAGES * STAGE_BYTES + EPI_BYTES);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + TC_STAGES;
+  uint64_t* tfull = bars + 2 * TC_STAGES;
+  uint64_t* tempty = bars + 2 * TC_STAGES + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * TC_STAGES + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (p.meta[M_OVERFLOW]) return;
+  const int64_t n_items = p.meta[M_ITEMS];
+  const int nkb = (p.d + TC_BK - 1) / TC_BK;
+  const int chunk_kb = p.chunk_kb;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < TC_STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&tfull[b], 1);
+      tc::mbar_init(&tempty[b], TC_M);
+    }
+    tc::fence_barrier_init();
+    tc::tma_prefetch(&tmA1);
+    if (p.has_lo) tc::tma_prefetch(&tmA2);
+    tc::tma_prefetch(&tmB1);
+    tc::tma_prefetch(&tmB2);
+  }
+  if (warp == 1) tc::tmem_alloc<TMEM_COLS>(tmem_holder);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const uint32_t bytes = (p.has_lo ? 2 * A_TILE : A_TILE) + 2 * B_TILE;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const ItemInfo I = decode_item(p, item);
+        for (int kb = 0; kb < nkb; ++kb) {
+          tc::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* st = smem + stage * STAGE_BYTES;
+          tc::mbar_arrive_expect_tx(&full[stage], bytes);
+          tc::tma_load_2d(st, &tmA1, &full[stage], kb * TC_BK, I.p0);
+          if (p.has_lo) tc::tma_load_2d(st + A_TILE, &tmA2, &full[stage], kb * TC_BK, I.p0);
+          tc::tma_load_2d(st + 2 * A_TILE, &tmB1, &full[stage], kb * TC_BK, I.pb0);
+          tc::tma_load_2d(st + 2 * A_TILE + B_TILE, &tmB2, &full[stage], kb * TC_BK, I.pb0);
+          if (++stage == TC_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = tc::idesc_f16_f32(TC_M, TC_N);
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t chunk_ctr = 0;
+      for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+        for (int kb0 = 0; kb0 < nkb; kb0 += chunk_kb) {
+          const uint32_t buf = chunk_ctr & 1, aph = (chunk_ctr >> 1) & 1;
+          tc::mbar_wait(&tempty[buf], aph ^ 1);
+          tc::tc_fence_after();
+          const uint32_t d1 = tmem_base + buf * 128;
+          const uint32_t d2 = d1 + TC_N;
+          const int kend = min(kb0 + chunk_kb, nkb);
+          for (int kb = kb0; kb < kend; ++kb) {
+            tc::mbar_wait(&full[stage], phase);
+            tc::tc_fence_after();
+            uint8_t* st = smem + stage * STAGE_BYTES;
+            const uint64_t a1 = tc::smem_desc_sw128(st);
+            const uint64_t a2 = tc::smem_desc_sw128(st + A_TILE);
+            const uint64_t b1 = tc::smem_desc_sw128(st + 2 * A_TILE);
+            const uint64_t b2 = tc::smem_desc_sw128(st + 2 * A_TILE + B_TILE);
+#pragma unroll
+            for (int k = 0; k < TC_BK / 16; ++k) {
+              const uint32_t acc = (kb > kb0 || k > 0) ? 1u : 0u;
+              const uint64_t adv = static_cast<uint64_t>(k * 2);  // 32 B in 16-B units
+              tc::mma_f16(d1, a1 + adv, b1 + adv, idesc, acc);
+              tc::mma_f16(d2, a1 + adv, b2 + adv, idesc, acc);
+              if (p.has_lo) tc::mma_f16(d2, a2 + adv, b1 + adv, idesc, 1u);
+            }
+            tc::mma_commit(&empty[stage]);
+            if (++stage == TC_STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          tc::mma_commit(&tfull[buf]);
+          ++chunk_ctr;
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------ epilogue
+    const int et = threadIdx.x - 64;      // 0..127
+    const int lb = 32 * (warp & 3);       // TMEM lane quarter of this warp
+    const int row = lb + lane;            // posting row within the tile
+    const bool gauss = p.mode == GIFT_SIM_GAUSSIAN;
+    uint32_t chunk_ctr = 0;
+    for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const ItemInfo I = decode_item(p, item);
+      const int nseg = I.seg1 - I.seg0;
+      for (int i = et; i <= nseg; i += TC_M) s_sp[i] = p.seg_pstart[I.seg0 + i];
+      if (et < TC_N) {
+        float q = 0.f;
+        if (et < I.nb) q = p.qn2[p.probe_list[I.pb0 + et] / p.ma];
+        s_qn2[et] = q;
+      }
+      float acc[TC_N];
+#pragma unroll
+      for (int n = 0; n < TC_N; ++n) acc[n] = 0.f;
+      for (int kb0 = 0; kb0 < nkb; kb0 += chunk_kb) {
+        const uint32_t buf = chunk_ctr & 1, aph = (chunk_ctr >> 1) & 1;
+        tc::mbar_wait(&tfull[buf], aph);
+        tc::tc_fence_after();
+        const uint32_t base = tmem_base + (static_cast<uint32_t>(lb) << 16) + buf * 128;
+#pragma unroll
+        for (int j = 0; j < TC_N / 16; ++j) {
+          float v1[16], v2[16];
+          tc::tmem_ld_x16(base + j * 16, v1);
+          tc::tmem_ld_x16(base + TC_N + j * 16, v2);
+          tc::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) acc[j * 16 + i] += fmaf(v2[i], SPLIT_INV, v1[i]);
+        }
+        tc::tc_fence_before();
+        tc::mbar_arrive(&tempty[buf]);
+        ++chunk_ctr;
+      }
+      const float pn = (I.p0 + row < I.p1) ? p.pnorm2[I.p0 + row] : 0.f;
+#pragma unroll
+      for (int n = 0; n < TC_N; ++n) {
+        float v = acc[n];
+        if (gauss) v = 2.0f * v - pn;
+        Ds[row * EPI_STRIDE + n] = v;
+      }
+      named_bar(1, TC_M);
+      const int64_t S_c = p.seg_off[I.c + 1] - p.seg_off[I.c];
+      const int64_t seg_base = p.seg_off[I.c];
+      const int64_t obase = p.outbase[I.c];
+      for (int idx = et; idx < nseg * I.nb; idx += TC_M) {
+        const int m = idx / nseg;
+        const int sl = idx - m * nseg;
+        const int sp0 = s_sp[sl], sp1 = s_sp[sl + 1];
+        const int r0 = max(sp0, I.p0) - I.p0, r1 = min(sp1, I.p1) - I.p0;
+        float mx = -INFINITY;
+        for (int r = r0; r < r1; ++r) mx = fmaxf(mx, Ds[r * EPI_STRIDE + m]);
+        float sim;
+        if (gauss)
+          sim = expf(-fmaxf(s_qn2[m] - mx, 0.f) * p.inv_sigma2);
+        else
+          sim = fminf(fmaxf(mx, 0.f), 1.f);
+        const int64_t o =
+            obase + static_cast<int64_t>(I.mt * TC_N + m) * S_c + (I.seg0 + sl - seg_base);
+        if (sp0 < I.p0 || sp1 > I.p1)
+          atomicMax(reinterpret_cast<int*>(p.out + o), __float_as_int(sim));
+        else
+          p.out[o] = sim;
+      }
+      named_bar(1, TC_M);
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc<TMEM_COLS>(tmem_base);
+  }
+}
+
+// x -> (h1, h2) fp16 planes, x = h1 + 2^-11 h2 (22 significant bits)
+__device__ __forceinline__ void split2(float x, __half& h1, __half& h2) {
+  h1 = __float2half_rn(x);
+  h2 = __float2half_rn((x - __half2float(h1)) * SPLIT_SCALE);
+}
+
+__global__ void split_planes_kernel(const float* __restrict__ x, int64_t n, __half* __restrict__ h1,
+                                    __half* __restrict__ h2) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (; i < n; i += stride) {
+    __half a, b;
+    split2(x[i], a, b);
+    h1[i] = a;
+    h2[i] = b;
+  }
+}
+
+// Sorted probe rows -> query planes: G[s] = split(Q[probe_list[s] / ma]).
+__global__ void probe_gather_split_kernel(const float* __restrict__ Q, int d, int ma,
+                                          const int32_t* __restrict__ probe_list,
+                                          const int32_t* __restrict__ probe_off, int K,
+                                          const int64_t* __restrict__ meta,
+                                          __half* __restrict__ g1, __half* __restrict__ g2) {
+  if (meta[M_OVERFLOW]) return;
+  const int s = blockIdx.x;
+  if (s >= probe_off[K]) return;
+  const int64_t view = probe_list[s] / ma;
+  const float* q = Q + view * d;
+  __half* o1 = g1 + static_cast<int64_t>(s) * d;
+  __half* o2 = g2 + static_cast<int64_t>(s) * d;
+  for (int k = threadIdx.x * 4; k < d; k += blockDim.x * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(q + k);
+    __half a0, a1, a2, a3, b0, b1, b2, b3;
+    split2(v.x, a0, b0);
+    split2(v.y, a1, b1);
+    split2(v.z, a2, b2);
+    split2(v.w, a3, b3);
+    reinterpret_cast<__half2*>(o1 + k)[0] = __halves2half2(a0, a1);
+    reinterpret_cast<__half2*>(o1 + k)[1] = __halves2half2(a2, a3);
+    reinterpret_cast<__half2*>(o2 + k)[0] = __halves2half2(b0, b1);
+    reinterpret_cast<__half2*>(o2 + k)[1] = __halves2half2(b2, b3);
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (fn == nullptr) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+static int make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t d, uint32_t box_rows) {
+  auto fn = encode_fn();
+  GIFT_REQUIRE(fn != nullptr, GIFT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {d, rows};
+  cuuint64_t strides[1] = {d * 2};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(TC_BK), box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                  es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  GIFT_REQUIRE(r == CUDA_SUCCESS, GIFT_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return GIFT_OK;
+}
+
+size_t tc_probe_plane_bytes(int64_t nprobes, int d) {
+  return align_up(static_cast<size_t>(nprobes) * d * 2, 1024);
+}
+
+bool tc_supported(const gift_fif_view* f) {
+  return f->feat_hi != nullptr && f->d % 8 == 0 && f->d >= 8 && f->n_postings > 0;
+}
+
+int launch_scan_tc(const gift_fif_view* f, const float* Q, int64_t nprobes_max, TcArgs a,
+                   __half* g1, __half* g2, cudaStream_t st, void* ev0, void* ev1) {
+  const int d = f->d;
+  probe_gather_split_kernel<<<static_cast<unsigned>(max64(nprobes_max, 1)), 128, 0, st>>>(
+      Q, d, a.ma, a.probe_list, a.probe_off, f->K, a.meta, g1, g2);
+  GIFT_LAUNCH_CHECK();
+  CUtensorMap mA1, mA2, mB1, mB2;
+  int rc = make_map(&mA1, f->feat_hi, f->n_postings, d, TC_M);
+  if (rc) return rc;
+  rc = make_map(&mA2, f->feat_lo ? f->feat_lo : f->feat_hi, f->n_postings, d, TC_M);
+  if (rc) return rc;
+  rc = make_map(&mB1, g1, max64(nprobes_max, 1), d, TC_N);
+  if (rc) return rc;
+  rc = make_map(&mB2, g2, max64(nprobes_max, 1), d, TC_N);
+  if (rc) return rc;
+  a.has_lo = f->feat_lo != nullptr ? 1 : 0;
+  GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_scan_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     SMEM_TC));
+  if (ev0) GIFT_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(ev0), st));
+  fif_scan_tc_kernel<<<sm_count(), TC_THREADS, SMEM_TC, st>>>(mA1, mA2, mB1, mB2, a);
+  GIFT_LAUNCH_CHECK();
+  if (ev1) GIFT_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(ev1), st));
+  return GIFT_OK;
+}
+
+}  // namespace gift
+
+using namespace gift;
+
+extern "C" int gift_split_planes(const float* x, int64_t n, void* h1, void* h2, void* stream) {
+  if (n <= 0) return GIFT_OK;
+  split_planes_kernel<<<static_cast<unsigned>(min64(cdiv(n, 256), 8192)), 256, 0,
+                        as_stream(stream)>>>(x, n, static_cast<__half*>(h1),
+                                             static_cast<__half*>(h2));
+  GIFT_LAUNCH_CHECK();
+  return GIFT_OK;
+}

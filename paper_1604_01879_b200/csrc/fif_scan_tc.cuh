@@ -1,0 +1,38 @@
+// Shared declarations of the two F-IF scan implementations (fif_scan.cu,
+// fif_scan_tc.cu).
+#pragma once
+#include "gift_common.cuh"
+
+namespace gift {
+
+enum Meta { M_ITEMS = 0, M_OUT_TOTAL = 1, M_OVERFLOW = 2, M_WORK = 3 };
+
+struct TcArgs {
+  const int64_t* item_off;
+  const int32_t* counts;
+  const int32_t* probe_off;
+  const int32_t* probe_list;
+  const int64_t* outbase;
+  float* out;
+  const int64_t* meta;
+  const int64_t* tile_off;
+  const int32_t* tile_pstart;
+  const int32_t* tile_pend;
+  const int32_t* tile_seg0;
+  const int32_t* tile_seg1;
+  const int64_t* seg_off;
+  const int32_t* seg_pstart;
+  const float* pnorm2;
+  const float* qn2;
+  int K, d, ma, mode;
+  float inv_sigma2;
+  int has_lo;
+  int chunk_kb;
+};
+
+bool tc_supported(const gift_fif_view* f);
+size_t tc_probe_plane_bytes(int64_t nprobes, int d);
+int launch_scan_tc(const gift_fif_view* f, const float* Q, int64_t nprobes_max, TcArgs a,
+                   __half* g1, __half* g2, cudaStream_t st, void* ev0, void* ev1);
+
+}  // namespace gift

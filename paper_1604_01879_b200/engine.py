@@ -140,6 +140,8 @@ class DeviceFif:
         v.centroids = self.cb.centroids.data_ptr()
         v.cnorm2 = self.cb.cnorm2.data_ptr()
         v.cmax_norm = self.cb.cmax
+        v.feat_hi = None if self.feat_hi is None else self.feat_hi.data_ptr()
+        v.feat_lo = None if self.feat_lo is None else self.feat_lo.data_ptr()
         self.view = v
         return v
 
@@ -201,8 +203,18 @@ class DeviceFif:
         return self
 
     def _finish(self, stream=None):
-        """Segments, scan tiles and the shape -> postings map."""
+        """Tensor-core operand planes, segments, scan tiles and the shape ->
+        postings map."""
         K, P, dev, n_local = self.cb.K, self.P, self.feat.device, self.n_local
+        self.feat_hi = self.feat_lo = None
+        if P and self.d % 8 == 0:
+            if self.feat.dtype == torch.float16:
+                self.feat_hi = self.feat  # exact: no correction plane
+            else:
+                self.feat_hi = torch.empty((P, self.d), dtype=torch.float16, device=dev)
+                self.feat_lo = torch.empty((P, self.d), dtype=torch.float16, device=dev)
+                nat.call("gift_split_planes", nat.ptr(self.feat), P * self.d,
+                         nat.ptr(self.feat_hi), nat.ptr(self.feat_lo), _sp(stream))
         ws = nat.workspace("build").get(nat.lib().gift_fif_build_ws_bytes(P, K))
         self.seg_off = torch.empty(K + 1, dtype=torch.int64, device=dev)
         nat.call("gift_fif_segments", nat.ptr(self.cell_off), nat.ptr(self.post_ord), K, P,
