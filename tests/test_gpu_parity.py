@@ -339,3 +339,30 @@ def test_query_many_pipelined_equals_batch():
     for r in range(len(ref)):
         assert [ids[i] for i in idx[r]] == [x[0] for x in ref[r]]
         np.testing.assert_array_equal(val[r], [x[1] for x in ref[r]])
+
+
+@pytest.mark.parametrize("similarity", ["gaussian", "cosine"])
+def test_tensor_core_scan_matches_oracle_at_c2_dims(similarity, monkeypatch):
+    """The tcgen05 scan (default for d % 8 == 0) and the CUDA-core scan both
+    match the f64 oracle at config-2 dimensions (d = 4096, K = 256, ma = 2)."""
+    views, _ = mixture_views(55, 300, 16, 4096, 55, mu0=-0.26, n_queries=8)
+    db, qs = views[:300], views[300:]
+    C = sampled_codebook(db, 256, 4)
+    assign = oracle.quantize_many(C, db.reshape(-1, 4096), 1).reshape(300, 16)
+    ref = oracle.build_fif(list(db), C, assign=assign)
+    fif = mt.build_fif_from_tensor(torch.from_numpy(db).to(dev()), Codebook(C), shape_ids(300))
+    assert fif.dev.feat_hi is not None  # tensor-core planes built
+    got = {}
+    for impl in ("tc", "simt"):
+        monkeypatch.setenv("GIFT_SCAN", impl)
+        got[impl] = mt.query_fif_batch(fif, qs, 2, similarity).cpu().numpy()
+    worst = 0.0
+    for q, g_tc, g_simt in zip(qs, got["tc"], got["simt"]):
+        e = oracle.query_fif(ref, q, 2, similarity,
+                             cells=oracle.quantize_many(C, q.astype(np.float64), 2))
+        nz = e > 0
+        worst = max(worst, float(np.max(np.abs(g_tc[nz] - e[nz]) / e[nz])) if nz.any() else 0.0)
+        np.testing.assert_allclose(g_tc, e, rtol=RTOL, atol=1e-12)
+        np.testing.assert_allclose(g_simt, e, rtol=RTOL, atol=1e-12)
+        assert ((g_tc == 0) == (e == 0)).all()
+    print(f"max relative error tc vs oracle ({similarity}): {worst:.2e}")
