@@ -184,6 +184,14 @@ int gift_topk_rows(const double* scores, int32_t B, int64_t n, int32_t k,
                    const int32_t* idrank, const int32_t* self_local,
                    int64_t ord_base, int32_t positive_only, int32_t* out_idx,
                    double* out_val, void* stream);
+/* Same, with a workspace of >= gift_topk_ws_bytes(B, n, k): rows are split
+ * into slices scanned by separate CTAs, then merged (identical result). */
+size_t gift_topk_ws_bytes(int32_t B, int64_t n, int32_t k);
+int gift_topk_rows_ex(const double* scores, int32_t B, int64_t n, int32_t k,
+                      const int32_t* idrank, const int32_t* self_local,
+                      int64_t ord_base, int32_t positive_only,
+                      int32_t* out_idx, double* out_val, void* ws,
+                      size_t ws_bytes, void* stream);
 
 /* ---- K5 activations (fixed-capacity rows: idx[B,cap] asc, val, cnt, norm) */
 /* build_activation (rerank.py:64-75) from a top-k result: first k1 positive

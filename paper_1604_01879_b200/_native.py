@@ -70,6 +70,9 @@ _SIGS = {
                                    _c_i32, _c_dbl, _c_p, _c_p, _c_sz, _c_p, _c_p, _c_p]),
     "gift_topk_rows": (_c_i32, [_c_p, _c_i32, _c_i64, _c_i32, _c_p, _c_p, _c_i64, _c_i32, _c_p,
                                 _c_p, _c_p]),
+    "gift_topk_ws_bytes": (_c_sz, [_c_i32, _c_i64, _c_i32]),
+    "gift_topk_rows_ex": (_c_i32, [_c_p, _c_i32, _c_i64, _c_i32, _c_p, _c_p, _c_i64, _c_i32, _c_p,
+                                   _c_p, _c_p, _c_sz, _c_p]),
     "gift_act_from_topk": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_p, _c_p,
                                     _c_p, _c_p]),
     "gift_act_mean": (_c_i32, [_c_p, _c_p, _c_p, _c_i32, _c_p, _c_i32, _c_i32, _c_i32, _c_p, _c_p,

@@ -224,120 +224,119 @@ __global__ void __launch_bounds__(simt::NTHR, 2) fif_scan_kernel(ScanArgs p) {
   }
 }
 
+struct ProbeRange {
+  int32_t sa, sb;  // segment sub-range of the probe's cell inside a shape range
+  int64_t base;    // compact index of (probe, segment 0 of the cell)
+  int64_t seg0;    // first segment of the cell
+};
+
+// One thread per (probe, shape range): the segment sub-range of the probe's
+// cell whose shapes fall inside the range (binary searches done in parallel,
+// not on the reduce kernel's critical path).
+__global__ void probe_ranges_kernel(const int32_t* __restrict__ cells,
+                                    const int32_t* __restrict__ probe_rank,
+                                    const int64_t* __restrict__ seg_off,
+                                    const int32_t* __restrict__ seg_ord,
+                                    const int64_t* __restrict__ outbase,
+                                    const int64_t* __restrict__ meta, int64_t nprobes,
+                                    int n_ranges, int64_t n_local, int64_t ord_base,
+                                    ProbeRange* __restrict__ rng) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= nprobes * n_ranges || meta[M_OVERFLOW]) return;
+  const int64_t probe = t / n_ranges;
+  const int r = static_cast<int>(t - probe * n_ranges);
+  const int c = cells[probe];
+  ProbeRange pr{0, 0, 0, 0};
+  if (c >= 0) {
+    const int64_t b0 = seg_off[c], b1 = seg_off[c + 1];
+    int64_t l = b0, h = b1;
+    if (n_ranges > 1) {
+      const int64_t glo = ord_base + static_cast<int64_t>(r) * RED_RS;
+      const int64_t ghi = ord_base + min64(static_cast<int64_t>(r + 1) * RED_RS, n_local);
+      while (l < h) {
+        int64_t mid = (l + h) >> 1;
+        if (seg_ord[mid] < glo) l = mid + 1; else h = mid;
+      }
+      int64_t l2 = l;
+      h = b1;
+      while (l2 < h) {
+        int64_t mid = (l2 + h) >> 1;
+        if (seg_ord[mid] < ghi) l2 = mid + 1; else h = mid;
+      }
+      h = l2;
+    }
+    pr.sa = static_cast<int32_t>(l - b0);
+    pr.sb = static_cast<int32_t>(h - b0);
+    pr.base = outbase[c] + static_cast<int64_t>(probe_rank[probe]) * (b1 - b0);
+    pr.seg0 = b0;
+  }
+  rng[t] = pr;
+}
+
 struct ReduceArgs {
-  const int32_t* cells;       // [B*V*ma]
-  const int32_t* probe_rank;  // [B*V*ma]
-  const int64_t* seg_off;
+  const ProbeRange* rng;      // [B*V*ma, n_ranges]
   const int32_t* seg_ord;
-  const int64_t* outbase;
   const float* out;
   const int64_t* meta;
   const int32_t* vq;
-  int V, ma;
+  int V, ma, n_ranges;
   int64_t n_local, ord_base;
   double* scores;
 };
 
+// Per (query, shape range): view_best = max over the ma slots of each view,
+// total += view_best in view order (f64), score = total / Vq
+// (matching.py:153-161).  One barrier per view: the slot maxima of view v go
+// to vb[v & 1] (atomicMax on non-negative float bits) while view v-1's maxima
+// are folded into the f64 accumulator and cleared (atomicExch: exactly one
+// slot's thread sees each non-zero maximum, so acc has a single writer).
 __global__ void __launch_bounds__(RED_THREADS) fif_reduce_kernel(ReduceArgs a) {
   extern __shared__ __align__(128) char smem[];
   double* acc = reinterpret_cast<double*>(smem);
-  float* vb = reinterpret_cast<float*>(acc + RED_RS);
-  __shared__ int s_sa, s_sb;
-  __shared__ int64_t s_base;
+  float* vb0 = reinterpret_cast<float*>(acc + RED_RS);
+  float* vb1 = vb0 + RED_RS;
   if (a.meta[M_OVERFLOW]) return;
   const int tid = threadIdx.x;
   const int b = blockIdx.y;
-  const int64_t lo = static_cast<int64_t>(blockIdx.x) * RED_RS;
-  const int64_t hi = min64(lo + RED_RS, a.n_local);
-  const int n = static_cast<int>(hi - lo);
-  const int64_t glo = a.ord_base + lo, ghi = a.ord_base + hi;
+  const int rg = blockIdx.x;
+  const int64_t lo = static_cast<int64_t>(rg) * RED_RS;
+  const int n = static_cast<int>(min64(lo + RED_RS, a.n_local) - lo);
+  const int64_t glo = a.ord_base + lo;
   for (int i = tid; i < n; i += RED_THREADS) {
     acc[i] = 0.0;
-    vb[i] = 0.f;
+    vb0[i] = 0.f;
+    vb1[i] = 0.f;
   }
   __syncthreads();
-  for (int v = 0; v < a.V; ++v) {
-    const int64_t pbase = (static_cast<int64_t>(b) * a.V + v) * a.ma;
-    // pass 1: view_best = max over the ma slots (matching.py:153-159)
-    for (int s = 0; s < a.ma; ++s) {
-      if (tid == 0) {
-        const int c = a.cells[pbase + s];
-        int sa = 0, sb = 0;
-        int64_t base = 0;
-        if (c >= 0) {
-          const int64_t b0 = a.seg_off[c], b1 = a.seg_off[c + 1];
-          int64_t l = b0, h = b1;
-          while (l < h) {
-            int64_t mid = (l + h) >> 1;
-            if (a.seg_ord[mid] < glo) l = mid + 1; else h = mid;
-          }
-          int64_t l2 = l, h2 = b1;
-          while (l2 < h2) {
-            int64_t mid = (l2 + h2) >> 1;
-            if (a.seg_ord[mid] < ghi) l2 = mid + 1; else h2 = mid;
-          }
-          sa = static_cast<int>(l - b0);
-          sb = static_cast<int>(l2 - b0);
-          base = a.outbase[c] + static_cast<int64_t>(a.probe_rank[pbase + s]) * (b1 - b0);
-        }
-        s_sa = sa;
-        s_sb = sb;
-        s_base = base;
-      }
-      __syncthreads();
-      const int sa = s_sa, sb = s_sb;
-      if (sa < sb) {
-        const int c = a.cells[pbase + s];
-        const int64_t b0 = a.seg_off[c];
-        const int64_t base = s_base;
-        for (int k = sa + tid; k < sb; k += RED_THREADS) {
-          const int o = static_cast<int>(a.seg_ord[b0 + k] - glo);
-          const float val = a.out[base + k];
+  const int64_t pbase = static_cast<int64_t>(b) * a.V * a.ma;
+  for (int v = 0; v <= a.V; ++v) {
+    if (v < a.V) {
+      float* vb = (v & 1) ? vb1 : vb0;
+      for (int s = 0; s < a.ma; ++s) {
+        const ProbeRange pr = a.rng[(pbase + static_cast<int64_t>(v) * a.ma + s) * a.n_ranges + rg];
+        for (int k = pr.sa + tid; k < pr.sb; k += RED_THREADS) {
+          const int o = static_cast<int>(a.seg_ord[pr.seg0 + k] - glo);
+          const float val = a.out[pr.base + k];
           if (a.ma == 1)
             acc[o] += static_cast<double>(val);
           else
-            vb[o] = fmaxf(vb[o], val);
+            atomicMax(reinterpret_cast<int*>(vb + o), __float_as_int(val));
         }
       }
-      __syncthreads();
     }
-    if (a.ma == 1) continue;
-    // pass 2: total += view_best (f64, view order), reset
-    for (int s = 0; s < a.ma; ++s) {
-      if (tid == 0) {
-        const int c = a.cells[pbase + s];
-        int sa = 0, sb = 0;
-        if (c >= 0) {
-          const int64_t b0 = a.seg_off[c], b1 = a.seg_off[c + 1];
-          int64_t l = b0, h = b1;
-          while (l < h) {
-            int64_t mid = (l + h) >> 1;
-            if (a.seg_ord[mid] < glo) l = mid + 1; else h = mid;
-          }
-          int64_t l2 = l, h2 = b1;
-          while (l2 < h2) {
-            int64_t mid = (l2 + h2) >> 1;
-            if (a.seg_ord[mid] < ghi) l2 = mid + 1; else h2 = mid;
-          }
-          sa = static_cast<int>(l - b0);
-          sb = static_cast<int>(l2 - b0);
-        }
-        s_sa = sa;
-        s_sb = sb;
-      }
-      __syncthreads();
-      const int sa = s_sa, sb = s_sb;
-      if (sa < sb) {
-        const int c = a.cells[pbase + s];
-        const int64_t b0 = a.seg_off[c];
-        for (int k = sa + tid; k < sb; k += RED_THREADS) {
-          const int o = static_cast<int>(a.seg_ord[b0 + k] - glo);
-          acc[o] += static_cast<double>(vb[o]);
-          vb[o] = 0.f;
+    if (a.ma > 1 && v > 0) {
+      float* vb = ((v - 1) & 1) ? vb1 : vb0;
+      for (int s = 0; s < a.ma; ++s) {
+        const ProbeRange pr =
+            a.rng[(pbase + static_cast<int64_t>(v - 1) * a.ma + s) * a.n_ranges + rg];
+        for (int k = pr.sa + tid; k < pr.sb; k += RED_THREADS) {
+          const int o = static_cast<int>(a.seg_ord[pr.seg0 + k] - glo);
+          const int old = atomicExch(reinterpret_cast<int*>(vb + o), 0);
+          if (old != 0) acc[o] += static_cast<double>(__int_as_float(old));
         }
       }
-      __syncthreads();
     }
+    __syncthreads();
   }
   const double denom = static_cast<double>(a.vq ? a.vq[b] : a.V);
   for (int i = tid; i < n; i += RED_THREADS)
@@ -367,6 +366,7 @@ struct ScoreWs {
   int64_t capacity;
   __half* g1;
   __half* g2;
+  ProbeRange* rng;
 };
 
 bool use_tc(const gift_fif_view* f) {
@@ -391,6 +391,8 @@ bool carve(Arena& ar, const gift_fif_view* f, int64_t nviews, int ma, ScoreWs& w
   w.probe_rank = ar.take<int32_t>(nprobes);
   w.qws_bytes = gift_quantize_ws_bytes(nviews, f->d, K, GIFT_F32);
   w.qws = ar.take<char>(static_cast<int64_t>(w.qws_bytes));
+  w.rng = ar.take<ProbeRange>(nprobes * cdiv(max64(f->n_local, 1), RED_RS));
+  if (!w.rng) return false;
   w.g1 = w.g2 = nullptr;
   if (use_tc(f)) {
     w.g1 = ar.take<__half>(nprobes * f->d + 512);
@@ -524,24 +526,27 @@ extern "C" int gift_fif_score_ex(const gift_fif_view* f, const float* Q, int32_t
     if (ev_scan_end) GIFT_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(ev_scan_end), st));
   }
 
+  const int n_ranges = static_cast<int>(cdiv(f->n_local, RED_RS));
+  probe_ranges_kernel<<<static_cast<unsigned>(cdiv(nprobes * n_ranges, 256)), 256, 0, st>>>(
+      w.cells, w.probe_rank, f->seg_off, f->seg_ord, w.outbase, w.meta, nprobes, n_ranges,
+      f->n_local, f->ord_base, w.rng);
+  GIFT_LAUNCH_CHECK();
   ReduceArgs ra;
-  ra.cells = w.cells;
-  ra.probe_rank = w.probe_rank;
-  ra.seg_off = f->seg_off;
+  ra.rng = w.rng;
   ra.seg_ord = f->seg_ord;
-  ra.outbase = w.outbase;
   ra.out = w.compact;
   ra.meta = w.meta;
   ra.vq = vq;
   ra.V = V;
   ra.ma = ma;
+  ra.n_ranges = n_ranges;
   ra.n_local = f->n_local;
   ra.ord_base = f->ord_base;
   ra.scores = out_scores;
-  const int red_smem = RED_RS * (8 + 4);
+  const int red_smem = RED_RS * (8 + 4 + 4);
   GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      red_smem));
-  dim3 rgrid(static_cast<unsigned>(cdiv(f->n_local, RED_RS)), static_cast<unsigned>(B));
+  dim3 rgrid(static_cast<unsigned>(n_ranges), static_cast<unsigned>(B));
   fif_reduce_kernel<<<rgrid, RED_THREADS, red_smem, st>>>(ra);
   GIFT_LAUNCH_CHECK();
   return GIFT_OK;

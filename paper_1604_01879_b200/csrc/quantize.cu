@@ -109,7 +109,7 @@ struct PairwisePlan {
 };
 
 // Postfix program of numpy's pairwise recursion for a length-d reduction.
-__device__ void build_plan(PairwisePlan& p, int d) {
+__host__ __device__ void build_plan(PairwisePlan& p, int d) {
   struct Frame {
     int off, n, state;
   };
@@ -157,16 +157,16 @@ __global__ void __launch_bounds__(QS_THREADS)
     quant_select_kernel(const float* __restrict__ approx, int64_t n, int K, int ma,
                         const void* __restrict__ X, int xdtype, int d, const float* __restrict__ C,
                         double cmax, const uint8_t* __restrict__ nz, int zero_key, int p2k,
-                        int32_t* __restrict__ out) {
+                        int32_t* __restrict__ out, const __grid_constant__ PairwisePlan plan) {
   extern __shared__ __align__(128) char smem[];
   float* a = reinterpret_cast<float*>(smem);
   double* cd = reinterpret_cast<double*>(smem + ((K * 4 + 15) / 16) * 16);
   int* ci = reinterpret_cast<int*>(cd + p2k);
-  __shared__ PairwisePlan plan;
   __shared__ double lv[QS_WARPS][MAX_LEAVES];
   __shared__ unsigned hist[256];
   __shared__ double s_red[QS_WARPS];
   __shared__ float s_redf[QS_WARPS];
+  __shared__ float s_small[QS_WARPS][8];
   __shared__ uint32_t s_prefix;
   __shared__ int s_rank, s_nc;
   __shared__ float s_kth;
@@ -188,10 +188,7 @@ __global__ void __launch_bounds__(QS_THREADS)
   for (int o = 16; o > 0; o >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
   if (lane == 0) s_red[warp] = xs;
   for (int c = tid; c < K; c += QS_THREADS) a[c] = approx[v * K + c];
-  if (tid == 0) {
-    build_plan(plan, d);
-    s_nc = 0;
-  }
+  if (tid == 0) s_nc = 0;
   __syncthreads();
   double xn2 = 0.0;
   for (int w = 0; w < QS_WARPS; ++w) xn2 += s_red[w];
@@ -208,6 +205,62 @@ __global__ void __launch_bounds__(QS_THREADS)
       float mm = INFINITY;
       for (int w = 0; w < QS_WARPS; ++w) mm = fminf(mm, s_redf[w]);
       s_kth = mm;
+    }
+    __syncthreads();
+  } else if (ma <= 8) {
+    // ma smallest values: per-thread sorted lists, then shuffle/shared merges
+    float loc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) loc[i] = INFINITY;
+    for (int c = tid; c < K; c += QS_THREADS) {
+      float x = a[c];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (i < ma && x < loc[i]) {
+          float t = loc[i];
+          loc[i] = x;
+          x = t;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      float oth[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) oth[i] = __shfl_xor_sync(0xffffffffu, loc[i], o);
+      float mrg[8];
+      int ia = 0, ib = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float va = loc[min(ia, 7)], vb = oth[min(ib, 7)];
+        if (va <= vb) {
+          mrg[i] = va;
+          ++ia;
+        } else {
+          mrg[i] = vb;
+          ++ib;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) loc[i] = mrg[i];
+    }
+    if (lane == 0)
+      for (int i = 0; i < 8; ++i) s_small[warp][i] = loc[i];
+    __syncthreads();
+    if (tid == 0) {
+      float all[QS_WARPS * 8];
+      for (int w = 0; w < QS_WARPS; ++w)
+        for (int i = 0; i < 8; ++i) all[w * 8 + i] = s_small[w][i];
+      // ma-th smallest of the merged multiset (ma <= 8)
+      for (int i = 0; i < ma; ++i) {
+        int best = i;
+        for (int j = i + 1; j < QS_WARPS * 8; ++j)
+          if (all[j] < all[best]) best = j;
+        float t = all[i];
+        all[i] = all[best];
+        all[best] = t;
+      }
+      s_kth = all[ma - 1];
     }
     __syncthreads();
   } else {
@@ -356,6 +409,8 @@ extern "C" int gift_quantize(const void* X, int32_t xdtype, int64_t n, int32_t d
   GIFT_CUDA_TRY(cudaFuncSetAttribute(quant_select_kernel,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(sel_smem)));
+  PairwisePlan plan;
+  build_plan(plan, d);
   const bool a_half = xdtype == GIFT_F16;
   const int approx_smem = a_half ? simt::Cfg<true>::SMEM : simt::Cfg<false>::SMEM;
   if (a_half)
@@ -396,7 +451,7 @@ extern "C" int gift_quantize(const void* X, int32_t xdtype, int64_t n, int32_t d
     GIFT_LAUNCH_CHECK();
     quant_select_kernel<<<static_cast<unsigned>(nr), QS_THREADS, sel_smem, st>>>(
         approx, nr, K, ma, xs, xdtype, d, C, cmax_norm, nz ? nz + r0 : nullptr, zero_key, p2k,
-        out_idx + r0 * ma);
+        out_idx + r0 * ma, plan);
     GIFT_LAUNCH_CHECK();
   }
   return GIFT_OK;

@@ -59,21 +59,50 @@ __device__ void bitonic_merge_desc(double* s, uint32_t* t, int32_t* j) {
   }
 }
 
-template <int CAP>
-__global__ void __launch_bounds__(TK_THREADS)
-    topk_rows_kernel(const double* __restrict__ scores, int64_t n, int k,
-                     const int32_t* __restrict__ idrank, const int32_t* __restrict__ self_local,
-                     int64_t ord_base, int positive_only, int32_t* __restrict__ out_idx,
-                     double* __restrict__ out_val) {
+struct TopkIn {
+  // dense rows (slice pass)
+  const double* scores;
+  int64_t n, slice_len;
+  const int32_t* idrank;
+  const int32_t* self_local;
+  int64_t ord_base;
+  // explicit candidates (merge pass): m per row, idx already global
+  const double* cs;
+  const uint32_t* ct;
+  const int32_t* ci;
+  int64_t m;
+};
+
+struct TopkOut {
+  int k, positive_only, final_out, nslices;
+  int32_t* out_idx;  // final: [B, k]
+  double* out_val;
+  double* cs;        // partial: [B, nslices, k]
+  uint32_t* ct;
+  int32_t* ci;
+};
+
+template <int CAP, bool DENSE>
+__global__ void __launch_bounds__(TK_THREADS) topk_kernel(const TopkIn in, const TopkOut out) {
   extern __shared__ __align__(128) char smem_raw[];
   TopkSmem<CAP>& S = *reinterpret_cast<TopkSmem<CAP>*>(smem_raw);
   __shared__ int s_cnt;
   __shared__ double s_ths;
   __shared__ uint32_t s_tht;
-  const int b = blockIdx.x;
+  const int b = blockIdx.y;
+  const int sl = blockIdx.x;
   const int tid = threadIdx.x;
-  const double* row = scores + static_cast<int64_t>(b) * n;
-  const int64_t self = self_local ? static_cast<int64_t>(self_local[b]) : -1;
+  const int k = out.k;
+  int64_t e0, e1;
+  if (DENSE) {
+    e0 = static_cast<int64_t>(sl) * in.slice_len;
+    e1 = min64(in.n, e0 + in.slice_len);
+  } else {
+    e0 = 0;
+    e1 = in.m;
+  }
+  const double* row = DENSE ? in.scores + static_cast<int64_t>(b) * in.n : nullptr;
+  const int64_t self = (DENSE && in.self_local) ? static_cast<int64_t>(in.self_local[b]) : -1;
   for (int i = tid; i < CAP; i += TK_THREADS) {
     S.bs[i] = -INFINITY;
     S.bt[i] = 0xffffffffu;
@@ -85,22 +114,32 @@ __global__ void __launch_bounds__(TK_THREADS)
     s_cnt = 0;
   }
   __syncthreads();
-  for (int64_t c0 = 0; c0 < n; c0 += CAP) {
+  for (int64_t c0 = e0; c0 < e1; c0 += CAP) {
     const double ths = s_ths;
     const uint32_t tht = s_tht;
     for (int i = tid; i < CAP; i += TK_THREADS) {
-      const int64_t jj = c0 + i;
-      if (jj < n) {
-        const double sc = row[jj];
-        const uint32_t tb =
-            jj == self ? 0u
-                       : 1u + static_cast<uint32_t>(idrank ? static_cast<int64_t>(idrank[jj])
-                                                           : ord_base + jj);
-        if (key_better(sc, tb, ths, tht)) {
+      const int64_t e = c0 + i;
+      if (e < e1) {
+        double sc;
+        uint32_t tb;
+        int32_t jj;
+        if (DENSE) {
+          sc = row[e];
+          tb = e == self ? 0u
+                         : 1u + static_cast<uint32_t>(in.idrank ? static_cast<int64_t>(in.idrank[e])
+                                                                : in.ord_base + e);
+          jj = static_cast<int32_t>(in.ord_base + e);
+        } else {
+          const int64_t at = static_cast<int64_t>(b) * in.m + e;
+          sc = in.cs[at];
+          tb = in.ct[at];
+          jj = in.ci[at];
+        }
+        if (jj >= 0 && key_better(sc, tb, ths, tht)) {
           int pos = atomicAdd(&s_cnt, 1);
           S.cs[pos] = sc;
           S.ct[pos] = tb;
-          S.cj[pos] = static_cast<int32_t>(jj);
+          S.cj[pos] = jj;
         }
       }
     }
@@ -117,9 +156,9 @@ __global__ void __launch_bounds__(TK_THREADS)
       bitonic_sort_desc<CAP>(S.cs, S.ct, S.cj);
       // top CAP of (best U cand) = elementwise better of best[i] and
       // cand[CAP-1-i]; staged in registers (two phases, no read/write race)
-      double ms[CAP / TK_THREADS > 0 ? CAP / TK_THREADS : 1];
-      uint32_t mt[CAP / TK_THREADS > 0 ? CAP / TK_THREADS : 1];
-      int32_t mj[CAP / TK_THREADS > 0 ? CAP / TK_THREADS : 1];
+      double ms[CAP / TK_THREADS];
+      uint32_t mt[CAP / TK_THREADS];
+      int32_t mj[CAP / TK_THREADS];
 #pragma unroll
       for (int q = 0; q < CAP / TK_THREADS; ++q) {
         const int i = tid + q * TK_THREADS;
@@ -147,23 +186,78 @@ __global__ void __launch_bounds__(TK_THREADS)
     }
   }
   for (int i = tid; i < k; i += TK_THREADS) {
-    int32_t j = S.bj[i];
-    double v = S.bs[i];
-    bool ok = j >= 0 && (!positive_only || v > 0.0);
-    out_idx[static_cast<int64_t>(b) * k + i] = ok ? static_cast<int32_t>(ord_base + j) : -1;
-    out_val[static_cast<int64_t>(b) * k + i] = ok ? v : 0.0;
+    const int32_t j = S.bj[i];
+    const double v = S.bs[i];
+    if (out.final_out) {
+      const bool ok = j >= 0 && (!out.positive_only || v > 0.0);
+      out.out_idx[static_cast<int64_t>(b) * k + i] = ok ? j : -1;
+      out.out_val[static_cast<int64_t>(b) * k + i] = ok ? v : 0.0;
+    } else {
+      const int64_t at = (static_cast<int64_t>(b) * out.nslices + sl) * k + i;
+      out.cs[at] = v;
+      out.ct[at] = S.bt[i];
+      out.ci[at] = j;
+    }
   }
 }
 
 template <int CAP>
 static int launch_topk(const double* scores, int B, int64_t n, int k, const int32_t* idrank,
                        const int32_t* self_local, int64_t ord_base, int positive_only,
-                       int32_t* out_idx, double* out_val, cudaStream_t st) {
+                       int32_t* out_idx, double* out_val, void* ws, size_t ws_bytes,
+                       cudaStream_t st) {
   const int smem = sizeof(TopkSmem<CAP>);
-  GIFT_CUDA_TRY(cudaFuncSetAttribute(topk_rows_kernel<CAP>,
+  GIFT_CUDA_TRY(cudaFuncSetAttribute(topk_kernel<CAP, true>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  topk_rows_kernel<CAP><<<B, TK_THREADS, smem, st>>>(scores, n, k, idrank, self_local, ord_base,
-                                                     positive_only, out_idx, out_val);
+  GIFT_CUDA_TRY(cudaFuncSetAttribute(topk_kernel<CAP, false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  // slices: enough CTAs to cover the GPU twice, each slice >= 2 * CAP keys
+  int64_t nsl = cdiv(2 * sm_count(), B);
+  nsl = min64(nsl, cdiv(n, 2 * CAP));
+  const size_t per = static_cast<size_t>(B) * k * (8 + 4 + 4);
+  if (ws == nullptr || nsl <= 1) nsl = 1;
+  while (nsl > 1 && per * nsl + 1024 > ws_bytes) --nsl;
+  TopkIn in{};
+  in.scores = scores;
+  in.n = n;
+  in.slice_len = cdiv(n, nsl);
+  in.idrank = idrank;
+  in.self_local = self_local;
+  in.ord_base = ord_base;
+  TopkOut out{};
+  out.k = k;
+  out.positive_only = positive_only;
+  out.out_idx = out_idx;
+  out.out_val = out_val;
+  if (nsl == 1) {
+    out.final_out = 1;
+    out.nslices = 1;
+    topk_kernel<CAP, true><<<dim3(1, B), TK_THREADS, smem, st>>>(in, out);
+    GIFT_LAUNCH_CHECK();
+    return GIFT_OK;
+  }
+  Arena ar(ws, ws_bytes);
+  const int64_t m = nsl * k;
+  double* cs = ar.take<double>(B * m);
+  uint32_t* ct = ar.take<uint32_t>(B * m);
+  int32_t* ci = ar.take<int32_t>(B * m);
+  GIFT_REQUIRE(cs && ct && ci, GIFT_ERR_CAPACITY, "top-k workspace too small");
+  out.final_out = 0;
+  out.nslices = static_cast<int>(nsl);
+  out.cs = cs;
+  out.ct = ct;
+  out.ci = ci;
+  topk_kernel<CAP, true><<<dim3(static_cast<unsigned>(nsl), B), TK_THREADS, smem, st>>>(in, out);
+  GIFT_LAUNCH_CHECK();
+  TopkIn in2{};
+  in2.cs = cs;
+  in2.ct = ct;
+  in2.ci = ci;
+  in2.m = m;
+  TopkOut out2 = out;
+  out2.final_out = 1;
+  out2.nslices = 1;
+  topk_kernel<CAP, false><<<dim3(1, B), TK_THREADS, smem, st>>>(in2, out2);
   GIFT_LAUNCH_CHECK();
   return GIFT_OK;
 }
@@ -172,16 +266,29 @@ static int launch_topk(const double* scores, int B, int64_t n, int k, const int3
 
 using namespace gift;
 
-extern "C" int gift_topk_rows(const double* scores, int32_t B, int64_t n, int32_t k,
-                              const int32_t* idrank, const int32_t* self_local, int64_t ord_base,
-                              int32_t positive_only, int32_t* out_idx, double* out_val,
-                              void* stream) {
+extern "C" size_t gift_topk_ws_bytes(int32_t B, int64_t n, int32_t k) {
+  int64_t nsl = min64(cdiv(2 * 148, max64(B, 1)), cdiv(max64(n, 1), 512));
+  return static_cast<size_t>(max64(B, 1)) * k * 16 * max64(nsl, 1) + 4096;
+}
+
+extern "C" int gift_topk_rows_ex(const double* scores, int32_t B, int64_t n, int32_t k,
+                                 const int32_t* idrank, const int32_t* self_local,
+                                 int64_t ord_base, int32_t positive_only, int32_t* out_idx,
+                                 double* out_val, void* ws, size_t ws_bytes, void* stream) {
   cudaStream_t st = as_stream(stream);
   GIFT_REQUIRE(k >= 1, GIFT_ERR_INVALID, "k must be >= 1");
   GIFT_REQUIRE(k <= 2048, GIFT_ERR_UNSUPPORTED, "k = %d > 2048", k);
   if (B <= 0) return GIFT_OK;
-  if (k <= 256) return launch_topk<256>(scores, B, n, k, idrank, self_local, ord_base, positive_only, out_idx, out_val, st);
-  if (k <= 512) return launch_topk<512>(scores, B, n, k, idrank, self_local, ord_base, positive_only, out_idx, out_val, st);
-  if (k <= 1024) return launch_topk<1024>(scores, B, n, k, idrank, self_local, ord_base, positive_only, out_idx, out_val, st);
-  return launch_topk<2048>(scores, B, n, k, idrank, self_local, ord_base, positive_only, out_idx, out_val, st);
+  if (k <= 256) return launch_topk<256>(scores, B, n, k, idrank, self_local, ord_base, positive_only, out_idx, out_val, ws, ws_bytes, st);
+  if (k <= 512) return launch_topk<512>(scores, B, n, k, idrank, self_local, ord_base, positive_only, out_idx, out_val, ws, ws_bytes, st);
+  if (k <= 1024) return launch_topk<1024>(scores, B, n, k, idrank, self_local, ord_base, positive_only, out_idx, out_val, ws, ws_bytes, st);
+  return launch_topk<2048>(scores, B, n, k, idrank, self_local, ord_base, positive_only, out_idx, out_val, ws, ws_bytes, st);
+}
+
+extern "C" int gift_topk_rows(const double* scores, int32_t B, int64_t n, int32_t k,
+                              const int32_t* idrank, const int32_t* self_local, int64_t ord_base,
+                              int32_t positive_only, int32_t* out_idx, double* out_val,
+                              void* stream) {
+  return gift_topk_rows_ex(scores, B, n, k, idrank, self_local, ord_base, positive_only, out_idx,
+                           out_val, nullptr, 0, stream);
 }

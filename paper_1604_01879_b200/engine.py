@@ -31,9 +31,10 @@ _DTYPE_CODE = {torch.float32: nat.GIFT_F32, torch.float16: nat.GIFT_F16,
 
 
 # libgift kernel launches of one QueryEngine.run batch (single channel, rerank):
-# view_prep, quantize approx + select, probe count, plan, scatter, compact
-# zero, scan, reduce (gift_fif_score) + top-k2, act_mean, sif_query, top-k.
-LAUNCHES_PER_BATCH = 13
+# view_prep, quantize approx + select, probe count, plan, scatter, compact zero,
+# query-plane gather, tcgen05 scan, probe ranges, reduce (gift_fif_score) +
+# top-k2 (slices + merge), act_mean, sif_query, top-k (slices + merge).
+LAUNCHES_PER_BATCH = 17
 
 
 def _bits(n: int) -> int:
@@ -343,9 +344,10 @@ def topk_rows(scores: torch.Tensor, k: int, *, idrank: torch.Tensor | None = Non
     B, n = scores.shape
     idx = torch.empty((B, k), dtype=torch.int32, device=scores.device)
     val = torch.empty((B, k), dtype=torch.float64, device=scores.device)
-    nat.call("gift_topk_rows", nat.ptr(scores.contiguous()), B, n, k, nat.ptr(idrank),
+    ws = nat.workspace("topk").get(nat.lib().gift_topk_ws_bytes(B, n, k))
+    nat.call("gift_topk_rows_ex", nat.ptr(scores.contiguous()), B, n, k, nat.ptr(idrank),
              nat.ptr(self_local), ord_base, int(positive_only), nat.ptr(idx), nat.ptr(val),
-             _sp(stream))
+             nat.ptr(ws), ws.numel(), _sp(stream))
     return idx, val
 
 
