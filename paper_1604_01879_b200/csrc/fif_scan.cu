@@ -23,7 +23,7 @@
 
 namespace gift {
 
-constexpr int RED_RS = 4096;  // shapes per reduce CTA
+constexpr int RED_RS = 4096;  // max shapes per reduce CTA (smem: 16 B per shape)
 constexpr int RED_THREADS = 256;
 constexpr int PLAN_THREADS = 1024;
 
@@ -239,7 +239,7 @@ __global__ void probe_ranges_kernel(const int32_t* __restrict__ cells,
                                     const int32_t* __restrict__ seg_ord,
                                     const int64_t* __restrict__ outbase,
                                     const int64_t* __restrict__ meta, int64_t nprobes,
-                                    int n_ranges, int64_t n_local, int64_t ord_base,
+                                    int n_ranges, int rs, int64_t n_local, int64_t ord_base,
                                     ProbeRange* __restrict__ rng) {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= nprobes * n_ranges || meta[M_OVERFLOW]) return;
@@ -251,8 +251,8 @@ __global__ void probe_ranges_kernel(const int32_t* __restrict__ cells,
     const int64_t b0 = seg_off[c], b1 = seg_off[c + 1];
     int64_t l = b0, h = b1;
     if (n_ranges > 1) {
-      const int64_t glo = ord_base + static_cast<int64_t>(r) * RED_RS;
-      const int64_t ghi = ord_base + min64(static_cast<int64_t>(r + 1) * RED_RS, n_local);
+      const int64_t glo = ord_base + static_cast<int64_t>(r) * rs;
+      const int64_t ghi = ord_base + min64(static_cast<int64_t>(r + 1) * rs, n_local);
       while (l < h) {
         int64_t mid = (l + h) >> 1;
         if (seg_ord[mid] < glo) l = mid + 1; else h = mid;
@@ -279,7 +279,7 @@ struct ReduceArgs {
   const float* out;
   const int64_t* meta;
   const int32_t* vq;
-  int V, ma, n_ranges;
+  int V, ma, n_ranges, rs;
   int64_t n_local, ord_base;
   double* scores;
 };
@@ -293,14 +293,14 @@ struct ReduceArgs {
 __global__ void __launch_bounds__(RED_THREADS) fif_reduce_kernel(ReduceArgs a) {
   extern __shared__ __align__(128) char smem[];
   double* acc = reinterpret_cast<double*>(smem);
-  float* vb0 = reinterpret_cast<float*>(acc + RED_RS);
-  float* vb1 = vb0 + RED_RS;
+  float* vb0 = reinterpret_cast<float*>(acc + a.rs);
+  float* vb1 = vb0 + a.rs;
   if (a.meta[M_OVERFLOW]) return;
   const int tid = threadIdx.x;
   const int b = blockIdx.y;
   const int rg = blockIdx.x;
-  const int64_t lo = static_cast<int64_t>(rg) * RED_RS;
-  const int n = static_cast<int>(min64(lo + RED_RS, a.n_local) - lo);
+  const int64_t lo = static_cast<int64_t>(rg) * a.rs;
+  const int n = static_cast<int>(min64(lo + a.rs, a.n_local) - lo);
   const int64_t glo = a.ord_base + lo;
   for (int i = tid; i < n; i += RED_THREADS) {
     acc[i] = 0.0;
@@ -391,7 +391,7 @@ bool carve(Arena& ar, const gift_fif_view* f, int64_t nviews, int ma, ScoreWs& w
   w.probe_rank = ar.take<int32_t>(nprobes);
   w.qws_bytes = gift_quantize_ws_bytes(nviews, f->d, K, GIFT_F32);
   w.qws = ar.take<char>(static_cast<int64_t>(w.qws_bytes));
-  w.rng = ar.take<ProbeRange>(nprobes * cdiv(max64(f->n_local, 1), RED_RS));
+  w.rng = ar.take<ProbeRange>(nprobes * max64(cdiv(max64(f->n_local, 1), 256), 1));
   if (!w.rng) return false;
   w.g1 = w.g2 = nullptr;
   if (use_tc(f)) {
@@ -445,8 +445,8 @@ extern "C" int gift_fif_score_ex(const gift_fif_view* f, const float* Q, int32_t
 
   int rc = gift_view_prep(Q, GIFT_F32, nviews, d, w.nz, w.qn2, stream);
   if (rc) return rc;
-  rc = gift_quantize(Q, GIFT_F32, nviews, d, f->centroids, f->cnorm2, K, f->cmax_norm, ma, w.nz, -1,
-                     w.cells, w.qws, w.qws_bytes, stream);
+  rc = quantize_impl(Q, GIFT_F32, nviews, d, f->centroids, f->cnorm2, K, f->cmax_norm, ma, w.nz,
+                     -1, w.cells, w.qws, w.qws_bytes, stream, false);
   if (rc) return rc;
   GIFT_CUDA_TRY(cudaMemsetAsync(w.counts, 0, sizeof(int32_t) * K, st));
   probe_count_kernel<<<static_cast<unsigned>(cdiv(nprobes, 256)), 256, 0, st>>>(w.cells, nprobes,
@@ -526,9 +526,14 @@ extern "C" int gift_fif_score_ex(const gift_fif_view* f, const float* Q, int32_t
     if (ev_scan_end) GIFT_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(ev_scan_end), st));
   }
 
-  const int n_ranges = static_cast<int>(cdiv(f->n_local, RED_RS));
+  // shape ranges: <= RED_RS shapes each, and enough (query, range) CTAs to
+  // cover the GPU twice
+  int64_t n_ranges64 = max64(cdiv(f->n_local, RED_RS), cdiv(2 * sm_count(), B));
+  n_ranges64 = min64(n_ranges64, cdiv(f->n_local, 256));
+  const int rs = static_cast<int>(cdiv(f->n_local, max64(n_ranges64, 1)));
+  const int n_ranges = static_cast<int>(cdiv(f->n_local, rs));
   probe_ranges_kernel<<<static_cast<unsigned>(cdiv(nprobes * n_ranges, 256)), 256, 0, st>>>(
-      w.cells, w.probe_rank, f->seg_off, f->seg_ord, w.outbase, w.meta, nprobes, n_ranges,
+      w.cells, w.probe_rank, f->seg_off, f->seg_ord, w.outbase, w.meta, nprobes, n_ranges, rs,
       f->n_local, f->ord_base, w.rng);
   GIFT_LAUNCH_CHECK();
   ReduceArgs ra;
@@ -540,10 +545,11 @@ extern "C" int gift_fif_score_ex(const gift_fif_view* f, const float* Q, int32_t
   ra.V = V;
   ra.ma = ma;
   ra.n_ranges = n_ranges;
+  ra.rs = rs;
   ra.n_local = f->n_local;
   ra.ord_base = f->ord_base;
   ra.scores = out_scores;
-  const int red_smem = RED_RS * (8 + 4 + 4);
+  const int red_smem = rs * (8 + 4 + 4);
   GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      red_smem));
   dim3 rgrid(static_cast<unsigned>(n_ranges), static_cast<unsigned>(B));

@@ -153,15 +153,48 @@ __device__ __forceinline__ float float_from_order_key(uint32_t u) {
   return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
 }
 
+__host__ __device__ __forceinline__ int xpad(int i) { return i + (i >> 7) * 8; }  // bank spread
+
+// numpy pairwise leaf (rows of 8..128 elements: 8 interleaved accumulators,
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), sequential tail; < 8: sequential from
+// 0.0) computed by a group of 8 lanes: lane j owns accumulator r_j, the tree
+// is three xor-shuffles.  The result is valid in the group's lane 0.
+__device__ double leaf_group(const float* __restrict__ xs, const void* X, int xdtype, int64_t xoff,
+                             const float* __restrict__ c, int off, int len, int gl,
+                             unsigned gmask) {
+  auto term = [&](int k) -> double {
+    const double xv = xs ? static_cast<double>(xs[xpad(k)]) : load_as_f64(X, xdtype, xoff + k);
+    const double t = __dsub_rn(static_cast<double>(c[k]), xv);
+    return __dmul_rn(t, t);
+  };
+  if (len < 8) {
+    double r = 0.0;
+    if (gl == 0)
+      for (int i = 0; i < len; ++i) r = __dadd_rn(r, term(off + i));
+    return r;
+  }
+  const int lim = len - (len % 8);
+  double r = term(off + gl);
+  for (int i = 8; i < lim; i += 8) r = __dadd_rn(r, term(off + i + gl));
+  r = __dadd_rn(r, __shfl_xor_sync(gmask, r, 1, 8));
+  r = __dadd_rn(r, __shfl_xor_sync(gmask, r, 2, 8));
+  r = __dadd_rn(r, __shfl_xor_sync(gmask, r, 4, 8));
+  if (gl == 0)
+    for (int i = lim; i < len; ++i) r = __dadd_rn(r, term(off + i));
+  return r;
+}
+
 __global__ void __launch_bounds__(QS_THREADS)
     quant_select_kernel(const float* __restrict__ approx, int64_t n, int K, int ma,
                         const void* __restrict__ X, int xdtype, int d, const float* __restrict__ C,
                         double cmax, const uint8_t* __restrict__ nz, int zero_key, int p2k,
-                        int32_t* __restrict__ out, const __grid_constant__ PairwisePlan plan) {
+                        int need_order, int stage_x, int32_t* __restrict__ out,
+                        const __grid_constant__ PairwisePlan plan) {
   extern __shared__ __align__(128) char smem[];
   float* a = reinterpret_cast<float*>(smem);
   double* cd = reinterpret_cast<double*>(smem + ((K * 4 + 15) / 16) * 16);
   int* ci = reinterpret_cast<int*>(cd + p2k);
+  float* xs = stage_x ? reinterpret_cast<float*>(ci + p2k) : nullptr;
   __shared__ double lv[QS_WARPS][MAX_LEAVES];
   __shared__ unsigned hist[256];
   __shared__ double s_red[QS_WARPS];
@@ -179,14 +212,15 @@ __global__ void __launch_bounds__(QS_THREADS)
     return;
   }
   const int64_t xoff = v * static_cast<int64_t>(d);
-  // |x| (f64) for the error margin
-  double xs = 0.0;
+  // stage x (exact in f32 for f32/f16 inputs) and |x| (f64) for the margin
+  double xsq = 0.0;
   for (int k = tid; k < d; k += QS_THREADS) {
-    double xv = load_as_f64(X, xdtype, xoff + k);
-    xs += xv * xv;
+    const double xv = load_as_f64(X, xdtype, xoff + k);
+    if (xs) xs[xpad(k)] = static_cast<float>(xv);
+    xsq += xv * xv;
   }
-  for (int o = 16; o > 0; o >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
-  if (lane == 0) s_red[warp] = xs;
+  for (int o = 16; o > 0; o >>= 1) xsq += __shfl_xor_sync(0xffffffffu, xsq, o);
+  if (lane == 0) s_red[warp] = xsq;
   for (int c = tid; c < K; c += QS_THREADS) a[c] = approx[v * K + c];
   if (tid == 0) s_nc = 0;
   __syncthreads();
@@ -208,7 +242,7 @@ __global__ void __launch_bounds__(QS_THREADS)
     }
     __syncthreads();
   } else if (ma <= 8) {
-    // ma smallest values: per-thread sorted lists, then shuffle/shared merges
+    // per-thread sorted lists, shuffle merges, final merge of the 4 warps
     float loc[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) loc[i] = INFINITY;
@@ -232,7 +266,7 @@ __global__ void __launch_bounds__(QS_THREADS)
       int ia = 0, ib = 0;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        float va = loc[min(ia, 7)], vb = oth[min(ib, 7)];
+        const float va = loc[min(ia, 7)], vb = oth[min(ib, 7)];
         if (va <= vb) {
           mrg[i] = va;
           ++ia;
@@ -251,12 +285,11 @@ __global__ void __launch_bounds__(QS_THREADS)
       float all[QS_WARPS * 8];
       for (int w = 0; w < QS_WARPS; ++w)
         for (int i = 0; i < 8; ++i) all[w * 8 + i] = s_small[w][i];
-      // ma-th smallest of the merged multiset (ma <= 8)
       for (int i = 0; i < ma; ++i) {
         int best = i;
         for (int j = i + 1; j < QS_WARPS * 8; ++j)
           if (all[j] < all[best]) best = j;
-        float t = all[i];
+        const float t = all[i];
         all[i] = all[best];
         all[best] = t;
       }
@@ -264,6 +297,7 @@ __global__ void __launch_bounds__(QS_THREADS)
     }
     __syncthreads();
   } else {
+    // radix select (large ma)
     if (tid == 0) {
       s_prefix = 0;
       s_rank = ma - 1;
@@ -314,15 +348,33 @@ __global__ void __launch_bounds__(QS_THREADS)
   }
   __syncthreads();
   const int nc = s_nc;
-  if (nc == ma && ma == 1) {
-    if (tid == 0) out[v * ma] = ci[0];
+  if (nc == ma && (ma == 1 || !need_order)) {
+    // the candidate set is the answer; only its order would need exact d2
+    if (tid == 0) {
+      for (int i = 1; i < ma; ++i)  // ascending index: deterministic slot order
+        for (int j = i; j > 0 && ci[j] < ci[j - 1]; --j) {
+          const int t = ci[j];
+          ci[j] = ci[j - 1];
+          ci[j - 1] = t;
+        }
+      for (int s = 0; s < ma; ++s) out[v * ma + s] = ci[s];
+    }
     return;
   }
-  // exact numpy-order d2 of every candidate (warp per candidate)
+  // exact numpy-order d2 of every candidate (one warp per candidate, 4
+  // leaves at a time on 8-lane groups)
+  const int grp = lane >> 3, gl = lane & 7;
+  const unsigned gmask = 0xFFu << (grp * 8);
   for (int q = warp; q < nc; q += QS_WARPS) {
     const float* crow = C + static_cast<int64_t>(ci[q]) * d;
-    for (int l = lane; l < plan.n_leaves; l += 32)
-      lv[warp][l] = leaf_sum(X, xdtype, xoff, crow, plan.leaf_off[l], plan.leaf_len[l]);
+    for (int l0 = 0; l0 < plan.n_leaves; l0 += 4) {
+      const int l = l0 + grp;
+      if (l < plan.n_leaves) {
+        const double r =
+            leaf_group(xs, X, xdtype, xoff, crow, plan.leaf_off[l], plan.leaf_len[l], gl, gmask);
+        if (gl == 0) lv[warp][l] = r;
+      }
+    }
     __syncwarp();
     if (lane == 0) {
       double stk[24];
@@ -331,16 +383,17 @@ __global__ void __launch_bounds__(QS_THREADS)
         if (plan.ops[o] == 0) {
           stk[sp++] = lv[warp][li++];
         } else {
-          double b = stk[--sp];
-          double aa = stk[--sp];
-          stk[sp++] = __dadd_rn(aa, b);
+          const double bb = stk[--sp];
+          const double aa = stk[--sp];
+          stk[sp++] = __dadd_rn(aa, bb);
         }
       }
       cd[q] = stk[0];
     }
     __syncwarp();
   }
-  // sort candidates ascending by (d2, index): bitonic over the next power of 2
+  __syncthreads();
+  // ascending (d2, index): bitonic over the next power of 2
   int p2 = 1;
   while (p2 < nc) p2 <<= 1;
   for (int i = nc + tid; i < p2; i += QS_THREADS) {
@@ -351,12 +404,12 @@ __global__ void __launch_bounds__(QS_THREADS)
   for (int size = 2; size <= p2; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       for (int i = tid; i < (p2 >> 1); i += QS_THREADS) {
-        int lo = 2 * stride * (i / stride) + (i % stride);
-        int hi = lo + stride;
-        bool up = (lo & size) == 0;
-        double dl = cd[lo], dh = cd[hi];
-        int il = ci[lo], ih = ci[hi];
-        bool hi_first = (dh < dl) || (dh == dl && ih < il);
+        const int lo = 2 * stride * (i / stride) + (i % stride);
+        const int hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const double dl = cd[lo], dh = cd[hi];
+        const int il = ci[lo], ih = ci[hi];
+        const bool hi_first = (dh < dl) || (dh == dl && ih < il);
         if (hi_first == up) {
           cd[lo] = dh;
           cd[hi] = dl;
@@ -386,10 +439,11 @@ extern "C" size_t gift_quantize_ws_bytes(int64_t n, int32_t d, int32_t K, int32_
   return per_row * rows + 4096 + 1024;
 }
 
-extern "C" int gift_quantize(const void* X, int32_t xdtype, int64_t n, int32_t d, const float* C,
-                             const double* cnorm2, int32_t K, double cmax_norm, int32_t ma,
-                             const uint8_t* nz, int32_t zero_key, int32_t* out_idx, void* ws,
-                             size_t ws_bytes, void* stream) {
+namespace gift {
+int quantize_impl(const void* X, int32_t xdtype, int64_t n, int32_t d, const float* C,
+                  const double* cnorm2, int32_t K, double cmax_norm, int32_t ma,
+                  const uint8_t* nz, int32_t zero_key, int32_t* out_idx, void* ws,
+                  size_t ws_bytes, void* stream, bool need_order) {
   cudaStream_t st = as_stream(stream);
   GIFT_REQUIRE(K >= 1 && d >= 1, GIFT_ERR_EMPTY, "empty codebook");
   GIFT_REQUIRE(ma >= 1 && ma <= K, GIFT_ERR_INVALID, "ma must be in [1, %d]", K);
@@ -405,7 +459,10 @@ extern "C" int gift_quantize(const void* X, int32_t xdtype, int64_t n, int32_t d
 
   int p2k = 1;
   while (p2k < K) p2k <<= 1;
-  const size_t sel_smem = ((static_cast<size_t>(K) * 4 + 15) / 16) * 16 + static_cast<size_t>(p2k) * 12;
+  const int stage_x = (xdtype != GIFT_F64) ? 1 : 0;
+  const size_t sel_smem = ((static_cast<size_t>(K) * 4 + 15) / 16) * 16 +
+                          static_cast<size_t>(p2k) * 12 +
+                          (stage_x ? static_cast<size_t>(xpad(d) + 16) * 4 : 0);
   GIFT_CUDA_TRY(cudaFuncSetAttribute(quant_select_kernel,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(sel_smem)));
@@ -451,8 +508,17 @@ extern "C" int gift_quantize(const void* X, int32_t xdtype, int64_t n, int32_t d
     GIFT_LAUNCH_CHECK();
     quant_select_kernel<<<static_cast<unsigned>(nr), QS_THREADS, sel_smem, st>>>(
         approx, nr, K, ma, xs, xdtype, d, C, cmax_norm, nz ? nz + r0 : nullptr, zero_key, p2k,
-        out_idx + r0 * ma, plan);
+        need_order ? 1 : 0, stage_x, out_idx + r0 * ma, plan);
     GIFT_LAUNCH_CHECK();
   }
   return GIFT_OK;
+}
+}  // namespace gift
+
+extern "C" int gift_quantize(const void* X, int32_t xdtype, int64_t n, int32_t d, const float* C,
+                             const double* cnorm2, int32_t K, double cmax_norm, int32_t ma,
+                             const uint8_t* nz, int32_t zero_key, int32_t* out_idx, void* ws,
+                             size_t ws_bytes, void* stream) {
+  return quantize_impl(X, xdtype, n, d, C, cnorm2, K, cmax_norm, ma, nz, zero_key, out_idx, ws,
+                       ws_bytes, stream, true);
 }

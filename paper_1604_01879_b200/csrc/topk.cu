@@ -114,10 +114,14 @@ __global__ void __launch_bounds__(TK_THREADS) topk_kernel(const TopkIn in, const
     s_cnt = 0;
   }
   __syncthreads();
-  for (int64_t c0 = e0; c0 < e1; c0 += CAP) {
+  // Stream the keys in sub-chunks of CAP/2; survivors of the running
+  // threshold are appended to the candidate buffer, which is sorted and
+  // merged into the best list only when it is half full (or at the end).
+  constexpr int SUB = CAP / 2;
+  for (int64_t c0 = e0; c0 < e1; c0 += SUB) {
     const double ths = s_ths;
     const uint32_t tht = s_tht;
-    for (int i = tid; i < CAP; i += TK_THREADS) {
+    for (int i = tid; i < SUB; i += TK_THREADS) {
       const int64_t e = c0 + i;
       if (e < e1) {
         double sc;
@@ -145,8 +149,9 @@ __global__ void __launch_bounds__(TK_THREADS) topk_kernel(const TopkIn in, const
     }
     __syncthreads();
     const int cnt = s_cnt;
-    __syncthreads();  // everyone has read s_cnt before the next chunk appends
-    if (cnt > 0) {
+    const bool last = c0 + SUB >= e1;
+    __syncthreads();  // everyone has read s_cnt before the next sub-chunk appends
+    if (cnt >= SUB || (last && cnt > 0)) {
       for (int i = cnt + tid; i < CAP; i += TK_THREADS) {
         S.cs[i] = -INFINITY;
         S.ct[i] = 0xffffffffu;

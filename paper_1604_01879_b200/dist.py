@@ -59,8 +59,10 @@ def _all_gather(t: torch.Tensor, group=None) -> torch.Tensor:
     G = dist.get_world_size(group)
     host = t.is_cuda and dist.get_backend(group) == "gloo"  # gloo: stage through host
     src = t.cpu() if host else t.contiguous()
-    buf = torch.empty((G,) + tuple(src.shape), dtype=src.dtype, device=src.device)
+    buf = torch.empty((G * src.shape[0],) + tuple(src.shape[1:]), dtype=src.dtype,
+                      device=src.device)
     dist.all_gather_into_tensor(buf, src, group=group)
+    buf = buf.view((G,) + tuple(src.shape))
     return buf.to(t.device) if host else buf
 
 
@@ -111,7 +113,7 @@ def build_sharded(X_local: torch.Tensor, cb: eg.DeviceCodebook, cfg, n_global: i
                  else torch.empty((b1 - b0, V, d), dtype=torch.float32, device=dev))
             _broadcast(Q, r, group)
             s = runner.score(fif, Q, cfg.ma, mode, cfg.sigma)
-            li, lv = eg.topk_rows(s, min(kk, fif.n_local), positive_only=True, ord_base=lo)
+            li, lv = eg.topk_rows(s, kk, positive_only=True, ord_base=lo)  # -1 padded: same shape on every rank
             gi, gv = all_gather_topk(lv, li, ordinal_tiebreak(li), kk, group)
             gi = gi.to(torch.int32).contiguous()
             eg.act_from_topk(gi, gv.contiguous(), k1, out=raw.rows(b0, b1))
@@ -162,7 +164,7 @@ class ShardedEngine:
         base = self.fif.ord_base
         if rerank:
             k2 = min(cfg.k2, self.n_global)
-            li, lv = eg.topk_rows(s, min(k2, self.fif.n_local), positive_only=True, ord_base=base)
+            li, lv = eg.topk_rows(s, k2, positive_only=True, ord_base=base)
             nbr, _ = all_gather_topk(lv, li, ordinal_tiebreak(li), k2, self.group)
             fa = eg.act_mean(self.raw, nbr.to(torch.int32).contiguous())
             final = self.sif.query(fa)
@@ -172,7 +174,7 @@ class ShardedEngine:
         loc_self = (self_global - base)
         loc_self = torch.where((loc_self >= 0) & (loc_self < self.fif.n_local), loc_self,
                                torch.full_like(loc_self, -1)).to(torch.int32)
-        li, lv = eg.topk_rows(final, min(k, self.fif.n_local), idrank=self.idrank[base:base +
+        li, lv = eg.topk_rows(final, k, idrank=self.idrank[base:base +
                               self.fif.n_local].contiguous(), self_local=loc_self, ord_base=base)
         tb = ranking_tiebreak(li, self.idrank, self_global)
         return all_gather_topk(lv, li, tb, k, self.group)
