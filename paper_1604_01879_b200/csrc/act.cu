@@ -58,63 +58,121 @@ __global__ void act_from_topk_kernel(const int32_t* __restrict__ tk_idx,
 }
 
 // mean_activation (rerank.py:90-100): dict accumulation in neighbour order,
-// coordinates sorted, divided by len(neighbor_list).  One thread per row.
-__global__ void act_mean_kernel(const int32_t* __restrict__ raw_idx,
-                                const double* __restrict__ raw_val,
-                                const int32_t* __restrict__ raw_cnt, int raw_cap,
-                                const int32_t* __restrict__ nbr, int B, int k2, int cap,
-                                int32_t* __restrict__ o_idx, double* __restrict__ o_val,
-                                int32_t* __restrict__ o_cnt, double* __restrict__ o_norm) {
-  const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+// coordinates sorted, divided by len(neighbor_list).  One warp per row: the
+// neighbours' sorted lists are staged in shared memory; an entry is the
+// "first" of its coordinate if no earlier list holds it (binary search);
+// first entries sum their coordinate over the lists in neighbour order (the
+// reference's acc.get(idx, 0.0) + val sequence) and land at the rank of
+// their coordinate among all first entries.
+constexpr int AM_WARPS = 2;
+constexpr int AM_MAX_E = 1024;
+
+__device__ __forceinline__ bool list_has(const int32_t* idx, int n, int x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (idx[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo < n && idx[lo] == x;
+}
+
+__global__ void __launch_bounds__(AM_WARPS * 32)
+    act_mean_kernel(const int32_t* __restrict__ raw_idx, const double* __restrict__ raw_val,
+                    const int32_t* __restrict__ raw_cnt, int raw_cap,
+                    const int32_t* __restrict__ nbr, int B, int k2, int cap,
+                    int32_t* __restrict__ o_idx, double* __restrict__ o_val,
+                    int32_t* __restrict__ o_cnt, double* __restrict__ o_norm) {
+  __shared__ int32_t s_idx[AM_WARPS][AM_MAX_E];
+  __shared__ double s_val[AM_WARPS][AM_MAX_E];
+  __shared__ int16_t s_lst[AM_WARPS][AM_MAX_E];
+  __shared__ int32_t s_first[AM_WARPS][AM_MAX_E];
+  __shared__ int32_t s_off[AM_WARPS][MAX_NBR + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * AM_WARPS + warp;
   if (b >= B) return;
-  int list[MAX_NBR];
-  int head[MAX_NBR];
-  int len[MAX_NBR];
-  int nl = 0;
-  for (int t = 0; t < k2; ++t) {
+  int32_t* I = s_idx[warp];
+  double* Vv = s_val[warp];
+  int16_t* L = s_lst[warp];
+  int32_t* F = s_first[warp];
+  int32_t* off = s_off[warp];
+  if (lane == 0) {
+    int nl = 0, e = 0;
+    off[0] = 0;
+    for (int t = 0; t < k2; ++t) {
+      const int q = nbr[b * k2 + t];
+      if (q < 0) continue;
+      e += raw_cnt[q];
+      off[++nl] = e;
+    }
+    off[MAX_NBR] = nl;
+  }
+  __syncwarp();
+  const int nl = off[MAX_NBR];
+  const int E = off[nl];
+  // stage the lists (list order = neighbour order)
+  for (int t = 0, tt = 0; t < k2; ++t) {
     const int q = nbr[b * k2 + t];
     if (q < 0) continue;
-    list[nl] = q;
-    head[nl] = 0;
-    len[nl] = raw_cnt[q];
-    ++nl;
+    const int n0 = off[tt], n = off[tt + 1] - off[tt];
+    for (int i = lane; i < n; i += 32) {
+      I[n0 + i] = raw_idx[static_cast<int64_t>(q) * raw_cap + i];
+      Vv[n0 + i] = raw_val[static_cast<int64_t>(q) * raw_cap + i];
+      L[n0 + i] = static_cast<int16_t>(tt);
+    }
+    ++tt;
   }
+  __syncwarp();
+  for (int e = lane; e < E; e += 32) {
+    const int x = I[e];
+    bool first = true;
+    for (int t = 0; t < L[e] && first; ++t)
+      if (list_has(I + off[t], off[t + 1] - off[t], x)) first = false;
+    F[e] = first ? 1 : 0;
+  }
+  __syncwarp();
   int32_t* oi = o_idx + b * cap;
   double* ov = o_val + b * cap;
-  int n = 0;
-  if (nl > 0) {
-    const double count = static_cast<double>(nl);
-    for (;;) {
-      int mn = 0x7fffffff;
-      for (int t = 0; t < nl; ++t)
-        if (head[t] < len[t]) mn = min(mn, raw_idx[static_cast<int64_t>(list[t]) * raw_cap + head[t]]);
-      if (mn == 0x7fffffff) break;
-      double acc = 0.0;
-      bool first = true;
-      for (int t = 0; t < nl; ++t) {
-        if (head[t] < len[t]) {
-          const int64_t at = static_cast<int64_t>(list[t]) * raw_cap + head[t];
-          if (raw_idx[at] == mn) {
-            acc = first ? __dadd_rn(0.0, raw_val[at]) : __dadd_rn(acc, raw_val[at]);
-            first = false;
-            ++head[t];
-          }
-        }
+  const double count = static_cast<double>(nl);
+  int n_out = 0;
+  for (int e = lane; e < E; e += 32) {
+    if (!F[e]) continue;
+    const int x = I[e];
+    int rank = 0;
+    for (int e2 = 0; e2 < E; ++e2) rank += (F[e2] && I[e2] < x) ? 1 : 0;
+    double acc = 0.0;
+    bool started = false;
+    for (int t = L[e]; t < nl; ++t) {
+      const int32_t* li = I + off[t];
+      const int n = off[t + 1] - off[t];
+      int lo = 0, hi = n;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (li[mid] < x) lo = mid + 1; else hi = mid;
       }
-      const double v = __ddiv_rn(acc, count);
-      if (v > 0.0 && n < cap) {
-        oi[n] = mn;
-        ov[n] = v;
-        ++n;
+      if (lo < n && li[lo] == x) {
+        const double v = Vv[off[t] + lo];
+        acc = started ? __dadd_rn(acc, v) : __dadd_rn(0.0, v);
+        started = true;
       }
     }
+    if (rank < cap) {
+      oi[rank] = x;
+      ov[rank] = __ddiv_rn(acc, count);
+    }
   }
-  for (int i = n; i < cap; ++i) {
+  for (int e = lane; e < E; e += 32) n_out += F[e];
+  for (int o = 16; o > 0; o >>= 1) n_out += __shfl_xor_sync(0xffffffffu, n_out, o);
+  __syncwarp();
+  // raw values are > 0, so every mean is > 0 (make_activation keeps all)
+  for (int i = n_out + lane; i < cap; i += 32) {
     oi[i] = -1;
     ov[i] = 0.0;
   }
-  o_cnt[b] = n;
-  o_norm[b] = seq_norm(ov, n);
+  __syncwarp();
+  if (lane == 0) {
+    o_cnt[b] = min(n_out, cap);
+    o_norm[b] = seq_norm(ov, min(n_out, cap));
+  }
 }
 
 __device__ __forceinline__ double np_power_scalar(double v, double e) {
@@ -261,8 +319,11 @@ extern "C" int gift_act_mean(const int32_t* raw_idx, const double* raw_val, cons
                              double* out_norm, void* stream) {
   GIFT_REQUIRE(k2 >= 0 && k2 <= MAX_NBR, GIFT_ERR_UNSUPPORTED, "k2 = %d > %d", k2, MAX_NBR);
   GIFT_REQUIRE(cap >= raw_cap * k2, GIFT_ERR_CAPACITY, "activation capacity too small");
+  GIFT_REQUIRE(raw_cap * k2 <= AM_MAX_E, GIFT_ERR_UNSUPPORTED, "k1 * k2 = %d > %d",
+               raw_cap * k2, AM_MAX_E);
   if (B <= 0) return GIFT_OK;
-  act_mean_kernel<<<static_cast<unsigned>(cdiv(B, 128)), 128, 0, as_stream(stream)>>>(
+  act_mean_kernel<<<static_cast<unsigned>(cdiv(B, AM_WARPS)), AM_WARPS * 32, 0,
+                    as_stream(stream)>>>(
       raw_idx, raw_val, raw_cnt, raw_cap, nbr, B, k2, cap, out_idx, out_val, out_cnt, out_norm);
   GIFT_LAUNCH_CHECK();
   return GIFT_OK;

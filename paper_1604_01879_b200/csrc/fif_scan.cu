@@ -23,7 +23,7 @@
 
 namespace gift {
 
-constexpr int RED_RS = 4096;  // max shapes per reduce CTA (smem: 16 B per shape)
+constexpr int64_t RED_SMEM = 64 * 1024;  // reduce CTA view-best tile budget
 constexpr int RED_THREADS = 256;
 constexpr int PLAN_THREADS = 1024;
 
@@ -284,63 +284,45 @@ struct ReduceArgs {
   double* scores;
 };
 
-// Per (query, shape range): view_best = max over the ma slots of each view,
-// total += view_best in view order (f64), score = total / Vq
-// (matching.py:153-161).  One barrier per view: the slot maxima of view v go
-// to vb[v & 1] (atomicMax on non-negative float bits) while view v-1's maxima
-// are folded into the f64 accumulator and cleared (atomicExch: exactly one
-// slot's thread sees each non-zero maximum, so acc has a single writer).
+// Per (query, shape range of rs shapes): every (view, slot) probe's
+// per-segment maxima are max-ed into vb[view][shape] (shared, atomicMax on
+// non-negative float bits: order-independent) in one parallel pass; then each
+// shape's column is summed in view order in f64 and divided by Vq —
+// total += view_best, score = total / Vq (matching.py:153-161), same add order.
 __global__ void __launch_bounds__(RED_THREADS) fif_reduce_kernel(ReduceArgs a) {
   extern __shared__ __align__(128) char smem[];
-  double* acc = reinterpret_cast<double*>(smem);
-  float* vb0 = reinterpret_cast<float*>(acc + a.rs);
-  float* vb1 = vb0 + a.rs;
+  float* vb = reinterpret_cast<float*>(smem);  // [V][rs]
   if (a.meta[M_OVERFLOW]) return;
   const int tid = threadIdx.x;
   const int b = blockIdx.y;
   const int rg = blockIdx.x;
-  const int64_t lo = static_cast<int64_t>(rg) * a.rs;
-  const int n = static_cast<int>(min64(lo + a.rs, a.n_local) - lo);
+  const int rs = a.rs;
+  const int64_t lo = static_cast<int64_t>(rg) * rs;
+  const int n = static_cast<int>(min64(lo + rs, a.n_local) - lo);
   const int64_t glo = a.ord_base + lo;
-  for (int i = tid; i < n; i += RED_THREADS) {
-    acc[i] = 0.0;
-    vb0[i] = 0.f;
-    vb1[i] = 0.f;
+  const int V = a.V;
+  for (int i = tid; i < V * rs; i += RED_THREADS) vb[i] = 0.f;
+  __syncthreads();
+  const int64_t pbase = static_cast<int64_t>(b) * V * a.ma;
+  const int nslot = V * a.ma;
+  // warp w takes probe slots w, w + 8, ...; lanes stride the slot's segments
+  const int warp = tid >> 5, lane = tid & 31;
+  for (int t = warp; t < nslot; t += RED_THREADS / 32) {
+    const ProbeRange pr = a.rng[(pbase + t) * a.n_ranges + rg];
+    float* row = vb + (t / a.ma) * rs;
+    for (int k = pr.sa + lane; k < pr.sb; k += 32) {
+      const int o = static_cast<int>(a.seg_ord[pr.seg0 + k] - glo);
+      const float val = a.out[pr.base + k];
+      atomicMax(reinterpret_cast<int*>(row + o), __float_as_int(val));
+    }
   }
   __syncthreads();
-  const int64_t pbase = static_cast<int64_t>(b) * a.V * a.ma;
-  for (int v = 0; v <= a.V; ++v) {
-    if (v < a.V) {
-      float* vb = (v & 1) ? vb1 : vb0;
-      for (int s = 0; s < a.ma; ++s) {
-        const ProbeRange pr = a.rng[(pbase + static_cast<int64_t>(v) * a.ma + s) * a.n_ranges + rg];
-        for (int k = pr.sa + tid; k < pr.sb; k += RED_THREADS) {
-          const int o = static_cast<int>(a.seg_ord[pr.seg0 + k] - glo);
-          const float val = a.out[pr.base + k];
-          if (a.ma == 1)
-            acc[o] += static_cast<double>(val);
-          else
-            atomicMax(reinterpret_cast<int*>(vb + o), __float_as_int(val));
-        }
-      }
-    }
-    if (a.ma > 1 && v > 0) {
-      float* vb = ((v - 1) & 1) ? vb1 : vb0;
-      for (int s = 0; s < a.ma; ++s) {
-        const ProbeRange pr =
-            a.rng[(pbase + static_cast<int64_t>(v - 1) * a.ma + s) * a.n_ranges + rg];
-        for (int k = pr.sa + tid; k < pr.sb; k += RED_THREADS) {
-          const int o = static_cast<int>(a.seg_ord[pr.seg0 + k] - glo);
-          const int old = atomicExch(reinterpret_cast<int*>(vb + o), 0);
-          if (old != 0) acc[o] += static_cast<double>(__int_as_float(old));
-        }
-      }
-    }
-    __syncthreads();
+  const double denom = static_cast<double>(a.vq ? a.vq[b] : V);
+  for (int o = tid; o < n; o += RED_THREADS) {
+    double acc = 0.0;
+    for (int v = 0; v < V; ++v) acc += static_cast<double>(vb[v * rs + o]);
+    a.scores[static_cast<int64_t>(b) * a.n_local + lo + o] = acc / denom;
   }
-  const double denom = static_cast<double>(a.vq ? a.vq[b] : a.V);
-  for (int i = tid; i < n; i += RED_THREADS)
-    a.scores[static_cast<int64_t>(b) * a.n_local + lo + i] = acc[i] / denom;
 }
 
 }  // namespace gift
@@ -375,7 +357,13 @@ bool use_tc(const gift_fif_view* f) {
   return tc_supported(f);
 }
 
-bool carve(Arena& ar, const gift_fif_view* f, int64_t nviews, int ma, ScoreWs& w) {
+int reduce_rs(int64_t V, int64_t n_local) {
+  int rs = static_cast<int>(RED_SMEM / (4 * max64(V, 1)));
+  rs = max(32, min(rs, 2048)) / 32 * 32;
+  return static_cast<int>(max64(min64(rs, n_local), 1));
+}
+
+bool carve(Arena& ar, const gift_fif_view* f, int64_t nviews, int V, int ma, ScoreWs& w) {
   const int K = f->K;
   const int64_t nprobes = nviews * ma;
   w.meta = ar.take<int64_t>(8);
@@ -391,7 +379,7 @@ bool carve(Arena& ar, const gift_fif_view* f, int64_t nviews, int ma, ScoreWs& w
   w.probe_rank = ar.take<int32_t>(nprobes);
   w.qws_bytes = gift_quantize_ws_bytes(nviews, f->d, K, GIFT_F32);
   w.qws = ar.take<char>(static_cast<int64_t>(w.qws_bytes));
-  w.rng = ar.take<ProbeRange>(nprobes * max64(cdiv(max64(f->n_local, 1), 256), 1));
+  w.rng = ar.take<ProbeRange>(nprobes * cdiv(max64(f->n_local, 1), reduce_rs(V, f->n_local)));
   if (!w.rng) return false;
   w.g1 = w.g2 = nullptr;
   if (use_tc(f)) {
@@ -412,7 +400,7 @@ extern "C" size_t gift_fif_score_ws_bytes(const gift_fif_view* f, int32_t B, int
                                           int64_t compact_capacity) {
   Arena ar(nullptr, SIZE_MAX / 2);
   ScoreWs w;
-  carve(ar, f, static_cast<int64_t>(B) * V, ma, w);
+  carve(ar, f, static_cast<int64_t>(B) * V, V, ma, w);
   return align_up(ar.used, 256) + static_cast<size_t>(compact_capacity) * sizeof(float) + 512;
 }
 
@@ -440,7 +428,7 @@ extern "C" int gift_fif_score_ex(const gift_fif_view* f, const float* Q, int32_t
   const int64_t nprobes = nviews * ma;
   Arena ar(ws, ws_bytes);
   ScoreWs w;
-  GIFT_REQUIRE(carve(ar, f, nviews, ma, w), GIFT_ERR_CAPACITY, "score workspace too small");
+  GIFT_REQUIRE(carve(ar, f, nviews, V, ma, w), GIFT_ERR_CAPACITY, "score workspace too small");
   const int K = f->K, d = f->d;
 
   int rc = gift_view_prep(Q, GIFT_F32, nviews, d, w.nz, w.qn2, stream);
@@ -526,11 +514,8 @@ extern "C" int gift_fif_score_ex(const gift_fif_view* f, const float* Q, int32_t
     if (ev_scan_end) GIFT_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(ev_scan_end), st));
   }
 
-  // shape ranges: <= RED_RS shapes each, and enough (query, range) CTAs to
-  // cover the GPU twice
-  int64_t n_ranges64 = max64(cdiv(f->n_local, RED_RS), cdiv(2 * sm_count(), B));
-  n_ranges64 = min64(n_ranges64, cdiv(f->n_local, 256));
-  const int rs = static_cast<int>(cdiv(f->n_local, max64(n_ranges64, 1)));
+  // shape ranges: a [V x rs] f32 view-best tile of <= RED_SMEM bytes per CTA
+  const int rs = reduce_rs(V, f->n_local);
   const int n_ranges = static_cast<int>(cdiv(f->n_local, rs));
   probe_ranges_kernel<<<static_cast<unsigned>(cdiv(nprobes * n_ranges, 256)), 256, 0, st>>>(
       w.cells, w.probe_rank, f->seg_off, f->seg_ord, w.outbase, w.meta, nprobes, n_ranges, rs,
@@ -549,7 +534,7 @@ extern "C" int gift_fif_score_ex(const gift_fif_view* f, const float* Q, int32_t
   ra.n_local = f->n_local;
   ra.ord_base = f->ord_base;
   ra.scores = out_scores;
-  const int red_smem = rs * (8 + 4 + 4);
+  const int red_smem = V * rs * 4;
   GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      red_smem));
   dim3 rgrid(static_cast<unsigned>(n_ranges), static_cast<unsigned>(B));

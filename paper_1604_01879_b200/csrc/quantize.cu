@@ -28,8 +28,7 @@ constexpr int MAX_D = 16384;
 template <bool A_HALF>
 __global__ void __launch_bounds__(simt::NTHR, 2)
     quant_approx_kernel(const void* __restrict__ X, int64_t n, int d, const float* __restrict__ C,
-                        const double* __restrict__ cn2, int K, float* __restrict__ approx,
-                        bool vec16) {
+                        int K, float* __restrict__ part, int ksplit, bool vec16) {
   extern __shared__ __align__(128) char smem[];
   const int64_t v0 = static_cast<int64_t>(blockIdx.x) * simt::TA;
   const int c0 = blockIdx.y * simt::TB;
@@ -39,6 +38,11 @@ __global__ void __launch_bounds__(simt::NTHR, 2)
   t.na = static_cast<int>(min64(simt::TA, n - v0));
   t.nb = min(simt::TB, K - c0);
   t.d = d;
+  // split-k: partial dot over [kbeg, kend) (multiple of BK)
+  const int kchunk = ((d + ksplit - 1) / ksplit + simt::BK - 1) / simt::BK * simt::BK;
+  t.kbeg = blockIdx.z * kchunk;
+  t.kend = min(d, t.kbeg + kchunk);
+  float* out = part + static_cast<int64_t>(blockIdx.z) * n * K;
   float acc[8][4];
   simt::mainloop<A_HALF>(
       smem, t, [&](int r) -> int64_t { return v0 + r; }, [&](int r) -> int64_t { return c0 + r; },
@@ -52,7 +56,7 @@ __global__ void __launch_bounds__(simt::NTHR, 2)
     for (int j = 0; j < 4; ++j) {
       int c = L.b_row(j);
       if (c >= t.nb) continue;
-      approx[(v0 + r) * K + c0 + c] = static_cast<float>(cn2[c0 + c]) - 2.0f * acc[i][j];
+      out[(v0 + r) * K + c0 + c] = acc[i][j];
     }
   }
 }
@@ -189,6 +193,7 @@ __global__ void __launch_bounds__(QS_THREADS)
                         const void* __restrict__ X, int xdtype, int d, const float* __restrict__ C,
                         double cmax, const uint8_t* __restrict__ nz, int zero_key, int p2k,
                         int need_order, int stage_x, int32_t* __restrict__ out,
+                        const double* __restrict__ cn2, int ksplit, int d_eff,
                         const __grid_constant__ PairwisePlan plan) {
   extern __shared__ __align__(128) char smem[];
   float* a = reinterpret_cast<float*>(smem);
@@ -221,7 +226,11 @@ __global__ void __launch_bounds__(QS_THREADS)
   }
   for (int o = 16; o > 0; o >>= 1) xsq += __shfl_xor_sync(0xffffffffu, xsq, o);
   if (lane == 0) s_red[warp] = xsq;
-  for (int c = tid; c < K; c += QS_THREADS) a[c] = approx[v * K + c];
+  for (int c = tid; c < K; c += QS_THREADS) {
+    float dot = approx[v * K + c];
+    for (int z = 1; z < ksplit; ++z) dot += approx[static_cast<int64_t>(z) * n * K + v * K + c];
+    a[c] = static_cast<float>(cn2[c]) - 2.0f * dot;
+  }
   if (tid == 0) s_nc = 0;
   __syncthreads();
   double xn2 = 0.0;
@@ -335,7 +344,9 @@ __global__ void __launch_bounds__(QS_THREADS)
   // rigorous margin M >= |approx + |x|^2 - d2_numpy|
   const double u32 = 5.9604644775390625e-08;  // 2^-24
   const double u64 = 1.1102230246251565e-16;  // 2^-53
-  const double gd = (d + 2) * u32 / (1.0 - (d + 2) * u32);
+  // split-k: each partial is a sequential chain of <= d_eff / ... terms;
+  // d_eff = chunk length + number of partial additions (+2)
+  const double gd = (d_eff + 2) * u32 / (1.0 - (d_eff + 2) * u32);
   const double M = 1.5 * (2.0 * (gd + 2.0 * u32) * xn * cmax + 3.0 * u32 * cmax * cmax +
                           2.0 * u32 * xn * cmax + (d + 4) * u64 * (xn + cmax) * (xn + cmax)) +
                    1e-30;
@@ -427,15 +438,19 @@ __global__ void __launch_bounds__(QS_THREADS)
 
 using namespace gift;
 
+constexpr int QA_MAX_SPLIT = 8;
+
 static int64_t quant_rows_for(size_t ws_bytes, int d, int K, int xdtype) {
-  size_t per_row = static_cast<size_t>(K) * 4 + (xdtype == GIFT_F64 ? static_cast<size_t>(d) * 4 : 0);
+  size_t per_row = static_cast<size_t>(K) * 4 * QA_MAX_SPLIT +
+                   (xdtype == GIFT_F64 ? static_cast<size_t>(d) * 4 : 0);
   if (ws_bytes < 4096) return 0;
   return static_cast<int64_t>((ws_bytes - 4096) / per_row);
 }
 
 extern "C" size_t gift_quantize_ws_bytes(int64_t n, int32_t d, int32_t K, int32_t xdtype) {
   int64_t rows = n < 16384 ? (n < 128 ? 128 : n) : 16384;
-  size_t per_row = static_cast<size_t>(K) * 4 + (xdtype == GIFT_F64 ? static_cast<size_t>(d) * 4 : 0);
+  size_t per_row = static_cast<size_t>(K) * 4 * QA_MAX_SPLIT +
+                   (xdtype == GIFT_F64 ? static_cast<size_t>(d) * 4 : 0);
   return per_row * rows + 4096 + 1024;
 }
 
@@ -478,7 +493,7 @@ int quantize_impl(const void* X, int32_t xdtype, int64_t n, int32_t d, const flo
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, approx_smem));
 
   Arena ar(ws, ws_bytes);
-  float* approx = ar.take<float>(rows * K);
+  float* approx = ar.take<float>(rows * K * QA_MAX_SPLIT);
   float* xconv = xdtype == GIFT_F64 ? ar.take<float>(rows * static_cast<int64_t>(d)) : nullptr;
   GIFT_REQUIRE(approx != nullptr && (xdtype != GIFT_F64 || xconv != nullptr), GIFT_ERR_CAPACITY,
                "quantize workspace too small");
@@ -498,17 +513,25 @@ int quantize_impl(const void* X, int32_t xdtype, int64_t n, int32_t d, const flo
     const bool aligned = (reinterpret_cast<uintptr_t>(a_src) % 16 == 0) &&
                          (reinterpret_cast<uintptr_t>(C) % 16 == 0);
     const bool vec16 = aligned && (a_half ? (d % 8 == 0) : (d % 4 == 0));
-    dim3 grid(static_cast<unsigned>(cdiv(nr, simt::TA)), static_cast<unsigned>(cdiv(K, simt::TB)));
+    // split-k so the grid covers the GPU ~2x (2 CTAs/SM), chunks >= 512
+    const int64_t tiles = cdiv(nr, simt::TA) * cdiv(K, simt::TB);
+    int ksplit = static_cast<int>(min64(cdiv(4 * sm_count(), tiles), QA_MAX_SPLIT));
+    ksplit = static_cast<int>(max64(1, min64(ksplit, d / 512)));
+    const int kchunk = ((d + ksplit - 1) / ksplit + simt::BK - 1) / simt::BK * simt::BK;
+    ksplit = (d + kchunk - 1) / kchunk;
+    const int d_eff = kchunk + ksplit;
+    dim3 grid(static_cast<unsigned>(cdiv(nr, simt::TA)), static_cast<unsigned>(cdiv(K, simt::TB)),
+              static_cast<unsigned>(ksplit));
     if (a_half)
-      quant_approx_kernel<true><<<grid, simt::NTHR, approx_smem, st>>>(a_src, nr, d, C, cnorm2, K,
-                                                                      approx, vec16);
+      quant_approx_kernel<true><<<grid, simt::NTHR, approx_smem, st>>>(a_src, nr, d, C, K, approx,
+                                                                      ksplit, vec16);
     else
-      quant_approx_kernel<false><<<grid, simt::NTHR, approx_smem, st>>>(a_src, nr, d, C, cnorm2, K,
-                                                                       approx, vec16);
+      quant_approx_kernel<false><<<grid, simt::NTHR, approx_smem, st>>>(a_src, nr, d, C, K, approx,
+                                                                       ksplit, vec16);
     GIFT_LAUNCH_CHECK();
     quant_select_kernel<<<static_cast<unsigned>(nr), QS_THREADS, sel_smem, st>>>(
         approx, nr, K, ma, xs, xdtype, d, C, cmax_norm, nz ? nz + r0 : nullptr, zero_key, p2k,
-        need_order ? 1 : 0, stage_x, out_idx + r0 * ma, plan);
+        need_order ? 1 : 0, stage_x, out_idx + r0 * ma, cnorm2, ksplit, d_eff, plan);
     GIFT_LAUNCH_CHECK();
   }
   return GIFT_OK;

@@ -38,7 +38,9 @@ struct TileRows {
   const void* a_base;  // element base of A rows (fp32 or fp16)
   const float* b_base;
   int na, nb;
-  int d;
+  int d;            // row stride (elements)
+  int kbeg = 0;     // k range [kbeg, kend) of this tile (split-k); kend < 0: d
+  int kend = -1;
   // row r of A starts at a_base + a_row(r) * d; same for B.
 };
 
@@ -49,6 +51,7 @@ __device__ __forceinline__ void load_stage(char* sA, char* sB, int k0, const Til
                                            ARowFn a_row, BRowFn b_row, bool vec16) {
   const int tid = threadIdx.x;
   const int d = t.d;
+  const int klim = t.kend < 0 ? d : t.kend;
   if (vec16) {
     if (!A_HALF) {
       // 128 rows x 8 chunks(16B) = 1024 chunk loads, 4 per thread
@@ -59,9 +62,9 @@ __device__ __forceinline__ void load_stage(char* sA, char* sB, int k0, const Til
         int k = k0 + c * 4;
         const float* src = static_cast<const float*>(t.a_base);
         int bytes = 0;
-        if (r < t.na && k < d) {
+        if (r < t.na && k < klim) {
           src = static_cast<const float*>(t.a_base) + a_row(r) * static_cast<int64_t>(d) + k;
-          bytes = min(16, (d - k) * 4);
+          bytes = min(16, (klim - k) * 4);
         }
         uint32_t dst = smem_u32(sA) + (r * 8 + (c ^ (r & 7))) * 16;
         cp_async16(dst, src, bytes);
@@ -75,9 +78,9 @@ __device__ __forceinline__ void load_stage(char* sA, char* sB, int k0, const Til
         int k = k0 + c * 8;
         const __half* src = static_cast<const __half*>(t.a_base);
         int bytes = 0;
-        if (r < t.na && k < d) {
+        if (r < t.na && k < klim) {
           src = static_cast<const __half*>(t.a_base) + a_row(r) * static_cast<int64_t>(d) + k;
-          bytes = min(16, (d - k) * 2);
+          bytes = min(16, (klim - k) * 2);
         }
         uint32_t dst = smem_u32(sA) + (r * 4 + (c ^ ((r >> 1) & 3))) * 16;
         cp_async16(dst, src, bytes);
@@ -91,9 +94,9 @@ __device__ __forceinline__ void load_stage(char* sA, char* sB, int k0, const Til
       int k = k0 + c * 4;
       const float* src = t.b_base;
       int bytes = 0;
-      if (r < t.nb && k < d) {
+      if (r < t.nb && k < klim) {
         src = t.b_base + b_row(r) * static_cast<int64_t>(d) + k;
-        bytes = min(16, (d - k) * 4);
+        bytes = min(16, (klim - k) * 4);
       }
       uint32_t dst = smem_u32(sB) + (r * 8 + (c ^ (r & 7))) * 16;
       cp_async16(dst, src, bytes);
@@ -105,7 +108,7 @@ __device__ __forceinline__ void load_stage(char* sA, char* sB, int k0, const Til
         int r = idx / BK, kk = idx % BK, k = k0 + kk;
         const float* src = static_cast<const float*>(t.a_base);
         int bytes = 0;
-        if (r < t.na && k < d) {
+        if (r < t.na && k < klim) {
           src = static_cast<const float*>(t.a_base) + a_row(r) * static_cast<int64_t>(d) + k;
           bytes = 4;
         }
@@ -117,7 +120,7 @@ __device__ __forceinline__ void load_stage(char* sA, char* sB, int k0, const Til
       for (int idx = tid; idx < TA * BK; idx += NTHR) {
         int r = idx / BK, kk = idx % BK, k = k0 + kk;
         __half v = __float2half(0.f);
-        if (r < t.na && k < d)
+        if (r < t.na && k < klim)
           v = static_cast<const __half*>(t.a_base)[a_row(r) * static_cast<int64_t>(d) + k];
         __half* dst = reinterpret_cast<__half*>(sA + (r * 4 + ((kk >> 3) ^ ((r >> 1) & 3))) * 16) +
                       (kk & 7);
@@ -128,7 +131,7 @@ __device__ __forceinline__ void load_stage(char* sA, char* sB, int k0, const Til
       int r = idx / BK, kk = idx % BK, k = k0 + kk;
       const float* src = t.b_base;
       int bytes = 0;
-      if (r < t.nb && k < d) {
+      if (r < t.nb && k < klim) {
         src = t.b_base + b_row(r) * static_cast<int64_t>(d) + k;
         bytes = 4;
       }
@@ -228,12 +231,13 @@ __device__ __forceinline__ void mainloop(char* smem, const TileRows& t, ARowFn a
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-  const int nk = (t.d + BK - 1) / BK;
+  const int kb0 = t.kbeg;
+  const int nk = ((t.kend < 0 ? t.d : t.kend) - kb0 + BK - 1) / BK;
 #pragma unroll
   for (int s = 0; s < NSTAGE - 1; ++s) {
     if (s < nk) {
       char* base = smem + s * C::STAGE;
-      load_stage<A_HALF>(base, base + C::A_STAGE, s * BK, t, a_row, b_row, vec16);
+      load_stage<A_HALF>(base, base + C::A_STAGE, kb0 + s * BK, t, a_row, b_row, vec16);
     }
     cp_async_commit();
   }
@@ -243,7 +247,7 @@ __device__ __forceinline__ void mainloop(char* smem, const TileRows& t, ARowFn a
     int nxt = kt + NSTAGE - 1;
     if (nxt < nk) {
       char* base = smem + (nxt % NSTAGE) * C::STAGE;
-      load_stage<A_HALF>(base, base + C::A_STAGE, nxt * BK, t, a_row, b_row, vec16);
+      load_stage<A_HALF>(base, base + C::A_STAGE, kb0 + nxt * BK, t, a_row, b_row, vec16);
     }
     cp_async_commit();
     const char* cur = smem + (kt % NSTAGE) * C::STAGE;
