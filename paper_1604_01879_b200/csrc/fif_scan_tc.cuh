@@ -42,4 +42,12 @@ size_t tc_probe_plane_bytes(int64_t nprobes, int d);
 int launch_scan_tc(const gift_fif_view* f, const float* Q, int64_t nprobes_max, TcArgs a,
                    __half* g1, __half* g2, cudaStream_t st, void* ev0, void* ev1);
 
+// tensor-core stage 1 of quantize (quant_tc.cu)
+double tc_dot_eps(int d);
+bool quant_tc_supported(int d, int xdtype);
+size_t quant_tc_ws_bytes(int64_t rows, int d, int K);
+int quant_approx_tc(const void* X, int xdtype, int64_t n, int d, const float* C, int K,
+                    float* part, int ksplit_max, int* ksplit_out, void* ws, size_t ws_bytes,
+                    cudaStream_t st);
+
 }  // namespace gift

@@ -15,6 +15,7 @@
 //      with the exact f64 pairwise-order arithmetic (__dsub_rn/__dmul_rn/
 //      __dadd_rn, no FMA contraction) and sorted by (d2, index).
 // The result is bit-identical to the reference's indices.
+#include "fif_scan_tc.cuh"
 #include "simt_tile.cuh"
 
 namespace gift {
@@ -193,7 +194,7 @@ __global__ void __launch_bounds__(QS_THREADS)
                         const void* __restrict__ X, int xdtype, int d, const float* __restrict__ C,
                         double cmax, const uint8_t* __restrict__ nz, int zero_key, int p2k,
                         int need_order, int stage_x, int32_t* __restrict__ out,
-                        const double* __restrict__ cn2, int ksplit, int d_eff,
+                        const double* __restrict__ cn2, int ksplit, double dot_eps,
                         const __grid_constant__ PairwisePlan plan) {
   extern __shared__ __align__(128) char smem[];
   float* a = reinterpret_cast<float*>(smem);
@@ -344,10 +345,10 @@ __global__ void __launch_bounds__(QS_THREADS)
   // rigorous margin M >= |approx + |x|^2 - d2_numpy|
   const double u32 = 5.9604644775390625e-08;  // 2^-24
   const double u64 = 1.1102230246251565e-16;  // 2^-53
-  // split-k: each partial is a sequential chain of <= d_eff / ... terms;
-  // d_eff = chunk length + number of partial additions (+2)
-  const double gd = (d_eff + 2) * u32 / (1.0 - (d_eff + 2) * u32);
-  const double M = 1.5 * (2.0 * (gd + 2.0 * u32) * xn * cmax + 3.0 * u32 * cmax * cmax +
+  // dot_eps bounds |fl(x.c) - x.c| / (|x| |c|) of stage 1 (CUDA-core split-k
+  // chains: gamma of the chunk length + partial additions; tensor cores:
+  // tc_dot_eps)
+  const double M = 1.5 * (2.0 * dot_eps * xn * cmax + 3.0 * u32 * cmax * cmax +
                           2.0 * u32 * xn * cmax + (d + 4) * u64 * (xn + cmax) * (xn + cmax)) +
                    1e-30;
   const double thresh = static_cast<double>(s_kth) + 2.0 * M;
@@ -440,18 +441,25 @@ using namespace gift;
 
 constexpr int QA_MAX_SPLIT = 8;
 
+static size_t quant_fixed_bytes(int d, int K) {
+  return 2 * align_up(static_cast<size_t>(K) * d * 2, 1024) + 16384;
+}
+static size_t quant_row_bytes(int d, int K) {
+  // partials + (f64 -> f32 conversion | two fp16 planes)
+  return static_cast<size_t>(K) * 4 * QA_MAX_SPLIT + static_cast<size_t>(d) * 4 + 64;
+}
+
 static int64_t quant_rows_for(size_t ws_bytes, int d, int K, int xdtype) {
-  size_t per_row = static_cast<size_t>(K) * 4 * QA_MAX_SPLIT +
-                   (xdtype == GIFT_F64 ? static_cast<size_t>(d) * 4 : 0);
-  if (ws_bytes < 4096) return 0;
-  return static_cast<int64_t>((ws_bytes - 4096) / per_row);
+  (void)xdtype;
+  const size_t fixed = quant_fixed_bytes(d, K);
+  if (ws_bytes < fixed) return 0;
+  return static_cast<int64_t>((ws_bytes - fixed) / quant_row_bytes(d, K));
 }
 
 extern "C" size_t gift_quantize_ws_bytes(int64_t n, int32_t d, int32_t K, int32_t xdtype) {
+  (void)xdtype;
   int64_t rows = n < 16384 ? (n < 128 ? 128 : n) : 16384;
-  size_t per_row = static_cast<size_t>(K) * 4 * QA_MAX_SPLIT +
-                   (xdtype == GIFT_F64 ? static_cast<size_t>(d) * 4 : 0);
-  return per_row * rows + 4096 + 1024;
+  return quant_row_bytes(d, K) * rows + quant_fixed_bytes(d, K) + 4096;
 }
 
 namespace gift {
@@ -497,6 +505,9 @@ int quantize_impl(const void* X, int32_t xdtype, int64_t n, int32_t d, const flo
   float* xconv = xdtype == GIFT_F64 ? ar.take<float>(rows * static_cast<int64_t>(d)) : nullptr;
   GIFT_REQUIRE(approx != nullptr && (xdtype != GIFT_F64 || xconv != nullptr), GIFT_ERR_CAPACITY,
                "quantize workspace too small");
+  const bool use_tc = quant_tc_supported(d, xdtype);
+  void* tc_ws = ar.base + align_up(ar.used, 256);
+  const size_t tc_ws_bytes = ar.remaining();
 
   const size_t esz = xdtype == GIFT_F16 ? 2 : (xdtype == GIFT_F64 ? 8 : 4);
   for (int64_t r0 = 0; r0 < n; r0 += rows) {
@@ -510,28 +521,40 @@ int quantize_impl(const void* X, int32_t xdtype, int64_t n, int32_t d, const flo
       GIFT_LAUNCH_CHECK();
       a_src = xconv;
     }
-    const bool aligned = (reinterpret_cast<uintptr_t>(a_src) % 16 == 0) &&
-                         (reinterpret_cast<uintptr_t>(C) % 16 == 0);
-    const bool vec16 = aligned && (a_half ? (d % 8 == 0) : (d % 4 == 0));
-    // split-k so the grid covers the GPU ~2x (2 CTAs/SM), chunks >= 512
-    const int64_t tiles = cdiv(nr, simt::TA) * cdiv(K, simt::TB);
-    int ksplit = static_cast<int>(min64(cdiv(4 * sm_count(), tiles), QA_MAX_SPLIT));
-    ksplit = static_cast<int>(max64(1, min64(ksplit, d / 512)));
-    const int kchunk = ((d + ksplit - 1) / ksplit + simt::BK - 1) / simt::BK * simt::BK;
-    ksplit = (d + kchunk - 1) / kchunk;
-    const int d_eff = kchunk + ksplit;
-    dim3 grid(static_cast<unsigned>(cdiv(nr, simt::TA)), static_cast<unsigned>(cdiv(K, simt::TB)),
-              static_cast<unsigned>(ksplit));
-    if (a_half)
-      quant_approx_kernel<true><<<grid, simt::NTHR, approx_smem, st>>>(a_src, nr, d, C, K, approx,
-                                                                      ksplit, vec16);
-    else
-      quant_approx_kernel<false><<<grid, simt::NTHR, approx_smem, st>>>(a_src, nr, d, C, K, approx,
-                                                                       ksplit, vec16);
-    GIFT_LAUNCH_CHECK();
+    int ksplit = 1;
+    double dot_eps;
+    if (use_tc) {
+      int rc = quant_approx_tc(xs, xdtype, nr, d, C, K, approx, QA_MAX_SPLIT, &ksplit, tc_ws,
+                               tc_ws_bytes, st);
+      if (rc) return rc;
+      dot_eps = tc_dot_eps(d);
+    } else {
+      const bool aligned = (reinterpret_cast<uintptr_t>(a_src) % 16 == 0) &&
+                           (reinterpret_cast<uintptr_t>(C) % 16 == 0);
+      const bool vec16 = aligned && (a_half ? (d % 8 == 0) : (d % 4 == 0));
+      // split-k so the grid covers the GPU ~2x (2 CTAs/SM), chunks >= 512
+      const int64_t tiles = cdiv(nr, simt::TA) * cdiv(K, simt::TB);
+      ksplit = static_cast<int>(min64(cdiv(4 * sm_count(), tiles), QA_MAX_SPLIT));
+      ksplit = static_cast<int>(max64(1, min64(ksplit, d / 512)));
+      const int kchunk = ((d + ksplit - 1) / ksplit + simt::BK - 1) / simt::BK * simt::BK;
+      ksplit = (d + kchunk - 1) / kchunk;
+      dim3 grid(static_cast<unsigned>(cdiv(nr, simt::TA)), static_cast<unsigned>(cdiv(K, simt::TB)),
+                static_cast<unsigned>(ksplit));
+      if (a_half)
+        quant_approx_kernel<true><<<grid, simt::NTHR, approx_smem, st>>>(a_src, nr, d, C, K, approx,
+                                                                        ksplit, vec16);
+      else
+        quant_approx_kernel<false><<<grid, simt::NTHR, approx_smem, st>>>(a_src, nr, d, C, K,
+                                                                         approx, ksplit, vec16);
+      GIFT_LAUNCH_CHECK();
+      // sequential fp32 FMA chain of kchunk terms + (ksplit - 1) partial adds
+      const double u32 = 0x1p-24;
+      const double m = kchunk + ksplit + 2;
+      dot_eps = m * u32 / (1.0 - m * u32) + 2.0 * u32;
+    }
     quant_select_kernel<<<static_cast<unsigned>(nr), QS_THREADS, sel_smem, st>>>(
         approx, nr, K, ma, xs, xdtype, d, C, cmax_norm, nz ? nz + r0 : nullptr, zero_key, p2k,
-        need_order ? 1 : 0, stage_x, out_idx + r0 * ma, cnorm2, ksplit, d_eff, plan);
+        need_order ? 1 : 0, stage_x, out_idx + r0 * ma, cnorm2, ksplit, dot_eps, plan);
     GIFT_LAUNCH_CHECK();
   }
   return GIFT_OK;
