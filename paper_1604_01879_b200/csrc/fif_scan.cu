@@ -305,15 +305,46 @@ __global__ void __launch_bounds__(RED_THREADS) fif_reduce_kernel(ReduceArgs a) {
   __syncthreads();
   const int64_t pbase = static_cast<int64_t>(b) * V * a.ma;
   const int nslot = V * a.ma;
-  // warp w takes probe slots w, w + 8, ...; lanes stride the slot's segments
+  // warp w owns slots [w * per, (w + 1) * per); their (slot, segment) pairs
+  // are flattened so every lane's loads are independent (latency overlap)
   const int warp = tid >> 5, lane = tid & 31;
-  for (int t = warp; t < nslot; t += RED_THREADS / 32) {
-    const ProbeRange pr = a.rng[(pbase + t) * a.n_ranges + rg];
-    float* row = vb + (t / a.ma) * rs;
-    for (int k = pr.sa + lane; k < pr.sb; k += 32) {
-      const int o = static_cast<int>(a.seg_ord[pr.seg0 + k] - glo);
-      const float val = a.out[pr.base + k];
-      atomicMax(reinterpret_cast<int*>(row + o), __float_as_int(val));
+  constexpr int NW = RED_THREADS / 32;
+  const int per = (nslot + NW - 1) / NW;
+  const int s0 = warp * per, s1 = min(nslot, s0 + per);
+  for (int c0 = s0; c0 < s1; c0 += 32) {
+    // lane j holds slot c0 + j's range
+    const int sj = c0 + lane;
+    ProbeRange pr{0, 0, 0, 0};
+    if (sj < s1) pr = a.rng[(pbase + sj) * a.n_ranges + rg];
+    const int len = pr.sb - pr.sa;
+    int incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    const int excl = incl - len;
+    for (int it0 = 0; it0 < total; it0 += 32) {  // warp-uniform trip count
+      const int it = it0 + lane;
+      // slot owning item `it`: largest j with excl_j <= it (shuffle search)
+      int j = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const int cand = j + step;
+        const int ex = __shfl_sync(0xffffffffu, excl, cand);
+        if (cand < 32 && ex <= it) j = cand;
+      }
+      const int ej = __shfl_sync(0xffffffffu, excl, j);
+      const int saj = __shfl_sync(0xffffffffu, pr.sa, j);
+      const int64_t seg0 = __shfl_sync(0xffffffffu, pr.seg0, j);
+      const int64_t base = __shfl_sync(0xffffffffu, pr.base, j);
+      if (it < total) {
+        const int k = saj + (it - ej);
+        const int o = static_cast<int>(a.seg_ord[seg0 + k] - glo);
+        const float val = a.out[base + k];
+        atomicMax(reinterpret_cast<int*>(vb + ((c0 + j) / a.ma) * rs + o), __float_as_int(val));
+      }
     }
   }
   __syncthreads();
@@ -434,7 +465,7 @@ extern "C" int gift_fif_score_ex(const gift_fif_view* f, const float* Q, int32_t
   int rc = gift_view_prep(Q, GIFT_F32, nviews, d, w.nz, w.qn2, stream);
   if (rc) return rc;
   rc = quantize_impl(Q, GIFT_F32, nviews, d, f->centroids, f->cnorm2, K, f->cmax_norm, ma, w.nz,
-                     -1, w.cells, w.qws, w.qws_bytes, stream, false);
+                     -1, w.cells, w.qws, w.qws_bytes, stream, false, w.qn2);
   if (rc) return rc;
   GIFT_CUDA_TRY(cudaMemsetAsync(w.counts, 0, sizeof(int32_t) * K, st));
   probe_count_kernel<<<static_cast<unsigned>(cdiv(nprobes, 256)), 256, 0, st>>>(w.cells, nprobes,

@@ -37,7 +37,7 @@ bool tc_supported(const gift_fif_view* f);
 int quantize_impl(const void* X, int32_t xdtype, int64_t n, int32_t d, const float* C,
                   const double* cnorm2, int32_t K, double cmax_norm, int32_t ma,
                   const uint8_t* nz, int32_t zero_key, int32_t* out_idx, void* ws,
-                  size_t ws_bytes, void* stream, bool need_order);
+                  size_t ws_bytes, void* stream, bool need_order, const float* xnorm2);
 size_t tc_probe_plane_bytes(int64_t nprobes, int d);
 int launch_scan_tc(const gift_fif_view* f, const float* Q, int64_t nprobes_max, TcArgs a,
                    __half* g1, __half* g2, cudaStream_t st, void* ev0, void* ev1);

@@ -195,6 +195,7 @@ __global__ void __launch_bounds__(QS_THREADS)
                         double cmax, const uint8_t* __restrict__ nz, int zero_key, int p2k,
                         int need_order, int stage_x, int32_t* __restrict__ out,
                         const double* __restrict__ cn2, int ksplit, double dot_eps,
+                        const int32_t* __restrict__ flags,
                         const __grid_constant__ PairwisePlan plan) {
   extern __shared__ __align__(128) char smem[];
   float* a = reinterpret_cast<float*>(smem);
@@ -213,6 +214,7 @@ __global__ void __launch_bounds__(QS_THREADS)
   const int64_t v = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (v >= n) return;
+  if (flags != nullptr && flags[v] == 0) return;  // done by the warp kernel
   if (nz != nullptr && nz[v] == 0) {
     for (int s = tid; s < ma; s += QS_THREADS) out[v * ma + s] = zero_key >= 0 ? zero_key : -1;
     return;
@@ -435,6 +437,177 @@ __global__ void __launch_bounds__(QS_THREADS)
   for (int s = tid; s < ma; s += QS_THREADS) out[v * ma + s] = ci[s];
 }
 
+
+// Fast path of stage 2 (ma <= 8): one warp per vector.  Pass 1 finds the
+// ma-th smallest approx value (per-lane sorted lists + xor-shuffle merges),
+// pass 2 collects the candidates under the margin with a ballot; unambiguous
+// sets are written directly, small candidate sets (<= QW_MAXC) are re-scored
+// exactly by the warp (8-lane pairwise leaves), anything larger is flagged
+// for the CTA-per-vector kernel above.
+constexpr int QW_WARPS = 8;
+constexpr int QW_MAXC = 32;
+
+__global__ void __launch_bounds__(QW_WARPS * 32)
+    quant_select_warp_kernel(const float* __restrict__ approx, int64_t n, int K, int ma,
+                             const void* __restrict__ X, int xdtype, int d,
+                             const float* __restrict__ C, double cmax,
+                             const uint8_t* __restrict__ nz, int zero_key, int need_order,
+                             int32_t* __restrict__ out, const double* __restrict__ cn2,
+                             int ksplit, double dot_eps, const float* __restrict__ xnorm2,
+                             int32_t* __restrict__ flags,
+                             const __grid_constant__ PairwisePlan plan) {
+  extern __shared__ __align__(16) double qw_lv[];  // [QW_WARPS][n_leaves]
+  __shared__ int s_ci[QW_WARPS][QW_MAXC];
+  __shared__ double s_cd[QW_WARPS][QW_MAXC];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t v = static_cast<int64_t>(blockIdx.x) * QW_WARPS + warp;
+  if (v >= n) return;
+  if (nz != nullptr && nz[v] == 0) {
+    for (int s = lane; s < ma; s += 32) out[v * ma + s] = zero_key >= 0 ? zero_key : -1;
+    if (lane == 0) flags[v] = 0;
+    return;
+  }
+  const int64_t xoff = v * static_cast<int64_t>(d);
+  double xn;
+  if (xnorm2 != nullptr) {
+    xn = sqrt(static_cast<double>(xnorm2[v])) * (1.0 + 1e-5) + 1e-300;
+  } else {
+    double xsq = 0.0;
+    for (int k = lane; k < d; k += 32) {
+      const double xv = load_as_f64(X, xdtype, xoff + k);
+      xsq += xv * xv;
+    }
+    for (int o = 16; o > 0; o >>= 1) xsq += __shfl_xor_sync(0xffffffffu, xsq, o);
+    xn = sqrt(xsq) * (1.0 + 1e-6) + 1e-300;
+  }
+  auto approx_at = [&](int c) -> float {
+    float dot = approx[v * K + c];
+    for (int z = 1; z < ksplit; ++z) dot += approx[static_cast<int64_t>(z) * n * K + v * K + c];
+    return static_cast<float>(cn2[c]) - 2.0f * dot;
+  };
+  // pass 1: ma-th smallest
+  float loc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) loc[i] = INFINITY;
+  for (int c = lane; c < K; c += 32) {
+    float x = approx_at(c);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (i < ma && x < loc[i]) {
+        const float t = loc[i];
+        loc[i] = x;
+        x = t;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    float oth[8], mrg[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) oth[i] = __shfl_xor_sync(0xffffffffu, loc[i], o);
+    int ia = 0, ib = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float va = loc[min(ia, 7)], vb = oth[min(ib, 7)];
+      if (va <= vb) {
+        mrg[i] = va;
+        ++ia;
+      } else {
+        mrg[i] = vb;
+        ++ib;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) loc[i] = mrg[i];
+  }
+  float kth = loc[0];
+#pragma unroll
+  for (int i = 1; i < 8; ++i)
+    if (i == ma - 1) kth = loc[i];
+  const double u32 = 0x1p-24, u64 = 0x1p-53;
+  const double M = 1.5 * (2.0 * dot_eps * xn * cmax + 3.0 * u32 * cmax * cmax +
+                          2.0 * u32 * xn * cmax + (d + 4) * u64 * (xn + cmax) * (xn + cmax)) +
+                   1e-30;
+  const double thresh = static_cast<double>(kth) + 2.0 * M;
+  // pass 2: candidates under the threshold
+  int cnt = 0;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int c0 = 0; c0 < K; c0 += 32) {
+    const int c = c0 + lane;
+    const bool hit = c < K && static_cast<double>(approx_at(c)) <= thresh;
+    const unsigned bal = __ballot_sync(0xffffffffu, hit);
+    const int pos = cnt + __popc(bal & lt);
+    if (hit && pos < QW_MAXC) s_ci[warp][pos] = c;
+    cnt += __popc(bal);
+  }
+  __syncwarp();
+  if (cnt > QW_MAXC) {
+    if (lane == 0) flags[v] = 1;  // large candidate set: CTA kernel
+    return;
+  }
+  int* ci = s_ci[warp];
+  double* cd = s_cd[warp];
+  if (cnt == ma && (ma == 1 || !need_order)) {
+    if (lane == 0) {
+      for (int i = 1; i < ma; ++i)
+        for (int j = i; j > 0 && ci[j] < ci[j - 1]; --j) {
+          const int t = ci[j];
+          ci[j] = ci[j - 1];
+          ci[j - 1] = t;
+        }
+      for (int s = 0; s < ma; ++s) out[v * ma + s] = ci[s];
+      flags[v] = 0;
+    }
+    return;
+  }
+  // exact numpy-order d2 of each candidate (4 leaves at a time per warp)
+  double* lv = qw_lv + warp * plan.n_leaves;
+  const int grp = lane >> 3, gl = lane & 7;
+  const unsigned gmask = 0xFFu << (grp * 8);
+  for (int q = 0; q < cnt; ++q) {
+    const float* crow = C + static_cast<int64_t>(ci[q]) * d;
+    for (int l0 = 0; l0 < plan.n_leaves; l0 += 4) {
+      const int l = l0 + grp;
+      if (l < plan.n_leaves) {
+        const double r =
+            leaf_group(nullptr, X, xdtype, xoff, crow, plan.leaf_off[l], plan.leaf_len[l], gl, gmask);
+        if (gl == 0) lv[l] = r;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      double stk[24];
+      int sp = 0, li = 0;
+      for (int o = 0; o < plan.n_ops; ++o) {
+        if (plan.ops[o] == 0) {
+          stk[sp++] = lv[li++];
+        } else {
+          const double bb = stk[--sp];
+          const double aa = stk[--sp];
+          stk[sp++] = __dadd_rn(aa, bb);
+        }
+      }
+      cd[q] = stk[0];
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    // insertion sort by (d2, index)
+    for (int i = 1; i < cnt; ++i)
+      for (int j = i; j > 0 && (cd[j] < cd[j - 1] || (cd[j] == cd[j - 1] && ci[j] < ci[j - 1]));
+           --j) {
+        const double td = cd[j];
+        cd[j] = cd[j - 1];
+        cd[j - 1] = td;
+        const int ti = ci[j];
+        ci[j] = ci[j - 1];
+        ci[j - 1] = ti;
+      }
+    for (int s = 0; s < ma; ++s) out[v * ma + s] = ci[s];
+    flags[v] = 0;
+  }
+}
+
 }  // namespace gift
 
 using namespace gift;
@@ -466,7 +639,7 @@ namespace gift {
 int quantize_impl(const void* X, int32_t xdtype, int64_t n, int32_t d, const float* C,
                   const double* cnorm2, int32_t K, double cmax_norm, int32_t ma,
                   const uint8_t* nz, int32_t zero_key, int32_t* out_idx, void* ws,
-                  size_t ws_bytes, void* stream, bool need_order) {
+                  size_t ws_bytes, void* stream, bool need_order, const float* xnorm2) {
   cudaStream_t st = as_stream(stream);
   GIFT_REQUIRE(K >= 1 && d >= 1, GIFT_ERR_EMPTY, "empty codebook");
   GIFT_REQUIRE(ma >= 1 && ma <= K, GIFT_ERR_INVALID, "ma must be in [1, %d]", K);
@@ -506,6 +679,9 @@ int quantize_impl(const void* X, int32_t xdtype, int64_t n, int32_t d, const flo
   GIFT_REQUIRE(approx != nullptr && (xdtype != GIFT_F64 || xconv != nullptr), GIFT_ERR_CAPACITY,
                "quantize workspace too small");
   const bool use_tc = quant_tc_supported(d, xdtype);
+  int32_t* flags = ma <= 8 ? ar.take<int32_t>(rows) : nullptr;
+  GIFT_REQUIRE(ma > 8 || flags != nullptr, GIFT_ERR_CAPACITY, "quantize workspace too small");
+  const int qw_smem = QW_WARPS * plan.n_leaves * 8;
   void* tc_ws = ar.base + align_up(ar.used, 256);
   const size_t tc_ws_bytes = ar.remaining();
 
@@ -552,9 +728,17 @@ int quantize_impl(const void* X, int32_t xdtype, int64_t n, int32_t d, const flo
       const double m = kchunk + ksplit + 2;
       dot_eps = m * u32 / (1.0 - m * u32) + 2.0 * u32;
     }
+    if (flags != nullptr) {
+      quant_select_warp_kernel<<<static_cast<unsigned>(cdiv(nr, QW_WARPS)), QW_WARPS * 32, qw_smem,
+                                 st>>>(approx, nr, K, ma, xs, xdtype, d, C, cmax_norm,
+                                       nz ? nz + r0 : nullptr, zero_key, need_order ? 1 : 0,
+                                       out_idx + r0 * ma, cnorm2, ksplit, dot_eps,
+                                       xnorm2 ? xnorm2 + r0 : nullptr, flags, plan);
+      GIFT_LAUNCH_CHECK();
+    }
     quant_select_kernel<<<static_cast<unsigned>(nr), QS_THREADS, sel_smem, st>>>(
         approx, nr, K, ma, xs, xdtype, d, C, cmax_norm, nz ? nz + r0 : nullptr, zero_key, p2k,
-        need_order ? 1 : 0, stage_x, out_idx + r0 * ma, cnorm2, ksplit, dot_eps, plan);
+        need_order ? 1 : 0, stage_x, out_idx + r0 * ma, cnorm2, ksplit, dot_eps, flags, plan);
     GIFT_LAUNCH_CHECK();
   }
   return GIFT_OK;
@@ -566,5 +750,5 @@ extern "C" int gift_quantize(const void* X, int32_t xdtype, int64_t n, int32_t d
                              const uint8_t* nz, int32_t zero_key, int32_t* out_idx, void* ws,
                              size_t ws_bytes, void* stream) {
   return quantize_impl(X, xdtype, n, d, C, cnorm2, K, cmax_norm, ma, nz, zero_key, out_idx, ws,
-                       ws_bytes, stream, true);
+                       ws_bytes, stream, true, nullptr);
 }

@@ -366,3 +366,23 @@ def test_tensor_core_scan_matches_oracle_at_c2_dims(similarity, monkeypatch):
         np.testing.assert_allclose(g_simt, e, rtol=RTOL, atol=1e-12)
         assert ((g_tc == 0) == (e == 0)).all()
     print(f"max relative error tc vs oracle ({similarity}): {worst:.2e}")
+
+
+@pytest.mark.parametrize("impl", ["tc", "simt"])
+def test_quantize_near_ties_and_scale(impl, monkeypatch):
+    """Bit-exact assignment under stress: midpoints of centroid pairs (d2 ties
+    up to rounding), exact duplicates (ties -> lower index), and 8k config-2
+    views, on both stage-1 implementations (tensor cores / CUDA cores)."""
+    monkeypatch.setenv("GIFT_QUANT", impl)
+    views, _ = mixture_views(321, 200, 16, 4096, 55, mu0=-0.26)
+    C = sampled_codebook(views, 256, 9)
+    C[200] = C[17]  # exact duplicate centroids
+    rng = np.random.default_rng(4)
+    a, b = rng.integers(0, 256, 300), rng.integers(0, 256, 300)
+    mids = ((C[a].astype(np.float64) + C[b].astype(np.float64)) / 2).astype(np.float32)
+    X = np.concatenate([mids, C[:50], mixture_views(322, 500, 16, 4096, 55, mu0=-0.26)[0]
+                        .reshape(-1, 4096)]).astype(np.float32)
+    cb = Codebook(C)
+    for ma in (1, 2, 3):
+        got = quantize_batch(cb, X, ma)
+        np.testing.assert_array_equal(got, oracle.quantize_many(C, X.astype(np.float64), ma))
