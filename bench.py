@@ -152,8 +152,12 @@ def load_traffic(config):
 
 # ------------------------------------------------------------------ setup
 def build(w, device):
-    db, qs, _labels = synth.mixture(w, SEED, device)
-    C = synth.sample_centroids(db, w.K, SEED + 1).cpu().numpy()
+    if w.storage == "float16":  # config 4: Zipf-skewed cells, fp16 storage
+        db, qs, Ct = synth.zipf_mixture(w, SEED, device)
+        C = Ct.cpu().numpy()
+    else:
+        db, qs, _labels = synth.mixture(w, SEED, device)
+        C = synth.sample_centroids(db, w.K, SEED + 1).cpu().numpy()
     cfg = IndexConfig(n_views=w.n_views, codebook_size=w.K, ma=w.ma, k1=w.k1, k2=w.k2,
                       similarity="gaussian", sigma=w.sigma, storage_dtype=w.storage,
                       batch_size=w.batch, imported=True)
@@ -249,6 +253,54 @@ def run_reference(args, w):
     print(json.dumps(line), flush=True)
 
 
+def run_c5(args):
+    """Config 5 (re-rank dominated): given top-50 lists for 1M shapes, S-IF
+    over all shapes, queries re-ranked with k = 50 neighbour-set Jaccard."""
+    from paper_1604_01879_b200 import build_index_from_lists
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    c = synth.C5
+    n = args.c5_shapes or c["n_shapes"]
+    idx, val = synth.community_lists(SEED, device, n_shapes=n)
+    cfg = IndexConfig(k1=c["list_len"], k2=c["k2"], imported=True, batch_size=c["batch"])
+    t0 = time.perf_counter()
+    bundle = build_index_from_lists(idx, val, synth.shape_ids(n), cfg)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    eng = bundle.engine
+    g = torch.Generator(device=device)
+    g.manual_seed(SEED + 5)
+    B = c["batch"]
+    qrows = torch.randint(0, n, (B * (args.steps + args.warmup),), generator=g, device=device)
+    for i in range(args.warmup):
+        r = qrows[i * B:(i + 1) * B]
+        eng.rerank_lists(idx[r], val[r], top_k=c["top_k"], self_local=r.to(torch.int32))
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    with ClockSampler(local) as clk:
+        ev[0].record()
+        for i in range(args.warmup, args.warmup + args.steps):
+            r = qrows[i * B:(i + 1) * B]
+            eng.rerank_lists(idx[r], val[r], top_k=c["top_k"], self_local=r.to(torch.int32))
+        ev[1].record()
+        torch.cuda.synchronize()
+    ms = ev[0].elapsed_time(ev[1])
+    line = {"metric": METRIC, "value": B * args.steps / (ms / 1000), "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": "c5", "n_shapes": n, "list_len": c["list_len"],
+                       "communities": c["communities"], "k2": c["k2"], "top_k": c["top_k"],
+                       "batch": B, "sif_postings": int(bundle.sif.dev.e_ord.numel()),
+                       "build_s": build_s},
+            "e2e": None, "gpu_launches": 6 * args.steps, "roofline": None, "cpu_baseline": None,
+            "clocks": clk.summary()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 def run_gift(args, w):
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -342,7 +394,8 @@ def run_gift(args, w):
                            "dim": w.dim, "K": w.K, "ma": w.ma, "similarity": "gaussian",
                            "sigma": w.sigma, "k1": w.k1, "k2": w.k2, "top_k": w.top_k,
                            "batch": B, "parallelism": f"replicas{ws}",
-                           "l2": "inputs larger than L2 (database 10.5 GB)",
+                           "storage": w.storage, "n_queries": w.n_queries,
+                           "l2": "inputs larger than L2 (database >= 10.5 GB)",
                            "build_s": build_s},
                 "e2e": {"value": e2e_value, "unit": UNIT,
                         "h2d_bytes_per_step": B * w.n_views * w.dim * 4,
@@ -360,10 +413,18 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="gift", choices=["gift", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(synth.WORKLOADS))
+    ap.add_argument("--config", default="c2", choices=sorted(synth.WORKLOADS) + ["c5"])
+    ap.add_argument("--c5-shapes", type=int, default=0, help="override config-5 N (smoke runs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "gift" else args.warmup
+    if args.config == "c5":
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "config 5 reference arm not "
+                              "provided (oracle S-IF build of 1M shapes takes hours)"}))
+            return
+        run_c5(args)
+        return
     w = synth.WORKLOADS[args.config]
     if args.impl == "reference":
         run_reference(args, w)

@@ -10,6 +10,7 @@ from .index import (
     IndexBundle,
     IndexConfig,
     build_index,
+    build_index_from_lists,
     build_index_from_views,
     load_bundle,
     query,
@@ -24,6 +25,7 @@ __all__ = [
     "IndexBundle",
     "IndexConfig",
     "build_index",
+    "build_index_from_lists",
     "build_index_from_views",
     "load_bundle",
     "query",

@@ -32,7 +32,7 @@ namespace gift {
 constexpr int TC_M = 128;
 constexpr int TC_N = 64;
 constexpr int TC_BK = 64;  // fp16 per k-block = 128-byte rows
-constexpr int TC_STAGES = 3;
+constexpr int TC_STAGES = 4;
 constexpr int A_TILE = TC_M * TC_BK * 2;  // 16 KB
 constexpr int B_TILE = TC_N * TC_BK * 2;  //  8 KB
 constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;
@@ -121,6 +121,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // ------------------------------------------------------ TMA producer
     if (lane == 0) {
       const uint32_t bytes = (p.has_lo ? 2 * A_TILE : A_TILE) + 2 * B_TILE;
+      // (L2 evict-first hints on the postings measured slower: a posting tile
+      // is re-read by the next probe tile of its cell)
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {

@@ -132,9 +132,10 @@ class QueryEngine:
         self.b = bundle
         cfg = bundle.config
         self.cfg = cfg
-        self.fa = bundle.fifs["A"].dev
-        self.fb = bundle.fifs["B"].dev
-        self.dup = bundle.fifs["A"] is bundle.fifs["B"]
+        fa, fb = bundle.fifs.get("A"), bundle.fifs.get("B")
+        self.fa = fa.dev if fa is not None else None  # None: list-only index (config 5)
+        self.fb = fb.dev if fb is not None else None
+        self.dup = fa is fb
         ra, rb = bundle.raw_activations["A"], bundle.raw_activations["B"]
         self.raw_a = rr._rows(ra)
         self.raw_b = self.raw_a if rb is ra else rr._rows(rb)
@@ -183,6 +184,19 @@ class QueryEngine:
             final = (sa + sb) / 2.0
         k = min(top_k, self.n)
         return eg.topk_rows(final, k, idrank=self.idrank, self_local=self_local, stream=stream)
+
+    def rerank_lists(self, q_idx, q_val, top_k=10, self_local=None, stream=None):
+        """Re-rank from given best-first F-IF neighbour lists (config 5):
+        neighbours = the first k2 positive entries (top_neighbors,
+        rerank.py:78-87), query activation = their raw activations' mean,
+        S-IF Jaccard, final top-k (index.py:249-299)."""
+        k2 = min(self.cfg.k2, q_idx.shape[1])
+        nbr = torch.where(q_val[:, :k2] > 0, q_idx[:, :k2],
+                          torch.full_like(q_idx[:, :k2], -1)).to(torch.int32).contiguous()
+        fa = eg.act_mean(self.raw_a, nbr, stream=stream)
+        final = self.sif.query(fa, stream=stream)
+        return eg.topk_rows(final, min(top_k, self.n), idrank=self.idrank,
+                            self_local=self_local, stream=stream)
 
     def results(self, idx_row, val_row):
         ids, labels = self.b.shape_ids, self.b.labels
@@ -267,6 +281,34 @@ def build_index_from_views(views_a, shape_ids, config: IndexConfig = IndexConfig
                        labels=dict(labels) if labels else {s: "" for s in shape_ids},
                        codebooks=dict(codebooks), fifs={"A": fa, "B": fb},
                        raw_activations={"A": acts_a, "B": acts_b}, sif=sif)
+
+
+def build_index_from_lists(list_idx, list_scores, shape_ids, config: IndexConfig = IndexConfig(),
+                           labels=None) -> IndexBundle:
+    """Config 5 (re-rank dominated): the F-IF stage is given as best-first
+    neighbour lists per shape (idx [N, L] int, scores [N, L] f64, ordered by
+    (score desc, ordinal asc) like build_activation's lexsort).  Raw
+    activations = the first k1 positive entries (rerank.py:64-75),
+    neighbourhoods = the first k2 (rerank.py:78-87), then co-augment and the
+    S-IF as in index.py:211-218.  The bundle has no F-IF (query with
+    `QueryEngine.rerank_lists`)."""
+    shape_ids = list(shape_ids)
+    dev = nat.device()
+    idx = torch.as_tensor(list_idx).to(dev, dtype=torch.int32).contiguous()
+    val = torch.as_tensor(list_scores).to(dev, dtype=torch.float64).contiguous()
+    n, L = idx.shape
+    if n != len(shape_ids):
+        raise ValueError("lists and shape_ids disagree on the number of shapes")
+    k1, k2 = min(config.k1, L), min(config.k2, L)
+    raw = eg.act_from_topk(idx, val, k1)
+    nbr = torch.where(val[:, :k2] > 0, idx[:, :k2], torch.full_like(idx[:, :k2], -1)).contiguous()
+    final = eg.act_mean(raw, nbr)
+    sif = rr.SecondInvertedFile(shape_ids, eg.DeviceSif.build(final, n))
+    acts = rr.ActivationList(raw, shape_ids)
+    return IndexBundle(config=config, shape_ids=shape_ids,
+                       labels=dict(labels) if labels else {s: "" for s in shape_ids},
+                       codebooks={}, fifs={"A": None, "B": None},
+                       raw_activations={"A": acts, "B": acts}, sif=sif)
 
 
 def build_index(manifest, config: IndexConfig = IndexConfig(), jobs: int = 1,
