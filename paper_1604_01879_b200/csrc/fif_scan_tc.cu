@@ -30,22 +30,24 @@
 namespace gift {
 
 constexpr int TC_M = 128;
-constexpr int TC_N = 64;
-constexpr int TC_BK = 64;  // fp16 per k-block = 128-byte rows
-constexpr int TC_STAGES = 4;
-constexpr int A_TILE = TC_M * TC_BK * 2;  // 16 KB
-constexpr int B_TILE = TC_N * TC_BK * 2;  //  8 KB
+constexpr int TC_NMAX = 128;  // probes per item: N = 64 or 128 (per item)
+constexpr int TC_BK = 64;     // fp16 per k-block = 128-byte rows
+constexpr int TC_STAGES = 3;
+constexpr int A_TILE = TC_M * TC_BK * 2;     // 16 KB
+constexpr int B_BOX = 64 * TC_BK * 2;        //  8 KB (one 64-row TMA box)
+constexpr int B_TILE = TC_NMAX * TC_BK * 2;  // 16 KB
 constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;
-constexpr int EPI_STRIDE = TC_N + 1;
+constexpr int EPI_COLS = 32;  // epilogue stages 32 probe columns at a time
+constexpr int EPI_STRIDE = EPI_COLS + 1;
 constexpr int EPI_BYTES = TC_M * EPI_STRIDE * 4;
 constexpr int TC_THREADS = 192;
-constexpr uint32_t TMEM_COLS = 256;  // 2 buffers x (D1[64] | D2[64])
+constexpr uint32_t TMEM_COLS = 512;  // 2 buffers x (D1[128] | D2[128])
 constexpr int SMEM_TC = TC_STAGES * STAGE_BYTES + EPI_BYTES + 256;
 constexpr float SPLIT_SCALE = 2048.0f;        // 2^11
 constexpr float SPLIT_INV = 1.0f / 2048.0f;
 
 struct ItemInfo {
-  int c, mt, p0, p1, seg0, seg1, nb, pb0;
+  int c, mt, p0, p1, seg0, seg1, nb, pb0, n;  // n: MMA N of the item (64 | 128)
 };
 
 __device__ __forceinline__ ItemInfo decode_item(const TcArgs& p, int64_t item) {
@@ -58,15 +60,16 @@ __device__ __forceinline__ ItemInfo decode_item(const TcArgs& p, int64_t item) {
   I.c = lo;
   const int64_t rem = item - p.item_off[lo];
   const int cnt = p.counts[lo];
-  const int nm = (cnt + TC_N - 1) / TC_N;
+  const int nm = (cnt + TC_NMAX - 1) / TC_NMAX;
   const int64_t t = p.tile_off[lo] + rem / nm;
   I.mt = static_cast<int>(rem % nm);
   I.p0 = p.tile_pstart[t];
   I.p1 = p.tile_pend[t];
   I.seg0 = p.tile_seg0[t];
   I.seg1 = p.tile_seg1[t];
-  I.nb = min(TC_N, cnt - I.mt * TC_N);
-  I.pb0 = p.probe_off[lo] + I.mt * TC_N;
+  I.nb = min(TC_NMAX, cnt - I.mt * TC_NMAX);
+  I.pb0 = p.probe_off[lo] + I.mt * TC_NMAX;
+  I.n = I.nb > 64 ? 128 : 64;
   return I;
 }
 
@@ -81,7 +84,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                        const __grid_constant__ CUtensorMap tmB2, const TcArgs p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ int32_t s_sp[TC_M + 2];
-  __shared__ float s_qn2[TC_N];
+  __shared__ float s_qn2[TC_NMAX];
   float* Ds = reinterpret_cast<float*>(smem + TC_STAGES * STAGE_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TC_STAGES * STAGE_BYTES + EPI_BYTES);
   uint64_t* full = bars;
@@ -119,22 +122,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer
+    // (L2 evict-first hints on the postings measured slower: a posting tile
+    // is re-read by the next probe tile of its cell)
     if (lane == 0) {
-      const uint32_t bytes = (p.has_lo ? 2 * A_TILE : A_TILE) + 2 * B_TILE;
-      // (L2 evict-first hints on the postings measured slower: a posting tile
-      // is re-read by the next probe tile of its cell)
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
         const ItemInfo I = decode_item(p, item);
+        const int nbox = I.n / 64;
+        const uint32_t bytes = (p.has_lo ? 2 * A_TILE : A_TILE) + 2 * nbox * B_BOX;
         for (int kb = 0; kb < nkb; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * STAGE_BYTES;
           tc::mbar_arrive_expect_tx(&full[stage], bytes);
           tc::tma_load_2d(st, &tmA1, &full[stage], kb * TC_BK, I.p0);
           if (p.has_lo) tc::tma_load_2d(st + A_TILE, &tmA2, &full[stage], kb * TC_BK, I.p0);
-          tc::tma_load_2d(st + 2 * A_TILE, &tmB1, &full[stage], kb * TC_BK, I.pb0);
-          tc::tma_load_2d(st + 2 * A_TILE + B_TILE, &tmB2, &full[stage], kb * TC_BK, I.pb0);
+          for (int x = 0; x < nbox; ++x) {
+            tc::tma_load_2d(st + 2 * A_TILE + x * B_BOX, &tmB1, &full[stage], kb * TC_BK,
+                            I.pb0 + 64 * x);
+            tc::tma_load_2d(st + 2 * A_TILE + B_TILE + x * B_BOX, &tmB2, &full[stage],
+                            kb * TC_BK, I.pb0 + 64 * x);
+          }
           if (++stage == TC_STAGES) {
             stage = 0;
             phase ^= 1;
@@ -145,17 +153,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      const uint32_t idesc = tc::idesc_f16_f32(TC_M, TC_N);
       int stage = 0;
       uint32_t phase = 0;
       uint32_t chunk_ctr = 0;
       for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const ItemInfo I = decode_item(p, item);
+        const uint32_t idesc = tc::idesc_f16_f32(TC_M, I.n);
         for (int kb0 = 0; kb0 < nkb; kb0 += chunk_kb) {
           const uint32_t buf = chunk_ctr & 1, aph = (chunk_ctr >> 1) & 1;
           tc::mbar_wait(&tempty[buf], aph ^ 1);
           tc::tc_fence_after();
-          const uint32_t d1 = tmem_base + buf * 128;
-          const uint32_t d2 = d1 + TC_N;
+          const uint32_t d1 = tmem_base + buf * 256;
+          const uint32_t d2 = d1 + TC_NMAX;
           const int kend = min(kb0 + chunk_kb, nkb);
           for (int kb = kb0; kb < kend; ++kb) {
             tc::mbar_wait(&full[stage], phase);
@@ -194,64 +203,75 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const ItemInfo I = decode_item(p, item);
       const int nseg = I.seg1 - I.seg0;
+      const int ng = I.n / 16;  // 16-column groups in use
       for (int i = et; i <= nseg; i += TC_M) s_sp[i] = p.seg_pstart[I.seg0 + i];
-      if (et < TC_N) {
+      for (int m = et; m < TC_NMAX; m += TC_M) {
         float q = 0.f;
-        if (et < I.nb) q = p.qn2[p.probe_list[I.pb0 + et] / p.ma];
-        s_qn2[et] = q;
+        if (m < I.nb) q = p.qn2[p.probe_list[I.pb0 + m] / p.ma];
+        s_qn2[m] = q;
       }
-      float acc[TC_N];
+      float acc[TC_NMAX];
 #pragma unroll
-      for (int n = 0; n < TC_N; ++n) acc[n] = 0.f;
+      for (int n = 0; n < TC_NMAX; ++n) acc[n] = 0.f;
       for (int kb0 = 0; kb0 < nkb; kb0 += chunk_kb) {
         const uint32_t buf = chunk_ctr & 1, aph = (chunk_ctr >> 1) & 1;
         tc::mbar_wait(&tfull[buf], aph);
         tc::tc_fence_after();
-        const uint32_t base = tmem_base + (static_cast<uint32_t>(lb) << 16) + buf * 128;
+        const uint32_t base = tmem_base + (static_cast<uint32_t>(lb) << 16) + buf * 256;
 #pragma unroll
-        for (int j = 0; j < TC_N / 16; ++j) {
-          float v1[16], v2[16];
-          tc::tmem_ld_x16(base + j * 16, v1);
-          tc::tmem_ld_x16(base + TC_N + j * 16, v2);
-          tc::tmem_ld_wait();
+        for (int j = 0; j < TC_NMAX / 16; ++j) {
+          if (j < ng) {
+            float v1[16], v2[16];
+            tc::tmem_ld_x16(base + j * 16, v1);
+            tc::tmem_ld_x16(base + TC_NMAX + j * 16, v2);
+            tc::tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) acc[j * 16 + i] += fmaf(v2[i], SPLIT_INV, v1[i]);
+            for (int i = 0; i < 16; ++i) acc[j * 16 + i] += fmaf(v2[i], SPLIT_INV, v1[i]);
+          }
         }
         tc::tc_fence_before();
         tc::mbar_arrive(&tempty[buf]);
         ++chunk_ctr;
       }
       const float pn = (I.p0 + row < I.p1) ? p.pnorm2[I.p0 + row] : 0.f;
-#pragma unroll
-      for (int n = 0; n < TC_N; ++n) {
-        float v = acc[n];
-        if (gauss) v = 2.0f * v - pn;
-        Ds[row * EPI_STRIDE + n] = v;
-      }
-      named_bar(1, TC_M);
       const int64_t S_c = p.seg_off[I.c + 1] - p.seg_off[I.c];
       const int64_t seg_base = p.seg_off[I.c];
       const int64_t obase = p.outbase[I.c];
-      for (int idx = et; idx < nseg * I.nb; idx += TC_M) {
-        const int m = idx / nseg;
-        const int sl = idx - m * nseg;
-        const int sp0 = s_sp[sl], sp1 = s_sp[sl + 1];
-        const int r0 = max(sp0, I.p0) - I.p0, r1 = min(sp1, I.p1) - I.p0;
-        float mx = -INFINITY;
-        for (int r = r0; r < r1; ++r) mx = fmaxf(mx, Ds[r * EPI_STRIDE + m]);
-        float sim;
-        if (gauss)
-          sim = expf(-fmaxf(s_qn2[m] - mx, 0.f) * p.inv_sigma2);
-        else
-          sim = fminf(fmaxf(mx, 0.f), 1.f);
-        const int64_t o =
-            obase + static_cast<int64_t>(I.mt * TC_N + m) * S_c + (I.seg0 + sl - seg_base);
-        if (sp0 < I.p0 || sp1 > I.p1)
-          atomicMax(reinterpret_cast<int*>(p.out + o), __float_as_int(sim));
-        else
-          p.out[o] = sim;
+      // 32-column slices: stage -> per-segment max over rows -> store
+#pragma unroll
+      for (int sl0 = 0; sl0 < TC_NMAX; sl0 += EPI_COLS) {
+        if (sl0 < I.nb) {
+#pragma unroll
+          for (int c = 0; c < EPI_COLS; ++c) {
+            float v = acc[sl0 + c];
+            if (gauss) v = 2.0f * v - pn;  // max_p(2q.p - |p|^2) <-> min_p |q-p|^2
+            Ds[row * EPI_STRIDE + c] = v;
+          }
+          named_bar(1, TC_M);
+          const int ncol = min(EPI_COLS, I.nb - sl0);
+          for (int idx = et; idx < nseg * ncol; idx += TC_M) {
+            const int mc = idx / nseg;
+            const int sl = idx - mc * nseg;
+            const int m = sl0 + mc;
+            const int sp0 = s_sp[sl], sp1 = s_sp[sl + 1];
+            const int r0 = max(sp0, I.p0) - I.p0, r1 = min(sp1, I.p1) - I.p0;
+            float mx = -INFINITY;
+            for (int r = r0; r < r1; ++r) mx = fmaxf(mx, Ds[r * EPI_STRIDE + mc]);
+            float sim;
+            if (gauss)
+              sim = expf(-fmaxf(s_qn2[m] - mx, 0.f) * p.inv_sigma2);
+            else
+              sim = fminf(fmaxf(mx, 0.f), 1.f);
+            const int64_t o = obase + static_cast<int64_t>(I.mt * TC_NMAX + m) * S_c +
+                              (I.seg0 + sl - seg_base);
+            if (sp0 < I.p0 || sp1 > I.p1)
+              atomicMax(reinterpret_cast<int*>(p.out + o), __float_as_int(sim));
+            else
+              p.out[o] = sim;
+          }
+          named_bar(1, TC_M);
+        }
       }
-      named_bar(1, TC_M);
     }
   }
   tc::tc_fence_before();
@@ -353,9 +373,9 @@ int launch_scan_tc(const gift_fif_view* f, const float* Q, int64_t nprobes_max, 
   if (rc) return rc;
   rc = make_map(&mA2, f->feat_lo ? f->feat_lo : f->feat_hi, f->n_postings, d, TC_M);
   if (rc) return rc;
-  rc = make_map(&mB1, g1, max64(nprobes_max, 1), d, TC_N);
+  rc = make_map(&mB1, g1, max64(nprobes_max, 1), d, 64);
   if (rc) return rc;
-  rc = make_map(&mB2, g2, max64(nprobes_max, 1), d, TC_N);
+  rc = make_map(&mB2, g2, max64(nprobes_max, 1), d, 64);
   if (rc) return rc;
   a.has_lo = f->feat_lo != nullptr ? 1 : 0;
   GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_scan_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
