@@ -174,6 +174,18 @@ int gift_fif_score_ex(const gift_fif_view* f, const float* Q, int32_t B,
                       size_t ws_bytes, void* stream, void* ev_scan_begin,
                       void* ev_scan_end);
 
+/* Same, and with cand_k in [1, 8] also the best cand_k shapes (score desc,
+ * ordinal asc; -1 padded) of every (query, shape range) of the reduce:
+ * cand_s/cand_i [B][gift_fif_score_ranges(f, V)][cand_k] — merged by
+ * gift_topk_cand into rerank.top_neighbors (rerank.py:78-87). */
+int gift_fif_score_ranges(const gift_fif_view* f, int32_t V);
+int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_t B,
+                       int32_t V, const int32_t* vq, int32_t ma, int32_t mode,
+                       double sigma, double* out_scores, void* ws,
+                       size_t ws_bytes, void* stream, void* ev_scan_begin,
+                       void* ev_scan_end, int32_t cand_k, double* cand_s,
+                       int32_t* cand_i);
+
 /* ---- K4 top-k: replaces the lexsort selections rerank.py:74, :86-87 and
  * index.py:290-294.  Per row of a dense f64 score matrix [B, n], returns the
  * k best by (score desc, tiebreak asc) where tiebreak(j) = 0 if
@@ -192,6 +204,12 @@ int gift_topk_rows_ex(const double* scores, int32_t B, int64_t n, int32_t k,
                       int64_t ord_base, int32_t positive_only,
                       int32_t* out_idx, double* out_val, void* ws,
                       size_t ws_bytes, void* stream);
+
+/* Best k of m explicit candidates per row (cs scores, ci global ordinals,
+ * -1 = none), key (score desc, ordinal asc); positive_only as above. */
+int gift_topk_cand(const double* cs, const int32_t* ci, int32_t B, int64_t m,
+                   int32_t k, int32_t positive_only, int32_t* out_idx,
+                   double* out_val, void* stream);
 
 /* ---- K5 activations (fixed-capacity rows: idx[B,cap] asc, val, cnt, norm) */
 /* build_activation (rerank.py:64-75) from a top-k result: first k1 positive

@@ -68,6 +68,11 @@ _SIGS = {
                                 _c_i32, _c_dbl, _c_p, _c_p, _c_sz, _c_p]),
     "gift_fif_score_ex": (_c_i32, [ctypes.POINTER(FifView), _c_p, _c_i32, _c_i32, _c_p, _c_i32,
                                    _c_i32, _c_dbl, _c_p, _c_p, _c_sz, _c_p, _c_p, _c_p]),
+    "gift_fif_score_ranges": (_c_i32, [ctypes.POINTER(FifView), _c_i32]),
+    "gift_fif_score_ex2": (_c_i32, [ctypes.POINTER(FifView), _c_p, _c_i32, _c_i32, _c_p, _c_i32,
+                                    _c_i32, _c_dbl, _c_p, _c_p, _c_sz, _c_p, _c_p, _c_p, _c_i32,
+                                    _c_p, _c_p]),
+    "gift_topk_cand": (_c_i32, [_c_p, _c_p, _c_i32, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_p]),
     "gift_topk_rows": (_c_i32, [_c_p, _c_i32, _c_i64, _c_i32, _c_p, _c_p, _c_i64, _c_i32, _c_p,
                                 _c_p, _c_p]),
     "gift_topk_ws_bytes": (_c_sz, [_c_i32, _c_i64, _c_i32]),

@@ -283,7 +283,16 @@ struct ReduceArgs {
   int V, ma, n_ranges, rs;
   int64_t n_local, ord_base;
   double* scores;
+  int cand_k;        // > 0: also emit the range's best cand_k (score desc, ordinal asc)
+  double* cand_s;    // [B][n_ranges][cand_k]
+  int32_t* cand_i;   // global ordinals, -1 padded
 };
+
+constexpr int RED_MAXK = 8;
+
+__device__ __forceinline__ bool cand_better(double s1, int32_t o1, double s2, int32_t o2) {
+  return s1 > s2 || (s1 == s2 && static_cast<uint32_t>(o1) < static_cast<uint32_t>(o2));
+}
 
 // Per (query, shape range of rs shapes): every (view, slot) probe's
 // per-segment maxima are max-ed into vb[view][shape] (shared, atomicMax on
@@ -350,10 +359,102 @@ __global__ void __launch_bounds__(RED_THREADS) fif_reduce_kernel(ReduceArgs a) {
   }
   __syncthreads();
   const double denom = static_cast<double>(a.vq ? a.vq[b] : V);
+  const int ck = a.cand_k;
+  double bs[RED_MAXK];
+  int32_t bo[RED_MAXK];
+#pragma unroll
+  for (int i = 0; i < RED_MAXK; ++i) {
+    bs[i] = -INFINITY;
+    bo[i] = -1;
+  }
   for (int o = tid; o < n; o += RED_THREADS) {
     double acc = 0.0;
     for (int v = 0; v < V; ++v) acc += static_cast<double>(vb[v * rs + o]);
-    a.scores[static_cast<int64_t>(b) * a.n_local + lo + o] = acc / denom;
+    const double sc = acc / denom;
+    a.scores[static_cast<int64_t>(b) * a.n_local + lo + o] = sc;
+    if (ck > 0) {  // per-thread sorted best list (ordinals ascend within a thread)
+      double x = sc;
+      int32_t xo = static_cast<int32_t>(glo + o);
+#pragma unroll
+      for (int i = 0; i < RED_MAXK; ++i) {
+        if (i < ck && cand_better(x, xo, bs[i], bo[i])) {
+          const double ts = bs[i];
+          const int32_t to = bo[i];
+          bs[i] = x;
+          bo[i] = xo;
+          x = ts;
+          xo = to;
+        }
+      }
+    }
+  }
+  if (ck > 0) {
+    __shared__ double s_bs[RED_THREADS / 32][RED_MAXK];
+    __shared__ int32_t s_bo[RED_THREADS / 32][RED_MAXK];
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      double os[RED_MAXK], ms[RED_MAXK];
+      int32_t oo[RED_MAXK], mo[RED_MAXK];
+#pragma unroll
+      for (int i = 0; i < RED_MAXK; ++i) {
+        os[i] = __shfl_xor_sync(0xffffffffu, bs[i], off);
+        oo[i] = __shfl_xor_sync(0xffffffffu, bo[i], off);
+      }
+      int ia = 0, ib = 0;
+#pragma unroll
+      for (int i = 0; i < RED_MAXK; ++i) {
+        const double sa = bs[min(ia, RED_MAXK - 1)], sb = os[min(ib, RED_MAXK - 1)];
+        const int32_t oa = bo[min(ia, RED_MAXK - 1)], ob = oo[min(ib, RED_MAXK - 1)];
+        if (cand_better(sa, oa, sb, ob) || (sa == sb && oa == ob)) {
+          ms[i] = sa;
+          mo[i] = oa;
+          ++ia;
+        } else {
+          ms[i] = sb;
+          mo[i] = ob;
+          ++ib;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < RED_MAXK; ++i) {
+        bs[i] = ms[i];
+        bo[i] = mo[i];
+      }
+    }
+    const int warp = tid >> 5, lane = tid & 31;
+    if (lane == 0)
+      for (int i = 0; i < RED_MAXK; ++i) {
+        s_bs[warp][i] = bs[i];
+        s_bo[warp][i] = bo[i];
+      }
+    __syncthreads();
+    if (tid == 0) {
+      double fs[RED_MAXK];
+      int32_t fo[RED_MAXK];
+      for (int i = 0; i < RED_MAXK; ++i) {
+        fs[i] = -INFINITY;
+        fo[i] = -1;
+      }
+      for (int w = 0; w < RED_THREADS / 32; ++w)
+        for (int j = 0; j < ck; ++j) {
+          double x = s_bs[w][j];
+          int32_t xo = s_bo[w][j];
+          for (int i = 0; i < ck; ++i)
+            if (cand_better(x, xo, fs[i], fo[i])) {
+              const double ts = fs[i];
+              const int32_t to = fo[i];
+              fs[i] = x;
+              fo[i] = xo;
+              x = ts;
+              xo = to;
+            }
+        }
+      const int64_t at = (static_cast<int64_t>(b) * a.n_ranges + rg) * ck;
+      for (int i = 0; i < ck; ++i) {
+        a.cand_s[at + i] = fo[i] >= 0 ? fs[i] : 0.0;
+        a.cand_i[at + i] = fo[i];
+      }
+    }
   }
 }
 
@@ -443,10 +544,25 @@ extern "C" int gift_fif_score(const gift_fif_view* f, const float* Q, int32_t B,
                            nullptr, nullptr);
 }
 
+extern "C" int gift_fif_score_ranges(const gift_fif_view* f, int32_t V) {
+  return static_cast<int>(cdiv(max64(f->n_local, 1), reduce_rs(V, f->n_local)));
+}
+
 extern "C" int gift_fif_score_ex(const gift_fif_view* f, const float* Q, int32_t B, int32_t V,
                                  const int32_t* vq, int32_t ma, int32_t mode, double sigma,
                                  double* out_scores, void* ws, size_t ws_bytes, void* stream,
                                  void* ev_scan_begin, void* ev_scan_end) {
+  return gift_fif_score_ex2(f, Q, B, V, vq, ma, mode, sigma, out_scores, ws, ws_bytes, stream,
+                            ev_scan_begin, ev_scan_end, 0, nullptr, nullptr);
+}
+
+extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_t B, int32_t V,
+                                  const int32_t* vq, int32_t ma, int32_t mode, double sigma,
+                                  double* out_scores, void* ws, size_t ws_bytes, void* stream,
+                                  void* ev_scan_begin, void* ev_scan_end, int32_t cand_k,
+                                  double* cand_s, int32_t* cand_i) {
+  GIFT_REQUIRE(cand_k >= 0 && cand_k <= RED_MAXK, GIFT_ERR_UNSUPPORTED,
+               "cand_k = %d > %d", cand_k, RED_MAXK);
   cudaStream_t st = as_stream(stream);
   GIFT_REQUIRE(f != nullptr, GIFT_ERR_INVALID, "null index");
   GIFT_REQUIRE(ma >= 1 && ma <= f->K, GIFT_ERR_INVALID, "ma must be in [1, %d]", f->K);
@@ -567,6 +683,9 @@ extern "C" int gift_fif_score_ex(const gift_fif_view* f, const float* Q, int32_t
   ra.n_local = f->n_local;
   ra.ord_base = f->ord_base;
   ra.scores = out_scores;
+  ra.cand_k = cand_s != nullptr ? cand_k : 0;
+  ra.cand_s = cand_s;
+  ra.cand_i = cand_i;
   const int red_smem = V * rs * 4;
   GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      red_smem));

@@ -485,12 +485,42 @@ __global__ void __launch_bounds__(QW_WARPS * 32)
     for (int z = 1; z < ksplit; ++z) dot += approx[static_cast<int64_t>(z) * n * K + v * K + c];
     return static_cast<float>(cn2[c]) - 2.0f * dot;
   };
-  // pass 1: ma-th smallest
+  // pass 1: ma-th smallest.  For K <= 512 the row stays in registers (all
+  // loads issued up front); larger codebooks re-read it in pass 2.
+  constexpr int QW_REG = 16;
+  const bool in_regs = K <= 32 * QW_REG;
+  float av[QW_REG];
+  if (in_regs) {
+#pragma unroll
+    for (int i = 0; i < QW_REG; ++i) {
+      const int c = lane + 32 * i;
+      av[i] = c < K ? approx[v * K + c] : 0.f;
+    }
+    for (int z = 1; z < ksplit; ++z) {
+#pragma unroll
+      for (int i = 0; i < QW_REG; ++i) {
+        const int c = lane + 32 * i;
+        if (c < K) av[i] += approx[static_cast<int64_t>(z) * n * K + v * K + c];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < QW_REG; ++i) {
+      const int c = lane + 32 * i;
+      av[i] = c < K ? static_cast<float>(cn2[c]) - 2.0f * av[i] : INFINITY;
+    }
+  }
   float loc[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) loc[i] = INFINITY;
-  for (int c = lane; c < K; c += 32) {
-    float x = approx_at(c);
+  for (int c = lane, ii = 0; c < K; c += 32, ++ii) {
+    float x = INFINITY;
+    if (in_regs) {
+#pragma unroll
+      for (int i = 0; i < QW_REG; ++i)
+        if (i == ii) x = av[i];
+    } else {
+      x = approx_at(c);
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       if (i < ma && x < loc[i]) {
@@ -532,9 +562,17 @@ __global__ void __launch_bounds__(QW_WARPS * 32)
   // pass 2: candidates under the threshold
   int cnt = 0;
   const unsigned lt = (1u << lane) - 1u;
-  for (int c0 = 0; c0 < K; c0 += 32) {
+  for (int c0 = 0, ii = 0; c0 < K; c0 += 32, ++ii) {
     const int c = c0 + lane;
-    const bool hit = c < K && static_cast<double>(approx_at(c)) <= thresh;
+    float x = INFINITY;
+    if (in_regs) {
+#pragma unroll
+      for (int i = 0; i < QW_REG; ++i)
+        if (i == ii) x = av[i];
+    } else if (c < K) {
+      x = approx_at(c);
+    }
+    const bool hit = c < K && static_cast<double>(x) <= thresh;
     const unsigned bal = __ballot_sync(0xffffffffu, hit);
     const int pos = cnt + __popc(bal & lt);
     if (hit && pos < QW_MAXC) s_ci[warp][pos] = c;

@@ -136,8 +136,8 @@ __global__ void __launch_bounds__(TK_THREADS) topk_kernel(const TopkIn in, const
         } else {
           const int64_t at = static_cast<int64_t>(b) * in.m + e;
           sc = in.cs[at];
-          tb = in.ct[at];
           jj = in.ci[at];
+          tb = in.ct ? in.ct[at] : static_cast<uint32_t>(jj);
         }
         if (jj >= 0 && key_better(sc, tb, ths, tht)) {
           int pos = atomicAdd(&s_cnt, 1);
@@ -296,4 +296,30 @@ extern "C" int gift_topk_rows(const double* scores, int32_t B, int64_t n, int32_
                               void* stream) {
   return gift_topk_rows_ex(scores, B, n, k, idrank, self_local, ord_base, positive_only, out_idx,
                            out_val, nullptr, 0, stream);
+}
+
+extern "C" int gift_topk_cand(const double* cs, const int32_t* ci, int32_t B, int64_t m, int32_t k,
+                              int32_t positive_only, int32_t* out_idx, double* out_val,
+                              void* stream) {
+  cudaStream_t st = as_stream(stream);
+  GIFT_REQUIRE(k >= 1 && k <= 256, GIFT_ERR_UNSUPPORTED, "k = %d outside [1, 256]", k);
+  if (B <= 0) return GIFT_OK;
+  const int smem = sizeof(TopkSmem<256>);
+  GIFT_CUDA_TRY(cudaFuncSetAttribute(topk_kernel<256, false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  TopkIn in{};
+  in.cs = cs;
+  in.ct = nullptr;
+  in.ci = ci;
+  in.m = m;
+  TopkOut out{};
+  out.k = k;
+  out.positive_only = positive_only;
+  out.final_out = 1;
+  out.nslices = 1;
+  out.out_idx = out_idx;
+  out.out_val = out_val;
+  topk_kernel<256, false><<<dim3(1, B), TK_THREADS, smem, st>>>(in, out);
+  GIFT_LAUNCH_CHECK();
+  return GIFT_OK;
 }

@@ -33,8 +33,9 @@ _DTYPE_CODE = {torch.float32: nat.GIFT_F32, torch.float16: nat.GIFT_F16,
 # libgift kernel launches of one QueryEngine.run batch (single channel, rerank):
 # view_prep, quantize approx + select, probe count, plan, scatter, compact zero,
 # query-plane gather, tcgen05 scan, probe ranges, reduce (gift_fif_score) +
-# top-k2 (slices + merge), act_mean, sif_query, top-k (slices + merge).
-LAUNCHES_PER_BATCH = 17
+# top-k2 merge of the reduce's per-range candidates, act_mean, sif_query,
+# top-k (slices + merge).
+LAUNCHES_PER_BATCH = 16
 
 
 def _bits(n: int) -> int:
@@ -293,8 +294,10 @@ class ScoreRunner:
 
     def score(self, fif: DeviceFif, Q: torch.Tensor, ma: int, mode: int = nat.SIM_COSINE,
               sigma: float = 0.5, vq: torch.Tensor | None = None, out: torch.Tensor | None = None,
-              stream=None, scan_events=None) -> torch.Tensor:
-        """Q: [B, V, d] f32 device -> f64 [B, n_local] (matching.py:136-161)."""
+              stream=None, scan_events=None, cand_k: int = 0):
+        """Q: [B, V, d] f32 device -> f64 [B, n_local] (matching.py:136-161).
+        With cand_k > 0 also returns the reduce's per-range best cand_k
+        (scores [B, m], ordinals [B, m]) for `topk_candidates`."""
         if Q.dim() != 3:
             raise ValueError("queries must be [B, V, d]")
         B, V, d = Q.shape
@@ -317,24 +320,41 @@ class ScoreRunner:
         checked = bound > self.MAX_BOUND
         if not checked:
             self.capacity = max(self.capacity, bound)
+        cs = ci = None
+        if cand_k > 0:
+            nr = lib.gift_fif_score_ranges(ctypes.byref(view), V)
+            cs = torch.empty((B, nr * cand_k), dtype=torch.float64, device=Q.device)
+            ci = torch.empty((B, nr * cand_k), dtype=torch.int32, device=Q.device)
         for _attempt in range(8):
             wsb = lib.gift_fif_score_ws_bytes(ctypes.byref(view), B, V, ma, self.capacity)
             ws = self.ws.get(wsb)
             ev0, ev1 = scan_events if scan_events is not None else (None, None)
-            nat.check(lib.gift_fif_score_ex(ctypes.byref(view), nat.ptr(Q), B, V, nat.ptr(vq), ma,
-                                            mode, float(sigma), nat.ptr(out), nat.ptr(ws),
-                                            ws.numel(), _sp(stream),
-                                            None if ev0 is None else ev0.cuda_event,
-                                            None if ev1 is None else ev1.cuda_event),
+            nat.check(lib.gift_fif_score_ex2(ctypes.byref(view), nat.ptr(Q), B, V, nat.ptr(vq), ma,
+                                             mode, float(sigma), nat.ptr(out), nat.ptr(ws),
+                                             ws.numel(), _sp(stream),
+                                             None if ev0 is None else ev0.cuda_event,
+                                             None if ev1 is None else ev1.cuda_event,
+                                             int(cand_k), nat.ptr(cs), nat.ptr(ci)),
                       "gift_fif_score")
             if not checked:
-                return out
+                return (out, cs, ci) if cand_k > 0 else out
             meta = ws[:64].view(torch.int64)
             status = meta[:3].cpu()
             if int(status[2]) == 0:
-                return out
+                return (out, cs, ci) if cand_k > 0 else out
             self.capacity = int(int(status[1]) * 1.25) + 1024
         raise RuntimeError("F-IF compact buffer kept overflowing")
+
+
+def topk_candidates(cs: torch.Tensor, ci: torch.Tensor, k: int, positive_only: bool = True,
+                    stream=None):
+    """K4 merge: best k of per-row candidate lists by (score desc, ordinal asc)."""
+    B, m = cs.shape
+    idx = torch.empty((B, k), dtype=torch.int32, device=cs.device)
+    val = torch.empty((B, k), dtype=torch.float64, device=cs.device)
+    nat.call("gift_topk_cand", nat.ptr(cs), nat.ptr(ci), B, m, k, int(positive_only), nat.ptr(idx),
+             nat.ptr(val), _sp(stream))
+    return idx, val
 
 
 def topk_rows(scores: torch.Tensor, k: int, *, idrank: torch.Tensor | None = None,

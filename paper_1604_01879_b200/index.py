@@ -175,6 +175,18 @@ class QueryEngine:
     def run(self, Qa, Qb=None, top_k=10, rerank=True, self_local=None, vq=None, vqb=None,
             stream=None, scan_events=None):
         """Device batch -> (idx [B, k] i32 global ordinals, val [B, k] f64)."""
+        if rerank and Qb is None and self.dup and self.raw_dup:
+            # single-channel fast path: the reduce emits per-range top-k2
+            # candidates, merged into the neighbour lists (rerank.py:78-87)
+            k2 = min(self.cfg.k2, self.n)
+            sa, cs, ci = self.runner.score(self.fa, Qa, self.cfg.ma, self.mode, self.cfg.sigma,
+                                           vq=vq, stream=stream, scan_events=scan_events,
+                                           cand_k=k2)
+            nbr, _ = eg.topk_candidates(cs, ci, k2, positive_only=True, stream=stream)
+            fa = eg.act_mean(self.raw_a, nbr, stream=stream)
+            final = self.sif.query(fa, stream=stream)
+            k = min(top_k, self.n)
+            return eg.topk_rows(final, k, idrank=self.idrank, self_local=self_local, stream=stream)
         sa, sb = self.scores(Qa, Qb, vq, vqb, stream, scan_events)
         if rerank:
             final = self.rerank(sa, sb, stream)
