@@ -301,6 +301,75 @@ def run_c5(args):
         print(json.dumps(line), flush=True)
 
 
+def run_sharded(args, w):
+    """Database sharded by shape over the ranks (dist.py): every rank holds
+    N / G shapes (all cells), queries are replicated, per-shard top-k2 and
+    top-k candidates are merged with NCCL all_gather_into_tensor."""
+    from paper_1604_01879_b200 import engine as eg2
+    from paper_1604_01879_b200.dist import ShardedEngine, build_sharded, shard_bounds
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=device)
+    else:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    if w.storage == "float16":
+        db, qs, Ct = synth.zipf_mixture(w, SEED, device)
+        C = Ct.cpu().numpy()
+    else:
+        db, qs, _ = synth.mixture(w, SEED, device)
+        C = synth.sample_centroids(db, w.K, SEED + 1).cpu().numpy()
+    lo, hi = shard_bounds(w.n_shapes, ws, rank)
+    X = db[lo:hi].contiguous()
+    del db
+    torch.cuda.empty_cache()
+    cfg = IndexConfig(n_views=w.n_views, codebook_size=w.K, ma=w.ma, k1=w.k1, k2=w.k2,
+                      similarity="gaussian", sigma=w.sigma, storage_dtype=w.storage,
+                      batch_size=w.batch, imported=True)
+    t0 = time.perf_counter()
+    fif, raw, sif = build_sharded(X, eg2.DeviceCodebook.from_numpy(C), cfg, w.n_shapes)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    del X
+    idrank = torch.arange(w.n_shapes, dtype=torch.int32, device=device)  # zero-padded ids
+    eng = ShardedEngine(fif, raw, sif, idrank, cfg, w.n_shapes)
+    B = w.batch
+    nb = max(1, qs.shape[0] // B)
+    batches = [qs[j * B:(j + 1) * B].contiguous() for j in range(nb)]
+    for i in range(args.warmup):
+        eng.run(batches[i % nb], w.top_k)
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    with ClockSampler(local) as clk:
+        dist.barrier()
+        torch.cuda.synchronize()
+        ev[0].record()
+        for i in range(args.steps):
+            eng.run(batches[(args.warmup + i) % nb], w.top_k)
+        ev[1].record()
+        torch.cuda.synchronize()
+        dist.barrier()
+    t = torch.tensor([ev[0].elapsed_time(ev[1])], dtype=torch.float64, device=device)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    if rank == 0:
+        line = {"metric": METRIC, "value": B * args.steps / (ms / 1000.0), "unit": UNIT,
+                "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": w.name, "n_shapes": w.n_shapes, "parallelism":
+                           f"shard{ws}", "batch": B, "top_k": w.top_k, "build_s": build_s},
+                "e2e": None, "gpu_launches": None, "roofline": None, "cpu_baseline": None,
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def run_gift(args, w):
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -416,6 +485,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(synth.WORKLOADS) + ["c5"])
     ap.add_argument("--c5-shapes", type=int, default=0, help="override config-5 N (smoke runs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", action="store_true",
+                    help="shard the database by shape over the ranks (configs 3/4)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "gift" else args.warmup
     if args.config == "c5":
@@ -428,6 +499,8 @@ def main():
     w = synth.WORKLOADS[args.config]
     if args.impl == "reference":
         run_reference(args, w)
+    elif args.shard:
+        run_sharded(args, w)
     else:
         run_gift(args, w)
 

@@ -290,9 +290,18 @@ struct ReduceArgs {
 
 constexpr int RED_MAXK = 8;
 
+struct Cand {
+  double s;
+  int32_t o;  // global ordinal, -1 = none (sorts last)
+};
 __device__ __forceinline__ bool cand_better(double s1, int32_t o1, double s2, int32_t o2) {
   return s1 > s2 || (s1 == s2 && static_cast<uint32_t>(o1) < static_cast<uint32_t>(o2));
 }
+struct CandBetter {
+  __device__ bool operator()(const Cand& x, const Cand& y) const {
+    return cand_better(x.s, x.o, y.s, y.o);
+  }
+};
 
 // Per (query, shape range of rs shapes): every (view, slot) probe's
 // per-segment maxima are max-ed into vb[view][shape] (shared, atomicMax on
@@ -360,99 +369,66 @@ __global__ void __launch_bounds__(RED_THREADS) fif_reduce_kernel(ReduceArgs a) {
   __syncthreads();
   const double denom = static_cast<double>(a.vq ? a.vq[b] : V);
   const int ck = a.cand_k;
-  double bs[RED_MAXK];
-  int32_t bo[RED_MAXK];
+  Cand best[RED_MAXK];
 #pragma unroll
-  for (int i = 0; i < RED_MAXK; ++i) {
-    bs[i] = -INFINITY;
-    bo[i] = -1;
-  }
+  for (int i = 0; i < RED_MAXK; ++i) best[i] = Cand{-INFINITY, -1};
   for (int o = tid; o < n; o += RED_THREADS) {
     double acc = 0.0;
     for (int v = 0; v < V; ++v) acc += static_cast<double>(vb[v * rs + o]);
     const double sc = acc / denom;
     a.scores[static_cast<int64_t>(b) * a.n_local + lo + o] = sc;
     if (ck > 0) {  // per-thread sorted best list (ordinals ascend within a thread)
-      double x = sc;
-      int32_t xo = static_cast<int32_t>(glo + o);
+      Cand x{sc, static_cast<int32_t>(glo + o)};
 #pragma unroll
       for (int i = 0; i < RED_MAXK; ++i) {
-        if (i < ck && cand_better(x, xo, bs[i], bo[i])) {
-          const double ts = bs[i];
-          const int32_t to = bo[i];
-          bs[i] = x;
-          bo[i] = xo;
-          x = ts;
-          xo = to;
+        if (cand_better(x.s, x.o, best[i].s, best[i].o)) {
+          const Cand t = best[i];
+          best[i] = x;
+          x = t;
         }
       }
     }
   }
   if (ck > 0) {
-    __shared__ double s_bs[RED_THREADS / 32][RED_MAXK];
-    __shared__ int32_t s_bo[RED_THREADS / 32][RED_MAXK];
+    __shared__ Cand s_best[RED_THREADS / 32][RED_MAXK];
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-      double os[RED_MAXK], ms[RED_MAXK];
-      int32_t oo[RED_MAXK], mo[RED_MAXK];
+      Cand other[RED_MAXK];
 #pragma unroll
       for (int i = 0; i < RED_MAXK; ++i) {
-        os[i] = __shfl_xor_sync(0xffffffffu, bs[i], off);
-        oo[i] = __shfl_xor_sync(0xffffffffu, bo[i], off);
+        other[i].s = __shfl_xor_sync(0xffffffffu, best[i].s, off);
+        other[i].o = __shfl_xor_sync(0xffffffffu, best[i].o, off);
       }
-      int ia = 0, ib = 0;
-#pragma unroll
-      for (int i = 0; i < RED_MAXK; ++i) {
-        const double sa = bs[min(ia, RED_MAXK - 1)], sb = os[min(ib, RED_MAXK - 1)];
-        const int32_t oa = bo[min(ia, RED_MAXK - 1)], ob = oo[min(ib, RED_MAXK - 1)];
-        if (cand_better(sa, oa, sb, ob) || (sa == sb && oa == ob)) {
-          ms[i] = sa;
-          mo[i] = oa;
-          ++ia;
-        } else {
-          ms[i] = sb;
-          mo[i] = ob;
-          ++ib;
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < RED_MAXK; ++i) {
-        bs[i] = ms[i];
-        bo[i] = mo[i];
-      }
+      merge8(best, other, CandBetter());
     }
     const int warp = tid >> 5, lane = tid & 31;
     if (lane == 0)
-      for (int i = 0; i < RED_MAXK; ++i) {
-        s_bs[warp][i] = bs[i];
-        s_bo[warp][i] = bo[i];
-      }
+#pragma unroll
+      for (int i = 0; i < RED_MAXK; ++i) s_best[warp][i] = best[i];
     __syncthreads();
-    if (tid == 0) {
-      double fs[RED_MAXK];
-      int32_t fo[RED_MAXK];
-      for (int i = 0; i < RED_MAXK; ++i) {
-        fs[i] = -INFINITY;
-        fo[i] = -1;
-      }
-      for (int w = 0; w < RED_THREADS / 32; ++w)
-        for (int j = 0; j < ck; ++j) {
-          double x = s_bs[w][j];
-          int32_t xo = s_bo[w][j];
-          for (int i = 0; i < ck; ++i)
-            if (cand_better(x, xo, fs[i], fo[i])) {
-              const double ts = fs[i];
-              const int32_t to = fo[i];
-              fs[i] = x;
-              fo[i] = xo;
-              x = ts;
-              xo = to;
-            }
+    if (tid < 32) {
+      Cand mine[RED_MAXK];
+#pragma unroll
+      for (int i = 0; i < RED_MAXK; ++i)
+        mine[i] = tid < RED_THREADS / 32 ? s_best[tid][i] : Cand{-INFINITY, -1};
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        Cand other[RED_MAXK];
+#pragma unroll
+        for (int i = 0; i < RED_MAXK; ++i) {
+          other[i].s = __shfl_xor_sync(0xffffffffu, mine[i].s, off);
+          other[i].o = __shfl_xor_sync(0xffffffffu, mine[i].o, off);
         }
+        merge8(mine, other, CandBetter());
+      }
+      if (tid == 0) {
       const int64_t at = (static_cast<int64_t>(b) * a.n_ranges + rg) * ck;
-      for (int i = 0; i < ck; ++i) {
-        a.cand_s[at + i] = fo[i] >= 0 ? fs[i] : 0.0;
-        a.cand_i[at + i] = fo[i];
+#pragma unroll
+      for (int i = 0; i < RED_MAXK; ++i)
+        if (i < ck) {
+          a.cand_s[at + i] = mine[i].o >= 0 ? mine[i].s : 0.0;
+          a.cand_i[at + i] = mine[i].o;
+        }
       }
     }
   }

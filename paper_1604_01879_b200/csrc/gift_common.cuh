@@ -100,6 +100,32 @@ __device__ __forceinline__ bool key_better(double s1, uint32_t t1, double s2, ui
   return s1 > s2 || (s1 == s2 && t1 < t2);
 }
 
+// Top-8 of the union of two sorted lists, static indices only (no local
+// memory): c[i] = better(a[i], b[7-i]) is bitonic; three half-cleaner stages
+// sort it.  `Better(x, y)` is a strict weak order ("x ranks before y").
+template <typename T, typename Better>
+__device__ __forceinline__ void merge8(T (&a)[8], const T (&b)[8], Better better) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const T y = b[7 - i];
+    if (better(y, a[i])) a[i] = y;
+  }
+#pragma unroll
+  for (int stride = 4; stride > 0; stride >>= 1) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if ((i & stride) == 0) {
+        const int j = i + stride;
+        if (better(a[j], a[i])) {
+          const T t = a[i];
+          a[i] = a[j];
+          a[j] = t;
+        }
+      }
+    }
+  }
+}
+
 // Block-wide exclusive scan of one value per thread (blockDim.x <= 1024,
 // multiple of 32).  Returns the exclusive prefix; *total receives the sum.
 template <typename T>

@@ -274,21 +274,7 @@ __global__ void __launch_bounds__(QS_THREADS)
       float oth[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) oth[i] = __shfl_xor_sync(0xffffffffu, loc[i], o);
-      float mrg[8];
-      int ia = 0, ib = 0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float va = loc[min(ia, 7)], vb = oth[min(ib, 7)];
-        if (va <= vb) {
-          mrg[i] = va;
-          ++ia;
-        } else {
-          mrg[i] = vb;
-          ++ib;
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) loc[i] = mrg[i];
+      merge8(loc, oth, [](float x, float y) { return x < y; });
     }
     if (lane == 0)
       for (int i = 0; i < 8; ++i) s_small[warp][i] = loc[i];
@@ -532,23 +518,10 @@ __global__ void __launch_bounds__(QW_WARPS * 32)
   }
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    float oth[8], mrg[8];
+    float oth[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) oth[i] = __shfl_xor_sync(0xffffffffu, loc[i], o);
-    int ia = 0, ib = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const float va = loc[min(ia, 7)], vb = oth[min(ib, 7)];
-      if (va <= vb) {
-        mrg[i] = va;
-        ++ia;
-      } else {
-        mrg[i] = vb;
-        ++ib;
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) loc[i] = mrg[i];
+    merge8(loc, oth, [](float x, float y) { return x < y; });
   }
   float kth = loc[0];
 #pragma unroll
