@@ -126,6 +126,22 @@ int gift_fif_gather(const void* src, int32_t dtype, int32_t d, int32_t V,
                     const uint32_t* perm, int64_t P, int64_t ord_base,
                     void* out_feat, int32_t* out_ord, float* out_pnorm2,
                     void* stream);
+/* Streamed build (database larger than what fits twice in HBM; the
+ * reference's build_fif, matching.py:106-133, over chunks of shapes):
+ * pass 1 quantizes chunk by chunk into one key per view and radix-sorts them
+ * (perm = cell-major view order); gift_perm_invert gives every view its
+ * posting (pos[view] = p, -1 for zero views); pass 2 calls gift_fif_scatter
+ * per chunk: rows of the chunk's views (global views view_base..) land at
+ * their postings in out_feat (storage dtype, may be NULL) and/or the
+ * tensor-core planes out_hi/out_lo (fp16, x = hi + 2^-11 lo; f16 storage
+ * needs only out_hi), with out_ord / out_pnorm2 exactly as gift_fif_gather. */
+int gift_perm_invert(const uint32_t* perm, int64_t P, int64_t n_total,
+                     int32_t* pos, void* stream);
+int gift_fif_scatter(const void* src, int32_t dtype, int32_t d, int32_t V,
+                     int64_t n_views, const int32_t* pos, int64_t view_base,
+                     int64_t ord_base, void* out_feat, void* out_hi,
+                     void* out_lo, int32_t* out_ord, float* out_pnorm2,
+                     void* stream);
 /* Segments = maximal runs of one shape inside one cell.  Two passes: with
  * seg_ord == NULL only seg_off[K+1] is written (read seg_off[K] = S), then
  * call again with seg_ord/seg_pstart allocated ([S], [S+1]). */
@@ -150,6 +166,11 @@ int gift_split_planes(const float* x, int64_t n, void* h1, void* h2,
 int gift_gather_rows_f32(const void* src, int32_t dtype, int32_t d,
                          const int64_t* idx, int64_t n, float* out,
                          void* stream);
+/* Same from the tensor-core planes of an index that keeps no storage copy
+ * (streamed config-3 build): out = hi + 2^-11 lo (22 significant bits). */
+int gift_gather_rows_planes(const void* hi, const void* lo, int32_t d,
+                            const int64_t* idx, int64_t n, float* out,
+                            void* stream);
 
 /* ---- K3 F-IF score: replaces matching.query_fif (matching.py:136-161) ----
  * Batched: Q is [B*V, d] f32 (B queries of V views).  Writes dense f64

@@ -12,6 +12,7 @@ from .index import (
     build_index,
     build_index_from_lists,
     build_index_from_views,
+    build_index_streamed,
     load_bundle,
     query,
     query_batch,
@@ -27,6 +28,7 @@ __all__ = [
     "build_index",
     "build_index_from_lists",
     "build_index_from_views",
+    "build_index_streamed",
     "load_bundle",
     "query",
     "query_batch",

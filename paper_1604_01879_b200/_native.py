@@ -56,6 +56,9 @@ _SIGS = {
     "gift_offsets_from_sorted": (_c_i32, [_c_p, _c_i64, _c_i64, _c_p, _c_p]),
     "gift_fif_gather": (_c_i32, [_c_p, _c_i32, _c_i32, _c_i32, _c_p, _c_i64, _c_i64, _c_p, _c_p,
                                  _c_p, _c_p]),
+    "gift_perm_invert": (_c_i32, [_c_p, _c_i64, _c_i64, _c_p, _c_p]),
+    "gift_fif_scatter": (_c_i32, [_c_p, _c_i32, _c_i32, _c_i32, _c_i64, _c_p, _c_i64, _c_i64, _c_p,
+                                  _c_p, _c_p, _c_p, _c_p, _c_p]),
     "gift_fif_build_ws_bytes": (_c_sz, [_c_i64, _c_i32]),
     "gift_fif_segments": (_c_i32, [_c_p, _c_p, _c_i32, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_sz,
                                    _c_p]),
@@ -63,6 +66,7 @@ _SIGS = {
                                 _c_p, _c_sz, _c_p]),
     "gift_split_planes": (_c_i32, [_c_p, _c_i64, _c_p, _c_p, _c_p]),
     "gift_gather_rows_f32": (_c_i32, [_c_p, _c_i32, _c_i32, _c_p, _c_i64, _c_p, _c_p]),
+    "gift_gather_rows_planes": (_c_i32, [_c_p, _c_p, _c_i32, _c_p, _c_i64, _c_p, _c_p]),
     "gift_fif_score_ws_bytes": (_c_sz, [ctypes.POINTER(FifView), _c_i32, _c_i32, _c_i32, _c_i64]),
     "gift_fif_score": (_c_i32, [ctypes.POINTER(FifView), _c_p, _c_i32, _c_i32, _c_p, _c_i32,
                                 _c_i32, _c_dbl, _c_p, _c_p, _c_sz, _c_p]),

@@ -10,25 +10,33 @@
 
 namespace gift {
 
+// One feature row: copy to the cell-major position (f32/f16 storage and/or
+// the tensor-core planes) and return its |x|^2 partial (f64 accumulate).
+// Shared by the in-HBM gather and the chunked (streamed) scatter so both
+// builds produce bit-identical rows and |p|^2.
 template <typename T>
-__global__ void fif_gather_kernel(const T* __restrict__ src, int d, int V,
-                                  const uint32_t* __restrict__ perm, int64_t P, int64_t ord_base,
-                                  T* __restrict__ out, int32_t* __restrict__ out_ord,
-                                  float* __restrict__ out_pn2, bool vec) {
-  const int64_t p = blockIdx.x;
-  if (p >= P) return;
-  const int64_t s = perm[p];
-  const T* in = src + s * d;
-  T* o = out + p * d;
+__device__ __forceinline__ double row_emit(const T* __restrict__ in, int d, bool vec,
+                                           T* __restrict__ o, __half* __restrict__ hi,
+                                           __half* __restrict__ lo) {
   double acc = 0.0;
   constexpr int W = 16 / sizeof(T);
   if (vec) {
     const uint4* in4 = reinterpret_cast<const uint4*>(in);
-    uint4* o4 = reinterpret_cast<uint4*>(o);
     for (int k = threadIdx.x; k < d / W; k += blockDim.x) {
       uint4 v = in4[k];
-      o4[k] = v;
+      if (o) reinterpret_cast<uint4*>(o)[k] = v;
       const T* e = reinterpret_cast<const T*>(&v);
+      if (hi) {
+        if constexpr (sizeof(T) == 4) {
+          __half h[W], l[W];
+#pragma unroll
+          for (int q = 0; q < W; ++q) split2(static_cast<float>(e[q]), h[q], l[q]);
+          reinterpret_cast<uint2*>(hi)[k] = *reinterpret_cast<const uint2*>(h);
+          if (lo) reinterpret_cast<uint2*>(lo)[k] = *reinterpret_cast<const uint2*>(l);
+        } else {
+          reinterpret_cast<uint4*>(hi)[k] = v;
+        }
+      }
 #pragma unroll
       for (int q = 0; q < W; ++q) {
         double x = static_cast<double>(static_cast<float>(e[q]));
@@ -38,21 +46,72 @@ __global__ void fif_gather_kernel(const T* __restrict__ src, int d, int V,
   } else {
     for (int k = threadIdx.x; k < d; k += blockDim.x) {
       T v = in[k];
-      o[k] = v;
-      double x = static_cast<double>(static_cast<float>(v));
+      if (o) o[k] = v;
+      const float f = static_cast<float>(v);
+      if (hi) {
+        __half h, l;
+        split2(f, h, l);
+        hi[k] = sizeof(T) == 4 ? h : __float2half_rn(f);
+        if (lo) lo[k] = l;
+      }
+      double x = static_cast<double>(f);
       acc += x * x;
     }
   }
+  return acc;
+}
+
+__device__ __forceinline__ float block_sum_f64_to_f32(double acc) {
   __shared__ double red[32];
   for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += red[w];
+  return static_cast<float>(t);
+}
+
+template <typename T>
+__global__ void fif_gather_kernel(const T* __restrict__ src, int d, int V,
+                                  const uint32_t* __restrict__ perm, int64_t P, int64_t ord_base,
+                                  T* __restrict__ out, int32_t* __restrict__ out_ord,
+                                  float* __restrict__ out_pn2, bool vec) {
+  const int64_t p = blockIdx.x;
+  if (p >= P) return;
+  const int64_t s = perm[p];
+  double acc = row_emit<T>(src + s * d, d, vec, out + p * d, nullptr, nullptr);
+  float t = block_sum_f64_to_f32(acc);
   if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += red[w];
-    out_pn2[p] = static_cast<float>(t);
+    out_pn2[p] = t;
     out_ord[p] = static_cast<int32_t>(ord_base + s / V);
   }
+}
+
+// Streamed build, pass 2: the chunk's view v (global view view_base + v) goes
+// to posting pos[v] (< 0: zero view, not stored).
+template <typename T>
+__global__ void fif_scatter_kernel(const T* __restrict__ src, int d, int V, int64_t nv,
+                                   const int32_t* __restrict__ pos, int64_t view_base,
+                                   int64_t ord_base, T* __restrict__ out, __half* __restrict__ hi,
+                                   __half* __restrict__ lo, int32_t* __restrict__ out_ord,
+                                   float* __restrict__ out_pn2, bool vec) {
+  const int64_t v = blockIdx.x;
+  if (v >= nv) return;
+  const int64_t p = pos[view_base + v];
+  if (p < 0) return;
+  double acc = row_emit<T>(src + v * d, d, vec, out ? out + p * d : nullptr,
+                           hi ? hi + p * d : nullptr, lo ? lo + p * d : nullptr);
+  float t = block_sum_f64_to_f32(acc);
+  if (threadIdx.x == 0) {
+    out_pn2[p] = t;
+    out_ord[p] = static_cast<int32_t>(ord_base + (view_base + v) / V);
+  }
+}
+
+__global__ void perm_invert_kernel(const uint32_t* __restrict__ perm, int64_t P,
+                                   int32_t* __restrict__ pos) {
+  int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p < P) pos[perm[p]] = static_cast<int32_t>(p);
 }
 
 __device__ __forceinline__ int cell_of(const int64_t* __restrict__ cell_off, int K, int64_t p) {
@@ -167,6 +226,51 @@ extern "C" int gift_fif_gather(const void* src, int32_t dtype, int32_t d, int32_
     fif_gather_kernel<__half><<<static_cast<unsigned>(P), threads, 0, st>>>(
         static_cast<const __half*>(src), d, V, perm, P, ord_base, static_cast<__half*>(out_feat),
         out_ord, out_pnorm2, vec);
+  }
+  GIFT_LAUNCH_CHECK();
+  return GIFT_OK;
+}
+
+extern "C" int gift_perm_invert(const uint32_t* perm, int64_t P, int64_t n_total, int32_t* pos,
+                                void* stream) {
+  cudaStream_t st = as_stream(stream);
+  GIFT_REQUIRE(P <= n_total && n_total < (int64_t(1) << 31), GIFT_ERR_INVALID,
+               "perm_invert: sizes out of range");
+  if (n_total > 0) GIFT_CUDA_TRY(cudaMemsetAsync(pos, 0xff, sizeof(int32_t) * n_total, st));
+  if (P > 0) {
+    perm_invert_kernel<<<static_cast<unsigned>(cdiv(P, 256)), 256, 0, st>>>(perm, P, pos);
+    GIFT_LAUNCH_CHECK();
+  }
+  return GIFT_OK;
+}
+
+extern "C" int gift_fif_scatter(const void* src, int32_t dtype, int32_t d, int32_t V,
+                                int64_t n_views, const int32_t* pos, int64_t view_base,
+                                int64_t ord_base, void* out_feat, void* out_hi, void* out_lo,
+                                int32_t* out_ord, float* out_pnorm2, void* stream) {
+  if (n_views <= 0) return GIFT_OK;
+  cudaStream_t st = as_stream(stream);
+  GIFT_REQUIRE(dtype == GIFT_F32 || dtype == GIFT_F16, GIFT_ERR_INVALID,
+               "feature storage must be f32 or f16");
+  GIFT_REQUIRE(out_feat != nullptr || out_hi != nullptr, GIFT_ERR_INVALID,
+               "fif_scatter: no feature destination");
+  GIFT_REQUIRE(dtype == GIFT_F16 || out_hi == nullptr || out_lo != nullptr, GIFT_ERR_INVALID,
+               "fif_scatter: f32 planes need both hi and lo");
+  const int threads = d >= 512 ? 256 : 128;
+  auto al = [](const void* p) { return p == nullptr || reinterpret_cast<uintptr_t>(p) % 16 == 0; };
+  if (dtype == GIFT_F32) {
+    bool vec = d % 4 == 0 && al(src) && al(out_feat) && al(out_hi) && al(out_lo) &&
+               (out_hi == nullptr || d % 4 == 0);
+    fif_scatter_kernel<float><<<static_cast<unsigned>(n_views), threads, 0, st>>>(
+        static_cast<const float*>(src), d, V, n_views, pos, view_base, ord_base,
+        static_cast<float*>(out_feat), static_cast<__half*>(out_hi), static_cast<__half*>(out_lo),
+        out_ord, out_pnorm2, vec);
+  } else {
+    bool vec = d % 8 == 0 && al(src) && al(out_feat) && al(out_hi);
+    fif_scatter_kernel<__half><<<static_cast<unsigned>(n_views), threads, 0, st>>>(
+        static_cast<const __half*>(src), d, V, n_views, pos, view_base, ord_base,
+        static_cast<__half*>(out_feat), static_cast<__half*>(out_hi), nullptr, out_ord, out_pnorm2,
+        vec);
   }
   GIFT_LAUNCH_CHECK();
   return GIFT_OK;

@@ -546,6 +546,8 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
   GIFT_REQUIRE(mode != GIFT_SIM_GAUSSIAN || sigma > 0, GIFT_ERR_INVALID, "sigma must be > 0");
   GIFT_REQUIRE(f->dtype == GIFT_F32 || f->dtype == GIFT_F16, GIFT_ERR_INVALID, "bad storage");
   GIFT_REQUIRE(f->n_postings < (int64_t(1) << 31), GIFT_ERR_UNSUPPORTED, "too many postings");
+  GIFT_REQUIRE(f->n_postings == 0 || f->feat != nullptr || use_tc(f), GIFT_ERR_UNSUPPORTED,
+               "index keeps no storage copy of its features: only the tcgen05 scan can run");
   if (B <= 0 || f->n_local <= 0) return GIFT_OK;
   GIFT_REQUIRE(V >= 1, GIFT_ERR_EMPTY, "view set is empty");
   const int64_t nviews = static_cast<int64_t>(B) * V;

@@ -43,7 +43,6 @@ constexpr int EPI_BYTES = TC_M * EPI_STRIDE * 4;
 constexpr int TC_THREADS = 192;
 constexpr uint32_t TMEM_COLS = 512;  // 2 buffers x (D1[128] | D2[128])
 constexpr int SMEM_TC = TC_STAGES * STAGE_BYTES + EPI_BYTES + 256;
-constexpr float SPLIT_SCALE = 2048.0f;        // 2^11
 constexpr float SPLIT_INV = 1.0f / 2048.0f;
 
 struct ItemInfo {
@@ -280,12 +279,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     tc::tc_fence_after();
     tc::tmem_dealloc<TMEM_COLS>(tmem_base);
   }
-}
-
-// x -> (h1, h2) fp16 planes, x = h1 + 2^-11 h2 (22 significant bits)
-__device__ __forceinline__ void split2(float x, __half& h1, __half& h2) {
-  h1 = __float2half_rn(x);
-  h2 = __float2half_rn((x - __half2float(h1)) * SPLIT_SCALE);
 }
 
 __global__ void split_planes_kernel(const float* __restrict__ x, int64_t n, __half* __restrict__ h1,

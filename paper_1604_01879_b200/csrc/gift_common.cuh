@@ -157,6 +157,17 @@ __device__ T block_exclusive_scan(T v, T* total, T* sbuf /* >= 32 */) {
   return warp_prefix + x - v;
 }
 
+
+// ------------------------------------------------------------------------
+// tensor-core operand planes: x -> (h1, h2) fp16, x = h1 + 2^-11 h2
+// (22 significant bits; the scan and quantize MMAs consume both planes)
+// ------------------------------------------------------------------------
+constexpr float SPLIT_SCALE = 2048.0f;  // 2^11
+__device__ __forceinline__ void split2(float x, __half& h1, __half& h2) {
+  h1 = __float2half_rn(x);
+  h2 = __float2half_rn((x - __half2float(h1)) * SPLIT_SCALE);
+}
+
 // ------------------------------------------------------------------------
 // host-side utilities implemented in util.cu
 // ------------------------------------------------------------------------

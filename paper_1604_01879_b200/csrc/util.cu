@@ -299,6 +299,18 @@ __global__ void gather_rows_f32_kernel(const void* __restrict__ src, int dtype, 
   for (int k = threadIdx.x; k < d; k += blockDim.x)
     out[r * d + k] = load_as_f32(src, dtype, s * d + k);
 }
+
+__global__ void gather_rows_planes_kernel(const __half* __restrict__ hi,
+                                          const __half* __restrict__ lo, int d,
+                                          const int64_t* __restrict__ idx, int64_t n,
+                                          float* __restrict__ out) {
+  int64_t r = blockIdx.x;
+  if (r >= n) return;
+  int64_t s = idx[r];
+  for (int k = threadIdx.x; k < d; k += blockDim.x)
+    out[r * d + k] = __fadd_rn(__half2float(hi[s * d + k]),
+                               __fmul_rn(__half2float(lo[s * d + k]), 1.0f / SPLIT_SCALE));
+}
 }  // namespace gift
 
 extern "C" int gift_offsets_from_sorted(const uint32_t* keys, int64_t n, int64_t nbuckets,
@@ -326,6 +338,16 @@ extern "C" int gift_gather_rows_f32(const void* src, int32_t dtype, int32_t d, c
   if (n <= 0) return GIFT_OK;
   cudaStream_t st = as_stream(stream);
   gather_rows_f32_kernel<<<static_cast<unsigned>(n), 128, 0, st>>>(src, dtype, d, idx, n, out);
+  GIFT_LAUNCH_CHECK();
+  return GIFT_OK;
+}
+
+extern "C" int gift_gather_rows_planes(const void* hi, const void* lo, int32_t d,
+                                       const int64_t* idx, int64_t n, float* out, void* stream) {
+  if (n <= 0) return GIFT_OK;
+  cudaStream_t st = as_stream(stream);
+  gather_rows_planes_kernel<<<static_cast<unsigned>(n), 128, 0, st>>>(
+      static_cast<const __half*>(hi), static_cast<const __half*>(lo), d, idx, n, out);
   GIFT_LAUNCH_CHECK();
   return GIFT_OK;
 }

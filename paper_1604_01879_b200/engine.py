@@ -24,7 +24,7 @@ import numpy as np
 import torch
 
 from . import _native as nat
-from .errors import DimensionMismatch, EmptySet
+from .errors import DimensionMismatch, EmptySet, Unsupported
 
 _DTYPE_CODE = {torch.float32: nat.GIFT_F32, torch.float16: nat.GIFT_F16,
                torch.float64: nat.GIFT_F64}
@@ -125,6 +125,20 @@ class DeviceFif:
 
     def __init__(self):
         self.view = None
+        self.feat = None
+        self.feat_hi = self.feat_lo = None
+
+    @property
+    def storage_dtype(self):
+        """Storage dtype of the database features (f32 or f16); an index
+        built without its storage copy keeps f32 semantics in the planes."""
+        if self.feat is not None:
+            return self.feat.dtype
+        return torch.float32
+
+    @property
+    def device(self):
+        return self.post_ord.device
 
     @property
     def P(self) -> int:
@@ -133,10 +147,11 @@ class DeviceFif:
     def bind(self):
         v = nat.FifView()
         v.K, v.d = self.cb.K, self.cb.d
-        v.dtype = _DTYPE_CODE[self.feat.dtype]
+        v.dtype = _DTYPE_CODE[self.storage_dtype]
         v.n_postings, v.n_segments, v.n_tiles = self.P, self.S, self.T
         v.n_local, v.ord_base = self.n_local, self.ord_base
-        for name in ("cell_off", "post_ord", "feat", "pnorm2", "seg_off", "seg_ord", "seg_pstart",
+        v.feat = None if self.feat is None else self.feat.data_ptr()
+        for name in ("cell_off", "post_ord", "pnorm2", "seg_off", "seg_ord", "seg_pstart",
                      "tile_off", "tile_pstart", "tile_pend", "tile_seg0", "tile_seg1"):
             setattr(v, name, getattr(self, name).data_ptr())
         v.centroids = self.cb.centroids.data_ptr()
@@ -191,6 +206,71 @@ class DeviceFif:
         return self
 
     @classmethod
+    def build_streamed(cls, provider, n_local: int, V: int, d: int, cb: DeviceCodebook,
+                       dtype=torch.float32, ord_base: int = 0, chunk: int = 512,
+                       keep_features: bool = False, stream=None) -> "DeviceFif":
+        """K2 over a database streamed in chunks of shapes (configs whose
+        features do not fit HBM twice, e.g. config 3's 105 GB):
+        `provider(s0, s1)` returns the device views [s1 - s0, V, d] of local
+        shapes s0..s1 (f32 or the storage dtype).  Pass 1 quantizes every
+        chunk into one key per view; the stable radix sort gives the same
+        cell-major (ordinal, view) order as `build`; pass 2 re-reads the
+        chunks and scatters their rows straight into the tensor-core planes
+        (and the storage-dtype copy only with keep_features)."""
+        if cb.d != d:
+            raise DimensionMismatch(f"view dim {d} != codebook dim {cb.d}")
+        if dtype not in (torch.float32, torch.float16):
+            raise ValueError("feature storage must be float32 or float16")
+        dev = cb.centroids.device
+        K = cb.K
+        self = cls()
+        self.cb, self.ord_base, self.n_local, self.V, self.d = cb, int(ord_base), n_local, V, d
+        nviews = n_local * V
+        keys = torch.empty(nviews, dtype=torch.int32, device=dev)
+        for s0 in range(0, n_local, chunk):
+            s1 = min(n_local, s0 + chunk)
+            X = provider(s0, s1).to(dtype).contiguous().view(-1, d)
+            nz, _ = view_prep(X, stream)
+            keys[s0 * V:s1 * V] = quantize_rows(cb, X, 1, nz=nz, zero_key=K,
+                                                stream=stream).view(-1)
+            del X
+        vals = torch.arange(nviews, dtype=torch.int32, device=dev)
+        radix_sort_pairs(keys, vals, _bits(K), stream)
+        cell_off_full = offsets_from_sorted(keys, K + 1, stream)
+        P = int(cell_off_full[K].item())
+        self.cell_off = cell_off_full[: K + 1].contiguous()
+        del keys
+        pos = torch.empty(max(nviews, 1), dtype=torch.int32, device=dev)
+        nat.call("gift_perm_invert", nat.ptr(vals), P, nviews, nat.ptr(pos), _sp(stream))
+        del vals
+        half = dtype == torch.float16
+        tc = P > 0 and d % 8 == 0
+        if not tc and not keep_features:
+            raise ValueError("dropping the storage copy needs the tensor-core planes (d % 8 == 0)")
+        self.feat = torch.empty((P, d), dtype=dtype, device=dev) if (keep_features or half) else None
+        if half:
+            self.feat_hi, self.feat_lo = self.feat, None
+        elif tc:
+            self.feat_hi = torch.empty((P, d), dtype=torch.float16, device=dev)
+            self.feat_lo = torch.empty((P, d), dtype=torch.float16, device=dev)
+        else:
+            self.feat_hi = self.feat_lo = None
+        self.post_ord = torch.empty(P, dtype=torch.int32, device=dev)
+        self.pnorm2 = torch.empty(P, dtype=torch.float32, device=dev)
+        for s0 in range(0, n_local, chunk):
+            s1 = min(n_local, s0 + chunk)
+            X = provider(s0, s1).to(dtype).contiguous()
+            nat.call("gift_fif_scatter", nat.ptr(X), _DTYPE_CODE[dtype], d, V, (s1 - s0) * V,
+                     nat.ptr(pos), s0 * V, self.ord_base,
+                     None if half else nat.ptr(self.feat), nat.ptr(self.feat_hi),
+                     None if half else nat.ptr(self.feat_lo), nat.ptr(self.post_ord),
+                     nat.ptr(self.pnorm2), _sp(stream))
+            del X
+        del pos
+        self._finish(stream, planes_ready=True)
+        return self
+
+    @classmethod
     def from_arrays(cls, cb: DeviceCodebook, cell_off: torch.Tensor, post_ord: torch.Tensor,
                     feat: torch.Tensor, n_local: int, n_views: int, ord_base: int = 0,
                     stream=None) -> "DeviceFif":
@@ -204,19 +284,22 @@ class DeviceFif:
         self._finish(stream)
         return self
 
-    def _finish(self, stream=None):
+    def _finish(self, stream=None, planes_ready: bool = False):
         """Tensor-core operand planes, segments, scan tiles and the shape ->
         postings map."""
-        K, P, dev, n_local = self.cb.K, self.P, self.feat.device, self.n_local
-        self.feat_hi = self.feat_lo = None
-        if P and self.d % 8 == 0:
+        K, P, dev, n_local = self.cb.K, self.P, self.post_ord.device, self.n_local
+        if planes_ready:
+            pass
+        elif P and self.d % 8 == 0:
             if self.feat.dtype == torch.float16:
-                self.feat_hi = self.feat  # exact: no correction plane
+                self.feat_hi, self.feat_lo = self.feat, None  # exact: no correction plane
             else:
                 self.feat_hi = torch.empty((P, self.d), dtype=torch.float16, device=dev)
                 self.feat_lo = torch.empty((P, self.d), dtype=torch.float16, device=dev)
                 nat.call("gift_split_planes", nat.ptr(self.feat), P * self.d,
                          nat.ptr(self.feat_hi), nat.ptr(self.feat_lo), _sp(stream))
+        else:
+            self.feat_hi = self.feat_lo = None
         ws = nat.workspace("build").get(nat.lib().gift_fif_build_ws_bytes(P, K))
         self.seg_off = torch.empty(K + 1, dtype=torch.int64, device=dev)
         nat.call("gift_fif_segments", nat.ptr(self.cell_off), nat.ptr(self.post_ord), K, P,
@@ -252,6 +335,9 @@ class DeviceFif:
 
     # -- host views (reference container attributes) ---------------------
     def host_lists(self):
+        if self.feat is None:
+            raise Unsupported("this index keeps only the tensor-core planes on the device "
+                              "(streamed build without keep_features): no stored features")
         off = self.cell_off.cpu().numpy()
         ords = self.post_ord.cpu().numpy()
         feats = self.feat.float().cpu().numpy()
@@ -277,8 +363,12 @@ class DeviceFif:
         if sel.numel():
             tmp = torch.empty((sel.numel(), self.d), dtype=torch.float32, device=local.device)
             src_rows = rows[sel].contiguous()
-            nat.call("gift_gather_rows_f32", nat.ptr(self.feat), _DTYPE_CODE[self.feat.dtype],
-                     self.d, nat.ptr(src_rows), sel.numel(), nat.ptr(tmp), _sp())
+            if self.feat is not None:
+                nat.call("gift_gather_rows_f32", nat.ptr(self.feat), _DTYPE_CODE[self.feat.dtype],
+                         self.d, nat.ptr(src_rows), sel.numel(), nat.ptr(tmp), _sp())
+            else:
+                nat.call("gift_gather_rows_planes", nat.ptr(self.feat_hi), nat.ptr(self.feat_lo),
+                         self.d, nat.ptr(src_rows), sel.numel(), nat.ptr(tmp), _sp())
             Q[sel] = tmp
         return Q.view(B, vmax, self.d), counts.to(torch.int32)
 

@@ -227,24 +227,67 @@ def _to_device_views(views, dtype):
     return t.to(nat.device()).to(dtype).contiguous()
 
 
-def _self_join(fif: eg.DeviceFif, X: torch.Tensor, cfg: IndexConfig, runner: eg.ScoreRunner,
-               batch: int):
+def _self_join(fif: eg.DeviceFif, X, cfg: IndexConfig, runner: eg.ScoreRunner,
+               batch: int, n: int | None = None, chunk: int = 0):
     """index.py:196-210: every database shape queried against the F-IF ->
-    raw top-k1 activations and top-k2 neighbour lists (device)."""
-    n = X.shape[0]
+    raw top-k1 activations and top-k2 neighbour lists (device).  X is the
+    device views [n, V, d] or a provider(s0, s1) of them (streamed build)."""
+    provider = X if callable(X) else None
+    if n is None:
+        n = X.shape[0]
+    dev = fif.device
     k1 = min(cfg.k1, n)
     kk = max(k1, min(cfg.k2, n))
-    raw = eg.ActRows.empty(n, max(k1, 1), X.device)
-    nbr = torch.full((n, max(min(cfg.k2, n), 1)), -1, dtype=torch.int32, device=X.device)
+    raw = eg.ActRows.empty(n, max(k1, 1), dev)
+    nbr = torch.full((n, max(min(cfg.k2, n), 1)), -1, dtype=torch.int32, device=dev)
     mode = mt.sim_mode(cfg.similarity)
-    for b0 in range(0, n, batch):
-        b1 = min(n, b0 + batch)
-        Q = X[b0:b1].float()
-        s = runner.score(fif, Q, cfg.ma, mode, cfg.sigma)
-        tidx, tval = eg.topk_rows(s, kk, positive_only=True)
-        eg.act_from_topk(tidx, tval, k1, out=raw.rows(b0, b1))
-        nbr[b0:b1] = tidx[:, : nbr.shape[1]]
+    step = max(chunk, batch) if provider is not None else n
+    for c0 in range(0, n, step):
+        c1 = min(n, c0 + step)
+        Xc = provider(c0, c1) if provider is not None else X
+        off = c0 if provider is not None else 0
+        for b0 in range(c0, c1, batch):
+            b1 = min(c1, b0 + batch)
+            Q = Xc[b0 - off:b1 - off].float()
+            s = runner.score(fif, Q, cfg.ma, mode, cfg.sigma)
+            tidx, tval = eg.topk_rows(s, kk, positive_only=True)
+            eg.act_from_topk(tidx, tval, k1, out=raw.rows(b0, b1))
+            nbr[b0:b1] = tidx[:, : nbr.shape[1]]
+        del Xc
     return raw, nbr
+
+
+def build_index_streamed(provider, shape_ids, n_views: int, dim: int,
+                         config: IndexConfig = IndexConfig(), *, codebooks, labels=None,
+                         chunk: int = 512, keep_features: bool = False,
+                         self_join_batch: int = 256) -> IndexBundle:
+    """Build from a database streamed in chunks of shapes (new; configs whose
+    features do not fit HBM twice): `provider(s0, s1)`
+    returns the device views [s1 - s0, n_views, dim] of shapes s0..s1 and is
+    called three times per chunk (quantize, scatter, self-join), so it must be
+    deterministic.  One feature set feeds both channels (D4).  Without
+    keep_features the F-IF holds only the tensor-core planes (22 significant
+    bits); the storage copy, `entry_features` and `save_fif` are then
+    unavailable (Unsupported)."""
+    shape_ids = list(shape_ids)
+    if not shape_ids:
+        raise EmptyManifest("no shapes listed")
+    n = len(shape_ids)
+    ca = codebooks["A"]
+    dfa = eg.DeviceFif.build_streamed(provider, n, n_views, dim, ca.device(),
+                                      dtype=config.torch_storage, chunk=chunk,
+                                      keep_features=keep_features)
+    fa = mt.FirstInvertedFile(ca, shape_ids, n_views, dfa)
+    runner = eg.ScoreRunner()
+    raw, nbr = _self_join(dfa, provider, config, runner, self_join_batch, n=n, chunk=chunk)
+    final = eg.act_mean(raw, nbr)  # co_augment with one channel (rerank.py:114-125)
+    sif = rr.SecondInvertedFile(shape_ids, eg.DeviceSif.build(final, n))
+    acts = rr.ActivationList(raw, shape_ids)
+    config = replace(config, n_views=max(1, n_views), codebook_size=ca.k)
+    return IndexBundle(config=config, shape_ids=shape_ids,
+                       labels=dict(labels) if labels else {s: "" for s in shape_ids},
+                       codebooks={"A": ca, "B": cb.Codebook(ca.centroids, "B", ca.seed)},
+                       fifs={"A": fa, "B": fa}, raw_activations={"A": acts, "B": acts}, sif=sif)
 
 
 def build_index_from_views(views_a, shape_ids, config: IndexConfig = IndexConfig(), *,

@@ -85,7 +85,7 @@ class FirstInvertedFile:
         lo, hi = (int(v) for v in self.dev.shape_off[loc:loc + 2].cpu())
         if hi == lo:
             raise EmptySet(f"shape ordinal {ordinal} has no stored views")
-        Q, _vq = self.dev.shape_views(torch.tensor([loc], device=self.dev.feat.device))
+        Q, _vq = self.dev.shape_views(torch.tensor([loc], device=self.dev.device))
         return Q[0].cpu().numpy()
 
 

@@ -38,6 +38,8 @@ class Workload:
 WORKLOADS = {
     "c1": Workload("c1", 1_000, 64, 256, 40, 64, 1, 0.5, 10, 4, 50, 100, 100, 0.0),
     "c2": Workload("c2", 10_000, 64, 4096, 55, 256, 2, 0.5, 10, 4, 100, 1_000, 64, -0.26),
+    # config 3: 105 GB of f32 views on one GPU -> streamed build, planes only
+    "c3": Workload("c3", 100_000, 64, 4096, 500, 1024, 2, 0.5, 10, 4, 100, 4_096, 256, -0.26),
     "c3s": Workload("c3s", 25_000, 64, 4096, 500, 1024, 2, 0.5, 10, 4, 100, 4_096, 256, -0.26),
     # config 4: 1M shapes x 20 views, d=1024 fp16, Zipf(1.1) cell occupancy over
     # K=4096 (classes biased toward Zipf-chosen centroids), ma=1
@@ -82,6 +84,79 @@ def mixture(w: Workload, seed: int, device, n_queries: int | None = None, block:
             qs[: hi - w.n_shapes] = x[cut:].to(dt).float()
         del x
     return db, qs, labels[: w.n_shapes]
+
+
+class BlockMixture:
+    """Config-3-scale mixture generated block by block: block b of `block`
+    shapes is drawn from its own seeded generator, so any shape range can be
+    regenerated on the device on demand (the streamed build reads the
+    database three times and never holds it whole).  Same distribution as
+    `mixture`: views = normalize(relu(mean[label] + 0.3 N(0, 1)))."""
+
+    def __init__(self, w: Workload, seed: int, device, block: int = 256):
+        self.w, self.seed, self.device, self.block = w, seed, device, block
+        g = torch.Generator(device=device)
+        g.manual_seed(seed)
+        self.means = torch.randn((w.n_classes, w.dim), generator=g, device=device) + w.mu0
+        self.labels = torch.randint(0, w.n_classes, (w.n_shapes + w.n_queries,), generator=g,
+                                    device=device)
+
+    def _block(self, b: int) -> torch.Tensor:
+        w = self.w
+        total = w.n_shapes + w.n_queries
+        b0, b1 = b * self.block, min(total, (b + 1) * self.block)
+        g = torch.Generator(device=self.device)
+        g.manual_seed(self.seed * 1_000_003 + 7919 * b + 1)
+        x = self.means[self.labels[b0:b1]][:, None, :] + 0.3 * torch.randn(
+            (b1 - b0, w.n_views, w.dim), generator=g, device=self.device)
+        x.clamp_(min=0.0)
+        n = x.norm(dim=2, keepdim=True)
+        return x / torch.where(n > 0, n, torch.ones_like(n))
+
+    def rows(self, s0: int, s1: int) -> torch.Tensor:
+        """Views of global rows s0..s1 (database rows, then query rows), f32."""
+        out = torch.empty((s1 - s0, self.w.n_views, self.w.dim), dtype=torch.float32,
+                          device=self.device)
+        b = s0 // self.block
+        while b * self.block < s1:
+            x = self._block(b)
+            lo = max(s0, b * self.block)
+            hi = min(s1, (b + 1) * self.block)
+            out[lo - s0:hi - s0] = x[lo - b * self.block:hi - b * self.block]
+            del x
+            b += 1
+        return out
+
+    def provider(self, base: int = 0):
+        """provider(s0, s1) over database shapes base + s0 .. base + s1."""
+        return lambda s0, s1: self.rows(base + s0, base + s1)
+
+    def queries(self) -> torch.Tensor:
+        return self.rows(self.w.n_shapes, self.w.n_shapes + self.w.n_queries)
+
+
+def sample_centroids_rows(mix: "BlockMixture", K: int, seed: int) -> torch.Tensor:
+    """`sample_centroids` without the whole database: the same seeded
+    permutation over all n_shapes x V views, the first K non-zero candidates
+    in permutation order, returned sorted by view index.  Each block holding
+    a candidate is generated once."""
+    w = mix.w
+    V = w.n_views
+    g = torch.Generator(device=mix.device)
+    g.manual_seed(seed)
+    perm = torch.randperm(w.n_shapes * V, generator=g, device=mix.device)
+    cand = perm[: 4 * K + 16].tolist()
+    rows = {}
+    by_block = {}
+    for v in cand:
+        by_block.setdefault((v // V) // mix.block, []).append(v)
+    for b, vs in by_block.items():
+        x = mix._block(b)
+        for v in vs:
+            rows[v] = x[v // V - b * mix.block, v % V].clone()
+        del x
+    nz = [v for v in cand if float(rows[v].abs().sum()) > 0][:K]
+    return torch.stack([rows[v] for v in sorted(nz)]).float().contiguous()
 
 
 def sample_centroids(db: torch.Tensor, K: int, seed: int) -> torch.Tensor:
