@@ -217,7 +217,33 @@ def golden_e2e():
         print(name, "done")
 
 
+def golden_bundles():
+    """The reference's own `save_bundle` directory (index.py:360-375) for the
+    tiny and small end-to-end cases, every file's bytes kept verbatim: the
+    GPU-built bundle must save to the same bytes (config, shapes, codebooks,
+    F-IF lists) and the GPU path must load and serve the reference's files."""
+    for case in E2E_CASES[:2]:
+        (name, seed, N, V, d, classes, K, ma, k1, k2, nq, top_k, zv) = case
+        views, _ = mixture_views(seed, N, V, d, classes, zero_views=zv, n_queries=nq)
+        db = views[:N]
+        ids = shape_ids(N)
+        C = sampled_codebook(db, K, seed + 1)
+        cfg = rix.IndexConfig(n_views=V, codebook_size=K, ma=ma, k1=k1, k2=k2, imported=True)
+        bundle = reference_bundle(db, ids, C, cfg)[0]
+        out = {}
+        with tempfile.TemporaryDirectory() as td:
+            rix.save_bundle(bundle, td)
+            for fn in sorted(os.listdir(td)):
+                with open(os.path.join(td, fn), "rb") as fh:
+                    out["file:" + fn] = np.frombuffer(fh.read(), dtype=np.uint8)
+        np.savez_compressed(os.path.join(HERE, f"bundle_{name}.npz"), **out)
+        print("bundle", name, "done")
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["bundles"]:
+        golden_bundles()
+        sys.exit(0)
     golden_quantize()
     print("quantize done")
     golden_fif()
@@ -225,3 +251,4 @@ if __name__ == "__main__":
     golden_rerank()
     print("rerank done")
     golden_e2e()
+    golden_bundles()
