@@ -78,6 +78,10 @@ typedef struct gift_fif_view {
   const void* feat_hi;       /* [P, d] fp16 plane h1 = rn(feat) (tensor-core  */
   const void* feat_lo;       /* scan); feat_lo: rn((feat-h1) 2^11), NULL for   */
                              /* fp16 storage (feat_hi == feat)                 */
+  /* shape -> segment map (optional; NULL selects the per-range reduce):      */
+  const int64_t* shape_seg_off; /* [n_local+1] segments of each local shape   */
+  const int32_t* shape_seg;     /* [S] global segment index, ascending cell   */
+  const int32_t* seg_cell;      /* [S] cell of each segment                   */
 } gift_fif_view;
 
 /* ---- library ---- */
@@ -197,9 +201,13 @@ int gift_fif_score_ex(const gift_fif_view* f, const float* Q, int32_t B,
 
 /* Same, and with cand_k in [1, 8] also the best cand_k shapes (score desc,
  * ordinal asc; -1 padded) of every (query, shape range) of the reduce:
- * cand_s/cand_i [B][gift_fif_score_ranges(f, V)][cand_k] — merged by
- * gift_topk_cand into rerank.top_neighbors (rerank.py:78-87). */
+ * cand_s/cand_i [B][gift_fif_score_ranges2(f, V, ma)][cand_k] — merged by
+ * gift_topk_cand into rerank.top_neighbors (rerank.py:78-87).  With
+ * cand_k > 0, out_scores may be NULL (candidates only, no dense scores).
+ * gift_fif_score_ranges is the ma-agnostic form (valid when the index has no
+ * shape -> segment map). */
 int gift_fif_score_ranges(const gift_fif_view* f, int32_t V);
+int gift_fif_score_ranges2(const gift_fif_view* f, int32_t V, int32_t ma);
 int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_t B,
                        int32_t V, const int32_t* vq, int32_t ma, int32_t mode,
                        double sigma, double* out_scores, void* ws,

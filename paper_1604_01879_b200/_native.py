@@ -40,6 +40,7 @@ class FifView(ctypes.Structure):
         ("tile_seg0", _c_p), ("tile_seg1", _c_p),
         ("centroids", _c_p), ("cnorm2", _c_p), ("cmax_norm", _c_dbl),
         ("feat_hi", _c_p), ("feat_lo", _c_p),
+        ("shape_seg_off", _c_p), ("shape_seg", _c_p), ("seg_cell", _c_p),
     ]
 
 
@@ -73,6 +74,7 @@ _SIGS = {
     "gift_fif_score_ex": (_c_i32, [ctypes.POINTER(FifView), _c_p, _c_i32, _c_i32, _c_p, _c_i32,
                                    _c_i32, _c_dbl, _c_p, _c_p, _c_sz, _c_p, _c_p, _c_p]),
     "gift_fif_score_ranges": (_c_i32, [ctypes.POINTER(FifView), _c_i32]),
+    "gift_fif_score_ranges2": (_c_i32, [ctypes.POINTER(FifView), _c_i32, _c_i32]),
     "gift_fif_score_ex2": (_c_i32, [ctypes.POINTER(FifView), _c_p, _c_i32, _c_i32, _c_p, _c_i32,
                                     _c_i32, _c_dbl, _c_p, _c_p, _c_sz, _c_p, _c_p, _c_p, _c_i32,
                                     _c_p, _c_p]),

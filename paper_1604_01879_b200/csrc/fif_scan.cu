@@ -434,6 +434,213 @@ __global__ void __launch_bounds__(RED_THREADS) fif_reduce_kernel(ReduceArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Shape-centric gather reduce (indexes carrying the shape -> segment map).
+//
+// The per-range reduce above zeroes and sums a [V x rs] view-best tile per
+// (query, shape range): B * N * V shared-memory work per batch, which at 1M
+// shapes dwarfs the compact buffer itself.  Here every (query, shape) pair is
+// visited once instead: the batch's probes are first folded into a bit table
+// mask[b][cell] (bit j = query slot j = view * ma + ma-slot probed that cell),
+// then a thread takes one shape, ORs the masks of the cells its segments lie
+// in, and walks the set bits in ascending order: bit j names exactly one probe
+// (cell c_j, rank r_j in the cell's probe list) and the shape's segment k in
+// c_j, whose best similarity is compact[outbase[c_j] + r_j * S_c + k].  The
+// ma slots of a view are max-ed, views are summed in ascending view order in
+// f64 (the reference's `total += view_best` order, matching.py:153-161), so
+// scores are deterministic; untouched shapes stay exactly 0.
+// A CTA owns GR_G queries x rs2 shapes: segment metadata is read once per
+// shape for the GR_G queries, scores are staged in shared memory and one warp
+// per query selects the range's best cand_k.
+constexpr int GR_THREADS = 256;
+constexpr int GR_G = 4;        // queries per CTA
+constexpr int GR_SEGC = 4;     // shape segments cached in registers
+constexpr int GR_RS_SMALL = 256, GR_RS_LARGE = 1024;
+
+int gather_rs(int64_t n_local) {
+  return static_cast<int>(min64(n_local >= 262144 ? GR_RS_LARGE : GR_RS_SMALL, max64(n_local, 1)));
+}
+
+__global__ void probe_mask_kernel(const int32_t* __restrict__ cells, int64_t nprobes, int slots,
+                                  int K, int W, uint32_t* __restrict__ mask) {
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= nprobes) return;
+  const int c = cells[p];
+  if (c < 0) return;
+  const int64_t b = p / slots;
+  const int j = static_cast<int>(p - b * slots);
+  atomicOr(mask + (b * K + c) * W + (j >> 5), 1u << (j & 31));
+}
+
+// Per (query, slot): the probe's cell and the compact offset of its row minus
+// the cell's first segment, so that compact[slot_base + global segment] is
+// the probe's best similarity for that segment (-1 cell: zero view).
+__global__ void probe_slot_kernel(const int32_t* __restrict__ cells,
+                                  const int32_t* __restrict__ probe_rank,
+                                  const int64_t* __restrict__ outbase,
+                                  const int64_t* __restrict__ seg_off, int64_t nprobes,
+                                  int64_t* __restrict__ slot_base) {
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= nprobes) return;
+  const int c = cells[p];
+  int64_t v = 0;
+  if (c >= 0) {
+    const int64_t so = seg_off[c];
+    v = outbase[c] + static_cast<int64_t>(probe_rank[p]) * (seg_off[c + 1] - so) - so;
+  }
+  slot_base[p] = v;
+}
+
+struct GatherArgs {
+  const uint32_t* mask;         // [B][K][W]
+  const int32_t* cells;         // [B * slots] probe cells
+  const int64_t* slot_base;     // [B * slots]
+  const int64_t* shape_seg_off; // [n_local + 1]
+  const int32_t* shape_seg;     // [S] global segment index, ascending cell
+  const int32_t* seg_cell;      // [S]
+  const float* out;             // compact (probe x segment) best similarities
+  const int64_t* meta;
+  const int32_t* vq;
+  int B, V, ma, K, rs, n_ranges, G;
+  int64_t n_local, ord_base;
+  double* scores;               // [B][n_local] or null (candidates only)
+  int cand_k;
+  double* cand_s;               // [B][n_ranges][cand_k]
+  int32_t* cand_i;
+};
+
+template <int W>
+__global__ void __launch_bounds__(GR_THREADS) fif_gather_reduce_kernel(GatherArgs a) {
+  extern __shared__ __align__(16) double s_sc[];  // [G][rs] scores, then slot tables
+  if (a.meta[M_OVERFLOW]) return;
+  const int rg = blockIdx.x;
+  const int G = a.G;
+  const int b0 = blockIdx.y * G;
+  const int nb = min(G, a.B - b0);
+  const int64_t lo = static_cast<int64_t>(rg) * a.rs;
+  const int n = static_cast<int>(min64(lo + a.rs, a.n_local) - lo);
+  const int slots = a.V * a.ma;
+  int64_t* s_base = reinterpret_cast<int64_t*>(s_sc + G * a.rs);  // [G][slots]
+  int32_t* s_cell = reinterpret_cast<int32_t*>(s_base + G * slots);
+  for (int i = threadIdx.x; i < nb * slots; i += GR_THREADS) {
+    const int64_t p = static_cast<int64_t>(b0) * slots + i;
+    s_base[i] = a.slot_base[p];
+    s_cell[i] = a.cells[p];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += GR_THREADS) {
+    const int64_t s = lo + i;
+    const int64_t g0 = a.shape_seg_off[s];
+    const int nseg = static_cast<int>(a.shape_seg_off[s + 1] - g0);
+    int sc_cell[GR_SEGC];
+    int32_t sc_seg[GR_SEGC];
+#pragma unroll
+    for (int j = 0; j < GR_SEGC; ++j) {
+      sc_seg[j] = j < nseg ? a.shape_seg[g0 + j] : 0;
+      sc_cell[j] = j < nseg ? a.seg_cell[sc_seg[j]] : -1;
+    }
+    for (int g = 0; g < nb; ++g) {
+      const int b = b0 + g;
+      const uint32_t* Mb = a.mask + static_cast<int64_t>(b) * a.K * W;
+      uint32_t U[W];
+#pragma unroll
+      for (int w = 0; w < W; ++w) U[w] = 0u;
+#pragma unroll
+      for (int j = 0; j < GR_SEGC; ++j)
+        if (j < nseg)
+#pragma unroll
+          for (int w = 0; w < W; ++w) U[w] |= __ldg(Mb + static_cast<int64_t>(sc_cell[j]) * W + w);
+      for (int j = GR_SEGC; j < nseg; ++j) {
+        const int c = a.seg_cell[a.shape_seg[g0 + j]];
+#pragma unroll
+        for (int w = 0; w < W; ++w) U[w] |= __ldg(Mb + static_cast<int64_t>(c) * W + w);
+      }
+      const int64_t* sb = s_base + g * slots;
+      const int32_t* scl = s_cell + g * slots;
+      double acc = 0.0;
+      float best = 0.f;
+      int cur_v = -1;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        uint32_t bits = U[w];
+        while (bits) {
+          const int j = w * 32 + (__ffs(bits) - 1);
+          bits &= bits - 1;
+          const int v = j / a.ma;
+          if (v != cur_v) {  // views ascend with j: flush the previous view's best
+            acc += static_cast<double>(best);
+            best = 0.f;
+            cur_v = v;
+          }
+          const int cj = scl[j];
+          int32_t sg = -1;
+#pragma unroll
+          for (int t = 0; t < GR_SEGC; ++t)
+            if (sc_cell[t] == cj) sg = sc_seg[t];
+          for (int t = GR_SEGC; sg < 0 && t < nseg; ++t) {
+            const int32_t x = a.shape_seg[g0 + t];
+            if (a.seg_cell[x] == cj) sg = x;
+          }
+          best = fmaxf(best, a.out[sb[j] + sg]);
+        }
+      }
+      acc += static_cast<double>(best);
+      const double denom = static_cast<double>(a.vq ? a.vq[b] : a.V);
+      const double score = acc / denom;
+      if (a.scores) a.scores[static_cast<int64_t>(b) * a.n_local + s] = score;
+      s_sc[g * a.rs + i] = score;
+    }
+  }
+  if (a.cand_k <= 0) return;
+  __syncthreads();
+  // one warp per query: lanes keep a sorted best-cand_k of a strided slice,
+  // then cand_k rounds of warp argmax (score desc, ordinal asc)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp >= nb) return;
+  const int g = warp, b = b0 + g;
+  const int ck = a.cand_k;
+  Cand lst[RED_MAXK];
+#pragma unroll
+  for (int t = 0; t < RED_MAXK; ++t) lst[t] = Cand{-INFINITY, -1};
+  for (int i = lane; i < n; i += 32) {  // ordinals ascend within a lane
+    Cand x{s_sc[g * a.rs + i], static_cast<int32_t>(a.ord_base + lo + i)};
+#pragma unroll
+    for (int t = 0; t < RED_MAXK; ++t) {
+      if (t < ck && cand_better(x.s, x.o, lst[t].s, lst[t].o)) {
+        const Cand y = lst[t];
+        lst[t] = x;
+        x = y;
+      }
+    }
+  }
+  const int64_t at = (static_cast<int64_t>(b) * a.n_ranges + rg) * ck;
+  for (int r = 0; r < ck; ++r) {
+    double bs = lst[0].s;
+    int32_t bo = lst[0].o;
+    int bl = lane;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double os = __shfl_xor_sync(0xffffffffu, bs, off);
+      const int32_t oo = __shfl_xor_sync(0xffffffffu, bo, off);
+      const int ol = __shfl_xor_sync(0xffffffffu, bl, off);
+      if (cand_better(os, oo, bs, bo) || (os == bs && oo == bo && ol < bl)) {
+        bs = os;
+        bo = oo;
+        bl = ol;
+      }
+    }
+    if (lane == 0) {
+      a.cand_s[at + r] = bo >= 0 ? bs : 0.0;
+      a.cand_i[at + r] = bo;
+    }
+    if (lane == bl) {  // pop the winner's head
+#pragma unroll
+      for (int t = 0; t + 1 < RED_MAXK; ++t) lst[t] = lst[t + 1];
+      lst[RED_MAXK - 1] = Cand{-INFINITY, -1};
+    }
+  }
+}
+
 }  // namespace gift
 
 using namespace gift;
@@ -458,6 +665,8 @@ struct ScoreWs {
   __half* g1;
   __half* g2;
   ProbeRange* rng;
+  uint32_t* mask;  // gather reduce: [B][K][W] probe bit table
+  int64_t* slot_base;  // gather reduce: [B * V * ma]
 };
 
 bool use_tc(const gift_fif_view* f) {
@@ -470,6 +679,16 @@ int reduce_rs(int64_t V, int64_t n_local) {
   int rs = static_cast<int>(RED_SMEM / (4 * max64(V, 1)));
   rs = max(32, min(rs, 2048)) / 32 * 32;
   return static_cast<int>(max64(min64(rs, n_local), 1));
+}
+
+// Mask words of the gather reduce (0: not applicable -> per-range reduce).
+int gather_words(const gift_fif_view* f, int V, int ma) {
+  if (f->shape_seg_off == nullptr || f->shape_seg == nullptr || f->seg_cell == nullptr) return 0;
+  const int64_t slots = static_cast<int64_t>(V) * ma;
+  if (slots > 128) return 0;
+  const char* e = getenv("GIFT_REDUCE");
+  if (e != nullptr && e[0] == 'r') return 0;  // GIFT_REDUCE=range forces the per-range reduce
+  return slots <= 32 ? 1 : slots <= 64 ? 2 : 4;
 }
 
 bool carve(Arena& ar, const gift_fif_view* f, int64_t nviews, int V, int ma, ScoreWs& w) {
@@ -488,8 +707,17 @@ bool carve(Arena& ar, const gift_fif_view* f, int64_t nviews, int V, int ma, Sco
   w.probe_rank = ar.take<int32_t>(nprobes);
   w.qws_bytes = gift_quantize_ws_bytes(nviews, f->d, K, GIFT_F32);
   w.qws = ar.take<char>(static_cast<int64_t>(w.qws_bytes));
-  w.rng = ar.take<ProbeRange>(nprobes * cdiv(max64(f->n_local, 1), reduce_rs(V, f->n_local)));
-  if (!w.rng) return false;
+  const int W = gather_words(f, V, ma);
+  w.rng = nullptr;
+  w.mask = nullptr;
+  if (W > 0) {
+    w.mask = ar.take<uint32_t>((nviews / V) * K * W);
+    w.slot_base = ar.take<int64_t>(nprobes);
+    if (!w.mask || !w.slot_base) return false;
+  } else {
+    w.rng = ar.take<ProbeRange>(nprobes * cdiv(max64(f->n_local, 1), reduce_rs(V, f->n_local)));
+    if (!w.rng) return false;
+  }
   w.g1 = w.g2 = nullptr;
   if (use_tc(f)) {
     w.g1 = ar.take<__half>(nprobes * f->d + 512);
@@ -524,6 +752,12 @@ extern "C" int gift_fif_score_ranges(const gift_fif_view* f, int32_t V) {
   return static_cast<int>(cdiv(max64(f->n_local, 1), reduce_rs(V, f->n_local)));
 }
 
+extern "C" int gift_fif_score_ranges2(const gift_fif_view* f, int32_t V, int32_t ma) {
+  if (gather_words(f, V, ma) > 0)
+    return static_cast<int>(cdiv(max64(f->n_local, 1), gather_rs(f->n_local)));
+  return gift_fif_score_ranges(f, V);
+}
+
 extern "C" int gift_fif_score_ex(const gift_fif_view* f, const float* Q, int32_t B, int32_t V,
                                  const int32_t* vq, int32_t ma, int32_t mode, double sigma,
                                  double* out_scores, void* ws, size_t ws_bytes, void* stream,
@@ -539,6 +773,8 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
                                   double* cand_s, int32_t* cand_i) {
   GIFT_REQUIRE(cand_k >= 0 && cand_k <= RED_MAXK, GIFT_ERR_UNSUPPORTED,
                "cand_k = %d > %d", cand_k, RED_MAXK);
+  GIFT_REQUIRE(out_scores != nullptr || cand_k > 0, GIFT_ERR_INVALID,
+               "out_scores may be NULL only with cand_k > 0");
   cudaStream_t st = as_stream(stream);
   GIFT_REQUIRE(f != nullptr, GIFT_ERR_INVALID, "null index");
   GIFT_REQUIRE(ma >= 1 && ma <= f->K, GIFT_ERR_INVALID, "ma must be in [1, %d]", f->K);
@@ -575,6 +811,13 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
   GIFT_LAUNCH_CHECK();
   compact_zero_kernel<<<sm_count() * 4, 256, 0, st>>>(w.compact, w.meta);
   GIFT_LAUNCH_CHECK();
+  if (w.mask != nullptr) {
+    const int Wm = gather_words(f, V, ma);
+    GIFT_CUDA_TRY(cudaMemsetAsync(w.mask, 0, sizeof(uint32_t) * B * K * Wm, st));
+    probe_mask_kernel<<<static_cast<unsigned>(cdiv(nprobes, 256)), 256, 0, st>>>(
+        w.cells, nprobes, V * ma, K, Wm, w.mask);
+    GIFT_LAUNCH_CHECK();
+  }
 
   if (use_tc(f)) {
     TcArgs ta;
@@ -641,6 +884,50 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
     if (ev_scan_end) GIFT_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(ev_scan_end), st));
   }
 
+  const int W = gather_words(f, V, ma);
+  if (W > 0) {
+    GatherArgs ga;
+    ga.mask = w.mask;
+    ga.cells = w.cells;
+    ga.slot_base = w.slot_base;
+    ga.shape_seg_off = f->shape_seg_off;
+    ga.shape_seg = f->shape_seg;
+    ga.seg_cell = f->seg_cell;
+    ga.out = w.compact;
+    ga.meta = w.meta;
+    ga.vq = vq;
+    ga.B = B;
+    ga.V = V;
+    ga.ma = ma;
+    ga.K = K;
+    ga.rs = gather_rs(f->n_local);
+    ga.n_ranges = static_cast<int>(cdiv(f->n_local, ga.rs));
+    ga.n_local = f->n_local;
+    ga.ord_base = f->ord_base;
+    ga.scores = out_scores;
+    ga.cand_k = cand_s != nullptr ? cand_k : 0;
+    ga.cand_s = cand_s;
+    ga.cand_i = cand_i;
+    // queries per CTA: GR_G, fewer when that leaves the GPU under-filled
+    ga.G = GR_G;
+    while (ga.G > 1 && ga.n_ranges * cdiv(B, ga.G) < 8LL * sm_count()) ga.G >>= 1;
+    probe_slot_kernel<<<static_cast<unsigned>(cdiv(nprobes, 256)), 256, 0, st>>>(
+        w.cells, w.probe_rank, w.outbase, f->seg_off, nprobes, w.slot_base);
+    GIFT_LAUNCH_CHECK();
+    const int smem = ga.G * ga.rs * static_cast<int>(sizeof(double)) +
+                     ga.G * V * ma * static_cast<int>(sizeof(int64_t) + sizeof(int32_t));
+    dim3 grid(static_cast<unsigned>(ga.n_ranges), static_cast<unsigned>(cdiv(B, ga.G)));
+    if (W == 1) {
+      fif_gather_reduce_kernel<1><<<grid, GR_THREADS, smem, st>>>(ga);
+    } else if (W == 2) {
+      fif_gather_reduce_kernel<2><<<grid, GR_THREADS, smem, st>>>(ga);
+    } else {
+      fif_gather_reduce_kernel<4><<<grid, GR_THREADS, smem, st>>>(ga);
+    }
+    GIFT_LAUNCH_CHECK();
+    return GIFT_OK;
+  }
+  GIFT_REQUIRE(out_scores != nullptr, GIFT_ERR_INVALID, "this index needs dense score output");
   // shape ranges: a [V x rs] f32 view-best tile of <= RED_SMEM bytes per CTA
   const int rs = reduce_rs(V, f->n_local);
   const int n_ranges = static_cast<int>(cdiv(f->n_local, rs));

@@ -49,12 +49,26 @@ struct ItemInfo {
   int c, mt, p0, p1, seg0, seg1, nb, pb0, n;  // n: MMA N of the item (64 | 128)
 };
 
-__device__ __forceinline__ ItemInfo decode_item(const TcArgs& p, int64_t item) {
-  int lo = 0, hi = p.K - 1;
-  while (lo < hi) {
-    int mid = (lo + hi + 1) >> 1;
-    if (p.item_off[mid] <= item) lo = mid; else hi = mid - 1;
+// Cell of an item: items ascend along each role's loop, so the search starts
+// at the previous item's cell (`hint`): one load when the item stays in that
+// cell, else a galloping then binary search over item_off[hint+1 .. K-1]
+// (a plain binary search over K = 4096 cells is 12 dependent global loads).
+__device__ __forceinline__ ItemInfo decode_item(const TcArgs& p, int64_t item, int& hint) {
+  int lo = hint;
+  if (p.item_off[lo + 1] <= item) {
+    int step = 1, hi = lo + 1;  // item_off[hi] <= item
+    while (hi + step < p.K && p.item_off[hi + step] <= item) {
+      hi += step;
+      step <<= 1;
+    }
+    lo = hi;
+    int top = min(hi + step, p.K) - 1;  // item_off[top + 1] > item (or top == K - 1)
+    while (lo < top) {
+      int mid = (lo + top + 1) >> 1;
+      if (p.item_off[mid] <= item) lo = mid; else top = mid - 1;
+    }
   }
+  hint = lo;
   ItemInfo I;
   I.c = lo;
   const int64_t rem = item - p.item_off[lo];
@@ -124,10 +138,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // (L2 evict-first hints on the postings measured slower: a posting tile
     // is re-read by the next probe tile of its cell)
     if (lane == 0) {
-      int stage = 0;
+      int stage = 0, hint = 0;
       uint32_t phase = 0;
       for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
-        const ItemInfo I = decode_item(p, item);
+        const ItemInfo I = decode_item(p, item, hint);
         const int nbox = I.n / 64;
         const uint32_t bytes = (p.has_lo ? 2 * A_TILE : A_TILE) + 2 * nbox * B_BOX;
         for (int kb = 0; kb < nkb; ++kb) {
@@ -155,8 +169,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       uint32_t chunk_ctr = 0;
+      int hint = 0;
       for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
-        const ItemInfo I = decode_item(p, item);
+        const ItemInfo I = decode_item(p, item, hint);
         const uint32_t idesc = tc::idesc_f16_f32(TC_M, I.n);
         for (int kb0 = 0; kb0 < nkb; kb0 += chunk_kb) {
           const uint32_t buf = chunk_ctr & 1, aph = (chunk_ctr >> 1) & 1;
@@ -199,8 +214,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int row = lb + lane;            // posting row within the tile
     const bool gauss = p.mode == GIFT_SIM_GAUSSIAN;
     uint32_t chunk_ctr = 0;
+    int hint = 0;
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
-      const ItemInfo I = decode_item(p, item);
+      const ItemInfo I = decode_item(p, item, hint);
       const int nseg = I.seg1 - I.seg0;
       const int ng = I.n / 16;  // 16-column groups in use
       for (int i = et; i <= nseg; i += TC_M) s_sp[i] = p.seg_pstart[I.seg0 + i];

@@ -159,6 +159,9 @@ class DeviceFif:
         v.cmax_norm = self.cb.cmax
         v.feat_hi = None if self.feat_hi is None else self.feat_hi.data_ptr()
         v.feat_lo = None if self.feat_lo is None else self.feat_lo.data_ptr()
+        v.shape_seg_off = self.shape_seg_off.data_ptr()
+        v.shape_seg = self.shape_seg.data_ptr()
+        v.seg_cell = self.seg_cell.data_ptr()
         self.view = v
         return v
 
@@ -330,7 +333,19 @@ class DeviceFif:
         radix_sort_pairs(k2, v2, _bits(n_local), stream)
         self.shape_off = offsets_from_sorted(k2, n_local, stream)  # [n_local+1]
         self.shape_post = v2.to(torch.int64)
-        self.smax = int((self.seg_off[1:] - self.seg_off[:-1]).max().item()) if K else 0
+        seg_sizes = self.seg_off[1:] - self.seg_off[:-1]
+        self.smax = int(seg_sizes.max().item()) if K else 0
+        # shape -> segments (ascending cell) for the gather reduce: stable sort
+        # of the segment indices by owner
+        self.seg_cell = torch.repeat_interleave(
+            torch.arange(K, dtype=torch.int32, device=dev), seg_sizes, output_size=S)
+        if S == 0:
+            self.seg_cell = torch.zeros(1, dtype=torch.int32, device=dev)
+        k3 = (self.seg_ord[:S] - self.ord_base).contiguous()
+        v3 = torch.arange(S, dtype=torch.int32, device=dev)
+        radix_sort_pairs(k3, v3, _bits(n_local), stream)
+        self.shape_seg_off = offsets_from_sorted(k3, n_local, stream)  # [n_local+1]
+        self.shape_seg = v3 if S else torch.zeros(1, dtype=torch.int32, device=dev)
         self.bind()
 
     # -- host views (reference container attributes) ---------------------
@@ -384,10 +399,12 @@ class ScoreRunner:
 
     def score(self, fif: DeviceFif, Q: torch.Tensor, ma: int, mode: int = nat.SIM_COSINE,
               sigma: float = 0.5, vq: torch.Tensor | None = None, out: torch.Tensor | None = None,
-              stream=None, scan_events=None, cand_k: int = 0):
+              stream=None, scan_events=None, cand_k: int = 0, dense: bool = True):
         """Q: [B, V, d] f32 device -> f64 [B, n_local] (matching.py:136-161).
         With cand_k > 0 also returns the reduce's per-range best cand_k
-        (scores [B, m], ordinals [B, m]) for `topk_candidates`."""
+        (scores [B, m], ordinals [B, m]) for `topk_candidates`; with
+        dense=False (and cand_k > 0) the dense scores are not written and the
+        first returned value is None."""
         if Q.dim() != 3:
             raise ValueError("queries must be [B, V, d]")
         B, V, d = Q.shape
@@ -400,7 +417,9 @@ class ScoreRunner:
         Q = Q.contiguous()
         if Q.dtype != torch.float32:
             Q = Q.float()
-        if out is None:
+        if not dense and cand_k <= 0:
+            raise ValueError("dense=False needs cand_k > 0")
+        if out is None and dense:
             out = torch.empty((B, fif.n_local), dtype=torch.float64, device=Q.device)
         view = fif.view
         lib = nat.lib()
@@ -412,7 +431,7 @@ class ScoreRunner:
             self.capacity = max(self.capacity, bound)
         cs = ci = None
         if cand_k > 0:
-            nr = lib.gift_fif_score_ranges(ctypes.byref(view), V)
+            nr = lib.gift_fif_score_ranges2(ctypes.byref(view), V, ma)
             cs = torch.empty((B, nr * cand_k), dtype=torch.float64, device=Q.device)
             ci = torch.empty((B, nr * cand_k), dtype=torch.int32, device=Q.device)
         for _attempt in range(8):

@@ -179,9 +179,9 @@ class QueryEngine:
             # single-channel fast path: the reduce emits per-range top-k2
             # candidates, merged into the neighbour lists (rerank.py:78-87)
             k2 = min(self.cfg.k2, self.n)
-            sa, cs, ci = self.runner.score(self.fa, Qa, self.cfg.ma, self.mode, self.cfg.sigma,
-                                           vq=vq, stream=stream, scan_events=scan_events,
-                                           cand_k=k2)
+            _, cs, ci = self.runner.score(self.fa, Qa, self.cfg.ma, self.mode, self.cfg.sigma,
+                                          vq=vq, stream=stream, scan_events=scan_events,
+                                          cand_k=k2, dense=False)
             nbr, _ = eg.topk_candidates(cs, ci, k2, positive_only=True, stream=stream)
             fa = eg.act_mean(self.raw_a, nbr, stream=stream)
             final = self.sif.query(fa, stream=stream)

@@ -386,3 +386,47 @@ def test_quantize_near_ties_and_scale(impl, monkeypatch):
     for ma in (1, 2, 3):
         got = quantize_batch(cb, X, ma)
         np.testing.assert_array_equal(got, oracle.quantize_many(C, X.astype(np.float64), ma))
+
+
+@pytest.mark.parametrize("V,ma,K", [(16, 1, 32), (16, 2, 32), (20, 3, 16), (64, 2, 64), (70, 2, 64)])
+def test_gather_reduce_equals_range_reduce(V, ma, K, monkeypatch):
+    """The shape-centric gather reduce (default when the index has its shape
+    -> segment map and V * ma <= 128) is bit-identical to the per-range
+    reduce: same per-view maxima, same ascending-view f64 sum.  Uniform
+    random views spread each shape over many cells (> 4 segments: the
+    uncached segment path); V * ma = 140 falls back to the range reduce."""
+    rng = np.random.default_rng(V * 100 + ma)
+    N, d = 300, 64
+    db = unit_nonneg_rows(rng, N * V, d).reshape(N, V, d)
+    db[rng.random((N, V)) < 0.05] = 0.0  # empty views
+    qs = unit_nonneg_rows(rng, 9 * V, d).reshape(9, V, d)
+    qs[0, 3] = 0.0
+    C = sampled_codebook(db, K, 5)
+    fif = mt.build_fif_from_tensor(torch.from_numpy(db).to(dev()), Codebook(C), shape_ids(N))
+    Q = torch.from_numpy(qs).to(dev())
+    run = eg.ScoreRunner()
+    got = {}
+    for impl in ("gather", "range"):
+        if impl == "range":
+            monkeypatch.setenv("GIFT_REDUCE", "range")
+        else:
+            monkeypatch.delenv("GIFT_REDUCE", raising=False)
+        for sim in ("cosine", "gaussian"):
+            s, cs, ci = run.score(fif.dev, Q, ma, mt.sim_mode(sim), 0.5, cand_k=4)
+            nbr, val = eg.topk_candidates(cs, ci, 4, positive_only=True)
+            got[impl, sim] = (s.cpu().numpy(), nbr.cpu().numpy(), val.cpu().numpy())
+    for sim in ("cosine", "gaussian"):
+        np.testing.assert_array_equal(got["gather", sim][0], got["range", sim][0])
+        np.testing.assert_array_equal(got["gather", sim][1], got["range", sim][1])
+        np.testing.assert_array_equal(got["gather", sim][2], got["range", sim][2])
+        ref = eg.topk_rows(torch.from_numpy(got["range", sim][0]).to(dev()), 4,
+                           positive_only=True)[0].cpu().numpy()
+        np.testing.assert_array_equal(got["gather", sim][1], ref)
+    if V * ma > 128:
+        return
+    monkeypatch.delenv("GIFT_REDUCE", raising=False)
+    # candidates-only mode (no dense scores) gives the same neighbour lists
+    s, cs, ci = run.score(fif.dev, Q, ma, mt.sim_mode("cosine"), 0.5, cand_k=4, dense=False)
+    assert s is None
+    nbr, _ = eg.topk_candidates(cs, ci, 4, positive_only=True)
+    np.testing.assert_array_equal(nbr.cpu().numpy(), got["gather", "cosine"][1])
