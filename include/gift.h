@@ -81,7 +81,7 @@ typedef struct gift_fif_view {
   /* shape -> segment map (optional; NULL selects the per-range reduce):      */
   const int64_t* shape_seg_off; /* [n_local+1] segments of each local shape   */
   const int32_t* shape_seg;     /* [S] global segment index, ascending cell   */
-  const int32_t* seg_cell;      /* [S] cell of each segment                   */
+  const int32_t* shape_seg_cell;/* [S] cell of segment shape_seg[g]           */
 } gift_fif_view;
 
 /* ---- library ---- */

@@ -40,7 +40,7 @@ class FifView(ctypes.Structure):
         ("tile_seg0", _c_p), ("tile_seg1", _c_p),
         ("centroids", _c_p), ("cnorm2", _c_p), ("cmax_norm", _c_dbl),
         ("feat_hi", _c_p), ("feat_lo", _c_p),
-        ("shape_seg_off", _c_p), ("shape_seg", _c_p), ("seg_cell", _c_p),
+        ("shape_seg_off", _c_p), ("shape_seg", _c_p), ("shape_seg_cell", _c_p),
     ]
 
 

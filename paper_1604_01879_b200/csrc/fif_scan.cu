@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(RED_THREADS) fif_reduce_kernel(ReduceArgs a) {
     double acc = 0.0;
     for (int v = 0; v < V; ++v) acc += static_cast<double>(vb[v * rs + o]);
     const double sc = acc / denom;
-    a.scores[static_cast<int64_t>(b) * a.n_local + lo + o] = sc;
+    if (a.scores) a.scores[static_cast<int64_t>(b) * a.n_local + lo + o] = sc;
     if (ck > 0) {  // per-thread sorted best list (ordinals ascend within a thread)
       Cand x{sc, static_cast<int32_t>(glo + o)};
 #pragma unroll
@@ -440,41 +440,32 @@ __global__ void __launch_bounds__(RED_THREADS) fif_reduce_kernel(ReduceArgs a) {
 // The per-range reduce above zeroes and sums a [V x rs] view-best tile per
 // (query, shape range): B * N * V shared-memory work per batch, which at 1M
 // shapes dwarfs the compact buffer itself.  Here every (query, shape) pair is
-// visited once instead: the batch's probes are first folded into a bit table
-// mask[b][cell] (bit j = query slot j = view * ma + ma-slot probed that cell),
-// then a thread takes one shape, ORs the masks of the cells its segments lie
-// in, and walks the set bits in ascending order: bit j names exactly one probe
-// (cell c_j, rank r_j in the cell's probe list) and the shape's segment k in
-// c_j, whose best similarity is compact[outbase[c_j] + r_j * S_c + k].  The
-// ma slots of a view are max-ed, views are summed in ascending view order in
-// f64 (the reference's `total += view_best` order, matching.py:153-161), so
-// scores are deterministic; untouched shapes stay exactly 0.
-// A CTA owns GR_G queries x rs2 shapes: segment metadata is read once per
-// shape for the GR_G queries, scores are staged in shared memory and one warp
-// per query selects the range's best cand_k.
+// visited once instead.  A CTA owns G queries x rs shapes; it first folds its
+// queries' probes into shared tables: a bitmap over the K cells (cell probed
+// by the query?) with per-word prefix counts, and for each probed cell the
+// bit set of query slots (slot j = view * ma + ma-slot) that probed it.  A
+// thread then takes one shape, tests the cells of its segments against the
+// bitmap, ORs the slot sets of the hits and walks the set bits in ascending
+// order: bit j names exactly one probe (cell c_j, row base_j of the compact
+// buffer) and the shape's segment g in c_j, whose best similarity is
+// compact[base_j + g].  The ma slots of a view are max-ed and views are summed
+// in ascending view order in f64 (the reference's `total += view_best`
+// order, matching.py:153-161): scores are deterministic and bit-identical to
+// the per-range reduce; untouched shapes stay exactly 0.  Scores are staged
+// in shared memory and one warp per query selects the range's best cand_k.
 constexpr int GR_THREADS = 256;
-constexpr int GR_G = 4;        // queries per CTA
-constexpr int GR_SEGC = 4;     // shape segments cached in registers
+constexpr int GR_G = 4;         // queries per CTA (fewer when the grid would under-fill)
+constexpr int GR_SEGC = 4;      // shape segments cached in registers
+constexpr int GR_MAXK = 16384;  // cells covered by the shared-memory bitmap
 constexpr int GR_RS_SMALL = 256, GR_RS_LARGE = 1024;
 
 int gather_rs(int64_t n_local) {
   return static_cast<int>(min64(n_local >= 262144 ? GR_RS_LARGE : GR_RS_SMALL, max64(n_local, 1)));
 }
 
-__global__ void probe_mask_kernel(const int32_t* __restrict__ cells, int64_t nprobes, int slots,
-                                  int K, int W, uint32_t* __restrict__ mask) {
-  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (p >= nprobes) return;
-  const int c = cells[p];
-  if (c < 0) return;
-  const int64_t b = p / slots;
-  const int j = static_cast<int>(p - b * slots);
-  atomicOr(mask + (b * K + c) * W + (j >> 5), 1u << (j & 31));
-}
-
-// Per (query, slot): the probe's cell and the compact offset of its row minus
-// the cell's first segment, so that compact[slot_base + global segment] is
-// the probe's best similarity for that segment (-1 cell: zero view).
+// Per (query, slot): the compact offset of the probe's row minus the cell's
+// first segment, so that compact[slot_base + global segment] is the probe's
+// best similarity for that segment.
 __global__ void probe_slot_kernel(const int32_t* __restrict__ cells,
                                   const int32_t* __restrict__ probe_rank,
                                   const int64_t* __restrict__ outbase,
@@ -492,26 +483,36 @@ __global__ void probe_slot_kernel(const int32_t* __restrict__ cells,
 }
 
 struct GatherArgs {
-  const uint32_t* mask;         // [B][K][W]
-  const int32_t* cells;         // [B * slots] probe cells
-  const int64_t* slot_base;     // [B * slots]
-  const int64_t* shape_seg_off; // [n_local + 1]
-  const int32_t* shape_seg;     // [S] global segment index, ascending cell
-  const int32_t* seg_cell;      // [S]
-  const float* out;             // compact (probe x segment) best similarities
+  const int32_t* cells;          // [B * slots] probe cells (-1: zero view)
+  const int64_t* slot_base;      // [B * slots]
+  const int64_t* shape_seg_off;  // [n_local + 1]
+  const int32_t* shape_seg;      // [S] global segment index, ascending cell
+  const int32_t* shape_seg_cell; // [S] its cell
+  const float* out;              // compact (probe x segment) best similarities
   const int64_t* meta;
   const int32_t* vq;
   int B, V, ma, K, rs, n_ranges, G;
   int64_t n_local, ord_base;
-  double* scores;               // [B][n_local] or null (candidates only)
+  double* scores;                // [B][n_local] or null (candidates only)
   int cand_k;
-  double* cand_s;               // [B][n_ranges][cand_k]
+  double* cand_s;                // [B][n_ranges][cand_k]
   int32_t* cand_i;
 };
 
+size_t gather_smem(int G, int rs, int K, int slots, int W) {
+  const int kw = (K + 31) / 32;
+  return static_cast<size_t>(G) * rs * 8           // staged scores
+         + static_cast<size_t>(G) * slots * 8      // slot bases
+         + static_cast<size_t>(G) * slots * 4      // slot cells
+         + static_cast<size_t>(G) * slots * W * 4  // slot sets of the probed cells
+         + static_cast<size_t>(G) * kw * 4         // cell bitmap
+         + static_cast<size_t>(G) * kw * 2         // prefix counts (u16)
+         + static_cast<size_t>(slots) + 16;        // view of each slot (u8)
+}
+
 template <int W>
 __global__ void __launch_bounds__(GR_THREADS) fif_gather_reduce_kernel(GatherArgs a) {
-  extern __shared__ __align__(16) double s_sc[];  // [G][rs] scores, then slot tables
+  extern __shared__ __align__(16) double s_sc[];  // [G][rs]
   if (a.meta[M_OVERFLOW]) return;
   const int rg = blockIdx.x;
   const int G = a.G;
@@ -520,14 +521,59 @@ __global__ void __launch_bounds__(GR_THREADS) fif_gather_reduce_kernel(GatherArg
   const int64_t lo = static_cast<int64_t>(rg) * a.rs;
   const int n = static_cast<int>(min64(lo + a.rs, a.n_local) - lo);
   const int slots = a.V * a.ma;
+  const int kw = (a.K + 31) >> 5;
   int64_t* s_base = reinterpret_cast<int64_t*>(s_sc + G * a.rs);  // [G][slots]
-  int32_t* s_cell = reinterpret_cast<int32_t*>(s_base + G * slots);
-  for (int i = threadIdx.x; i < nb * slots; i += GR_THREADS) {
+  int32_t* s_cell = reinterpret_cast<int32_t*>(s_base + G * slots); // [G][slots]
+  uint32_t* s_set = reinterpret_cast<uint32_t*>(s_cell + G * slots); // [G][slots][W]
+  uint32_t* s_bm = s_set + G * slots * W;                            // [G][kw]
+  uint16_t* s_pre = reinterpret_cast<uint16_t*>(s_bm + G * kw);      // [G][kw]
+  uint8_t* s_view = reinterpret_cast<uint8_t*>(s_pre + G * kw);       // [slots] view of a slot
+  for (int i = threadIdx.x; i < slots; i += GR_THREADS) s_view[i] = static_cast<uint8_t>(i / a.ma);
+  // ---- per-CTA probe tables of the G queries
+  for (int i = threadIdx.x; i < G * kw; i += GR_THREADS) s_bm[i] = 0u;
+  for (int i = threadIdx.x; i < G * slots * W; i += GR_THREADS) s_set[i] = 0u;
+  for (int i = threadIdx.x; i < G * slots; i += GR_THREADS) {
+    const int g = i / slots;
+    const bool live = g < nb;
     const int64_t p = static_cast<int64_t>(b0) * slots + i;
-    s_base[i] = a.slot_base[p];
-    s_cell[i] = a.cells[p];
+    s_base[i] = live ? a.slot_base[p] : 0;
+    s_cell[i] = live ? a.cells[p] : -1;
   }
   __syncthreads();
+  for (int i = threadIdx.x; i < G * slots; i += GR_THREADS) {
+    const int c = s_cell[i];
+    if (c >= 0) atomicOr(s_bm + (i / slots) * kw + (c >> 5), 1u << (c & 31));
+  }
+  __syncthreads();
+  {  // exclusive prefix popcounts of each query's bitmap words (one warp per query)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int g = warp; g < G; g += GR_THREADS / 32) {
+      int carry = 0;
+      for (int w0 = 0; w0 < kw; w0 += 32) {
+        const int w = w0 + lane;
+        const int c = w < kw ? __popc(s_bm[g * kw + w]) : 0;
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        if (w < kw) s_pre[g * kw + w] = static_cast<uint16_t>(carry + incl - c);
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < G * slots; i += GR_THREADS) {
+    const int c = s_cell[i];
+    if (c < 0) continue;
+    const int g = i / slots, j = i - g * slots;
+    const uint32_t word = s_bm[g * kw + (c >> 5)];
+    const int rank = s_pre[g * kw + (c >> 5)] + __popc(word & ((1u << (c & 31)) - 1u));
+    atomicOr(s_set + (g * slots + rank) * W + (j >> 5), 1u << (j & 31));
+  }
+  __syncthreads();
+  // ---- one thread per shape, G queries each
   for (int i = threadIdx.x; i < n; i += GR_THREADS) {
     const int64_t s = lo + i;
     const int64_t g0 = a.shape_seg_off[s];
@@ -537,56 +583,116 @@ __global__ void __launch_bounds__(GR_THREADS) fif_gather_reduce_kernel(GatherArg
 #pragma unroll
     for (int j = 0; j < GR_SEGC; ++j) {
       sc_seg[j] = j < nseg ? a.shape_seg[g0 + j] : 0;
-      sc_cell[j] = j < nseg ? a.seg_cell[sc_seg[j]] : -1;
+      sc_cell[j] = j < nseg ? a.shape_seg_cell[g0 + j] : -1;
     }
     for (int g = 0; g < nb; ++g) {
       const int b = b0 + g;
-      const uint32_t* Mb = a.mask + static_cast<int64_t>(b) * a.K * W;
+      const uint32_t* bm = s_bm + g * kw;
+      const uint16_t* pre = s_pre + g * kw;
+      const uint32_t* set = s_set + g * slots * W;
       uint32_t U[W];
 #pragma unroll
       for (int w = 0; w < W; ++w) U[w] = 0u;
 #pragma unroll
-      for (int j = 0; j < GR_SEGC; ++j)
-        if (j < nseg)
+      for (int j = 0; j < GR_SEGC + 1; ++j) {
+        // j < GR_SEGC: cached segment j; j == GR_SEGC: the uncached rest
+        const int jend = j < GR_SEGC ? min(j + 1, nseg) : nseg;
+        for (int jj = j; jj < jend; ++jj) {
+        const int c = j < GR_SEGC ? sc_cell[j] : a.shape_seg_cell[g0 + jj];
+        const uint32_t word = bm[c >> 5];
+        if ((word >> (c & 31)) & 1u) {
+          const int rank = pre[c >> 5] + __popc(word & ((1u << (c & 31)) - 1u));
 #pragma unroll
-          for (int w = 0; w < W; ++w) U[w] |= __ldg(Mb + static_cast<int64_t>(sc_cell[j]) * W + w);
-      for (int j = GR_SEGC; j < nseg; ++j) {
-        const int c = a.seg_cell[a.shape_seg[g0 + j]];
-#pragma unroll
-        for (int w = 0; w < W; ++w) U[w] |= __ldg(Mb + static_cast<int64_t>(c) * W + w);
+          for (int w = 0; w < W; ++w) U[w] |= set[rank * W + w];
+        }
+        }
       }
       const int64_t* sb = s_base + g * slots;
       const int32_t* scl = s_cell + g * slots;
       double acc = 0.0;
       float best = 0.f;
       int cur_v = -1;
+      // set bits in ascending order, four at a time: the four compact loads
+      // are independent (memory-level parallelism), the view fold is serial.
+      // Fast path: ma == 1 and a single segment (every bit is its own view in
+      // the shape's only cell) -> acc += compact[base_j + seg], j ascending.
+      if (a.ma == 1 && nseg == 1) {
+        const int32_t sg0 = sc_seg[0];
+        while (true) {
+          int jj[4];
+          bool ok[4];
+          float val[4];
 #pragma unroll
-      for (int w = 0; w < W; ++w) {
-        uint32_t bits = U[w];
-        while (bits) {
-          const int j = w * 32 + (__ffs(bits) - 1);
-          bits &= bits - 1;
-          const int v = j / a.ma;
-          if (v != cur_v) {  // views ascend with j: flush the previous view's best
-            acc += static_cast<double>(best);
-            best = 0.f;
-            cur_v = v;
-          }
-          const int cj = scl[j];
-          int32_t sg = -1;
+          for (int t = 0; t < 4; ++t) {
+            ok[t] = false;
+            jj[t] = 0;
 #pragma unroll
-          for (int t = 0; t < GR_SEGC; ++t)
-            if (sc_cell[t] == cj) sg = sc_seg[t];
-          for (int t = GR_SEGC; sg < 0 && t < nseg; ++t) {
-            const int32_t x = a.shape_seg[g0 + t];
-            if (a.seg_cell[x] == cj) sg = x;
+            for (int w = 0; w < W; ++w) {
+              if (!ok[t] && U[w]) {
+                jj[t] = w * 32 + (__ffs(U[w]) - 1);
+                U[w] &= U[w] - 1u;
+                ok[t] = true;
+              }
+            }
           }
-          best = fmaxf(best, a.out[sb[j] + sg]);
+          if (!ok[0]) break;
+#pragma unroll
+          for (int t = 0; t < 4; ++t) val[t] = ok[t] ? a.out[sb[jj[t]] + sg0] : 0.f;
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            if (ok[t]) acc += static_cast<double>(val[t]);
+          if (!ok[3]) break;
         }
+      }
+      while (true) {
+        int jj[4];
+        bool ok[4];
+        float val[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          ok[t] = false;
+          jj[t] = 0;
+#pragma unroll
+          for (int w = 0; w < W; ++w) {
+            if (!ok[t] && U[w]) {
+              jj[t] = w * 32 + (__ffs(U[w]) - 1);
+              U[w] &= U[w] - 1u;
+              ok[t] = true;
+            }
+          }
+        }
+        if (!ok[0]) break;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          val[t] = 0.f;
+          if (ok[t]) {
+            const int cj = scl[jj[t]];
+            int32_t sg = -1;
+#pragma unroll
+            for (int q = 0; q < GR_SEGC; ++q)
+              if (sc_cell[q] == cj) sg = sc_seg[q];
+            for (int q = GR_SEGC; sg < 0 && q < nseg; ++q)
+              if (a.shape_seg_cell[g0 + q] == cj) sg = a.shape_seg[g0 + q];
+            val[t] = a.out[sb[jj[t]] + sg];
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          if (ok[t]) {
+            const int v = s_view[jj[t]];
+            if (v != cur_v) {  // views ascend with j: flush the previous view's best
+              acc += static_cast<double>(best);
+              best = 0.f;
+              cur_v = v;
+            }
+            best = fmaxf(best, val[t]);
+          }
+        }
+        if (!ok[3]) break;
       }
       acc += static_cast<double>(best);
       const double denom = static_cast<double>(a.vq ? a.vq[b] : a.V);
-      const double score = acc / denom;
+      const double score = acc == 0.0 ? 0.0 : acc / denom;
       if (a.scores) a.scores[static_cast<int64_t>(b) * a.n_local + s] = score;
       s_sc[g * a.rs + i] = score;
     }
@@ -599,24 +705,43 @@ __global__ void __launch_bounds__(GR_THREADS) fif_gather_reduce_kernel(GatherArg
   if (warp >= nb) return;
   const int g = warp, b = b0 + g;
   const int ck = a.cand_k;
-  Cand lst[RED_MAXK];
+  double ls[RED_MAXK];
+  int32_t lo_[RED_MAXK];
 #pragma unroll
-  for (int t = 0; t < RED_MAXK; ++t) lst[t] = Cand{-INFINITY, -1};
+  for (int t = 0; t < RED_MAXK; ++t) {
+    ls[t] = -INFINITY;
+    lo_[t] = -1;
+  }
   for (int i = lane; i < n; i += 32) {  // ordinals ascend within a lane
-    Cand x{s_sc[g * a.rs + i], static_cast<int32_t>(a.ord_base + lo + i)};
+    double xs = s_sc[g * a.rs + i];
+    int32_t xo = static_cast<int32_t>(a.ord_base + lo + i);
+    double lastv = ls[0];  // ls[ck - 1] without dynamic register indexing
+    int32_t lasto = lo_[0];
+#pragma unroll
+    for (int t = 1; t < RED_MAXK; ++t)
+      if (t == ck - 1) {
+        lastv = ls[t];
+        lasto = lo_[t];
+      }
+    if (!cand_better(xs, xo, lastv, lasto)) continue;
 #pragma unroll
     for (int t = 0; t < RED_MAXK; ++t) {
-      if (t < ck && cand_better(x.s, x.o, lst[t].s, lst[t].o)) {
-        const Cand y = lst[t];
-        lst[t] = x;
-        x = y;
+      if (t < ck && cand_better(xs, xo, ls[t], lo_[t])) {
+        const double ys = ls[t];
+        const int32_t yo = lo_[t];
+        ls[t] = xs;
+        lo_[t] = xo;
+        xs = ys;
+        xo = yo;
       }
     }
   }
   const int64_t at = (static_cast<int64_t>(b) * a.n_ranges + rg) * ck;
-  for (int r = 0; r < ck; ++r) {
-    double bs = lst[0].s;
-    int32_t bo = lst[0].o;
+#pragma unroll
+  for (int r = 0; r < RED_MAXK; ++r) {
+    if (r >= ck) break;
+    double bs = ls[0];
+    int32_t bo = lo_[0];
     int bl = lane;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
@@ -635,8 +760,12 @@ __global__ void __launch_bounds__(GR_THREADS) fif_gather_reduce_kernel(GatherArg
     }
     if (lane == bl) {  // pop the winner's head
 #pragma unroll
-      for (int t = 0; t + 1 < RED_MAXK; ++t) lst[t] = lst[t + 1];
-      lst[RED_MAXK - 1] = Cand{-INFINITY, -1};
+      for (int t = 0; t + 1 < RED_MAXK; ++t) {
+        ls[t] = ls[t + 1];
+        lo_[t] = lo_[t + 1];
+      }
+      ls[RED_MAXK - 1] = -INFINITY;
+      lo_[RED_MAXK - 1] = -1;
     }
   }
 }
@@ -665,7 +794,6 @@ struct ScoreWs {
   __half* g1;
   __half* g2;
   ProbeRange* rng;
-  uint32_t* mask;  // gather reduce: [B][K][W] probe bit table
   int64_t* slot_base;  // gather reduce: [B * V * ma]
 };
 
@@ -683,12 +811,19 @@ int reduce_rs(int64_t V, int64_t n_local) {
 
 // Mask words of the gather reduce (0: not applicable -> per-range reduce).
 int gather_words(const gift_fif_view* f, int V, int ma) {
-  if (f->shape_seg_off == nullptr || f->shape_seg == nullptr || f->seg_cell == nullptr) return 0;
+  if (f->shape_seg_off == nullptr || f->shape_seg == nullptr || f->shape_seg_cell == nullptr)
+    return 0;
   const int64_t slots = static_cast<int64_t>(V) * ma;
-  if (slots > 128) return 0;
+  if (slots > 128 || f->K > GR_MAXK) return 0;
+  const int W = slots <= 32 ? 1 : slots <= 64 ? 2 : 4;
+  // GIFT_REDUCE=range|gather forces one reduce; by default the gather reduce
+  // serves few slots per query (its per-bit work grows with V * ma, the
+  // per-range tile's with V): measured faster on config 4 (V * ma = 20),
+  // slower on config 2 (V * ma = 128)
   const char* e = getenv("GIFT_REDUCE");
-  if (e != nullptr && e[0] == 'r') return 0;  // GIFT_REDUCE=range forces the per-range reduce
-  return slots <= 32 ? 1 : slots <= 64 ? 2 : 4;
+  if (e != nullptr && e[0] == 'r') return 0;
+  if (e != nullptr && e[0] == 'g') return W;
+  return W == 1 ? W : 0;
 }
 
 bool carve(Arena& ar, const gift_fif_view* f, int64_t nviews, int V, int ma, ScoreWs& w) {
@@ -709,11 +844,10 @@ bool carve(Arena& ar, const gift_fif_view* f, int64_t nviews, int V, int ma, Sco
   w.qws = ar.take<char>(static_cast<int64_t>(w.qws_bytes));
   const int W = gather_words(f, V, ma);
   w.rng = nullptr;
-  w.mask = nullptr;
+  w.slot_base = nullptr;
   if (W > 0) {
-    w.mask = ar.take<uint32_t>((nviews / V) * K * W);
     w.slot_base = ar.take<int64_t>(nprobes);
-    if (!w.mask || !w.slot_base) return false;
+    if (!w.slot_base) return false;
   } else {
     w.rng = ar.take<ProbeRange>(nprobes * cdiv(max64(f->n_local, 1), reduce_rs(V, f->n_local)));
     if (!w.rng) return false;
@@ -811,13 +945,6 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
   GIFT_LAUNCH_CHECK();
   compact_zero_kernel<<<sm_count() * 4, 256, 0, st>>>(w.compact, w.meta);
   GIFT_LAUNCH_CHECK();
-  if (w.mask != nullptr) {
-    const int Wm = gather_words(f, V, ma);
-    GIFT_CUDA_TRY(cudaMemsetAsync(w.mask, 0, sizeof(uint32_t) * B * K * Wm, st));
-    probe_mask_kernel<<<static_cast<unsigned>(cdiv(nprobes, 256)), 256, 0, st>>>(
-        w.cells, nprobes, V * ma, K, Wm, w.mask);
-    GIFT_LAUNCH_CHECK();
-  }
 
   if (use_tc(f)) {
     TcArgs ta;
@@ -887,12 +1014,11 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
   const int W = gather_words(f, V, ma);
   if (W > 0) {
     GatherArgs ga;
-    ga.mask = w.mask;
     ga.cells = w.cells;
     ga.slot_base = w.slot_base;
     ga.shape_seg_off = f->shape_seg_off;
     ga.shape_seg = f->shape_seg;
-    ga.seg_cell = f->seg_cell;
+    ga.shape_seg_cell = f->shape_seg_cell;
     ga.out = w.compact;
     ga.meta = w.meta;
     ga.vq = vq;
@@ -914,20 +1040,24 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
     probe_slot_kernel<<<static_cast<unsigned>(cdiv(nprobes, 256)), 256, 0, st>>>(
         w.cells, w.probe_rank, w.outbase, f->seg_off, nprobes, w.slot_base);
     GIFT_LAUNCH_CHECK();
-    const int smem = ga.G * ga.rs * static_cast<int>(sizeof(double)) +
-                     ga.G * V * ma * static_cast<int>(sizeof(int64_t) + sizeof(int32_t));
+    const int smem = static_cast<int>(gather_smem(ga.G, ga.rs, K, V * ma, W));
     dim3 grid(static_cast<unsigned>(ga.n_ranges), static_cast<unsigned>(cdiv(B, ga.G)));
     if (W == 1) {
+      GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_gather_reduce_kernel<1>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       fif_gather_reduce_kernel<1><<<grid, GR_THREADS, smem, st>>>(ga);
     } else if (W == 2) {
+      GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_gather_reduce_kernel<2>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       fif_gather_reduce_kernel<2><<<grid, GR_THREADS, smem, st>>>(ga);
     } else {
+      GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_gather_reduce_kernel<4>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       fif_gather_reduce_kernel<4><<<grid, GR_THREADS, smem, st>>>(ga);
     }
     GIFT_LAUNCH_CHECK();
     return GIFT_OK;
   }
-  GIFT_REQUIRE(out_scores != nullptr, GIFT_ERR_INVALID, "this index needs dense score output");
   // shape ranges: a [V x rs] f32 view-best tile of <= RED_SMEM bytes per CTA
   const int rs = reduce_rs(V, f->n_local);
   const int n_ranges = static_cast<int>(cdiv(f->n_local, rs));

@@ -161,7 +161,7 @@ class DeviceFif:
         v.feat_lo = None if self.feat_lo is None else self.feat_lo.data_ptr()
         v.shape_seg_off = self.shape_seg_off.data_ptr()
         v.shape_seg = self.shape_seg.data_ptr()
-        v.seg_cell = self.seg_cell.data_ptr()
+        v.shape_seg_cell = self.shape_seg_cell.data_ptr()
         self.view = v
         return v
 
@@ -337,15 +337,18 @@ class DeviceFif:
         self.smax = int(seg_sizes.max().item()) if K else 0
         # shape -> segments (ascending cell) for the gather reduce: stable sort
         # of the segment indices by owner
-        self.seg_cell = torch.repeat_interleave(
+        seg_cell = torch.repeat_interleave(
             torch.arange(K, dtype=torch.int32, device=dev), seg_sizes, output_size=S)
-        if S == 0:
-            self.seg_cell = torch.zeros(1, dtype=torch.int32, device=dev)
         k3 = (self.seg_ord[:S] - self.ord_base).contiguous()
         v3 = torch.arange(S, dtype=torch.int32, device=dev)
         radix_sort_pairs(k3, v3, _bits(n_local), stream)
         self.shape_seg_off = offsets_from_sorted(k3, n_local, stream)  # [n_local+1]
-        self.shape_seg = v3 if S else torch.zeros(1, dtype=torch.int32, device=dev)
+        if S:
+            self.shape_seg = v3
+            self.shape_seg_cell = seg_cell[v3.long()].contiguous()
+        else:
+            self.shape_seg = torch.zeros(1, dtype=torch.int32, device=dev)
+            self.shape_seg_cell = torch.zeros(1, dtype=torch.int32, device=dev)
         self.bind()
 
     # -- host views (reference container attributes) ---------------------

@@ -43,10 +43,7 @@ def main():
     B = w.batch
     batches = [qs[j * B:(j + 1) * B].contiguous() for j in range(max(1, qs.shape[0] // B))]
     for impl in args.reduce.split(","):
-        if impl == "range":
-            os.environ["GIFT_REDUCE"] = "range"
-        else:
-            os.environ.pop("GIFT_REDUCE", None)
+        os.environ["GIFT_REDUCE"] = impl
         profile(eng, w, batches, args.steps, impl, build_s)
         if args.kernels:
             from torch.profiler import ProfilerActivity
@@ -70,7 +67,6 @@ def profile(eng, w, batches, steps, impl, build_s):
     names = ["quantize", "score", "scan", "topk_cand", "act_mean", "sif_query", "topk_final"]
     tot = {n: 0.0 for n in names}
     k2 = min(eng.cfg.k2, eng.n)
-    dense = impl == "range"  # the per-range reduce always writes dense scores
     for it in range(steps + 2):
         Q = batches[it % len(batches)]
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(8)]
@@ -83,7 +79,7 @@ def profile(eng, w, batches, steps, impl, build_s):
         eg.quantize_rows(eng.fa.cb, flat, eng.cfg.ma, nz=nz)
         ev[1].record()
         _, cs, ci = eng.runner.score(eng.fa, Q, eng.cfg.ma, eng.mode, eng.cfg.sigma,
-                                     scan_events=sev, cand_k=k2, dense=dense)
+                                     scan_events=sev, cand_k=k2, dense=False)
         ev[2].record()
         nbr, _ = eg.topk_candidates(cs, ci, k2, positive_only=True)
         ev[3].record()
