@@ -285,6 +285,27 @@ int gift_sif_query(const int64_t* e_off, const int32_t* e_ord,
                    const int32_t* q_cnt, const double* q_norm, int32_t B,
                    int32_t cap, double* out_scores, void* stream);
 
+/* query_sif + the final ranking of index.query (index.py:290-294) without
+ * dense rows: touched shapes only, plus the reference's zero-score fill (self
+ * first, then id-rank order).  Returns the k best by (score desc, tiebreak
+ * asc) exactly like gift_topk_rows over the dense scores.  acc_rows:
+ * n_acc_rows x n_local f64, all zero on entry and on return (caller-owned
+ * scratch).  order[r] = local shape of id rank r (inverse of idrank).
+ * max_touched: an upper bound of the shapes one query can touch (support cap
+ * x the longest S-IF entry). */
+size_t gift_sif_query_topk_ws_bytes(int32_t B, int64_t n_local, int32_t k,
+                                    int64_t max_touched);
+int gift_sif_query_topk(const int64_t* e_off, const int32_t* e_ord,
+                        const double* e_val, const double* norms,
+                        int64_t n_global, int64_t n_local, const int32_t* q_idx,
+                        const double* q_val, const int32_t* q_cnt,
+                        const double* q_norm, int32_t B, int32_t cap,
+                        double* acc_rows, int32_t n_acc_rows,
+                        const int32_t* order, const int32_t* idrank,
+                        const int32_t* self_local, int64_t ord_base, int32_t k,
+                        int64_t max_touched, int32_t* out_idx, double* out_val,
+                        void* ws, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

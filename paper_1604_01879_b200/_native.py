@@ -95,6 +95,10 @@ _SIGS = {
     "gift_sif_permute": (_c_i32, [_c_p, _c_p, _c_p, _c_i64, _c_p, _c_p, _c_p]),
     "gift_sif_query": (_c_i32, [_c_p, _c_p, _c_p, _c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p,
                                 _c_i32, _c_i32, _c_p, _c_p]),
+    "gift_sif_query_topk_ws_bytes": (_c_sz, [_c_i32, _c_i64, _c_i32, _c_i64]),
+    "gift_sif_query_topk": (_c_i32, [_c_p, _c_p, _c_p, _c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p,
+                                     _c_p, _c_i32, _c_i32, _c_p, _c_i32, _c_p, _c_p, _c_p,
+                                     _c_i64, _c_i32, _c_i64, _c_p, _c_p, _c_p, _c_sz, _c_p]),
 }
 
 EXPORTED = tuple(_SIGS)

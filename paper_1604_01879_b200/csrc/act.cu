@@ -296,6 +296,100 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// query_sif + the final ranking (rerank.py:211-230, index.py:290-294) without
+// the dense [B, n] row: a CTA serves queries b = blockIdx.x, + gridDim.x, ...
+// with its own zero-initialised f64 accumulator row in global memory.  Entries
+// are visited in ascending coordinate order with a barrier between entries
+// (every acc[j] is the reference's left-to-right f64 sum); the first touch of
+// j appends it to the query's candidate row.  Before the touched accumulators
+// are finalised and cleared back to zero, one warp adds the zero-score fill
+// the reference's lexsort would rank next: self (tiebreak 0) if untouched,
+// then the first k untouched shapes by id rank.  The rows (score, tiebreak,
+// global ordinal) go to the top-k merge pass, which ranks them exactly like
+// the dense path (touched scores are > 0, so the fill only matters when fewer
+// than k shapes are touched).
+__global__ void __launch_bounds__(256)
+    sif_query_sparse_kernel(const int64_t* __restrict__ e_off, const int32_t* __restrict__ e_ord,
+                            const double* __restrict__ e_val, const double* __restrict__ norms,
+                            int64_t n_global, int64_t n_local, const int32_t* __restrict__ q_idx,
+                            const double* __restrict__ q_val, const int32_t* __restrict__ q_cnt,
+                            const double* __restrict__ q_norm, int B, int cap,
+                            double* __restrict__ acc_rows, const int32_t* __restrict__ order,
+                            const int32_t* __restrict__ idrank, const int32_t* __restrict__ self_local,
+                            int64_t ord_base, int k_fill, int64_t m, double* __restrict__ cs,
+                            uint32_t* __restrict__ ct, int32_t* __restrict__ ci,
+                            int32_t* __restrict__ row_cnt) {
+  __shared__ int s_cnt;
+  double* acc = acc_rows + static_cast<int64_t>(blockIdx.x) * n_local;
+  const int tid = threadIdx.x;
+  for (int b = blockIdx.x; b < B; b += gridDim.x) {
+    if (tid == 0) s_cnt = 0;
+    __syncthreads();
+    const int64_t row = static_cast<int64_t>(b) * m;
+    const int cnt = q_cnt[b];
+    for (int e = 0; e < cnt; ++e) {
+      const int64_t i = q_idx[static_cast<int64_t>(b) * cap + e];
+      if (i < 0 || i >= n_global) continue;
+      const double v = q_val[static_cast<int64_t>(b) * cap + e];
+      const int64_t p0 = e_off[i], p1 = e_off[i + 1];
+      for (int64_t p = p0 + tid; p < p1; p += blockDim.x) {
+        const int32_t j = e_ord[p];
+        const double old = acc[j];
+        if (old == 0.0) ci[row + atomicAdd(&s_cnt, 1)] = j;  // contributions are > 0
+        acc[j] = __dadd_rn(old, fmin(v, e_val[p]));
+      }
+      __syncthreads();
+    }
+    const int T = s_cnt;
+    const int64_t sl = self_local ? static_cast<int64_t>(self_local[b]) : -1;
+    if (tid < 32) {  // zero-score fill, one warp
+      const int lane = tid;
+      int pos = T;
+      if (sl >= 0 && sl < n_local && acc[sl] == 0.0) {
+        if (lane == 0) {
+          cs[row + pos] = 0.0;
+          ct[row + pos] = 0u;
+          ci[row + pos] = static_cast<int32_t>(ord_base + sl);
+        }
+        ++pos;
+      }
+      int nf = 0;
+      for (int64_t r0 = 0; nf < k_fill && r0 < n_local; r0 += 32) {
+        const int64_t r = r0 + lane;
+        int32_t j = -1;
+        bool hit = false;
+        if (r < n_local) {
+          j = order[r];
+          hit = j != sl && acc[j] == 0.0;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, hit);
+        const int before = __popc(bal & ((1u << lane) - 1u));
+        if (hit && nf + before < k_fill) {
+          const int64_t at = row + pos + nf + before;
+          cs[at] = 0.0;
+          ct[at] = 1u + static_cast<uint32_t>(idrank ? static_cast<int64_t>(idrank[j]) : ord_base + j);
+          ci[at] = static_cast<int32_t>(ord_base + j);
+        }
+        nf = min(k_fill, nf + __popc(bal));
+      }
+      if (lane == 0) row_cnt[b] = pos + nf;
+    }
+    __syncthreads();
+    const double qn = q_norm[b];
+    for (int t = tid; t < T; t += blockDim.x) {
+      const int32_t j = ci[row + t];
+      const double a = acc[j];
+      acc[j] = 0.0;
+      cs[row + t] = __ddiv_rn(a, __dsub_rn(__dadd_rn(qn, norms[j]), a));
+      ct[row + t] = j == sl ? 0u
+                            : 1u + static_cast<uint32_t>(idrank ? static_cast<int64_t>(idrank[j])
+                                                                : ord_base + j);
+      ci[row + t] = static_cast<int32_t>(ord_base + j);
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace gift
 
 using namespace gift;
@@ -378,4 +472,39 @@ extern "C" int gift_sif_query(const int64_t* e_off, const int32_t* e_ord, const 
       e_off, e_ord, e_val, norms, n_global, n_local, q_idx, q_val, q_cnt, q_norm, cap, out_scores);
   GIFT_LAUNCH_CHECK();
   return GIFT_OK;
+}
+
+extern "C" int gift_sif_query_topk(const int64_t* e_off, const int32_t* e_ord, const double* e_val,
+                                   const double* norms, int64_t n_global, int64_t n_local,
+                                   const int32_t* q_idx, const double* q_val,
+                                   const int32_t* q_cnt, const double* q_norm, int32_t B,
+                                   int32_t cap, double* acc_rows, int32_t n_acc_rows,
+                                   const int32_t* order, const int32_t* idrank,
+                                   const int32_t* self_local, int64_t ord_base, int32_t k,
+                                   int64_t max_touched, int32_t* out_idx, double* out_val,
+                                   void* ws, size_t ws_bytes, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  GIFT_REQUIRE(k >= 1 && k <= 256, GIFT_ERR_UNSUPPORTED, "k = %d outside [1, 256]", k);
+  GIFT_REQUIRE(n_acc_rows >= 1 && acc_rows != nullptr && order != nullptr, GIFT_ERR_INVALID,
+               "sparse S-IF query needs accumulator rows and the id-rank order");
+  if (B <= 0 || n_local <= 0) return GIFT_OK;
+  const int64_t m = min64(max_touched, n_local) + k + 1;
+  Arena ar(ws, ws_bytes);
+  double* cs = ar.take<double>(static_cast<int64_t>(B) * m);
+  uint32_t* ct = ar.take<uint32_t>(static_cast<int64_t>(B) * m);
+  int32_t* ci = ar.take<int32_t>(static_cast<int64_t>(B) * m);
+  int32_t* cnt = ar.take<int32_t>(B);
+  GIFT_REQUIRE(cs && ct && ci && cnt, GIFT_ERR_CAPACITY, "sparse S-IF workspace too small");
+  const int grid = min(B, n_acc_rows);
+  sif_query_sparse_kernel<<<static_cast<unsigned>(grid), 256, 0, st>>>(
+      e_off, e_ord, e_val, norms, n_global, n_local, q_idx, q_val, q_cnt, q_norm, B, cap, acc_rows,
+      order, idrank, self_local, ord_base, k, m, cs, ct, ci, cnt);
+  GIFT_LAUNCH_CHECK();
+  return topk_rows_from_lists(cs, ct, ci, cnt, B, m, k, 0, out_idx, out_val, st);
+}
+
+extern "C" size_t gift_sif_query_topk_ws_bytes(int32_t B, int64_t n_local, int32_t k,
+                                               int64_t max_touched) {
+  const int64_t m = min64(max_touched, n_local) + k + 1;
+  return static_cast<size_t>(B) * m * 16 + static_cast<size_t>(B) * 4 + 4096;
 }

@@ -181,4 +181,10 @@ int scan_exclusive_i32_to_i64(const int32_t* in, int64_t* out, int64_t n, bool w
 
 int sm_count();
 
+// topk.cu: merge pass over explicit candidate rows (score, tiebreak, ordinal)
+int topk_rows_from_lists(const double* cs, const uint32_t* ct, const int32_t* ci,
+                         const int32_t* counts, int32_t B, int64_t m, int32_t k,
+                         int32_t positive_only, int32_t* out_idx, double* out_val,
+                         cudaStream_t st);
+
 }  // namespace gift

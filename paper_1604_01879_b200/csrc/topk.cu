@@ -71,6 +71,7 @@ struct TopkIn {
   const uint32_t* ct;
   const int32_t* ci;
   int64_t m;
+  const int32_t* counts;  // optional: valid candidates per row (<= m)
 };
 
 struct TopkOut {
@@ -99,7 +100,7 @@ __global__ void __launch_bounds__(TK_THREADS) topk_kernel(const TopkIn in, const
     e1 = min64(in.n, e0 + in.slice_len);
   } else {
     e0 = 0;
-    e1 = in.m;
+    e1 = in.counts ? min64(in.m, static_cast<int64_t>(in.counts[b])) : in.m;
   }
   const double* row = DENSE ? in.scores + static_cast<int64_t>(b) * in.n : nullptr;
   const int64_t self = (DENSE && in.self_local) ? static_cast<int64_t>(in.self_local[b]) : -1;
@@ -267,9 +268,39 @@ static int launch_topk(const double* scores, int B, int64_t n, int k, const int3
   return GIFT_OK;
 }
 
+// Best k of explicit (score, tiebreak, global ordinal) rows with per-row
+// counts: the merge pass of the dense top-k (used by the sparse S-IF query).
+int topk_rows_from_lists(const double* cs, const uint32_t* ct, const int32_t* ci,
+                         const int32_t* counts, int32_t B, int64_t m, int32_t k,
+                         int32_t positive_only, int32_t* out_idx, double* out_val,
+                         cudaStream_t st) {
+  GIFT_REQUIRE(k >= 1 && k <= 256, GIFT_ERR_UNSUPPORTED, "k = %d outside [1, 256]", k);
+  if (B <= 0) return GIFT_OK;
+  const int smem = sizeof(TopkSmem<256>);
+  GIFT_CUDA_TRY(cudaFuncSetAttribute(topk_kernel<256, false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  TopkIn in{};
+  in.cs = cs;
+  in.ct = ct;
+  in.ci = ci;
+  in.m = m;
+  in.counts = counts;
+  TopkOut out{};
+  out.k = k;
+  out.positive_only = positive_only;
+  out.final_out = 1;
+  out.nslices = 1;
+  out.out_idx = out_idx;
+  out.out_val = out_val;
+  topk_kernel<256, false><<<dim3(1, B), TK_THREADS, smem, st>>>(in, out);
+  GIFT_LAUNCH_CHECK();
+  return GIFT_OK;
+}
+
 }  // namespace gift
 
 using namespace gift;
+
 
 extern "C" size_t gift_topk_ws_bytes(int32_t B, int64_t n, int32_t k) {
   int64_t nsl = min64(cdiv(2 * 148, max64(B, 1)), cdiv(max64(n, 1), 512));

@@ -603,6 +603,51 @@ class DeviceSif:
                  nat.ptr(e_ord), nat.ptr(e_val), _sp(stream))
         return cls(e_off, e_ord[:nnz], e_val[:nnz], final.norm.clone(), n_global, ord_base)
 
+    @property
+    def max_list(self) -> int:
+        """Longest S-IF entry (bounds the shapes one query entry touches)."""
+        ml = getattr(self, "_max_list", None)
+        if ml is None:
+            ml = int((self.e_off[1:] - self.e_off[:-1]).max().item()) if self.n_global else 0
+            self._max_list = ml
+        return ml
+
+    def _acc_rows(self, B: int) -> torch.Tensor:
+        """Zeroed f64 accumulator rows for the sparse query (kept zero by the
+        kernel): up to 2 per SM, within ~2.5 GB."""
+        sms = torch.cuda.get_device_properties(self.norms.device).multi_processor_count
+        want = max(1, min(B, 2 * sms, (2_500_000_000 // 8) // max(self.n_local, 1)))
+        acc = getattr(self, "_acc", None)
+        if acc is None or acc.shape[0] < want:
+            acc = torch.zeros((want, max(self.n_local, 1)), dtype=torch.float64,
+                              device=self.norms.device)
+            self._acc = acc
+        return acc
+
+    def query_topk(self, q: ActRows, k: int, order: torch.Tensor, idrank: torch.Tensor | None,
+                   self_local: torch.Tensor | None = None, stream=None):
+        """Sparse query_sif + final top-k (index.py:290-294): identical to
+        topk_rows(self.query(q), k, idrank=..., self_local=...) without the
+        dense [B, n] rows."""
+        B = q.n
+        dev = q.idx.device
+        idx = torch.empty((B, k), dtype=torch.int32, device=dev)
+        val = torch.empty((B, k), dtype=torch.float64, device=dev)
+        if B == 0:
+            return idx, val
+        bound = q.cap * self.max_list
+        lib = nat.lib()
+        ws = nat.workspace("sif_topk").get(
+            lib.gift_sif_query_topk_ws_bytes(B, self.n_local, k, bound))
+        acc = self._acc_rows(B)
+        nat.call("gift_sif_query_topk", nat.ptr(self.e_off), nat.ptr(self.e_ord),
+                 nat.ptr(self.e_val), nat.ptr(self.norms), self.n_global, self.n_local,
+                 nat.ptr(q.idx), nat.ptr(q.val), nat.ptr(q.cnt), nat.ptr(q.norm), B, q.cap,
+                 nat.ptr(acc), acc.shape[0], nat.ptr(order), nat.ptr(idrank),
+                 nat.ptr(self_local), self.ord_base, k, bound, nat.ptr(idx), nat.ptr(val),
+                 nat.ptr(ws), ws.numel(), _sp(stream))
+        return idx, val
+
     def query(self, q: ActRows, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         """rerank.py:211-230 for a batch -> dense f64 [B, n_local]."""
         B = q.n

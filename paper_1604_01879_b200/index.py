@@ -146,6 +146,7 @@ class QueryEngine:
         rank = np.empty(self.n, dtype=np.int32)
         rank[np.asarray(order, dtype=np.int64)] = np.arange(self.n, dtype=np.int32)
         self.idrank = torch.from_numpy(rank).to(nat.device())
+        self.order = torch.from_numpy(np.asarray(order, dtype=np.int32)).to(nat.device())
         self.ord_of = {sid: i for i, sid in enumerate(bundle.shape_ids)}
         self.runner = eg.ScoreRunner()
         self.mode = mt.sim_mode(cfg.similarity)
@@ -161,6 +162,10 @@ class QueryEngine:
 
     def rerank(self, sa, sb, stream=None):
         """index.py:249-258 for a batch of channel scores -> dense f64."""
+        return self.sif.query(self.rerank_act(sa, sb, stream), stream=stream)
+
+    def rerank_act(self, sa, sb, stream=None) -> eg.ActRows:
+        """The query-time context activation of rerank_scores (index.py:249-256)."""
         k2 = min(self.cfg.k2, self.n)
         na, _ = eg.topk_rows(sa, k2, positive_only=True, stream=stream)
         nb = na if sb is sa else eg.topk_rows(sb, k2, positive_only=True, stream=stream)[0]
@@ -170,7 +175,7 @@ class QueryEngine:
         else:
             fb = eg.act_mean(self.raw_b, na, stream=stream)
             final = eg.act_aggregate(fa, fb, self.cfg.alpha, stream=stream)
-        return self.sif.query(final, stream=stream)
+        return final
 
     def run(self, Qa, Qb=None, top_k=10, rerank=True, self_local=None, vq=None, vqb=None,
             stream=None, scan_events=None):
@@ -184,13 +189,11 @@ class QueryEngine:
                                           cand_k=k2, dense=False)
             nbr, _ = eg.topk_candidates(cs, ci, k2, positive_only=True, stream=stream)
             fa = eg.act_mean(self.raw_a, nbr, stream=stream)
-            final = self.sif.query(fa, stream=stream)
-            k = min(top_k, self.n)
-            return eg.topk_rows(final, k, idrank=self.idrank, self_local=self_local, stream=stream)
+            return self._sif_rank(fa, top_k, self_local, stream)
         sa, sb = self.scores(Qa, Qb, vq, vqb, stream, scan_events)
         if rerank:
-            final = self.rerank(sa, sb, stream)
-        elif sb is sa:
+            return self._sif_rank(self.rerank_act(sa, sb, stream), top_k, self_local, stream)
+        if sb is sa:
             final = sa  # np.mean([s, s], axis=0) == s exactly
         else:
             final = (sa + sb) / 2.0
@@ -206,9 +209,16 @@ class QueryEngine:
         nbr = torch.where(q_val[:, :k2] > 0, q_idx[:, :k2],
                           torch.full_like(q_idx[:, :k2], -1)).to(torch.int32).contiguous()
         fa = eg.act_mean(self.raw_a, nbr, stream=stream)
-        final = self.sif.query(fa, stream=stream)
-        return eg.topk_rows(final, min(top_k, self.n), idrank=self.idrank,
-                            self_local=self_local, stream=stream)
+        return self._sif_rank(fa, top_k, self_local, stream)
+
+    def _sif_rank(self, q: eg.ActRows, top_k, self_local=None, stream=None):
+        """S-IF query + final ranking (index.py:290-299): sparse over the
+        touched shapes for k <= 256, else the dense row + top-k."""
+        k = min(top_k, self.n)
+        if k <= 256:
+            return self.sif.query_topk(q, k, self.order, self.idrank, self_local, stream=stream)
+        final = self.sif.query(q, stream=stream)
+        return eg.topk_rows(final, k, idrank=self.idrank, self_local=self_local, stream=stream)
 
     def results(self, idx_row, val_row):
         ids, labels = self.b.shape_ids, self.b.labels

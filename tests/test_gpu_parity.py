@@ -4,6 +4,7 @@ golden vectors and the CPU oracle on the same seeded inputs."""
 import io
 import os
 import tempfile
+import types
 
 import numpy as np
 import pytest
@@ -426,3 +427,35 @@ def test_gather_reduce_equals_range_reduce(V, ma, K, monkeypatch):
         assert s is None
         nbr, _ = eg.topk_candidates(cs, ci, 4, positive_only=True)
         np.testing.assert_array_equal(nbr.cpu().numpy(), got["gather", "cosine"][1])
+
+
+@pytest.mark.parametrize("k", [1, 10, 100, 256])
+def test_sparse_sif_ranking_equals_dense(k):
+    """Sparse S-IF query + ranking (touched shapes + zero-score fill) is
+    identical to top-k over the dense query_sif rows: shuffled id ranks,
+    self inside / outside the touched set, an empty query support (pure
+    fill), fewer touched shapes than k; repeated calls (scratch re-zeroed)."""
+    rng = np.random.default_rng(k)
+    N, B = 500, 37
+    acts = []
+    for j in range(N):
+        idx = np.sort(rng.choice(N, size=rng.integers(1, 6), replace=False))
+        val = rng.random(len(idx)) + 0.01
+        acts.append(types.SimpleNamespace(indices=idx, values=val, norm=float(np.sum(val))))
+    raw = eg.ActRows.from_host(acts, 5)
+    sif = eg.DeviceSif.build(raw, N)
+    nbr = torch.from_numpy(rng.integers(-1, N, size=(B, 4)).astype(np.int32)).to(dev())
+    nbr[0] = -1  # empty support: zero-score fill only
+    q = eg.act_mean(raw, nbr)
+    rank = rng.permutation(N).astype(np.int32)
+    idrank = torch.from_numpy(rank).to(dev())
+    order = torch.from_numpy(np.argsort(rank).astype(np.int32)).to(dev())
+    self_local = torch.from_numpy(rng.integers(0, N, size=B).astype(np.int32)).to(dev())
+    self_local[1] = nbr[1, 0].clamp(min=0)  # self likely touched
+    kk = min(k, N)
+    di, dv = eg.topk_rows(sif.query(q), kk, idrank=idrank, self_local=self_local)
+    for _ in range(2):
+        si, sv = sif.query_topk(q, kk, order, idrank, self_local)
+        np.testing.assert_array_equal(si.cpu().numpy(), di.cpu().numpy())
+        np.testing.assert_array_equal(sv.cpu().numpy(), dv.cpu().numpy())
+    assert float(sif._acc.abs().sum()) == 0.0

@@ -85,9 +85,8 @@ def profile(eng, w, batches, steps, impl, build_s):
         ev[3].record()
         fa = eg.act_mean(eng.raw_a, nbr)
         ev[4].record()
-        final = eng.sif.query(fa)
         ev[5].record()
-        eg.topk_rows(final, min(w.top_k, eng.n), idrank=eng.idrank)
+        eng._sif_rank(fa, w.top_k)  # sparse S-IF query + final ranking
         ev[6].record()
         torch.cuda.synchronize()
         if it < 2:
