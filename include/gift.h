@@ -82,6 +82,7 @@ typedef struct gift_fif_view {
   const int64_t* shape_seg_off; /* [n_local+1] segments of each local shape   */
   const int32_t* shape_seg;     /* [S] global segment index, ascending cell   */
   const int32_t* shape_seg_cell;/* [S] cell of segment shape_seg[g]           */
+  int64_t max_cell_segments;    /* max over cells of its segment count         */
 } gift_fif_view;
 
 /* ---- library ---- */

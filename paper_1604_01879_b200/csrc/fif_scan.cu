@@ -488,10 +488,13 @@ struct GatherArgs {
   const int64_t* shape_seg_off;  // [n_local + 1]
   const int32_t* shape_seg;      // [S] global segment index, ascending cell
   const int32_t* shape_seg_cell; // [S] its cell
+  const int64_t* seg_off;        // [K + 1]
+  const int32_t* seg_ord;        // [S] global shape ordinal of each segment
   const float* out;              // compact (probe x segment) best similarities
   const int64_t* meta;
   const int32_t* vq;
   int B, V, ma, K, rs, n_ranges, G;
+  int chunk, nchunk;             // owner reduce: segments per CTA, chunks per cell
   int64_t n_local, ord_base;
   double* scores;                // [B][n_local] or null (candidates only)
   int cand_k;
@@ -510,238 +513,252 @@ size_t gather_smem(int G, int rs, int K, int slots, int W) {
          + static_cast<size_t>(slots) + 16;        // view of each slot (u8)
 }
 
+// Shared-memory probe tables of G queries (layout of gather_smem after the
+// staged scores).
+struct GrTabs {
+  int64_t* base;   // [G][slots]
+  int32_t* cell;   // [G][slots]
+  uint32_t* set;   // [G][slots][W]
+  uint32_t* bm;    // [G][kw]
+  uint16_t* pre;   // [G][kw]
+  uint8_t* view;   // [slots]
+  int kw, slots;
+};
+
 template <int W>
-__global__ void __launch_bounds__(GR_THREADS) fif_gather_reduce_kernel(GatherArgs a) {
-  extern __shared__ __align__(16) double s_sc[];  // [G][rs]
-  if (a.meta[M_OVERFLOW]) return;
-  const int rg = blockIdx.x;
-  const int G = a.G;
-  const int b0 = blockIdx.y * G;
-  const int nb = min(G, a.B - b0);
-  const int64_t lo = static_cast<int64_t>(rg) * a.rs;
-  const int n = static_cast<int>(min64(lo + a.rs, a.n_local) - lo);
-  const int slots = a.V * a.ma;
-  const int kw = (a.K + 31) >> 5;
-  int64_t* s_base = reinterpret_cast<int64_t*>(s_sc + G * a.rs);  // [G][slots]
-  int32_t* s_cell = reinterpret_cast<int32_t*>(s_base + G * slots); // [G][slots]
-  uint32_t* s_set = reinterpret_cast<uint32_t*>(s_cell + G * slots); // [G][slots][W]
-  uint32_t* s_bm = s_set + G * slots * W;                            // [G][kw]
-  uint16_t* s_pre = reinterpret_cast<uint16_t*>(s_bm + G * kw);      // [G][kw]
-  uint8_t* s_view = reinterpret_cast<uint8_t*>(s_pre + G * kw);       // [slots] view of a slot
-  for (int i = threadIdx.x; i < slots; i += GR_THREADS) s_view[i] = static_cast<uint8_t>(i / a.ma);
-  // ---- per-CTA probe tables of the G queries
-  for (int i = threadIdx.x; i < G * kw; i += GR_THREADS) s_bm[i] = 0u;
-  for (int i = threadIdx.x; i < G * slots * W; i += GR_THREADS) s_set[i] = 0u;
-  for (int i = threadIdx.x; i < G * slots; i += GR_THREADS) {
-    const int g = i / slots;
-    const bool live = g < nb;
+__device__ __forceinline__ GrTabs carve_tabs(double* after_scores, int G, int slots, int K) {
+  GrTabs t;
+  t.slots = slots;
+  t.kw = (K + 31) >> 5;
+  t.base = reinterpret_cast<int64_t*>(after_scores);
+  t.cell = reinterpret_cast<int32_t*>(t.base + G * slots);
+  t.set = reinterpret_cast<uint32_t*>(t.cell + G * slots);
+  t.bm = t.set + G * slots * W;
+  t.pre = reinterpret_cast<uint16_t*>(t.bm + G * t.kw);
+  t.view = reinterpret_cast<uint8_t*>(t.pre + G * t.kw);
+  return t;
+}
+
+// Block-wide: fold the probes of queries b0 .. b0+nb-1 into the tables.
+template <int W>
+__device__ void build_tabs(const GatherArgs& a, const GrTabs& t, int G, int b0, int nb) {
+  const int slots = t.slots, kw = t.kw;
+  for (int i = threadIdx.x; i < slots; i += blockDim.x) t.view[i] = static_cast<uint8_t>(i / a.ma);
+  for (int i = threadIdx.x; i < G * kw; i += blockDim.x) t.bm[i] = 0u;
+  for (int i = threadIdx.x; i < G * slots * W; i += blockDim.x) t.set[i] = 0u;
+  for (int i = threadIdx.x; i < G * slots; i += blockDim.x) {
+    const bool live = i / slots < nb;
     const int64_t p = static_cast<int64_t>(b0) * slots + i;
-    s_base[i] = live ? a.slot_base[p] : 0;
-    s_cell[i] = live ? a.cells[p] : -1;
+    t.base[i] = live ? a.slot_base[p] : 0;
+    t.cell[i] = live ? a.cells[p] : -1;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < G * slots; i += GR_THREADS) {
-    const int c = s_cell[i];
-    if (c >= 0) atomicOr(s_bm + (i / slots) * kw + (c >> 5), 1u << (c & 31));
+  for (int i = threadIdx.x; i < G * slots; i += blockDim.x) {
+    const int c = t.cell[i];
+    if (c >= 0) atomicOr(t.bm + (i / slots) * kw + (c >> 5), 1u << (c & 31));
   }
   __syncthreads();
   {  // exclusive prefix popcounts of each query's bitmap words (one warp per query)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int g = warp; g < G; g += GR_THREADS / 32) {
+    for (int g = warp; g < G; g += blockDim.x / 32) {
       int carry = 0;
       for (int w0 = 0; w0 < kw; w0 += 32) {
         const int w = w0 + lane;
-        const int c = w < kw ? __popc(s_bm[g * kw + w]) : 0;
+        const int c = w < kw ? __popc(t.bm[g * kw + w]) : 0;
         int incl = c;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const int y = __shfl_up_sync(0xffffffffu, incl, o);
           if (lane >= o) incl += y;
         }
-        if (w < kw) s_pre[g * kw + w] = static_cast<uint16_t>(carry + incl - c);
+        if (w < kw) t.pre[g * kw + w] = static_cast<uint16_t>(carry + incl - c);
         carry += __shfl_sync(0xffffffffu, incl, 31);
       }
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < G * slots; i += GR_THREADS) {
-    const int c = s_cell[i];
+  for (int i = threadIdx.x; i < G * slots; i += blockDim.x) {
+    const int c = t.cell[i];
     if (c < 0) continue;
     const int g = i / slots, j = i - g * slots;
-    const uint32_t word = s_bm[g * kw + (c >> 5)];
-    const int rank = s_pre[g * kw + (c >> 5)] + __popc(word & ((1u << (c & 31)) - 1u));
-    atomicOr(s_set + (g * slots + rank) * W + (j >> 5), 1u << (j & 31));
+    const uint32_t word = t.bm[g * kw + (c >> 5)];
+    const int rank = t.pre[g * kw + (c >> 5)] + __popc(word & ((1u << (c & 31)) - 1u));
+    atomicOr(t.set + (g * slots + rank) * W + (j >> 5), 1u << (j & 31));
   }
   __syncthreads();
-  // ---- one thread per shape, G queries each
-  for (int i = threadIdx.x; i < n; i += GR_THREADS) {
-    const int64_t s = lo + i;
-    const int64_t g0 = a.shape_seg_off[s];
-    const int nseg = static_cast<int>(a.shape_seg_off[s + 1] - g0);
-    int sc_cell[GR_SEGC];
-    int32_t sc_seg[GR_SEGC];
+}
+
+struct ShapeSegs {
+  int64_t g0;
+  int nseg;
+  int cell[GR_SEGC];
+  int32_t seg[GR_SEGC];
+};
+
+__device__ __forceinline__ ShapeSegs load_segs(const GatherArgs& a, int64_t s) {
+  ShapeSegs h;
+  h.g0 = a.shape_seg_off[s];
+  h.nseg = static_cast<int>(a.shape_seg_off[s + 1] - h.g0);
 #pragma unroll
-    for (int j = 0; j < GR_SEGC; ++j) {
-      sc_seg[j] = j < nseg ? a.shape_seg[g0 + j] : 0;
-      sc_cell[j] = j < nseg ? a.shape_seg_cell[g0 + j] : -1;
-    }
-    for (int g = 0; g < nb; ++g) {
-      const int b = b0 + g;
-      const uint32_t* bm = s_bm + g * kw;
-      const uint16_t* pre = s_pre + g * kw;
-      const uint32_t* set = s_set + g * slots * W;
-      uint32_t U[W];
+  for (int j = 0; j < GR_SEGC; ++j) {
+    h.seg[j] = j < h.nseg ? a.shape_seg[h.g0 + j] : 0;
+    h.cell[j] = j < h.nseg ? a.shape_seg_cell[h.g0 + j] : -1;
+  }
+  return h;
+}
+
+__device__ __forceinline__ bool probed(const GrTabs& t, int g, int c) {
+  return (t.bm[g * t.kw + (c >> 5)] >> (c & 31)) & 1u;
+}
+
+// f64 sum over the views (ascending) of the best similarity over the view's
+// ma slots whose cell holds a segment of the shape: the reference's
+// `total += view_best` (matching.py:153-161) for one (query g, shape).
+template <int W>
+__device__ __forceinline__ double pair_acc(const GatherArgs& a, const GrTabs& t, int g,
+                                           const ShapeSegs& h) {
+  const int kw = t.kw, slots = t.slots;
+  const uint32_t* bm = t.bm + g * kw;
+  const uint16_t* pre = t.pre + g * kw;
+  const uint32_t* set = t.set + g * slots * W;
+  uint32_t U[W];
 #pragma unroll
-      for (int w = 0; w < W; ++w) U[w] = 0u;
+  for (int w = 0; w < W; ++w) U[w] = 0u;
 #pragma unroll
-      for (int j = 0; j < GR_SEGC + 1; ++j) {
-        // j < GR_SEGC: cached segment j; j == GR_SEGC: the uncached rest
-        const int jend = j < GR_SEGC ? min(j + 1, nseg) : nseg;
-        for (int jj = j; jj < jend; ++jj) {
-        const int c = j < GR_SEGC ? sc_cell[j] : a.shape_seg_cell[g0 + jj];
-        const uint32_t word = bm[c >> 5];
-        if ((word >> (c & 31)) & 1u) {
-          const int rank = pre[c >> 5] + __popc(word & ((1u << (c & 31)) - 1u));
+  for (int j = 0; j < GR_SEGC + 1; ++j) {
+    // j < GR_SEGC: cached segment j; j == GR_SEGC: the uncached rest
+    const int jend = j < GR_SEGC ? min(j + 1, h.nseg) : h.nseg;
+    for (int jj = j; jj < jend; ++jj) {
+      const int c = j < GR_SEGC ? h.cell[j] : a.shape_seg_cell[h.g0 + jj];
+      const uint32_t word = bm[c >> 5];
+      if ((word >> (c & 31)) & 1u) {
+        const int rank = pre[c >> 5] + __popc(word & ((1u << (c & 31)) - 1u));
 #pragma unroll
-          for (int w = 0; w < W; ++w) U[w] |= set[rank * W + w];
-        }
-        }
+        for (int w = 0; w < W; ++w) U[w] |= set[rank * W + w];
       }
-      const int64_t* sb = s_base + g * slots;
-      const int32_t* scl = s_cell + g * slots;
-      double acc = 0.0;
-      float best = 0.f;
-      int cur_v = -1;
-      // set bits in ascending order, four at a time: the four compact loads
-      // are independent (memory-level parallelism), the view fold is serial.
-      // Fast path: ma == 1 and a single segment (every bit is its own view in
-      // the shape's only cell) -> acc += compact[base_j + seg], j ascending.
-      if (a.ma == 1 && nseg == 1) {
-        const int32_t sg0 = sc_seg[0];
-        while (true) {
-          int jj[4];
-          bool ok[4];
-          float val[4];
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            ok[t] = false;
-            jj[t] = 0;
-#pragma unroll
-            for (int w = 0; w < W; ++w) {
-              if (!ok[t] && U[w]) {
-                jj[t] = w * 32 + (__ffs(U[w]) - 1);
-                U[w] &= U[w] - 1u;
-                ok[t] = true;
-              }
-            }
-          }
-          if (!ok[0]) break;
-#pragma unroll
-          for (int t = 0; t < 4; ++t) val[t] = ok[t] ? a.out[sb[jj[t]] + sg0] : 0.f;
-#pragma unroll
-          for (int t = 0; t < 4; ++t)
-            if (ok[t]) acc += static_cast<double>(val[t]);
-          if (!ok[3]) break;
-        }
-      }
-      while (true) {
-        int jj[4];
-        bool ok[4];
-        float val[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          ok[t] = false;
-          jj[t] = 0;
-#pragma unroll
-          for (int w = 0; w < W; ++w) {
-            if (!ok[t] && U[w]) {
-              jj[t] = w * 32 + (__ffs(U[w]) - 1);
-              U[w] &= U[w] - 1u;
-              ok[t] = true;
-            }
-          }
-        }
-        if (!ok[0]) break;
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          val[t] = 0.f;
-          if (ok[t]) {
-            const int cj = scl[jj[t]];
-            int32_t sg = -1;
-#pragma unroll
-            for (int q = 0; q < GR_SEGC; ++q)
-              if (sc_cell[q] == cj) sg = sc_seg[q];
-            for (int q = GR_SEGC; sg < 0 && q < nseg; ++q)
-              if (a.shape_seg_cell[g0 + q] == cj) sg = a.shape_seg[g0 + q];
-            val[t] = a.out[sb[jj[t]] + sg];
-          }
-        }
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          if (ok[t]) {
-            const int v = s_view[jj[t]];
-            if (v != cur_v) {  // views ascend with j: flush the previous view's best
-              acc += static_cast<double>(best);
-              best = 0.f;
-              cur_v = v;
-            }
-            best = fmaxf(best, val[t]);
-          }
-        }
-        if (!ok[3]) break;
-      }
-      acc += static_cast<double>(best);
-      const double denom = static_cast<double>(a.vq ? a.vq[b] : a.V);
-      const double score = acc == 0.0 ? 0.0 : acc / denom;
-      if (a.scores) a.scores[static_cast<int64_t>(b) * a.n_local + s] = score;
-      s_sc[g * a.rs + i] = score;
     }
   }
-  if (a.cand_k <= 0) return;
-  __syncthreads();
-  // one warp per query: lanes keep a sorted best-cand_k of a strided slice,
-  // then cand_k rounds of warp argmax (score desc, ordinal asc)
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp >= nb) return;
-  const int g = warp, b = b0 + g;
-  const int ck = a.cand_k;
-  double ls[RED_MAXK];
-  int32_t lo_[RED_MAXK];
+  const int64_t* sb = t.base + g * slots;
+  const int32_t* scl = t.cell + g * slots;
+  double acc = 0.0;
+  float best = 0.f;
+  int cur_v = -1;
+  // set bits in ascending order, four at a time: the four compact loads are
+  // independent (memory-level parallelism), the view fold is serial.
+  // Fast path: ma == 1 and a single segment (every bit is its own view in the
+  // shape's only cell) -> acc += compact[base_j + seg], j ascending.
+  if (a.ma == 1 && h.nseg == 1) {
+    const int32_t sg0 = h.seg[0];
+    while (true) {
+      int jj[4];
+      bool ok[4];
+      float val[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        ok[q] = false;
+        jj[q] = 0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          if (!ok[q] && U[w]) {
+            jj[q] = w * 32 + (__ffs(U[w]) - 1);
+            U[w] &= U[w] - 1u;
+            ok[q] = true;
+          }
+        }
+      }
+      if (!ok[0]) break;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) val[q] = ok[q] ? a.out[sb[jj[q]] + sg0] : 0.f;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (ok[q]) acc += static_cast<double>(val[q]);
+      if (!ok[3]) break;
+    }
+  }
+  while (true) {
+    int jj[4];
+    bool ok[4];
+    float val[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      ok[q] = false;
+      jj[q] = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        if (!ok[q] && U[w]) {
+          jj[q] = w * 32 + (__ffs(U[w]) - 1);
+          U[w] &= U[w] - 1u;
+          ok[q] = true;
+        }
+      }
+    }
+    if (!ok[0]) break;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      val[q] = 0.f;
+      if (ok[q]) {
+        const int cj = scl[jj[q]];
+        int32_t sg = -1;
+#pragma unroll
+        for (int r = 0; r < GR_SEGC; ++r)
+          if (h.cell[r] == cj) sg = h.seg[r];
+        for (int r = GR_SEGC; sg < 0 && r < h.nseg; ++r)
+          if (a.shape_seg_cell[h.g0 + r] == cj) sg = a.shape_seg[h.g0 + r];
+        val[q] = a.out[sb[jj[q]] + sg];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (ok[q]) {
+        const int v = t.view[jj[q]];
+        if (v != cur_v) {  // views ascend with j: flush the previous view's best
+          acc += static_cast<double>(best);
+          best = 0.f;
+          cur_v = v;
+        }
+        best = fmaxf(best, val[q]);
+      }
+    }
+    if (!ok[3]) break;
+  }
+  return acc + static_cast<double>(best);
+}
+
+// Sorted best-ck insertion (score desc, ordinal asc) into per-thread lists.
+__device__ __forceinline__ void cand_insert(double (&ls)[RED_MAXK], int32_t (&lo)[RED_MAXK],
+                                            int ck, double xs, int32_t xo) {
+  double lastv = ls[0];  // ls[ck - 1] without dynamic register indexing
+  int32_t lasto = lo[0];
+#pragma unroll
+  for (int t = 1; t < RED_MAXK; ++t)
+    if (t == ck - 1) {
+      lastv = ls[t];
+      lasto = lo[t];
+    }
+  if (!cand_better(xs, xo, lastv, lasto)) return;
 #pragma unroll
   for (int t = 0; t < RED_MAXK; ++t) {
-    ls[t] = -INFINITY;
-    lo_[t] = -1;
-  }
-  for (int i = lane; i < n; i += 32) {  // ordinals ascend within a lane
-    double xs = s_sc[g * a.rs + i];
-    int32_t xo = static_cast<int32_t>(a.ord_base + lo + i);
-    double lastv = ls[0];  // ls[ck - 1] without dynamic register indexing
-    int32_t lasto = lo_[0];
-#pragma unroll
-    for (int t = 1; t < RED_MAXK; ++t)
-      if (t == ck - 1) {
-        lastv = ls[t];
-        lasto = lo_[t];
-      }
-    if (!cand_better(xs, xo, lastv, lasto)) continue;
-#pragma unroll
-    for (int t = 0; t < RED_MAXK; ++t) {
-      if (t < ck && cand_better(xs, xo, ls[t], lo_[t])) {
-        const double ys = ls[t];
-        const int32_t yo = lo_[t];
-        ls[t] = xs;
-        lo_[t] = xo;
-        xs = ys;
-        xo = yo;
-      }
+    if (t < ck && cand_better(xs, xo, ls[t], lo[t])) {
+      const double ys = ls[t];
+      const int32_t yo = lo[t];
+      ls[t] = xs;
+      lo[t] = xo;
+      xs = ys;
+      xo = yo;
     }
   }
-  const int64_t at = (static_cast<int64_t>(b) * a.n_ranges + rg) * ck;
+}
+
+// Warp: the ck best of the lanes' sorted lists, in order, via ck rounds of
+// argmax; lane 0 receives them in (os, oo).
+__device__ __forceinline__ void warp_select(double (&ls)[RED_MAXK], int32_t (&lo)[RED_MAXK],
+                                            int ck, double* os_out, int32_t* oo_out) {
+  const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int r = 0; r < RED_MAXK; ++r) {
     if (r >= ck) break;
     double bs = ls[0];
-    int32_t bo = lo_[0];
+    int32_t bo = lo[0];
     int bl = lane;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
@@ -755,18 +772,176 @@ __global__ void __launch_bounds__(GR_THREADS) fif_gather_reduce_kernel(GatherArg
       }
     }
     if (lane == 0) {
-      a.cand_s[at + r] = bo >= 0 ? bs : 0.0;
-      a.cand_i[at + r] = bo;
+      os_out[r] = bs;
+      oo_out[r] = bo;
     }
     if (lane == bl) {  // pop the winner's head
 #pragma unroll
       for (int t = 0; t + 1 < RED_MAXK; ++t) {
         ls[t] = ls[t + 1];
-        lo_[t] = lo_[t + 1];
+        lo[t] = lo[t + 1];
       }
       ls[RED_MAXK - 1] = -INFINITY;
-      lo_[RED_MAXK - 1] = -1;
+      lo[RED_MAXK - 1] = -1;
     }
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(GR_THREADS) fif_gather_reduce_kernel(GatherArgs a) {
+  extern __shared__ __align__(16) double s_sc[];  // [G][rs], then the probe tables
+  if (a.meta[M_OVERFLOW]) return;
+  const int rg = blockIdx.x;
+  const int G = a.G;
+  const int b0 = blockIdx.y * G;
+  const int nb = min(G, a.B - b0);
+  const int64_t lo = static_cast<int64_t>(rg) * a.rs;
+  const int n = static_cast<int>(min64(lo + a.rs, a.n_local) - lo);
+  const GrTabs t = carve_tabs<W>(s_sc + G * a.rs, G, a.V * a.ma, a.K);
+  build_tabs<W>(a, t, G, b0, nb);
+  // ---- one thread per shape, G queries each
+  for (int i = threadIdx.x; i < n; i += GR_THREADS) {
+    const int64_t s = lo + i;
+    const ShapeSegs h = load_segs(a, s);
+    for (int g = 0; g < nb; ++g) {
+      const int b = b0 + g;
+      const double acc = pair_acc<W>(a, t, g, h);
+      const double denom = static_cast<double>(a.vq ? a.vq[b] : a.V);
+      const double score = acc == 0.0 ? 0.0 : acc / denom;
+      if (a.scores) a.scores[static_cast<int64_t>(b) * a.n_local + s] = score;
+      s_sc[g * a.rs + i] = score;
+    }
+  }
+  if (a.cand_k <= 0) return;
+  __syncthreads();
+  // one warp per query: lanes keep a sorted best-cand_k of a strided slice
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp >= nb) return;
+  const int g = warp, b = b0 + g;
+  const int ck = a.cand_k;
+  double ls[RED_MAXK];
+  int32_t lo_[RED_MAXK];
+#pragma unroll
+  for (int q = 0; q < RED_MAXK; ++q) {
+    ls[q] = -INFINITY;
+    lo_[q] = -1;
+  }
+  for (int i = lane; i < n; i += 32)  // ordinals ascend within a lane
+    cand_insert(ls, lo_, ck, s_sc[g * a.rs + i], static_cast<int32_t>(a.ord_base + lo + i));
+  double os[RED_MAXK];
+  int32_t oo[RED_MAXK];
+  warp_select(ls, lo_, ck, os, oo);
+  if (lane == 0) {
+    const int64_t at = (static_cast<int64_t>(b) * a.n_ranges + rg) * ck;
+#pragma unroll
+    for (int r = 0; r < RED_MAXK; ++r)
+      if (r < ck) {
+        a.cand_s[at + r] = oo[r] >= 0 ? os[r] : 0.0;
+        a.cand_i[at + r] = oo[r];
+      }
+  }
+}
+
+// Owner reduce: only the shapes a query touches.  CTA (query b, slot j,
+// chunk) serves the chunk-th run of `chunk` segments of cell c_j when j is the
+// query's first slot probing c_j; a thread takes one segment's shape and
+// scores it only if c_j is the first (lowest) of the shape's cells the query
+// probed (its owner), so every touched pair is scored exactly once, with the
+// gather reduce's per-pair sum.  Dense scores (if requested) are zeroed
+// beforehand; candidates: the CTA's best cand_k, rows [b][slots * nchunk].
+template <int W>
+__global__ void __launch_bounds__(GR_THREADS) fif_owner_reduce_kernel(GatherArgs a) {
+  extern __shared__ __align__(16) double s_tab[];
+  __shared__ int s_skip;
+  __shared__ double s_ws[GR_THREADS / 32][RED_MAXK];
+  __shared__ int32_t s_wo[GR_THREADS / 32][RED_MAXK];
+  if (a.meta[M_OVERFLOW]) return;
+  const int slots = a.V * a.ma;
+  const int b = blockIdx.x / slots, j = blockIdx.x - b * slots;
+  const int chunk_id = blockIdx.y;
+  const int ck = a.cand_k;
+  const int64_t cand_at =
+      ((static_cast<int64_t>(b) * slots + j) * a.nchunk + chunk_id) * static_cast<int64_t>(ck);
+  const int c = a.cells[static_cast<int64_t>(b) * slots + j];
+  int64_t k0 = 0, k1 = 0;
+  if (c >= 0) {
+    const int64_t S_c = a.seg_off[c + 1] - a.seg_off[c];
+    k0 = static_cast<int64_t>(chunk_id) * a.chunk;
+    k1 = min64(S_c, k0 + a.chunk);
+  }
+  if (threadIdx.x == 0) s_skip = k0 >= k1;
+  __syncthreads();
+  if (!s_skip) {  // an earlier slot of the query probing the same cell owns it
+    bool dup = false;
+    for (int jj = threadIdx.x; jj < j; jj += GR_THREADS)
+      dup |= a.cells[static_cast<int64_t>(b) * slots + jj] == c;
+    if (__syncthreads_or(dup) && threadIdx.x == 0) s_skip = 1;
+  }
+  __syncthreads();
+  if (s_skip) {
+    if (ck > 0)
+      for (int r = threadIdx.x; r < ck; r += GR_THREADS) {
+        a.cand_s[cand_at + r] = 0.0;
+        a.cand_i[cand_at + r] = -1;
+      }
+    return;
+  }
+  const GrTabs t = carve_tabs<W>(s_tab, 1, slots, a.K);
+  build_tabs<W>(a, t, 1, b, 1);
+  const double denom = static_cast<double>(a.vq ? a.vq[b] : a.V);
+  double ls[RED_MAXK];
+  int32_t lo_[RED_MAXK];
+#pragma unroll
+  for (int q = 0; q < RED_MAXK; ++q) {
+    ls[q] = -INFINITY;
+    lo_[q] = -1;
+  }
+  const int64_t so = a.seg_off[c];
+  for (int64_t k = k0 + threadIdx.x; k < k1; k += GR_THREADS) {
+    const int32_t ord = a.seg_ord[so + k];
+    const int64_t s = ord - a.ord_base;
+    const ShapeSegs h = load_segs(a, s);
+    // owner test: the first of the shape's cells (ascending) the query probed
+    int first = -1;
+#pragma unroll
+    for (int r = 0; r < GR_SEGC; ++r)
+      if (first < 0 && r < h.nseg && probed(t, 0, h.cell[r])) first = h.cell[r];
+    for (int r = GR_SEGC; first < 0 && r < h.nseg; ++r) {
+      const int cc = a.shape_seg_cell[h.g0 + r];
+      if (probed(t, 0, cc)) first = cc;
+    }
+    if (first != c) continue;
+    const double acc = pair_acc<W>(a, t, 0, h);
+    const double score = acc == 0.0 ? 0.0 : acc / denom;
+    if (a.scores) a.scores[static_cast<int64_t>(b) * a.n_local + s] = score;
+    if (ck > 0) cand_insert(ls, lo_, ck, score, ord);
+  }
+  if (ck <= 0) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double os[RED_MAXK];
+  int32_t oo[RED_MAXK];
+  warp_select(ls, lo_, ck, os, oo);
+  if (lane == 0)
+#pragma unroll
+    for (int r = 0; r < RED_MAXK; ++r) {
+      s_ws[warp][r] = r < ck ? os[r] : -INFINITY;
+      s_wo[warp][r] = r < ck ? oo[r] : -1;
+    }
+  __syncthreads();
+  if (warp == 0) {  // merge the warps' lists: lane w < 8 holds warp w's list
+#pragma unroll
+    for (int q = 0; q < RED_MAXK; ++q) {
+      ls[q] = lane < GR_THREADS / 32 ? s_ws[lane][q] : -INFINITY;
+      lo_[q] = lane < GR_THREADS / 32 ? s_wo[lane][q] : -1;
+    }
+    warp_select(ls, lo_, ck, os, oo);
+    if (lane == 0)
+#pragma unroll
+      for (int r = 0; r < RED_MAXK; ++r)
+        if (r < ck) {
+          a.cand_s[cand_at + r] = oo[r] >= 0 ? os[r] : 0.0;
+          a.cand_i[cand_at + r] = oo[r];
+        }
   }
 }
 
@@ -809,21 +984,35 @@ int reduce_rs(int64_t V, int64_t n_local) {
   return static_cast<int>(max64(min64(rs, n_local), 1));
 }
 
-// Mask words of the gather reduce (0: not applicable -> per-range reduce).
+constexpr int OWN_CHUNK = 4096;  // owner reduce: segments per CTA
+
+enum ReduceMode { RM_RANGE = 0, RM_GATHER = 1, RM_OWNER = 2 };
+
+// Mask words of the gather / owner reduce (0: not applicable -> per-range).
 int gather_words(const gift_fif_view* f, int V, int ma) {
   if (f->shape_seg_off == nullptr || f->shape_seg == nullptr || f->shape_seg_cell == nullptr)
     return 0;
   const int64_t slots = static_cast<int64_t>(V) * ma;
   if (slots > 128 || f->K > GR_MAXK) return 0;
-  const int W = slots <= 32 ? 1 : slots <= 64 ? 2 : 4;
-  // GIFT_REDUCE=range|gather forces one reduce; by default the gather reduce
-  // serves few slots per query (its per-bit work grows with V * ma, the
-  // per-range tile's with V): measured faster on config 4 (V * ma = 20),
-  // slower on config 2 (V * ma = 128)
+  return slots <= 32 ? 1 : slots <= 64 ? 2 : 4;
+}
+
+// GIFT_REDUCE=range|gather|owner forces one reduce.  Default: the owner
+// reduce (touched pairs only) for few slots per query (its per-bit work
+// grows with V * ma, the per-range tile's with V): measured faster on
+// config 4 (V * ma = 20), the per-range reduce on config 2 (V * ma = 128).
+int reduce_mode(const gift_fif_view* f, int V, int ma) {
+  const int W = gather_words(f, V, ma);
+  if (W == 0) return RM_RANGE;
   const char* e = getenv("GIFT_REDUCE");
-  if (e != nullptr && e[0] == 'r') return 0;
-  if (e != nullptr && e[0] == 'g') return W;
-  return W == 1 ? W : 0;
+  if (e != nullptr && e[0] == 'r') return RM_RANGE;
+  if (e != nullptr && e[0] == 'g') return RM_GATHER;
+  if (e != nullptr && e[0] == 'o') return RM_OWNER;
+  return W == 1 ? RM_OWNER : RM_RANGE;
+}
+
+int owner_nchunk(const gift_fif_view* f) {
+  return static_cast<int>(max64(1, cdiv(max64(f->max_cell_segments, 1), OWN_CHUNK)));
 }
 
 bool carve(Arena& ar, const gift_fif_view* f, int64_t nviews, int V, int ma, ScoreWs& w) {
@@ -842,10 +1031,9 @@ bool carve(Arena& ar, const gift_fif_view* f, int64_t nviews, int V, int ma, Sco
   w.probe_rank = ar.take<int32_t>(nprobes);
   w.qws_bytes = gift_quantize_ws_bytes(nviews, f->d, K, GIFT_F32);
   w.qws = ar.take<char>(static_cast<int64_t>(w.qws_bytes));
-  const int W = gather_words(f, V, ma);
   w.rng = nullptr;
   w.slot_base = nullptr;
-  if (W > 0) {
+  if (reduce_mode(f, V, ma) != RM_RANGE) {
     w.slot_base = ar.take<int64_t>(nprobes);
     if (!w.slot_base) return false;
   } else {
@@ -887,8 +1075,9 @@ extern "C" int gift_fif_score_ranges(const gift_fif_view* f, int32_t V) {
 }
 
 extern "C" int gift_fif_score_ranges2(const gift_fif_view* f, int32_t V, int32_t ma) {
-  if (gather_words(f, V, ma) > 0)
-    return static_cast<int>(cdiv(max64(f->n_local, 1), gather_rs(f->n_local)));
+  const int mode = reduce_mode(f, V, ma);
+  if (mode == RM_GATHER) return static_cast<int>(cdiv(max64(f->n_local, 1), gather_rs(f->n_local)));
+  if (mode == RM_OWNER) return V * ma * owner_nchunk(f);
   return gift_fif_score_ranges(f, V);
 }
 
@@ -1011,14 +1200,17 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
     if (ev_scan_end) GIFT_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(ev_scan_end), st));
   }
 
-  const int W = gather_words(f, V, ma);
-  if (W > 0) {
+  const int rmode = reduce_mode(f, V, ma);
+  if (rmode != RM_RANGE) {
+    const int W = gather_words(f, V, ma);
     GatherArgs ga;
     ga.cells = w.cells;
     ga.slot_base = w.slot_base;
     ga.shape_seg_off = f->shape_seg_off;
     ga.shape_seg = f->shape_seg;
     ga.shape_seg_cell = f->shape_seg_cell;
+    ga.seg_off = f->seg_off;
+    ga.seg_ord = f->seg_ord;
     ga.out = w.compact;
     ga.meta = w.meta;
     ga.vq = vq;
@@ -1026,20 +1218,48 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
     ga.V = V;
     ga.ma = ma;
     ga.K = K;
-    ga.rs = gather_rs(f->n_local);
-    ga.n_ranges = static_cast<int>(cdiv(f->n_local, ga.rs));
     ga.n_local = f->n_local;
     ga.ord_base = f->ord_base;
     ga.scores = out_scores;
     ga.cand_k = cand_s != nullptr ? cand_k : 0;
     ga.cand_s = cand_s;
     ga.cand_i = cand_i;
-    // queries per CTA: GR_G, fewer when that leaves the GPU under-filled
-    ga.G = GR_G;
-    while (ga.G > 1 && ga.n_ranges * cdiv(B, ga.G) < 8LL * sm_count()) ga.G >>= 1;
     probe_slot_kernel<<<static_cast<unsigned>(cdiv(nprobes, 256)), 256, 0, st>>>(
         w.cells, w.probe_rank, w.outbase, f->seg_off, nprobes, w.slot_base);
     GIFT_LAUNCH_CHECK();
+    if (rmode == RM_OWNER) {
+      ga.G = 1;
+      ga.rs = 0;
+      ga.chunk = OWN_CHUNK;
+      ga.nchunk = owner_nchunk(f);
+      ga.n_ranges = V * ma * ga.nchunk;
+      if (out_scores)
+        GIFT_CUDA_TRY(cudaMemsetAsync(out_scores, 0, sizeof(double) * B * f->n_local, st));
+      const int smem = static_cast<int>(gather_smem(1, 0, K, V * ma, W));
+      dim3 grid(static_cast<unsigned>(static_cast<int64_t>(B) * V * ma),
+                static_cast<unsigned>(ga.nchunk));
+      if (W == 1) {
+        GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_owner_reduce_kernel<1>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        fif_owner_reduce_kernel<1><<<grid, GR_THREADS, smem, st>>>(ga);
+      } else if (W == 2) {
+        GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_owner_reduce_kernel<2>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        fif_owner_reduce_kernel<2><<<grid, GR_THREADS, smem, st>>>(ga);
+      } else {
+        GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_owner_reduce_kernel<4>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        fif_owner_reduce_kernel<4><<<grid, GR_THREADS, smem, st>>>(ga);
+      }
+      GIFT_LAUNCH_CHECK();
+      return GIFT_OK;
+    }
+    ga.rs = gather_rs(f->n_local);
+    ga.n_ranges = static_cast<int>(cdiv(f->n_local, ga.rs));
+    ga.chunk = ga.nchunk = 0;
+    // queries per CTA: GR_G, fewer when that leaves the GPU under-filled
+    ga.G = GR_G;
+    while (ga.G > 1 && ga.n_ranges * cdiv(B, ga.G) < 8LL * sm_count()) ga.G >>= 1;
     const int smem = static_cast<int>(gather_smem(ga.G, ga.rs, K, V * ma, W));
     dim3 grid(static_cast<unsigned>(ga.n_ranges), static_cast<unsigned>(cdiv(B, ga.G)));
     if (W == 1) {

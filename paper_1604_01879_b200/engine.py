@@ -162,6 +162,7 @@ class DeviceFif:
         v.shape_seg_off = self.shape_seg_off.data_ptr()
         v.shape_seg = self.shape_seg.data_ptr()
         v.shape_seg_cell = self.shape_seg_cell.data_ptr()
+        v.max_cell_segments = self.smax
         self.view = v
         return v
 

@@ -391,9 +391,9 @@ def test_quantize_near_ties_and_scale(impl, monkeypatch):
 
 @pytest.mark.parametrize("V,ma,K", [(16, 1, 32), (16, 2, 32), (20, 3, 16), (64, 2, 64), (70, 2, 64)])
 def test_gather_reduce_equals_range_reduce(V, ma, K, monkeypatch):
-    """The shape-centric gather reduce (default when the index has its shape
-    -> segment map and V * ma <= 128) is bit-identical to the per-range
-    reduce: same per-view maxima, same ascending-view f64 sum.  Uniform
+    """The shape-centric gather and owner reduces (available when the index
+    has its shape -> segment map and V * ma <= 128) are bit-identical to the
+    per-range reduce: same per-view maxima, same ascending-view f64 sum.  Uniform
     random views spread each shape over many cells (> 4 segments: the
     uncached segment path); V * ma = 140 falls back to the range reduce."""
     rng = np.random.default_rng(V * 100 + ma)
@@ -407,21 +407,21 @@ def test_gather_reduce_equals_range_reduce(V, ma, K, monkeypatch):
     Q = torch.from_numpy(qs).to(dev())
     run = eg.ScoreRunner()
     got = {}
-    for impl in ("gather", "range"):
+    for impl in ("gather", "range", "owner"):
         monkeypatch.setenv("GIFT_REDUCE", impl)
         for sim in ("cosine", "gaussian"):
             s, cs, ci = run.score(fif.dev, Q, ma, mt.sim_mode(sim), 0.5, cand_k=4)
             nbr, val = eg.topk_candidates(cs, ci, 4, positive_only=True)
             got[impl, sim] = (s.cpu().numpy(), nbr.cpu().numpy(), val.cpu().numpy())
     for sim in ("cosine", "gaussian"):
-        np.testing.assert_array_equal(got["gather", sim][0], got["range", sim][0])
-        np.testing.assert_array_equal(got["gather", sim][1], got["range", sim][1])
-        np.testing.assert_array_equal(got["gather", sim][2], got["range", sim][2])
+        for impl in ("gather", "owner"):
+            for t in range(3):
+                np.testing.assert_array_equal(got[impl, sim][t], got["range", sim][t])
         ref = eg.topk_rows(torch.from_numpy(got["range", sim][0]).to(dev()), 4,
                            positive_only=True)[0].cpu().numpy()
         np.testing.assert_array_equal(got["gather", sim][1], ref)
     # candidates-only mode (no dense scores) gives the same neighbour lists
-    for impl in ("gather", "range"):
+    for impl in ("gather", "range", "owner"):
         monkeypatch.setenv("GIFT_REDUCE", impl)
         s, cs, ci = run.score(fif.dev, Q, ma, mt.sim_mode("cosine"), 0.5, cand_k=4, dense=False)
         assert s is None
