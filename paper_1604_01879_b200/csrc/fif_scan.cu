@@ -998,9 +998,12 @@ int gather_words(const gift_fif_view* f, int V, int ma) {
 }
 
 // GIFT_REDUCE=range|gather|owner forces one reduce.  Default: the owner
-// reduce (touched pairs only) for few slots per query (its per-bit work
-// grows with V * ma, the per-range tile's with V): measured faster on
-// config 4 (V * ma = 20), the per-range reduce on config 2 (V * ma = 128).
+// reduce (touched pairs only) on large shards, whose per-range [V x rs]
+// tiles cost B * N * V: measured 4.1 vs 28 ms on config 4 (1M shapes),
+// 1.2 vs 3.1 ms on config 3 (100k); the per-range reduce on small shards
+// (config 2, 10k shapes: 0.10 vs 0.37 ms).
+constexpr int64_t OWNER_MIN_SHAPES = 32768;
+
 int reduce_mode(const gift_fif_view* f, int V, int ma) {
   const int W = gather_words(f, V, ma);
   if (W == 0) return RM_RANGE;
@@ -1008,7 +1011,7 @@ int reduce_mode(const gift_fif_view* f, int V, int ma) {
   if (e != nullptr && e[0] == 'r') return RM_RANGE;
   if (e != nullptr && e[0] == 'g') return RM_GATHER;
   if (e != nullptr && e[0] == 'o') return RM_OWNER;
-  return W == 1 ? RM_OWNER : RM_RANGE;
+  return f->n_local >= OWNER_MIN_SHAPES ? RM_OWNER : RM_RANGE;
 }
 
 int owner_nchunk(const gift_fif_view* f) {
@@ -1161,6 +1164,8 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
     ta.has_lo = 0;
     const char* ck = getenv("GIFT_TC_CHUNK_KB");
     ta.chunk_kb = ck ? atoi(ck) : 4;
+    const char* mo = getenv("GIFT_TC_ORDER");
+    ta.mt_major = (mo != nullptr && mo[0] == 'm') ? 1 : 0;
     if (ta.chunk_kb < 1) ta.chunk_kb = 1;
     int rc2 = launch_scan_tc(f, Q, nprobes, ta, w.g1, w.g2, st, ev_scan_begin, ev_scan_end);
     if (rc2) return rc2;

@@ -9,17 +9,19 @@
 // planes x = h1 + 2^-11 h2 (h1 = rn(x), h2 = rn((x - h1) 2^11), 22 significant
 // bits); the dot is  D1 + 2^-11 D2,  D1 = sum a1 b1,  D2 = sum (a1 b2 + a2 b1),
 // three kind::f16 MMAs per k-step with fp32 accumulation in TMEM.  fp16
-// products are exact in fp32.  The accumulators are drained to registers every
-// `chunk_kb` k-blocks (and summed there in fp32, round-to-nearest) so the
-// tensor-core accumulation chains stay short.  Database planes are built once
+// products are exact in fp32 but the tensor-core accumulate is not: D1 is
+// drained to registers every `chunk_kb` k-blocks (and summed there in fp32,
+// round-to-nearest) so its accumulation chains stay short; D2 carries terms
+// 2^11 smaller and is drained once per item.  Database planes are built once
 // (gift_split_planes); query planes per batch (gather_split kernel below).
 //
 // Warp roles (1 CTA / SM, persistent, static round-robin over items):
-//   warp 0      TMA producer: A1/A2 (postings, 128 x 64 fp16, 128B swizzle) and
-//               B1/B2 (probes, 64 x 64) per k-block into a 3-stage ring;
-//   warp 1      MMA issuer: 12 tcgen05.mma (M=128, N=64, K=16) per k-block into
-//               one of two TMEM accumulator pairs (D1 | D2), tcgen05.commit
-//               releases smem stages and hands full accumulators over;
+//   warp 0      TMA producer: A1[/A2] (postings, 128 x 64 fp16, 128B swizzle)
+//               and B1/B2 (probes, 64 or 128 x 64) per k-block into a 3-stage
+//               (4-stage without the A2 plane) ring;
+//   warp 1      MMA issuer: 2-3 tcgen05.mma (M=128, N=64|128, K=16) per k-step
+//               into D1 (double-buffered per chunk) and D2 (per item);
+//               tcgen05.commit releases smem stages and hands accumulators over;
 //   warps 2..5  epilogue: tcgen05.ld drains (row = TMEM lane), fp32 sums,
 //               similarity transform, per-segment max over rows, store.
 #include <cudaTypedefs.h>
@@ -32,17 +34,25 @@ namespace gift {
 constexpr int TC_M = 128;
 constexpr int TC_NMAX = 128;  // probes per item: N = 64 or 128 (per item)
 constexpr int TC_BK = 64;     // fp16 per k-block = 128-byte rows
-constexpr int TC_STAGES = 3;
 constexpr int A_TILE = TC_M * TC_BK * 2;     // 16 KB
 constexpr int B_BOX = 64 * TC_BK * 2;        //  8 KB (one 64-row TMA box)
 constexpr int B_TILE = TC_NMAX * TC_BK * 2;  // 16 KB
-constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;
+// stage = A1 [A2] B1 B2: 64 KB with the database lo plane (3 stages), 48 KB
+// without (fp16 storage: 4 stages) in the same ring budget
+constexpr int STAGE_LO = 2 * A_TILE + 2 * B_TILE;
+constexpr int STAGE_NOLO = A_TILE + 2 * B_TILE;
+constexpr int RING_BYTES = 3 * STAGE_LO;  // 192 KB
+constexpr int MAX_STAGES = 4;
 constexpr int EPI_COLS = 32;  // epilogue stages 32 probe columns at a time
 constexpr int EPI_STRIDE = EPI_COLS + 1;
 constexpr int EPI_BYTES = TC_M * EPI_STRIDE * 4;
 constexpr int TC_THREADS = 192;
-constexpr uint32_t TMEM_COLS = 512;  // 2 buffers x (D1[128] | D2[128])
-constexpr int SMEM_TC = TC_STAGES * STAGE_BYTES + EPI_BYTES + 256;
+// TMEM: D1 (hi x hi) double-buffered per k-chunk, drained every chunk_kb
+// k-blocks (short tensor-core accumulation chains: the fp32 accumulate is
+// not exact); D2 (the 2^-11-scaled correction terms) double-buffered per
+// item, drained once per item (its accumulation error is 2^-11 smaller)
+constexpr uint32_t TMEM_COLS = 512;  // D1[2][128] | D2[2][128]
+constexpr int SMEM_TC = RING_BYTES + EPI_BYTES + 256;
 constexpr float SPLIT_INV = 1.0f / 2048.0f;
 
 struct ItemInfo {
@@ -74,8 +84,15 @@ __device__ __forceinline__ ItemInfo decode_item(const TcArgs& p, int64_t item, i
   const int64_t rem = item - p.item_off[lo];
   const int cnt = p.counts[lo];
   const int nm = (cnt + TC_NMAX - 1) / TC_NMAX;
-  const int64_t t = p.tile_off[lo] + rem / nm;
-  I.mt = static_cast<int>(rem % nm);
+  int64_t t;
+  if (p.mt_major) {  // neighbouring CTAs share a probe tile (B), stream posting tiles
+    const int64_t T = p.tile_off[lo + 1] - p.tile_off[lo];
+    t = p.tile_off[lo] + rem % T;
+    I.mt = static_cast<int>(rem / T);
+  } else {  // neighbouring CTAs share a posting tile (A)
+    t = p.tile_off[lo] + rem / nm;
+    I.mt = static_cast<int>(rem % nm);
+  }
   I.p0 = p.tile_pstart[t];
   I.p1 = p.tile_pend[t];
   I.seg0 = p.tile_seg0[t];
@@ -98,13 +115,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ int32_t s_sp[TC_M + 2];
   __shared__ float s_qn2[TC_NMAX];
-  float* Ds = reinterpret_cast<float*>(smem + TC_STAGES * STAGE_BYTES);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TC_STAGES * STAGE_BYTES + EPI_BYTES);
+  float* Ds = reinterpret_cast<float*>(smem + RING_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + RING_BYTES + EPI_BYTES);
   uint64_t* full = bars;
-  uint64_t* empty = bars + TC_STAGES;
-  uint64_t* tfull = bars + 2 * TC_STAGES;
-  uint64_t* tempty = bars + 2 * TC_STAGES + 2;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * TC_STAGES + 4);
+  uint64_t* empty = bars + MAX_STAGES;
+  uint64_t* tfull = bars + 2 * MAX_STAGES;   // D1 chunk buffers
+  uint64_t* tempty = tfull + 2;
+  uint64_t* dfull = tempty + 2;              // D2 item buffers
+  uint64_t* dempty = dfull + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(dempty + 2);
+  const int has_lo = p.has_lo;
+  const int stage_bytes = has_lo ? STAGE_LO : STAGE_NOLO;
+  const int nstages = has_lo ? 3 : 4;
+  const int b_off = has_lo ? 2 * A_TILE : A_TILE;  // B1 offset in a stage
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (p.meta[M_OVERFLOW]) return;
@@ -113,13 +136,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int chunk_kb = p.chunk_kb;
 
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < TC_STAGES; ++s) {
+    for (int s = 0; s < MAX_STAGES; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&tfull[b], 1);
       tc::mbar_init(&tempty[b], TC_M);
+      tc::mbar_init(&dfull[b], 1);
+      tc::mbar_init(&dempty[b], TC_M);
     }
     tc::fence_barrier_init();
     tc::tma_prefetch(&tmA1);
@@ -143,20 +168,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
         const ItemInfo I = decode_item(p, item, hint);
         const int nbox = I.n / 64;
-        const uint32_t bytes = (p.has_lo ? 2 * A_TILE : A_TILE) + 2 * nbox * B_BOX;
+        const uint32_t bytes = (has_lo ? 2 * A_TILE : A_TILE) + 2 * nbox * B_BOX;
         for (int kb = 0; kb < nkb; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* st = smem + stage * STAGE_BYTES;
+          uint8_t* st = smem + stage * stage_bytes;
           tc::mbar_arrive_expect_tx(&full[stage], bytes);
           tc::tma_load_2d(st, &tmA1, &full[stage], kb * TC_BK, I.p0);
-          if (p.has_lo) tc::tma_load_2d(st + A_TILE, &tmA2, &full[stage], kb * TC_BK, I.p0);
+          if (has_lo) tc::tma_load_2d(st + A_TILE, &tmA2, &full[stage], kb * TC_BK, I.p0);
           for (int x = 0; x < nbox; ++x) {
-            tc::tma_load_2d(st + 2 * A_TILE + x * B_BOX, &tmB1, &full[stage], kb * TC_BK,
+            tc::tma_load_2d(st + b_off + x * B_BOX, &tmB1, &full[stage], kb * TC_BK,
                             I.pb0 + 64 * x);
-            tc::tma_load_2d(st + 2 * A_TILE + B_TILE + x * B_BOX, &tmB2, &full[stage],
+            tc::tma_load_2d(st + b_off + B_TILE + x * B_BOX, &tmB2, &full[stage],
                             kb * TC_BK, I.pb0 + 64 * x);
           }
-          if (++stage == TC_STAGES) {
+          if (++stage == nstages) {
             stage = 0;
             phase ^= 1;
           }
@@ -168,36 +193,40 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      uint32_t chunk_ctr = 0;
+      uint32_t chunk_ctr = 0, item_ctr = 0;
       int hint = 0;
       for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
         const ItemInfo I = decode_item(p, item, hint);
         const uint32_t idesc = tc::idesc_f16_f32(TC_M, I.n);
+        const uint32_t ib = item_ctr & 1, iph = (item_ctr >> 1) & 1;
+        tc::mbar_wait(&dempty[ib], iph ^ 1);  // D2 buffer of this item free
+        tc::tc_fence_after();
+        const uint32_t d2 = tmem_base + 256 + ib * TC_NMAX;
         for (int kb0 = 0; kb0 < nkb; kb0 += chunk_kb) {
           const uint32_t buf = chunk_ctr & 1, aph = (chunk_ctr >> 1) & 1;
           tc::mbar_wait(&tempty[buf], aph ^ 1);
           tc::tc_fence_after();
-          const uint32_t d1 = tmem_base + buf * 256;
-          const uint32_t d2 = d1 + TC_NMAX;
+          const uint32_t d1 = tmem_base + buf * TC_NMAX;
           const int kend = min(kb0 + chunk_kb, nkb);
           for (int kb = kb0; kb < kend; ++kb) {
             tc::mbar_wait(&full[stage], phase);
             tc::tc_fence_after();
-            uint8_t* st = smem + stage * STAGE_BYTES;
+            uint8_t* st = smem + stage * stage_bytes;
             const uint64_t a1 = tc::smem_desc_sw128(st);
             const uint64_t a2 = tc::smem_desc_sw128(st + A_TILE);
-            const uint64_t b1 = tc::smem_desc_sw128(st + 2 * A_TILE);
-            const uint64_t b2 = tc::smem_desc_sw128(st + 2 * A_TILE + B_TILE);
+            const uint64_t b1 = tc::smem_desc_sw128(st + b_off);
+            const uint64_t b2 = tc::smem_desc_sw128(st + b_off + B_TILE);
 #pragma unroll
             for (int k = 0; k < TC_BK / 16; ++k) {
-              const uint32_t acc = (kb > kb0 || k > 0) ? 1u : 0u;
+              const uint32_t acc1 = (kb > kb0 || k > 0) ? 1u : 0u;
+              const uint32_t acc2 = (kb > 0 || k > 0) ? 1u : 0u;
               const uint64_t adv = static_cast<uint64_t>(k * 2);  // 32 B in 16-B units
-              tc::mma_f16(d1, a1 + adv, b1 + adv, idesc, acc);
-              tc::mma_f16(d2, a1 + adv, b2 + adv, idesc, acc);
-              if (p.has_lo) tc::mma_f16(d2, a2 + adv, b1 + adv, idesc, 1u);
+              tc::mma_f16(d1, a1 + adv, b1 + adv, idesc, acc1);
+              tc::mma_f16(d2, a1 + adv, b2 + adv, idesc, acc2);
+              if (has_lo) tc::mma_f16(d2, a2 + adv, b1 + adv, idesc, 1u);
             }
             tc::mma_commit(&empty[stage]);
-            if (++stage == TC_STAGES) {
+            if (++stage == nstages) {
               stage = 0;
               phase ^= 1;
             }
@@ -205,6 +234,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           tc::mma_commit(&tfull[buf]);
           ++chunk_ctr;
         }
+        tc::mma_commit(&dfull[ib]);
+        ++item_ctr;
       }
     }
   } else {
@@ -213,7 +244,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int lb = 32 * (warp & 3);       // TMEM lane quarter of this warp
     const int row = lb + lane;            // posting row within the tile
     const bool gauss = p.mode == GIFT_SIM_GAUSSIAN;
-    uint32_t chunk_ctr = 0;
+    uint32_t chunk_ctr = 0, item_ctr = 0;
     int hint = 0;
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const ItemInfo I = decode_item(p, item, hint);
@@ -228,25 +259,52 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       float acc[TC_NMAX];
 #pragma unroll
       for (int n = 0; n < TC_NMAX; ++n) acc[n] = 0.f;
+      const uint32_t lane_off = static_cast<uint32_t>(lb) << 16;
       for (int kb0 = 0; kb0 < nkb; kb0 += chunk_kb) {
         const uint32_t buf = chunk_ctr & 1, aph = (chunk_ctr >> 1) & 1;
         tc::mbar_wait(&tfull[buf], aph);
         tc::tc_fence_after();
-        const uint32_t base = tmem_base + (static_cast<uint32_t>(lb) << 16) + buf * 256;
+        const uint32_t base = tmem_base + lane_off + buf * TC_NMAX;
 #pragma unroll
-        for (int j = 0; j < TC_NMAX / 16; ++j) {
+        for (int j = 0; j < TC_NMAX / 16; j += 2) {
           if (j < ng) {
             float v1[16], v2[16];
             tc::tmem_ld_x16(base + j * 16, v1);
-            tc::tmem_ld_x16(base + TC_NMAX + j * 16, v2);
+            tc::tmem_ld_x16(base + (j + 1) * 16, v2);  // ng is even or the column is unused
             tc::tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 16; ++i) acc[j * 16 + i] += fmaf(v2[i], SPLIT_INV, v1[i]);
+            for (int i = 0; i < 16; ++i) {
+              acc[j * 16 + i] += v1[i];
+              acc[(j + 1) * 16 + i] += v2[i];
+            }
           }
         }
         tc::tc_fence_before();
         tc::mbar_arrive(&tempty[buf]);
         ++chunk_ctr;
+      }
+      {  // the item's correction terms, once: acc += 2^-11 D2
+        const uint32_t ib = item_ctr & 1, iph = (item_ctr >> 1) & 1;
+        tc::mbar_wait(&dfull[ib], iph);
+        tc::tc_fence_after();
+        const uint32_t base = tmem_base + lane_off + 256 + ib * TC_NMAX;
+#pragma unroll
+        for (int j = 0; j < TC_NMAX / 16; j += 2) {
+          if (j < ng) {
+            float v1[16], v2[16];
+            tc::tmem_ld_x16(base + j * 16, v1);
+            tc::tmem_ld_x16(base + (j + 1) * 16, v2);
+            tc::tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              acc[j * 16 + i] = fmaf(v1[i], SPLIT_INV, acc[j * 16 + i]);
+              acc[(j + 1) * 16 + i] = fmaf(v2[i], SPLIT_INV, acc[(j + 1) * 16 + i]);
+            }
+          }
+        }
+        tc::tc_fence_before();
+        tc::mbar_arrive(&dempty[ib]);
+        ++item_ctr;
       }
       const float pn = (I.p0 + row < I.p1) ? p.pnorm2[I.p0 + row] : 0.f;
       const int64_t S_c = p.seg_off[I.c + 1] - p.seg_off[I.c];

@@ -28,6 +28,7 @@ struct TcArgs {
   float inv_sigma2;
   int has_lo;
   int chunk_kb;
+  int mt_major;  // item order within a cell: probe-tile-major (1) or posting-tile-major (0)
 };
 
 bool tc_supported(const gift_fif_view* f);

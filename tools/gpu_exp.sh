@@ -1,5 +1,6 @@
 set -x
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
-timeout 300 python tools/stage_profile.py --config c4s --steps 3 --reduce owner,gather,range --kernels > gpurun_out/stages_c4s.json 2> gpurun_out/stages_c4s.err; echo st4s=$?
-timeout 300 python tools/stage_profile.py --config c2 --steps 3 --reduce owner,gather,range > gpurun_out/stages_c2.json 2> gpurun_out/stages_c2.err; echo st2=$?
-timeout 900 python tools/stage_profile.py --config c4 --steps 3 --reduce owner,gather --kernels > gpurun_out/stages_c4.json 2> gpurun_out/stages_c4.err; echo st4=$?
+timeout 600 python bench.py --steps 10 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; echo b2=$?
+timeout 1800 python bench.py --config c4 --steps 5 --warmup 3 > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err; echo c4=$?
+timeout 1800 python bench.py --config c3 --steps 8 --warmup 3 > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err; echo c3=$?
+timeout 600 python bench.py --config c5 --steps 5 > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err; echo c5=$?
