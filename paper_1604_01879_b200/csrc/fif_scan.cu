@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(PLAN_THREADS)
                       const int64_t* __restrict__ tile_off, int32_t* __restrict__ probe_off,
                       int64_t* __restrict__ outbase, int64_t* __restrict__ item_off,
                       int32_t* __restrict__ cursor, int64_t* __restrict__ meta, int64_t capacity,
-                      int ptile) {
+                      int ptile, int tile_div) {
   __shared__ int64_t sbuf[32];
   const int per = (K + PLAN_THREADS - 1) / PLAN_THREADS;
   const int c0 = threadIdx.x * per;
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(PLAN_THREADS)
     int64_t T = tile_off[c + 1] - tile_off[c];
     s_cnt += n;
     s_out += n * S;
-    s_items += T * ((n + ptile - 1) / ptile);
+    s_items += (T + tile_div - 1) / tile_div * ((n + ptile - 1) / ptile);
   }
   int64_t tot_cnt, tot_out, tot_items;
   int64_t p_cnt = block_exclusive_scan<int64_t>(s_cnt, &tot_cnt, sbuf);
@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(PLAN_THREADS)
     cursor[c] = 0;
     p_cnt += n;
     p_out += n * S;
-    p_items += T * ((n + ptile - 1) / ptile);
+    p_items += (T + tile_div - 1) / tile_div * ((n + ptile - 1) / ptile);
   }
   if (threadIdx.x == 0) {
     probe_off[K] = static_cast<int32_t>(tot_cnt);
@@ -1130,7 +1130,8 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
   GIFT_LAUNCH_CHECK();
   probe_plan_kernel<<<1, PLAN_THREADS, 0, st>>>(w.counts, K, f->seg_off, f->tile_off, w.probe_off,
                                                 w.outbase, w.item_off, w.cursor, w.meta, w.capacity,
-                                                use_tc(f) ? 128 : simt::TB);
+                                                use_tc(f) ? 128 : simt::TB,
+                                                use_tc(f) && tc_pair_enabled() ? 2 : 1);
   GIFT_LAUNCH_CHECK();
   probe_scatter_kernel<<<static_cast<unsigned>(cdiv(nprobes, 256)), 256, 0, st>>>(
       w.cells, nprobes, w.probe_off, w.cursor, w.probe_list, w.probe_rank);

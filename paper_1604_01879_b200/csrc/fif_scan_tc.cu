@@ -37,12 +37,9 @@ constexpr int TC_BK = 64;     // fp16 per k-block = 128-byte rows
 constexpr int A_TILE = TC_M * TC_BK * 2;     // 16 KB
 constexpr int B_BOX = 64 * TC_BK * 2;        //  8 KB (one 64-row TMA box)
 constexpr int B_TILE = TC_NMAX * TC_BK * 2;  // 16 KB
-// stage = A1 [A2] B1 B2: 64 KB with the database lo plane (3 stages), 48 KB
-// without (fp16 storage: 4 stages) in the same ring budget
+// ring budget: three single-CTA stages of A1 A2 B1 B2 (see Ring<> below)
 constexpr int STAGE_LO = 2 * A_TILE + 2 * B_TILE;
-constexpr int STAGE_NOLO = A_TILE + 2 * B_TILE;
 constexpr int RING_BYTES = 3 * STAGE_LO;  // 192 KB
-constexpr int MAX_STAGES = 4;
 constexpr int EPI_COLS = 32;  // epilogue stages 32 probe columns at a time
 constexpr int EPI_STRIDE = EPI_COLS + 1;
 constexpr int EPI_BYTES = TC_M * EPI_STRIDE * 4;
@@ -57,13 +54,18 @@ constexpr float SPLIT_INV = 1.0f / 2048.0f;
 
 struct ItemInfo {
   int c, mt, p0, p1, seg0, seg1, nb, pb0, n;  // n: MMA N of the item (64 | 128)
+  bool live;  // pair mode: this CTA's posting tile exists (else a duplicate, no output)
 };
 
 // Cell of an item: items ascend along each role's loop, so the search starts
 // at the previous item's cell (`hint`): one load when the item stays in that
 // cell, else a galloping then binary search over item_off[hint+1 .. K-1]
 // (a plain binary search over K = 4096 cells is 12 dependent global loads).
-__device__ __forceinline__ ItemInfo decode_item(const TcArgs& p, int64_t item, int& hint) {
+// Pair mode: an item is (two consecutive posting tiles, one probe tile); CTA
+// `rank` of the pair takes tile 2 tp + rank.
+template <bool PAIR>
+__device__ __forceinline__ ItemInfo decode_item(const TcArgs& p, int64_t item, int& hint,
+                                                int rank) {
   int lo = hint;
   if (p.item_off[lo + 1] <= item) {
     int step = 1, hi = lo + 1;  // item_off[hi] <= item
@@ -84,15 +86,23 @@ __device__ __forceinline__ ItemInfo decode_item(const TcArgs& p, int64_t item, i
   const int64_t rem = item - p.item_off[lo];
   const int cnt = p.counts[lo];
   const int nm = (cnt + TC_NMAX - 1) / TC_NMAX;
-  int64_t t;
-  if (p.mt_major) {  // neighbouring CTAs share a probe tile (B), stream posting tiles
-    const int64_t T = p.tile_off[lo + 1] - p.tile_off[lo];
-    t = p.tile_off[lo] + rem % T;
-    I.mt = static_cast<int>(rem / T);
-  } else {  // neighbouring CTAs share a posting tile (A)
-    t = p.tile_off[lo] + rem / nm;
+  const int64_t T = p.tile_off[lo + 1] - p.tile_off[lo];
+  int64_t tt;  // tile index within the cell
+  if (PAIR) {
+    tt = 2 * (rem / nm) + rank;
     I.mt = static_cast<int>(rem % nm);
+    I.live = tt < T;
+    if (!I.live) tt -= 1;  // odd tile count: the second CTA recomputes the first tile
+  } else if (p.mt_major) {  // neighbouring CTAs share a probe tile (B)
+    tt = rem % T;
+    I.mt = static_cast<int>(rem / T);
+    I.live = true;
+  } else {  // neighbouring CTAs share a posting tile (A)
+    tt = rem / nm;
+    I.mt = static_cast<int>(rem % nm);
+    I.live = true;
   }
+  const int64_t t = p.tile_off[lo] + tt;
   I.p0 = p.tile_pstart[t];
   I.p1 = p.tile_pend[t];
   I.seg0 = p.tile_seg0[t];
@@ -107,54 +117,82 @@ __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
 }
 
+// Stage layouts.  Single CTA: A1 [A2] B1 B2 (B = N probe rows).  CTA pair
+// (cta_group::2, M = 256): each CTA holds its own posting tile's A1 [A2] and
+// half of the probe rows of B1 and B2 (N / 2 each); the pair's MMA reads the
+// other halves from the peer's smem at the same offsets.
+template <bool PAIR>
+struct Ring {
+  static constexpr int B_PART = PAIR ? B_TILE / 2 : B_TILE;
+  static constexpr int LO = 2 * A_TILE + 2 * B_PART;
+  static constexpr int NOLO = A_TILE + 2 * B_PART;
+  static constexpr int STAGES_LO = RING_BYTES / LO;      // 3 | 4
+  static constexpr int STAGES_NOLO = RING_BYTES / NOLO;  // 4 | 6
+};
+constexpr int MAX_RING_STAGES = 6;
+
+template <bool PAIR>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     fif_scan_tc_kernel(const __grid_constant__ CUtensorMap tmA1,
                        const __grid_constant__ CUtensorMap tmA2,
                        const __grid_constant__ CUtensorMap tmB1,
-                       const __grid_constant__ CUtensorMap tmB2, const TcArgs p) {
+                       const __grid_constant__ CUtensorMap tmB2,
+                       const __grid_constant__ CUtensorMap tmB1h,
+                       const __grid_constant__ CUtensorMap tmB2h, const TcArgs p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ int32_t s_sp[TC_M + 2];
   __shared__ float s_qn2[TC_NMAX];
   float* Ds = reinterpret_cast<float*>(smem + RING_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + RING_BYTES + EPI_BYTES);
   uint64_t* full = bars;
-  uint64_t* empty = bars + MAX_STAGES;
-  uint64_t* tfull = bars + 2 * MAX_STAGES;   // D1 chunk buffers
+  uint64_t* empty = bars + MAX_RING_STAGES;
+  uint64_t* tfull = bars + 2 * MAX_RING_STAGES;  // D1 chunk buffers
   uint64_t* tempty = tfull + 2;
-  uint64_t* dfull = tempty + 2;              // D2 item buffers
+  uint64_t* dfull = tempty + 2;                  // D2 item buffers
   uint64_t* dempty = dfull + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(dempty + 2);
   const int has_lo = p.has_lo;
-  const int stage_bytes = has_lo ? STAGE_LO : STAGE_NOLO;
-  const int nstages = has_lo ? 3 : 4;
+  const int stage_bytes = has_lo ? Ring<PAIR>::LO : Ring<PAIR>::NOLO;
+  const int nstages = has_lo ? Ring<PAIR>::STAGES_LO : Ring<PAIR>::STAGES_NOLO;
   const int b_off = has_lo ? 2 * A_TILE : A_TILE;  // B1 offset in a stage
+  constexpr int B_PART = Ring<PAIR>::B_PART;
+  const uint32_t rank = PAIR ? tc::cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  // item sequence: per CTA, or per pair (both CTAs walk the same items)
+  const int64_t first = PAIR ? blockIdx.x / 2 : blockIdx.x;
+  const int64_t stride = PAIR ? gridDim.x / 2 : gridDim.x;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (p.meta[M_OVERFLOW]) return;
+  if (p.meta[M_OVERFLOW]) return;  // uniform over the grid (both CTAs of a pair)
   const int64_t n_items = p.meta[M_ITEMS];
   const int nkb = (p.d + TC_BK - 1) / TC_BK;
   const int chunk_kb = p.chunk_kb;
 
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < MAX_STAGES; ++s) {
+    for (int s = 0; s < MAX_RING_STAGES; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&tfull[b], 1);
-      tc::mbar_init(&tempty[b], TC_M);
+      tc::mbar_init(&tempty[b], PAIR ? 2 * TC_M : TC_M);  // pair: both CTAs' epilogues
       tc::mbar_init(&dfull[b], 1);
-      tc::mbar_init(&dempty[b], TC_M);
+      tc::mbar_init(&dempty[b], PAIR ? 2 * TC_M : TC_M);
     }
     tc::fence_barrier_init();
     tc::tma_prefetch(&tmA1);
-    if (p.has_lo) tc::tma_prefetch(&tmA2);
-    tc::tma_prefetch(&tmB1);
-    tc::tma_prefetch(&tmB2);
+    if (has_lo) tc::tma_prefetch(&tmA2);
+    tc::tma_prefetch(PAIR ? &tmB1h : &tmB1);
+    tc::tma_prefetch(PAIR ? &tmB2h : &tmB2);
   }
-  if (warp == 1) tc::tmem_alloc<TMEM_COLS>(tmem_holder);
+  if (warp == 1) {
+    if (PAIR)
+      tc::tmem_alloc_2sm<TMEM_COLS>(tmem_holder);
+    else
+      tc::tmem_alloc<TMEM_COLS>(tmem_holder);
+  }
   tc::tc_fence_before();
-  __syncthreads();
+  if (PAIR) tc::cluster_sync(); else __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
@@ -165,21 +203,38 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (lane == 0) {
       int stage = 0, hint = 0;
       uint32_t phase = 0;
-      for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
-        const ItemInfo I = decode_item(p, item, hint);
-        const int nbox = I.n / 64;
-        const uint32_t bytes = (has_lo ? 2 * A_TILE : A_TILE) + 2 * nbox * B_BOX;
+      for (int64_t item = first; item < n_items; item += stride) {
+        const ItemInfo I = decode_item<PAIR>(p, item, hint, rank);
+        const int brows = PAIR ? I.n / 2 : I.n;            // probe rows this CTA loads
+        const uint32_t a_bytes = has_lo ? 2 * A_TILE : A_TILE;
+        const uint32_t bytes = a_bytes + 2 * brows * TC_BK * 2;
         for (int kb = 0; kb < nkb; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * stage_bytes;
-          tc::mbar_arrive_expect_tx(&full[stage], bytes);
-          tc::tma_load_2d(st, &tmA1, &full[stage], kb * TC_BK, I.p0);
-          if (has_lo) tc::tma_load_2d(st + A_TILE, &tmA2, &full[stage], kb * TC_BK, I.p0);
-          for (int x = 0; x < nbox; ++x) {
-            tc::tma_load_2d(st + b_off + x * B_BOX, &tmB1, &full[stage], kb * TC_BK,
-                            I.pb0 + 64 * x);
-            tc::tma_load_2d(st + b_off + B_TILE + x * B_BOX, &tmB2, &full[stage],
-                            kb * TC_BK, I.pb0 + 64 * x);
+          if (PAIR) {
+            // both CTAs' bytes complete on the leader's full barrier
+            const uint32_t lbar = tc::mapa(&full[stage], 0);
+            if (leader) tc::mbar_arrive_expect_tx(&full[stage], 2 * bytes);
+            tc::tma_load_2d_2sm(st, &tmA1, lbar, kb * TC_BK, I.p0);
+            if (has_lo) tc::tma_load_2d_2sm(st + A_TILE, &tmA2, lbar, kb * TC_BK, I.p0);
+            const int r0 = I.pb0 + static_cast<int>(rank) * brows;
+            if (brows == 64) {
+              tc::tma_load_2d_2sm(st + b_off, &tmB1, lbar, kb * TC_BK, r0);
+              tc::tma_load_2d_2sm(st + b_off + B_PART, &tmB2, lbar, kb * TC_BK, r0);
+            } else {
+              tc::tma_load_2d_2sm(st + b_off, &tmB1h, lbar, kb * TC_BK, r0);
+              tc::tma_load_2d_2sm(st + b_off + B_PART, &tmB2h, lbar, kb * TC_BK, r0);
+            }
+          } else {
+            tc::mbar_arrive_expect_tx(&full[stage], bytes);
+            tc::tma_load_2d(st, &tmA1, &full[stage], kb * TC_BK, I.p0);
+            if (has_lo) tc::tma_load_2d(st + A_TILE, &tmA2, &full[stage], kb * TC_BK, I.p0);
+            for (int x = 0; x < I.n / 64; ++x) {
+              tc::tma_load_2d(st + b_off + x * B_BOX, &tmB1, &full[stage], kb * TC_BK,
+                              I.pb0 + 64 * x);
+              tc::tma_load_2d(st + b_off + B_TILE + x * B_BOX, &tmB2, &full[stage],
+                              kb * TC_BK, I.pb0 + 64 * x);
+            }
           }
           if (++stage == nstages) {
             stage = 0;
@@ -190,14 +245,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // (pair: the leader issues cta_group::2 MMAs for both CTAs)
+    if (lane == 0 && leader) {
       int stage = 0;
       uint32_t phase = 0;
       uint32_t chunk_ctr = 0, item_ctr = 0;
       int hint = 0;
-      for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
-        const ItemInfo I = decode_item(p, item, hint);
-        const uint32_t idesc = tc::idesc_f16_f32(TC_M, I.n);
+      for (int64_t item = first; item < n_items; item += stride) {
+        const ItemInfo I = decode_item<PAIR>(p, item, hint, rank);
+        const uint32_t idesc = tc::idesc_f16_f32(PAIR ? 2 * TC_M : TC_M, I.n);
         const uint32_t ib = item_ctr & 1, iph = (item_ctr >> 1) & 1;
         tc::mbar_wait(&dempty[ib], iph ^ 1);  // D2 buffer of this item free
         tc::tc_fence_after();
@@ -215,26 +271,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const uint64_t a1 = tc::smem_desc_sw128(st);
             const uint64_t a2 = tc::smem_desc_sw128(st + A_TILE);
             const uint64_t b1 = tc::smem_desc_sw128(st + b_off);
-            const uint64_t b2 = tc::smem_desc_sw128(st + b_off + B_TILE);
+            const uint64_t b2 = tc::smem_desc_sw128(st + b_off + B_PART);
 #pragma unroll
             for (int k = 0; k < TC_BK / 16; ++k) {
               const uint32_t acc1 = (kb > kb0 || k > 0) ? 1u : 0u;
               const uint32_t acc2 = (kb > 0 || k > 0) ? 1u : 0u;
               const uint64_t adv = static_cast<uint64_t>(k * 2);  // 32 B in 16-B units
-              tc::mma_f16(d1, a1 + adv, b1 + adv, idesc, acc1);
-              tc::mma_f16(d2, a1 + adv, b2 + adv, idesc, acc2);
-              if (has_lo) tc::mma_f16(d2, a2 + adv, b1 + adv, idesc, 1u);
+              if (PAIR) {
+                tc::mma_f16_2sm(d1, a1 + adv, b1 + adv, idesc, acc1);
+                tc::mma_f16_2sm(d2, a1 + adv, b2 + adv, idesc, acc2);
+                if (has_lo) tc::mma_f16_2sm(d2, a2 + adv, b1 + adv, idesc, 1u);
+              } else {
+                tc::mma_f16(d1, a1 + adv, b1 + adv, idesc, acc1);
+                tc::mma_f16(d2, a1 + adv, b2 + adv, idesc, acc2);
+                if (has_lo) tc::mma_f16(d2, a2 + adv, b1 + adv, idesc, 1u);
+              }
             }
-            tc::mma_commit(&empty[stage]);
+            if (PAIR) tc::mma_commit_2sm(&empty[stage], 0x3); else tc::mma_commit(&empty[stage]);
             if (++stage == nstages) {
               stage = 0;
               phase ^= 1;
             }
           }
-          tc::mma_commit(&tfull[buf]);
+          if (PAIR) tc::mma_commit_2sm(&tfull[buf], 0x3); else tc::mma_commit(&tfull[buf]);
           ++chunk_ctr;
         }
-        tc::mma_commit(&dfull[ib]);
+        if (PAIR) tc::mma_commit_2sm(&dfull[ib], 0x3); else tc::mma_commit(&dfull[ib]);
         ++item_ctr;
       }
     }
@@ -246,8 +308,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const bool gauss = p.mode == GIFT_SIM_GAUSSIAN;
     uint32_t chunk_ctr = 0, item_ctr = 0;
     int hint = 0;
-    for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
-      const ItemInfo I = decode_item(p, item, hint);
+    // accumulator release: own barrier, or the pair leader's (remote arrive)
+    const uint32_t rel_t0 = PAIR ? tc::mapa(&tempty[0], 0) : 0u;
+    const uint32_t rel_t1 = PAIR ? tc::mapa(&tempty[1], 0) : 0u;
+    const uint32_t rel_d0 = PAIR ? tc::mapa(&dempty[0], 0) : 0u;
+    const uint32_t rel_d1 = PAIR ? tc::mapa(&dempty[1], 0) : 0u;
+    for (int64_t item = first; item < n_items; item += stride) {
+      const ItemInfo I = decode_item<PAIR>(p, item, hint, rank);
       const int nseg = I.seg1 - I.seg0;
       const int ng = I.n / 16;  // 16-column groups in use
       for (int i = et; i <= nseg; i += TC_M) s_sp[i] = p.seg_pstart[I.seg0 + i];
@@ -270,7 +337,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if (j < ng) {
             float v1[16], v2[16];
             tc::tmem_ld_x16(base + j * 16, v1);
-            tc::tmem_ld_x16(base + (j + 1) * 16, v2);  // ng is even or the column is unused
+            tc::tmem_ld_x16(base + (j + 1) * 16, v2);  // ng is even
             tc::tmem_ld_wait();
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
@@ -280,7 +347,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
         }
         tc::tc_fence_before();
-        tc::mbar_arrive(&tempty[buf]);
+        if (PAIR)
+          tc::mbar_arrive_cluster(buf ? rel_t1 : rel_t0);
+        else
+          tc::mbar_arrive(&tempty[buf]);
         ++chunk_ctr;
       }
       {  // the item's correction terms, once: acc += 2^-11 D2
@@ -303,8 +373,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
         }
         tc::tc_fence_before();
-        tc::mbar_arrive(&dempty[ib]);
+        if (PAIR)
+          tc::mbar_arrive_cluster(ib ? rel_d1 : rel_d0);
+        else
+          tc::mbar_arrive(&dempty[ib]);
         ++item_ctr;
+      }
+      if (!I.live) {  // pair: duplicate tile, nothing to write (keep s_sp reuse ordered)
+        named_bar(1, TC_M);
+        continue;
       }
       const float pn = (I.p0 + row < I.p1) ? p.pnorm2[I.p0 + row] : 0.f;
       const int64_t S_c = p.seg_off[I.c + 1] - p.seg_off[I.c];
@@ -348,10 +425,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
   }
   tc::tc_fence_before();
-  __syncthreads();
+  if (PAIR) tc::cluster_sync(); else __syncthreads();
   if (warp == 1) {
     tc::tc_fence_after();
-    tc::tmem_dealloc<TMEM_COLS>(tmem_base);
+    if (PAIR)
+      tc::tmem_dealloc_2sm<TMEM_COLS>(tmem_base);
+    else
+      tc::tmem_dealloc<TMEM_COLS>(tmem_base);
   }
 }
 
@@ -429,13 +509,19 @@ bool tc_supported(const gift_fif_view* f) {
   return f->feat_hi != nullptr && f->d % 8 == 0 && f->d >= 8 && f->n_postings > 0;
 }
 
+bool tc_pair_enabled() {
+  const char* e = getenv("GIFT_TC_PAIR");
+  return e != nullptr && e[0] == '1';
+}
+
 int launch_scan_tc(const gift_fif_view* f, const float* Q, int64_t nprobes_max, TcArgs a,
                    __half* g1, __half* g2, cudaStream_t st, void* ev0, void* ev1) {
   const int d = f->d;
+  const bool pair = tc_pair_enabled() && sm_count() >= 2;
   probe_gather_split_kernel<<<static_cast<unsigned>(max64(nprobes_max, 1)), 128, 0, st>>>(
       Q, d, a.ma, a.probe_list, a.probe_off, f->K, a.meta, g1, g2);
   GIFT_LAUNCH_CHECK();
-  CUtensorMap mA1, mA2, mB1, mB2;
+  CUtensorMap mA1, mA2, mB1, mB2, mB1h, mB2h;
   int rc = make_map(&mA1, f->feat_hi, f->n_postings, d, TC_M);
   if (rc) return rc;
   rc = make_map(&mA2, f->feat_lo ? f->feat_lo : f->feat_hi, f->n_postings, d, TC_M);
@@ -444,11 +530,35 @@ int launch_scan_tc(const gift_fif_view* f, const float* Q, int64_t nprobes_max, 
   if (rc) return rc;
   rc = make_map(&mB2, g2, max64(nprobes_max, 1), d, 64);
   if (rc) return rc;
+  rc = make_map(&mB1h, g1, max64(nprobes_max, 1), d, 32);
+  if (rc) return rc;
+  rc = make_map(&mB2h, g2, max64(nprobes_max, 1), d, 32);
+  if (rc) return rc;
   a.has_lo = f->feat_lo != nullptr ? 1 : 0;
-  GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_scan_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     SMEM_TC));
   if (ev0) GIFT_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(ev0), st));
-  fif_scan_tc_kernel<<<sm_count(), TC_THREADS, SMEM_TC, st>>>(mA1, mA2, mB1, mB2, a);
+  if (pair) {
+    GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_scan_tc_kernel<true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TC));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(sm_count() / 2 * 2));
+    cfg.blockDim = dim3(TC_THREADS);
+    cfg.dynamicSmemBytes = SMEM_TC;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    GIFT_CUDA_TRY(cudaLaunchKernelEx(&cfg, fif_scan_tc_kernel<true>, mA1, mA2, mB1, mB2, mB1h,
+                                     mB2h, a));
+  } else {
+    GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_scan_tc_kernel<false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TC));
+    fif_scan_tc_kernel<false><<<sm_count(), TC_THREADS, SMEM_TC, st>>>(mA1, mA2, mB1, mB2, mB1h,
+                                                                       mB2h, a);
+  }
   GIFT_LAUNCH_CHECK();
   if (ev1) GIFT_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(ev1), st));
   return GIFT_OK;

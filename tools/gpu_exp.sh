@@ -1,6 +1,5 @@
 set -x
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
-timeout 600 python bench.py --steps 10 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; echo b2=$?
-timeout 1800 python bench.py --config c4 --steps 5 --warmup 3 > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err; echo c4=$?
-timeout 1800 python bench.py --config c3 --steps 8 --warmup 3 > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err; echo c3=$?
-timeout 600 python bench.py --config c5 --steps 5 > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err; echo c5=$?
+GIFT_TC_PAIR=1 timeout 300 python -m pytest tests/test_gpu_parity.py -x -q -s -k "tensor_core_scan or fp16_storage or query_fif_vs_oracle or end_to_end" > gpurun_out/pair_acc.log 2>&1; echo pairacc=$?
+nvidia-smi --query-gpu=name,memory.used --format=csv >> gpurun_out/pair_acc.log
+GIFT_TC_PAIR=1 timeout 300 python tools/stage_profile.py --config c4s --steps 3 --reduce owner > gpurun_out/stages_c4s_pair.json 2> gpurun_out/stages_c4s_pair.err; echo st4s=$?
+GIFT_TC_PAIR=1 timeout 300 python tools/stage_profile.py --config c2 --steps 3 --reduce range > gpurun_out/stages_c2_pair.json 2> gpurun_out/stages_c2_pair.err; echo st2=$?
