@@ -1167,6 +1167,8 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
     ta.chunk_kb = ck ? atoi(ck) : 4;
     const char* mo = getenv("GIFT_TC_ORDER");
     ta.mt_major = (mo != nullptr && mo[0] == 'm') ? 1 : 0;
+    const char* dbg = getenv("GIFT_TC_DBG");
+    ta.dbg = dbg ? atoi(dbg) : 0;
     if (ta.chunk_kb < 1) ta.chunk_kb = 1;
     int rc2 = launch_scan_tc(f, Q, nprobes, ta, w.g1, w.g2, st, ev_scan_begin, ev_scan_end);
     if (rc2) return rc2;

@@ -43,7 +43,8 @@ constexpr int RING_BYTES = 3 * STAGE_LO;  // 192 KB
 constexpr int EPI_COLS = 32;  // epilogue stages 32 probe columns at a time
 constexpr int EPI_STRIDE = EPI_COLS + 1;
 constexpr int EPI_BYTES = TC_M * EPI_STRIDE * 4;
-constexpr int TC_THREADS = 192;
+constexpr int TC_THREADS = 224;  // producer, MMA, scheduler, 4 epilogue warps
+constexpr int ITEM_RING = 8;     // decoded work items in flight (scheduler -> roles)
 // TMEM: D1 (hi x hi) double-buffered per k-chunk, drained every chunk_kb
 // k-blocks (short tensor-core accumulation chains: the fp32 accumulate is
 // not exact); D2 (the 2^-11-scaled correction terms) double-buffered per
@@ -142,6 +143,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ int32_t s_sp[TC_M + 2];
   __shared__ float s_qn2[TC_NMAX];
+  __shared__ ItemInfo s_item[ITEM_RING];
+  __shared__ __align__(8) uint64_t ifull[ITEM_RING], iempty[ITEM_RING];
   float* Ds = reinterpret_cast<float*>(smem + RING_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + RING_BYTES + EPI_BYTES);
   uint64_t* full = bars;
@@ -173,6 +176,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
     }
+    for (int r = 0; r < ITEM_RING; ++r) {
+      tc::mbar_init(&ifull[r], 1);
+      tc::mbar_init(&iempty[r], (PAIR && !leader) ? 2 : 3);  // producer, [MMA,] epilogue
+    }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&tfull[b], 1);
       tc::mbar_init(&tempty[b], PAIR ? 2 * TC_M : TC_M);  // pair: both CTAs' epilogues
@@ -201,17 +208,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // (L2 evict-first hints on the postings measured slower: a posting tile
     // is re-read by the next probe tile of its cell)
     if (lane == 0) {
-      int stage = 0, hint = 0;
-      uint32_t phase = 0;
-      for (int64_t item = first; item < n_items; item += stride) {
-        const ItemInfo I = decode_item<PAIR>(p, item, hint, rank);
+      int stage = 0;
+      uint32_t phase = 0, it = 0;
+      for (int64_t item = first; item < n_items; item += stride, ++it) {
+        const uint32_t slot = it % ITEM_RING, iph = (it / ITEM_RING) & 1;
+        tc::mbar_wait(&ifull[slot], iph);
+        const ItemInfo I = s_item[slot];
+        tc::mbar_arrive(&iempty[slot]);
         const int brows = PAIR ? I.n / 2 : I.n;            // probe rows this CTA loads
         const uint32_t a_bytes = has_lo ? 2 * A_TILE : A_TILE;
         const uint32_t bytes = a_bytes + 2 * brows * TC_BK * 2;
         for (int kb = 0; kb < nkb; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * stage_bytes;
-          if (PAIR) {
+          if (p.dbg & 8) {  // timing experiment: MMA pipeline without loads
+            if (!PAIR || leader) tc::mbar_arrive(&full[stage]);
+          } else if (PAIR) {
             // both CTAs' bytes complete on the leader's full barrier
             const uint32_t lbar = tc::mapa(&full[stage], 0);
             if (leader) tc::mbar_arrive_expect_tx(&full[stage], 2 * bytes);
@@ -250,9 +262,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       uint32_t chunk_ctr = 0, item_ctr = 0;
-      int hint = 0;
       for (int64_t item = first; item < n_items; item += stride) {
-        const ItemInfo I = decode_item<PAIR>(p, item, hint, rank);
+        const uint32_t slot = item_ctr % ITEM_RING, sph = (item_ctr / ITEM_RING) & 1;
+        tc::mbar_wait(&ifull[slot], sph);
+        const ItemInfo I = s_item[slot];
+        tc::mbar_arrive(&iempty[slot]);
         const uint32_t idesc = tc::idesc_f16_f32(PAIR ? 2 * TC_M : TC_M, I.n);
         const uint32_t ib = item_ctr & 1, iph = (item_ctr >> 1) & 1;
         tc::mbar_wait(&dempty[ib], iph ^ 1);  // D2 buffer of this item free
@@ -274,6 +288,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const uint64_t b2 = tc::smem_desc_sw128(st + b_off + B_PART);
 #pragma unroll
             for (int k = 0; k < TC_BK / 16; ++k) {
+              if (p.dbg & 4) break;  // timing experiment: load pipeline without MMAs
               const uint32_t acc1 = (kb > kb0 || k > 0) ? 1u : 0u;
               const uint32_t acc2 = (kb > 0 || k > 0) ? 1u : 0u;
               const uint64_t adv = static_cast<uint64_t>(k * 2);  // 32 B in 16-B units
@@ -300,21 +315,40 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         ++item_ctr;
       }
     }
+  } else if (warp == 2) {
+    // ------------------------------------------------------ scheduler
+    // decodes the work items ahead of the other roles (the cell search and
+    // tile lookups are dependent global loads that would otherwise stall the
+    // MMA issuer between items)
+    if (lane == 0) {
+      int hint = 0;
+      uint32_t it = 0;
+      for (int64_t item = first; item < n_items; item += stride, ++it) {
+        const uint32_t slot = it % ITEM_RING, iph = (it / ITEM_RING) & 1;
+        const ItemInfo I = decode_item<PAIR>(p, item, hint, rank);
+        tc::mbar_wait(&iempty[slot], iph ^ 1);
+        s_item[slot] = I;
+        tc::mbar_arrive(&ifull[slot]);
+      }
+    }
   } else {
     // ------------------------------------------------------ epilogue
-    const int et = threadIdx.x - 64;      // 0..127
+    const int et = threadIdx.x - 96;      // 0..127
     const int lb = 32 * (warp & 3);       // TMEM lane quarter of this warp
     const int row = lb + lane;            // posting row within the tile
     const bool gauss = p.mode == GIFT_SIM_GAUSSIAN;
     uint32_t chunk_ctr = 0, item_ctr = 0;
-    int hint = 0;
     // accumulator release: own barrier, or the pair leader's (remote arrive)
     const uint32_t rel_t0 = PAIR ? tc::mapa(&tempty[0], 0) : 0u;
     const uint32_t rel_t1 = PAIR ? tc::mapa(&tempty[1], 0) : 0u;
     const uint32_t rel_d0 = PAIR ? tc::mapa(&dempty[0], 0) : 0u;
     const uint32_t rel_d1 = PAIR ? tc::mapa(&dempty[1], 0) : 0u;
     for (int64_t item = first; item < n_items; item += stride) {
-      const ItemInfo I = decode_item<PAIR>(p, item, hint, rank);
+      const uint32_t slot = item_ctr % ITEM_RING, sph = (item_ctr / ITEM_RING) & 1;
+      tc::mbar_wait(&ifull[slot], sph);
+      const ItemInfo I = s_item[slot];
+      named_bar(2, TC_M);  // every epilogue thread has its copy
+      if (et == 0) tc::mbar_arrive(&iempty[slot]);
       const int nseg = I.seg1 - I.seg0;
       const int ng = I.n / 16;  // 16-column groups in use
       for (int i = et; i <= nseg; i += TC_M) s_sp[i] = p.seg_pstart[I.seg0 + i];
@@ -334,7 +368,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const uint32_t base = tmem_base + lane_off + buf * TC_NMAX;
 #pragma unroll
         for (int j = 0; j < TC_NMAX / 16; j += 2) {
-          if (j < ng) {
+          if (j < ng && !(p.dbg & 2)) {
             float v1[16], v2[16];
             tc::tmem_ld_x16(base + j * 16, v1);
             tc::tmem_ld_x16(base + (j + 1) * 16, v2);  // ng is even
@@ -379,7 +413,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           tc::mbar_arrive(&dempty[ib]);
         ++item_ctr;
       }
-      if (!I.live) {  // pair: duplicate tile, nothing to write (keep s_sp reuse ordered)
+      if (!I.live || (p.dbg & 1)) {  // pair: duplicate tile, nothing to write
         named_bar(1, TC_M);
         continue;
       }

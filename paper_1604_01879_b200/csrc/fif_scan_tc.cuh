@@ -29,6 +29,8 @@ struct TcArgs {
   int has_lo;
   int chunk_kb;
   int mt_major;  // item order within a cell: probe-tile-major (1) or posting-tile-major (0)
+  int dbg;       // timing experiments only (GIFT_TC_DBG bits; outputs invalid): 1 = skip
+                 // the epilogue tail, 2 = skip the TMEM drains, 4 = no MMAs, 8 = no loads
 };
 
 bool tc_supported(const gift_fif_view* f);
