@@ -968,6 +968,7 @@ struct ScoreWs {
   int64_t capacity;
   __half* g1;
   __half* g2;
+  float* qn2s;
   ProbeRange* rng;
   int64_t* slot_base;  // gather reduce: [B * V * ma]
 };
@@ -1044,9 +1045,11 @@ bool carve(Arena& ar, const gift_fif_view* f, int64_t nviews, int V, int ma, Sco
     if (!w.rng) return false;
   }
   w.g1 = w.g2 = nullptr;
+  w.qn2s = nullptr;
   if (use_tc(f)) {
     w.g1 = ar.take<__half>(nprobes * f->d + 512);
     w.g2 = ar.take<__half>(nprobes * f->d + 512);
+    w.qn2s = ar.take<float>(nprobes + 128);
     if (!w.g1 || !w.g2) return false;
   }
   if (!w.meta || !w.nz || !w.qn2 || !w.cells || !w.counts || !w.cursor || !w.probe_off ||
@@ -1157,6 +1160,7 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
     ta.seg_pstart = f->seg_pstart;
     ta.pnorm2 = f->pnorm2;
     ta.qn2 = w.qn2;
+    ta.qn2s = w.qn2s;
     ta.K = K;
     ta.d = d;
     ta.ma = ma;

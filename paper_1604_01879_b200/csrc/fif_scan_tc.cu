@@ -110,7 +110,7 @@ __device__ __forceinline__ ItemInfo decode_item(const TcArgs& p, int64_t item, i
   I.seg1 = p.tile_seg1[t];
   I.nb = min(TC_NMAX, cnt - I.mt * TC_NMAX);
   I.pb0 = p.probe_off[lo] + I.mt * TC_NMAX;
-  I.n = I.nb > 64 ? 128 : 64;
+  I.n = (I.nb > 64 || (p.dbg & 16)) ? 128 : 64;  // dbg 16: timing experiment, N = 128 always
   return I;
 }
 
@@ -207,21 +207,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // ------------------------------------------------------ TMA producer
     // (L2 evict-first hints on the postings measured slower: a posting tile
     // is re-read by the next probe tile of its cell)
-    if (lane == 0) {
+    // whole warp runs the loop (warp-uniform operands), one elected lane issues
+    {
       int stage = 0;
       uint32_t phase = 0, it = 0;
       for (int64_t item = first; item < n_items; item += stride, ++it) {
         const uint32_t slot = it % ITEM_RING, iph = (it / ITEM_RING) & 1;
         tc::mbar_wait(&ifull[slot], iph);
         const ItemInfo I = s_item[slot];
-        tc::mbar_arrive(&iempty[slot]);
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&iempty[slot]);
         const int brows = PAIR ? I.n / 2 : I.n;            // probe rows this CTA loads
         const uint32_t a_bytes = has_lo ? 2 * A_TILE : A_TILE;
         const uint32_t bytes = a_bytes + 2 * brows * TC_BK * 2;
         for (int kb = 0; kb < nkb; ++kb) {
+          if (p.dbg & 32) break;  // timing experiment: no smem ring at all
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * stage_bytes;
-          if (p.dbg & 8) {  // timing experiment: MMA pipeline without loads
+          if (!tc::elect_one()) {
+            // other lanes: nothing to issue
+          } else if (p.dbg & 8) {  // timing experiment: MMA pipeline without loads
             if (!PAIR || leader) tc::mbar_arrive(&full[stage]);
           } else if (PAIR) {
             // both CTAs' bytes complete on the leader's full barrier
@@ -241,13 +246,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             tc::mbar_arrive_expect_tx(&full[stage], bytes);
             tc::tma_load_2d(st, &tmA1, &full[stage], kb * TC_BK, I.p0);
             if (has_lo) tc::tma_load_2d(st + A_TILE, &tmA2, &full[stage], kb * TC_BK, I.p0);
+            // B1 rows then B2 rows back to back: one N = 2n MMA operand [b1 | b2]
             for (int x = 0; x < I.n / 64; ++x) {
               tc::tma_load_2d(st + b_off + x * B_BOX, &tmB1, &full[stage], kb * TC_BK,
                               I.pb0 + 64 * x);
-              tc::tma_load_2d(st + b_off + B_TILE + x * B_BOX, &tmB2, &full[stage],
+              tc::tma_load_2d(st + b_off + I.n * TC_BK * 2 + x * B_BOX, &tmB2, &full[stage],
                               kb * TC_BK, I.pb0 + 64 * x);
             }
           }
+          __syncwarp();
           if (++stage == nstages) {
             stage = 0;
             phase ^= 1;
@@ -258,7 +265,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------ MMA issuer
     // (pair: the leader issues cta_group::2 MMAs for both CTAs)
-    if (lane == 0 && leader) {
+    // The whole warp runs the loop (waits, descriptor arithmetic: warp-uniform
+    // values); one elected lane issues the MMAs and commits.
+    if (leader) {
       int stage = 0;
       uint32_t phase = 0;
       uint32_t chunk_ctr = 0, item_ctr = 0;
@@ -266,52 +275,67 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const uint32_t slot = item_ctr % ITEM_RING, sph = (item_ctr / ITEM_RING) & 1;
         tc::mbar_wait(&ifull[slot], sph);
         const ItemInfo I = s_item[slot];
-        tc::mbar_arrive(&iempty[slot]);
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&iempty[slot]);
         const uint32_t idesc = tc::idesc_f16_f32(PAIR ? 2 * TC_M : TC_M, I.n);
+        const uint32_t idesc2 = tc::idesc_f16_f32(TC_M, 2 * I.n);  // single CTA: [b1 | b2]
         const uint32_t ib = item_ctr & 1, iph = (item_ctr >> 1) & 1;
-        tc::mbar_wait(&dempty[ib], iph ^ 1);  // D2 buffer of this item free
-        tc::tc_fence_after();
-        const uint32_t d2 = tmem_base + 256 + ib * TC_NMAX;
+        uint32_t d2 = 0;
+        if (PAIR) {
+          tc::mbar_wait(&dempty[ib], iph ^ 1);  // D2 buffer of this item free
+          tc::tc_fence_after();
+          d2 = tmem_base + 256 + ib * TC_NMAX;
+        }
         for (int kb0 = 0; kb0 < nkb; kb0 += chunk_kb) {
           const uint32_t buf = chunk_ctr & 1, aph = (chunk_ctr >> 1) & 1;
           tc::mbar_wait(&tempty[buf], aph ^ 1);
           tc::tc_fence_after();
-          const uint32_t d1 = tmem_base + buf * TC_NMAX;
+          // pair: D1 per chunk buffer, D2 per item; single: [D1 | D2] per chunk buffer
+          const uint32_t d1 = tmem_base + buf * (PAIR ? TC_NMAX : 2 * TC_NMAX);
           const int kend = min(kb0 + chunk_kb, nkb);
           for (int kb = kb0; kb < kend; ++kb) {
-            tc::mbar_wait(&full[stage], phase);
+            if (!(p.dbg & 32)) tc::mbar_wait(&full[stage], phase);
             tc::tc_fence_after();
             uint8_t* st = smem + stage * stage_bytes;
             const uint64_t a1 = tc::smem_desc_sw128(st);
             const uint64_t a2 = tc::smem_desc_sw128(st + A_TILE);
             const uint64_t b1 = tc::smem_desc_sw128(st + b_off);
             const uint64_t b2 = tc::smem_desc_sw128(st + b_off + B_PART);
+            if (tc::elect_one()) {
 #pragma unroll
-            for (int k = 0; k < TC_BK / 16; ++k) {
-              if (p.dbg & 4) break;  // timing experiment: load pipeline without MMAs
-              const uint32_t acc1 = (kb > kb0 || k > 0) ? 1u : 0u;
-              const uint32_t acc2 = (kb > 0 || k > 0) ? 1u : 0u;
-              const uint64_t adv = static_cast<uint64_t>(k * 2);  // 32 B in 16-B units
-              if (PAIR) {
-                tc::mma_f16_2sm(d1, a1 + adv, b1 + adv, idesc, acc1);
-                tc::mma_f16_2sm(d2, a1 + adv, b2 + adv, idesc, acc2);
-                if (has_lo) tc::mma_f16_2sm(d2, a2 + adv, b1 + adv, idesc, 1u);
-              } else {
-                tc::mma_f16(d1, a1 + adv, b1 + adv, idesc, acc1);
-                tc::mma_f16(d2, a1 + adv, b2 + adv, idesc, acc2);
-                if (has_lo) tc::mma_f16(d2, a2 + adv, b1 + adv, idesc, 1u);
+              for (int k = 0; k < TC_BK / 16; ++k) {
+                if (p.dbg & 4) break;  // timing experiment: load pipeline without MMAs
+                const uint32_t acc1 = (kb > kb0 || k > 0) ? 1u : 0u;
+                const uint32_t acc2 = (kb > 0 || k > 0) ? 1u : 0u;
+                const uint64_t adv = static_cast<uint64_t>(k * 2);  // 32 B in 16-B units
+                if (PAIR) {
+                  tc::mma_f16_2sm(d1, a1 + adv, b1 + adv, idesc, acc1);
+                  tc::mma_f16_2sm(d2, a1 + adv, b2 + adv, idesc, acc2);
+                  if (has_lo) tc::mma_f16_2sm(d2, a2 + adv, b1 + adv, idesc, 1u);
+                } else {
+                  // a1 . [b1 | b2] -> [D1 | D2] (A read once), then D2 += a2 . b1
+                  tc::mma_f16(d1, a1 + adv, b1 + adv, idesc2, acc1);
+                  if (has_lo) tc::mma_f16(d1 + I.n, a2 + adv, b1 + adv, idesc, 1u);
+                }
+              }
+              if (!(p.dbg & 32)) {
+                if (PAIR) tc::mma_commit_2sm(&empty[stage], 0x3); else tc::mma_commit(&empty[stage]);
               }
             }
-            if (PAIR) tc::mma_commit_2sm(&empty[stage], 0x3); else tc::mma_commit(&empty[stage]);
+            __syncwarp();
             if (++stage == nstages) {
               stage = 0;
               phase ^= 1;
             }
           }
-          if (PAIR) tc::mma_commit_2sm(&tfull[buf], 0x3); else tc::mma_commit(&tfull[buf]);
+          if (tc::elect_one()) {
+            if (PAIR) tc::mma_commit_2sm(&tfull[buf], 0x3); else tc::mma_commit(&tfull[buf]);
+          }
+          __syncwarp();
           ++chunk_ctr;
         }
-        if (PAIR) tc::mma_commit_2sm(&dfull[ib], 0x3); else tc::mma_commit(&dfull[ib]);
+        if (PAIR && tc::elect_one()) tc::mma_commit_2sm(&dfull[ib], 0x3);
+        __syncwarp();
         ++item_ctr;
       }
     }
@@ -351,12 +375,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       if (et == 0) tc::mbar_arrive(&iempty[slot]);
       const int nseg = I.seg1 - I.seg0;
       const int ng = I.n / 16;  // 16-column groups in use
-      for (int i = et; i <= nseg; i += TC_M) s_sp[i] = p.seg_pstart[I.seg0 + i];
-      for (int m = et; m < TC_NMAX; m += TC_M) {
-        float q = 0.f;
-        if (m < I.nb) q = p.qn2[p.probe_list[I.pb0 + m] / p.ma];
-        s_qn2[m] = q;
-      }
+      // tail inputs, loaded now and staged to shared memory only at the tail
+      // (their latency overlaps the drains): segment starts (nseg + 1 <= 129)
+      // and the probe-sorted |q|^2
+      const int sp_a = et <= nseg ? p.seg_pstart[I.seg0 + et] : 0;
+      const int sp_b = et + TC_M <= nseg ? p.seg_pstart[I.seg0 + et + TC_M] : 0;
+      const float qn_r = et < I.nb ? p.qn2s[I.pb0 + et] : 0.f;
       float acc[TC_NMAX];
 #pragma unroll
       for (int n = 0; n < TC_NMAX; ++n) acc[n] = 0.f;
@@ -365,18 +389,33 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const uint32_t buf = chunk_ctr & 1, aph = (chunk_ctr >> 1) & 1;
         tc::mbar_wait(&tfull[buf], aph);
         tc::tc_fence_after();
-        const uint32_t base = tmem_base + lane_off + buf * TC_NMAX;
+        if (PAIR) {
+          const uint32_t base = tmem_base + lane_off + buf * TC_NMAX;
 #pragma unroll
-        for (int j = 0; j < TC_NMAX / 16; j += 2) {
-          if (j < ng && !(p.dbg & 2)) {
-            float v1[16], v2[16];
-            tc::tmem_ld_x16(base + j * 16, v1);
-            tc::tmem_ld_x16(base + (j + 1) * 16, v2);  // ng is even
-            tc::tmem_ld_wait();
+          for (int j = 0; j < TC_NMAX / 16; j += 2) {
+            if (j < ng && !(p.dbg & 2)) {
+              float v1[16], v2[16];
+              tc::tmem_ld_x16(base + j * 16, v1);
+              tc::tmem_ld_x16(base + (j + 1) * 16, v2);  // ng is even
+              tc::tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              acc[j * 16 + i] += v1[i];
-              acc[(j + 1) * 16 + i] += v2[i];
+              for (int i = 0; i < 16; ++i) {
+                acc[j * 16 + i] += v1[i];
+                acc[(j + 1) * 16 + i] += v2[i];
+              }
+            }
+          }
+        } else {  // [D1 | D2] of this chunk: acc += D1 + 2^-11 D2
+          const uint32_t base = tmem_base + lane_off + buf * 2 * TC_NMAX;
+#pragma unroll
+          for (int j = 0; j < TC_NMAX / 16; ++j) {
+            if (j < ng && !(p.dbg & 2)) {
+              float v1[16], v2[16];
+              tc::tmem_ld_x16(base + j * 16, v1);
+              tc::tmem_ld_x16(base + I.n + j * 16, v2);
+              tc::tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) acc[j * 16 + i] += fmaf(v2[i], SPLIT_INV, v1[i]);
             }
           }
         }
@@ -387,7 +426,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           tc::mbar_arrive(&tempty[buf]);
         ++chunk_ctr;
       }
-      {  // the item's correction terms, once: acc += 2^-11 D2
+      if (!PAIR) {
+        ++item_ctr;
+      } else {  // the item's correction terms, once: acc += 2^-11 D2
         const uint32_t ib = item_ctr & 1, iph = (item_ctr >> 1) & 1;
         tc::mbar_wait(&dfull[ib], iph);
         tc::tc_fence_after();
@@ -417,10 +458,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         named_bar(1, TC_M);
         continue;
       }
+      if (et <= nseg) s_sp[et] = sp_a;
+      if (et + TC_M <= nseg) s_sp[et + TC_M] = sp_b;
+      s_qn2[et] = qn_r;
       const float pn = (I.p0 + row < I.p1) ? p.pnorm2[I.p0 + row] : 0.f;
       const int64_t S_c = p.seg_off[I.c + 1] - p.seg_off[I.c];
       const int64_t seg_base = p.seg_off[I.c];
       const int64_t obase = p.outbase[I.c];
+      // thread -> (column mc = et % 32, segments et / 32, +4, ...): no division
+      const int mc = et & (EPI_COLS - 1), sg0 = et >> 5;
       // 32-column slices: stage -> per-segment max over rows -> store
 #pragma unroll
       for (int sl0 = 0; sl0 < TC_NMAX; sl0 += EPI_COLS) {
@@ -433,10 +479,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
           named_bar(1, TC_M);
           const int ncol = min(EPI_COLS, I.nb - sl0);
-          for (int idx = et; idx < nseg * ncol; idx += TC_M) {
-            const int mc = idx / nseg;
-            const int sl = idx - mc * nseg;
-            const int m = sl0 + mc;
+          const int m = sl0 + mc;
+          for (int sl = sg0; mc < ncol && sl < nseg; sl += TC_M / EPI_COLS) {
             const int sp0 = s_sp[sl], sp1 = s_sp[sl + 1];
             const int r0 = max(sp0, I.p0) - I.p0, r1 = min(sp1, I.p1) - I.p0;
             float mx = -INFINITY;
@@ -486,11 +530,14 @@ __global__ void probe_gather_split_kernel(const float* __restrict__ Q, int d, in
                                           const int32_t* __restrict__ probe_list,
                                           const int32_t* __restrict__ probe_off, int K,
                                           const int64_t* __restrict__ meta,
-                                          __half* __restrict__ g1, __half* __restrict__ g2) {
+                                          __half* __restrict__ g1, __half* __restrict__ g2,
+                                          const float* __restrict__ qn2,
+                                          float* __restrict__ qn2s) {
   if (meta[M_OVERFLOW]) return;
   const int s = blockIdx.x;
   if (s >= probe_off[K]) return;
   const int64_t view = probe_list[s] / ma;
+  if (threadIdx.x == 0) qn2s[s] = qn2[view];  // |q|^2 in probe order (scan epilogue)
   const float* q = Q + view * d;
   __half* o1 = g1 + static_cast<int64_t>(s) * d;
   __half* o2 = g2 + static_cast<int64_t>(s) * d;
@@ -553,7 +600,7 @@ int launch_scan_tc(const gift_fif_view* f, const float* Q, int64_t nprobes_max, 
   const int d = f->d;
   const bool pair = tc_pair_enabled() && sm_count() >= 2;
   probe_gather_split_kernel<<<static_cast<unsigned>(max64(nprobes_max, 1)), 128, 0, st>>>(
-      Q, d, a.ma, a.probe_list, a.probe_off, f->K, a.meta, g1, g2);
+      Q, d, a.ma, a.probe_list, a.probe_off, f->K, a.meta, g1, g2, a.qn2, a.qn2s);
   GIFT_LAUNCH_CHECK();
   CUtensorMap mA1, mA2, mB1, mB2, mB1h, mB2h;
   int rc = make_map(&mA1, f->feat_hi, f->n_postings, d, TC_M);

@@ -24,6 +24,7 @@ struct TcArgs {
   const int32_t* seg_pstart;
   const float* pnorm2;
   const float* qn2;
+  float* qn2s;  // [nprobes] |q|^2 in probe (cell-major) order, written by the gather
   int K, d, ma, mode;
   float inv_sigma2;
   int has_lo;

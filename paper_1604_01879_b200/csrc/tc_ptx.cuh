@@ -149,6 +149,20 @@ __host__ __device__ constexpr uint32_t idesc_f16_f32(uint32_t M, uint32_t N) {
          | ((M >> 4) << 24);       // M / 16
 }
 
+// one lane of a converged warp (the others skip): lets the compiler keep the
+// warp-uniform MMA operands in uniform registers
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "elect.sync _|P, 0xffffffff;\n"
+      "selp.u32 %0, 1, 0, P;\n"
+      "}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // ------------------------------------------------------------- CTA pairs
 // (cluster of 2 on one TPC; cta_group::2 MMA spans both SMs' smem and TMEM)
 __device__ __forceinline__ uint32_t cluster_ctarank() {
