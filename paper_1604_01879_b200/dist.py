@@ -153,6 +153,10 @@ class ShardedEngine:
         self.runner = eg.ScoreRunner()
         from .matching import sim_mode
         self.mode = sim_mode(cfg.similarity)
+        base, n_local = fif.ord_base, fif.n_local
+        self.idrank_local = idrank[base:base + n_local].contiguous()
+        # local shapes in global id-rank order (the sparse S-IF's zero-score fill)
+        self.order_local = torch.argsort(self.idrank_local).to(torch.int32).contiguous()
 
     def run(self, Q: torch.Tensor, top_k: int, rerank: bool = True, self_global=None):
         cfg = self.cfg
@@ -160,21 +164,27 @@ class ShardedEngine:
         dev = Q.device
         if self_global is None:
             self_global = torch.full((B,), -1, dtype=torch.int64, device=dev)
-        s = self.runner.score(self.fif, Q, cfg.ma, self.mode, cfg.sigma)
         base = self.fif.ord_base
-        if rerank:
-            k2 = min(cfg.k2, self.n_global)
-            li, lv = eg.topk_rows(s, k2, positive_only=True, ord_base=base)
-            nbr, _ = all_gather_topk(lv, li, ordinal_tiebreak(li), k2, self.group)
-            fa = eg.act_mean(self.raw, nbr.to(torch.int32).contiguous())
-            final = self.sif.query(fa)
-        else:
-            final = s
         k = min(top_k, self.n_global)
         loc_self = (self_global - base)
         loc_self = torch.where((loc_self >= 0) & (loc_self < self.fif.n_local), loc_self,
                                torch.full_like(loc_self, -1)).to(torch.int32)
-        li, lv = eg.topk_rows(final, k, idrank=self.idrank[base:base +
-                              self.fif.n_local].contiguous(), self_local=loc_self, ord_base=base)
+        if rerank:
+            # local top-k2 straight from the reduce's candidates (no dense row)
+            k2 = min(cfg.k2, self.n_global)
+            _, cs, ci = self.runner.score(self.fif, Q, cfg.ma, self.mode, cfg.sigma, cand_k=k2,
+                                          dense=False)
+            li, lv = eg.topk_candidates(cs, ci, k2, positive_only=True)
+            nbr, _ = all_gather_topk(lv, li, ordinal_tiebreak(li), k2, self.group)
+            fa = eg.act_mean(self.raw, nbr.to(torch.int32).contiguous())
+            if k <= 256:
+                li, lv = self.sif.query_topk(fa, k, self.order_local, self.idrank_local, loc_self)
+            else:
+                li, lv = eg.topk_rows(self.sif.query(fa), k, idrank=self.idrank_local,
+                                      self_local=loc_self, ord_base=base)
+        else:
+            s = self.runner.score(self.fif, Q, cfg.ma, self.mode, cfg.sigma)
+            li, lv = eg.topk_rows(s, k, idrank=self.idrank_local, self_local=loc_self,
+                                  ord_base=base)
         tb = ranking_tiebreak(li, self.idrank, self_global)
         return all_gather_topk(lv, li, tb, k, self.group)

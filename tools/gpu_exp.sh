@@ -1,4 +1,3 @@
 set -x
-timeout 1800 python bench.py --config c4 --steps 5 --warmup 3 > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err; echo c4=$?
-timeout 600 python bench.py --steps 10 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; echo b2=$?
-timeout 1800 python bench.py --config c3 --steps 8 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err; echo c3=$?
+timeout 600 python -m pytest tests/test_gpu_sharded.py tests/test_gpu_streamed.py -x -q > gpurun_out/pytest_shard.log 2>&1; echo pytest=$?
+timeout 900 python bench.py --config c4s --shard --steps 5 > gpurun_out/bench_c4s_shard.json 2> gpurun_out/bench_c4s_shard.err; echo sh=$?
