@@ -159,6 +159,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int nstages = has_lo ? Ring<PAIR>::STAGES_LO : Ring<PAIR>::STAGES_NOLO;
   const int b_off = has_lo ? 2 * A_TILE : A_TILE;  // B1 offset in a stage
   constexpr int B_PART = Ring<PAIR>::B_PART;
+  // combined B operand [b1 | b2] (one N = 2n MMA per k-step, A read once):
+  // always on a single CTA; on a pair only without the lo plane (CTA r then
+  // holds plane r: the pair's B is exactly [b1 | b2]); a pair with the lo
+  // plane keeps three MMAs with half of each plane per CTA and D2 per item
+  const bool cb = !PAIR || !has_lo;
   const uint32_t rank = PAIR ? tc::cluster_ctarank() : 0u;
   const bool leader = rank == 0;
   // item sequence: per CTA, or per pair (both CTAs walk the same items)
@@ -217,9 +222,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const ItemInfo I = s_item[slot];
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&iempty[slot]);
-        const int brows = PAIR ? I.n / 2 : I.n;            // probe rows this CTA loads
+        const int brows = PAIR ? I.n / 2 : I.n;            // probe rows per plane half
         const uint32_t a_bytes = has_lo ? 2 * A_TILE : A_TILE;
-        const uint32_t bytes = a_bytes + 2 * brows * TC_BK * 2;
+        // this CTA's B bytes: both planes (single), one whole plane (pair, cb),
+        // half of each plane (pair, lo)
+        const uint32_t bytes = a_bytes + (PAIR && cb ? I.n : 2 * brows) * TC_BK * 2;
         for (int kb = 0; kb < nkb; ++kb) {
           if (p.dbg & 32) break;  // timing experiment: no smem ring at all
           tc::mbar_wait(&empty[stage], phase ^ 1);
@@ -235,7 +242,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             tc::tma_load_2d_2sm(st, &tmA1, lbar, kb * TC_BK, I.p0);
             if (has_lo) tc::tma_load_2d_2sm(st + A_TILE, &tmA2, lbar, kb * TC_BK, I.p0);
             const int r0 = I.pb0 + static_cast<int>(rank) * brows;
-            if (brows == 64) {
+            if (cb) {  // CTA r: plane r, all n probe rows
+              const CUtensorMap* pm = rank == 0 ? &tmB1 : &tmB2;
+              for (int x = 0; x < I.n / 64; ++x)
+                tc::tma_load_2d_2sm(st + b_off + x * B_BOX, pm, lbar, kb * TC_BK,
+                                    I.pb0 + 64 * x);
+            } else if (brows == 64) {
               tc::tma_load_2d_2sm(st + b_off, &tmB1, lbar, kb * TC_BK, r0);
               tc::tma_load_2d_2sm(st + b_off + B_PART, &tmB2, lbar, kb * TC_BK, r0);
             } else {
@@ -278,10 +290,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&iempty[slot]);
         const uint32_t idesc = tc::idesc_f16_f32(PAIR ? 2 * TC_M : TC_M, I.n);
-        const uint32_t idesc2 = tc::idesc_f16_f32(TC_M, 2 * I.n);  // single CTA: [b1 | b2]
+        const uint32_t idesc2 = tc::idesc_f16_f32(PAIR ? 2 * TC_M : TC_M, 2 * I.n);  // [b1 | b2]
         const uint32_t ib = item_ctr & 1, iph = (item_ctr >> 1) & 1;
         uint32_t d2 = 0;
-        if (PAIR) {
+        if (!cb) {
           tc::mbar_wait(&dempty[ib], iph ^ 1);  // D2 buffer of this item free
           tc::tc_fence_after();
           d2 = tmem_base + 256 + ib * TC_NMAX;
@@ -291,7 +303,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           tc::mbar_wait(&tempty[buf], aph ^ 1);
           tc::tc_fence_after();
           // pair: D1 per chunk buffer, D2 per item; single: [D1 | D2] per chunk buffer
-          const uint32_t d1 = tmem_base + buf * (PAIR ? TC_NMAX : 2 * TC_NMAX);
+          const uint32_t d1 = tmem_base + buf * (cb ? 2 * TC_NMAX : TC_NMAX);
           const int kend = min(kb0 + chunk_kb, nkb);
           for (int kb = kb0; kb < kend; ++kb) {
             if (!(p.dbg & 32)) tc::mbar_wait(&full[stage], phase);
@@ -308,10 +320,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const uint32_t acc1 = (kb > kb0 || k > 0) ? 1u : 0u;
                 const uint32_t acc2 = (kb > 0 || k > 0) ? 1u : 0u;
                 const uint64_t adv = static_cast<uint64_t>(k * 2);  // 32 B in 16-B units
-                if (PAIR) {
+                if (PAIR && cb) {  // [D1 | D2] = a1 . [b1 | b2], M = 256
+                  tc::mma_f16_2sm(d1, a1 + adv, b1 + adv, idesc2, acc1);
+                } else if (PAIR) {
                   tc::mma_f16_2sm(d1, a1 + adv, b1 + adv, idesc, acc1);
                   tc::mma_f16_2sm(d2, a1 + adv, b2 + adv, idesc, acc2);
-                  if (has_lo) tc::mma_f16_2sm(d2, a2 + adv, b1 + adv, idesc, 1u);
+                  tc::mma_f16_2sm(d2, a2 + adv, b1 + adv, idesc, 1u);
                 } else {
                   // a1 . [b1 | b2] -> [D1 | D2] (A read once), then D2 += a2 . b1
                   tc::mma_f16(d1, a1 + adv, b1 + adv, idesc2, acc1);
@@ -334,7 +348,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           __syncwarp();
           ++chunk_ctr;
         }
-        if (PAIR && tc::elect_one()) tc::mma_commit_2sm(&dfull[ib], 0x3);
+        if (!cb && tc::elect_one()) tc::mma_commit_2sm(&dfull[ib], 0x3);
         __syncwarp();
         ++item_ctr;
       }
@@ -389,7 +403,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const uint32_t buf = chunk_ctr & 1, aph = (chunk_ctr >> 1) & 1;
         tc::mbar_wait(&tfull[buf], aph);
         tc::tc_fence_after();
-        if (PAIR) {
+        if (!cb) {
           const uint32_t base = tmem_base + lane_off + buf * TC_NMAX;
 #pragma unroll
           for (int j = 0; j < TC_NMAX / 16; j += 2) {
@@ -426,7 +440,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           tc::mbar_arrive(&tempty[buf]);
         ++chunk_ctr;
       }
-      if (!PAIR) {
+      if (cb) {
         ++item_ctr;
       } else {  // the item's correction terms, once: acc += 2^-11 D2
         const uint32_t ib = item_ctr & 1, iph = (item_ctr >> 1) & 1;
