@@ -1134,7 +1134,7 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
   probe_plan_kernel<<<1, PLAN_THREADS, 0, st>>>(w.counts, K, f->seg_off, f->tile_off, w.probe_off,
                                                 w.outbase, w.item_off, w.cursor, w.meta, w.capacity,
                                                 use_tc(f) ? 128 : simt::TB,
-                                                use_tc(f) && tc_pair_enabled() ? 2 : 1);
+                                                use_tc(f) && tc_pair_enabled(f) ? 2 : 1);
   GIFT_LAUNCH_CHECK();
   probe_scatter_kernel<<<static_cast<unsigned>(cdiv(nprobes, 256)), 256, 0, st>>>(
       w.cells, nprobes, w.probe_off, w.cursor, w.probe_list, w.probe_rank);

@@ -35,9 +35,10 @@ struct TcArgs {
 };
 
 bool tc_supported(const gift_fif_view* f);
-// GIFT_TC_PAIR=1: the scan runs on CTA pairs (cta_group::2, M = 256): a work
-// item is two consecutive posting tiles of a cell x one probe tile
-bool tc_pair_enabled();
+// The scan on CTA pairs (cta_group::2, M = 256): a work item is two
+// consecutive posting tiles of a cell x one probe tile.  GIFT_TC_PAIR=0|1
+// overrides the default (pairs with the f32 lo plane).
+bool tc_pair_enabled(const gift_fif_view* f);
 // quantize with need_order = false: when exactly ma candidates survive the
 // margin test their order is not resolved (the F-IF scan takes a max over
 // the ma cells, matching.py:153-159, so only the set matters)
