@@ -1,4 +1,4 @@
 set -x
-for pair in 0 1 0 1; do
-GIFT_TC_PAIR=$pair timeout 600 python bench.py --steps 10 --no-cpu-baseline >> gpurun_out/bench_c2_pp.json 2> /dev/null; echo b2=$?
-done
+C4="python tools/stage_profile.py --config c4s --steps 1 --reduce owner"
+timeout 300 $C4 > gpurun_out/plain_c4.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:fif_scan_tc -s 99 -c 1 -o gpurun_out/scan_c4s_src $C4 > gpurun_out/ncu_src.log 2>&1; echo s4=$?
