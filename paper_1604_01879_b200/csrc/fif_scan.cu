@@ -494,7 +494,8 @@ struct GatherArgs {
   const int64_t* meta;
   const int32_t* vq;
   int B, V, ma, K, rs, n_ranges, G;
-  int chunk, nchunk;             // owner reduce: segments per CTA, chunks per cell
+  int chunk, nchunk;             // owner reduce: segments per item, max items per cell
+  const int64_t* work_off;       // owner reduce: [B * slots + 1] work-list offsets per probe
   int64_t n_local, ord_base;
   double* scores;                // [B][n_local] or null (candidates only)
   int cand_k;
@@ -849,45 +850,63 @@ __global__ void __launch_bounds__(GR_THREADS) fif_gather_reduce_kernel(GatherArg
 // probed (its owner), so every touched pair is scored exactly once, with the
 // gather reduce's per-pair sum.  Dense scores (if requested) are zeroed
 // beforehand; candidates: the CTA's best cand_k, rows [b][slots * nchunk].
+// Owner work list: probe p = (query b, slot j) contributes ceil(S_c / chunk)
+// work items when j is the query's first slot probing its cell c (else 0).
+__global__ void owner_count_kernel(const int32_t* __restrict__ cells,
+                                   const int64_t* __restrict__ seg_off, int64_t nprobes, int slots,
+                                   int chunk, const int64_t* __restrict__ meta,
+                                   int32_t* __restrict__ cnt) {
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= nprobes) return;
+  const int c = cells[p];
+  int n = 0;
+  if (c >= 0 && !meta[M_OVERFLOW]) {
+    const int64_t b0 = p - p % slots;
+    bool first = true;
+    for (int64_t q = b0; q < p; ++q) first &= cells[q] != c;
+    if (first) n = static_cast<int>((seg_off[c + 1] - seg_off[c] + chunk - 1) / chunk);
+  }
+  cnt[p] = n;
+}
+
 template <int W>
 __global__ void __launch_bounds__(GR_THREADS) fif_owner_reduce_kernel(GatherArgs a) {
   extern __shared__ __align__(16) double s_tab[];
-  __shared__ int s_skip;
   __shared__ double s_ws[GR_THREADS / 32][RED_MAXK];
   __shared__ int32_t s_wo[GR_THREADS / 32][RED_MAXK];
   if (a.meta[M_OVERFLOW]) return;
   const int slots = a.V * a.ma;
-  const int b = blockIdx.x / slots, j = blockIdx.x - b * slots;
-  const int chunk_id = blockIdx.y;
+  const int64_t nprobes = static_cast<int64_t>(a.B) * slots;
+  const int64_t n_work = a.work_off[nprobes];
   const int ck = a.cand_k;
+  const GrTabs t = carve_tabs<W>(s_tab, 1, slots, a.K);
+  int tab_b = -1;  // query whose tables are in shared memory
+  // contiguous runs of the (query-major) work list per CTA: consecutive items
+  // mostly share the query, so its tables are built once per run
+  const int64_t per = (n_work + gridDim.x - 1) / gridDim.x;
+  const int64_t w0 = static_cast<int64_t>(blockIdx.x) * per;
+  const int64_t w1 = min64(n_work, w0 + per);
+  for (int64_t w = w0; w < w1; ++w) {
+  // probe of work item w: largest p with work_off[p] <= w
+  int64_t lo = 0, hi = nprobes - 1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) >> 1;
+    if (a.work_off[mid] <= w) lo = mid; else hi = mid - 1;
+  }
+  const int64_t pr = lo;
+  const int b = static_cast<int>(pr / slots), j = static_cast<int>(pr - static_cast<int64_t>(b) * slots);
+  const int chunk_id = static_cast<int>(w - a.work_off[pr]);
   const int64_t cand_at =
       ((static_cast<int64_t>(b) * slots + j) * a.nchunk + chunk_id) * static_cast<int64_t>(ck);
-  const int c = a.cells[static_cast<int64_t>(b) * slots + j];
-  int64_t k0 = 0, k1 = 0;
-  if (c >= 0) {
-    const int64_t S_c = a.seg_off[c + 1] - a.seg_off[c];
-    k0 = static_cast<int64_t>(chunk_id) * a.chunk;
-    k1 = min64(S_c, k0 + a.chunk);
+  const int c = a.cells[pr];
+  const int64_t S_c = a.seg_off[c + 1] - a.seg_off[c];
+  const int64_t k0 = static_cast<int64_t>(chunk_id) * a.chunk;
+  const int64_t k1 = min64(S_c, k0 + a.chunk);
+  if (b != tab_b) {
+    __syncthreads();  // previous item's readers are done with the tables
+    build_tabs<W>(a, t, 1, b, 1);
+    tab_b = b;
   }
-  if (threadIdx.x == 0) s_skip = k0 >= k1;
-  __syncthreads();
-  if (!s_skip) {  // an earlier slot of the query probing the same cell owns it
-    bool dup = false;
-    for (int jj = threadIdx.x; jj < j; jj += GR_THREADS)
-      dup |= a.cells[static_cast<int64_t>(b) * slots + jj] == c;
-    if (__syncthreads_or(dup) && threadIdx.x == 0) s_skip = 1;
-  }
-  __syncthreads();
-  if (s_skip) {
-    if (ck > 0)
-      for (int r = threadIdx.x; r < ck; r += GR_THREADS) {
-        a.cand_s[cand_at + r] = 0.0;
-        a.cand_i[cand_at + r] = -1;
-      }
-    return;
-  }
-  const GrTabs t = carve_tabs<W>(s_tab, 1, slots, a.K);
-  build_tabs<W>(a, t, 1, b, 1);
   const double denom = static_cast<double>(a.vq ? a.vq[b] : a.V);
   double ls[RED_MAXK];
   int32_t lo_[RED_MAXK];
@@ -916,32 +935,35 @@ __global__ void __launch_bounds__(GR_THREADS) fif_owner_reduce_kernel(GatherArgs
     if (a.scores) a.scores[static_cast<int64_t>(b) * a.n_local + s] = score;
     if (ck > 0) cand_insert(ls, lo_, ck, score, ord);
   }
-  if (ck <= 0) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double os[RED_MAXK];
-  int32_t oo[RED_MAXK];
-  warp_select(ls, lo_, ck, os, oo);
-  if (lane == 0)
-#pragma unroll
-    for (int r = 0; r < RED_MAXK; ++r) {
-      s_ws[warp][r] = r < ck ? os[r] : -INFINITY;
-      s_wo[warp][r] = r < ck ? oo[r] : -1;
-    }
-  __syncthreads();
-  if (warp == 0) {  // merge the warps' lists: lane w < 8 holds warp w's list
-#pragma unroll
-    for (int q = 0; q < RED_MAXK; ++q) {
-      ls[q] = lane < GR_THREADS / 32 ? s_ws[lane][q] : -INFINITY;
-      lo_[q] = lane < GR_THREADS / 32 ? s_wo[lane][q] : -1;
-    }
+  if (ck > 0) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double os[RED_MAXK];
+    int32_t oo[RED_MAXK];
     warp_select(ls, lo_, ck, os, oo);
     if (lane == 0)
 #pragma unroll
-      for (int r = 0; r < RED_MAXK; ++r)
-        if (r < ck) {
-          a.cand_s[cand_at + r] = oo[r] >= 0 ? os[r] : 0.0;
-          a.cand_i[cand_at + r] = oo[r];
-        }
+      for (int r = 0; r < RED_MAXK; ++r) {
+        s_ws[warp][r] = r < ck ? os[r] : -INFINITY;
+        s_wo[warp][r] = r < ck ? oo[r] : -1;
+      }
+    __syncthreads();
+    if (warp == 0) {  // merge the warps' lists: lane w < 8 holds warp w's list
+#pragma unroll
+      for (int q = 0; q < RED_MAXK; ++q) {
+        ls[q] = lane < GR_THREADS / 32 ? s_ws[lane][q] : -INFINITY;
+        lo_[q] = lane < GR_THREADS / 32 ? s_wo[lane][q] : -1;
+      }
+      warp_select(ls, lo_, ck, os, oo);
+      if (lane == 0)
+#pragma unroll
+        for (int r = 0; r < RED_MAXK; ++r)
+          if (r < ck) {
+            a.cand_s[cand_at + r] = oo[r] >= 0 ? os[r] : 0.0;
+            a.cand_i[cand_at + r] = oo[r];
+          }
+    }
+    __syncthreads();  // s_ws reuse by the next item
+  }
   }
 }
 
@@ -971,6 +993,10 @@ struct ScoreWs {
   float* qn2s;
   ProbeRange* rng;
   int64_t* slot_base;  // gather reduce: [B * V * ma]
+  int32_t* own_cnt;    // owner reduce: work items per probe
+  int64_t* own_off;    // [nprobes + 1]
+  void* own_ws;        // scan workspace
+  size_t own_ws_bytes;
 };
 
 bool use_tc(const gift_fif_view* f) {
@@ -1037,9 +1063,20 @@ bool carve(Arena& ar, const gift_fif_view* f, int64_t nviews, int V, int ma, Sco
   w.qws = ar.take<char>(static_cast<int64_t>(w.qws_bytes));
   w.rng = nullptr;
   w.slot_base = nullptr;
+  w.own_cnt = nullptr;
+  w.own_off = nullptr;
+  w.own_ws = nullptr;
+  w.own_ws_bytes = 0;
   if (reduce_mode(f, V, ma) != RM_RANGE) {
     w.slot_base = ar.take<int64_t>(nprobes);
     if (!w.slot_base) return false;
+    if (reduce_mode(f, V, ma) == RM_OWNER) {
+      w.own_cnt = ar.take<int32_t>(nprobes);
+      w.own_off = ar.take<int64_t>(nprobes + 1);
+      w.own_ws_bytes = scan_ws_bytes(nprobes + 1);
+      w.own_ws = ar.take<char>(static_cast<int64_t>(w.own_ws_bytes));
+      if (!w.own_cnt || !w.own_off || !w.own_ws) return false;
+    }
   } else {
     w.rng = ar.take<ProbeRange>(nprobes * cdiv(max64(f->n_local, 1), reduce_rs(V, f->n_local)));
     if (!w.rng) return false;
@@ -1247,9 +1284,20 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
       ga.n_ranges = V * ma * ga.nchunk;
       if (out_scores)
         GIFT_CUDA_TRY(cudaMemsetAsync(out_scores, 0, sizeof(double) * B * f->n_local, st));
+      if (ga.cand_k > 0) {  // slots without work keep "no candidate"
+        const size_t nc = static_cast<size_t>(B) * ga.n_ranges * ga.cand_k;
+        GIFT_CUDA_TRY(cudaMemsetAsync(cand_s, 0, sizeof(double) * nc, st));
+        GIFT_CUDA_TRY(cudaMemsetAsync(cand_i, 0xff, sizeof(int32_t) * nc, st));
+      }
+      owner_count_kernel<<<static_cast<unsigned>(cdiv(nprobes, 256)), 256, 0, st>>>(
+          w.cells, f->seg_off, nprobes, V * ma, OWN_CHUNK, w.meta, w.own_cnt);
+      GIFT_LAUNCH_CHECK();
+      rc = scan_exclusive_i32_to_i64(w.own_cnt, w.own_off, nprobes, true, w.own_ws,
+                                     w.own_ws_bytes, st);
+      if (rc) return rc;
+      ga.work_off = w.own_off;
       const int smem = static_cast<int>(gather_smem(1, 0, K, V * ma, W));
-      dim3 grid(static_cast<unsigned>(static_cast<int64_t>(B) * V * ma),
-                static_cast<unsigned>(ga.nchunk));
+      dim3 grid(static_cast<unsigned>(sm_count() * 8));
       if (W == 1) {
         GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_owner_reduce_kernel<1>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
