@@ -50,11 +50,15 @@ extern "C" {
 /* Device-resident first inverted file of one shard (cell-major CSR).
  * Replaces matching.FirstInvertedFile (matching.py:64-103).  Built by the
  * gift_fif_* build calls below; all pointers are device pointers. */
+#define GIFT_FIF_TILED_SEGMENTS 1
+
 typedef struct gift_fif_view {
   int32_t K;                 /* codebook size                                 */
   int32_t d;                 /* feature dimension                             */
   int32_t dtype;             /* storage dtype of feat: GIFT_F32 / GIFT_F16    */
-  int32_t pad0;
+  int32_t flags;             /* GIFT_FIF_TILED_SEGMENTS: no segment is longer   */
+                             /* than a scan tile (every compact entry is       */
+                             /* written once; no zero-fill needed)             */
   int64_t n_postings;        /* P                                             */
   int64_t n_segments;        /* S: (cell, shape) runs                          */
   int64_t n_tiles;           /* T: scan tiles (whole segments, <= tile_n)     */

@@ -20,6 +20,7 @@ LIB_PATH = os.path.join(_HERE, "libgift.so")
 
 GIFT_F32, GIFT_F16, GIFT_F64 = 0, 1, 2
 SIM_COSINE, SIM_GAUSSIAN = 0, 1
+FIF_TILED_SEGMENTS = 1  # gift_fif_view.flags (include/gift.h)
 
 _c_i32 = ctypes.c_int32
 _c_i64 = ctypes.c_int64
@@ -31,7 +32,7 @@ _c_p = ctypes.c_void_p
 class FifView(ctypes.Structure):
     """Mirror of `gift_fif_view` (include/gift.h)."""
     _fields_ = [
-        ("K", _c_i32), ("d", _c_i32), ("dtype", _c_i32), ("pad0", _c_i32),
+        ("K", _c_i32), ("d", _c_i32), ("dtype", _c_i32), ("flags", _c_i32),
         ("n_postings", _c_i64), ("n_segments", _c_i64), ("n_tiles", _c_i64),
         ("n_local", _c_i64), ("ord_base", _c_i64),
         ("cell_off", _c_p), ("post_ord", _c_p), ("feat", _c_p), ("pnorm2", _c_p),

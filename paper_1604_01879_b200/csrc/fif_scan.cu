@@ -1176,8 +1176,10 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
   probe_scatter_kernel<<<static_cast<unsigned>(cdiv(nprobes, 256)), 256, 0, st>>>(
       w.cells, nprobes, w.probe_off, w.cursor, w.probe_list, w.probe_rank);
   GIFT_LAUNCH_CHECK();
-  compact_zero_kernel<<<sm_count() * 4, 256, 0, st>>>(w.compact, w.meta);
-  GIFT_LAUNCH_CHECK();
+  if (!(f->flags & GIFT_FIF_TILED_SEGMENTS) || !use_tc(f)) {  // atomicMax targets need zeros
+    compact_zero_kernel<<<sm_count() * 4, 256, 0, st>>>(w.compact, w.meta);
+    GIFT_LAUNCH_CHECK();
+  }
 
   if (use_tc(f)) {
     TcArgs ta;

@@ -163,6 +163,7 @@ class DeviceFif:
         v.shape_seg = self.shape_seg.data_ptr()
         v.shape_seg_cell = self.shape_seg_cell.data_ptr()
         v.max_cell_segments = self.smax
+        v.flags = nat.FIF_TILED_SEGMENTS if self.seg_len_max <= nat.lib().gift_fif_tile_n() else 0
         self.view = v
         return v
 
@@ -335,6 +336,7 @@ class DeviceFif:
         self.shape_off = offsets_from_sorted(k2, n_local, stream)  # [n_local+1]
         self.shape_post = v2.to(torch.int64)
         seg_sizes = self.seg_off[1:] - self.seg_off[:-1]
+        self.seg_len_max = int((self.seg_pstart[1:S + 1] - self.seg_pstart[:S]).max().item()) if S else 0
         self.smax = int(seg_sizes.max().item()) if K else 0
         # shape -> segments (ascending cell) for the gather reduce: stable sort
         # of the segment indices by owner

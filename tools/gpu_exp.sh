@@ -1,4 +1,4 @@
 set -x
 timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
-timeout 300 python tools/stage_profile.py --config c4s --steps 3 --reduce owner --kernels > gpurun_out/st_c4s_ow.json 2> /dev/null; echo st=$?
-timeout 1500 python tools/stage_profile.py --config c3 --steps 3 --reduce owner --kernels > gpurun_out/st_c3_ow.json 2> /dev/null; echo st=$?
+timeout 1800 python bench.py --config c4 --steps 5 --warmup 3 > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err; echo c4=$?
+timeout 600 python bench.py --steps 10 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; echo b2=$?
