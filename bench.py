@@ -151,13 +151,22 @@ def scan_work(eng, Q, w, top_k):
     return nbytes, flops
 
 
-def load_traffic(config):
-    path = os.path.join(ROOT, "profiles", "scan_traffic.json")
+def load_ncu(config):
+    """ncu --set full summary of this workload's scan / quantizer launch
+    (profiles/ncu_summary.json, captured on one timed-path batch)."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as fh:
-            return json.load(fh).get(config)
+            return json.load(fh).get(config) or {}
     except (OSError, ValueError):
+        return {}
+
+
+def load_traffic(config):
+    n = load_ncu(config)
+    if "scan_dram_read_bytes" not in n:
         return None
+    return n["scan_dram_read_bytes"] + n.get("scan_dram_write_bytes", 0)
 
 
 # ------------------------------------------------------------------ setup
@@ -493,6 +502,10 @@ def run_gift(args, w):
                      "achieved_tflops": achieved_tf, "tensor_frac": achieved_tf / tpeak,
                      "fp16_mma_products_per_alg_product": split,
                      "tensor_pipe_frac_incl_split": achieved_tf * split / tpeak})
+    ncu = load_ncu(w.name)
+    quant_ncu = ({"kernel": ncu["quantize_kernel"], "tensor_hmma_active_pct":
+                  ncu["quantize_tensor_hmma_active_pct"], "source": "ncu --set full"}
+                 if "quantize_kernel" in ncu else None)
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and eng.fa.feat is not None:
@@ -522,7 +535,8 @@ def run_gift(args, w):
                         "h2d_bytes_per_step": B * w.n_views * w.dim * 4,
                         "d2h_bytes_per_step": B * w.top_k * 12},
                 "gpu_launches": eg.LAUNCHES_PER_BATCH * args.steps,
-                "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary()}
+                "roofline": roofline, "quantize": quant_ncu, "cpu_baseline": cpu,
+                "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
