@@ -87,6 +87,10 @@ typedef struct gift_fif_view {
   const int32_t* shape_seg;     /* [S] global segment index, ascending cell   */
   const int32_t* shape_seg_cell;/* [S] cell of segment shape_seg[g]           */
   int64_t max_cell_segments;    /* max over cells of its segment count         */
+  /* compressed tile store of the planes (optional, f32 storage; NULL: the   */
+  /* scan reads the dense planes), built by gift_cts_build                   */
+  const uint8_t* cts;
+  const int64_t* cts_off;       /* [n_tiles * d/64 + 1] block byte offsets     */
 } gift_fif_view;
 
 /* ---- library ---- */
@@ -109,6 +113,19 @@ int gift_quantize(const void* X, int32_t xdtype, int64_t n, int32_t d,
                   double cmax_norm, int32_t ma, const uint8_t* nz,
                   int32_t zero_key, int32_t* out_idx, void* ws,
                   size_t ws_bytes, void* stream);
+
+/* ---- compressed tile store of the f32 planes (scan input for HBM-bound
+ * indexes): per (scan tile, 64-wide k-block) a block of row masks, row value
+ * offsets and the non-zero (hi, lo) pairs, 128-byte aligned.  Call with
+ * out == NULL to write block_off (sizes scanned to offsets, block_off[T*nkb]
+ * = total bytes), then with out (>= total bytes) to fill the blocks.  The
+ * scan uses the store when every block fits gift_cts_stage_limit() bytes. */
+size_t gift_cts_ws_bytes(int64_t n_tiles, int32_t d);
+int gift_cts_build(const void* feat_hi, const void* feat_lo, int64_t n_postings,
+                   int32_t d, const int32_t* tile_pstart, const int32_t* tile_pend,
+                   int64_t n_tiles, int64_t* block_off, void* out, void* ws,
+                   size_t ws_bytes, void* stream);
+int gift_cts_stage_limit(void);
 
 /* Per-view non-zero flag and |x|^2 (f64 accumulate, stored f32).
  * `row.any()` tests of matching.py:121 / :150. */

@@ -43,6 +43,7 @@ class FifView(ctypes.Structure):
         ("feat_hi", _c_p), ("feat_lo", _c_p),
         ("shape_seg_off", _c_p), ("shape_seg", _c_p), ("shape_seg_cell", _c_p),
         ("max_cell_segments", _c_i64),
+        ("cts", _c_p), ("cts_off", _c_p),
     ]
 
 
@@ -76,6 +77,10 @@ _SIGS = {
     "gift_fif_score_ex": (_c_i32, [ctypes.POINTER(FifView), _c_p, _c_i32, _c_i32, _c_p, _c_i32,
                                    _c_i32, _c_dbl, _c_p, _c_p, _c_sz, _c_p, _c_p, _c_p]),
     "gift_fif_score_ranges": (_c_i32, [ctypes.POINTER(FifView), _c_i32]),
+    "gift_cts_ws_bytes": (_c_sz, [_c_i64, _c_i32]),
+    "gift_cts_build": (_c_i32, [_c_p, _c_p, _c_i64, _c_i32, _c_p, _c_p, _c_i64, _c_p, _c_p, _c_p,
+                                _c_sz, _c_p]),
+    "gift_cts_stage_limit": (_c_i32, []),
     "gift_fif_score_ranges2": (_c_i32, [ctypes.POINTER(FifView), _c_i32, _c_i32]),
     "gift_fif_score_ex2": (_c_i32, [ctypes.POINTER(FifView), _c_p, _c_i32, _c_i32, _c_p, _c_i32,
                                     _c_i32, _c_dbl, _c_p, _c_p, _c_sz, _c_p, _c_p, _c_p, _c_i32,

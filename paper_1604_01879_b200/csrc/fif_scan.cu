@@ -1212,6 +1212,9 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
     ta.mt_major = (mo != nullptr && mo[0] == 'm') ? 1 : 0;
     const char* dbg = getenv("GIFT_TC_DBG");
     ta.dbg = dbg ? atoi(dbg) : 0;
+    const bool cts_ok = cts_enabled(f);
+    ta.cts = cts_ok ? f->cts : nullptr;
+    ta.cts_off = cts_ok ? f->cts_off : nullptr;
     if (ta.chunk_kb < 1) ta.chunk_kb = 1;
     int rc2 = launch_scan_tc(f, Q, nprobes, ta, w.g1, w.g2, st, ev_scan_begin, ev_scan_end);
     if (rc2) return rc2;

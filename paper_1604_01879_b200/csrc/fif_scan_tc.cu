@@ -55,6 +55,7 @@ constexpr float SPLIT_INV = 1.0f / 2048.0f;
 
 struct ItemInfo {
   int c, mt, p0, p1, seg0, seg1, nb, pb0, n;  // n: MMA N of the item (64 | 128)
+  int t;      // global scan tile index
   bool live;  // pair mode: this CTA's posting tile exists (else a duplicate, no output)
 };
 
@@ -104,6 +105,7 @@ __device__ __forceinline__ ItemInfo decode_item(const TcArgs& p, int64_t item, i
     I.live = true;
   }
   const int64_t t = p.tile_off[lo] + tt;
+  I.t = static_cast<int>(t);
   I.p0 = p.tile_pstart[t];
   I.p1 = p.tile_pend[t];
   I.seg0 = p.tile_seg0[t];
@@ -527,6 +529,331 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Scan over the compressed tile store (f32 planes; experimental, built only
+// with GIFT_CTS=1).
+//
+// Same items, MMAs and epilogue as fif_scan_tc_kernel (single CTA, combined
+// [b1 | b2] operand, D2 += a2 . b1), but the posting planes arrive as the
+// sparse blocks of fif_build.cu (one cp.async.bulk per (tile, k-block) into a
+// 3-slot staging ring) and 4 expander warps rebuild the dense 128B-swizzled
+// tiles (thread = tile row: mask walk, predicated half2 loads, 16-byte
+// stores), then issue the probe planes' TMA into the same stage.  Bit-identical
+// to the dense single-CTA scan (tested); measured slower than the dense scan
+// on config 2 (1.99 vs 1.38 ms): the expansion's shared-memory traffic, not
+// HBM, becomes the bound.
+//   warp 0 bulk producer | 1 MMA | 2 scheduler | 3-6 epilogue | 7-10 expand
+constexpr int CTS_THREADS = 352;
+constexpr int CTS_STAGES = 2;                        // dense stages: A1 A2 B (64 KB)
+constexpr int CTS_STAGE = STAGE_LO;
+constexpr int CTS_NSTG = 3;                          // staging slots
+constexpr int CTS_STG_BYTES = 25 * 1024;
+constexpr int CTS_RING = CTS_STAGES * CTS_STAGE + CTS_NSTG * CTS_STG_BYTES;
+constexpr int SMEM_CTS = CTS_RING + EPI_BYTES + 256;
+constexpr int CTS_HDR_BYTES = 128 * 8 + 128 * 2;
+
+bool cts_enabled(const gift_fif_view* f) {
+  const char* ce = getenv("GIFT_CTS");
+  return f->cts != nullptr && f->cts_off != nullptr && f->feat_lo != nullptr && f->d % 64 == 0 &&
+         !(ce != nullptr && ce[0] == '0');
+}
+
+__global__ void __launch_bounds__(CTS_THREADS, 1)
+    fif_scan_cts_kernel(const __grid_constant__ CUtensorMap tmB1,
+                        const __grid_constant__ CUtensorMap tmB2, const TcArgs p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ int32_t s_sp[TC_M + 2];
+  __shared__ float s_qn2[TC_NMAX];
+  __shared__ ItemInfo s_item[ITEM_RING];
+  __shared__ __align__(8) uint64_t ifull[ITEM_RING], iempty[ITEM_RING];
+  uint8_t* stg = smem + CTS_STAGES * CTS_STAGE;
+  float* Ds = reinterpret_cast<float*>(smem + CTS_RING);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + CTS_RING + EPI_BYTES);
+  uint64_t* full = bars;                    // dense stages
+  uint64_t* empty = full + CTS_STAGES;
+  uint64_t* sfull = empty + CTS_STAGES;     // staging slots
+  uint64_t* sempty = sfull + CTS_NSTG;
+  uint64_t* tfull = sempty + CTS_NSTG;      // D chunk buffers
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int64_t first = blockIdx.x, stride = gridDim.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (p.meta[M_OVERFLOW]) return;
+  const int64_t n_items = p.meta[M_ITEMS];
+  const int nkb = p.d / TC_BK;
+  const int chunk_kb = p.chunk_kb;
+
+  if (warp == 0 && lane == 0) {
+    for (int r = 0; r < ITEM_RING; ++r) {
+      tc::mbar_init(&ifull[r], 1);
+      tc::mbar_init(&iempty[r], 4);  // producer, MMA, epilogue, expander
+    }
+    for (int s = 0; s < CTS_STAGES; ++s) {
+      tc::mbar_init(&full[s], TC_M);  // the 128 expander threads (one with B's bytes)
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < CTS_NSTG; ++s) {
+      tc::mbar_init(&sfull[s], 1);
+      tc::mbar_init(&sempty[s], TC_M);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&tfull[b], 1);
+      tc::mbar_init(&tempty[b], TC_M);
+    }
+    tc::fence_barrier_init();
+    tc::tma_prefetch(&tmB1);
+    tc::tma_prefetch(&tmB2);
+  }
+  if (warp == 1) tc::tmem_alloc<TMEM_COLS>(tmem_holder);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    // ------------------------------------------------ bulk producer (staging)
+    int slot = 0;
+    uint32_t sph = 0, it = 0;
+    for (int64_t item = first; item < n_items; item += stride, ++it) {
+      const uint32_t rs = it % ITEM_RING, rph = (it / ITEM_RING) & 1;
+      tc::mbar_wait(&ifull[rs], rph);
+      const ItemInfo I = s_item[rs];
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&iempty[rs]);
+      for (int kb = 0; kb < nkb; ++kb) {
+        tc::mbar_wait(&sempty[slot], sph ^ 1);
+        if (tc::elect_one()) {
+          const int64_t bi = static_cast<int64_t>(I.t) * nkb + kb;
+          const int64_t o0 = p.cts_off[bi];
+          const uint32_t bytes = static_cast<uint32_t>(p.cts_off[bi + 1] - o0);
+          tc::mbar_arrive_expect_tx(&sfull[slot], bytes);
+          tc::bulk_load(stg + slot * CTS_STG_BYTES, p.cts + o0, bytes, &sfull[slot]);
+        }
+        __syncwarp();
+        if (++slot == CTS_NSTG) {
+          slot = 0;
+          sph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer (whole warp)
+    int stage = 0;
+    uint32_t phase = 0, chunk_ctr = 0, it = 0;
+    for (int64_t item = first; item < n_items; item += stride, ++it) {
+      const uint32_t rs = it % ITEM_RING, rph = (it / ITEM_RING) & 1;
+      tc::mbar_wait(&ifull[rs], rph);
+      const ItemInfo I = s_item[rs];
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&iempty[rs]);
+      const uint32_t idesc = tc::idesc_f16_f32(TC_M, I.n);
+      const uint32_t idesc2 = tc::idesc_f16_f32(TC_M, 2 * I.n);
+      for (int kb0 = 0; kb0 < nkb; kb0 += chunk_kb) {
+        const uint32_t buf = chunk_ctr & 1, aph = (chunk_ctr >> 1) & 1;
+        tc::mbar_wait(&tempty[buf], aph ^ 1);
+        tc::tc_fence_after();
+        const uint32_t d1 = tmem_base + buf * 2 * TC_NMAX;
+        const int kend = min(kb0 + chunk_kb, nkb);
+        for (int kb = kb0; kb < kend; ++kb) {
+          tc::mbar_wait(&full[stage], phase);
+          tc::tc_fence_after();
+          uint8_t* st = smem + stage * CTS_STAGE;
+          const uint64_t a1 = tc::smem_desc_sw128(st);
+          const uint64_t a2 = tc::smem_desc_sw128(st + A_TILE);
+          const uint64_t b1 = tc::smem_desc_sw128(st + 2 * A_TILE);
+          if (tc::elect_one()) {
+#pragma unroll
+            for (int k = 0; k < TC_BK / 16; ++k) {
+              const uint32_t acc1 = (kb > kb0 || k > 0) ? 1u : 0u;
+              const uint64_t adv = static_cast<uint64_t>(k * 2);
+              tc::mma_f16(d1, a1 + adv, b1 + adv, idesc2, acc1);
+              tc::mma_f16(d1 + I.n, a2 + adv, b1 + adv, idesc, 1u);
+            }
+            tc::mma_commit(&empty[stage]);
+          }
+          __syncwarp();
+          if (++stage == CTS_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (tc::elect_one()) tc::mma_commit(&tfull[buf]);
+        __syncwarp();
+        ++chunk_ctr;
+      }
+    }
+  } else if (warp == 2) {
+    // ------------------------------------------------ scheduler
+    if (lane == 0) {
+      int hint = 0;
+      uint32_t it = 0;
+      for (int64_t item = first; item < n_items; item += stride, ++it) {
+        const uint32_t rs = it % ITEM_RING, rph = (it / ITEM_RING) & 1;
+        const ItemInfo I = decode_item<false>(p, item, hint, 0);
+        tc::mbar_wait(&iempty[rs], rph ^ 1);
+        s_item[rs] = I;
+        tc::mbar_arrive(&ifull[rs]);
+      }
+    }
+  } else if (warp >= 7) {
+    // ------------------------------------------------ expanders (thread = row)
+    const int r = threadIdx.x - 7 * 32;  // 0..127
+    int stage = 0, slot = 0;
+    uint32_t phase = 0, sph = 0, it = 0;
+    const uint32_t sw = static_cast<uint32_t>(r & 7);
+    const int row_off = (r >> 3) * 1024 + (r & 7) * 128;
+    for (int64_t item = first; item < n_items; item += stride, ++it) {
+      const uint32_t rs = it % ITEM_RING, rph = (it / ITEM_RING) & 1;
+      tc::mbar_wait(&ifull[rs], rph);
+      const ItemInfo I = s_item[rs];
+      named_bar(3, TC_M);
+      if (r == 0) tc::mbar_arrive(&iempty[rs]);
+      const uint32_t bbytes = 2u * I.n * TC_BK * 2;
+      for (int kb = 0; kb < nkb; ++kb) {
+        tc::mbar_wait(&empty[stage], phase ^ 1);  // MMA done with this stage
+        uint8_t* st = smem + stage * CTS_STAGE;
+        if (r == 0) {  // probe planes [b1 | b2] of this k-block (bytes registered below)
+          for (int x = 0; x < I.n / 64; ++x) {
+            tc::tma_load_2d(st + 2 * A_TILE + x * B_BOX, &tmB1, &full[stage], kb * TC_BK,
+                            I.pb0 + 64 * x);
+            tc::tma_load_2d(st + 2 * A_TILE + I.n * TC_BK * 2 + x * B_BOX, &tmB2, &full[stage],
+                            kb * TC_BK, I.pb0 + 64 * x);
+          }
+        }
+        tc::mbar_wait(&sfull[slot], sph);
+        if (!(p.dbg & 64)) {  // dbg 64: timing experiment without the expansion
+          const uint8_t* blk = stg + slot * CTS_STG_BYTES;
+          const uint64_t m = reinterpret_cast<const uint64_t*>(blk)[r];
+          const uint32_t* vals = reinterpret_cast<const uint32_t*>(
+              blk + CTS_HDR_BYTES + 16 * reinterpret_cast<const uint16_t*>(blk + 1024)[r]);
+          int cnt = 0;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {  // 16-byte chunk q = elements 8q .. 8q+7
+            uint32_t hw[4], lw[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int c0 = q * 8 + e * 2;
+              const bool b0 = (m >> c0) & 1ull, b1 = (m >> (c0 + 1)) & 1ull;
+              const uint32_t v0 = b0 ? vals[cnt] : 0u;
+              cnt += b0;
+              const uint32_t v1 = b1 ? vals[cnt] : 0u;
+              cnt += b1;
+              hw[e] = (v0 & 0xffffu) | (v1 << 16);
+              lw[e] = (v0 >> 16) | (v1 & 0xffff0000u);
+            }
+            const int cpos = row_off + static_cast<int>((static_cast<uint32_t>(q) ^ sw) * 16);
+            *reinterpret_cast<uint4*>(st + cpos) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            *reinterpret_cast<uint4*>(st + A_TILE + cpos) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+          }
+        }
+        tc::mbar_arrive(&sempty[slot]);     // staging slot read
+        tc::fence_proxy_async_smem();       // expanded tile -> tensor-core proxy
+        if (r == 0)  // the TMA bytes may land before this: tx-count goes transiently negative
+          tc::mbar_arrive_expect_tx(&full[stage], bbytes);
+        else
+          tc::mbar_arrive(&full[stage]);
+        if (++stage == CTS_STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+        if (++slot == CTS_NSTG) {
+          slot = 0;
+          sph ^= 1;
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue (warps 3..6)
+    const int et = threadIdx.x - 96;
+    const int lb = 32 * (warp & 3);
+    const int row = lb + lane;
+    const bool gauss = p.mode == GIFT_SIM_GAUSSIAN;
+    uint32_t chunk_ctr = 0, it = 0;
+    for (int64_t item = first; item < n_items; item += stride, ++it) {
+      const uint32_t rs = it % ITEM_RING, rph = (it / ITEM_RING) & 1;
+      tc::mbar_wait(&ifull[rs], rph);
+      const ItemInfo I = s_item[rs];
+      named_bar(2, TC_M);
+      if (et == 0) tc::mbar_arrive(&iempty[rs]);
+      const int nseg = I.seg1 - I.seg0;
+      const int ng = I.n / 16;
+      const int sp_a = et <= nseg ? p.seg_pstart[I.seg0 + et] : 0;
+      const int sp_b = et + TC_M <= nseg ? p.seg_pstart[I.seg0 + et + TC_M] : 0;
+      const float qn_r = et < I.nb ? p.qn2s[I.pb0 + et] : 0.f;
+      float acc[TC_NMAX];
+#pragma unroll
+      for (int n = 0; n < TC_NMAX; ++n) acc[n] = 0.f;
+      const uint32_t lane_off = static_cast<uint32_t>(lb) << 16;
+      for (int kb0 = 0; kb0 < nkb; kb0 += chunk_kb) {
+        const uint32_t buf = chunk_ctr & 1, aph = (chunk_ctr >> 1) & 1;
+        tc::mbar_wait(&tfull[buf], aph);
+        tc::tc_fence_after();
+        const uint32_t base = tmem_base + lane_off + buf * 2 * TC_NMAX;
+#pragma unroll
+        for (int j = 0; j < TC_NMAX / 16; ++j) {
+          if (j < ng) {
+            float v1[16], v2[16];
+            tc::tmem_ld_x16(base + j * 16, v1);
+            tc::tmem_ld_x16(base + I.n + j * 16, v2);
+            tc::tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc[j * 16 + i] += fmaf(v2[i], SPLIT_INV, v1[i]);
+          }
+        }
+        tc::tc_fence_before();
+        tc::mbar_arrive(&tempty[buf]);
+        ++chunk_ctr;
+      }
+      if (et <= nseg) s_sp[et] = sp_a;
+      if (et + TC_M <= nseg) s_sp[et + TC_M] = sp_b;
+      s_qn2[et] = qn_r;
+      const float pn = (I.p0 + row < I.p1) ? p.pnorm2[I.p0 + row] : 0.f;
+      const int64_t S_c = p.seg_off[I.c + 1] - p.seg_off[I.c];
+      const int64_t seg_base = p.seg_off[I.c];
+      const int64_t obase = p.outbase[I.c];
+      const int mc = et & (EPI_COLS - 1), sg0 = et >> 5;
+#pragma unroll
+      for (int sl0 = 0; sl0 < TC_NMAX; sl0 += EPI_COLS) {
+        if (sl0 < I.nb) {
+#pragma unroll
+          for (int c = 0; c < EPI_COLS; ++c) {
+            float v = acc[sl0 + c];
+            if (gauss) v = 2.0f * v - pn;
+            Ds[row * EPI_STRIDE + c] = v;
+          }
+          named_bar(1, TC_M);
+          const int ncol = min(EPI_COLS, I.nb - sl0);
+          const int m = sl0 + mc;
+          for (int sl = sg0; mc < ncol && sl < nseg; sl += TC_M / EPI_COLS) {
+            const int sp0 = s_sp[sl], sp1 = s_sp[sl + 1];
+            const int r0 = max(sp0, I.p0) - I.p0, r1 = min(sp1, I.p1) - I.p0;
+            float mx = -INFINITY;
+            for (int rr = r0; rr < r1; ++rr) mx = fmaxf(mx, Ds[rr * EPI_STRIDE + mc]);
+            float sim;
+            if (gauss)
+              sim = expf(-fmaxf(s_qn2[m] - mx, 0.f) * p.inv_sigma2);
+            else
+              sim = fminf(fmaxf(mx, 0.f), 1.f);
+            const int64_t o = obase + static_cast<int64_t>(I.mt * TC_NMAX + m) * S_c +
+                              (I.seg0 + sl - seg_base);
+            if (sp0 < I.p0 || sp1 > I.p1)
+              atomicMax(reinterpret_cast<int*>(p.out + o), __float_as_int(sim));
+            else
+              p.out[o] = sim;
+          }
+          named_bar(1, TC_M);
+        }
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc<TMEM_COLS>(tmem_base);
+  }
+}
+
 __global__ void split_planes_kernel(const float* __restrict__ x, int64_t n, __half* __restrict__ h1,
                                     __half* __restrict__ h2) {
   int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -608,6 +935,7 @@ bool tc_supported(const gift_fif_view* f) {
 // traffic per SM; config 3 scan 16.3 -> 15.1 ms, config 2 unchanged), single
 // CTAs for fp16 storage (config 4: the pair is ~7% slower there)
 bool tc_pair_enabled(const gift_fif_view* f) {
+  if (cts_enabled(f)) return false;  // the compressed-store scan runs on single CTAs
   const char* e = getenv("GIFT_TC_PAIR");
   if (e != nullptr && (e[0] == '0' || e[0] == '1')) return e[0] == '1' && sm_count() >= 2;
   return f->feat_lo != nullptr && sm_count() >= 2;
@@ -635,7 +963,11 @@ int launch_scan_tc(const gift_fif_view* f, const float* Q, int64_t nprobes_max, 
   if (rc) return rc;
   a.has_lo = f->feat_lo != nullptr ? 1 : 0;
   if (ev0) GIFT_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(ev0), st));
-  if (pair) {
+  if (a.cts != nullptr) {
+    GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_scan_cts_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_CTS));
+    fif_scan_cts_kernel<<<sm_count(), CTS_THREADS, SMEM_CTS, st>>>(mB1, mB2, a);
+  } else if (pair) {
     GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_scan_tc_kernel<true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TC));
     cudaLaunchConfig_t cfg = {};
@@ -675,3 +1007,5 @@ extern "C" int gift_split_planes(const float* x, int64_t n, void* h1, void* h2, 
   GIFT_LAUNCH_CHECK();
   return GIFT_OK;
 }
+
+extern "C" int gift_cts_stage_limit(void) { return gift::CTS_STG_BYTES; }

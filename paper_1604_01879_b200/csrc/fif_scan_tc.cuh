@@ -30,6 +30,8 @@ struct TcArgs {
   int has_lo;
   int chunk_kb;
   int mt_major;  // item order within a cell: probe-tile-major (1) or posting-tile-major (0)
+  const uint8_t* cts;      // compressed tile store of the planes (fif_build.cu) or null
+  const int64_t* cts_off;  // [T * nkb + 1] block byte offsets
   int dbg;       // timing experiments only (GIFT_TC_DBG bits; outputs invalid): 1 = skip
                  // the epilogue tail, 2 = skip the TMEM drains, 4 = no MMAs, 8 = no loads
 };
@@ -39,6 +41,8 @@ bool tc_supported(const gift_fif_view* f);
 // consecutive posting tiles of a cell x one probe tile.  GIFT_TC_PAIR=0|1
 // overrides the default (pairs with the f32 lo plane).
 bool tc_pair_enabled(const gift_fif_view* f);
+// the index carries a compressed tile store and GIFT_CTS != 0
+bool cts_enabled(const gift_fif_view* f);
 // quantize with need_order = false: when exactly ma candidates survive the
 // margin test their order is not resolved (the F-IF scan takes a max over
 // the ma cells, matching.py:153-159, so only the set matters)

@@ -163,6 +163,8 @@ class DeviceFif:
         v.shape_seg = self.shape_seg.data_ptr()
         v.shape_seg_cell = self.shape_seg_cell.data_ptr()
         v.max_cell_segments = self.smax
+        v.cts = None if getattr(self, "cts", None) is None else self.cts.data_ptr()
+        v.cts_off = None if getattr(self, "cts_off", None) is None else self.cts_off.data_ptr()
         v.flags = nat.FIF_TILED_SEGMENTS if self.seg_len_max <= nat.lib().gift_fif_tile_n() else 0
         self.view = v
         return v
@@ -335,6 +337,7 @@ class DeviceFif:
         radix_sort_pairs(k2, v2, _bits(n_local), stream)
         self.shape_off = offsets_from_sorted(k2, n_local, stream)  # [n_local+1]
         self.shape_post = v2.to(torch.int64)
+        self._build_cts(stream)
         seg_sizes = self.seg_off[1:] - self.seg_off[:-1]
         self.seg_len_max = int((self.seg_pstart[1:S + 1] - self.seg_pstart[:S]).max().item()) if S else 0
         self.smax = int(seg_sizes.max().item()) if K else 0
@@ -353,6 +356,37 @@ class DeviceFif:
             self.shape_seg = torch.zeros(1, dtype=torch.int32, device=dev)
             self.shape_seg_cell = torch.zeros(1, dtype=torch.int32, device=dev)
         self.bind()
+
+    def _build_cts(self, stream=None):
+        """Compressed tile store of the f32 planes (lossless sparse blocks per
+        (scan tile, 64-wide k-block), read by the experimental compressed
+        scan).  Built only with GIFT_CTS=1 (the expansion measured slower than
+        the dense-plane scan); skipped for fp16 storage, d % 64 != 0, blocks
+        over the scan's staging slot or not enough free HBM."""
+        import os
+
+        self.cts = self.cts_off = None
+        if (self.feat_lo is None or self.d % 64 != 0 or self.T == 0
+                or os.environ.get("GIFT_CTS", "0") != "1"):
+            return
+        lib = nat.lib()
+        dev = self.post_ord.device
+        nkb = self.d // 64
+        off = torch.empty(self.T * nkb + 1, dtype=torch.int64, device=dev)
+        ws = nat.workspace("build").get(lib.gift_cts_ws_bytes(self.T, self.d))
+        nat.call("gift_cts_build", nat.ptr(self.feat_hi), nat.ptr(self.feat_lo), self.P, self.d,
+                 nat.ptr(self.tile_pstart), nat.ptr(self.tile_pend), self.T, nat.ptr(off), None,
+                 nat.ptr(ws), ws.numel(), _sp(stream))
+        total = int(off[-1].item())
+        biggest = int((off[1:] - off[:-1]).max().item())
+        free, _ = torch.cuda.mem_get_info(dev)
+        if biggest > lib.gift_cts_stage_limit() or total + (8 << 30) > free:
+            return
+        self.cts = torch.empty(max(total, 16), dtype=torch.uint8, device=dev)
+        nat.call("gift_cts_build", nat.ptr(self.feat_hi), nat.ptr(self.feat_lo), self.P, self.d,
+                 nat.ptr(self.tile_pstart), nat.ptr(self.tile_pend), self.T, nat.ptr(off),
+                 nat.ptr(self.cts), nat.ptr(ws), ws.numel(), _sp(stream))
+        self.cts_off = off
 
     # -- host views (reference container attributes) ---------------------
     def host_lists(self):

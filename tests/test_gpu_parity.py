@@ -459,3 +459,32 @@ def test_sparse_sif_ranking_equals_dense(k):
         np.testing.assert_array_equal(si.cpu().numpy(), di.cpu().numpy())
         np.testing.assert_array_equal(sv.cpu().numpy(), dv.cpu().numpy())
     assert float(sif._acc.abs().sum()) == 0.0
+
+
+@pytest.mark.parametrize("similarity", ["gaussian", "cosine"])
+def test_compressed_tile_store_scan_bit_identical(similarity, monkeypatch):
+    """The (experimental, opt-in) scan over the compressed tile store (sparse
+    (hi, lo) blocks expanded in shared memory) gives exactly the scores of the
+    single-CTA dense-plane scan (same MMAs on the same operands), and matches
+    the oracle."""
+    views, _ = mixture_views(77, 300, 16, 4096, 55, mu0=-0.26, n_queries=8)
+    views[5, 3] = 0.0  # an empty view
+    db, qs = views[:300], views[300:]
+    C = sampled_codebook(db, 64, 4)
+    monkeypatch.setenv("GIFT_CTS", "1")  # the store is opt-in
+    fif = mt.build_fif_from_tensor(torch.from_numpy(db).to(dev()), Codebook(C), shape_ids(300))
+    assert fif.dev.cts is not None, "compressed tile store not built"
+    dense = fif.dev.P * 4096 * 4
+    assert fif.dev.cts.numel() < 0.7 * dense  # ReLU-sparse: well under the dense bytes
+    got = {}
+    for mode in ("cts", "dense"):
+        monkeypatch.setenv("GIFT_CTS", "1" if mode == "cts" else "0")
+        monkeypatch.setenv("GIFT_TC_PAIR", "0")
+        got[mode] = mt.query_fif_batch(fif, qs, 2, similarity).cpu().numpy()
+    np.testing.assert_array_equal(got["cts"], got["dense"])
+    assign = oracle.quantize_many(C, db.reshape(-1, 4096), 1).reshape(300, 16)
+    ref = oracle.build_fif(list(db), C, assign=assign)
+    for q, g in zip(qs, got["cts"]):
+        e = oracle.query_fif(ref, q, 2, similarity,
+                             cells=oracle.quantize_many(C, q.astype(np.float64), 2))
+        np.testing.assert_allclose(g, e, rtol=RTOL, atol=1e-12)

@@ -1,9 +1,5 @@
 set -x
-C2="python tools/stage_profile.py --config c2 --steps 1 --reduce range"
-C4="python tools/stage_profile.py --config c4s --steps 1 --reduce owner"
-timeout 300 $C2 > gpurun_out/plain_c2.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:fif_scan_tc -s 40 -c 1 -o gpurun_out/q_scan_c2 $C2 > gpurun_out/ncu_a.log 2>&1; echo a=$?
-timeout 900 ncu --set full --clock-control none -k regex:quant_approx_tc -s 80 -c 1 -o gpurun_out/q_quant_c2 $C2 > gpurun_out/ncu_b.log 2>&1; echo b=$?
-timeout 300 $C4 > gpurun_out/plain_c4.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:fif_scan_tc -s 196 -c 1 -o gpurun_out/q_scan_c4s $C4 > gpurun_out/ncu_c.log 2>&1; echo c=$?
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:quant_approx_tc --csv --log-file gpurun_out/quant_list.csv $C2 > gpurun_out/ncu_d.log 2>&1; echo d=$?
+timeout 300 python -m pytest tests/test_gpu_parity.py -x -q -k "compressed_tile" > gpurun_out/cts_test.log 2>&1; echo cts=$?
+for dbg in 0 64; do
+GIFT_CTS=1 GIFT_TC_DBG=$dbg timeout 300 python tools/stage_profile.py --config c2 --steps 5 --reduce range > gpurun_out/st_c2_cts_$dbg.json 2> /dev/null; echo st=$?
+done
