@@ -62,22 +62,30 @@ class ClockSampler:
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu: int):
+    def __init__(self, gpu: int, period_ms: int = 200):
         self.gpu = gpu
+        self.period_ms = period_ms
         self.proc = None
         self.lines = []
 
     def __enter__(self):
+        if os.environ.get("GIFT_BENCH_NO_SMI") == "1":  # diagnostics: no sampler
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms",
+                 os.environ.get("GIFT_SMI_MS", str(self.period_ms))],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except OSError:
             self.proc = None
-        time.sleep(0.3)
+        # nvidia-smi's start-up (NVML init) stalls the GPU for tens of ms:
+        # wait for its first samples before the caller's timed region starts
+        t0 = time.time()
+        while self.proc is not None and len(self.lines) < 2 and time.time() - t0 < 15.0:
+            time.sleep(0.05)
         return self
 
     def _read(self):
@@ -112,6 +120,21 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
+def warm(fn, iters: int, min_s: float = 0.25):
+    """Untimed warm-up: at least `iters` calls and `min_s` seconds of
+    back-to-back GPU work, ending with a synchronize.  Runs inside the clock
+    sampler so the timed region starts on a busy GPU (a GPU left idle while
+    the sampler starts loses ~30 ms to the clock ramp on latency-bound steps)."""
+    t0 = time.time()
+    i = 0
+    while i < iters or time.time() - t0 < min_s:
+        fn(i)
+        i += 1
+        if i >= iters:
+            torch.cuda.synchronize()
+    torch.cuda.synchronize()
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -119,6 +142,14 @@ def measured_peaks():
         return float(p["hbm_gbs"]), "measured"
     except (OSError, KeyError, ValueError):
         return 6650.0, "fallback"
+
+
+def nat_reduce_mode(eng, w):
+    import ctypes
+
+    from paper_1604_01879_b200 import _native as nat
+
+    return nat.lib().gift_fif_reduce_mode(ctypes.byref(eng.fa.view), w.n_views, w.ma)
 
 
 def measured_tensor_peak():
@@ -316,12 +347,14 @@ def run_c5(args):
     g.manual_seed(SEED + 5)
     B = c["batch"]
     qrows = torch.randint(0, n, (B * (args.steps + args.warmup),), generator=g, device=device)
-    for i in range(args.warmup):
-        r = qrows[i * B:(i + 1) * B]
-        eng.rerank_lists(idx[r], val[r], top_k=c["top_k"], self_local=r.to(torch.int32))
-    torch.cuda.synchronize()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+
+    def step(i):
+        r = qrows[(i % args.warmup) * B:(i % args.warmup + 1) * B]
+        eng.rerank_lists(idx[r], val[r], top_k=c["top_k"], self_local=r.to(torch.int32))
+
     with ClockSampler(local) as clk:
+        warm(step, args.warmup)
         ev[0].record()
         for i in range(args.warmup, args.warmup + args.steps):
             r = qrows[i * B:(i + 1) * B]
@@ -337,7 +370,7 @@ def run_c5(args):
                        "communities": c["communities"], "k2": c["k2"], "top_k": c["top_k"],
                        "batch": B, "sif_postings": int(bundle.sif.dev.e_ord.numel()),
                        "build_s": build_s},
-            "e2e": None, "gpu_launches": 6 * args.steps, "roofline": None, "cpu_baseline": None,
+            "e2e": None, "gpu_launches": 3 * args.steps, "roofline": None, "cpu_baseline": None,
             "clocks": clk.summary()}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -382,11 +415,9 @@ def run_sharded(args, w):
     B = w.batch
     nb = max(1, qs.shape[0] // B)
     batches = [qs[j * B:(j + 1) * B].contiguous() for j in range(nb)]
-    for i in range(args.warmup):
-        eng.run(batches[i % nb], w.top_k)
-    torch.cuda.synchronize()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     with ClockSampler(local) as clk:
+        warm(lambda i: eng.run(batches[i % nb], w.top_k), args.warmup)
         dist.barrier()
         torch.cuda.synchronize()
         ev[0].record()
@@ -424,10 +455,6 @@ def run_gift(args, w):
     nb = max(1, qs.shape[0] // B)
     order = [(rank + i * ws) % nb for i in range(args.steps + args.warmup)]
     batches = [qs[j * B:(j + 1) * B].contiguous() for j in range(nb)]
-    for i in range(args.warmup):
-        eng.run(batches[order[i]], top_k=w.top_k, rerank=True)
-    torch.cuda.synchronize()
-
     stream = torch.cuda.current_stream()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     scan_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -436,6 +463,8 @@ def run_gift(args, w):
         a.record(stream)
         b.record(stream)
     with ClockSampler(local) as clk:
+        warm(lambda i: eng.run(batches[order[i % args.warmup]], top_k=w.top_k, rerank=True),
+             args.warmup)
         if ws > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -534,7 +563,7 @@ def run_gift(args, w):
                 "e2e": {"value": e2e_value, "unit": UNIT,
                         "h2d_bytes_per_step": B * w.n_views * w.dim * 4,
                         "d2h_bytes_per_step": B * w.top_k * 12},
-                "gpu_launches": eg.LAUNCHES_PER_BATCH * args.steps,
+                "gpu_launches": eg.LAUNCHES_PER_BATCH[nat_reduce_mode(eng, w)] * args.steps,
                 "roofline": roofline, "quantize": quant_ncu, "cpu_baseline": cpu,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)

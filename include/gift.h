@@ -230,6 +230,8 @@ int gift_fif_score_ex(const gift_fif_view* f, const float* Q, int32_t B,
  * shape -> segment map). */
 int gift_fif_score_ranges(const gift_fif_view* f, int32_t V);
 int gift_fif_score_ranges2(const gift_fif_view* f, int32_t V, int32_t ma);
+/* Reduce the score call will use: 0 per-range tiles, 1 gather, 2 owner. */
+int gift_fif_reduce_mode(const gift_fif_view* f, int32_t V, int32_t ma);
 int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_t B,
                        int32_t V, const int32_t* vq, int32_t ma, int32_t mode,
                        double sigma, double* out_scores, void* ws,
@@ -311,8 +313,9 @@ int gift_sif_query(const int64_t* e_off, const int32_t* e_ord,
  * dense rows: touched shapes only, plus the reference's zero-score fill (self
  * first, then id-rank order).  Returns the k best by (score desc, tiebreak
  * asc) exactly like gift_topk_rows over the dense scores.  acc_rows:
- * n_acc_rows x n_local f64, all zero on entry and on return (caller-owned
- * scratch).  order[r] = local shape of id rank r (inverse of idrank).
+ * n_acc_rows rows of acc_stride (>= n_local) f64, all zero on entry and on
+ * return (caller-owned scratch; a stride that is not a multiple of a large
+ * power of two keeps the rows' hot entries on different DRAM channels).  order[r] = local shape of id rank r (inverse of idrank).
  * max_touched: an upper bound of the shapes one query can touch (support cap
  * x the longest S-IF entry). */
 size_t gift_sif_query_topk_ws_bytes(int32_t B, int64_t n_local, int32_t k,
@@ -323,7 +326,8 @@ int gift_sif_query_topk(const int64_t* e_off, const int32_t* e_ord,
                         const double* q_val, const int32_t* q_cnt,
                         const double* q_norm, int32_t B, int32_t cap,
                         double* acc_rows, int32_t n_acc_rows,
-                        const int32_t* order, const int32_t* idrank,
+                        int64_t acc_stride, const int32_t* order,
+                        const int32_t* idrank,
                         const int32_t* self_local, int64_t ord_base, int32_t k,
                         int64_t max_touched, int32_t* out_idx, double* out_val,
                         void* ws, size_t ws_bytes, void* stream);

@@ -82,6 +82,7 @@ _SIGS = {
                                 _c_sz, _c_p]),
     "gift_cts_stage_limit": (_c_i32, []),
     "gift_fif_score_ranges2": (_c_i32, [ctypes.POINTER(FifView), _c_i32, _c_i32]),
+    "gift_fif_reduce_mode": (_c_i32, [ctypes.POINTER(FifView), _c_i32, _c_i32]),
     "gift_fif_score_ex2": (_c_i32, [ctypes.POINTER(FifView), _c_p, _c_i32, _c_i32, _c_p, _c_i32,
                                     _c_i32, _c_dbl, _c_p, _c_p, _c_sz, _c_p, _c_p, _c_p, _c_i32,
                                     _c_p, _c_p]),
@@ -104,7 +105,7 @@ _SIGS = {
                                 _c_i32, _c_i32, _c_p, _c_p]),
     "gift_sif_query_topk_ws_bytes": (_c_sz, [_c_i32, _c_i64, _c_i32, _c_i64]),
     "gift_sif_query_topk": (_c_i32, [_c_p, _c_p, _c_p, _c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p,
-                                     _c_p, _c_i32, _c_i32, _c_p, _c_i32, _c_p, _c_p, _c_p,
+                                     _c_p, _c_i32, _c_i32, _c_p, _c_i32, _c_i64, _c_p, _c_p, _c_p,
                                      _c_i64, _c_i32, _c_i64, _c_p, _c_p, _c_p, _c_sz, _c_p]),
 }
 

@@ -314,13 +314,14 @@ __global__ void __launch_bounds__(256)
                             int64_t n_global, int64_t n_local, const int32_t* __restrict__ q_idx,
                             const double* __restrict__ q_val, const int32_t* __restrict__ q_cnt,
                             const double* __restrict__ q_norm, int B, int cap,
-                            double* __restrict__ acc_rows, const int32_t* __restrict__ order,
+                            double* __restrict__ acc_rows, int64_t acc_stride,
+                            const int32_t* __restrict__ order,
                             const int32_t* __restrict__ idrank, const int32_t* __restrict__ self_local,
                             int64_t ord_base, int k_fill, int64_t m, double* __restrict__ cs,
                             uint32_t* __restrict__ ct, int32_t* __restrict__ ci,
                             int32_t* __restrict__ row_cnt) {
   __shared__ int s_cnt;
-  double* acc = acc_rows + static_cast<int64_t>(blockIdx.x) * n_local;
+  double* acc = acc_rows + static_cast<int64_t>(blockIdx.x) * acc_stride;
   const int tid = threadIdx.x;
   for (int b = blockIdx.x; b < B; b += gridDim.x) {
     if (tid == 0) s_cnt = 0;
@@ -479,7 +480,8 @@ extern "C" int gift_sif_query_topk(const int64_t* e_off, const int32_t* e_ord, c
                                    const int32_t* q_idx, const double* q_val,
                                    const int32_t* q_cnt, const double* q_norm, int32_t B,
                                    int32_t cap, double* acc_rows, int32_t n_acc_rows,
-                                   const int32_t* order, const int32_t* idrank,
+                                   int64_t acc_stride, const int32_t* order,
+                                   const int32_t* idrank,
                                    const int32_t* self_local, int64_t ord_base, int32_t k,
                                    int64_t max_touched, int32_t* out_idx, double* out_val,
                                    void* ws, size_t ws_bytes, void* stream) {
@@ -487,6 +489,7 @@ extern "C" int gift_sif_query_topk(const int64_t* e_off, const int32_t* e_ord, c
   GIFT_REQUIRE(k >= 1 && k <= 256, GIFT_ERR_UNSUPPORTED, "k = %d outside [1, 256]", k);
   GIFT_REQUIRE(n_acc_rows >= 1 && acc_rows != nullptr && order != nullptr, GIFT_ERR_INVALID,
                "sparse S-IF query needs accumulator rows and the id-rank order");
+  GIFT_REQUIRE(acc_stride >= n_local, GIFT_ERR_INVALID, "accumulator row stride < n_local");
   if (B <= 0 || n_local <= 0) return GIFT_OK;
   const int64_t m = min64(max_touched, n_local) + k + 1;
   Arena ar(ws, ws_bytes);
@@ -498,7 +501,7 @@ extern "C" int gift_sif_query_topk(const int64_t* e_off, const int32_t* e_ord, c
   const int grid = min(B, n_acc_rows);
   sif_query_sparse_kernel<<<static_cast<unsigned>(grid), 256, 0, st>>>(
       e_off, e_ord, e_val, norms, n_global, n_local, q_idx, q_val, q_cnt, q_norm, B, cap, acc_rows,
-      order, idrank, self_local, ord_base, k, m, cs, ct, ci, cnt);
+      acc_stride, order, idrank, self_local, ord_base, k, m, cs, ct, ci, cnt);
   GIFT_LAUNCH_CHECK();
   return topk_rows_from_lists(cs, ct, ci, cnt, B, m, k, 0, out_idx, out_val, st);
 }

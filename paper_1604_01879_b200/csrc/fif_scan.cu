@@ -1117,6 +1117,10 @@ extern "C" int gift_fif_score_ranges(const gift_fif_view* f, int32_t V) {
   return static_cast<int>(cdiv(max64(f->n_local, 1), reduce_rs(V, f->n_local)));
 }
 
+extern "C" int gift_fif_reduce_mode(const gift_fif_view* f, int32_t V, int32_t ma) {
+  return reduce_mode(f, V, ma);
+}
+
 extern "C" int gift_fif_score_ranges2(const gift_fif_view* f, int32_t V, int32_t ma) {
   const int mode = reduce_mode(f, V, ma);
   if (mode == RM_GATHER) return static_cast<int>(cdiv(max64(f->n_local, 1), gather_rs(f->n_local)));

@@ -32,10 +32,14 @@ _DTYPE_CODE = {torch.float32: nat.GIFT_F32, torch.float16: nat.GIFT_F16,
 
 # libgift kernel launches of one QueryEngine.run batch (single channel, rerank):
 # view_prep, quantize approx + select, probe count, plan, scatter, compact zero,
-# query-plane gather, tcgen05 scan, probe ranges, reduce (gift_fif_score) +
-# top-k2 merge of the reduce's per-range candidates, act_mean, sif_query,
-# top-k (slices + merge).
-LAUNCHES_PER_BATCH = 16
+# query-plane gather, tcgen05 scan, reduce (gift_fif_score) + top-k2 merge of
+# the reduce's candidates, act_mean, sparse S-IF query, final top-k merge.
+# libgift kernel launches per query batch on the single-channel fast path
+# (counted from the ncu launch lists, profiles/r01/launches_stage_*.csv):
+# view prep, 2 split-plane, approx, 2 select, count, plan, scatter, gather,
+# scan, then range reduce (ranges + reduce) or owner reduce (slot, count,
+# 4 scan kernels, owner), then top-k2, act_mean, sparse S-IF, top-k.
+LAUNCHES_PER_BATCH = {0: 17, 1: 16, 2: 22}  # by gift_fif_reduce_mode
 
 
 def _bits(n: int) -> int:
@@ -653,11 +657,14 @@ class DeviceSif:
         """Zeroed f64 accumulator rows for the sparse query (kept zero by the
         kernel): up to 2 per SM, within ~2.5 GB."""
         sms = torch.cuda.get_device_properties(self.norms.device).multi_processor_count
-        want = max(1, min(B, 2 * sms, (2_500_000_000 // 8) // max(self.n_local, 1)))
+        # row stride: n_local rounded to 64 doubles plus 40 (320 B): rows whose
+        # stride is a multiple of a large power of two put the same hot shape
+        # of every row on the same DRAM channel (measured 2.3x slower on C5)
+        stride = (max(self.n_local, 1) + 63) // 64 * 64 + 40
+        want = max(1, min(B, 2 * sms, (2_500_000_000 // 8) // stride))
         acc = getattr(self, "_acc", None)
         if acc is None or acc.shape[0] < want:
-            acc = torch.zeros((want, max(self.n_local, 1)), dtype=torch.float64,
-                              device=self.norms.device)
+            acc = torch.zeros((want, stride), dtype=torch.float64, device=self.norms.device)
             self._acc = acc
         return acc
 
@@ -680,7 +687,7 @@ class DeviceSif:
         nat.call("gift_sif_query_topk", nat.ptr(self.e_off), nat.ptr(self.e_ord),
                  nat.ptr(self.e_val), nat.ptr(self.norms), self.n_global, self.n_local,
                  nat.ptr(q.idx), nat.ptr(q.val), nat.ptr(q.cnt), nat.ptr(q.norm), B, q.cap,
-                 nat.ptr(acc), acc.shape[0], nat.ptr(order), nat.ptr(idrank),
+                 nat.ptr(acc), acc.shape[0], acc.shape[1], nat.ptr(order), nat.ptr(idrank),
                  nat.ptr(self_local), self.ord_base, k, bound, nat.ptr(idx), nat.ptr(val),
                  nat.ptr(ws), ws.numel(), _sp(stream))
         return idx, val

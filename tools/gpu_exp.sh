@@ -1,5 +1,5 @@
 set -x
-timeout 300 python -m pytest tests/test_gpu_parity.py -x -q -k "compressed_tile" > gpurun_out/cts_test.log 2>&1; echo cts=$?
-for dbg in 0 64; do
-GIFT_CTS=1 GIFT_TC_DBG=$dbg timeout 300 python tools/stage_profile.py --config c2 --steps 5 --reduce range > gpurun_out/st_c2_cts_$dbg.json 2> /dev/null; echo st=$?
-done
+timeout 600 python bench.py --config c5 --steps 5 >> gpurun_out/b5_a.json 2> gpurun_out/b5_a.err; echo a=$?
+timeout 600 python bench.py --config c5 --steps 5 >> gpurun_out/b5_a.json 2> /dev/null; echo a=$?
+timeout 600 python bench.py --steps 10 >> gpurun_out/b2_a.json 2> gpurun_out/b2_a.err; echo c2=$?
+timeout 900 python bench.py --config c4s --shard --steps 5 >> gpurun_out/b4s.json 2> gpurun_out/b4s.err; echo c4s=$?
