@@ -151,12 +151,13 @@ class QueryEngine:
         self.runner = eg.ScoreRunner()
         self.mode = mt.sim_mode(cfg.similarity)
 
-    def scores(self, Qa, Qb=None, vq=None, vqb=None, stream=None, scan_events=None):
-        sa = self.runner.score(self.fa, Qa, self.cfg.ma, self.mode, self.cfg.sigma, vq=vq,
+    def scores(self, Qa, Qb=None, vq=None, vqb=None, stream=None, scan_events=None, ma=None):
+        ma = self.cfg.ma if ma is None else ma
+        sa = self.runner.score(self.fa, Qa, ma, self.mode, self.cfg.sigma, vq=vq,
                                stream=stream, scan_events=scan_events)
         if Qb is None and self.dup:
             return sa, sa
-        sb = self.runner.score(self.fb, Qa if Qb is None else Qb, self.cfg.ma, self.mode,
+        sb = self.runner.score(self.fb, Qa if Qb is None else Qb, ma, self.mode,
                                self.cfg.sigma, vq=vq if vqb is None else vqb, stream=stream)
         return sa, sb
 
@@ -178,8 +179,19 @@ class QueryEngine:
         return final
 
     def run(self, Qa, Qb=None, top_k=10, rerank=True, self_local=None, vq=None, vqb=None,
-            stream=None, scan_events=None):
-        """Device batch -> (idx [B, k] i32 global ordinals, val [B, k] f64)."""
+            stream=None, scan_events=None, exact=False):
+        """Device batch -> (idx [B, k] i32 global ordinals, val [B, k] f64).
+        exact: every query view probes every cell (ma = K), which is the
+        reference's exact set similarity (index.py:230-243, matching.py:55-61:
+        mean over the query views of the best match over all target views;
+        the ma = K degeneracy of test_matching.py:127-140)."""
+        if exact:
+            sa, sb = self.scores(Qa, Qb, vq, vqb, stream, scan_events, ma=self.fa.cb.K)
+            if rerank:
+                return self._sif_rank(self.rerank_act(sa, sb, stream), top_k, self_local, stream)
+            final = sa if sb is sa else (sa + sb) / 2.0
+            return eg.topk_rows(final, min(top_k, self.n), idrank=self.idrank,
+                                self_local=self_local, stream=stream)
         if rerank and Qb is None and self.dup and self.raw_dup:
             # single-channel fast path: the reduce emits per-range top-k2
             # candidates, merged into the neighbour lists (rerank.py:78-87)
@@ -433,9 +445,9 @@ def query(bundle: IndexBundle, target, top_k: int = 10, exact: bool = False,
     Returns ([(shape_id, score, label)], {"render": s, "match": s})."""
     if bundle.n_shapes == 0:
         raise EmptyIndex("index holds no shapes")
-    if exact:
-        raise Unsupported("exact Hausdorff ranking is outside the GPU path (SURVEY.md §8(f))")
     eng = bundle.engine
+    if exact and eng.fa is None:
+        raise Unsupported("exact ranking needs the stored view features (F-IF)")
     ma_, mb_, sid = _viewset_mats(bundle, target)
     t0 = time.perf_counter()
     qa = mt._as_query_tensor(ma_, bundle.fifs["A"].dim)[None]
@@ -443,7 +455,7 @@ def query(bundle: IndexBundle, target, top_k: int = 10, exact: bool = False,
     if not (eng.dup and (mb_ is ma_ or np.array_equal(np.asarray(ma_), np.asarray(mb_)))):
         qb = mt._as_query_tensor(mb_, bundle.fifs["B"].dim)[None]
     self_local = torch.tensor([eng.ord_of.get(sid, -1)], dtype=torch.int32, device=qa.device)
-    idx, val = eng.run(qa, qb, top_k=top_k, rerank=rerank, self_local=self_local)
+    idx, val = eng.run(qa, qb, top_k=top_k, rerank=rerank, self_local=self_local, exact=exact)
     idx, val = idx.cpu().numpy(), val.cpu().numpy()
     t1 = time.perf_counter()
     return eng.results(idx[0], val[0]), {"render": 0.0, "match": t1 - t0}

@@ -240,9 +240,37 @@ def golden_bundles():
         print("bundle", name, "done")
 
 
+def golden_exact():
+    """Reference rankings with exact=True (index.py:230-243: exact set
+    similarity against every database shape), with and without re-ranking."""
+    for case in E2E_CASES[:2]:
+        (name, seed, N, V, d, classes, K, ma, k1, k2, nq, top_k, zv) = case
+        views, _ = mixture_views(seed, N, V, d, classes, zero_views=zv, n_queries=nq)
+        db, qs = views[:N], views[N:]
+        ids = shape_ids(N)
+        C = sampled_codebook(db, K, seed + 1)
+        cfg = rix.IndexConfig(n_views=V, codebook_size=K, ma=ma, k1=k1, k2=k2, imported=True)
+        bundle = reference_bundle(db, ids, C, cfg)[0]
+        out = {}
+        for rerank, tag in ((True, "rr"), (False, "nr")):
+            rid, rsc = [], []
+            for q in qs:
+                res, _t = rix.query(bundle, as_viewset("query", q), top_k=top_k, exact=True,
+                                    rerank=rerank)
+                rid.append([ids.index(r[0]) for r in res])
+                rsc.append([r[1] for r in res])
+            out[f"x_{tag}_ids"] = np.array(rid, dtype=np.int64)
+            out[f"x_{tag}_scores"] = np.array(rsc)
+        np.savez_compressed(os.path.join(HERE, f"exact_{name}.npz"), **out)
+        print("exact", name, "done")
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["bundles"]:
         golden_bundles()
+        sys.exit(0)
+    if sys.argv[1:] == ["exact"]:
+        golden_exact()
         sys.exit(0)
     golden_quantize()
     print("quantize done")
@@ -252,3 +280,4 @@ if __name__ == "__main__":
     print("rerank done")
     golden_e2e()
     golden_bundles()
+    golden_exact()

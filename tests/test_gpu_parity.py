@@ -488,3 +488,19 @@ def test_compressed_tile_store_scan_bit_identical(similarity, monkeypatch):
         e = oracle.query_fif(ref, q, 2, similarity,
                              cells=oracle.quantize_many(C, q.astype(np.float64), 2))
         np.testing.assert_allclose(g, e, rtol=RTOL, atol=1e-12)
+
+
+@pytest.mark.parametrize("case", E2E_CASES[:2], ids=[c[0] for c in E2E_CASES[:2]])
+def test_exact_ranking_against_reference(case):
+    """query(exact=True): every view probes every cell (ma = K) = the
+    reference's exact set similarity (index.py:230-243); rankings with and
+    without re-ranking match the reference's (golden exact_*.npz)."""
+    name, seed, N, V, d, classes, K, ma, k1, k2, nq, top_k, zv = case
+    g = load_golden(f"exact_{name}.npz")
+    bundle, db, qs, ids, C = _e2e_bundle(case)
+    for rerank, tag in ((True, "rr"), (False, "nr")):
+        for qi, q in enumerate(qs):
+            res, _ = gift.query(bundle, ViewSet.from_matrix("query", q), top_k=top_k,
+                                exact=True, rerank=rerank)
+            assert_ranking_close([ids.index(r[0]) for r in res], [r[1] for r in res],
+                                 g[f"x_{tag}_ids"][qi], g[f"x_{tag}_scores"][qi])
