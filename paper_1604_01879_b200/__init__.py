@@ -13,6 +13,7 @@ from .index import (
     build_index_from_lists,
     build_index_from_views,
     build_index_streamed,
+    evaluate_index,
     load_bundle,
     query,
     query_batch,
@@ -29,6 +30,7 @@ __all__ = [
     "build_index_from_lists",
     "build_index_from_views",
     "build_index_streamed",
+    "evaluate_index",
     "load_bundle",
     "query",
     "query_batch",

@@ -560,6 +560,58 @@ def query_many(bundle: IndexBundle, views_host: torch.Tensor, top_k: int = 10,
     return out_idx.numpy(), out_val.numpy()
 
 
+# ------------------------------------------------------------------ evaluation
+def evaluate_index(bundle: IndexBundle, exact: bool = False, rerank: bool = True,
+                   batch_size: int | None = None):
+    """Every labelled database shape (class of >= 2) queried with its stored
+    views, excluded from its own ranking, scored (index.py:317-333).  The
+    queries run through the device pipeline in batches; each query's ranking
+    key (score desc, shape id asc) is resolved on the device as the 1-based
+    ranks of its relevant shapes: rank(j) = 1 + #{i != self : key_i < key_j}."""
+    from . import evaluation as ev
+
+    eng = bundle.engine
+    if eng.fa is None:
+        raise Unsupported("evaluation needs the stored view features (F-IF)")
+    ids, labels = bundle.shape_ids, bundle.labels
+    lab = [labels.get(s, "") for s in ids]
+    sizes = {}
+    for x in lab:
+        sizes[x] = sizes.get(x, 0) + 1
+    keep = [i for i in range(eng.n) if sizes[lab[i]] >= 2]
+    skipped = eng.n - len(keep)
+    dev = nat.device()
+    codes = {x: c for c, x in enumerate(sorted(sizes))}
+    lab_dev = torch.tensor([codes[x] for x in lab], dtype=torch.int32, device=dev)
+    rank_dev = eng.idrank.to(torch.int64)
+    bs = batch_size or bundle.config.batch_size
+    per_query = []
+    for b0 in range(0, len(keep), bs):
+        rows = torch.tensor(keep[b0:b0 + bs], dtype=torch.int64, device=dev)
+        Q, vq = eng.fa.shape_views(rows)  # query_by_id: stored views, cell-major
+        # the reference's query_by_id passes every stored view (no zero views)
+        sa, sb = eng.scores(Q, None, vq=vq, ma=eng.fa.cb.K if exact else None)
+        final = eng.rerank(sa, sb) if rerank else (sa if sb is sa else (sa + sb) / 2.0)
+        B = rows.numel()
+        ar = torch.arange(B, device=dev)
+        final = final.clone()
+        final[ar, rows] = float("nan")  # the query itself leaves the ranking
+        own = lab_dev[rows]
+        for r in range(B):
+            s = final[r]
+            rel = torch.nonzero((lab_dev == own[r]) & (torch.arange(eng.n, device=dev) !=
+                                                       rows[r])).view(-1)
+            sv = s[rel][:, None]
+            rv = rank_dev[rel][:, None]
+            valid = ~torch.isnan(s)
+            better = (s[None, :] > sv) | ((s[None, :] == sv) & (rank_dev[None, :] < rv))
+            ranks = 1 + (better & valid[None, :]).sum(dim=1)
+            ranks = torch.sort(ranks).values.cpu().numpy()
+            i = keep[b0 + r]
+            per_query.append(ev.metrics_from_ranks(ranks, sizes[lab[i]], lab[i]))
+    return ev.aggregate_report(per_query, n_skipped=skipped)
+
+
 # ------------------------------------------------------------------ persistence
 def save_bundle(bundle: IndexBundle, out_dir) -> Path:
     """Versioned directory with deterministic bytes (index.py:360-375)."""

@@ -60,3 +60,10 @@ E2E_CASES = [
     ("small", 12, 120, 8, 32, 8, 12, 2, 6, 3, 10, 20, 0),
     ("c1like", 13, 400, 16, 64, 12, 16, 1, 10, 4, 12, 50, 0),
 ]
+
+# evaluate_index cases (overlapping classes: retrieval is imperfect):
+# (name, seed, N, V, d, classes, K, ma, k1, k2, sigma)
+EVAL_CASES = [
+    ("noisy", 21, 150, 8, 32, 10, 12, 2, 6, 3, 1.2),
+    ("noisy2", 22, 90, 6, 24, 6, 8, 1, 5, 2, 1.6),
+]

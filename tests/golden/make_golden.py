@@ -22,7 +22,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 sys.path.insert(0, "/root/reference/pkg/src")
 
-from cases import E2E_CASES, mixture_views, sampled_codebook, shape_ids, unit_nonneg_rows  # noqa: E402
+from cases import E2E_CASES, EVAL_CASES, mixture_views, sampled_codebook, shape_ids, unit_nonneg_rows  # noqa: E402
 from shapesearch import codebook as rcb  # noqa: E402
 from shapesearch import features as rft  # noqa: E402
 from shapesearch import index as rix  # noqa: E402
@@ -265,7 +265,35 @@ def golden_exact():
         print("exact", name, "done")
 
 
+def golden_eval():
+    """Reference evaluate_index (index.py:317-333) with the mixture classes as
+    labels: metrics with / without re-ranking, and exact."""
+    import dataclasses
+
+    for case in EVAL_CASES:
+        (name, seed, N, V, d, classes, K, ma, k1, k2, sigma) = case
+        views, labels = mixture_views(seed, N, V, d, classes, sigma=sigma, zero_views=3)
+        db = views[:N]
+        ids = shape_ids(N)
+        C = sampled_codebook(db, K, seed + 1)
+        cfg = rix.IndexConfig(n_views=V, codebook_size=K, ma=ma, k1=k1, k2=k2, imported=True)
+        bundle = reference_bundle(db, ids, C, cfg)[0]
+        bundle = dataclasses.replace(bundle, labels={ids[i]: f"c{labels[i]}" for i in range(N)})
+        out = {}
+        for tag, kw in (("rr", dict(rerank=True)), ("nr", dict(rerank=False)),
+                        ("x", dict(exact=True, rerank=False))):
+            rep = rix.evaluate_index(bundle, **kw)
+            out[f"{tag}_metrics"] = np.array([rep.nn, rep.ft, rep.st, rep.map, rep.auc])
+            out[f"{tag}_pr11"] = rep.pr11
+            out[f"{tag}_counts"] = np.array([rep.n_queries, rep.n_skipped])
+        np.savez_compressed(os.path.join(HERE, f"eval_{name}.npz"), **out)
+        print("eval", name, "done")
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["eval"]:
+        golden_eval()
+        sys.exit(0)
     if sys.argv[1:] == ["bundles"]:
         golden_bundles()
         sys.exit(0)
@@ -281,3 +309,4 @@ if __name__ == "__main__":
     golden_e2e()
     golden_bundles()
     golden_exact()
+    golden_eval()

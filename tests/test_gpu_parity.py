@@ -11,7 +11,7 @@ import pytest
 import torch
 
 import oracle
-from cases import E2E_CASES, mixture_views, sampled_codebook, shape_ids, unit_nonneg_rows
+from cases import E2E_CASES, EVAL_CASES, mixture_views, sampled_codebook, shape_ids, unit_nonneg_rows
 from conftest import load_golden
 from helpers import RTOL, assert_act_close, assert_ranking_close, unpack_acts, unpack_lists
 
@@ -504,3 +504,28 @@ def test_exact_ranking_against_reference(case):
                                 exact=True, rerank=rerank)
             assert_ranking_close([ids.index(r[0]) for r in res], [r[1] for r in res],
                                  g[f"x_{tag}_ids"][qi], g[f"x_{tag}_scores"][qi])
+
+
+@pytest.mark.parametrize("case", EVAL_CASES, ids=[c[0] for c in EVAL_CASES])
+def test_evaluate_index_against_reference(case):
+    """evaluate_index (index.py:317-333; NN/FT/ST/MAP/AUC of evaluation.py)
+    with re-ranking, without, and exact, against the reference's reports on
+    overlapping classes (golden eval_*.npz)."""
+    name, seed, N, V, d, classes, K, ma, k1, k2, sigma = case
+    g = load_golden(f"eval_{name}.npz")
+    views, labels = mixture_views(seed, N, V, d, classes, sigma=sigma, zero_views=3)
+    ids = shape_ids(N)
+    C = sampled_codebook(views, K, seed + 1)
+    cfg = gift.IndexConfig(n_views=V, codebook_size=K, ma=ma, k1=k1, k2=k2, imported=True)
+    bundle = gift.build_index_from_views(
+        views, ids, cfg, codebooks={"A": Codebook(C, "A"), "B": Codebook(C, "B")},
+        labels={ids[i]: f"c{labels[i]}" for i in range(N)})
+    for tag, kw in (("rr", dict(rerank=True)), ("nr", dict(rerank=False)),
+                    ("x", dict(exact=True, rerank=False))):
+        rep = gift.evaluate_index(bundle, **kw)
+        got = np.array([rep.nn, rep.ft, rep.st, rep.map, rep.auc])
+        assert [rep.n_queries, rep.n_skipped] == list(g[f"{tag}_counts"])
+        # identical rankings give identical metrics; a swap of scores tied
+        # within the 1e-5 tolerance moves a metric by at most ~1 / N
+        np.testing.assert_allclose(got, g[f"{tag}_metrics"], atol=2.0 / N)
+        np.testing.assert_allclose(rep.pr11, g[f"{tag}_pr11"], atol=2.0 / N)

@@ -132,3 +132,23 @@ def test_gaussian_restatement_properties(rng):
                     assert (s >= prev - 1e-15).all()
                 prev = s
             np.testing.assert_allclose(prev, ex, atol=1e-12)
+
+
+def test_evaluation_metrics_restatement():
+    """paper_1604_01879_b200.evaluation restates evaluation.py:44-88: known
+    rankings (host-only)."""
+    from paper_1604_01879_b200 import evaluation as ev
+    from paper_1604_01879_b200.errors import NoValidQueries, SingletonClass
+
+    m = ev.score_ranking("a", ["a", "b", "a", "b", "b"], 3)  # relevant at ranks 1 and 3
+    assert (m.nn, m.ft, m.st) == (1.0, 0.5, 1.0)
+    assert m.ap == pytest.approx((1 / 1 + 2 / 3) / 2)
+    np.testing.assert_allclose(m.pr11, [1.0] * 6 + [2 / 3] * 5)
+    m2 = ev.score_ranking("a", ["b", "b", "b"], 2)
+    assert (m2.nn, m2.ft, m2.ap) == (0.0, 0.0, 0.0)
+    rep = ev.aggregate_report([m, m2], n_skipped=1)
+    assert rep.n_queries == 2 and rep.nn == 0.5
+    with pytest.raises(SingletonClass):
+        ev.score_ranking("a", ["b"], 1)
+    with pytest.raises(NoValidQueries):
+        ev.aggregate_report([])
