@@ -20,11 +20,13 @@
 
 namespace gift {
 
-constexpr int QS_THREADS = 128;
+constexpr int QS_THREADS = 256;
+constexpr int QS_LV = 2048;  // leaf sums staged per exact pass (16 KB)
 constexpr int QS_WARPS = QS_THREADS / 32;
 constexpr int MAX_LEAVES = 256;  // leaves are >= 64 elements -> d <= 16384
 constexpr int MAX_K = 8192;
 constexpr int MAX_D = 16384;
+constexpr int QA_MAX_SPLIT = 8;  // split-k partials of stage 1
 
 template <bool A_HALF>
 __global__ void __launch_bounds__(simt::NTHR, 2)
@@ -67,43 +69,6 @@ __global__ void f64_to_f32_kernel(const double* __restrict__ in, float* __restri
   int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (; i < n; i += stride) out[i] = static_cast<float>(in[i]);
-}
-
-// --- numpy pairwise summation of (c - x)^2 over one leaf (n <= 128) ---------
-__device__ __forceinline__ double sq_term(const void* X, int xdtype, int64_t xoff,
-                                          const float* __restrict__ c, int k) {
-  double xv = load_as_f64(X, xdtype, xoff + k);
-  double t = __dsub_rn(static_cast<double>(c[k]), xv);
-  return __dmul_rn(t, t);
-}
-
-__device__ double leaf_sum(const void* X, int xdtype, int64_t xoff, const float* __restrict__ c,
-                           int off, int len) {
-  if (len < 8) {
-    double r = 0.0;
-    for (int i = 0; i < len; ++i) r = __dadd_rn(r, sq_term(X, xdtype, xoff, c, off + i));
-    return r;
-  }
-  double r0 = sq_term(X, xdtype, xoff, c, off + 0), r1 = sq_term(X, xdtype, xoff, c, off + 1),
-         r2 = sq_term(X, xdtype, xoff, c, off + 2), r3 = sq_term(X, xdtype, xoff, c, off + 3),
-         r4 = sq_term(X, xdtype, xoff, c, off + 4), r5 = sq_term(X, xdtype, xoff, c, off + 5),
-         r6 = sq_term(X, xdtype, xoff, c, off + 6), r7 = sq_term(X, xdtype, xoff, c, off + 7);
-  int i = 8;
-  const int lim = len - (len % 8);
-  for (; i < lim; i += 8) {
-    r0 = __dadd_rn(r0, sq_term(X, xdtype, xoff, c, off + i + 0));
-    r1 = __dadd_rn(r1, sq_term(X, xdtype, xoff, c, off + i + 1));
-    r2 = __dadd_rn(r2, sq_term(X, xdtype, xoff, c, off + i + 2));
-    r3 = __dadd_rn(r3, sq_term(X, xdtype, xoff, c, off + i + 3));
-    r4 = __dadd_rn(r4, sq_term(X, xdtype, xoff, c, off + i + 4));
-    r5 = __dadd_rn(r5, sq_term(X, xdtype, xoff, c, off + i + 5));
-    r6 = __dadd_rn(r6, sq_term(X, xdtype, xoff, c, off + i + 6));
-    r7 = __dadd_rn(r7, sq_term(X, xdtype, xoff, c, off + i + 7));
-  }
-  double res = __dadd_rn(__dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3)),
-                         __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
-  for (; i < len; ++i) res = __dadd_rn(res, sq_term(X, xdtype, xoff, c, off + i));
-  return res;
 }
 
 struct PairwisePlan {
@@ -160,33 +125,85 @@ __device__ __forceinline__ float float_from_order_key(uint32_t u) {
 
 __host__ __device__ __forceinline__ int xpad(int i) { return i + (i >> 7) * 8; }  // bank spread
 
-// numpy pairwise leaf (rows of 8..128 elements: 8 interleaved accumulators,
-// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), sequential tail; < 8: sequential from
-// 0.0) computed by a group of 8 lanes: lane j owns accumulator r_j, the tree
-// is three xor-shuffles.  The result is valid in the group's lane 0.
-__device__ double leaf_group(const float* __restrict__ xs, const void* X, int xdtype, int64_t xoff,
-                             const float* __restrict__ c, int off, int len, int gl,
-                             unsigned gmask) {
-  auto term = [&](int k) -> double {
-    const double xv = xs ? static_cast<double>(xs[xpad(k)]) : load_as_f64(X, xdtype, xoff + k);
-    const double t = __dsub_rn(static_cast<double>(c[k]), xv);
+// Exact numpy-order d2 of candidate centroids, all candidates of a view at
+// once: one thread per (candidate, leaf, accumulator) chain.  A leaf of len
+// >= 8 elements is 8 interleaved accumulators r_j = sum_s term(off + j + 8s)
+// (s < len / 8), combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) -- three
+// xor-shuffles over 8 aligned lanes -- plus a sequential tail; a leaf of < 8
+// elements is a sequential sum from 0.0.  A chain issues all of its loads
+// before its first add (one memory round trip per chain).  Leaf sums land in
+// `lvs` [cand][leaf]; the caller combines them with the plan's postfix
+// program.  Must be called by all threads of the CTA (warp-uniform trip
+// count; returns after a __syncthreads).
+template <int NTHR>
+__device__ void exact_leaves(const float* __restrict__ xs, const void* X, int xdtype, int64_t xoff,
+                             const float* __restrict__ C, int d, const int* ci, int q0, int nq,
+                             const PairwisePlan& plan, double* lvs) {
+  const int tid = threadIdx.x;
+  const int nch = plan.n_leaves * 8;
+  const int units = nq * nch;
+  auto xat = [&](int k) -> double {
+    return xs ? static_cast<double>(xs[xpad(k)]) : load_as_f64(X, xdtype, xoff + k);
+  };
+  auto sq = [](double c, double x) {
+    const double t = __dsub_rn(c, x);
     return __dmul_rn(t, t);
   };
-  if (len < 8) {
+  for (int u0 = 0; u0 < units; u0 += NTHR) {
+    const int u = u0 + tid;
+    const bool act = u < units;
+    const int q = act ? u / nch : 0;
+    const int rem = u - q * nch;
+    const int l = rem >> 3, j = rem & 7;
+    const int off = act ? plan.leaf_off[l] : 0, len = act ? plan.leaf_len[l] : 0;
+    const int lim = len - len % 8;
+    const float* crow = C + static_cast<int64_t>(ci[q0 + q]) * d;
     double r = 0.0;
-    if (gl == 0)
-      for (int i = 0; i < len; ++i) r = __dadd_rn(r, term(off + i));
-    return r;
+    if (act && len >= 8) {
+      double xv[16];
+      float cv[16];
+#pragma unroll
+      for (int s = 0; s < 16; ++s) {
+        const bool ok = 8 * s < lim;
+        xv[s] = ok ? xat(off + j + 8 * s) : 0.0;
+        cv[s] = ok ? crow[off + j + 8 * s] : 0.f;
+      }
+      r = sq(static_cast<double>(cv[0]), xv[0]);
+#pragma unroll
+      for (int s = 1; s < 16; ++s)
+        if (8 * s < lim) r = __dadd_rn(r, sq(static_cast<double>(cv[s]), xv[s]));
+    }
+    r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
+    r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));
+    r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 4));
+    if (act && j == 0) {
+      if (len < 8) {
+        r = 0.0;
+        for (int i = 0; i < len; ++i) r = __dadd_rn(r, sq(static_cast<double>(crow[off + i]), xat(off + i)));
+      } else {
+        for (int i = lim; i < len; ++i)
+          r = __dadd_rn(r, sq(static_cast<double>(crow[off + i]), xat(off + i)));
+      }
+      lvs[q * plan.n_leaves + l] = r;
+    }
   }
-  const int lim = len - (len % 8);
-  double r = term(off + gl);
-  for (int i = 8; i < lim; i += 8) r = __dadd_rn(r, term(off + i + gl));
-  r = __dadd_rn(r, __shfl_xor_sync(gmask, r, 1, 8));
-  r = __dadd_rn(r, __shfl_xor_sync(gmask, r, 2, 8));
-  r = __dadd_rn(r, __shfl_xor_sync(gmask, r, 4, 8));
-  if (gl == 0)
-    for (int i = lim; i < len; ++i) r = __dadd_rn(r, term(off + i));
-  return r;
+  __syncthreads();
+}
+
+// Postfix program of the pairwise recursion over one candidate's leaf sums.
+__device__ double combine_leaves(const PairwisePlan& plan, const double* lv) {
+  double stk[24];
+  int sp = 0, li = 0;
+  for (int o = 0; o < plan.n_ops; ++o) {
+    if (plan.ops[o] == 0) {
+      stk[sp++] = lv[li++];
+    } else {
+      const double bb = stk[--sp];
+      const double aa = stk[--sp];
+      stk[sp++] = __dadd_rn(aa, bb);
+    }
+  }
+  return stk[0];
 }
 
 __global__ void __launch_bounds__(QS_THREADS)
@@ -195,14 +212,15 @@ __global__ void __launch_bounds__(QS_THREADS)
                         double cmax, const uint8_t* __restrict__ nz, int zero_key, int p2k,
                         int need_order, int stage_x, int32_t* __restrict__ out,
                         const double* __restrict__ cn2, int ksplit, double dot_eps,
-                        const int32_t* __restrict__ flags,
+                        const int32_t* __restrict__ list,
+                        const int32_t* __restrict__ list_count,
                         const __grid_constant__ PairwisePlan plan) {
   extern __shared__ __align__(128) char smem[];
   float* a = reinterpret_cast<float*>(smem);
   double* cd = reinterpret_cast<double*>(smem + ((K * 4 + 15) / 16) * 16);
   int* ci = reinterpret_cast<int*>(cd + p2k);
   float* xs = stage_x ? reinterpret_cast<float*>(ci + p2k) : nullptr;
-  __shared__ double lv[QS_WARPS][MAX_LEAVES];
+  __shared__ double lvs[QS_LV];
   __shared__ unsigned hist[256];
   __shared__ double s_red[QS_WARPS];
   __shared__ float s_redf[QS_WARPS];
@@ -211,10 +229,10 @@ __global__ void __launch_bounds__(QS_THREADS)
   __shared__ int s_rank, s_nc;
   __shared__ float s_kth;
 
-  const int64_t v = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (v >= n) return;
-  if (flags != nullptr && flags[v] == 0) return;  // done by the warp kernel
+  // persistent CTAs over the views the warp kernel left (all views without it)
+  const int64_t total = list != nullptr ? static_cast<int64_t>(*list_count) : n;
+  auto one = [&](const int64_t v) {
   if (nz != nullptr && nz[v] == 0) {
     for (int s = tid; s < ma; s += QS_THREADS) out[v * ma + s] = zero_key >= 0 ? zero_key : -1;
     return;
@@ -222,16 +240,50 @@ __global__ void __launch_bounds__(QS_THREADS)
   const int64_t xoff = v * static_cast<int64_t>(d);
   // stage x (exact in f32 for f32/f16 inputs) and |x| (f64) for the margin
   double xsq = 0.0;
-  for (int k = tid; k < d; k += QS_THREADS) {
-    const double xv = load_as_f64(X, xdtype, xoff + k);
-    if (xs) xs[xpad(k)] = static_cast<float>(xv);
-    xsq += xv * xv;
+  const float* xf = static_cast<const float*>(X) + xoff;
+  if (xs != nullptr && xdtype == GIFT_F32 && (d & 3) == 0 &&
+      (reinterpret_cast<uintptr_t>(xf) & 15) == 0) {
+    const int d4 = d >> 2;
+    const float4* x4 = reinterpret_cast<const float4*>(xf);
+    for (int k0 = tid; k0 < d4; k0 += 4 * QS_THREADS) {
+      float4 t[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = k0 + u * QS_THREADS;
+        t[u] = k < d4 ? x4[k] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = k0 + u * QS_THREADS;
+        if (k < d4) {
+          float* dst = xs + xpad(4 * k);
+          dst[0] = t[u].x;
+          dst[1] = t[u].y;
+          dst[2] = t[u].z;
+          dst[3] = t[u].w;
+          xsq += static_cast<double>(t[u].x) * t[u].x + static_cast<double>(t[u].y) * t[u].y +
+                 static_cast<double>(t[u].z) * t[u].z + static_cast<double>(t[u].w) * t[u].w;
+        }
+      }
+    }
+  } else {
+    for (int k = tid; k < d; k += QS_THREADS) {
+      const double xv = load_as_f64(X, xdtype, xoff + k);
+      if (xs) xs[xpad(k)] = static_cast<float>(xv);
+      xsq += xv * xv;
+    }
   }
   for (int o = 16; o > 0; o >>= 1) xsq += __shfl_xor_sync(0xffffffffu, xsq, o);
   if (lane == 0) s_red[warp] = xsq;
   for (int c = tid; c < K; c += QS_THREADS) {
-    float dot = approx[v * K + c];
-    for (int z = 1; z < ksplit; ++z) dot += approx[static_cast<int64_t>(z) * n * K + v * K + c];
+    float pz[QA_MAX_SPLIT];
+#pragma unroll
+    for (int z = 0; z < QA_MAX_SPLIT; ++z)
+      pz[z] = z < ksplit ? approx[static_cast<int64_t>(z) * n * K + v * K + c] : 0.f;
+    float dot = pz[0];
+#pragma unroll
+    for (int z = 1; z < QA_MAX_SPLIT; ++z)
+      if (z < ksplit) dot += pz[z];
     a[c] = static_cast<float>(cn2[c]) - 2.0f * dot;
   }
   if (tid == 0) s_nc = 0;
@@ -361,38 +413,15 @@ __global__ void __launch_bounds__(QS_THREADS)
     }
     return;
   }
-  // exact numpy-order d2 of every candidate (one warp per candidate, 4
-  // leaves at a time on 8-lane groups)
-  const int grp = lane >> 3, gl = lane & 7;
-  const unsigned gmask = 0xFFu << (grp * 8);
-  for (int q = warp; q < nc; q += QS_WARPS) {
-    const float* crow = C + static_cast<int64_t>(ci[q]) * d;
-    for (int l0 = 0; l0 < plan.n_leaves; l0 += 4) {
-      const int l = l0 + grp;
-      if (l < plan.n_leaves) {
-        const double r =
-            leaf_group(xs, X, xdtype, xoff, crow, plan.leaf_off[l], plan.leaf_len[l], gl, gmask);
-        if (gl == 0) lv[warp][l] = r;
-      }
-    }
-    __syncwarp();
-    if (lane == 0) {
-      double stk[24];
-      int sp = 0, li = 0;
-      for (int o = 0; o < plan.n_ops; ++o) {
-        if (plan.ops[o] == 0) {
-          stk[sp++] = lv[warp][li++];
-        } else {
-          const double bb = stk[--sp];
-          const double aa = stk[--sp];
-          stk[sp++] = __dadd_rn(aa, bb);
-        }
-      }
-      cd[q] = stk[0];
-    }
-    __syncwarp();
+  // exact numpy-order d2 of every candidate, QS_LV / n_leaves candidates per
+  // pass
+  const int per = QS_LV / plan.n_leaves;
+  for (int q0 = 0; q0 < nc; q0 += per) {
+    const int nq = min(per, nc - q0);
+    exact_leaves<QS_THREADS>(xs, X, xdtype, xoff, C, d, ci, q0, nq, plan, lvs);
+    for (int q = tid; q < nq; q += QS_THREADS) cd[q0 + q] = combine_leaves(plan, lvs + q * plan.n_leaves);
+    __syncthreads();
   }
-  __syncthreads();
   // ascending (d2, index): bitonic over the next power of 2
   int p2 = 1;
   while (p2 < nc) p2 <<= 1;
@@ -421,17 +450,20 @@ __global__ void __launch_bounds__(QS_THREADS)
     }
   }
   for (int s = tid; s < ma; s += QS_THREADS) out[v * ma + s] = ci[s];
+  };
+  for (int64_t i = blockIdx.x; i < total; i += gridDim.x) {
+    one(list != nullptr ? static_cast<int64_t>(list[i]) : i);
+    __syncthreads();
+  }
 }
 
 
 // Fast path of stage 2 (ma <= 8): one warp per vector.  Pass 1 finds the
 // ma-th smallest approx value (per-lane sorted lists + xor-shuffle merges),
 // pass 2 collects the candidates under the margin with a ballot; unambiguous
-// sets are written directly, small candidate sets (<= QW_MAXC) are re-scored
-// exactly by the warp (8-lane pairwise leaves), anything larger is flagged
-// for the CTA-per-vector kernel above.
+// sets are written directly, every other view is flagged for the exact
+// re-check of the CTA-per-vector kernel above (a few percent of the views).
 constexpr int QW_WARPS = 8;
-constexpr int QW_MAXC = 32;
 
 __global__ void __launch_bounds__(QW_WARPS * 32)
     quant_select_warp_kernel(const float* __restrict__ approx, int64_t n, int K, int ma,
@@ -440,17 +472,13 @@ __global__ void __launch_bounds__(QW_WARPS * 32)
                              const uint8_t* __restrict__ nz, int zero_key, int need_order,
                              int32_t* __restrict__ out, const double* __restrict__ cn2,
                              int ksplit, double dot_eps, const float* __restrict__ xnorm2,
-                             int32_t* __restrict__ flags,
-                             const __grid_constant__ PairwisePlan plan) {
-  extern __shared__ __align__(16) double qw_lv[];  // [QW_WARPS][n_leaves]
-  __shared__ int s_ci[QW_WARPS][QW_MAXC];
-  __shared__ double s_cd[QW_WARPS][QW_MAXC];
+                             int32_t* __restrict__ list, int32_t* __restrict__ list_count) {
+  __shared__ int s_ci[QW_WARPS][8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t v = static_cast<int64_t>(blockIdx.x) * QW_WARPS + warp;
   if (v >= n) return;
   if (nz != nullptr && nz[v] == 0) {
     for (int s = lane; s < ma; s += 32) out[v * ma + s] = zero_key >= 0 ? zero_key : -1;
-    if (lane == 0) flags[v] = 0;
     return;
   }
   const int64_t xoff = v * static_cast<int64_t>(d);
@@ -548,16 +576,11 @@ __global__ void __launch_bounds__(QW_WARPS * 32)
     const bool hit = c < K && static_cast<double>(x) <= thresh;
     const unsigned bal = __ballot_sync(0xffffffffu, hit);
     const int pos = cnt + __popc(bal & lt);
-    if (hit && pos < QW_MAXC) s_ci[warp][pos] = c;
+    if (hit && pos < 8) s_ci[warp][pos] = c;
     cnt += __popc(bal);
   }
   __syncwarp();
-  if (cnt > QW_MAXC) {
-    if (lane == 0) flags[v] = 1;  // large candidate set: CTA kernel
-    return;
-  }
   int* ci = s_ci[warp];
-  double* cd = s_cd[warp];
   if (cnt == ma && (ma == 1 || !need_order)) {
     if (lane == 0) {
       for (int i = 1; i < ma; ++i)
@@ -567,63 +590,15 @@ __global__ void __launch_bounds__(QW_WARPS * 32)
           ci[j - 1] = t;
         }
       for (int s = 0; s < ma; ++s) out[v * ma + s] = ci[s];
-      flags[v] = 0;
     }
     return;
   }
-  // exact numpy-order d2 of each candidate (4 leaves at a time per warp)
-  double* lv = qw_lv + warp * plan.n_leaves;
-  const int grp = lane >> 3, gl = lane & 7;
-  const unsigned gmask = 0xFFu << (grp * 8);
-  for (int q = 0; q < cnt; ++q) {
-    const float* crow = C + static_cast<int64_t>(ci[q]) * d;
-    for (int l0 = 0; l0 < plan.n_leaves; l0 += 4) {
-      const int l = l0 + grp;
-      if (l < plan.n_leaves) {
-        const double r =
-            leaf_group(nullptr, X, xdtype, xoff, crow, plan.leaf_off[l], plan.leaf_len[l], gl, gmask);
-        if (gl == 0) lv[l] = r;
-      }
-    }
-    __syncwarp();
-    if (lane == 0) {
-      double stk[24];
-      int sp = 0, li = 0;
-      for (int o = 0; o < plan.n_ops; ++o) {
-        if (plan.ops[o] == 0) {
-          stk[sp++] = lv[li++];
-        } else {
-          const double bb = stk[--sp];
-          const double aa = stk[--sp];
-          stk[sp++] = __dadd_rn(aa, bb);
-        }
-      }
-      cd[q] = stk[0];
-    }
-    __syncwarp();
-  }
-  if (lane == 0) {
-    // insertion sort by (d2, index)
-    for (int i = 1; i < cnt; ++i)
-      for (int j = i; j > 0 && (cd[j] < cd[j - 1] || (cd[j] == cd[j - 1] && ci[j] < ci[j - 1]));
-           --j) {
-        const double td = cd[j];
-        cd[j] = cd[j - 1];
-        cd[j - 1] = td;
-        const int ti = ci[j];
-        ci[j] = ci[j - 1];
-        ci[j - 1] = ti;
-      }
-    for (int s = 0; s < ma; ++s) out[v * ma + s] = ci[s];
-    flags[v] = 0;
-  }
+  if (lane == 0) list[atomicAdd(list_count, 1)] = static_cast<int32_t>(v);  // exact re-check
 }
 
 }  // namespace gift
 
 using namespace gift;
-
-constexpr int QA_MAX_SPLIT = 8;
 
 static size_t quant_fixed_bytes(int d, int K) {
   return 2 * align_up(static_cast<size_t>(K) * d * 2, 1024) + 16384;
@@ -690,9 +665,11 @@ int quantize_impl(const void* X, int32_t xdtype, int64_t n, int32_t d, const flo
   GIFT_REQUIRE(approx != nullptr && (xdtype != GIFT_F64 || xconv != nullptr), GIFT_ERR_CAPACITY,
                "quantize workspace too small");
   const bool use_tc = quant_tc_supported(d, xdtype);
-  int32_t* flags = ma <= 8 ? ar.take<int32_t>(rows) : nullptr;
-  GIFT_REQUIRE(ma > 8 || flags != nullptr, GIFT_ERR_CAPACITY, "quantize workspace too small");
-  const int qw_smem = QW_WARPS * plan.n_leaves * 8;
+  // views left for the CTA kernel by the warp kernel (+ their count)
+  int32_t* list = ma <= 8 ? ar.take<int32_t>(rows + 1) : nullptr;
+  GIFT_REQUIRE(ma > 8 || list != nullptr, GIFT_ERR_CAPACITY, "quantize workspace too small");
+  int32_t* list_count = list != nullptr ? list + rows : nullptr;
+  const int sel_grid = sm_count() * 4;
   void* tc_ws = ar.base + align_up(ar.used, 256);
   const size_t tc_ws_bytes = ar.remaining();
 
@@ -739,17 +716,19 @@ int quantize_impl(const void* X, int32_t xdtype, int64_t n, int32_t d, const flo
       const double m = kchunk + ksplit + 2;
       dot_eps = m * u32 / (1.0 - m * u32) + 2.0 * u32;
     }
-    if (flags != nullptr) {
-      quant_select_warp_kernel<<<static_cast<unsigned>(cdiv(nr, QW_WARPS)), QW_WARPS * 32, qw_smem,
+    if (list != nullptr) {
+      GIFT_CUDA_TRY(cudaMemsetAsync(list_count, 0, sizeof(int32_t), st));
+      quant_select_warp_kernel<<<static_cast<unsigned>(cdiv(nr, QW_WARPS)), QW_WARPS * 32, 0,
                                  st>>>(approx, nr, K, ma, xs, xdtype, d, C, cmax_norm,
                                        nz ? nz + r0 : nullptr, zero_key, need_order ? 1 : 0,
                                        out_idx + r0 * ma, cnorm2, ksplit, dot_eps,
-                                       xnorm2 ? xnorm2 + r0 : nullptr, flags, plan);
+                                       xnorm2 ? xnorm2 + r0 : nullptr, list, list_count);
       GIFT_LAUNCH_CHECK();
     }
-    quant_select_kernel<<<static_cast<unsigned>(nr), QS_THREADS, sel_smem, st>>>(
+    quant_select_kernel<<<static_cast<unsigned>(min64(nr, sel_grid)), QS_THREADS, sel_smem, st>>>(
         approx, nr, K, ma, xs, xdtype, d, C, cmax_norm, nz ? nz + r0 : nullptr, zero_key, p2k,
-        need_order ? 1 : 0, stage_x, out_idx + r0 * ma, cnorm2, ksplit, dot_eps, flags, plan);
+        need_order ? 1 : 0, stage_x, out_idx + r0 * ma, cnorm2, ksplit, dot_eps, list, list_count,
+        plan);
     GIFT_LAUNCH_CHECK();
   }
   return GIFT_OK;

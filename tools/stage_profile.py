@@ -32,6 +32,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--kernels", action="store_true",
                     help="also print per-kernel device time (torch.profiler / CUPTI)")
+    ap.add_argument("--no-quantize", action="store_true",
+                    help="skip the separately timed quantize call (kernel totals = pipeline only)")
     ap.add_argument("--reduce", default="gather,range",
                     help="comma list of reduce implementations to time (GIFT_REDUCE)")
     args = ap.parse_args()
@@ -44,13 +46,14 @@ def main():
     batches = [qs[j * B:(j + 1) * B].contiguous() for j in range(max(1, qs.shape[0] // B))]
     for impl in args.reduce.split(","):
         os.environ["GIFT_REDUCE"] = impl
-        profile(eng, w, batches, args.steps, impl, build_s)
+        profile(eng, w, batches, args.steps, impl, build_s, not args.no_quantize)
         if args.kernels:
             from torch.profiler import ProfilerActivity
             from torch.profiler import profile as tprof
 
             with tprof(activities=[ProfilerActivity.CUDA]) as prof:
-                profile(eng, w, batches, args.steps, impl + "+cupti", build_s)
+                profile(eng, w, batches, args.steps, impl + "+cupti", build_s,
+                        not args.no_quantize)
             rows = []
             for e in prof.key_averages():
                 t = getattr(e, "device_time_total", None) or getattr(e, "cuda_time_total", 0)
@@ -62,7 +65,7 @@ def main():
                               [[round(t, 4), c, k] for t, c, k in rows[:25]]}), flush=True)
 
 
-def profile(eng, w, batches, steps, impl, build_s):
+def profile(eng, w, batches, steps, impl, build_s, quant=True):
     B = w.batch
     names = ["quantize", "score", "scan", "topk_cand", "act_mean", "sif_query", "topk_final"]
     tot = {n: 0.0 for n in names}
@@ -75,8 +78,9 @@ def profile(eng, w, batches, steps, impl, build_s):
             e.record()
         flat = Q.reshape(-1, Q.shape[-1])
         ev[0].record()
-        nz, _ = eg.view_prep(flat)
-        eg.quantize_rows(eng.fa.cb, flat, eng.cfg.ma, nz=nz)
+        if quant:
+            nz, _ = eg.view_prep(flat)
+            eg.quantize_rows(eng.fa.cb, flat, eng.cfg.ma, nz=nz)
         ev[1].record()
         _, cs, ci = eng.runner.score(eng.fa, Q, eng.cfg.ma, eng.mode, eng.cfg.sigma,
                                      scan_events=sev, cand_k=k2, dense=False)
