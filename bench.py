@@ -38,6 +38,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 from paper_1604_01879_b200 import IndexConfig, build_index_from_views, query_many  # noqa: E402
+from paper_1604_01879_b200.index import lane_streams  # noqa: E402
 from paper_1604_01879_b200 import engine as eg  # noqa: E402
 from paper_1604_01879_b200 import synth  # noqa: E402
 from paper_1604_01879_b200.codebook import Codebook  # noqa: E402
@@ -456,22 +457,38 @@ def run_gift(args, w):
     order = [(rank + i * ws) % nb for i in range(args.steps + args.warmup)]
     batches = [qs[j * B:(j + 1) * B].contiguous() for j in range(nb)]
     stream = torch.cuda.current_stream()
+    # batch i runs on lane i % L: its own stream and scratch, so one batch's
+    # quantize / reduce / re-rank kernels overlap the other batch's scan
+    L = max(1, args.lanes)
+    lanes = [stream] if L == 1 else lane_streams(L)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     scan_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(args.steps)]
-    for a, b in scan_ev:  # torch creates the CUDA events lazily, on first record
-        a.record(stream)
-        b.record(stream)
+    for i, (a, b) in enumerate(scan_ev):  # torch creates CUDA events lazily, on first record
+        a.record(lanes[i % L])
+        b.record(lanes[i % L])
+
+    def step(i, bi, sev=None):
+        s = lanes[i % L]
+        with torch.cuda.stream(s):
+            eng.run(batches[bi], top_k=w.top_k, rerank=True, scan_events=sev)
+
     with ClockSampler(local) as clk:
-        warm(lambda i: eng.run(batches[order[i % args.warmup]], top_k=w.top_k, rerank=True),
-             args.warmup)
+        for s in lanes:
+            s.wait_stream(stream)
+        warm(lambda i: step(i, order[i % args.warmup]), max(args.warmup, L))
+        for s in lanes:
+            stream.wait_stream(s)
         if ws > 1:
             dist.barrier()
         torch.cuda.synchronize()
         ev[0].record(stream)
+        for s in lanes:
+            s.wait_event(ev[0])
         for i in range(args.steps):
-            eng.run(batches[order[args.warmup + i]], top_k=w.top_k, rerank=True,
-                    scan_events=scan_ev[i])
+            step(i, order[args.warmup + i], scan_ev[i])
+        for s in lanes:
+            stream.wait_stream(s)
         ev[1].record(stream)
         torch.cuda.synchronize()
         if ws > 1:
@@ -489,12 +506,12 @@ def run_gift(args, w):
     host = torch.empty((args.steps * B, w.n_views, w.dim), dtype=torch.float32, pin_memory=True)
     for i in range(args.steps):
         host[i * B:(i + 1) * B].copy_(batches[order[args.warmup + i]])
-    query_many(bundle, host[:B], top_k=w.top_k)  # warm
+    query_many(bundle, host[:L * B], top_k=w.top_k, lanes=L)  # warm
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    query_many(bundle, host, top_k=w.top_k)
+    query_many(bundle, host, top_k=w.top_k, lanes=L)
     e2e_s = time.perf_counter() - t0
     t = torch.tensor([e2e_s], dtype=torch.float64, device=device)
     if ws > 1:
@@ -555,7 +572,7 @@ def run_gift(args, w):
                            "dim": w.dim, "K": w.K, "ma": w.ma, "similarity": "gaussian",
                            "sigma": w.sigma, "k1": w.k1, "k2": w.k2, "top_k": w.top_k,
                            "batch": B, "parallelism": f"replicas{ws}",
-                           "storage": w.storage, "n_queries": w.n_queries,
+                           "lanes": L, "storage": w.storage, "n_queries": w.n_queries,
                            "l2": "inputs larger than L2 (database >= 10.5 GB)",
                            "features": "planes only (streamed build)" if eng.fa.feat is None
                            else "storage copy + planes",
@@ -580,6 +597,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(synth.WORKLOADS) + ["c5"])
     ap.add_argument("--c5-shapes", type=int, default=0, help="override config-5 N (smoke runs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--lanes", type=int, default=4,
+                    help="batches in flight on separate streams (1 = serial)")
     ap.add_argument("--shard", action="store_true",
                     help="shard the database by shape over the ranks (configs 3/4)")
     args = ap.parse_args()

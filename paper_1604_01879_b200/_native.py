@@ -192,11 +192,14 @@ class Workspace:
 _ws_local = threading.local()
 
 
-def workspace(slot: str = "default") -> Workspace:
+def workspace(slot: str = "default", stream=None) -> Workspace:
+    """Scratch buffer of `slot` for the launches on `stream` (default: the
+    current stream): work queued on different streams never shares scratch."""
     d = getattr(_ws_local, "pool", None)
     if d is None:
         d = _ws_local.pool = {}
-    ws = d.get(slot)
+    key = (slot, stream_ptr(stream))
+    ws = d.get(key)
     if ws is None:
-        ws = d[slot] = Workspace()
+        ws = d[key] = Workspace()
     return ws

@@ -25,6 +25,7 @@ namespace gift {
 
 constexpr int64_t RED_SMEM = 64 * 1024;  // reduce CTA view-best tile budget
 constexpr int RED_THREADS = 256;
+constexpr int RED_MAX_RS = 2048;  // shapes per reduce range (reduce_rs cap)
 constexpr int PLAN_THREADS = 1024;
 
 
@@ -290,18 +291,74 @@ struct ReduceArgs {
 
 constexpr int RED_MAXK = 8;
 
-struct Cand {
-  double s;
-  int32_t o;  // global ordinal, -1 = none (sorts last)
-};
+// candidate order: score descending, then global ordinal ascending (-1 =
+// none sorts last)
 __device__ __forceinline__ bool cand_better(double s1, int32_t o1, double s2, int32_t o2) {
   return s1 > s2 || (s1 == s2 && static_cast<uint32_t>(o1) < static_cast<uint32_t>(o2));
 }
-struct CandBetter {
-  __device__ bool operator()(const Cand& x, const Cand& y) const {
-    return cand_better(x.s, x.o, y.s, y.o);
+
+// Sorted best-ck insertion (score desc, ordinal asc) into per-thread lists.
+__device__ __forceinline__ void cand_insert(double (&ls)[RED_MAXK], int32_t (&lo)[RED_MAXK],
+                                            int ck, double xs, int32_t xo) {
+  double lastv = ls[0];  // ls[ck - 1] without dynamic register indexing
+  int32_t lasto = lo[0];
+#pragma unroll
+  for (int t = 1; t < RED_MAXK; ++t)
+    if (t == ck - 1) {
+      lastv = ls[t];
+      lasto = lo[t];
+    }
+  if (!cand_better(xs, xo, lastv, lasto)) return;
+#pragma unroll
+  for (int t = 0; t < RED_MAXK; ++t) {
+    if (t < ck && cand_better(xs, xo, ls[t], lo[t])) {
+      const double ys = ls[t];
+      const int32_t yo = lo[t];
+      ls[t] = xs;
+      lo[t] = xo;
+      xs = ys;
+      xo = yo;
+    }
   }
-};
+}
+
+// Warp: the ck best of the lanes' sorted lists, in order, via ck rounds of
+// argmax; lane 0 receives them in (os, oo).
+__device__ __forceinline__ void warp_select(double (&ls)[RED_MAXK], int32_t (&lo)[RED_MAXK],
+                                            int ck, double* os_out, int32_t* oo_out) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int r = 0; r < RED_MAXK; ++r) {
+    if (r >= ck) break;
+    double bs = ls[0];
+    int32_t bo = lo[0];
+    int bl = lane;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double os = __shfl_xor_sync(0xffffffffu, bs, off);
+      const int32_t oo = __shfl_xor_sync(0xffffffffu, bo, off);
+      const int ol = __shfl_xor_sync(0xffffffffu, bl, off);
+      if (cand_better(os, oo, bs, bo) || (os == bs && oo == bo && ol < bl)) {
+        bs = os;
+        bo = oo;
+        bl = ol;
+      }
+    }
+    if (lane == 0) {
+      os_out[r] = bs;
+      oo_out[r] = bo;
+    }
+    if (lane == bl) {  // pop the winner's head
+#pragma unroll
+      for (int t = 0; t + 1 < RED_MAXK; ++t) {
+        ls[t] = ls[t + 1];
+        lo[t] = lo[t + 1];
+      }
+      ls[RED_MAXK - 1] = -INFINITY;
+      lo[RED_MAXK - 1] = -1;
+    }
+  }
+}
 
 // Per (query, shape range of rs shapes): every (view, slot) probe's
 // per-segment maxima are max-ed into vb[view][shape] (shared, atomicMax on
@@ -320,115 +377,162 @@ __global__ void __launch_bounds__(RED_THREADS) fif_reduce_kernel(ReduceArgs a) {
   const int n = static_cast<int>(min64(lo + rs, a.n_local) - lo);
   const int64_t glo = a.ord_base + lo;
   const int V = a.V;
-  for (int i = tid; i < V * rs; i += RED_THREADS) vb[i] = 0.f;
+  for (int i = tid; i < (V * rs) >> 2; i += RED_THREADS)
+    reinterpret_cast<float4*>(vb)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int i = ((V * rs) & ~3) + tid; i < V * rs; i += RED_THREADS) vb[i] = 0.f;
   __syncthreads();
   const int64_t pbase = static_cast<int64_t>(b) * V * a.ma;
   const int nslot = V * a.ma;
-  // warp w owns slots [w * per, (w + 1) * per); their (slot, segment) pairs
-  // are flattened so every lane's loads are independent (latency overlap)
+  // warp w owns slots [w * per, (w + 1) * per)
   const int warp = tid >> 5, lane = tid & 31;
   constexpr int NW = RED_THREADS / 32;
   const int per = (nslot + NW - 1) / NW;
   const int s0 = warp * per, s1 = min(nslot, s0 + per);
+  // shapes with a positive view best: the only columns worth summing
+  __shared__ uint32_t s_touch[RED_MAX_RS / 32];
+  __shared__ int s_list[RED_MAX_RS];
+  __shared__ int s_nt;
+  for (int i = tid; i < RED_MAX_RS / 32; i += RED_THREADS) s_touch[i] = 0u;
+  if (tid == 0) s_nt = 0;
+  __syncthreads();
+  auto put = [&](int row, int o, float val) {
+    atomicMax(reinterpret_cast<int*>(vb + row * rs + o), __float_as_int(val));
+    if (val > 0.f) atomicOr(&s_touch[o >> 5], 1u << (o & 31));
+  };
+  constexpr int RED_UNROLL = 4;
   for (int c0 = s0; c0 < s1; c0 += 32) {
     // lane j holds slot c0 + j's range
     const int sj = c0 + lane;
     ProbeRange pr{0, 0, 0, 0};
     if (sj < s1) pr = a.rng[(pbase + sj) * a.n_ranges + rg];
     const int len = pr.sb - pr.sa;
+    const int maxlen = __reduce_max_sync(0xffffffffu, len);
+    const int total = __reduce_add_sync(0xffffffffu, len);
+    if (maxlen * 32 <= 2 * total + 64) {
+      // balanced: every lane walks its own slot, RED_UNROLL items per pass
+      // with all loads issued before the first atomic
+      const int row = sj / a.ma;
+      for (int k0 = 0; k0 < maxlen; k0 += RED_UNROLL) {
+        int oo[RED_UNROLL];
+        float vv[RED_UNROLL];
+#pragma unroll
+        for (int u = 0; u < RED_UNROLL; ++u) {
+          const int k = pr.sa + k0 + u;
+          if (k0 + u < len) {
+            oo[u] = static_cast<int>(a.seg_ord[pr.seg0 + k] - glo);
+            vv[u] = a.out[pr.base + k];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < RED_UNROLL; ++u)
+          if (k0 + u < len) put(row, oo[u], vv[u]);
+      }
+      continue;
+    }
+    // skewed: the warp's (slot, segment) pairs are flattened so every lane
+    // has work (slot of item `it` found by a shuffle search over the
+    // exclusive prefix of the lengths)
     int incl = len;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int y = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += y;
     }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
     const int excl = incl - len;
-    for (int it0 = 0; it0 < total; it0 += 32) {  // warp-uniform trip count
-      const int it = it0 + lane;
-      // slot owning item `it`: largest j with excl_j <= it (shuffle search)
-      int j = 0;
+    for (int it0 = 0; it0 < total; it0 += 32 * RED_UNROLL) {  // warp-uniform trip count
+      int oo[RED_UNROLL], row[RED_UNROLL];
+      float vv[RED_UNROLL];
 #pragma unroll
-      for (int step = 16; step > 0; step >>= 1) {
-        const int cand = j + step;
-        const int ex = __shfl_sync(0xffffffffu, excl, cand);
-        if (cand < 32 && ex <= it) j = cand;
+      for (int u = 0; u < RED_UNROLL; ++u) {
+        const int it = it0 + u * 32 + lane;
+        int j = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const int cand = j + step;
+          const int ex = __shfl_sync(0xffffffffu, excl, cand);
+          if (cand < 32 && ex <= it) j = cand;
+        }
+        const int ej = __shfl_sync(0xffffffffu, excl, j);
+        const int saj = __shfl_sync(0xffffffffu, pr.sa, j);
+        const int64_t seg0 = __shfl_sync(0xffffffffu, pr.seg0, j);
+        const int64_t base = __shfl_sync(0xffffffffu, pr.base, j);
+        row[u] = -1;
+        if (it < total) {
+          const int k = saj + (it - ej);
+          oo[u] = static_cast<int>(a.seg_ord[seg0 + k] - glo);
+          vv[u] = a.out[base + k];
+          row[u] = (c0 + j) / a.ma;
+        }
       }
-      const int ej = __shfl_sync(0xffffffffu, excl, j);
-      const int saj = __shfl_sync(0xffffffffu, pr.sa, j);
-      const int64_t seg0 = __shfl_sync(0xffffffffu, pr.seg0, j);
-      const int64_t base = __shfl_sync(0xffffffffu, pr.base, j);
-      if (it < total) {
-        const int k = saj + (it - ej);
-        const int o = static_cast<int>(a.seg_ord[seg0 + k] - glo);
-        const float val = a.out[base + k];
-        atomicMax(reinterpret_cast<int*>(vb + ((c0 + j) / a.ma) * rs + o), __float_as_int(val));
-      }
+#pragma unroll
+      for (int u = 0; u < RED_UNROLL; ++u)
+        if (row[u] >= 0) put(row[u], oo[u], vv[u]);
     }
+  }
+  __syncthreads();
+  // touched shapes -> list; each one's column is summed in view order in f64
+  // (untouched columns are all zero: their sum is exactly 0.0) and the f64
+  // total parked in rows 0-1 of its own column
+  for (int o = tid; o < n; o += RED_THREADS)
+    if ((s_touch[o >> 5] >> (o & 31)) & 1u) s_list[atomicAdd(&s_nt, 1)] = o;
+  __syncthreads();
+  const int nt = s_nt;
+  for (int t = tid; t < nt; t += RED_THREADS) {
+    const int o = s_list[t];
+    double acc = 0.0;
+    for (int v = 0; v < V; ++v) acc += static_cast<double>(vb[v * rs + o]);
+    const int2 w = make_int2(__double2loint(acc), __double2hiint(acc));
+    vb[o] = __int_as_float(w.x);
+    vb[rs + o] = __int_as_float(w.y);
   }
   __syncthreads();
   const double denom = static_cast<double>(a.vq ? a.vq[b] : V);
   const int ck = a.cand_k;
-  Cand best[RED_MAXK];
+  double ls[RED_MAXK];
+  int32_t lo_[RED_MAXK];
 #pragma unroll
-  for (int i = 0; i < RED_MAXK; ++i) best[i] = Cand{-INFINITY, -1};
+  for (int i = 0; i < RED_MAXK; ++i) {
+    ls[i] = -INFINITY;
+    lo_[i] = -1;
+  }
   for (int o = tid; o < n; o += RED_THREADS) {
-    double acc = 0.0;
-    for (int v = 0; v < V; ++v) acc += static_cast<double>(vb[v * rs + o]);
+    const bool hit = (s_touch[o >> 5] >> (o & 31)) & 1u;
+    const double acc =
+        hit ? __hiloint2double(__float_as_int(vb[rs + o]), __float_as_int(vb[o])) : 0.0;
     const double sc = acc / denom;
     if (a.scores) a.scores[static_cast<int64_t>(b) * a.n_local + lo + o] = sc;
-    if (ck > 0) {  // per-thread sorted best list (ordinals ascend within a thread)
-      Cand x{sc, static_cast<int32_t>(glo + o)};
-#pragma unroll
-      for (int i = 0; i < RED_MAXK; ++i) {
-        if (cand_better(x.s, x.o, best[i].s, best[i].o)) {
-          const Cand t = best[i];
-          best[i] = x;
-          x = t;
-        }
-      }
-    }
+    if (ck > 0) cand_insert(ls, lo_, ck, sc, static_cast<int32_t>(glo + o));
   }
   if (ck > 0) {
-    __shared__ Cand s_best[RED_THREADS / 32][RED_MAXK];
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      Cand other[RED_MAXK];
-#pragma unroll
-      for (int i = 0; i < RED_MAXK; ++i) {
-        other[i].s = __shfl_xor_sync(0xffffffffu, best[i].s, off);
-        other[i].o = __shfl_xor_sync(0xffffffffu, best[i].o, off);
-      }
-      merge8(best, other, CandBetter());
-    }
-    const int warp = tid >> 5, lane = tid & 31;
+    // per warp: ck rounds of argmax over the lanes' lists; then warp 0 over
+    // the warps' lists
+    __shared__ double s_bs[NW][RED_MAXK];
+    __shared__ int32_t s_bo[NW][RED_MAXK];
+    double os[RED_MAXK];
+    int32_t oo[RED_MAXK];
+    warp_select(ls, lo_, ck, os, oo);
     if (lane == 0)
 #pragma unroll
-      for (int i = 0; i < RED_MAXK; ++i) s_best[warp][i] = best[i];
+      for (int r = 0; r < RED_MAXK; ++r) {
+        s_bs[warp][r] = r < ck ? os[r] : -INFINITY;
+        s_bo[warp][r] = r < ck ? oo[r] : -1;
+      }
     __syncthreads();
     if (tid < 32) {
-      Cand mine[RED_MAXK];
 #pragma unroll
-      for (int i = 0; i < RED_MAXK; ++i)
-        mine[i] = tid < RED_THREADS / 32 ? s_best[tid][i] : Cand{-INFINITY, -1};
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        Cand other[RED_MAXK];
-#pragma unroll
-        for (int i = 0; i < RED_MAXK; ++i) {
-          other[i].s = __shfl_xor_sync(0xffffffffu, mine[i].s, off);
-          other[i].o = __shfl_xor_sync(0xffffffffu, mine[i].o, off);
-        }
-        merge8(mine, other, CandBetter());
+      for (int r = 0; r < RED_MAXK; ++r) {
+        ls[r] = lane < NW ? s_bs[lane][r] : -INFINITY;
+        lo_[r] = lane < NW ? s_bo[lane][r] : -1;
       }
-      if (tid == 0) {
-      const int64_t at = (static_cast<int64_t>(b) * a.n_ranges + rg) * ck;
+      warp_select(ls, lo_, ck, os, oo);
+      if (lane == 0) {
+        const int64_t at = (static_cast<int64_t>(b) * a.n_ranges + rg) * ck;
 #pragma unroll
-      for (int i = 0; i < RED_MAXK; ++i)
-        if (i < ck) {
-          a.cand_s[at + i] = mine[i].o >= 0 ? mine[i].s : 0.0;
-          a.cand_i[at + i] = mine[i].o;
-        }
+        for (int r = 0; r < RED_MAXK; ++r)
+          if (r < ck) {
+            a.cand_s[at + r] = oo[r] >= 0 ? os[r] : 0.0;
+            a.cand_i[at + r] = oo[r];
+          }
       }
     }
   }
@@ -725,68 +829,6 @@ __device__ __forceinline__ double pair_acc(const GatherArgs& a, const GrTabs& t,
   return acc + static_cast<double>(best);
 }
 
-// Sorted best-ck insertion (score desc, ordinal asc) into per-thread lists.
-__device__ __forceinline__ void cand_insert(double (&ls)[RED_MAXK], int32_t (&lo)[RED_MAXK],
-                                            int ck, double xs, int32_t xo) {
-  double lastv = ls[0];  // ls[ck - 1] without dynamic register indexing
-  int32_t lasto = lo[0];
-#pragma unroll
-  for (int t = 1; t < RED_MAXK; ++t)
-    if (t == ck - 1) {
-      lastv = ls[t];
-      lasto = lo[t];
-    }
-  if (!cand_better(xs, xo, lastv, lasto)) return;
-#pragma unroll
-  for (int t = 0; t < RED_MAXK; ++t) {
-    if (t < ck && cand_better(xs, xo, ls[t], lo[t])) {
-      const double ys = ls[t];
-      const int32_t yo = lo[t];
-      ls[t] = xs;
-      lo[t] = xo;
-      xs = ys;
-      xo = yo;
-    }
-  }
-}
-
-// Warp: the ck best of the lanes' sorted lists, in order, via ck rounds of
-// argmax; lane 0 receives them in (os, oo).
-__device__ __forceinline__ void warp_select(double (&ls)[RED_MAXK], int32_t (&lo)[RED_MAXK],
-                                            int ck, double* os_out, int32_t* oo_out) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int r = 0; r < RED_MAXK; ++r) {
-    if (r >= ck) break;
-    double bs = ls[0];
-    int32_t bo = lo[0];
-    int bl = lane;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const double os = __shfl_xor_sync(0xffffffffu, bs, off);
-      const int32_t oo = __shfl_xor_sync(0xffffffffu, bo, off);
-      const int ol = __shfl_xor_sync(0xffffffffu, bl, off);
-      if (cand_better(os, oo, bs, bo) || (os == bs && oo == bo && ol < bl)) {
-        bs = os;
-        bo = oo;
-        bl = ol;
-      }
-    }
-    if (lane == 0) {
-      os_out[r] = bs;
-      oo_out[r] = bo;
-    }
-    if (lane == bl) {  // pop the winner's head
-#pragma unroll
-      for (int t = 0; t + 1 < RED_MAXK; ++t) {
-        ls[t] = ls[t + 1];
-        lo[t] = lo[t + 1];
-      }
-      ls[RED_MAXK - 1] = -INFINITY;
-      lo[RED_MAXK - 1] = -1;
-    }
-  }
-}
 
 template <int W>
 __global__ void __launch_bounds__(GR_THREADS) fif_gather_reduce_kernel(GatherArgs a) {
@@ -1007,7 +1049,7 @@ bool use_tc(const gift_fif_view* f) {
 
 int reduce_rs(int64_t V, int64_t n_local) {
   int rs = static_cast<int>(RED_SMEM / (4 * max64(V, 1)));
-  rs = max(32, min(rs, 2048)) / 32 * 32;
+  rs = max(32, min(rs, RED_MAX_RS)) / 32 * 32;
   return static_cast<int>(max64(min64(rs, n_local), 1));
 }
 
@@ -1370,7 +1412,7 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
   ra.cand_k = cand_s != nullptr ? cand_k : 0;
   ra.cand_s = cand_s;
   ra.cand_i = cand_i;
-  const int red_smem = V * rs * 4;
+  const int red_smem = max(V, 2) * rs * 4;  // rows 0-1 also park the f64 totals
   GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      red_smem));
   dim3 rgrid(static_cast<unsigned>(n_ranges), static_cast<unsigned>(B));

@@ -268,6 +268,66 @@ static int launch_topk(const double* scores, int B, int64_t n, int k, const int3
   return GIFT_OK;
 }
 
+// Small-k merge of explicit candidate rows (k <= 8): one warp per row.  Each
+// lane keeps the sorted best 8 of its strided entries, five xor-shuffle
+// merges (merge8) give the row's best 8; same keys and output as topk_kernel.
+struct TkKey {
+  double s;
+  uint32_t t;
+  int32_t j;
+};
+struct TkBetter {
+  __device__ bool operator()(const TkKey& x, const TkKey& y) const {
+    return key_better(x.s, x.t, y.s, y.t);
+  }
+};
+constexpr int TKS_WARPS = 8;
+
+__global__ void __launch_bounds__(TKS_WARPS * 32)
+    topk_small_kernel(const TopkIn in, const TopkOut out, int B) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x * TKS_WARPS + warp;
+  if (b >= B) return;
+  const int64_t e1 = in.counts ? min64(in.m, static_cast<int64_t>(in.counts[b])) : in.m;
+  TkKey best[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) best[i] = TkKey{-INFINITY, 0xffffffffu, -1};
+  const int64_t row = static_cast<int64_t>(b) * in.m;
+  for (int64_t e = lane; e < e1; e += 32) {
+    TkKey x{in.cs[row + e], 0u, in.ci[row + e]};
+    if (x.j < 0) continue;
+    x.t = in.ct ? in.ct[row + e] : static_cast<uint32_t>(x.j);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (TkBetter()(x, best[i])) {
+        const TkKey t = best[i];
+        best[i] = x;
+        x = t;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    TkKey oth[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      oth[i].s = __shfl_xor_sync(0xffffffffu, best[i].s, o);
+      oth[i].t = __shfl_xor_sync(0xffffffffu, best[i].t, o);
+      oth[i].j = __shfl_xor_sync(0xffffffffu, best[i].j, o);
+    }
+    merge8(best, oth, TkBetter());
+  }
+  const int k = out.k;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if (lane == i && i < k) {
+      const bool ok = best[i].j >= 0 && (!out.positive_only || best[i].s > 0.0);
+      out.out_idx[static_cast<int64_t>(b) * k + i] = ok ? best[i].j : -1;
+      out.out_val[static_cast<int64_t>(b) * k + i] = ok ? best[i].s : 0.0;
+    }
+  }
+}
+
 // Best k of explicit (score, tiebreak, global ordinal) rows with per-row
 // counts: the merge pass of the dense top-k (used by the sparse S-IF query).
 int topk_rows_from_lists(const double* cs, const uint32_t* ct, const int32_t* ci,
@@ -292,7 +352,12 @@ int topk_rows_from_lists(const double* cs, const uint32_t* ct, const int32_t* ci
   out.nslices = 1;
   out.out_idx = out_idx;
   out.out_val = out_val;
-  topk_kernel<256, false><<<dim3(1, B), TK_THREADS, smem, st>>>(in, out);
+  if (k <= 8) {
+    topk_small_kernel<<<static_cast<unsigned>(cdiv(B, TKS_WARPS)), TKS_WARPS * 32, 0, st>>>(in, out,
+                                                                                          B);
+  } else {
+    topk_kernel<256, false><<<dim3(1, B), TK_THREADS, smem, st>>>(in, out);
+  }
   GIFT_LAUNCH_CHECK();
   return GIFT_OK;
 }
@@ -350,7 +415,12 @@ extern "C" int gift_topk_cand(const double* cs, const int32_t* ci, int32_t B, in
   out.nslices = 1;
   out.out_idx = out_idx;
   out.out_val = out_val;
-  topk_kernel<256, false><<<dim3(1, B), TK_THREADS, smem, st>>>(in, out);
+  if (k <= 8) {
+    topk_small_kernel<<<static_cast<unsigned>(cdiv(B, TKS_WARPS)), TKS_WARPS * 32, 0, st>>>(in, out,
+                                                                                          B);
+  } else {
+    topk_kernel<256, false><<<dim3(1, B), TK_THREADS, smem, st>>>(in, out);
+  }
   GIFT_LAUNCH_CHECK();
   return GIFT_OK;
 }

@@ -86,7 +86,7 @@ def quantize_rows(cb: DeviceCodebook, X: torch.Tensor, ma: int, nz: torch.Tensor
         raise ValueError(f"ma must be in [1, {cb.K}]")
     out = torch.empty((n, ma), dtype=torch.int32, device=X.device)
     wsb = nat.lib().gift_quantize_ws_bytes(n, d, cb.K, _DTYPE_CODE[X.dtype])
-    ws = nat.workspace("quantize").get(wsb)
+    ws = nat.workspace("quantize", stream).get(wsb)
     nat.call("gift_quantize", nat.ptr(X), _DTYPE_CODE[X.dtype], n, d, nat.ptr(cb.centroids),
              nat.ptr(cb.cnorm2), cb.K, cb.cmax, ma, nat.ptr(nz), zero_key, nat.ptr(out),
              nat.ptr(ws), ws.numel(), _sp(stream))
@@ -110,7 +110,7 @@ def radix_sort_pairs(keys: torch.Tensor, vals: torch.Tensor, key_bits: int, stre
         return keys, vals
     kt = torch.empty_like(keys)
     vt = torch.empty_like(vals)
-    ws = nat.workspace("radix").get(nat.lib().gift_radix_sort_ws_bytes(n))
+    ws = nat.workspace("radix", stream).get(nat.lib().gift_radix_sort_ws_bytes(n))
     nat.call("gift_radix_sort_pairs", nat.ptr(keys), nat.ptr(vals), n, key_bits, nat.ptr(kt),
              nat.ptr(vt), nat.ptr(ws), ws.numel(), _sp(stream))
     return keys, vals
@@ -311,7 +311,7 @@ class DeviceFif:
                          nat.ptr(self.feat_hi), nat.ptr(self.feat_lo), _sp(stream))
         else:
             self.feat_hi = self.feat_lo = None
-        ws = nat.workspace("build").get(nat.lib().gift_fif_build_ws_bytes(P, K))
+        ws = nat.workspace("build", stream).get(nat.lib().gift_fif_build_ws_bytes(P, K))
         self.seg_off = torch.empty(K + 1, dtype=torch.int64, device=dev)
         nat.call("gift_fif_segments", nat.ptr(self.cell_off), nat.ptr(self.post_ord), K, P,
                  nat.ptr(self.seg_off), None, None, nat.ptr(ws), ws.numel(), _sp(stream))
@@ -377,7 +377,7 @@ class DeviceFif:
         dev = self.post_ord.device
         nkb = self.d // 64
         off = torch.empty(self.T * nkb + 1, dtype=torch.int64, device=dev)
-        ws = nat.workspace("build").get(lib.gift_cts_ws_bytes(self.T, self.d))
+        ws = nat.workspace("build", stream).get(lib.gift_cts_ws_bytes(self.T, self.d))
         nat.call("gift_cts_build", nat.ptr(self.feat_hi), nat.ptr(self.feat_lo), self.P, self.d,
                  nat.ptr(self.tile_pstart), nat.ptr(self.tile_pend), self.T, nat.ptr(off), None,
                  nat.ptr(ws), ws.numel(), _sp(stream))
@@ -439,7 +439,7 @@ class ScoreRunner:
 
     def __init__(self):
         self.capacity = 1 << 22
-        self.ws = nat.Workspace()
+        self._ws = {}  # stream handle -> Workspace (batches in flight on two streams)
 
     def score(self, fif: DeviceFif, Q: torch.Tensor, ma: int, mode: int = nat.SIM_COSINE,
               sigma: float = 0.5, vq: torch.Tensor | None = None, out: torch.Tensor | None = None,
@@ -480,7 +480,7 @@ class ScoreRunner:
             ci = torch.empty((B, nr * cand_k), dtype=torch.int32, device=Q.device)
         for _attempt in range(8):
             wsb = lib.gift_fif_score_ws_bytes(ctypes.byref(view), B, V, ma, self.capacity)
-            ws = self.ws.get(wsb)
+            ws = self._ws.setdefault(_sp(stream), nat.Workspace()).get(wsb)
             ev0, ev1 = scan_events if scan_events is not None else (None, None)
             nat.check(lib.gift_fif_score_ex2(ctypes.byref(view), nat.ptr(Q), B, V, nat.ptr(vq), ma,
                                              mode, float(sigma), nat.ptr(out), nat.ptr(ws),
@@ -517,7 +517,7 @@ def topk_rows(scores: torch.Tensor, k: int, *, idrank: torch.Tensor | None = Non
     B, n = scores.shape
     idx = torch.empty((B, k), dtype=torch.int32, device=scores.device)
     val = torch.empty((B, k), dtype=torch.float64, device=scores.device)
-    ws = nat.workspace("topk").get(nat.lib().gift_topk_ws_bytes(B, n, k))
+    ws = nat.workspace("topk", stream).get(nat.lib().gift_topk_ws_bytes(B, n, k))
     nat.call("gift_topk_rows_ex", nat.ptr(scores.contiguous()), B, n, k, nat.ptr(idrank),
              nat.ptr(self_local), ord_base, int(positive_only), nat.ptr(idx), nat.ptr(val),
              nat.ptr(ws), ws.numel(), _sp(stream))
@@ -623,7 +623,7 @@ class DeviceSif:
         dev = final.idx.device
         n = final.n
         row_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
-        ws = nat.workspace("sif").get((1 << 20) + 16 * n)
+        ws = nat.workspace("sif", stream).get((1 << 20) + 16 * n)
         nat.call("gift_act_compact", nat.ptr(final.idx), nat.ptr(final.val), nat.ptr(final.cnt),
                  final.cap, n, nat.ptr(row_off), None, None, None, None, nat.ptr(ws), ws.numel(),
                  _sp(stream))
@@ -653,19 +653,23 @@ class DeviceSif:
             self._max_list = ml
         return ml
 
-    def _acc_rows(self, B: int) -> torch.Tensor:
+    def _acc_rows(self, B: int, stream=None) -> torch.Tensor:
         """Zeroed f64 accumulator rows for the sparse query (kept zero by the
-        kernel): up to 2 per SM, within ~2.5 GB."""
+        kernel): up to 2 per SM, within ~2.5 GB; one set per stream."""
         sms = torch.cuda.get_device_properties(self.norms.device).multi_processor_count
         # row stride: n_local rounded to 64 doubles plus 40 (320 B): rows whose
         # stride is a multiple of a large power of two put the same hot shape
         # of every row on the same DRAM channel (measured 2.3x slower on C5)
         stride = (max(self.n_local, 1) + 63) // 64 * 64 + 40
         want = max(1, min(B, 2 * sms, (2_500_000_000 // 8) // stride))
-        acc = getattr(self, "_acc", None)
+        pool = self.__dict__.setdefault("_acc", {})
+        key = _sp(stream)
+        acc = pool.get(key)
         if acc is None or acc.shape[0] < want:
             acc = torch.zeros((want, stride), dtype=torch.float64, device=self.norms.device)
-            self._acc = acc
+            if stream is not None:
+                torch.cuda.current_stream().synchronize()  # zeroed before `stream` uses it
+            pool[key] = acc
         return acc
 
     def query_topk(self, q: ActRows, k: int, order: torch.Tensor, idrank: torch.Tensor | None,
@@ -681,9 +685,9 @@ class DeviceSif:
             return idx, val
         bound = q.cap * self.max_list
         lib = nat.lib()
-        ws = nat.workspace("sif_topk").get(
+        ws = nat.workspace("sif_topk", stream).get(
             lib.gift_sif_query_topk_ws_bytes(B, self.n_local, k, bound))
-        acc = self._acc_rows(B)
+        acc = self._acc_rows(B, stream)
         nat.call("gift_sif_query_topk", nat.ptr(self.e_off), nat.ptr(self.e_ord),
                  nat.ptr(self.e_val), nat.ptr(self.norms), self.n_global, self.n_local,
                  nat.ptr(q.idx), nat.ptr(q.val), nat.ptr(q.cnt), nat.ptr(q.norm), B, q.cap,

@@ -514,49 +514,73 @@ def query_batch(bundle: IndexBundle, views, top_k: int = 10, rerank: bool = True
     return out
 
 
+_LANES: dict = {}
+
+
+def lane_streams(n: int) -> list:
+    """The first n persistent side streams of the current device (scratch
+    buffers are kept per stream, so reusing the streams reuses them)."""
+    dev = torch.cuda.current_device()
+    have = _LANES.setdefault(dev, [])
+    while len(have) < n:
+        have.append(torch.cuda.Stream(device=dev))
+    return have[:n]
+
+
 def query_many(bundle: IndexBundle, views_host: torch.Tensor, top_k: int = 10,
-               rerank: bool = True, batch_size: int | None = None):
+               rerank: bool = True, batch_size: int | None = None, lanes: int = 2):
     """Throughput API (new): queries from pinned host memory [Q, V, d] f32,
-    processed in device batches with the host->device copy of batch i+1
-    overlapped with the compute of batch i on a second stream.  Returns host
-    (idx [Q, k] int32 global ordinals, val [Q, k] f64)."""
+    processed in device batches on `lanes` compute streams, the host->device
+    copy of the next batches overlapped with the compute on a copy stream.
+    Returns host (idx [Q, k] int32 global ordinals, val [Q, k] f64)."""
     eng = bundle.engine
     bs = batch_size or bundle.config.batch_size
     Qn, V, d = views_host.shape
     k = min(top_k, eng.n)
     dev = nat.device()
-    comp = torch.cuda.current_stream()
-    copy = torch.cuda.Stream()
-    bufs = [torch.empty((bs, V, d), dtype=torch.float32, device=dev) for _ in range(2)]
-    ready = [torch.cuda.Event() for _ in range(2)]
-    free = [torch.cuda.Event() for _ in range(2)]
+    main = torch.cuda.current_stream()
+    L = max(1, int(lanes))
+    # batch i computes on lane i % L (its own stream and scratch), so one
+    # batch's quantize / reduce / re-rank kernels overlap the other's scan
+    comp = [main] if L == 1 else lane_streams(L)
+    copy = lane_streams(L + 1)[L]
+    NB = max(2, L)  # input buffers: batch i lands in buffer i % NB
+    bufs = [torch.empty((bs, V, d), dtype=torch.float32, device=dev) for _ in range(NB)]
+    ready = [torch.cuda.Event() for _ in range(NB)]
+    free = [torch.cuda.Event() for _ in range(NB)]
     out_idx = torch.empty((Qn, k), dtype=torch.int32, pin_memory=True)
     out_val = torch.empty((Qn, k), dtype=torch.float64, pin_memory=True)
     nb = (Qn + bs - 1) // bs
 
     def issue(i):
-        s = i % 2
+        s = i % NB
         b0, b1 = i * bs, min(Qn, (i + 1) * bs)
         with torch.cuda.stream(copy):
             copy.wait_event(free[s])
             bufs[s][: b1 - b0].copy_(views_host[b0:b1], non_blocking=True)
             ready[s].record(copy)
 
-    free[0].record(comp)
-    free[1].record(comp)
-    if nb:
-        issue(0)
+    for c in comp:
+        c.wait_stream(main)
+    for s in range(NB):
+        free[s].record(main)
+    for i in range(min(NB, nb)):
+        issue(i)
     for i in range(nb):
-        s = i % 2
-        if i + 1 < nb:
-            issue(i + 1)
+        s = i % NB
         b0, b1 = i * bs, min(Qn, (i + 1) * bs)
-        comp.wait_event(ready[s])
-        idx, val = eng.run(bufs[s][: b1 - b0], top_k=k, rerank=rerank)
-        free[s].record(comp)
-        out_idx[b0:b1].copy_(idx, non_blocking=True)
-        out_val[b0:b1].copy_(val, non_blocking=True)
-    comp.synchronize()
+        cs = comp[i % L]
+        with torch.cuda.stream(cs):
+            cs.wait_event(ready[s])
+            idx, val = eng.run(bufs[s][: b1 - b0], top_k=k, rerank=rerank)
+            free[s].record(cs)
+            out_idx[b0:b1].copy_(idx, non_blocking=True)
+            out_val[b0:b1].copy_(val, non_blocking=True)
+        if i + NB < nb:
+            issue(i + NB)
+    for c in comp:
+        main.wait_stream(c)
+    main.synchronize()
     return out_idx.numpy(), out_val.numpy()
 
 
