@@ -127,6 +127,13 @@ int gift_cts_build(const void* feat_hi, const void* feat_lo, int64_t n_postings,
                    size_t ws_bytes, void* stream);
 int gift_cts_stage_limit(void);
 
+/* GIFTFT1 ingest: out[r, :] = f32(x[r, :] / norms[r]) (IEEE f64 division),
+ * rows with norms[r] == 0 copied unchanged -- features.py:67-71 `_unit`, the
+ * per-row re-normalization of import_features (features.py:140-185); norms
+ * are the host's f64 sqrt(x.dot(x)).  x and out may alias. */
+int gift_normalize_rows(const float* x, const double* norms, int64_t rows, int32_t d,
+                        float* out, void* stream);
+
 /* Per-view non-zero flag and |x|^2 (f64 accumulate, stored f32).
  * `row.any()` tests of matching.py:121 / :150. */
 int gift_view_prep(const void* X, int32_t xdtype, int64_t nviews, int32_t d,

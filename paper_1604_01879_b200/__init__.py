@@ -6,10 +6,12 @@ Drop-in for the reference package `shapesearch` on that path: the public API
 (`__init__.py:9-29` of the reference) keeps its names and semantics.
 """
 
+from .features import FeatureFile, import_features, write_features
 from .index import (
     IndexBundle,
     IndexConfig,
     build_index,
+    build_index_from_feature_file,
     build_index_from_lists,
     build_index_from_views,
     build_index_streamed,
@@ -24,9 +26,13 @@ from .index import (
 )
 
 __all__ = [
+    "FeatureFile",
+    "import_features",
+    "write_features",
     "IndexBundle",
     "IndexConfig",
     "build_index",
+    "build_index_from_feature_file",
     "build_index_from_lists",
     "build_index_from_views",
     "build_index_streamed",

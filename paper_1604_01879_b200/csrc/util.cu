@@ -290,6 +290,22 @@ __global__ void view_prep_kernel(const void* __restrict__ X, int dtype, int64_t 
   }
 }
 
+// GIFTFT1 ingest (features.py:67-71): row = (row_f64 / |row|) rounded to f32,
+// rows with |row| == 0 copied unchanged.  |row| comes from the host (numpy's
+// x.dot(x) of the reference, whose summation order belongs to its BLAS); the
+// division and the rounding are IEEE here as there.
+__global__ void normalize_rows_kernel(const float* x, const double* __restrict__ norms,
+                                      int64_t rows, int d, float* out) {  // x may alias out
+  const int64_t n = rows * d;
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (; i < n; i += stride) {
+    const double nr = norms[i / d];
+    const float v = x[i];
+    out[i] = nr == 0.0 ? v : __double2float_rn(__ddiv_rn(static_cast<double>(v), nr));
+  }
+}
+
 __global__ void gather_rows_f32_kernel(const void* __restrict__ src, int dtype, int d,
                                        const int64_t* __restrict__ idx, int64_t n,
                                        float* __restrict__ out) {
@@ -319,6 +335,17 @@ extern "C" int gift_offsets_from_sorted(const uint32_t* keys, int64_t n, int64_t
   int64_t cnt = nbuckets + 1;
   offsets_from_sorted_kernel<<<static_cast<unsigned>(cdiv(cnt, 256)), 256, 0, st>>>(keys, n,
                                                                                    nbuckets, out_off);
+  GIFT_LAUNCH_CHECK();
+  return GIFT_OK;
+}
+
+extern "C" int gift_normalize_rows(const float* x, const double* norms, int64_t rows, int32_t d,
+                                   float* out, void* stream) {
+  GIFT_REQUIRE(rows >= 0 && d >= 1, GIFT_ERR_INVALID, "bad shape");
+  if (rows == 0) return GIFT_OK;
+  cudaStream_t st = as_stream(stream);
+  normalize_rows_kernel<<<static_cast<unsigned>(min64(cdiv(rows * d, 256), 148 * 16)), 256, 0, st>>>(
+      x, norms, rows, d, out);
   GIFT_LAUNCH_CHECK();
   return GIFT_OK;
 }

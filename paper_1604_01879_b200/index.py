@@ -12,6 +12,7 @@ pipelined queries, D6), and IndexConfig fields `similarity`, `sigma`,
 from __future__ import annotations
 
 import json
+import os
 import logging
 import time
 from dataclasses import asdict, dataclass, field, fields, replace
@@ -404,24 +405,48 @@ def build_index(manifest, config: IndexConfig = IndexConfig(), jobs: int = 1,
     if set(feature_files) != set(CHANNELS):
         raise ChannelMismatch(f"feature files required for channels {CHANNELS}")
     config = replace(config, imported=True)
-    imported = {ch: ft.import_features(feature_files[ch], ch) for ch in CHANNELS}
-    mats = {ch: [] for ch in CHANNELS}
+    # device ingest (features.FeatureFile): rows stream from the files to the
+    # GPU and are re-normalized there, bit-identical to import_features
+    ffs = {ch: ft.FeatureFile(feature_files[ch], ch) for ch in CHANNELS}
+    sel = {ch: [] for ch in CHANNELS}
     ids, labels = [], {}
     for path, label in rows:
         sid = Path(path).stem
-        if sid not in imported["A"] or sid not in imported["B"]:
+        if sid not in ffs["A"]._index or sid not in ffs["B"]._index:
             log.warning("skipping shape %s: not present in feature files", sid)
             continue
         ids.append(sid)
         labels[sid] = label
         for ch in CHANNELS:
-            mats[ch].append(imported[ch][sid].matrix(ch))
+            sel[ch].append(ffs[ch].index_of(sid))
     if not ids:
         raise AllShapesFailed("every shape in the manifest failed to build")
-    va, vb = np.stack(mats["A"]), np.stack(mats["B"])
-    same = va.shape == vb.shape and np.array_equal(va, vb)
-    return build_index_from_views(va, ids, config, views_b=None if same else vb, labels=labels,
+    va = ffs["A"].device_rows(sel["A"])
+    if (os.path.realpath(ffs["A"].path) == os.path.realpath(ffs["B"].path)
+            and sel["A"] == sel["B"]):
+        vb = None  # one feature set feeds both channels (D4)
+    else:
+        vb = ffs["B"].device_rows(sel["B"])
+        if vb.shape == va.shape and torch.equal(va, vb):
+            vb = None
+    return build_index_from_views(va, ids, config, views_b=vb, labels=labels,
                                   codebooks=codebooks)
+
+
+def build_index_from_feature_file(path, config: IndexConfig = IndexConfig(), *, codebooks,
+                                  labels=None, chunk: int = 512, self_join_batch: int = 256,
+                                  keep_features: bool = False) -> IndexBundle:
+    """One GIFTFT1 file feeding both channels (D4), streamed through the
+    chunked build (`build_index_streamed`): shapes are read from the file,
+    normalized on the GPU and consumed chunk by chunk, so the database never
+    sits in host memory (SURVEY.md §8(f) row 2, config-3 scale)."""
+    f = ft.FeatureFile(path, "A")
+    if not len(f):
+        raise EmptyManifest(f"feature file {path} lists no shapes")
+    config = replace(config, imported=True)
+    return build_index_streamed(f.provider(), f.shape_ids, f.n_views, f.dim, config,
+                                codebooks=codebooks, labels=labels, chunk=chunk,
+                                keep_features=keep_features, self_join_batch=self_join_batch)
 
 
 # ------------------------------------------------------------------ query

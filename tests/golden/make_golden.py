@@ -290,7 +290,36 @@ def golden_eval():
         print("eval", name, "done")
 
 
+def golden_ingest():
+    """A GIFTFT1 file written by the reference's write_features (features.py
+    :121-137) from seeded raw rows -- scales 1e-3..1e3, all-zero rows, a
+    repeated id, a UTF-8 id -- and the reference's import_features result
+    (features.py:140-185: f64 row norm, divide, round to f32)."""
+    rng = np.random.default_rng(77)
+    ids = ["a", "shape_\u03b2", "c" * 40, "a", "z", "s0009"]
+    V, d = 6, 300
+    vss = []
+    for sid in ids:
+        m = rng.standard_normal((V, d)) * 10.0 ** rng.uniform(-3, 3, (V, 1))
+        m = np.abs(m).astype(np.float32) if sid != "z" else m.astype(np.float32)
+        m[rng.random(V) < 0.25] = 0.0
+        vss.append(as_viewset(sid, m, channels=("A",)))
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "feat.bin")
+        rft.write_features(path, vss, "A")
+        blob = open(path, "rb").read()
+        imp = rft.import_features(path, "A")
+    out = {"blob": np.frombuffer(blob, dtype=np.uint8),
+           "ids": np.array(list(imp), dtype=object).astype(str),
+           "mats": np.stack([imp[s].matrix("A") for s in imp])}
+    np.savez_compressed(os.path.join(HERE, "ingest.npz"), **out)
+    print("ingest done")
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["ingest"]:
+        golden_ingest()
+        sys.exit(0)
     if sys.argv[1:] == ["eval"]:
         golden_eval()
         sys.exit(0)
@@ -310,3 +339,4 @@ if __name__ == "__main__":
     golden_bundles()
     golden_exact()
     golden_eval()
+    golden_ingest()
