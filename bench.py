@@ -38,7 +38,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 from paper_1604_01879_b200 import IndexConfig, build_index_from_views, query_many  # noqa: E402
-from paper_1604_01879_b200.index import lane_streams  # noqa: E402
+from paper_1604_01879_b200.index import LANE_RESERVE_SMS, lane_streams  # noqa: E402
 from paper_1604_01879_b200 import engine as eg  # noqa: E402
 from paper_1604_01879_b200 import synth  # noqa: E402
 from paper_1604_01879_b200.codebook import Codebook  # noqa: E402
@@ -119,6 +119,13 @@ class ClockSampler:
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
                 "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# (batches in flight, SMs the scan leaves to the other lanes) per config:
+# config 2's non-scan kernels are ~20% of a step and overlap the next
+# batches' scans; config 3 gains little (owner reduce, 105 GB) and loses with
+# reserved SMs; config 4's tensor-bound scan gains nothing
+DEFAULT_LANES = {"c1": (4, LANE_RESERVE_SMS), "c2": (4, LANE_RESERVE_SMS), "c3": (2, 0)}
 
 
 def warm(fn, iters: int, min_s: float = 0.25):
@@ -459,7 +466,8 @@ def run_gift(args, w):
     stream = torch.cuda.current_stream()
     # batch i runs on lane i % L: its own stream and scratch, so one batch's
     # quantize / reduce / re-rank kernels overlap the other batch's scan
-    L = max(1, args.lanes)
+    lanes_default, reserve_default = DEFAULT_LANES.get(w.name, (1, 0))
+    L = max(1, args.lanes if args.lanes is not None else lanes_default)
     lanes = [stream] if L == 1 else lane_streams(L)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     scan_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -467,6 +475,12 @@ def run_gift(args, w):
     for i, (a, b) in enumerate(scan_ev):  # torch creates CUDA events lazily, on first record
         a.record(lanes[i % L])
         b.record(lanes[i % L])
+
+    # SMs the scan leaves to the other lanes' kernels (DEFAULT_LANES)
+    if args.reserve_sms is not None:
+        eng.reserve_sms = args.reserve_sms
+    else:
+        eng.reserve_sms = reserve_default if L > 1 else 0
 
     def step(i, bi, sev=None):
         s = lanes[i % L]
@@ -493,8 +507,28 @@ def run_gift(args, w):
         torch.cuda.synchronize()
         if ws > 1:
             dist.barrier()
+        # the scan's own duration: with batches in flight a scan's events also
+        # span its wait behind the previous batch's scan, so the kernel time
+        # for the roofline comes from the same batches run one at a time
+        # right after (CUDA events on the launching stream, inside the sampler)
+        if L > 1:
+            reserve, eng.reserve_sms = eng.reserve_sms, 0
+            serial_ev = [(torch.cuda.Event(enable_timing=True),
+                          torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+            for a, b in serial_ev:
+                a.record(stream)
+                b.record(stream)
+            torch.cuda.synchronize()
+            for i in range(args.steps):
+                eng.run(batches[order[args.warmup + i]], top_k=w.top_k, rerank=True,
+                        scan_events=serial_ev[i])
+            torch.cuda.synchronize()
+            eng.reserve_sms = reserve
+        else:
+            serial_ev = scan_ev
     ms = ev[0].elapsed_time(ev[1])
-    scan_ms = [a.elapsed_time(b) for a, b in scan_ev]
+    scan_ms = [a.elapsed_time(b) for a, b in serial_ev]
+    scan_ms_overlapped = [a.elapsed_time(b) for a, b in scan_ev]
     t = torch.tensor([ms], dtype=torch.float64, device=device)
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -506,12 +540,13 @@ def run_gift(args, w):
     host = torch.empty((args.steps * B, w.n_views, w.dim), dtype=torch.float32, pin_memory=True)
     for i in range(args.steps):
         host[i * B:(i + 1) * B].copy_(batches[order[args.warmup + i]])
-    query_many(bundle, host[:L * B], top_k=w.top_k, lanes=L)  # warm
+    query_many(bundle, host[:L * B], top_k=w.top_k, lanes=L,
+               reserve_sms=eng.reserve_sms)  # warm
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    query_many(bundle, host, top_k=w.top_k, lanes=L)
+    query_many(bundle, host, top_k=w.top_k, lanes=L, reserve_sms=eng.reserve_sms)
     e2e_s = time.perf_counter() - t0
     t = torch.tensor([e2e_s], dtype=torch.float64, device=device)
     if ws > 1:
@@ -543,6 +578,9 @@ def run_gift(args, w):
     roofline.update({"kernel": "fif_scan_tc_kernel", "peak_source": peak_kind,
                      "traffic": load_traffic(w.name), "alg_bytes_per_launch": nbytes,
                      "alg_flops_per_launch": flops, "scan_ms_avg": scan_avg_ms,
+                     "scan_ms_measured": ("serial pass over the timed batches" if L > 1
+                                          else "timed region"),
+                     "scan_ms_avg_in_flight": sum(scan_ms_overlapped) / len(scan_ms_overlapped),
                      "scan_share_of_step": scan_avg_ms * args.steps / ms,
                      "achieved_gbs": achieved, "hbm_frac": achieved / peak,
                      "achieved_tflops": achieved_tf, "tensor_frac": achieved_tf / tpeak,
@@ -572,7 +610,8 @@ def run_gift(args, w):
                            "dim": w.dim, "K": w.K, "ma": w.ma, "similarity": "gaussian",
                            "sigma": w.sigma, "k1": w.k1, "k2": w.k2, "top_k": w.top_k,
                            "batch": B, "parallelism": f"replicas{ws}",
-                           "lanes": L, "storage": w.storage, "n_queries": w.n_queries,
+                           "lanes": L, "scan_reserved_sms": eng.reserve_sms,
+                           "storage": w.storage, "n_queries": w.n_queries,
                            "l2": "inputs larger than L2 (database >= 10.5 GB)",
                            "features": "planes only (streamed build)" if eng.fa.feat is None
                            else "storage copy + planes",
@@ -597,8 +636,12 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(synth.WORKLOADS) + ["c5"])
     ap.add_argument("--c5-shapes", type=int, default=0, help="override config-5 N (smoke runs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--lanes", type=int, default=4,
-                    help="batches in flight on separate streams (1 = serial)")
+    ap.add_argument("--reserve-sms", type=int, default=None,
+                    help="SMs the scan leaves to other lanes (default per config, "
+                         "DEFAULT_LANES)")
+    ap.add_argument("--lanes", type=int, default=None,
+                    help="batches in flight on separate streams (1 = serial; default "
+                         "per config, DEFAULT_LANES)")
     ap.add_argument("--shard", action="store_true",
                     help="shard the database by shape over the ranks (configs 3/4)")
     args = ap.parse_args()

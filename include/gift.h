@@ -51,6 +51,9 @@ extern "C" {
  * Replaces matching.FirstInvertedFile (matching.py:64-103).  Built by the
  * gift_fif_* build calls below; all pointers are device pointers. */
 #define GIFT_FIF_TILED_SEGMENTS 1
+/* flags bits 8-15: SMs the F-IF scan leaves to the kernels of other query
+ * batches in flight on other streams (0: one persistent scan CTA per SM) */
+#define GIFT_FIF_RESERVE_SMS(n) (((n) & 255) << 8)
 
 typedef struct gift_fif_view {
   int32_t K;                 /* codebook size                                 */
@@ -58,7 +61,8 @@ typedef struct gift_fif_view {
   int32_t dtype;             /* storage dtype of feat: GIFT_F32 / GIFT_F16    */
   int32_t flags;             /* GIFT_FIF_TILED_SEGMENTS: no segment is longer   */
                              /* than a scan tile (every compact entry is       */
-                             /* written once; no zero-fill needed)             */
+                             /* written once; no zero-fill needed);            */
+                             /* GIFT_FIF_RESERVE_SMS(n)                        */
   int64_t n_postings;        /* P                                             */
   int64_t n_segments;        /* S: (cell, shape) runs                          */
   int64_t n_tiles;           /* T: scan tiles (whole segments, <= tile_n)     */

@@ -22,6 +22,11 @@ GIFT_F32, GIFT_F16, GIFT_F64 = 0, 1, 2
 SIM_COSINE, SIM_GAUSSIAN = 0, 1
 FIF_TILED_SEGMENTS = 1  # gift_fif_view.flags (include/gift.h)
 
+
+def fif_reserve_sms(n: int) -> int:
+    """GIFT_FIF_RESERVE_SMS(n): flags bits 8-15."""
+    return (int(n) & 255) << 8
+
 _c_i32 = ctypes.c_int32
 _c_i64 = ctypes.c_int64
 _c_sz = ctypes.c_size_t

@@ -934,6 +934,16 @@ bool tc_supported(const gift_fif_view* f) {
 // CTA pairs by default with the f32 lo plane (configs 2/3: half the L2 -> smem
 // traffic per SM; config 3 scan 16.3 -> 15.1 ms, config 2 unchanged), single
 // CTAs for fp16 storage (config 4: the pair is ~7% slower there)
+// persistent scan CTAs: one per SM minus the view's GIFT_FIF_RESERVE_SMS
+// (left to the kernels of other batches in flight); GIFT_SCAN_CTAS=n overrides
+static int scan_ctas(const gift_fif_view* f) {
+  const char* e = getenv("GIFT_SCAN_CTAS");
+  const int n = e != nullptr ? atoi(e) : 0;
+  if (n > 0) return min(n, sm_count());
+  const int reserve = (f->flags >> 8) & 255;
+  return max(2, sm_count() - reserve);
+}
+
 bool tc_pair_enabled(const gift_fif_view* f) {
   if (cts_enabled(f)) return false;  // the compressed-store scan runs on single CTAs
   const char* e = getenv("GIFT_TC_PAIR");
@@ -966,12 +976,12 @@ int launch_scan_tc(const gift_fif_view* f, const float* Q, int64_t nprobes_max, 
   if (a.cts != nullptr) {
     GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_scan_cts_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_CTS));
-    fif_scan_cts_kernel<<<sm_count(), CTS_THREADS, SMEM_CTS, st>>>(mB1, mB2, a);
+    fif_scan_cts_kernel<<<scan_ctas(f), CTS_THREADS, SMEM_CTS, st>>>(mB1, mB2, a);
   } else if (pair) {
     GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_scan_tc_kernel<true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TC));
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(sm_count() / 2 * 2));
+    cfg.gridDim = dim3(static_cast<unsigned>(max(2, scan_ctas(f) / 2 * 2)));
     cfg.blockDim = dim3(TC_THREADS);
     cfg.dynamicSmemBytes = SMEM_TC;
     cfg.stream = st;
@@ -987,8 +997,8 @@ int launch_scan_tc(const gift_fif_view* f, const float* Q, int64_t nprobes_max, 
   } else {
     GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_scan_tc_kernel<false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TC));
-    fif_scan_tc_kernel<false><<<sm_count(), TC_THREADS, SMEM_TC, st>>>(mA1, mA2, mB1, mB2, mB1h,
-                                                                       mB2h, a);
+    fif_scan_tc_kernel<false><<<scan_ctas(f), TC_THREADS, SMEM_TC, st>>>(mA1, mA2, mB1, mB2, mB1h,
+                                                                         mB2h, a);
   }
   GIFT_LAUNCH_CHECK();
   if (ev1) GIFT_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(ev1), st));

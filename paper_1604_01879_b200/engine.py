@@ -443,12 +443,14 @@ class ScoreRunner:
 
     def score(self, fif: DeviceFif, Q: torch.Tensor, ma: int, mode: int = nat.SIM_COSINE,
               sigma: float = 0.5, vq: torch.Tensor | None = None, out: torch.Tensor | None = None,
-              stream=None, scan_events=None, cand_k: int = 0, dense: bool = True):
+              stream=None, scan_events=None, cand_k: int = 0, dense: bool = True,
+              reserve_sms: int = 0):
         """Q: [B, V, d] f32 device -> f64 [B, n_local] (matching.py:136-161).
         With cand_k > 0 also returns the reduce's per-range best cand_k
         (scores [B, m], ordinals [B, m]) for `topk_candidates`; with
         dense=False (and cand_k > 0) the dense scores are not written and the
-        first returned value is None."""
+        first returned value is None.  reserve_sms: SMs the scan leaves to the
+        kernels of other batches in flight (GIFT_FIF_RESERVE_SMS)."""
         if Q.dim() != 3:
             raise ValueError("queries must be [B, V, d]")
         B, V, d = Q.shape
@@ -466,6 +468,9 @@ class ScoreRunner:
         if out is None and dense:
             out = torch.empty((B, fif.n_local), dtype=torch.float64, device=Q.device)
         view = fif.view
+        if reserve_sms:
+            view = type(view).from_buffer_copy(view)
+            view.flags = (view.flags & ~0xFF00) | nat.fif_reserve_sms(reserve_sms)
         lib = nat.lib()
         # upper bound of the compact (probe x segment) buffer: if it fits the
         # budget, size for it and skip the host round trip on the overflow flag

@@ -150,16 +150,21 @@ class QueryEngine:
         self.order = torch.from_numpy(np.asarray(order, dtype=np.int32)).to(nat.device())
         self.ord_of = {sid: i for i, sid in enumerate(bundle.shape_ids)}
         self.runner = eg.ScoreRunner()
+        # SMs the F-IF scan leaves to other batches' kernels (query_many sets
+        # it while several batches are in flight)
+        self.reserve_sms = 0
         self.mode = mt.sim_mode(cfg.similarity)
 
     def scores(self, Qa, Qb=None, vq=None, vqb=None, stream=None, scan_events=None, ma=None):
         ma = self.cfg.ma if ma is None else ma
         sa = self.runner.score(self.fa, Qa, ma, self.mode, self.cfg.sigma, vq=vq,
-                               stream=stream, scan_events=scan_events)
+                               stream=stream, scan_events=scan_events,
+                               reserve_sms=self.reserve_sms)
         if Qb is None and self.dup:
             return sa, sa
         sb = self.runner.score(self.fb, Qa if Qb is None else Qb, ma, self.mode,
-                               self.cfg.sigma, vq=vq if vqb is None else vqb, stream=stream)
+                               self.cfg.sigma, vq=vq if vqb is None else vqb, stream=stream,
+                               reserve_sms=self.reserve_sms)
         return sa, sb
 
     def rerank(self, sa, sb, stream=None):
@@ -199,7 +204,8 @@ class QueryEngine:
             k2 = min(self.cfg.k2, self.n)
             _, cs, ci = self.runner.score(self.fa, Qa, self.cfg.ma, self.mode, self.cfg.sigma,
                                           vq=vq, stream=stream, scan_events=scan_events,
-                                          cand_k=k2, dense=False)
+                                          cand_k=k2, dense=False,
+                                          reserve_sms=self.reserve_sms)
             nbr, _ = eg.topk_candidates(cs, ci, k2, positive_only=True, stream=stream)
             fa = eg.act_mean(self.raw_a, nbr, stream=stream)
             return self._sif_rank(fa, top_k, self_local, stream)
@@ -540,6 +546,7 @@ def query_batch(bundle: IndexBundle, views, top_k: int = 10, rerank: bool = True
 
 
 _LANES: dict = {}
+LANE_RESERVE_SMS = 20  # config 2, 4 lanes: 40.6k -> 42.7k q/s (tools/lane_trace.py)
 
 
 def lane_streams(n: int) -> list:
@@ -553,11 +560,15 @@ def lane_streams(n: int) -> list:
 
 
 def query_many(bundle: IndexBundle, views_host: torch.Tensor, top_k: int = 10,
-               rerank: bool = True, batch_size: int | None = None, lanes: int = 2):
+               rerank: bool = True, batch_size: int | None = None, lanes: int = 2,
+               reserve_sms: int | None = None):
     """Throughput API (new): queries from pinned host memory [Q, V, d] f32,
     processed in device batches on `lanes` compute streams, the host->device
     copy of the next batches overlapped with the compute on a copy stream.
-    Returns host (idx [Q, k] int32 global ordinals, val [Q, k] f64)."""
+    With lanes > 1 the scan leaves `reserve_sms` SMs (default
+    LANE_RESERVE_SMS) to the other batches' kernels, which cannot share an SM
+    with a scan CTA (shared memory / TMEM).  Returns host (idx [Q, k] int32
+    global ordinals, val [Q, k] f64)."""
     eng = bundle.engine
     bs = batch_size or bundle.config.batch_size
     Qn, V, d = views_host.shape
@@ -567,7 +578,8 @@ def query_many(bundle: IndexBundle, views_host: torch.Tensor, top_k: int = 10,
     L = max(1, int(lanes))
     # batch i computes on lane i % L (its own stream and scratch), so one
     # batch's quantize / reduce / re-rank kernels overlap the other's scan
-    comp = [main] if L == 1 else lane_streams(L)
+    # side streams only: the legacy default stream would serialize with the copies
+    comp = lane_streams(L)
     copy = lane_streams(L + 1)[L]
     NB = max(2, L)  # input buffers: batch i lands in buffer i % NB
     bufs = [torch.empty((bs, V, d), dtype=torch.float32, device=dev) for _ in range(NB)]
@@ -585,6 +597,10 @@ def query_many(bundle: IndexBundle, views_host: torch.Tensor, top_k: int = 10,
             bufs[s][: b1 - b0].copy_(views_host[b0:b1], non_blocking=True)
             ready[s].record(copy)
 
+    prev_reserve = eng.reserve_sms
+    if reserve_sms is None:
+        reserve_sms = LANE_RESERVE_SMS if L > 1 else 0
+    eng.reserve_sms = reserve_sms
     for c in comp:
         c.wait_stream(main)
     for s in range(NB):
@@ -605,6 +621,7 @@ def query_many(bundle: IndexBundle, views_host: torch.Tensor, top_k: int = 10,
             issue(i + NB)
     for c in comp:
         main.wait_stream(c)
+    eng.reserve_sms = prev_reserve
     main.synchronize()
     return out_idx.numpy(), out_val.numpy()
 

@@ -1,2 +1,4 @@
 timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
-timeout 600 python tools/ingest_bench.py --shapes 2000 > gpurun_out/ingest.json 2> gpurun_out/ingest.err; echo ing=$?
+timeout 600 python bench.py > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
+timeout 1500 python bench.py --config c3 --steps 8 --no-cpu-baseline > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
+timeout 1500 python bench.py --config c4 --steps 5 --no-cpu-baseline > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err
