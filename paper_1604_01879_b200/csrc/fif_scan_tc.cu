@@ -397,6 +397,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int sp_a = et <= nseg ? p.seg_pstart[I.seg0 + et] : 0;
       const int sp_b = et + TC_M <= nseg ? p.seg_pstart[I.seg0 + et + TC_M] : 0;
       const float qn_r = et < I.nb ? p.qn2s[I.pb0 + et] : 0.f;
+      // the row's |p|^2 and the cell's output coordinates, loaded now too
+      // (posting-indexed |p|^2 misses L2: its latency would sit in the tail)
+      const float pn = (gauss && I.p0 + row < I.p1) ? p.pnorm2[I.p0 + row] : 0.f;
+      const int64_t seg_base = p.seg_off[I.c];
+      const int64_t S_c = p.seg_off[I.c + 1] - seg_base;
+      const int64_t obase = p.outbase[I.c];
       float acc[TC_NMAX];
 #pragma unroll
       for (int n = 0; n < TC_NMAX; ++n) acc[n] = 0.f;
@@ -477,10 +483,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       if (et <= nseg) s_sp[et] = sp_a;
       if (et + TC_M <= nseg) s_sp[et + TC_M] = sp_b;
       s_qn2[et] = qn_r;
-      const float pn = (I.p0 + row < I.p1) ? p.pnorm2[I.p0 + row] : 0.f;
-      const int64_t S_c = p.seg_off[I.c + 1] - p.seg_off[I.c];
-      const int64_t seg_base = p.seg_off[I.c];
-      const int64_t obase = p.outbase[I.c];
       // thread -> (column mc = et % 32, segments et / 32, +4, ...): no division
       const int mc = et & (EPI_COLS - 1), sg0 = et >> 5;
       // 32-column slices: stage -> per-segment max over rows -> store
