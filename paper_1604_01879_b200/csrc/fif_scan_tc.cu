@@ -43,14 +43,12 @@ constexpr int RING_BYTES = 3 * STAGE_LO;  // 192 KB
 constexpr int EPI_COLS = 32;  // epilogue stages 32 probe columns at a time
 constexpr int EPI_STRIDE = EPI_COLS + 1;
 constexpr int EPI_BYTES = TC_M * EPI_STRIDE * 4;
-constexpr int TC_THREADS = 224;  // producer, MMA, scheduler, 4 epilogue warps
 constexpr int ITEM_RING = 8;     // decoded work items in flight (scheduler -> roles)
 // TMEM: D1 (hi x hi) double-buffered per k-chunk, drained every chunk_kb
 // k-blocks (short tensor-core accumulation chains: the fp32 accumulate is
 // not exact); D2 (the 2^-11-scaled correction terms) double-buffered per
 // item, drained once per item (its accumulation error is 2^-11 smaller)
 constexpr uint32_t TMEM_COLS = 512;  // D1[2][128] | D2[2][128]
-constexpr int SMEM_TC = RING_BYTES + EPI_BYTES + 256;
 constexpr float SPLIT_INV = 1.0f / 2048.0f;
 
 struct ItemInfo {
@@ -134,8 +132,23 @@ struct Ring {
 };
 constexpr int MAX_RING_STAGES = 6;
 
+// Epilogue column groups: the single-CTA kernel (fp16 storage, config 4; its
+// epilogue paces the tensor cores) runs two groups of 4 epilogue warps, each
+// draining and reducing half of the probe columns; the CTA-pair kernel keeps
+// one group (and the shared memory other batches' kernels can share an SM
+// with).
 template <bool PAIR>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+struct Epi {
+  static constexpr int G = PAIR ? 1 : 2;
+  static constexpr int THREADS = 96 + 128 * G;  // producer, MMA, scheduler, 4 G epilogue
+  static constexpr int COLS = PAIR ? EPI_COLS : EPI_COLS / 2;  // tail slice width
+  static constexpr int STRIDE = COLS + 1;
+  static constexpr int DS = TC_M * STRIDE;  // floats of one group's staging tile
+  static constexpr int SMEM = RING_BYTES + G * DS * 4 + 256;
+};
+
+template <bool PAIR>
+__global__ void __launch_bounds__(Epi<PAIR>::THREADS, 1)
     fif_scan_tc_kernel(const __grid_constant__ CUtensorMap tmA1,
                        const __grid_constant__ CUtensorMap tmA2,
                        const __grid_constant__ CUtensorMap tmB1,
@@ -143,12 +156,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                        const __grid_constant__ CUtensorMap tmB1h,
                        const __grid_constant__ CUtensorMap tmB2h, const TcArgs p) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ int32_t s_sp[TC_M + 2];
+  constexpr int G = Epi<PAIR>::G;
+  __shared__ int32_t s_sp[G * (TC_M + 2)];
   __shared__ float s_qn2[TC_NMAX];
   __shared__ ItemInfo s_item[ITEM_RING];
   __shared__ __align__(8) uint64_t ifull[ITEM_RING], iempty[ITEM_RING];
   float* Ds = reinterpret_cast<float*>(smem + RING_BYTES);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + RING_BYTES + EPI_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + RING_BYTES + G * Epi<PAIR>::DS * 4);
   uint64_t* full = bars;
   uint64_t* empty = bars + MAX_RING_STAGES;
   uint64_t* tfull = bars + 2 * MAX_RING_STAGES;  // D1 chunk buffers
@@ -185,11 +199,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int r = 0; r < ITEM_RING; ++r) {
       tc::mbar_init(&ifull[r], 1);
-      tc::mbar_init(&iempty[r], (PAIR && !leader) ? 2 : 3);  // producer, [MMA,] epilogue
+      tc::mbar_init(&iempty[r], (PAIR && !leader) ? 2 : 2 + G);  // producer, [MMA,] epilogues
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&tfull[b], 1);
-      tc::mbar_init(&tempty[b], PAIR ? 2 * TC_M : TC_M);  // pair: both CTAs' epilogues
+      tc::mbar_init(&tempty[b], PAIR ? 2 * TC_M : G * TC_M);  // pair: both CTAs' epilogues
       tc::mbar_init(&dfull[b], 1);
       tc::mbar_init(&dempty[b], PAIR ? 2 * TC_M : TC_M);
     }
@@ -373,7 +387,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
   } else {
     // ------------------------------------------------------ epilogue
-    const int et = threadIdx.x - 96;      // 0..127
+    // G groups of 4 warps; group eg drains and reduces probe columns
+    // [eg n / G, (eg + 1) n / G) of every item
+    const int et = threadIdx.x - 96;      // 0 .. 128 G - 1
+    const int eg = et >> 7;               // column group
+    const int e = et & (TC_M - 1);        // thread within the group
+    const int bar_tail = 1 + 2 * eg, bar_item = 2 + 2 * eg;
+    constexpr int EC = Epi<PAIR>::COLS, ES = Epi<PAIR>::STRIDE;
+    float* Dg = Ds + eg * Epi<PAIR>::DS;
+    int32_t* sp_s = s_sp + eg * (TC_M + 2);
     const int lb = 32 * (warp & 3);       // TMEM lane quarter of this warp
     const int row = lb + lane;            // posting row within the tile
     const bool gauss = p.mode == GIFT_SIM_GAUSSIAN;
@@ -387,34 +409,37 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const uint32_t slot = item_ctr % ITEM_RING, sph = (item_ctr / ITEM_RING) & 1;
       tc::mbar_wait(&ifull[slot], sph);
       const ItemInfo I = s_item[slot];
-      named_bar(2, TC_M);  // every epilogue thread has its copy
-      if (et == 0) tc::mbar_arrive(&iempty[slot]);
+      named_bar(bar_item, TC_M);  // every thread of the group has its copy
+      if (e == 0) tc::mbar_arrive(&iempty[slot]);
       const int nseg = I.seg1 - I.seg0;
-      const int ng = I.n / 16;  // 16-column groups in use
+      const int hn = I.n / G;     // this group's columns: [c0, c0 + hn)
+      const int c0 = eg * hn;
+      const int ng = hn / 16;     // its 16-column groups
       // tail inputs, loaded now and staged to shared memory only at the tail
       // (their latency overlaps the drains): segment starts (nseg + 1 <= 129)
       // and the probe-sorted |q|^2
-      const int sp_a = et <= nseg ? p.seg_pstart[I.seg0 + et] : 0;
-      const int sp_b = et + TC_M <= nseg ? p.seg_pstart[I.seg0 + et + TC_M] : 0;
-      const float qn_r = et < I.nb ? p.qn2s[I.pb0 + et] : 0.f;
+      const int sp_a = e <= nseg ? p.seg_pstart[I.seg0 + e] : 0;
+      const int sp_b = e + TC_M <= nseg ? p.seg_pstart[I.seg0 + e + TC_M] : 0;
+      const float qn_r = (e < hn && c0 + e < I.nb) ? p.qn2s[I.pb0 + c0 + e] : 0.f;
       // the row's |p|^2 and the cell's output coordinates, loaded now too
       // (posting-indexed |p|^2 misses L2: its latency would sit in the tail)
       const float pn = (gauss && I.p0 + row < I.p1) ? p.pnorm2[I.p0 + row] : 0.f;
       const int64_t seg_base = p.seg_off[I.c];
       const int64_t S_c = p.seg_off[I.c + 1] - seg_base;
       const int64_t obase = p.outbase[I.c];
-      float acc[TC_NMAX];
+      constexpr int NA = TC_NMAX / G;
+      float acc[NA];
 #pragma unroll
-      for (int n = 0; n < TC_NMAX; ++n) acc[n] = 0.f;
+      for (int n = 0; n < NA; ++n) acc[n] = 0.f;
       const uint32_t lane_off = static_cast<uint32_t>(lb) << 16;
       for (int kb0 = 0; kb0 < nkb; kb0 += chunk_kb) {
         const uint32_t buf = chunk_ctr & 1, aph = (chunk_ctr >> 1) & 1;
         tc::mbar_wait(&tfull[buf], aph);
         tc::tc_fence_after();
         if (!cb) {
-          const uint32_t base = tmem_base + lane_off + buf * TC_NMAX;
+          const uint32_t base = tmem_base + lane_off + buf * TC_NMAX + c0;
 #pragma unroll
-          for (int j = 0; j < TC_NMAX / 16; j += 2) {
+          for (int j = 0; j < NA / 16; j += 2) {
             if (j < ng && !(p.dbg & 2)) {
               float v1[16], v2[16];
               tc::tmem_ld_x16(base + j * 16, v1);
@@ -428,9 +453,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
           }
         } else {  // [D1 | D2] of this chunk: acc += D1 + 2^-11 D2
-          const uint32_t base = tmem_base + lane_off + buf * 2 * TC_NMAX;
+          const uint32_t base = tmem_base + lane_off + buf * 2 * TC_NMAX + c0;
 #pragma unroll
-          for (int j = 0; j < TC_NMAX / 16; ++j) {
+          for (int j = 0; j < NA / 16; ++j) {
             if (j < ng && !(p.dbg & 2)) {
               float v1[16], v2[16];
               tc::tmem_ld_x16(base + j * 16, v1);
@@ -454,9 +479,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const uint32_t ib = item_ctr & 1, iph = (item_ctr >> 1) & 1;
         tc::mbar_wait(&dfull[ib], iph);
         tc::tc_fence_after();
-        const uint32_t base = tmem_base + lane_off + 256 + ib * TC_NMAX;
+        const uint32_t base = tmem_base + lane_off + 256 + ib * TC_NMAX + c0;
 #pragma unroll
-        for (int j = 0; j < TC_NMAX / 16; j += 2) {
+        for (int j = 0; j < NA / 16; j += 2) {
           if (j < ng) {
             float v1[16], v2[16];
             tc::tmem_ld_x16(base + j * 16, v1);
@@ -477,32 +502,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         ++item_ctr;
       }
       if (!I.live || (p.dbg & 1)) {  // pair: duplicate tile, nothing to write
-        named_bar(1, TC_M);
+        named_bar(bar_tail, TC_M);
         continue;
       }
-      if (et <= nseg) s_sp[et] = sp_a;
-      if (et + TC_M <= nseg) s_sp[et + TC_M] = sp_b;
-      s_qn2[et] = qn_r;
-      // thread -> (column mc = et % 32, segments et / 32, +4, ...): no division
-      const int mc = et & (EPI_COLS - 1), sg0 = et >> 5;
-      // 32-column slices: stage -> per-segment max over rows -> store
+      if (e <= nseg) sp_s[e] = sp_a;
+      if (e + TC_M <= nseg) sp_s[e + TC_M] = sp_b;
+      if (e < hn) s_qn2[c0 + e] = qn_r;
+      // thread -> (column mc = e % EC, segments e / EC, + TC_M / EC, ...)
+      const int mc = e & (EC - 1), sg0 = e / EC;
+      // EC-column slices: stage -> per-segment max over rows -> store
 #pragma unroll
-      for (int sl0 = 0; sl0 < TC_NMAX; sl0 += EPI_COLS) {
-        if (sl0 < I.nb) {
+      for (int sl0 = 0; sl0 < NA; sl0 += EC) {
+        if (sl0 < hn && c0 + sl0 < I.nb) {
 #pragma unroll
-          for (int c = 0; c < EPI_COLS; ++c) {
+          for (int c = 0; c < EC; ++c) {
             float v = acc[sl0 + c];
             if (gauss) v = 2.0f * v - pn;  // max_p(2q.p - |p|^2) <-> min_p |q-p|^2
-            Ds[row * EPI_STRIDE + c] = v;
+            Dg[row * ES + c] = v;
           }
-          named_bar(1, TC_M);
-          const int ncol = min(EPI_COLS, I.nb - sl0);
-          const int m = sl0 + mc;
-          for (int sl = sg0; mc < ncol && sl < nseg; sl += TC_M / EPI_COLS) {
-            const int sp0 = s_sp[sl], sp1 = s_sp[sl + 1];
+          named_bar(bar_tail, TC_M);
+          const int ncol = min(EC, I.nb - (c0 + sl0));
+          const int m = c0 + sl0 + mc;
+          for (int sl = sg0; mc < ncol && sl < nseg; sl += TC_M / EC) {
+            const int sp0 = sp_s[sl], sp1 = sp_s[sl + 1];
             const int r0 = max(sp0, I.p0) - I.p0, r1 = min(sp1, I.p1) - I.p0;
             float mx = -INFINITY;
-            for (int r = r0; r < r1; ++r) mx = fmaxf(mx, Ds[r * EPI_STRIDE + mc]);
+            for (int r = r0; r < r1; ++r) mx = fmaxf(mx, Dg[r * ES + mc]);
             float sim;
             if (gauss)
               sim = expf(-fmaxf(s_qn2[m] - mx, 0.f) * p.inv_sigma2);
@@ -510,12 +535,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               sim = fminf(fmaxf(mx, 0.f), 1.f);
             const int64_t o = obase + static_cast<int64_t>(I.mt * TC_NMAX + m) * S_c +
                               (I.seg0 + sl - seg_base);
-            if (sp0 < I.p0 || sp1 > I.p1)
+            if (p.dbg & 64) {  // timing experiment: no compact stores
+              if (sim == -1.f) p.out[o] = sim;
+            } else if (sp0 < I.p0 || sp1 > I.p1) {
               atomicMax(reinterpret_cast<int*>(p.out + o), __float_as_int(sim));
-            else
+            } else {
               p.out[o] = sim;
+            }
           }
-          named_bar(1, TC_M);
+          named_bar(bar_tail, TC_M);
         }
       }
     }
@@ -981,11 +1009,12 @@ int launch_scan_tc(const gift_fif_view* f, const float* Q, int64_t nprobes_max, 
     fif_scan_cts_kernel<<<scan_ctas(f), CTS_THREADS, SMEM_CTS, st>>>(mB1, mB2, a);
   } else if (pair) {
     GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_scan_tc_kernel<true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TC));
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       Epi<true>::SMEM));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(max(2, scan_ctas(f) / 2 * 2)));
-    cfg.blockDim = dim3(TC_THREADS);
-    cfg.dynamicSmemBytes = SMEM_TC;
+    cfg.blockDim = dim3(Epi<true>::THREADS);
+    cfg.dynamicSmemBytes = Epi<true>::SMEM;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -998,9 +1027,10 @@ int launch_scan_tc(const gift_fif_view* f, const float* Q, int64_t nprobes_max, 
                                      mB2h, a));
   } else {
     GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_scan_tc_kernel<false>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TC));
-    fif_scan_tc_kernel<false><<<scan_ctas(f), TC_THREADS, SMEM_TC, st>>>(mA1, mA2, mB1, mB2, mB1h,
-                                                                         mB2h, a);
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       Epi<false>::SMEM));
+    fif_scan_tc_kernel<false><<<scan_ctas(f), Epi<false>::THREADS, Epi<false>::SMEM, st>>>(
+        mA1, mA2, mB1, mB2, mB1h, mB2h, a);
   }
   GIFT_LAUNCH_CHECK();
   if (ev1) GIFT_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(ev1), st));
