@@ -134,21 +134,20 @@ constexpr int MAX_RING_STAGES = 6;
 
 // Epilogue column groups: the single-CTA kernel (fp16 storage, config 4; its
 // epilogue paces the tensor cores) runs two groups of 4 epilogue warps, each
-// draining and reducing half of the probe columns; the CTA-pair kernel keeps
-// one group (and the shared memory other batches' kernels can share an SM
-// with).
-template <bool PAIR>
+// draining and reducing half of the probe columns; the f32-plane CTA-pair
+// kernel (HBM-bound) keeps one group and the shared memory other batches'
+// kernels can share an SM with.
+template <int G>
 struct Epi {
-  static constexpr int G = PAIR ? 1 : 2;
   static constexpr int THREADS = 96 + 128 * G;  // producer, MMA, scheduler, 4 G epilogue
-  static constexpr int COLS = PAIR ? EPI_COLS : EPI_COLS / 2;  // tail slice width
+  static constexpr int COLS = G == 1 ? EPI_COLS : EPI_COLS / 2;  // tail slice width
   static constexpr int STRIDE = COLS + 1;
   static constexpr int DS = TC_M * STRIDE;  // floats of one group's staging tile
   static constexpr int SMEM = RING_BYTES + G * DS * 4 + 256;
 };
 
-template <bool PAIR>
-__global__ void __launch_bounds__(Epi<PAIR>::THREADS, 1)
+template <bool PAIR, int G>
+__global__ void __launch_bounds__(Epi<G>::THREADS, 1)
     fif_scan_tc_kernel(const __grid_constant__ CUtensorMap tmA1,
                        const __grid_constant__ CUtensorMap tmA2,
                        const __grid_constant__ CUtensorMap tmB1,
@@ -156,13 +155,12 @@ __global__ void __launch_bounds__(Epi<PAIR>::THREADS, 1)
                        const __grid_constant__ CUtensorMap tmB1h,
                        const __grid_constant__ CUtensorMap tmB2h, const TcArgs p) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  constexpr int G = Epi<PAIR>::G;
   __shared__ int32_t s_sp[G * (TC_M + 2)];
   __shared__ float s_qn2[TC_NMAX];
   __shared__ ItemInfo s_item[ITEM_RING];
   __shared__ __align__(8) uint64_t ifull[ITEM_RING], iempty[ITEM_RING];
   float* Ds = reinterpret_cast<float*>(smem + RING_BYTES);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + RING_BYTES + G * Epi<PAIR>::DS * 4);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + RING_BYTES + G * Epi<G>::DS * 4);
   uint64_t* full = bars;
   uint64_t* empty = bars + MAX_RING_STAGES;
   uint64_t* tfull = bars + 2 * MAX_RING_STAGES;  // D1 chunk buffers
@@ -199,13 +197,13 @@ __global__ void __launch_bounds__(Epi<PAIR>::THREADS, 1)
     }
     for (int r = 0; r < ITEM_RING; ++r) {
       tc::mbar_init(&ifull[r], 1);
-      tc::mbar_init(&iempty[r], (PAIR && !leader) ? 2 : 2 + G);  // producer, [MMA,] epilogues
+      tc::mbar_init(&iempty[r], (PAIR && !leader) ? 1 + G : 2 + G);  // producer, [MMA,] epilogues
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&tfull[b], 1);
-      tc::mbar_init(&tempty[b], PAIR ? 2 * TC_M : G * TC_M);  // pair: both CTAs' epilogues
+      tc::mbar_init(&tempty[b], (PAIR ? 2 : 1) * G * TC_M);  // pair: both CTAs' epilogues
       tc::mbar_init(&dfull[b], 1);
-      tc::mbar_init(&dempty[b], PAIR ? 2 * TC_M : TC_M);
+      tc::mbar_init(&dempty[b], (PAIR ? 2 : 1) * G * TC_M);
     }
     tc::fence_barrier_init();
     tc::tma_prefetch(&tmA1);
@@ -393,8 +391,8 @@ __global__ void __launch_bounds__(Epi<PAIR>::THREADS, 1)
     const int eg = et >> 7;               // column group
     const int e = et & (TC_M - 1);        // thread within the group
     const int bar_tail = 1 + 2 * eg, bar_item = 2 + 2 * eg;
-    constexpr int EC = Epi<PAIR>::COLS, ES = Epi<PAIR>::STRIDE;
-    float* Dg = Ds + eg * Epi<PAIR>::DS;
+    constexpr int EC = Epi<G>::COLS, ES = Epi<G>::STRIDE;
+    float* Dg = Ds + eg * Epi<G>::DS;
     int32_t* sp_s = s_sp + eg * (TC_M + 2);
     const int lb = 32 * (warp & 3);       // TMEM lane quarter of this warp
     const int row = lb + lane;            // posting row within the tile
@@ -981,6 +979,29 @@ bool tc_pair_enabled(const gift_fif_view* f) {
   return f->feat_lo != nullptr && sm_count() >= 2;
 }
 
+template <int G>
+static cudaError_t launch_pair(int ctas, cudaStream_t st, const CUtensorMap& mA1,
+                               const CUtensorMap& mA2, const CUtensorMap& mB1,
+                               const CUtensorMap& mB2, const CUtensorMap& mB1h,
+                               const CUtensorMap& mB2h, const TcArgs& a) {
+  cudaError_t e = cudaFuncSetAttribute(fif_scan_tc_kernel<true, G>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, Epi<G>::SMEM);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(max(2, ctas / 2 * 2)));
+  cfg.blockDim = dim3(Epi<G>::THREADS);
+  cfg.dynamicSmemBytes = Epi<G>::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fif_scan_tc_kernel<true, G>, mA1, mA2, mB1, mB2, mB1h, mB2h, a);
+}
+
 int launch_scan_tc(const gift_fif_view* f, const float* Q, int64_t nprobes_max, TcArgs a,
                    __half* g1, __half* g2, cudaStream_t st, void* ev0, void* ev1) {
   const int d = f->d;
@@ -1007,29 +1028,15 @@ int launch_scan_tc(const gift_fif_view* f, const float* Q, int64_t nprobes_max, 
     GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_scan_cts_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_CTS));
     fif_scan_cts_kernel<<<scan_ctas(f), CTS_THREADS, SMEM_CTS, st>>>(mB1, mB2, a);
-  } else if (pair) {
-    GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_scan_tc_kernel<true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       Epi<true>::SMEM));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(max(2, scan_ctas(f) / 2 * 2)));
-    cfg.blockDim = dim3(Epi<true>::THREADS);
-    cfg.dynamicSmemBytes = Epi<true>::SMEM;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    GIFT_CUDA_TRY(cudaLaunchKernelEx(&cfg, fif_scan_tc_kernel<true>, mA1, mA2, mB1, mB2, mB1h,
-                                     mB2h, a));
+  } else if (pair && a.has_lo) {
+    GIFT_CUDA_TRY(launch_pair<1>(scan_ctas(f), st, mA1, mA2, mB1, mB2, mB1h, mB2h, a));
+  } else if (pair) {  // fp16 storage: tensor-bound, two epilogue groups
+    GIFT_CUDA_TRY(launch_pair<2>(scan_ctas(f), st, mA1, mA2, mB1, mB2, mB1h, mB2h, a));
   } else {
-    GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_scan_tc_kernel<false>,
+    GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_scan_tc_kernel<false, 2>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       Epi<false>::SMEM));
-    fif_scan_tc_kernel<false><<<scan_ctas(f), Epi<false>::THREADS, Epi<false>::SMEM, st>>>(
+                                       Epi<2>::SMEM));
+    fif_scan_tc_kernel<false, 2><<<scan_ctas(f), Epi<2>::THREADS, Epi<2>::SMEM, st>>>(
         mA1, mA2, mB1, mB2, mB1h, mB2h, a);
   }
   GIFT_LAUNCH_CHECK();
