@@ -1256,6 +1256,8 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
     ta.chunk_kb = ck ? atoi(ck) : 4;
     const char* mo = getenv("GIFT_TC_ORDER");
     ta.mt_major = (mo != nullptr && mo[0] == 'm') ? 1 : 0;
+    const char* sched = getenv("GIFT_TC_SCHED");
+    ta.dyn = (sched != nullptr && sched[0] == 's') ? 0 : 1;
     const char* dbg = getenv("GIFT_TC_DBG");
     ta.dbg = dbg ? atoi(dbg) : 0;
     const bool cts_ok = cts_enabled(f);

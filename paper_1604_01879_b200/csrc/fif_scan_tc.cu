@@ -159,6 +159,9 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
   __shared__ float s_qn2[TC_NMAX];
   __shared__ ItemInfo s_item[ITEM_RING];
   __shared__ __align__(8) uint64_t ifull[ITEM_RING], iempty[ITEM_RING];
+  // pair: item indices the leader's scheduler fetched, pushed into the peer
+  __shared__ __align__(8) int64_t s_next[ITEM_RING];
+  __shared__ __align__(8) uint64_t xfull[ITEM_RING], xempty[ITEM_RING];
   float* Ds = reinterpret_cast<float*>(smem + RING_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + RING_BYTES + G * Epi<G>::DS * 4);
   uint64_t* full = bars;
@@ -196,6 +199,8 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
       tc::mbar_init(&empty[s], 1);
     }
     for (int r = 0; r < ITEM_RING; ++r) {
+      tc::mbar_init(&xfull[r], 1);
+      tc::mbar_init(&xempty[r], 1);
       tc::mbar_init(&ifull[r], 1);
       tc::mbar_init(&iempty[r], (PAIR && !leader) ? 1 + G : 2 + G);  // producer, [MMA,] epilogues
     }
@@ -230,12 +235,13 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
     {
       int stage = 0;
       uint32_t phase = 0, it = 0;
-      for (int64_t item = first; item < n_items; item += stride, ++it) {
+      for (;; ++it) {  // items from the scheduler until its stop entry
         const uint32_t slot = it % ITEM_RING, iph = (it / ITEM_RING) & 1;
         tc::mbar_wait(&ifull[slot], iph);
         const ItemInfo I = s_item[slot];
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&iempty[slot]);
+        if (I.c < 0) break;
         const int brows = PAIR ? I.n / 2 : I.n;            // probe rows per plane half
         const uint32_t a_bytes = has_lo ? 2 * A_TILE : A_TILE;
         // this CTA's B bytes: both planes (single), one whole plane (pair, cb),
@@ -297,12 +303,13 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       uint32_t chunk_ctr = 0, item_ctr = 0;
-      for (int64_t item = first; item < n_items; item += stride) {
+      for (;;) {
         const uint32_t slot = item_ctr % ITEM_RING, sph = (item_ctr / ITEM_RING) & 1;
         tc::mbar_wait(&ifull[slot], sph);
         const ItemInfo I = s_item[slot];
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&iempty[slot]);
+        if (I.c < 0) break;
         const uint32_t idesc = tc::idesc_f16_f32(PAIR ? 2 * TC_M : TC_M, I.n);
         const uint32_t idesc2 = tc::idesc_f16_f32(PAIR ? 2 * TC_M : TC_M, 2 * I.n);  // [b1 | b2]
         const uint32_t ib = item_ctr & 1, iph = (item_ctr >> 1) & 1;
@@ -372,15 +379,45 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
     // decodes the work items ahead of the other roles (the cell search and
     // tile lookups are dependent global loads that would otherwise stall the
     // MMA issuer between items)
+    // Items are taken from a global counter (meta[M_WORK], zeroed by the
+    // plan kernel) as CTAs become free, so the probe tiles of one posting
+    // tile (consecutive items) run at the same time on neighbouring SMs and
+    // the posting tile's re-reads hit L2 (a static stride lets the CTAs drift
+    // apart); GIFT_TC_SCHED=static restores the stride.  Pair: the leader
+    // fetches and pushes each index into the peer's s_next ring.
     if (lane == 0) {
       int hint = 0;
-      uint32_t it = 0;
-      for (int64_t item = first; item < n_items; item += stride, ++it) {
+      unsigned long long* work =
+          reinterpret_cast<unsigned long long*>(const_cast<int64_t*>(p.meta) + M_WORK);
+      const uint32_t peer_next = PAIR ? tc::mapa(&s_next[0], 1) : 0u;
+      const uint32_t peer_full = PAIR ? tc::mapa(&xfull[0], 1) : 0u;
+      const uint32_t lead_empty = PAIR ? tc::mapa(&xempty[0], 0) : 0u;
+      for (uint32_t it = 0;; ++it) {
         const uint32_t slot = it % ITEM_RING, iph = (it / ITEM_RING) & 1;
-        const ItemInfo I = decode_item<PAIR>(p, item, hint, rank);
+        int64_t item;
+        if (!PAIR || leader) {
+          item = p.dyn ? static_cast<int64_t>(atomicAdd(work, 1ull))
+                       : first + static_cast<int64_t>(it) * stride;
+          if (PAIR) {
+            tc::mbar_wait(&xempty[slot], iph ^ 1);  // the peer took this slot's last index
+            tc::st_cluster_u64(peer_next + slot * 8, item);
+            tc::mbar_arrive_cluster(peer_full + slot * 8);
+          }
+        } else {
+          tc::mbar_wait_cluster(&xfull[slot], iph);
+          item = s_next[slot];
+          tc::mbar_arrive_cluster(lead_empty + slot * 8);
+        }
+        ItemInfo I;
+        if (item < n_items) {
+          I = decode_item<PAIR>(p, item, hint, rank);
+        } else {
+          I.c = -1;  // stop entry for every role
+        }
         tc::mbar_wait(&iempty[slot], iph ^ 1);
         s_item[slot] = I;
         tc::mbar_arrive(&ifull[slot]);
+        if (item >= n_items) break;
       }
     }
   } else {
@@ -403,12 +440,13 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
     const uint32_t rel_t1 = PAIR ? tc::mapa(&tempty[1], 0) : 0u;
     const uint32_t rel_d0 = PAIR ? tc::mapa(&dempty[0], 0) : 0u;
     const uint32_t rel_d1 = PAIR ? tc::mapa(&dempty[1], 0) : 0u;
-    for (int64_t item = first; item < n_items; item += stride) {
+    for (;;) {
       const uint32_t slot = item_ctr % ITEM_RING, sph = (item_ctr / ITEM_RING) & 1;
       tc::mbar_wait(&ifull[slot], sph);
       const ItemInfo I = s_item[slot];
       named_bar(bar_item, TC_M);  // every thread of the group has its copy
       if (e == 0) tc::mbar_arrive(&iempty[slot]);
+      if (I.c < 0) break;
       const int nseg = I.seg1 - I.seg0;
       const int hn = I.n / G;     // this group's columns: [c0, c0 + hn)
       const int c0 = eg * hn;

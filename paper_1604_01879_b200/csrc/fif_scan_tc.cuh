@@ -30,6 +30,7 @@ struct TcArgs {
   int has_lo;
   int chunk_kb;
   int mt_major;  // item order within a cell: probe-tile-major (1) or posting-tile-major (0)
+  int dyn;       // items from the meta[M_WORK] counter (1) or a static CTA stride (0)
   const uint8_t* cts;      // compressed tile store of the planes (fif_build.cu) or null
   const int64_t* cts_off;  // [T * nkb + 1] block byte offsets
   int dbg;       // timing experiments only (GIFT_TC_DBG bits; outputs invalid): 1 = skip

@@ -194,6 +194,24 @@ __device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(smem_addr(p)), "r"(rank));
   return r;
 }
+// 64-bit store into a peer CTA's shared memory (shared::cluster address)
+__device__ __forceinline__ void st_cluster_u64(uint32_t cluster_addr, int64_t v) {
+  asm volatile("st.shared::cluster.u64 [%0], %1;\n" ::"r"(cluster_addr), "l"(v) : "memory");
+}
+// wait with cluster-scope acquire (data written by a peer CTA before its
+// release-arrive on this barrier)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_addr(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_bar) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_bar)
                : "memory");

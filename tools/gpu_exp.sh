@@ -1,1 +1,1 @@
-timeout 1500 ncu --set full --import-source on --clock-control none -k regex:fif_scan_tc -s 30 -c 1 -o gpurun_out/scan_c4s_g2 python tools/stage_profile.py --config c4s --steps 1 --reduce owner > gpurun_out/ncu_c4s.log 2>&1; echo ncu=$?
+for sc in static dyn; do GIFT_TC_SCHED=$sc timeout 1500 python bench.py --config c3 --steps 8 --lanes 1 --no-cpu-baseline > gpurun_out/c3_$sc.json 2> gpurun_out/c3_$sc.err; done
