@@ -123,9 +123,9 @@ class ClockSampler:
 
 # (batches in flight, SMs the scan leaves to the other lanes) per config:
 # config 2's non-scan kernels are ~20% of a step and overlap the next
-# batches' scans; config 3 gains little (owner reduce, 105 GB) and loses with
-# reserved SMs; config 4's tensor-bound scan gains nothing
-DEFAULT_LANES = {"c1": (4, LANE_RESERVE_SMS), "c2": (4, LANE_RESERVE_SMS), "c3": (2, 0)}
+# batches' scans; config 3 (owner reduce, 105 GB) and config 4 (tensor-bound
+# scan) measured no gain
+DEFAULT_LANES = {"c1": (4, LANE_RESERVE_SMS), "c2": (4, LANE_RESERVE_SMS)}
 
 
 def warm(fn, iters: int, min_s: float = 0.25):
