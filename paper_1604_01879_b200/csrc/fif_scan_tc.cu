@@ -146,7 +146,7 @@ struct Epi {
   static constexpr int SMEM = RING_BYTES + G * DS * 4 + 256;
 };
 
-template <bool PAIR, int G>
+template <bool PAIR, int G, bool LO>
 __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
     fif_scan_tc_kernel(const __grid_constant__ CUtensorMap tmA1,
                        const __grid_constant__ CUtensorMap tmA2,
@@ -171,16 +171,16 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
   uint64_t* dfull = tempty + 2;                  // D2 item buffers
   uint64_t* dempty = dfull + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(dempty + 2);
-  const int has_lo = p.has_lo;
-  const int stage_bytes = has_lo ? Ring<PAIR>::LO : Ring<PAIR>::NOLO;
-  const int nstages = has_lo ? Ring<PAIR>::STAGES_LO : Ring<PAIR>::STAGES_NOLO;
-  const int b_off = has_lo ? 2 * A_TILE : A_TILE;  // B1 offset in a stage
+  constexpr bool has_lo = LO;  // the f32 storage's lo plane (compile time: lean MMA loop)
+  constexpr int stage_bytes = has_lo ? Ring<PAIR>::LO : Ring<PAIR>::NOLO;
+  constexpr int nstages = has_lo ? Ring<PAIR>::STAGES_LO : Ring<PAIR>::STAGES_NOLO;
+  constexpr int b_off = has_lo ? 2 * A_TILE : A_TILE;  // B1 offset in a stage
   constexpr int B_PART = Ring<PAIR>::B_PART;
   // combined B operand [b1 | b2] (one N = 2n MMA per k-step, A read once):
   // always on a single CTA; on a pair only without the lo plane (CTA r then
   // holds plane r: the pair's B is exactly [b1 | b2]); a pair with the lo
   // plane keeps three MMAs with half of each plane per CTA and D2 per item
-  const bool cb = !PAIR || !has_lo;
+  constexpr bool cb = !PAIR || !has_lo;
   const uint32_t rank = PAIR ? tc::cluster_ctarank() : 0u;
   const bool leader = rank == 0;
   // item sequence: per CTA, or per pair (both CTAs walk the same items)
@@ -1017,12 +1017,12 @@ bool tc_pair_enabled(const gift_fif_view* f) {
   return f->feat_lo != nullptr && sm_count() >= 2;
 }
 
-template <int G>
+template <int G, bool LO>
 static cudaError_t launch_pair(int ctas, cudaStream_t st, const CUtensorMap& mA1,
                                const CUtensorMap& mA2, const CUtensorMap& mB1,
                                const CUtensorMap& mB2, const CUtensorMap& mB1h,
                                const CUtensorMap& mB2h, const TcArgs& a) {
-  cudaError_t e = cudaFuncSetAttribute(fif_scan_tc_kernel<true, G>,
+  cudaError_t e = cudaFuncSetAttribute(fif_scan_tc_kernel<true, G, LO>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, Epi<G>::SMEM);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -1037,7 +1037,8 @@ static cudaError_t launch_pair(int ctas, cudaStream_t st, const CUtensorMap& mA1
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, fif_scan_tc_kernel<true, G>, mA1, mA2, mB1, mB2, mB1h, mB2h, a);
+  return cudaLaunchKernelEx(&cfg, fif_scan_tc_kernel<true, G, LO>, mA1, mA2, mB1, mB2, mB1h, mB2h,
+                            a);
 }
 
 int launch_scan_tc(const gift_fif_view* f, const float* Q, int64_t nprobes_max, TcArgs a,
@@ -1067,14 +1068,20 @@ int launch_scan_tc(const gift_fif_view* f, const float* Q, int64_t nprobes_max, 
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_CTS));
     fif_scan_cts_kernel<<<scan_ctas(f), CTS_THREADS, SMEM_CTS, st>>>(mB1, mB2, a);
   } else if (pair && a.has_lo) {
-    GIFT_CUDA_TRY(launch_pair<1>(scan_ctas(f), st, mA1, mA2, mB1, mB2, mB1h, mB2h, a));
+    GIFT_CUDA_TRY((launch_pair<1, true>(scan_ctas(f), st, mA1, mA2, mB1, mB2, mB1h, mB2h, a)));
   } else if (pair) {  // fp16 storage: tensor-bound, two epilogue groups
-    GIFT_CUDA_TRY(launch_pair<2>(scan_ctas(f), st, mA1, mA2, mB1, mB2, mB1h, mB2h, a));
+    GIFT_CUDA_TRY((launch_pair<2, false>(scan_ctas(f), st, mA1, mA2, mB1, mB2, mB1h, mB2h, a)));
+  } else if (a.has_lo) {
+    GIFT_CUDA_TRY((cudaFuncSetAttribute(fif_scan_tc_kernel<false, 2, true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        Epi<2>::SMEM)));
+    fif_scan_tc_kernel<false, 2, true><<<scan_ctas(f), Epi<2>::THREADS, Epi<2>::SMEM, st>>>(
+        mA1, mA2, mB1, mB2, mB1h, mB2h, a);
   } else {
-    GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_scan_tc_kernel<false, 2>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       Epi<2>::SMEM));
-    fif_scan_tc_kernel<false, 2><<<scan_ctas(f), Epi<2>::THREADS, Epi<2>::SMEM, st>>>(
+    GIFT_CUDA_TRY((cudaFuncSetAttribute(fif_scan_tc_kernel<false, 2, false>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        Epi<2>::SMEM)));
+    fif_scan_tc_kernel<false, 2, false><<<scan_ctas(f), Epi<2>::THREADS, Epi<2>::SMEM, st>>>(
         mA1, mA2, mB1, mB2, mB1h, mB2h, a);
   }
   GIFT_LAUNCH_CHECK();
