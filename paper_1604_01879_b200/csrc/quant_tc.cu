@@ -1,12 +1,16 @@
 // K1 stage 1 on the tensor cores: partial dots  part[z][v][c] = x_v . c_c over
 // the z-th k-split, with the same fp16 two-plane operands as the tcgen05 scan
-// (x = h1 + 2^-11 h2, three kind::f16 MMAs per k-step, fp32 TMEM accumulators
-// drained to registers every 4 k-blocks).  The select stage (quantize.cu)
-// widens its margin by the error coefficient `tc_dot_eps()` so the exact
-// re-check still decides every assignment bit-exactly.
+// (x = h1 + 2^-11 h2; per k-step one N = 256 MMA x1 . [c1 | c2] -> [D1 | D2]
+// over the back-to-back centroid planes (x1 read once) and, with the query lo
+// plane, D2 += x2 . c1; fp32 TMEM accumulators drained to registers every 4
+// k-blocks).  The select stage (quantize.cu) widens its margin by the error
+// coefficient `tc_dot_eps()` so the exact re-check still decides every
+// assignment bit-exactly.
 //
-// Tiles: M = 128 vectors x N = 64 centroids; warp 0 TMA, warp 1 MMA, warps
-// 2..5 epilogue (same roles as fif_scan_tc.cu).
+// Tiles: M = 128 vectors x N = 128 centroids; warp 0 TMA, warp 1 MMA, warps
+// 2..9 epilogue in two column groups (same roles as fif_scan_tc.cu); producer
+// and MMA loops run
+// warp-wide and issue from one elected lane (descriptors stay uniform).
 #include <cudaTypedefs.h>
 
 #include "fif_scan_tc.cuh"
@@ -15,12 +19,14 @@
 namespace gift {
 
 namespace {
-constexpr int QM = 128, QN = 64, QBK = 64, QSTAGES = 4;
+constexpr int QM = 128, QN = 128, QBK = 64, QSTAGES = 3;
 constexpr int QA_TILE = QM * QBK * 2;  // 16 KB
-constexpr int QB_TILE = QN * QBK * 2;  //  8 KB
+constexpr int QB_TILE = QN * QBK * 2;  // 16 KB
 constexpr int QSTAGE = 2 * QA_TILE + 2 * QB_TILE;
-constexpr int QTHREADS = 192;
-constexpr uint32_t QTMEM = 256;
+constexpr int QEG = 2;                    // epilogue groups of 4 warps (QN / QEG columns each)
+constexpr int QNG = QN / QEG;
+constexpr int QTHREADS = 64 + 128 * QEG;
+constexpr uint32_t QTMEM = 512;  // [D1 | D2] x 2 chunk buffers
 constexpr int QSMEM = QSTAGES * QSTAGE + 256;
 constexpr int QCHUNK_KB = 4;
 constexpr float QSPLIT_INV = 1.0f / 2048.0f;
@@ -57,7 +63,7 @@ __global__ void __launch_bounds__(QTHREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&tfull[b], 1);
-      tc::mbar_init(&tempty[b], QM);
+      tc::mbar_init(&tempty[b], QEG * QM);
     }
     tc::fence_barrier_init();
     tc::tma_prefetch(&tmX1);
@@ -82,7 +88,7 @@ __global__ void __launch_bounds__(QTHREADS, 1)
   };
 
   if (warp == 0) {
-    if (lane == 0) {
+    {
       const uint32_t bytes = (p.has_lo ? 2 * QA_TILE : QA_TILE) + 2 * QB_TILE;
       int stage = 0;
       uint32_t phase = 0;
@@ -93,12 +99,16 @@ __global__ void __launch_bounds__(QTHREADS, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * QSTAGE;
-          tc::mbar_arrive_expect_tx(&full[stage], bytes);
-          tc::tma_load_2d(st, &tmX1, &full[stage], kb * QBK, static_cast<int32_t>(r0));
-          if (p.has_lo)
-            tc::tma_load_2d(st + QA_TILE, &tmX2, &full[stage], kb * QBK, static_cast<int32_t>(r0));
-          tc::tma_load_2d(st + 2 * QA_TILE, &tmC1, &full[stage], kb * QBK, c0);
-          tc::tma_load_2d(st + 2 * QA_TILE + QB_TILE, &tmC2, &full[stage], kb * QBK, c0);
+          if (tc::elect_one()) {
+            tc::mbar_arrive_expect_tx(&full[stage], bytes);
+            tc::tma_load_2d(st, &tmX1, &full[stage], kb * QBK, static_cast<int32_t>(r0));
+            if (p.has_lo)
+              tc::tma_load_2d(st + QA_TILE, &tmX2, &full[stage], kb * QBK,
+                              static_cast<int32_t>(r0));
+            tc::tma_load_2d(st + 2 * QA_TILE, &tmC1, &full[stage], kb * QBK, c0);
+            tc::tma_load_2d(st + 2 * QA_TILE + QB_TILE, &tmC2, &full[stage], kb * QBK, c0);
+          }
+          __syncwarp();
           if (++stage == QSTAGES) {
             stage = 0;
             phase ^= 1;
@@ -107,8 +117,9 @@ __global__ void __launch_bounds__(QTHREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {
       const uint32_t idesc = tc::idesc_f16_f32(QM, QN);
+      const uint32_t idesc2 = tc::idesc_f16_f32(QM, 2 * QN);  // [c1 | c2]
       int stage = 0;
       uint32_t phase = 0, chunk_ctr = 0;
       for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
@@ -119,7 +130,7 @@ __global__ void __launch_bounds__(QTHREADS, 1)
           const uint32_t buf = chunk_ctr & 1, aph = (chunk_ctr >> 1) & 1;
           tc::mbar_wait(&tempty[buf], aph ^ 1);
           tc::tc_fence_after();
-          const uint32_t d1 = tmem_base + buf * 128, d2 = d1 + QN;
+          const uint32_t d1 = tmem_base + buf * 2 * QN, d2 = d1 + QN;
           const int kend = min(ck + QCHUNK_KB, kb1);
           for (int kb = ck; kb < kend; ++kb) {
             tc::mbar_wait(&full[stage], phase);
@@ -128,22 +139,24 @@ __global__ void __launch_bounds__(QTHREADS, 1)
             const uint64_t a1 = tc::smem_desc_sw128(st);
             const uint64_t a2 = tc::smem_desc_sw128(st + QA_TILE);
             const uint64_t b1 = tc::smem_desc_sw128(st + 2 * QA_TILE);
-            const uint64_t b2 = tc::smem_desc_sw128(st + 2 * QA_TILE + QB_TILE);
+            if (tc::elect_one()) {
 #pragma unroll
-            for (int k = 0; k < QBK / 16; ++k) {
-              const uint32_t acc = (kb > ck || k > 0) ? 1u : 0u;
-              const uint64_t adv = static_cast<uint64_t>(k * 2);
-              tc::mma_f16(d1, a1 + adv, b1 + adv, idesc, acc);
-              tc::mma_f16(d2, a1 + adv, b2 + adv, idesc, acc);
-              if (p.has_lo) tc::mma_f16(d2, a2 + adv, b1 + adv, idesc, 1u);
+              for (int k = 0; k < QBK / 16; ++k) {
+                const uint32_t acc = (kb > ck || k > 0) ? 1u : 0u;
+                const uint64_t adv = static_cast<uint64_t>(k * 2);
+                tc::mma_f16(d1, a1 + adv, b1 + adv, idesc2, acc);  // [D1 | D2] = x1 . [c1 | c2]
+                if (p.has_lo) tc::mma_f16(d2, a2 + adv, b1 + adv, idesc, 1u);
+              }
+              tc::mma_commit(&empty[stage]);
             }
-            tc::mma_commit(&empty[stage]);
+            __syncwarp();
             if (++stage == QSTAGES) {
               stage = 0;
               phase ^= 1;
             }
           }
-          tc::mma_commit(&tfull[buf]);
+          if (tc::elect_one()) tc::mma_commit(&tfull[buf]);
+          __syncwarp();
           ++chunk_ctr;
         }
       }
@@ -151,22 +164,24 @@ __global__ void __launch_bounds__(QTHREADS, 1)
   } else {
     const int lb = 32 * (warp & 3);
     const int row = lb + lane;
+    const int cg = (warp - 2) / 4 * QNG;  // this group's first column of the tile
     uint32_t chunk_ctr = 0;
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       int64_t r0;
       int c0, kb0, kb1;
       decode(item, r0, c0, kb0, kb1);
       const int z = static_cast<int>(item % p.ksplit);
-      float acc[QN];
+      float acc[QNG];
 #pragma unroll
-      for (int c = 0; c < QN; ++c) acc[c] = 0.f;
+      for (int c = 0; c < QNG; ++c) acc[c] = 0.f;
       for (int ck = kb0; ck < kb1; ck += QCHUNK_KB) {
         const uint32_t buf = chunk_ctr & 1, aph = (chunk_ctr >> 1) & 1;
         tc::mbar_wait(&tfull[buf], aph);
         tc::tc_fence_after();
-        const uint32_t base = tmem_base + (static_cast<uint32_t>(lb) << 16) + buf * 128;
+        const uint32_t base =
+            tmem_base + (static_cast<uint32_t>(lb) << 16) + buf * 2 * QN + cg;
 #pragma unroll
-        for (int j = 0; j < QN / 16; ++j) {
+        for (int j = 0; j < QNG / 16; ++j) {
           float v1[16], v2[16];
           tc::tmem_ld_x16(base + j * 16, v1);
           tc::tmem_ld_x16(base + QN + j * 16, v2);
@@ -180,16 +195,16 @@ __global__ void __launch_bounds__(QTHREADS, 1)
       }
       const int64_t v = r0 + row;
       if (v < p.n) {
-        float* out = p.part + (static_cast<int64_t>(z) * p.n + v) * p.K + c0;
-        const int nc = min(QN, p.K - c0);
-        if (nc == QN && (p.K % 4) == 0) {
+        float* out = p.part + (static_cast<int64_t>(z) * p.n + v) * p.K + c0 + cg;
+        const int nc = min(QNG, p.K - c0 - cg);
+        if (nc == QNG && (p.K % 4) == 0) {
 #pragma unroll
-          for (int c = 0; c < QN; c += 4)
+          for (int c = 0; c < QNG; c += 4)
             *reinterpret_cast<float4*>(out + c) =
                 make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
         } else {
 #pragma unroll
-          for (int c = 0; c < QN; ++c)
+          for (int c = 0; c < QNG; ++c)
             if (c < nc) out[c] = acc[c];
         }
       }
