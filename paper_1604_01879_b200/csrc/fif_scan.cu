@@ -911,11 +911,13 @@ __global__ void owner_count_kernel(const int32_t* __restrict__ cells,
   cnt[p] = n;
 }
 
+// candidate lists per owner work item: one per warp (no CTA barrier per item;
+// the top-k2 merge downstream takes OWN_WARPS times more candidates)
+constexpr int OWN_WARPS = GR_THREADS / 32;
+
 template <int W>
 __global__ void __launch_bounds__(GR_THREADS) fif_owner_reduce_kernel(GatherArgs a) {
   extern __shared__ __align__(16) double s_tab[];
-  __shared__ double s_ws[GR_THREADS / 32][RED_MAXK];
-  __shared__ int32_t s_wo[GR_THREADS / 32][RED_MAXK];
   if (a.meta[M_OVERFLOW]) return;
   const int slots = a.V * a.ma;
   const int64_t nprobes = static_cast<int64_t>(a.B) * slots;
@@ -939,7 +941,8 @@ __global__ void __launch_bounds__(GR_THREADS) fif_owner_reduce_kernel(GatherArgs
   const int b = static_cast<int>(pr / slots), j = static_cast<int>(pr - static_cast<int64_t>(b) * slots);
   const int chunk_id = static_cast<int>(w - a.work_off[pr]);
   const int64_t cand_at =
-      ((static_cast<int64_t>(b) * slots + j) * a.nchunk + chunk_id) * static_cast<int64_t>(ck);
+      (((static_cast<int64_t>(b) * slots + j) * a.nchunk + chunk_id) * OWN_WARPS +
+       (threadIdx.x >> 5)) * static_cast<int64_t>(ck);
   const int c = a.cells[pr];
   const int64_t S_c = a.seg_off[c + 1] - a.seg_off[c];
   const int64_t k0 = static_cast<int64_t>(chunk_id) * a.chunk;
@@ -977,34 +980,17 @@ __global__ void __launch_bounds__(GR_THREADS) fif_owner_reduce_kernel(GatherArgs
     if (a.scores) a.scores[static_cast<int64_t>(b) * a.n_local + s] = score;
     if (ck > 0) cand_insert(ls, lo_, ck, score, ord);
   }
-  if (ck > 0) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (ck > 0) {  // this warp's best ck
     double os[RED_MAXK];
     int32_t oo[RED_MAXK];
     warp_select(ls, lo_, ck, os, oo);
-    if (lane == 0)
+    if ((threadIdx.x & 31) == 0)
 #pragma unroll
-      for (int r = 0; r < RED_MAXK; ++r) {
-        s_ws[warp][r] = r < ck ? os[r] : -INFINITY;
-        s_wo[warp][r] = r < ck ? oo[r] : -1;
-      }
-    __syncthreads();
-    if (warp == 0) {  // merge the warps' lists: lane w < 8 holds warp w's list
-#pragma unroll
-      for (int q = 0; q < RED_MAXK; ++q) {
-        ls[q] = lane < GR_THREADS / 32 ? s_ws[lane][q] : -INFINITY;
-        lo_[q] = lane < GR_THREADS / 32 ? s_wo[lane][q] : -1;
-      }
-      warp_select(ls, lo_, ck, os, oo);
-      if (lane == 0)
-#pragma unroll
-        for (int r = 0; r < RED_MAXK; ++r)
-          if (r < ck) {
-            a.cand_s[cand_at + r] = oo[r] >= 0 ? os[r] : 0.0;
-            a.cand_i[cand_at + r] = oo[r];
-          }
-    }
-    __syncthreads();  // s_ws reuse by the next item
+      for (int r = 0; r < RED_MAXK; ++r)
+        if (r < ck) {
+          a.cand_s[cand_at + r] = oo[r] >= 0 ? os[r] : 0.0;
+          a.cand_i[cand_at + r] = oo[r];
+        }
   }
   }
 }
@@ -1166,7 +1152,7 @@ extern "C" int gift_fif_reduce_mode(const gift_fif_view* f, int32_t V, int32_t m
 extern "C" int gift_fif_score_ranges2(const gift_fif_view* f, int32_t V, int32_t ma) {
   const int mode = reduce_mode(f, V, ma);
   if (mode == RM_GATHER) return static_cast<int>(cdiv(max64(f->n_local, 1), gather_rs(f->n_local)));
-  if (mode == RM_OWNER) return V * ma * owner_nchunk(f);
+  if (mode == RM_OWNER) return V * ma * owner_nchunk(f) * OWN_WARPS;
   return gift_fif_score_ranges(f, V);
 }
 
@@ -1334,7 +1320,7 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
       ga.rs = 0;
       ga.chunk = OWN_CHUNK;
       ga.nchunk = owner_nchunk(f);
-      ga.n_ranges = V * ma * ga.nchunk;
+      ga.n_ranges = V * ma * ga.nchunk * OWN_WARPS;
       if (out_scores)
         GIFT_CUDA_TRY(cudaMemsetAsync(out_scores, 0, sizeof(double) * B * f->n_local, st));
       if (ga.cand_k > 0) {  // slots without work keep "no candidate"
