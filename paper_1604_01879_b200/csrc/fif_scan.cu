@@ -560,6 +560,7 @@ __global__ void __launch_bounds__(RED_THREADS) fif_reduce_kernel(ReduceArgs a) {
 constexpr int GR_THREADS = 256;
 constexpr int GR_G = 4;         // queries per CTA (fewer when the grid would under-fill)
 constexpr int GR_SEGC = 4;      // shape segments cached in registers
+constexpr int GR_PC = 8;        // probed cells of a shape kept for the slot lookups
 constexpr int GR_MAXK = 16384;  // cells covered by the shared-memory bitmap
 constexpr int GR_RS_SMALL = 256, GR_RS_LARGE = 1024;
 
@@ -729,6 +730,13 @@ __device__ __forceinline__ double pair_acc(const GatherArgs& a, const GrTabs& t,
   uint32_t U[W];
 #pragma unroll
   for (int w = 0; w < W; ++w) U[w] = 0u;
+  // the shape's probed cells and their segments, kept in registers for the
+  // per-bit lookups below (GR_PC of them; more fall back to a global search)
+  int pc[GR_PC];
+  int32_t ps[GR_PC];
+  int npc = 0;
+#pragma unroll
+  for (int q = 0; q < GR_PC; ++q) pc[q] = -1;
 #pragma unroll
   for (int j = 0; j < GR_SEGC + 1; ++j) {
     // j < GR_SEGC: cached segment j; j == GR_SEGC: the uncached rest
@@ -740,6 +748,14 @@ __device__ __forceinline__ double pair_acc(const GatherArgs& a, const GrTabs& t,
         const int rank = pre[c >> 5] + __popc(word & ((1u << (c & 31)) - 1u));
 #pragma unroll
         for (int w = 0; w < W; ++w) U[w] |= set[rank * W + w];
+        const int32_t sgv = j < GR_SEGC ? h.seg[j] : a.shape_seg[h.g0 + jj];
+#pragma unroll
+        for (int q = 0; q < GR_PC; ++q)
+          if (q == npc) {
+            pc[q] = c;
+            ps[q] = sgv;
+          }
+        ++npc;
       }
     }
   }
@@ -805,10 +821,15 @@ __device__ __forceinline__ double pair_acc(const GatherArgs& a, const GrTabs& t,
         const int cj = scl[jj[q]];
         int32_t sg = -1;
 #pragma unroll
-        for (int r = 0; r < GR_SEGC; ++r)
-          if (h.cell[r] == cj) sg = h.seg[r];
-        for (int r = GR_SEGC; sg < 0 && r < h.nseg; ++r)
-          if (a.shape_seg_cell[h.g0 + r] == cj) sg = a.shape_seg[h.g0 + r];
+        for (int r = 0; r < GR_PC; ++r)
+          if (pc[r] == cj) sg = ps[r];
+        if (sg < 0 && npc > GR_PC) {  // more probed cells than registers: search
+#pragma unroll
+          for (int r = 0; r < GR_SEGC; ++r)
+            if (h.cell[r] == cj) sg = h.seg[r];
+          for (int r = GR_SEGC; sg < 0 && r < h.nseg; ++r)
+            if (a.shape_seg_cell[h.g0 + r] == cj) sg = a.shape_seg[h.g0 + r];
+        }
         val[q] = a.out[sb[jj[q]] + sg];
       }
     }
