@@ -283,20 +283,26 @@ struct TkBetter {
 };
 constexpr int TKS_WARPS = 8;
 
+// WPR = 1: one warp per row (TKS_WARPS rows per CTA); WPR = TKS_WARPS: one CTA
+// per row (long rows: the owner reduce's per-warp candidate lists), the warps'
+// best-8 lists merged by warp 0 through shared memory.
+template <int WPR>
 __global__ void __launch_bounds__(TKS_WARPS * 32)
     topk_small_kernel(const TopkIn in, const TopkOut out, int B) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int b = blockIdx.x * TKS_WARPS + warp;
+  const int b = WPR == 1 ? blockIdx.x * TKS_WARPS + warp : blockIdx.x;
   if (b >= B) return;
   const int64_t e1 = in.counts ? min64(in.m, static_cast<int64_t>(in.counts[b])) : in.m;
   TkKey best[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) best[i] = TkKey{-INFINITY, 0xffffffffu, -1};
   const int64_t row = static_cast<int64_t>(b) * in.m;
-  for (int64_t e = lane; e < e1; e += 32) {
+  const int64_t e0 = WPR == 1 ? lane : warp * 32 + lane;
+  for (int64_t e = e0; e < e1; e += 32 * WPR) {
     TkKey x{in.cs[row + e], 0u, in.ci[row + e]};
     if (x.j < 0) continue;
     x.t = in.ct ? in.ct[row + e] : static_cast<uint32_t>(x.j);
+    if (!TkBetter()(x, best[7])) continue;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       if (TkBetter()(x, best[i])) {
@@ -306,16 +312,31 @@ __global__ void __launch_bounds__(TKS_WARPS * 32)
       }
     }
   }
+  auto warp_merge = [&]() {
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    TkKey oth[8];
+    for (int o = 1; o < 32; o <<= 1) {
+      TkKey oth[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      oth[i].s = __shfl_xor_sync(0xffffffffu, best[i].s, o);
-      oth[i].t = __shfl_xor_sync(0xffffffffu, best[i].t, o);
-      oth[i].j = __shfl_xor_sync(0xffffffffu, best[i].j, o);
+      for (int i = 0; i < 8; ++i) {
+        oth[i].s = __shfl_xor_sync(0xffffffffu, best[i].s, o);
+        oth[i].t = __shfl_xor_sync(0xffffffffu, best[i].t, o);
+        oth[i].j = __shfl_xor_sync(0xffffffffu, best[i].j, o);
+      }
+      merge8(best, oth, TkBetter());
     }
-    merge8(best, oth, TkBetter());
+  };
+  warp_merge();
+  if (WPR > 1) {
+    __shared__ TkKey s_best[WPR > 1 ? WPR : 1][8];
+    if (lane == 0)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s_best[warp][i] = best[i];
+    __syncthreads();
+    if (warp != 0) return;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      best[i] = lane < WPR ? s_best[lane][i] : TkKey{-INFINITY, 0xffffffffu, -1};
+    warp_merge();
   }
   const int k = out.k;
 #pragma unroll
@@ -326,6 +347,14 @@ __global__ void __launch_bounds__(TKS_WARPS * 32)
       out.out_val[static_cast<int64_t>(b) * k + i] = ok ? best[i].s : 0.0;
     }
   }
+}
+
+static void launch_topk_small(const TopkIn& in, const TopkOut& out, int B, cudaStream_t st) {
+  if (in.m >= 2048)
+    topk_small_kernel<TKS_WARPS><<<static_cast<unsigned>(B), TKS_WARPS * 32, 0, st>>>(in, out, B);
+  else
+    topk_small_kernel<1><<<static_cast<unsigned>(cdiv(B, TKS_WARPS)), TKS_WARPS * 32, 0, st>>>(
+        in, out, B);
 }
 
 // Best k of explicit (score, tiebreak, global ordinal) rows with per-row
@@ -353,8 +382,7 @@ int topk_rows_from_lists(const double* cs, const uint32_t* ct, const int32_t* ci
   out.out_idx = out_idx;
   out.out_val = out_val;
   if (k <= 8) {
-    topk_small_kernel<<<static_cast<unsigned>(cdiv(B, TKS_WARPS)), TKS_WARPS * 32, 0, st>>>(in, out,
-                                                                                          B);
+    launch_topk_small(in, out, B, st);
   } else {
     topk_kernel<256, false><<<dim3(1, B), TK_THREADS, smem, st>>>(in, out);
   }
@@ -416,8 +444,7 @@ extern "C" int gift_topk_cand(const double* cs, const int32_t* ci, int32_t B, in
   out.out_idx = out_idx;
   out.out_val = out_val;
   if (k <= 8) {
-    topk_small_kernel<<<static_cast<unsigned>(cdiv(B, TKS_WARPS)), TKS_WARPS * 32, 0, st>>>(in, out,
-                                                                                          B);
+    launch_topk_small(in, out, B, st);
   } else {
     topk_kernel<256, false><<<dim3(1, B), TK_THREADS, smem, st>>>(in, out);
   }
