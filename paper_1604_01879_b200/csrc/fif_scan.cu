@@ -936,8 +936,10 @@ __global__ void owner_count_kernel(const int32_t* __restrict__ cells,
 // the top-k2 merge downstream takes OWN_WARPS times more candidates)
 constexpr int OWN_WARPS = GR_THREADS / 32;
 
+// Latency-bound (dependent gathers per pair): 4 CTAs per SM (64 registers,
+// some spills) measured faster than 2 (config 4: 3.3 -> 2.1 ms per batch).
 template <int W>
-__global__ void __launch_bounds__(GR_THREADS) fif_owner_reduce_kernel(GatherArgs a) {
+__global__ void __launch_bounds__(GR_THREADS, 4) fif_owner_reduce_kernel(GatherArgs a) {
   extern __shared__ __align__(16) double s_tab[];
   if (a.meta[M_OVERFLOW]) return;
   const int slots = a.V * a.ma;
