@@ -526,15 +526,7 @@ __global__ void __launch_bounds__(QW_WARPS * 32)
   float loc[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) loc[i] = INFINITY;
-  for (int c = lane, ii = 0; c < K; c += 32, ++ii) {
-    float x = INFINITY;
-    if (in_regs) {
-#pragma unroll
-      for (int i = 0; i < QW_REG; ++i)
-        if (i == ii) x = av[i];
-    } else {
-      x = approx_at(c);
-    }
+  auto insert = [&](float x) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       if (i < ma && x < loc[i]) {
@@ -542,6 +534,24 @@ __global__ void __launch_bounds__(QW_WARPS * 32)
         loc[i] = x;
         x = t;
       }
+    }
+  };
+  // large codebooks: QW_UNR row values per lane loaded before they are
+  // inserted (memory-level parallelism; the row is re-read in pass 2)
+  constexpr int QW_UNR = 8;
+  if (in_regs) {
+#pragma unroll
+    for (int i = 0; i < QW_REG; ++i) insert(av[i]);
+  } else {
+    for (int c0 = lane; c0 < K; c0 += 32 * QW_UNR) {
+      float xs[QW_UNR];
+#pragma unroll
+      for (int u = 0; u < QW_UNR; ++u) {
+        const int c = c0 + 32 * u;
+        xs[u] = c < K ? approx_at(c) : INFINITY;
+      }
+#pragma unroll
+      for (int u = 0; u < QW_UNR; ++u) insert(xs[u]);
     }
   }
 #pragma unroll
@@ -563,21 +573,27 @@ __global__ void __launch_bounds__(QW_WARPS * 32)
   // pass 2: candidates under the threshold
   int cnt = 0;
   const unsigned lt = (1u << lane) - 1u;
-  for (int c0 = 0, ii = 0; c0 < K; c0 += 32, ++ii) {
-    const int c = c0 + lane;
-    float x = INFINITY;
-    if (in_regs) {
-#pragma unroll
-      for (int i = 0; i < QW_REG; ++i)
-        if (i == ii) x = av[i];
-    } else if (c < K) {
-      x = approx_at(c);
-    }
+  auto collect = [&](int c, float x) {  // warp-uniform call
     const bool hit = c < K && static_cast<double>(x) <= thresh;
     const unsigned bal = __ballot_sync(0xffffffffu, hit);
     const int pos = cnt + __popc(bal & lt);
     if (hit && pos < 8) s_ci[warp][pos] = c;
     cnt += __popc(bal);
+  };
+  if (in_regs) {
+#pragma unroll
+    for (int i = 0; i < QW_REG; ++i) collect(lane + 32 * i, av[i]);
+  } else {
+    for (int b0 = 0; b0 < K; b0 += 32 * QW_UNR) {
+      float xs[QW_UNR];
+#pragma unroll
+      for (int u = 0; u < QW_UNR; ++u) {
+        const int c = b0 + 32 * u + lane;
+        xs[u] = c < K ? approx_at(c) : INFINITY;
+      }
+#pragma unroll
+      for (int u = 0; u < QW_UNR; ++u) collect(b0 + 32 * u + lane, xs[u]);
+    }
   }
   __syncwarp();
   int* ci = s_ci[warp];

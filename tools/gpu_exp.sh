@@ -1,3 +1,3 @@
 timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
-timeout 1500 python bench.py --config c4 --steps 5 --no-cpu-baseline > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err
-timeout 1500 python bench.py --config c3 --steps 8 --no-cpu-baseline > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
+timeout 1500 python tools/lane_trace.py --config c4 --lanes 1 --steps 4 > gpurun_out/lt_c4_l1.json 2> gpurun_out/lt_c4_l1.err
+timeout 1500 python tools/lane_trace.py --config c3 --lanes 1 --steps 4 > gpurun_out/lt_c3_l1.json 2> gpurun_out/lt_c3_l1.err
