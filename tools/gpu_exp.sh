@@ -1,1 +1,3 @@
-timeout 1500 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,lts__t_sector_hit_rate.pct --clock-control none -k regex:fif_scan_tc -s 44 -c 3 --csv --log-file gpurun_out/scan_c2_dram.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --lanes 1 > gpurun_out/ncu_c2.log 2>&1; echo ncu=$?
+GIFT_CTS=1 GIFT_TC_DBG=64 timeout 900 python bench.py --no-cpu-baseline --lanes 1 > gpurun_out/c2_cts64.json 2> gpurun_out/c2_cts64.err
+GIFT_CTS=1 GIFT_TC_DBG=3 timeout 900 python bench.py --no-cpu-baseline --lanes 1 > gpurun_out/c2_cts3.json 2> gpurun_out/c2_cts3.err
+GIFT_CTS=1 GIFT_TC_DBG=67 timeout 900 python bench.py --no-cpu-baseline --lanes 1 > gpurun_out/c2_cts67.json 2> gpurun_out/c2_cts67.err
