@@ -298,9 +298,16 @@ def test_persistence_round_trip_and_bytes():
             assert gift.query_by_id(loaded, sid, top_k=20)[0] == gift.query_by_id(bundle, sid, top_k=20)[0]
 
 
-def test_fp16_storage_matches_widened_oracle():
+@pytest.mark.parametrize("variant", ["default", "pair", "static"])
+def test_fp16_storage_matches_widened_oracle(variant, monkeypatch):
     """Config 4 storage (D5): fp16 features, fp32 accumulation; the oracle
-    sees the same fp16 values widened to f32."""
+    sees the same fp16 values widened to f32.  Variants: the single-CTA scan
+    with two epilogue groups (default), CTA pairs (GIFT_TC_PAIR=1) and the
+    static item stride (GIFT_TC_SCHED=static)."""
+    if variant == "pair":
+        monkeypatch.setenv("GIFT_TC_PAIR", "1")
+    if variant == "static":
+        monkeypatch.setenv("GIFT_TC_SCHED", "static")
     views, _ = mixture_views(21, 200, 20, 1024, 16, n_queries=4)
     v16 = views.astype(np.float16)
     db, qs = v16[:200], v16[200:].astype(np.float32)
@@ -332,13 +339,15 @@ def test_sif_self_score_exactly_one_at_scale():
         assert sc[j, j] == 1.0
 
 
-@pytest.mark.parametrize("lanes", [1, 2, 3])
-def test_query_many_pipelined_equals_batch(lanes):
-    """Batches in flight on 1-3 compute streams (own scratch each) return the
-    serial results, bit for bit."""
+@pytest.mark.parametrize("lanes,reserve", [(1, 0), (2, 0), (3, 20)])
+def test_query_many_pipelined_equals_batch(lanes, reserve):
+    """Batches in flight on 1-3 compute streams (own scratch each; the scan
+    optionally leaving SMs to the other lanes) return the serial results, bit
+    for bit."""
     bundle, db, qs, ids, C = _e2e_bundle(E2E_CASES[2])
     host = torch.from_numpy(np.concatenate([qs, db[:20]])).pin_memory()
-    idx, val = gift.query_many(bundle, host, top_k=30, batch_size=5, lanes=lanes)
+    idx, val = gift.query_many(bundle, host, top_k=30, batch_size=5, lanes=lanes,
+                               reserve_sms=reserve)
     ref = gift.query_batch(bundle, host.numpy(), top_k=30)
     for r in range(len(ref)):
         assert [ids[i] for i in idx[r]] == [x[0] for x in ref[r]]
@@ -357,18 +366,27 @@ def test_tensor_core_scan_matches_oracle_at_c2_dims(similarity, monkeypatch):
     fif = mt.build_fif_from_tensor(torch.from_numpy(db).to(dev()), Codebook(C), shape_ids(300))
     assert fif.dev.feat_hi is not None  # tensor-core planes built
     got = {}
-    for impl in ("tc", "simt"):
-        monkeypatch.setenv("GIFT_SCAN", impl)
+    # tc: CTA pairs (default with the f32 lo plane); tc_single: one CTA, two
+    # epilogue groups; tc_static: static item stride instead of the counter
+    for impl, env in (("tc", {}), ("tc_single", {"GIFT_TC_PAIR": "0"}),
+                      ("tc_static", {"GIFT_TC_SCHED": "static"}), ("simt", {})):
+        monkeypatch.setenv("GIFT_SCAN", "simt" if impl == "simt" else "tc")
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
         got[impl] = mt.query_fif_batch(fif, qs, 2, similarity).cpu().numpy()
+        for k in env:
+            monkeypatch.delenv(k)
+    np.testing.assert_array_equal(got["tc_static"], got["tc"])  # same items, same order
     worst = 0.0
-    for q, g_tc, g_simt in zip(qs, got["tc"], got["simt"]):
+    for i, q in enumerate(qs):
         e = oracle.query_fif(ref, q, 2, similarity,
                              cells=oracle.quantize_many(C, q.astype(np.float64), 2))
         nz = e > 0
+        g_tc = got["tc"][i]
         worst = max(worst, float(np.max(np.abs(g_tc[nz] - e[nz]) / e[nz])) if nz.any() else 0.0)
-        np.testing.assert_allclose(g_tc, e, rtol=RTOL, atol=1e-12)
-        np.testing.assert_allclose(g_simt, e, rtol=RTOL, atol=1e-12)
-        assert ((g_tc == 0) == (e == 0)).all()
+        for impl in ("tc", "tc_single", "simt"):
+            np.testing.assert_allclose(got[impl][i], e, rtol=RTOL, atol=1e-12)
+            assert ((got[impl][i] == 0) == (e == 0)).all()
     print(f"max relative error tc vs oracle ({similarity}): {worst:.2e}")
 
 
