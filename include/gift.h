@@ -138,6 +138,25 @@ int gift_cts_stage_limit(void);
 int gift_normalize_rows(const float* x, const double* norms, int64_t rows, int32_t d,
                         float* out, void* stream);
 
+/* ---- codebook training (codebook.py:37-108, train_codebook) ----------------
+ * Device half of k-means++ and Lloyd's iterations in f64; the host runs the
+ * reference's control flow and numpy RNG stream.
+ * gift_rows_sqnorm_f64: out[r] = sum_j X[r,j]^2 in numpy's pairwise order
+ *   ((points * points).sum(axis=1), codebook.py:39-41).
+ * gift_kmeans_assign: per point the nearest center by
+ *   max((|x|^2 - 2 x.c) + |c|^2, 0) (codebook.py:37-45), ties to the lower
+ *   index (argmin, codebook.py:84-85); out_label / out_mind2 may be NULL.
+ * gift_kmeans_update: out[c,:] = (sum of X[order[m],:] for m in
+ *   [off[c], off[c+1]) in that order, from 0.0) / (off[c+1] - off[c])
+ *   (np.add.at + division, codebook.py:96-98); order = points stably sorted
+ *   by label. */
+int gift_rows_sqnorm_f64(const double* X, int64_t n, int32_t d, double* out, void* stream);
+int gift_kmeans_assign(const double* X, int64_t n, int32_t d, const double* C, int32_t k,
+                       const double* xn2, const double* cn2, int32_t* out_label,
+                       double* out_mind2, void* stream);
+int gift_kmeans_update(const double* X, int64_t n, int32_t d, const int64_t* order,
+                       const int64_t* off, int32_t k, double* out_centers, void* stream);
+
 /* Per-view non-zero flag and |x|^2 (f64 accumulate, stored f32).
  * `row.any()` tests of matching.py:121 / :150. */
 int gift_view_prep(const void* X, int32_t xdtype, int64_t nviews, int32_t d,

@@ -18,7 +18,7 @@ __all__ = [
     "seq_sum", "make_activation", "build_activation", "top_neighbors",
     "mean_activation", "co_augment", "aggregate", "Sif", "build_sif",
     "query_sif", "jaccard_dense", "OracleIndex", "lexsort_rank",
-    "oracle_lib",
+    "oracle_lib", "train_codebook",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -474,3 +474,54 @@ class OracleIndex:
         va = self.fifs["A"].shape_matrix(o)
         vb = None if self.single else self.fifs["B"].shape_matrix(o)
         return self.query(va, vb, self_id=shape_id, top_k=top_k, rerank=rerank)
+
+
+# ------------------------------------------------------------------ codebook training
+def _sq_dists(points, centers):
+    """codebook.py:37-45: (|x|^2 - 2 x.c) + |c|^2 (BLAS product), clamped at 0."""
+    d2 = ((points * points).sum(axis=1)[:, None] - 2.0 * points @ centers.T
+          + (centers * centers).sum(axis=1)[None, :])
+    np.maximum(d2, 0.0, out=d2)
+    return d2
+
+
+def train_codebook(features, k: int, seed: int = 0, max_iters: int = 50) -> np.ndarray:
+    """codebook.py:48-108 restated: k-means++ seeding (rng.integers for the
+    first center, rng.choice(n, p=D^2 / sum) per further center, rng.integers
+    when every distance is 0), then Lloyd iterations with the empty-cluster
+    repair (the largest cluster donates its farthest member) until the
+    relative cost change drops under 1e-4.  Returns f32 centroids (k, d)."""
+    points = np.asarray(features, dtype=np.float64)
+    n = points.shape[0]
+    if n < k:
+        points = np.tile(points, (-(-k // n), 1))
+        n = points.shape[0]
+    rng = np.random.default_rng(seed)
+    centers = np.empty((k, points.shape[1]), dtype=np.float64)
+    centers[0] = points[rng.integers(0, n)]
+    closest = _sq_dists(points, centers[:1])[:, 0]
+    for i in range(1, k):
+        total = closest.sum()
+        idx = int(rng.integers(0, n)) if total <= 0.0 else int(rng.choice(n, p=closest / total))
+        centers[i] = points[idx]
+        np.minimum(closest, _sq_dists(points, centers[i:i + 1])[:, 0], out=closest)
+    prev = None
+    for _ in range(max_iters):
+        d2 = _sq_dists(points, centers)
+        lab = d2.argmin(axis=1)
+        cost = float(d2[np.arange(n), lab].sum())
+        counts = np.bincount(lab, minlength=k)
+        for e in np.flatnonzero(counts == 0):
+            donor = int(counts.argmax())
+            members = np.flatnonzero(lab == donor)
+            steal = members[d2[members, donor].argmax()]
+            lab[steal] = e
+            counts[donor] -= 1
+            counts[e] += 1
+        new = np.zeros_like(centers)
+        np.add.at(new, lab, points)
+        centers = new / counts[:, None]
+        if prev is not None and abs(prev - cost) / max(prev, 1e-300) < 1e-4:
+            break
+        prev = cost
+    return centers.astype(np.float32)

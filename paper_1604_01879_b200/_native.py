@@ -59,6 +59,10 @@ _SIGS = {
     "gift_quantize_ws_bytes": (_c_sz, [_c_i64, _c_i32, _c_i32, _c_i32]),
     "gift_quantize": (_c_i32, [_c_p, _c_i32, _c_i64, _c_i32, _c_p, _c_p, _c_i32, _c_dbl, _c_i32,
                                _c_p, _c_i32, _c_p, _c_p, _c_sz, _c_p]),
+    "gift_rows_sqnorm_f64": (_c_i32, [_c_p, _c_i64, _c_i32, _c_p, _c_p]),
+    "gift_kmeans_assign": (_c_i32, [_c_p, _c_i64, _c_i32, _c_p, _c_i32, _c_p, _c_p, _c_p, _c_p,
+                                    _c_p]),
+    "gift_kmeans_update": (_c_i32, [_c_p, _c_i64, _c_i32, _c_p, _c_p, _c_i32, _c_p, _c_p]),
     "gift_normalize_rows": (_c_i32, [_c_p, _c_p, _c_i64, _c_i32, _c_p, _c_p]),
     "gift_view_prep": (_c_i32, [_c_p, _c_i32, _c_i64, _c_i32, _c_p, _c_p, _c_p]),
     "gift_radix_sort_ws_bytes": (_c_sz, [_c_i64]),

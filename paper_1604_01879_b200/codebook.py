@@ -1,9 +1,10 @@
-"""Codebook container and the GPU quantizer.
+"""Codebook container, the GPU quantizer and codebook training.
 
-Mirrors `shapesearch.codebook` (codebook.py:22-34 Codebook, :111-124
-quantize, :127-145 persistence).  Codebook training (k-means, codebook.py:37-108)
-is outside the GPU path (divergence D3): codebooks are given,
-e.g. `sample_codebook` (seeded DB rows, the BASELINE.json configs' rule).
+Mirrors `shapesearch.codebook` (codebook.py:22-34 Codebook, :37-108
+train_codebook, :111-124 quantize, :127-145 persistence).  The benchmark
+configs use given codebooks (`sample_codebook`: seeded DB rows, the
+BASELINE.json configs' rule, divergence D3); `train_codebook` runs the
+reference's k-means++ + Lloyd on the device.
 """
 
 from __future__ import annotations
@@ -18,6 +19,8 @@ from . import engine as eg
 from .errors import DimensionMismatch, EmptyInput, FormatError
 
 DEFAULT_K = 256
+DEFAULT_MAX_ITERS = 50  # codebook.py:18-19
+CONVERGENCE_TOL = 1e-4
 _DEV_CACHE: dict = {}
 
 
@@ -54,6 +57,105 @@ def sample_codebook(vectors, k: int, seed: int = 0, channel: str = "") -> Codebo
     rng = np.random.default_rng(seed)
     pick = rng.choice(nz, size=k, replace=len(nz) < k)
     return Codebook(centroids=flat[np.sort(pick)].copy(), channel=channel, seed=seed)
+
+
+def train_codebook(features, k: int, seed: int = 0, max_iters: int = DEFAULT_MAX_ITERS,
+                   channel: str = "") -> Codebook:
+    """Lloyd's k-means with k-means++ seeding (codebook.py:48-108).  The host
+    runs the reference's control flow and its numpy RNG stream: the same
+    draws in the same order (rng.integers for the first center, one
+    rng.random per Generator.choice(n, p=...) -- cdf = cumsum(p) / cdf[-1],
+    searchsorted(side='right') -- and rng.integers when every distance is
+    0), the same empty-cluster repair (largest cluster donates its farthest
+    member) and the same relative-cost convergence test.  The device computes
+    the f64 distances (gift_kmeans_assign: |x|^2 in numpy's pairwise order,
+    the same formula and clamp, ties to the lower index) and the new centers
+    (gift_kmeans_update: members summed in point order, np.add.at's order).
+    Only the x.c dot products are summed in another order than the
+    reference's BLAS, so a label can differ only for a point equidistant to
+    two centers within a few ulps."""
+    from . import _native as nat
+
+    points = np.asarray(features, dtype=np.float64)
+    if points.ndim != 2 or points.shape[0] == 0:
+        raise EmptyInput("no training vectors")
+    n, d = points.shape
+    if n < k:
+        reps = -(-k // n)  # duplicate inputs up to >= k points
+        points = np.tile(points, (reps, 1))
+        n = points.shape[0]
+    dev = nat.device()
+    X = torch.from_numpy(np.ascontiguousarray(points)).to(dev)
+    xn2 = torch.empty(n, dtype=torch.float64, device=dev)
+    nat.call("gift_rows_sqnorm_f64", nat.ptr(X), n, d, nat.ptr(xn2), nat.stream_ptr())
+    labels = torch.empty(n, dtype=torch.int32, device=dev)
+    mind2 = torch.empty(n, dtype=torch.float64, device=dev)
+
+    def assign(C, want_labels=True):
+        cn2 = torch.empty(C.shape[0], dtype=torch.float64, device=dev)
+        nat.call("gift_rows_sqnorm_f64", nat.ptr(C), C.shape[0], d, nat.ptr(cn2),
+                 nat.stream_ptr())
+        nat.call("gift_kmeans_assign", nat.ptr(X), n, d, nat.ptr(C), C.shape[0], nat.ptr(xn2),
+                 nat.ptr(cn2), nat.ptr(labels) if want_labels else None, nat.ptr(mind2),
+                 nat.stream_ptr())
+        return mind2.cpu().numpy()
+
+    # k-means++ (codebook.py:48-61)
+    rng = np.random.default_rng(seed)
+    centers = np.empty((k, d), dtype=np.float64)
+    centers[0] = points[rng.integers(0, n)]
+    closest = assign(torch.from_numpy(centers[:1].copy()).to(dev), want_labels=False)
+    for i in range(1, k):
+        total = closest.sum()
+        if total <= 0.0:
+            idx = int(rng.integers(0, n))
+        else:
+            cdf = (closest / total).cumsum()  # Generator.choice(n, p=closest / total)
+            cdf /= cdf[-1]
+            idx = int(cdf.searchsorted(rng.random(), side="right"))
+        centers[i] = points[idx]
+        np.minimum(closest, assign(torch.from_numpy(centers[i:i + 1].copy()).to(dev),
+                                   want_labels=False), out=closest)
+    # Lloyd (codebook.py:76-104)
+    C = torch.from_numpy(centers).to(dev)
+    prev_cost = None
+    for _ in range(max_iters):
+        d2min = assign(C)
+        lab = labels.cpu().numpy().astype(np.int64)
+        cost = float(d2min.sum())
+        counts = np.bincount(lab, minlength=k)
+        for empty in np.flatnonzero(counts == 0):
+            donor = int(counts.argmax())
+            members = np.flatnonzero(lab == donor)
+            dd = np.empty(len(members))
+            Cd = C[donor:donor + 1].contiguous()
+            cn2 = torch.empty(1, dtype=torch.float64, device=dev)
+            nat.call("gift_rows_sqnorm_f64", nat.ptr(Cd), 1, d, nat.ptr(cn2), nat.stream_ptr())
+            sub = X[torch.from_numpy(members).to(dev)].contiguous()
+            sub_n2 = xn2[torch.from_numpy(members).to(dev)].contiguous()
+            out = torch.empty(len(members), dtype=torch.float64, device=dev)
+            nat.call("gift_kmeans_assign", nat.ptr(sub), len(members), d, nat.ptr(Cd), 1,
+                     nat.ptr(sub_n2), nat.ptr(cn2), None, nat.ptr(out), nat.stream_ptr())
+            dd[:] = out.cpu().numpy()
+            steal = members[dd.argmax()]
+            lab[steal] = empty
+            counts[donor] -= 1
+            counts[empty] += 1
+        order = torch.from_numpy(np.argsort(lab, kind="stable")).to(dev)
+        off = torch.from_numpy(np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)).to(dev)
+        newC = torch.empty((k, d), dtype=torch.float64, device=dev)
+        nat.call("gift_kmeans_update", nat.ptr(X), n, d, nat.ptr(order), nat.ptr(off), k,
+                 nat.ptr(newC), nat.stream_ptr())
+        C = newC
+        if prev_cost is not None:
+            denom = max(prev_cost, 1e-300)
+            if abs(prev_cost - cost) / denom < CONVERGENCE_TOL:
+                break
+        prev_cost = cost
+    cb = Codebook(centroids=C.cpu().numpy().astype(np.float32), channel=channel, seed=seed)
+    if np.isnan(cb.centroids).any():
+        raise EmptyInput("k-means produced NaN centroids")
+    return cb
 
 
 def quantize(codebook: Codebook, x, ma: int = 1) -> np.ndarray:

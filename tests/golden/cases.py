@@ -67,3 +67,23 @@ EVAL_CASES = [
     ("noisy", 21, 150, 8, 32, 10, 12, 2, 6, 3, 1.2),
     ("noisy2", 22, 90, 6, 24, 6, 8, 1, 5, 2, 1.6),
 ]
+
+
+def kmeans_inputs(name):
+    """Seeded training sets for codebook training (codebook.py:64-108):
+    (features, k, seed, max_iters)."""
+    rng = np.random.default_rng({"mix": 41, "tiny": 42, "dup": 43, "wide": 44}[name])
+    if name == "mix":
+        x, _ = mixture_views(41, 40, 5, 32, 6, sigma=0.5)
+        return x.reshape(-1, 32).astype(np.float64), 8, 7, 50
+    if name == "tiny":  # fewer vectors than centers: tiled
+        return rng.random((5, 6)), 12, 3, 50
+    if name == "dup":  # exact duplicates: zero-distance draws and empty clusters
+        base = rng.random((3, 4))
+        return base[rng.integers(0, 3, 40)], 6, 11, 20
+    if name == "wide":  # d > 128: the pairwise-summed norms recurse
+        return unit_nonneg_rows(rng, 150, 300).astype(np.float64), 6, 5, 50
+    raise KeyError(name)
+
+
+KMEANS_CASES = ["mix", "tiny", "dup", "wide"]

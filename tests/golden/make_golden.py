@@ -22,7 +22,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 sys.path.insert(0, "/root/reference/pkg/src")
 
-from cases import E2E_CASES, EVAL_CASES, mixture_views, sampled_codebook, shape_ids, unit_nonneg_rows  # noqa: E402
+from cases import (E2E_CASES, EVAL_CASES, KMEANS_CASES, kmeans_inputs, mixture_views,  # noqa: E402
+                   sampled_codebook, shape_ids, unit_nonneg_rows)
 from shapesearch import codebook as rcb  # noqa: E402
 from shapesearch import features as rft  # noqa: E402
 from shapesearch import index as rix  # noqa: E402
@@ -290,6 +291,18 @@ def golden_eval():
         print("eval", name, "done")
 
 
+def golden_kmeans():
+    """Reference train_codebook (codebook.py:64-108: k-means++ seeding, Lloyd
+    iterations, empty-cluster repair) on the seeded sets of cases.py."""
+    out = {}
+    for name in KMEANS_CASES:
+        x, k, seed, iters = kmeans_inputs(name)
+        cb = rcb.train_codebook(x, k, seed=seed, max_iters=iters, channel="A")
+        out[f"{name}_centroids"] = cb.centroids
+    np.savez_compressed(os.path.join(HERE, "kmeans.npz"), **out)
+    print("kmeans done")
+
+
 def golden_ingest():
     """A GIFTFT1 file written by the reference's write_features (features.py
     :121-137) from seeded raw rows -- scales 1e-3..1e3, all-zero rows, a
@@ -320,6 +333,9 @@ if __name__ == "__main__":
     if sys.argv[1:] == ["ingest"]:
         golden_ingest()
         sys.exit(0)
+    if sys.argv[1:] == ["kmeans"]:
+        golden_kmeans()
+        sys.exit(0)
     if sys.argv[1:] == ["eval"]:
         golden_eval()
         sys.exit(0)
@@ -340,3 +356,4 @@ if __name__ == "__main__":
     golden_exact()
     golden_eval()
     golden_ingest()
+    golden_kmeans()

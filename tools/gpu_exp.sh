@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
+timeout 900 python tools/kmeans_bench.py > gpurun_out/kmeans_bench.json 2> gpurun_out/kmeans_bench.err; echo km=$?
