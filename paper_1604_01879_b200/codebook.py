@@ -76,22 +76,25 @@ def train_codebook(features, k: int, seed: int = 0, max_iters: int = DEFAULT_MAX
     two centers within a few ulps."""
     from . import _native as nat
 
-    points = np.asarray(features, dtype=np.float64)
-    if points.ndim != 2 or points.shape[0] == 0:
-        raise EmptyInput("no training vectors")
-    n, d = points.shape
-    if n < k:
-        reps = -(-k // n)  # duplicate inputs up to >= k points
-        points = np.tile(points, (reps, 1))
-        n = points.shape[0]
     dev = nat.device()
-    X = torch.from_numpy(np.ascontiguousarray(points)).to(dev)
+    if torch.is_tensor(features):  # device rows stay on the device
+        X = features.to(dev, torch.float64)
+    else:
+        X = torch.from_numpy(np.ascontiguousarray(np.asarray(features, dtype=np.float64))).to(dev)
+    if X.dim() != 2 or X.shape[0] == 0:
+        raise EmptyInput("no training vectors")
+    n, d = X.shape
+    if n < k:
+        X = X.repeat(-(-k // n), 1)  # duplicate inputs up to >= k points (np.tile)
+        n = X.shape[0]
+    X = X.contiguous()
     xn2 = torch.empty(n, dtype=torch.float64, device=dev)
     nat.call("gift_rows_sqnorm_f64", nat.ptr(X), n, d, nat.ptr(xn2), nat.stream_ptr())
     labels = torch.empty(n, dtype=torch.int32, device=dev)
     mind2 = torch.empty(n, dtype=torch.float64, device=dev)
 
     def assign(C, want_labels=True):
+        C = C.contiguous()
         cn2 = torch.empty(C.shape[0], dtype=torch.float64, device=dev)
         nat.call("gift_rows_sqnorm_f64", nat.ptr(C), C.shape[0], d, nat.ptr(cn2),
                  nat.stream_ptr())
@@ -102,9 +105,9 @@ def train_codebook(features, k: int, seed: int = 0, max_iters: int = DEFAULT_MAX
 
     # k-means++ (codebook.py:48-61)
     rng = np.random.default_rng(seed)
-    centers = np.empty((k, d), dtype=np.float64)
-    centers[0] = points[rng.integers(0, n)]
-    closest = assign(torch.from_numpy(centers[:1].copy()).to(dev), want_labels=False)
+    centers = torch.empty((k, d), dtype=torch.float64, device=dev)
+    centers[0] = X[int(rng.integers(0, n))]
+    closest = assign(centers[:1], want_labels=False)
     for i in range(1, k):
         total = closest.sum()
         if total <= 0.0:
@@ -113,11 +116,10 @@ def train_codebook(features, k: int, seed: int = 0, max_iters: int = DEFAULT_MAX
             cdf = (closest / total).cumsum()  # Generator.choice(n, p=closest / total)
             cdf /= cdf[-1]
             idx = int(cdf.searchsorted(rng.random(), side="right"))
-        centers[i] = points[idx]
-        np.minimum(closest, assign(torch.from_numpy(centers[i:i + 1].copy()).to(dev),
-                                   want_labels=False), out=closest)
+        centers[i] = X[idx]
+        np.minimum(closest, assign(centers[i:i + 1], want_labels=False), out=closest)
     # Lloyd (codebook.py:76-104)
-    C = torch.from_numpy(centers).to(dev)
+    C = centers
     prev_cost = None
     for _ in range(max_iters):
         d2min = assign(C)

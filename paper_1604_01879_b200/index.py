@@ -398,7 +398,10 @@ def build_index_from_lists(list_idx, list_scores, shape_ids, config: IndexConfig
 def build_index(manifest, config: IndexConfig = IndexConfig(), jobs: int = 1,
                 feature_files: dict | None = None, codebooks=None) -> IndexBundle:
     """index.py:146-227 from precomputed feature files ({"A": path, "B":
-    path}); mesh rendering (index.py:106-139) is outside the GPU path."""
+    path}); mesh rendering (index.py:106-139) is outside the GPU path.
+    Without `codebooks` each channel's codebook is trained like the
+    reference's (k-means over the non-zero views, codebook_size, seed) by
+    `codebook.train_codebook` on the device."""
     if isinstance(manifest, (str, Path)):
         rows = read_manifest(manifest)
     else:
@@ -435,6 +438,16 @@ def build_index(manifest, config: IndexConfig = IndexConfig(), jobs: int = 1,
         vb = ffs["B"].device_rows(sel["B"])
         if vb.shape == va.shape and torch.equal(va, vb):
             vb = None
+    if codebooks is None:
+        # index.py:186-193: k-means per channel over the non-zero views, on the device
+        codebooks = {}
+        for ch, v in (("A", va), ("B", va if vb is None else vb)):
+            if ch == "B" and vb is None:  # same rows, same seed: the same centroids
+                codebooks["B"] = cb.Codebook(codebooks["A"].centroids, "B", config.seed)
+                continue
+            rows = v.reshape(-1, v.shape[-1])
+            codebooks[ch] = cb.train_codebook(rows[rows.any(dim=1)], k=config.codebook_size,
+                                              seed=config.seed, channel=ch)
     return build_index_from_views(va, ids, config, views_b=vb, labels=labels,
                                   codebooks=codebooks)
 

@@ -303,6 +303,36 @@ def golden_kmeans():
     print("kmeans done")
 
 
+def golden_trained_bundle():
+    """Reference build_index (index.py:146-227) from two GIFTFT1 feature files
+    with no codebooks given: k-means codebooks per channel (index.py:186-193),
+    then the F-IF, self-join, re-rank and S-IF.  Saved: the feature files,
+    the manifest rows and every file of the reference's saved bundle."""
+    x, labels = mixture_views(51, 60, 6, 32, 5, sigma=0.5, zero_views=4)
+    rng = np.random.default_rng(52)
+    xb = np.abs(x + 0.05 * rng.standard_normal(x.shape)).astype(np.float32)
+    ids = shape_ids(60)
+    out = {}
+    with tempfile.TemporaryDirectory() as td:
+        paths = {}
+        for ch, feats in (("A", x), ("B", xb)):
+            paths[ch] = os.path.join(td, f"feat_{ch}.bin")
+            rft.write_features(paths[ch], [as_viewset(s, feats[i], channels=(ch,))
+                                           for i, s in enumerate(ids)], ch)
+            out[f"feat_{ch}"] = np.frombuffer(open(paths[ch], "rb").read(), dtype=np.uint8)
+        rows = [(f"/meshes/{s}.off", f"c{labels[i]}") for i, s in enumerate(ids)]
+        cfg = rix.IndexConfig(n_views=6, codebook_size=8, ma=2, k1=5, k2=2)
+        bundle = rix.build_index(rows, cfg, feature_files=paths)
+        bd = os.path.join(td, "bundle")
+        rix.save_bundle(bundle, bd)
+        for fn in sorted(os.listdir(bd)):
+            out["file:" + fn] = np.frombuffer(open(os.path.join(bd, fn), "rb").read(),
+                                              dtype=np.uint8)
+    out["labels"] = np.array([f"c{l}" for l in labels])
+    np.savez_compressed(os.path.join(HERE, "bundle_trained.npz"), **out)
+    print("trained bundle done")
+
+
 def golden_ingest():
     """A GIFTFT1 file written by the reference's write_features (features.py
     :121-137) from seeded raw rows -- scales 1e-3..1e3, all-zero rows, a
@@ -336,6 +366,9 @@ if __name__ == "__main__":
     if sys.argv[1:] == ["kmeans"]:
         golden_kmeans()
         sys.exit(0)
+    if sys.argv[1:] == ["trained"]:
+        golden_trained_bundle()
+        sys.exit(0)
     if sys.argv[1:] == ["eval"]:
         golden_eval()
         sys.exit(0)
@@ -357,3 +390,4 @@ if __name__ == "__main__":
     golden_eval()
     golden_ingest()
     golden_kmeans()
+    golden_trained_bundle()

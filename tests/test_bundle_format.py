@@ -154,3 +154,49 @@ def test_reference_bundle_loads_and_serves(case):
         out = gift.save_bundle(bundle, os.path.join(td, "again"))
         for fn in os.listdir(out):
             assert open(os.path.join(out, fn), "rb").read() == ref_files(name)[fn], fn
+
+
+@pytest.mark.gpu
+def test_build_index_trains_codebooks_like_the_reference():
+    """build_index(manifest, feature_files) without codebooks: each channel's
+    codebook is trained on the device (k-means++ / Lloyd, index.py:186-193)
+    and the saved bundle equals the reference's build_index output
+    (tests/golden/bundle_trained.npz): config, shapes, codebooks and F-IF
+    lists byte for byte; activations and S-IF on the same supports within
+    the score tolerance."""
+    import paper_1604_01879_b200 as gift
+    from paper_1604_01879_b200 import rerank as rr
+
+    g = load_golden("bundle_trained.npz")
+    files = {k[len("file:"):]: g[k].tobytes() for k in g if k.startswith("file:")}
+    labels = list(g["labels"])
+    ids = shape_ids(len(labels))
+    with tempfile.TemporaryDirectory() as td:
+        paths = {}
+        for ch in ("A", "B"):
+            paths[ch] = os.path.join(td, f"feat_{ch}.bin")
+            with open(paths[ch], "wb") as fh:
+                fh.write(g[f"feat_{ch}"].tobytes())
+        rows = [(f"/meshes/{s}.off", lab) for s, lab in zip(ids, labels)]
+        cfg = gift.IndexConfig(n_views=6, codebook_size=8, ma=2, k1=5, k2=2)
+        bundle = gift.build_index(rows, cfg, feature_files=paths)
+        out = gift.save_bundle(bundle, os.path.join(td, "gpu"))
+        got = {fn: open(os.path.join(out, fn), "rb").read() for fn in os.listdir(out)}
+        assert set(got) == set(files)
+        for fn in BYTE_EXACT:
+            assert got[fn] == files[fn], fn
+        for ch in ("A", "B"):
+            a = _parse_acts(got[f"activations_{ch}.bin"], td)
+            r = _parse_acts(files[f"activations_{ch}.bin"], td)
+            for x, y in zip(a, r, strict=True):
+                assert x.owner == y.owner
+                np.testing.assert_array_equal(x.indices, y.indices)
+                np.testing.assert_allclose(x.values, y.values, rtol=RTOL, atol=1e-12)
+        sg = rr.load_sif(write_dir({"sif.bin": got["sif.bin"]}, os.path.join(td, "s1")) +
+                         "/sif.bin")
+        sr = rr.load_sif(write_dir({"sif.bin": files["sif.bin"]}, os.path.join(td, "s2")) +
+                         "/sif.bin")
+        for o1, o2, v1, v2 in zip(sg.entry_ordinals, sr.entry_ordinals, sg.entry_values,
+                                  sr.entry_values, strict=True):
+            np.testing.assert_array_equal(o1, o2)
+            np.testing.assert_allclose(v1, v2, rtol=RTOL, atol=1e-12)

@@ -1,1 +1,1 @@
-timeout 900 python tools/kmeans_bench.py > gpurun_out/kmeans_bench.json 2> gpurun_out/kmeans_bench.err; echo km=$?
+timeout 900 python -m pytest tests/test_bundle_format.py tests/test_kmeans.py tests/test_ingest.py -q > gpurun_out/pytest_tb.log 2>&1; echo pytest=$?
