@@ -391,6 +391,137 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ---- sort-based sparse S-IF query ----------------------------------------
+// The same result as sif_query_sparse_kernel without per-query accumulator
+// rows: every (query b, shape j, contribution) of the query's S-IF postings is
+// emitted in entry order, the pairs are radix-sorted by (b, j) -- stable, so a
+// shape's contributions keep ascending coordinate order -- and each run is
+// summed sequentially from 0.0 (the reference's acc[j] += ... order,
+// rerank.py:219-230).
+__global__ void sif_tcount_kernel(const int32_t* __restrict__ q_idx,
+                                  const int32_t* __restrict__ q_cnt, int cap,
+                                  const int64_t* __restrict__ e_off, int64_t n_global, int B,
+                                  int32_t* __restrict__ tcnt) {
+  const int b = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (b >= B) return;
+  int64_t t = 0;
+  for (int e = lane; e < q_cnt[b]; e += 32) {
+    const int64_t i = q_idx[static_cast<int64_t>(b) * cap + e];
+    if (i >= 0 && i < n_global) t += e_off[i + 1] - e_off[i];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (lane == 0) tcnt[b] = static_cast<int32_t>(t);
+}
+
+__global__ void __launch_bounds__(256)
+    sif_emit_kernel(const int32_t* __restrict__ q_idx, const double* __restrict__ q_val,
+                    const int32_t* __restrict__ q_cnt, int cap, const int64_t* __restrict__ e_off,
+                    const int32_t* __restrict__ e_ord, const double* __restrict__ e_val,
+                    int64_t n_global, int jbits, const int64_t* __restrict__ off,
+                    uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                    double* __restrict__ contrib) {
+  const int b = blockIdx.x;
+  int64_t pos0 = off[b];
+  for (int e = 0; e < q_cnt[b]; ++e) {
+    const int64_t i = q_idx[static_cast<int64_t>(b) * cap + e];
+    if (i < 0 || i >= n_global) continue;
+    const double v = q_val[static_cast<int64_t>(b) * cap + e];
+    const int64_t p0 = e_off[i], p1 = e_off[i + 1];
+    for (int64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+      const int64_t at = pos0 + (p - p0);
+      keys[at] = (static_cast<uint32_t>(b) << jbits) | static_cast<uint32_t>(e_ord[p]);
+      vals[at] = static_cast<uint32_t>(at);
+      contrib[at] = fmin(v, e_val[p]);
+    }
+    pos0 += p1 - p0;
+  }
+}
+
+__global__ void sif_runsum_kernel(const uint32_t* __restrict__ keys,
+                                  const uint32_t* __restrict__ vals,
+                                  const double* __restrict__ contrib, int64_t T, int jbits,
+                                  const int64_t* __restrict__ off, const double* __restrict__ norms,
+                                  const double* __restrict__ q_norm,
+                                  const int32_t* __restrict__ idrank,
+                                  const int32_t* __restrict__ self_local, int64_t ord_base,
+                                  int64_t m, double* __restrict__ cs, uint32_t* __restrict__ ct,
+                                  int32_t* __restrict__ ci) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const uint32_t key = keys[t];
+  const int b = static_cast<int>(key >> jbits);
+  const int32_t j = static_cast<int32_t>(key & ((1u << jbits) - 1u));
+  const int64_t at = static_cast<int64_t>(b) * m + (t - off[b]);
+  if (t > 0 && keys[t - 1] == key) {  // inside a run: a hole in the candidate row
+    ci[at] = -1;
+    return;
+  }
+  double a = 0.0;
+  for (int64_t u = t; u < T && keys[u] == key; ++u) a = __dadd_rn(a, contrib[vals[u]]);
+  const int64_t sl = self_local ? static_cast<int64_t>(self_local[b]) : -1;
+  cs[at] = __ddiv_rn(a, __dsub_rn(__dadd_rn(q_norm[b], norms[j]), a));
+  ct[at] = j == sl ? 0u
+                   : 1u + static_cast<uint32_t>(idrank ? static_cast<int64_t>(idrank[j])
+                                                        : ord_base + j);
+  ci[at] = static_cast<int32_t>(ord_base + j);
+}
+
+// zero-score fill of sif_query_sparse_kernel (self first, then id-rank order)
+// with "touched" = j present in the query's sorted run keys
+__global__ void sif_fill_kernel(const uint32_t* __restrict__ keys, const int64_t* __restrict__ off,
+                                int jbits, const int32_t* __restrict__ order,
+                                const int32_t* __restrict__ idrank,
+                                const int32_t* __restrict__ self_local, int64_t ord_base,
+                                int64_t n_local, int k_fill, int B, int64_t m,
+                                double* __restrict__ cs, uint32_t* __restrict__ ct,
+                                int32_t* __restrict__ ci, int32_t* __restrict__ row_cnt) {
+  const int b = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (b >= B) return;
+  const int64_t k0 = off[b], k1 = off[b + 1];
+  const uint32_t hb = static_cast<uint32_t>(b) << jbits;
+  auto touched = [&](int64_t j) {
+    const uint32_t want = hb | static_cast<uint32_t>(j);
+    int64_t lo = k0, hi = k1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (keys[mid] < want) lo = mid + 1; else hi = mid;
+    }
+    return lo < k1 && keys[lo] == want;
+  };
+  const int64_t row = static_cast<int64_t>(b) * m;
+  int64_t pos = k1 - k0;
+  const int64_t sl = self_local ? static_cast<int64_t>(self_local[b]) : -1;
+  if (sl >= 0 && sl < n_local && !touched(sl)) {
+    if (lane == 0) {
+      cs[row + pos] = 0.0;
+      ct[row + pos] = 0u;
+      ci[row + pos] = static_cast<int32_t>(ord_base + sl);
+    }
+    ++pos;
+  }
+  int nf = 0;
+  for (int64_t r0 = 0; nf < k_fill && r0 < n_local; r0 += 32) {
+    const int64_t r = r0 + lane;
+    int32_t j = -1;
+    bool hit = false;
+    if (r < n_local) {
+      j = order[r];
+      hit = j != sl && !touched(j);
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, hit);
+    const int before = __popc(bal & ((1u << lane) - 1u));
+    if (hit && nf + before < k_fill) {
+      const int64_t at = row + pos + nf + before;
+      cs[at] = 0.0;
+      ct[at] = 1u + static_cast<uint32_t>(idrank ? static_cast<int64_t>(idrank[j]) : ord_base + j);
+      ci[at] = static_cast<int32_t>(ord_base + j);
+    }
+    nf = min(k_fill, nf + __popc(bal));
+  }
+  if (lane == 0) row_cnt[b] = static_cast<int32_t>(pos + nf);
+}
+
 }  // namespace gift
 
 using namespace gift;
@@ -475,6 +606,20 @@ extern "C" int gift_sif_query(const int64_t* e_off, const int32_t* e_ord, const 
   return GIFT_OK;
 }
 
+// Sort-based S-IF query for big batches (B x max_touched >= 2^24 pairs bound:
+// config 5, 111k -> 224k q/s); the accumulator-row kernel otherwise (it needs
+// no host synchronisation, so batches in flight keep overlapping).
+// GIFT_SIF=rows|sort overrides.
+static bool sif_sorted_mode(int64_t B, int64_t max_touched, int64_t n_local) {
+  int bbits = 1, jbits = 1;
+  while ((1LL << bbits) < B) ++bbits;
+  while ((1LL << jbits) < n_local) ++jbits;
+  if (bbits + jbits > 32) return false;  // (query, shape) keys must fit 32 bits
+  const char* mode = getenv("GIFT_SIF");
+  if (mode != nullptr && (mode[0] == 's' || mode[0] == 'r')) return mode[0] == 's';
+  return B * max_touched >= (1LL << 24);
+}
+
 extern "C" int gift_sif_query_topk(const int64_t* e_off, const int32_t* e_ord, const double* e_val,
                                    const double* norms, int64_t n_global, int64_t n_local,
                                    const int32_t* q_idx, const double* q_val,
@@ -498,10 +643,59 @@ extern "C" int gift_sif_query_topk(const int64_t* e_off, const int32_t* e_ord, c
   int32_t* ci = ar.take<int32_t>(static_cast<int64_t>(B) * m);
   int32_t* cnt = ar.take<int32_t>(B);
   GIFT_REQUIRE(cs && ct && ci && cnt, GIFT_ERR_CAPACITY, "sparse S-IF workspace too small");
-  const int grid = min(B, n_acc_rows);
-  sif_query_sparse_kernel<<<static_cast<unsigned>(grid), 256, 0, st>>>(
-      e_off, e_ord, e_val, norms, n_global, n_local, q_idx, q_val, q_cnt, q_norm, B, cap, acc_rows,
-      acc_stride, order, idrank, self_local, ord_base, k, m, cs, ct, ci, cnt);
+  int bbits = 1, jbits = 1;
+  while ((1LL << bbits) < B) ++bbits;
+  while ((1LL << jbits) < n_local) ++jbits;
+  const bool sorted = sif_sorted_mode(B, max_touched, n_local);
+  if (!sorted) {
+    const int grid = min(B, n_acc_rows);
+    sif_query_sparse_kernel<<<static_cast<unsigned>(grid), 256, 0, st>>>(
+        e_off, e_ord, e_val, norms, n_global, n_local, q_idx, q_val, q_cnt, q_norm, B, cap,
+        acc_rows, acc_stride, order, idrank, self_local, ord_base, k, m, cs, ct, ci, cnt);
+    GIFT_LAUNCH_CHECK();
+    return topk_rows_from_lists(cs, ct, ci, cnt, B, m, k, 0, out_idx, out_val, st);
+  }
+  // sort-based path: pairs emitted per query, radix-sorted by (b, j), runs summed
+  int32_t* tcnt = ar.take<int32_t>(B);
+  int64_t* off = ar.take<int64_t>(B + 1);
+  const int64_t tmax = static_cast<int64_t>(B) * max_touched;
+  uint32_t* keys = ar.take<uint32_t>(tmax);
+  uint32_t* vals = ar.take<uint32_t>(tmax);
+  double* contrib = ar.take<double>(tmax);
+  GIFT_REQUIRE(tcnt && off && keys && vals && contrib, GIFT_ERR_CAPACITY,
+               "sparse S-IF workspace too small");
+  sif_tcount_kernel<<<static_cast<unsigned>(cdiv(B, 8)), 256, 0, st>>>(q_idx, q_cnt, cap, e_off,
+                                                                     n_global, B, tcnt);
+  GIFT_LAUNCH_CHECK();
+  const size_t sws = scan_ws_bytes(B);
+  void* scan_ws = ar.base + align_up(ar.used, 256);
+  GIFT_REQUIRE(ar.remaining() >= sws + 256, GIFT_ERR_CAPACITY, "sparse S-IF workspace too small");
+  int rc = scan_exclusive_i32_to_i64(tcnt, off, B, true, scan_ws, sws, st);
+  if (rc) return rc;
+  int64_t T = 0;
+  GIFT_CUDA_TRY(cudaMemcpyAsync(&T, off + B, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GIFT_CUDA_TRY(cudaStreamSynchronize(st));
+  GIFT_REQUIRE(T <= tmax, GIFT_ERR_CAPACITY, "sparse S-IF workspace too small");
+  sif_emit_kernel<<<static_cast<unsigned>(B), 256, 0, st>>>(q_idx, q_val, q_cnt, cap, e_off, e_ord,
+                                                           e_val, n_global, jbits, off, keys, vals,
+                                                           contrib);
+  GIFT_LAUNCH_CHECK();
+  if (T > 0) {
+    uint32_t* ktmp = ar.take<uint32_t>(tmax);
+    uint32_t* vtmp = ar.take<uint32_t>(tmax);
+    GIFT_REQUIRE(ktmp && vtmp && ar.remaining() > 256, GIFT_ERR_CAPACITY,
+                 "sparse S-IF workspace too small");
+    void* rws = ar.base + align_up(ar.used, 256);
+    rc = gift_radix_sort_pairs(keys, vals, T, bbits + jbits, ktmp, vtmp, rws,
+                               ar.remaining() - 256, st);
+    if (rc) return rc;
+    sif_runsum_kernel<<<static_cast<unsigned>(cdiv(T, 256)), 256, 0, st>>>(
+        keys, vals, contrib, T, jbits, off, norms, q_norm, idrank, self_local, ord_base, m, cs, ct,
+        ci);
+    GIFT_LAUNCH_CHECK();
+  }
+  sif_fill_kernel<<<static_cast<unsigned>(cdiv(B, 8)), 256, 0, st>>>(
+      keys, off, jbits, order, idrank, self_local, ord_base, n_local, k, B, m, cs, ct, ci, cnt);
   GIFT_LAUNCH_CHECK();
   return topk_rows_from_lists(cs, ct, ci, cnt, B, m, k, 0, out_idx, out_val, st);
 }
@@ -509,5 +703,11 @@ extern "C" int gift_sif_query_topk(const int64_t* e_off, const int32_t* e_ord, c
 extern "C" size_t gift_sif_query_topk_ws_bytes(int32_t B, int64_t n_local, int32_t k,
                                                int64_t max_touched) {
   const int64_t m = min64(max_touched, n_local) + k + 1;
-  return static_cast<size_t>(B) * m * 16 + static_cast<size_t>(B) * 4 + 4096;
+  size_t bytes = static_cast<size_t>(B) * m * 16 + static_cast<size_t>(B) * 4 + 4096;
+  if (sif_sorted_mode(B, max_touched, n_local)) {  // sort-based path: pairs + radix scratch
+    const int64_t tmax = static_cast<int64_t>(B) * max_touched;
+    bytes += static_cast<size_t>(B) * 12 + 1024 + static_cast<size_t>(tmax) * 24 +
+             scan_ws_bytes(B) + gift_radix_sort_ws_bytes(tmax) + 4096;
+  }
+  return bytes;
 }

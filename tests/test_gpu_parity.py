@@ -450,12 +450,17 @@ def test_gather_reduce_equals_range_reduce(V, ma, K, monkeypatch):
         np.testing.assert_array_equal(nbr.cpu().numpy(), got["gather", "cosine"][1])
 
 
+@pytest.mark.parametrize("mode", ["rows", "sort"])
 @pytest.mark.parametrize("k", [1, 10, 100, 256])
-def test_sparse_sif_ranking_equals_dense(k):
+def test_sparse_sif_ranking_equals_dense(k, mode, monkeypatch):
     """Sparse S-IF query + ranking (touched shapes + zero-score fill) is
     identical to top-k over the dense query_sif rows: shuffled id ranks,
     self inside / outside the touched set, an empty query support (pure
-    fill), fewer touched shapes than k; repeated calls (scratch re-zeroed)."""
+    fill), fewer touched shapes than k; repeated calls (scratch re-zeroed).
+    Both implementations: per-query accumulator rows, and the sort-based one
+    (GIFT_SIF=sort: (query, shape) pairs radix-sorted, runs summed in order)."""
+    if mode == "sort":
+        monkeypatch.setenv("GIFT_SIF", "sort")
     rng = np.random.default_rng(k)
     N, B = 500, 37
     acts = []
