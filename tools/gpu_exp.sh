@@ -1,1 +1,2 @@
-timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench_c2.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1; echo ncu=$?
+timeout 1500 python bench.py --config c3 --steps 8 --no-cpu-baseline > gpurun_out/c3_def.json 2> gpurun_out/c3_def.err
+GIFT_SIF=rows timeout 1500 python bench.py --config c3 --steps 8 --no-cpu-baseline > gpurun_out/c3_rows.json 2> gpurun_out/c3_rows.err
