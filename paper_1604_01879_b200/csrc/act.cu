@@ -438,10 +438,19 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+__global__ void sif_runflag_kernel(const uint32_t* __restrict__ keys, int64_t T,
+                                   int32_t* __restrict__ flag) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t < T) flag[t] = (t == 0 || keys[t - 1] != keys[t]) ? 1 : 0;
+}
+
+// One thread per run start; rpos = exclusive scan of the run-start flags, so
+// a query's runs fill its candidate row densely.
 __global__ void sif_runsum_kernel(const uint32_t* __restrict__ keys,
                                   const uint32_t* __restrict__ vals,
                                   const double* __restrict__ contrib, int64_t T, int jbits,
-                                  const int64_t* __restrict__ off, const double* __restrict__ norms,
+                                  const int64_t* __restrict__ off, const int64_t* __restrict__ rpos,
+                                  const double* __restrict__ norms,
                                   const double* __restrict__ q_norm,
                                   const int32_t* __restrict__ idrank,
                                   const int32_t* __restrict__ self_local, int64_t ord_base,
@@ -450,13 +459,10 @@ __global__ void sif_runsum_kernel(const uint32_t* __restrict__ keys,
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= T) return;
   const uint32_t key = keys[t];
+  if (t > 0 && keys[t - 1] == key) return;  // inside a run
   const int b = static_cast<int>(key >> jbits);
   const int32_t j = static_cast<int32_t>(key & ((1u << jbits) - 1u));
-  const int64_t at = static_cast<int64_t>(b) * m + (t - off[b]);
-  if (t > 0 && keys[t - 1] == key) {  // inside a run: a hole in the candidate row
-    ci[at] = -1;
-    return;
-  }
+  const int64_t at = static_cast<int64_t>(b) * m + (rpos[t] - rpos[off[b]]);
   double a = 0.0;
   for (int64_t u = t; u < T && keys[u] == key; ++u) a = __dadd_rn(a, contrib[vals[u]]);
   const int64_t sl = self_local ? static_cast<int64_t>(self_local[b]) : -1;
@@ -470,7 +476,7 @@ __global__ void sif_runsum_kernel(const uint32_t* __restrict__ keys,
 // zero-score fill of sif_query_sparse_kernel (self first, then id-rank order)
 // with "touched" = j present in the query's sorted run keys
 __global__ void sif_fill_kernel(const uint32_t* __restrict__ keys, const int64_t* __restrict__ off,
-                                int jbits, const int32_t* __restrict__ order,
+                                const int64_t* __restrict__ rpos, int jbits, const int32_t* __restrict__ order,
                                 const int32_t* __restrict__ idrank,
                                 const int32_t* __restrict__ self_local, int64_t ord_base,
                                 int64_t n_local, int k_fill, int B, int64_t m,
@@ -490,7 +496,7 @@ __global__ void sif_fill_kernel(const uint32_t* __restrict__ keys, const int64_t
     return lo < k1 && keys[lo] == want;
   };
   const int64_t row = static_cast<int64_t>(b) * m;
-  int64_t pos = k1 - k0;
+  int64_t pos = rpos[k1] - rpos[k0];  // the query's touched shapes
   const int64_t sl = self_local ? static_cast<int64_t>(self_local[b]) : -1;
   if (sl >= 0 && sl < n_local && !touched(sl)) {
     if (lane == 0) {
@@ -662,7 +668,9 @@ extern "C" int gift_sif_query_topk(const int64_t* e_off, const int32_t* e_ord, c
   uint32_t* keys = ar.take<uint32_t>(tmax);
   uint32_t* vals = ar.take<uint32_t>(tmax);
   double* contrib = ar.take<double>(tmax);
-  GIFT_REQUIRE(tcnt && off && keys && vals && contrib, GIFT_ERR_CAPACITY,
+  int32_t* rflag = ar.take<int32_t>(tmax);
+  int64_t* rpos = ar.take<int64_t>(tmax + 1);
+  GIFT_REQUIRE(tcnt && off && keys && vals && contrib && rflag && rpos, GIFT_ERR_CAPACITY,
                "sparse S-IF workspace too small");
   sif_tcount_kernel<<<static_cast<unsigned>(cdiv(B, 8)), 256, 0, st>>>(q_idx, q_cnt, cap, e_off,
                                                                      n_global, B, tcnt);
@@ -689,13 +697,21 @@ extern "C" int gift_sif_query_topk(const int64_t* e_off, const int32_t* e_ord, c
     rc = gift_radix_sort_pairs(keys, vals, T, bbits + jbits, ktmp, vtmp, rws,
                                ar.remaining() - 256, st);
     if (rc) return rc;
-    sif_runsum_kernel<<<static_cast<unsigned>(cdiv(T, 256)), 256, 0, st>>>(
-        keys, vals, contrib, T, jbits, off, norms, q_norm, idrank, self_local, ord_base, m, cs, ct,
-        ci);
+    sif_runflag_kernel<<<static_cast<unsigned>(cdiv(T, 256)), 256, 0, st>>>(keys, T, rflag);
     GIFT_LAUNCH_CHECK();
+    rc = scan_exclusive_i32_to_i64(rflag, rpos, T, true, ar.base + align_up(ar.used, 256),
+                                   ar.remaining() - 256, st);
+    if (rc) return rc;
+    sif_runsum_kernel<<<static_cast<unsigned>(cdiv(T, 256)), 256, 0, st>>>(
+        keys, vals, contrib, T, jbits, off, rpos, norms, q_norm, idrank, self_local, ord_base, m,
+        cs, ct, ci);
+    GIFT_LAUNCH_CHECK();
+  } else {
+    GIFT_CUDA_TRY(cudaMemsetAsync(rpos, 0, sizeof(int64_t), st));
   }
   sif_fill_kernel<<<static_cast<unsigned>(cdiv(B, 8)), 256, 0, st>>>(
-      keys, off, jbits, order, idrank, self_local, ord_base, n_local, k, B, m, cs, ct, ci, cnt);
+      keys, off, rpos, jbits, order, idrank, self_local, ord_base, n_local, k, B, m, cs, ct, ci,
+      cnt);
   GIFT_LAUNCH_CHECK();
   return topk_rows_from_lists(cs, ct, ci, cnt, B, m, k, 0, out_idx, out_val, st);
 }
@@ -706,8 +722,8 @@ extern "C" size_t gift_sif_query_topk_ws_bytes(int32_t B, int64_t n_local, int32
   size_t bytes = static_cast<size_t>(B) * m * 16 + static_cast<size_t>(B) * 4 + 4096;
   if (sif_sorted_mode(B, max_touched, n_local)) {  // sort-based path: pairs + radix scratch
     const int64_t tmax = static_cast<int64_t>(B) * max_touched;
-    bytes += static_cast<size_t>(B) * 12 + 1024 + static_cast<size_t>(tmax) * 24 +
-             scan_ws_bytes(B) + gift_radix_sort_ws_bytes(tmax) + 4096;
+    bytes += static_cast<size_t>(B) * 12 + 1024 + static_cast<size_t>(tmax) * 36 + 8 +
+             scan_ws_bytes(B) + scan_ws_bytes(tmax) + gift_radix_sort_ws_bytes(tmax) + 8192;
   }
   return bytes;
 }
