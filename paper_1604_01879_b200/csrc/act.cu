@@ -438,10 +438,16 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-__global__ void sif_runflag_kernel(const uint32_t* __restrict__ keys, int64_t T,
-                                   int32_t* __restrict__ flag) {
+// run-start flags, and the contributions gathered into sorted order (one
+// independent load per thread instead of the run sums' dependent gathers)
+__global__ void sif_runflag_kernel(const uint32_t* __restrict__ keys,
+                                   const uint32_t* __restrict__ vals,
+                                   const double* __restrict__ contrib, int64_t T,
+                                   int32_t* __restrict__ flag, double* __restrict__ sorted) {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t < T) flag[t] = (t == 0 || keys[t - 1] != keys[t]) ? 1 : 0;
+  if (t >= T) return;
+  flag[t] = (t == 0 || keys[t - 1] != keys[t]) ? 1 : 0;
+  sorted[t] = contrib[vals[t]];
 }
 
 // One thread per run start; rpos = exclusive scan of the run-start flags, so
@@ -464,7 +470,7 @@ __global__ void sif_runsum_kernel(const uint32_t* __restrict__ keys,
   const int32_t j = static_cast<int32_t>(key & ((1u << jbits) - 1u));
   const int64_t at = static_cast<int64_t>(b) * m + (rpos[t] - rpos[off[b]]);
   double a = 0.0;
-  for (int64_t u = t; u < T && keys[u] == key; ++u) a = __dadd_rn(a, contrib[vals[u]]);
+  for (int64_t u = t; u < T && keys[u] == key; ++u) a = __dadd_rn(a, contrib[u]);
   const int64_t sl = self_local ? static_cast<int64_t>(self_local[b]) : -1;
   cs[at] = __ddiv_rn(a, __dsub_rn(__dadd_rn(q_norm[b], norms[j]), a));
   ct[at] = j == sl ? 0u
@@ -697,13 +703,17 @@ extern "C" int gift_sif_query_topk(const int64_t* e_off, const int32_t* e_ord, c
     rc = gift_radix_sort_pairs(keys, vals, T, bbits + jbits, ktmp, vtmp, rws,
                                ar.remaining() - 256, st);
     if (rc) return rc;
-    sif_runflag_kernel<<<static_cast<unsigned>(cdiv(T, 256)), 256, 0, st>>>(keys, T, rflag);
+    double* csorted = ar.take<double>(tmax);
+    GIFT_REQUIRE(csorted != nullptr && ar.remaining() > 256, GIFT_ERR_CAPACITY,
+                 "sparse S-IF workspace too small");
+    sif_runflag_kernel<<<static_cast<unsigned>(cdiv(T, 256)), 256, 0, st>>>(keys, vals, contrib, T,
+                                                                          rflag, csorted);
     GIFT_LAUNCH_CHECK();
     rc = scan_exclusive_i32_to_i64(rflag, rpos, T, true, ar.base + align_up(ar.used, 256),
                                    ar.remaining() - 256, st);
     if (rc) return rc;
     sif_runsum_kernel<<<static_cast<unsigned>(cdiv(T, 256)), 256, 0, st>>>(
-        keys, vals, contrib, T, jbits, off, rpos, norms, q_norm, idrank, self_local, ord_base, m,
+        keys, vals, csorted, T, jbits, off, rpos, norms, q_norm, idrank, self_local, ord_base, m,
         cs, ct, ci);
     GIFT_LAUNCH_CHECK();
   } else {
@@ -722,7 +732,7 @@ extern "C" size_t gift_sif_query_topk_ws_bytes(int32_t B, int64_t n_local, int32
   size_t bytes = static_cast<size_t>(B) * m * 16 + static_cast<size_t>(B) * 4 + 4096;
   if (sif_sorted_mode(B, max_touched, n_local)) {  // sort-based path: pairs + radix scratch
     const int64_t tmax = static_cast<int64_t>(B) * max_touched;
-    bytes += static_cast<size_t>(B) * 12 + 1024 + static_cast<size_t>(tmax) * 36 + 8 +
+    bytes += static_cast<size_t>(B) * 12 + 1024 + static_cast<size_t>(tmax) * 44 + 8 +
              scan_ws_bytes(B) + scan_ws_bytes(tmax) + gift_radix_sort_ws_bytes(tmax) + 8192;
   }
   return bytes;
