@@ -30,16 +30,6 @@ _DTYPE_CODE = {torch.float32: nat.GIFT_F32, torch.float16: nat.GIFT_F16,
                torch.float64: nat.GIFT_F64}
 
 
-# libgift kernel launches of one QueryEngine.run batch (single channel, rerank):
-# view_prep, quantize approx + select, probe count, plan, scatter, compact zero,
-# query-plane gather, tcgen05 scan, reduce (gift_fif_score) + top-k2 merge of
-# the reduce's candidates, act_mean, sparse S-IF query, final top-k merge.
-# libgift kernel launches per query batch on the single-channel fast path
-# (counted from the ncu launch lists, profiles/r01/launches_stage_*.csv):
-# view prep, 2 split-plane, approx, 2 select, count, plan, scatter, gather,
-# scan, then range reduce (ranges + reduce) or owner reduce (slot, count,
-# 4 scan kernels, owner), then top-k2, act_mean, sparse S-IF, top-k.
-LAUNCHES_PER_BATCH = {0: 17, 1: 16, 2: 22}  # by gift_fif_reduce_mode
 
 
 def _bits(n: int) -> int:
