@@ -560,7 +560,11 @@ __global__ void __launch_bounds__(RED_THREADS) fif_reduce_kernel(ReduceArgs a) {
 constexpr int GR_THREADS = 256;
 constexpr int GR_G = 4;         // queries per CTA (fewer when the grid would under-fill)
 constexpr int GR_SEGC = 4;      // shape segments cached in registers
-constexpr int GR_PC = 8;        // probed cells of a shape kept for the slot lookups
+// probed cells of a shape kept in registers for the slot lookups: 16 with
+// many slots (config 3: 0.83 -> 0.65 ms), 8 with one slot word (config 4,
+// where 16 spills: 2.1 -> 2.7 ms)
+template <int W>
+__host__ __device__ constexpr int gr_pc() { return W >= 2 ? 16 : 8; }
 constexpr int GR_MAXK = 16384;  // cells covered by the shared-memory bitmap
 constexpr int GR_RS_SMALL = 256, GR_RS_LARGE = 1024;
 
@@ -732,6 +736,7 @@ __device__ __forceinline__ double pair_acc(const GatherArgs& a, const GrTabs& t,
   for (int w = 0; w < W; ++w) U[w] = 0u;
   // the shape's probed cells and their segments, kept in registers for the
   // per-bit lookups below (GR_PC of them; more fall back to a global search)
+  constexpr int GR_PC = gr_pc<W>();
   int pc[GR_PC];
   int32_t ps[GR_PC];
   int npc = 0;
