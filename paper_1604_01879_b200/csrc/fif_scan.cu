@@ -941,10 +941,12 @@ __global__ void owner_count_kernel(const int32_t* __restrict__ cells,
 // the top-k2 merge downstream takes OWN_WARPS times more candidates)
 constexpr int OWN_WARPS = GR_THREADS / 32;
 
-// Latency-bound (dependent gathers per pair): 4 CTAs per SM (64 registers,
-// some spills) measured faster than 2 (config 4: 3.3 -> 2.1 ms per batch).
+// Latency-bound (dependent gathers per pair): 4 CTAs per SM with one slot
+// word (64 registers, some spills; config 4: 3.3 -> 2.1 ms per batch), 3 with
+// more (80 registers for the larger probed-cell cache; config 3: 0.69 ->
+// 0.59 ms).
 template <int W>
-__global__ void __launch_bounds__(GR_THREADS, 4) fif_owner_reduce_kernel(GatherArgs a) {
+__global__ void __launch_bounds__(GR_THREADS, W >= 2 ? 3 : 4) fif_owner_reduce_kernel(GatherArgs a) {
   extern __shared__ __align__(16) double s_tab[];
   if (a.meta[M_OVERFLOW]) return;
   const int slots = a.V * a.ma;
