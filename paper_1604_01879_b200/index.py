@@ -559,7 +559,7 @@ def query_batch(bundle: IndexBundle, views, top_k: int = 10, rerank: bool = True
 
 
 _LANES: dict = {}
-LANE_RESERVE_SMS = 20  # config 2, 4 lanes: 40.6k -> 42.7k q/s (tools/lane_trace.py)
+LANE_RESERVE_SMS = 44  # config 2, 4 lanes, 3 runs each: 0 SMs ~40.6k, 20 41.2k, 28 41.9k, 36-64 42.2-42.5k q/s
 
 
 def lane_streams(n: int) -> list:
