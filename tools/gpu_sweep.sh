@@ -1,1 +1,1 @@
-for rep in 1 2 3; do for r in 52 64; do timeout 600 python bench.py --no-cpu-baseline --reserve-sms $r > gpurun_out/sw_r${r}_$rep.json 2>/dev/null; done; done
+for rep in 1 2 3; do for l in 4 6; do timeout 600 python bench.py --no-cpu-baseline --lanes $l > gpurun_out/sw_l${l}_$rep.json 2>/dev/null; done; done
