@@ -1,1 +1,3 @@
-for rep in 1 2 3; do for l in 4 6; do timeout 600 python bench.py --no-cpu-baseline --lanes $l > gpurun_out/sw_l${l}_$rep.json 2>/dev/null; done; done
+timeout 1500 python bench.py --config c3 --steps 8 --no-cpu-baseline --lanes 1 > gpurun_out/c3_l1.json 2>/dev/null
+timeout 1500 python bench.py --config c3 --steps 8 --no-cpu-baseline --lanes 2 --reserve-sms 44 > gpurun_out/c3_l2r44.json 2>/dev/null
+timeout 1500 python bench.py --config c3 --steps 8 --no-cpu-baseline --lanes 3 --reserve-sms 44 > gpurun_out/c3_l3r44.json 2>/dev/null
