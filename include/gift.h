@@ -54,6 +54,26 @@ extern "C" {
 /* flags bits 8-15: SMs the F-IF scan leaves to the kernels of other query
  * batches in flight on other streams (0: one persistent scan CTA per SM) */
 #define GIFT_FIF_RESERVE_SMS(n) (((n) & 255) << 8)
+/* Kernel variants (all bit-identical or within the same 1e-5 contract; the
+ * defaults are the measured-fastest per index).  Selected by
+ * the caller through the view -- the library reads no environment.        */
+#define GIFT_FIF_SCAN_SIMT (1 << 16)   /* CUDA-core scan instead of tcgen05   */
+#define GIFT_FIF_QUANT_SIMT (1 << 17)  /* CUDA-core quantize stage 1          */
+#define GIFT_FIF_REDUCE_SHIFT 18       /* bits 18-19: view-best reduce:       */
+#define GIFT_FIF_REDUCE_AUTO 0         /*   by shard size (owner >= 32k)      */
+#define GIFT_FIF_REDUCE_RANGE 1
+#define GIFT_FIF_REDUCE_GATHER 2
+#define GIFT_FIF_REDUCE_OWNER 3
+#define GIFT_FIF_REDUCE(m) (((m) & 3) << GIFT_FIF_REDUCE_SHIFT)
+#define GIFT_FIF_SCHED_STATIC (1 << 20) /* static CTA stride over scan items   */
+#define GIFT_FIF_PAIR_SHIFT 21          /* bits 21-22: cta_group::2 scan:      */
+#define GIFT_FIF_PAIR_AUTO 0            /*   pairs iff the f32 lo plane exists */
+#define GIFT_FIF_PAIR_OFF 1
+#define GIFT_FIF_PAIR_ON 2
+#define GIFT_FIF_PAIR(m) (((m) & 3) << GIFT_FIF_PAIR_SHIFT)
+#define GIFT_FIF_DRAIN_SHIFT 24         /* bits 24-26: D1 drain interval in    */
+#define GIFT_FIF_DRAIN_KB(n) (((n) & 7) << GIFT_FIF_DRAIN_SHIFT) /* k-blocks, */
+                                        /* 1..4 (0 = 4); > 4 is rejected       */
 
 typedef struct gift_fif_view {
   int32_t K;                 /* codebook size                                 */
@@ -62,7 +82,7 @@ typedef struct gift_fif_view {
   int32_t flags;             /* GIFT_FIF_TILED_SEGMENTS: no segment is longer   */
                              /* than a scan tile (every compact entry is       */
                              /* written once; no zero-fill needed);            */
-                             /* GIFT_FIF_RESERVE_SMS(n)                        */
+                             /* GIFT_FIF_RESERVE_SMS(n); kernel variants below */
   int64_t n_postings;        /* P                                             */
   int64_t n_segments;        /* S: (cell, shape) runs                          */
   int64_t n_tiles;           /* T: scan tiles (whole segments, <= tile_n)     */
@@ -91,10 +111,6 @@ typedef struct gift_fif_view {
   const int32_t* shape_seg;     /* [S] global segment index, ascending cell   */
   const int32_t* shape_seg_cell;/* [S] cell of segment shape_seg[g]           */
   int64_t max_cell_segments;    /* max over cells of its segment count         */
-  /* compressed tile store of the planes (optional, f32 storage; NULL: the   */
-  /* scan reads the dense planes), built by gift_cts_build                   */
-  const uint8_t* cts;
-  const int64_t* cts_off;       /* [n_tiles * d/64 + 1] block byte offsets     */
 } gift_fif_view;
 
 /* ---- library ---- */
@@ -117,19 +133,14 @@ int gift_quantize(const void* X, int32_t xdtype, int64_t n, int32_t d,
                   double cmax_norm, int32_t ma, const uint8_t* nz,
                   int32_t zero_key, int32_t* out_idx, void* ws,
                   size_t ws_bytes, void* stream);
-
-/* ---- compressed tile store of the f32 planes (scan input for HBM-bound
- * indexes): per (scan tile, 64-wide k-block) a block of row masks, row value
- * offsets and the non-zero (hi, lo) pairs, 128-byte aligned.  Call with
- * out == NULL to write block_off (sizes scanned to offsets, block_off[T*nkb]
- * = total bytes), then with out (>= total bytes) to fill the blocks.  The
- * scan uses the store when every block fits gift_cts_stage_limit() bytes. */
-size_t gift_cts_ws_bytes(int64_t n_tiles, int32_t d);
-int gift_cts_build(const void* feat_hi, const void* feat_lo, int64_t n_postings,
-                   int32_t d, const int32_t* tile_pstart, const int32_t* tile_pend,
-                   int64_t n_tiles, int64_t* block_off, void* out, void* ws,
-                   size_t ws_bytes, void* stream);
-int gift_cts_stage_limit(void);
+/* gift_quantize with explicit stage-1 selection: flags = 0 (tensor cores
+ * when d % 8 == 0) or GIFT_QUANT_SIMT (CUDA cores); same results. */
+#define GIFT_QUANT_SIMT 1
+int gift_quantize_ex(const void* X, int32_t xdtype, int64_t n, int32_t d,
+                     const float* C, const double* cnorm2, int32_t K,
+                     double cmax_norm, int32_t ma, const uint8_t* nz,
+                     int32_t zero_key, int32_t* out_idx, void* ws,
+                     size_t ws_bytes, int32_t flags, void* stream);
 
 /* GIFTFT1 ingest: out[r, :] = f32(x[r, :] / norms[r]) (IEEE f64 division),
  * rows with norms[r] == 0 copied unchanged -- features.py:67-71 `_unit`, the
@@ -348,8 +359,13 @@ int gift_sif_query(const int64_t* e_off, const int32_t* e_ord,
  * power of two keeps the rows' hot entries on different DRAM channels).  order[r] = local shape of id rank r (inverse of idrank).
  * max_touched: an upper bound of the shapes one query can touch (support cap
  * x the longest S-IF entry). */
+/* flags: 0 = by batch size (the sort-based path for B x max_touched >= 2^24),
+ * GIFT_SIF_ROWS = per-query accumulator rows, GIFT_SIF_SORT = sort-based
+ * (identical results) */
+#define GIFT_SIF_ROWS 1
+#define GIFT_SIF_SORT 2
 size_t gift_sif_query_topk_ws_bytes(int32_t B, int64_t n_local, int32_t k,
-                                    int64_t max_touched);
+                                    int64_t max_touched, int32_t flags);
 int gift_sif_query_topk(const int64_t* e_off, const int32_t* e_ord,
                         const double* e_val, const double* norms,
                         int64_t n_global, int64_t n_local, const int32_t* q_idx,
@@ -360,7 +376,7 @@ int gift_sif_query_topk(const int64_t* e_off, const int32_t* e_ord,
                         const int32_t* idrank,
                         const int32_t* self_local, int64_t ord_base, int32_t k,
                         int64_t max_touched, int32_t* out_idx, double* out_val,
-                        void* ws, size_t ws_bytes, void* stream);
+                        void* ws, size_t ws_bytes, int32_t flags, void* stream);
 
 #ifdef __cplusplus
 }

@@ -21,11 +21,25 @@ LIB_PATH = os.path.join(_HERE, "libgift.so")
 GIFT_F32, GIFT_F16, GIFT_F64 = 0, 1, 2
 SIM_COSINE, SIM_GAUSSIAN = 0, 1
 FIF_TILED_SEGMENTS = 1  # gift_fif_view.flags (include/gift.h)
+# kernel variants selected through gift_fif_view.flags (include/gift.h)
+FIF_SCAN_SIMT = 1 << 16
+FIF_QUANT_SIMT = 1 << 17
+FIF_REDUCE = {"auto": 0, "range": 1 << 18, "gather": 2 << 18, "owner": 3 << 18}
+FIF_SCHED_STATIC = 1 << 20
+FIF_PAIR = {"auto": 0, "off": 1 << 21, "on": 2 << 21}
+FIF_VARIANT_MASK = (1 << 16) | (1 << 17) | (3 << 18) | (1 << 20) | (3 << 21) | (7 << 24)
+QUANT_SIMT = 1        # gift_quantize_ex flags
+SIF_ROWS, SIF_SORT = 1, 2  # gift_sif_query_topk flags
 
 
 def fif_reserve_sms(n: int) -> int:
     """GIFT_FIF_RESERVE_SMS(n): flags bits 8-15."""
     return (int(n) & 255) << 8
+
+
+def fif_drain_kb(n: int) -> int:
+    """GIFT_FIF_DRAIN_KB(n): flags bits 24-26 (1..4; 0 = the default 4)."""
+    return (int(n) & 7) << 24
 
 _c_i32 = ctypes.c_int32
 _c_i64 = ctypes.c_int64
@@ -48,7 +62,6 @@ class FifView(ctypes.Structure):
         ("feat_hi", _c_p), ("feat_lo", _c_p),
         ("shape_seg_off", _c_p), ("shape_seg", _c_p), ("shape_seg_cell", _c_p),
         ("max_cell_segments", _c_i64),
-        ("cts", _c_p), ("cts_off", _c_p),
     ]
 
 
@@ -59,6 +72,8 @@ _SIGS = {
     "gift_quantize_ws_bytes": (_c_sz, [_c_i64, _c_i32, _c_i32, _c_i32]),
     "gift_quantize": (_c_i32, [_c_p, _c_i32, _c_i64, _c_i32, _c_p, _c_p, _c_i32, _c_dbl, _c_i32,
                                _c_p, _c_i32, _c_p, _c_p, _c_sz, _c_p]),
+    "gift_quantize_ex": (_c_i32, [_c_p, _c_i32, _c_i64, _c_i32, _c_p, _c_p, _c_i32, _c_dbl,
+                                  _c_i32, _c_p, _c_i32, _c_p, _c_p, _c_sz, _c_i32, _c_p]),
     "gift_rows_sqnorm_f64": (_c_i32, [_c_p, _c_i64, _c_i32, _c_p, _c_p]),
     "gift_kmeans_assign": (_c_i32, [_c_p, _c_i64, _c_i32, _c_p, _c_i32, _c_p, _c_p, _c_p, _c_p,
                                     _c_p]),
@@ -87,10 +102,6 @@ _SIGS = {
     "gift_fif_score_ex": (_c_i32, [ctypes.POINTER(FifView), _c_p, _c_i32, _c_i32, _c_p, _c_i32,
                                    _c_i32, _c_dbl, _c_p, _c_p, _c_sz, _c_p, _c_p, _c_p]),
     "gift_fif_score_ranges": (_c_i32, [ctypes.POINTER(FifView), _c_i32]),
-    "gift_cts_ws_bytes": (_c_sz, [_c_i64, _c_i32]),
-    "gift_cts_build": (_c_i32, [_c_p, _c_p, _c_i64, _c_i32, _c_p, _c_p, _c_i64, _c_p, _c_p, _c_p,
-                                _c_sz, _c_p]),
-    "gift_cts_stage_limit": (_c_i32, []),
     "gift_fif_score_ranges2": (_c_i32, [ctypes.POINTER(FifView), _c_i32, _c_i32]),
     "gift_fif_reduce_mode": (_c_i32, [ctypes.POINTER(FifView), _c_i32, _c_i32]),
     "gift_fif_score_ex2": (_c_i32, [ctypes.POINTER(FifView), _c_p, _c_i32, _c_i32, _c_p, _c_i32,
@@ -113,10 +124,11 @@ _SIGS = {
     "gift_sif_permute": (_c_i32, [_c_p, _c_p, _c_p, _c_i64, _c_p, _c_p, _c_p]),
     "gift_sif_query": (_c_i32, [_c_p, _c_p, _c_p, _c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p,
                                 _c_i32, _c_i32, _c_p, _c_p]),
-    "gift_sif_query_topk_ws_bytes": (_c_sz, [_c_i32, _c_i64, _c_i32, _c_i64]),
+    "gift_sif_query_topk_ws_bytes": (_c_sz, [_c_i32, _c_i64, _c_i32, _c_i64, _c_i32]),
     "gift_sif_query_topk": (_c_i32, [_c_p, _c_p, _c_p, _c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p,
                                      _c_p, _c_i32, _c_i32, _c_p, _c_i32, _c_i64, _c_p, _c_p, _c_p,
-                                     _c_i64, _c_i32, _c_i64, _c_p, _c_p, _c_p, _c_sz, _c_p]),
+                                     _c_i64, _c_i32, _c_i64, _c_p, _c_p, _c_p, _c_sz, _c_i32,
+                                     _c_p]),
 }
 
 EXPORTED = tuple(_SIGS)

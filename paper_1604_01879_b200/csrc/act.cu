@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(AM_WARPS * 32)
   __shared__ double s_val[AM_WARPS][AM_MAX_E];
   __shared__ int16_t s_lst[AM_WARPS][AM_MAX_E];
   __shared__ int32_t s_first[AM_WARPS][AM_MAX_E];
-  __shared__ int32_t s_off[AM_WARPS][MAX_NBR + 1];
+  __shared__ int32_t s_off[AM_WARPS][MAX_NBR + 2];  // list ends [0, nl], nl at MAX_NBR + 1
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t b = static_cast<int64_t>(blockIdx.x) * AM_WARPS + warp;
   if (b >= B) return;
@@ -104,10 +104,10 @@ __global__ void __launch_bounds__(AM_WARPS * 32)
       e += raw_cnt[q];
       off[++nl] = e;
     }
-    off[MAX_NBR] = nl;
+    off[MAX_NBR + 1] = nl;
   }
   __syncwarp();
-  const int nl = off[MAX_NBR];
+  const int nl = off[MAX_NBR + 1];
   const int E = off[nl];
   // stage the lists (list order = neighbour order)
   for (int t = 0, tt = 0; t < k2; ++t) {
@@ -621,14 +621,14 @@ extern "C" int gift_sif_query(const int64_t* e_off, const int32_t* e_ord, const 
 // Sort-based S-IF query for big batches (B x max_touched >= 2^24 pairs bound:
 // config 5, 111k -> 224k q/s); the accumulator-row kernel otherwise (it needs
 // no host synchronisation, so batches in flight keep overlapping).
-// GIFT_SIF=rows|sort overrides.
-static bool sif_sorted_mode(int64_t B, int64_t max_touched, int64_t n_local) {
+// flags GIFT_SIF_ROWS / GIFT_SIF_SORT override.
+static bool sif_sorted_mode(int64_t B, int64_t max_touched, int64_t n_local, int32_t flags) {
   int bbits = 1, jbits = 1;
   while ((1LL << bbits) < B) ++bbits;
   while ((1LL << jbits) < n_local) ++jbits;
   if (bbits + jbits > 32) return false;  // (query, shape) keys must fit 32 bits
-  const char* mode = getenv("GIFT_SIF");
-  if (mode != nullptr && (mode[0] == 's' || mode[0] == 'r')) return mode[0] == 's';
+  if (flags & GIFT_SIF_ROWS) return false;
+  if (flags & GIFT_SIF_SORT) return true;
   return B * max_touched >= (1LL << 24);
 }
 
@@ -641,8 +641,11 @@ extern "C" int gift_sif_query_topk(const int64_t* e_off, const int32_t* e_ord, c
                                    const int32_t* idrank,
                                    const int32_t* self_local, int64_t ord_base, int32_t k,
                                    int64_t max_touched, int32_t* out_idx, double* out_val,
-                                   void* ws, size_t ws_bytes, void* stream) {
+                                   void* ws, size_t ws_bytes, int32_t flags, void* stream) {
   cudaStream_t st = as_stream(stream);
+  GIFT_REQUIRE((flags & ~(GIFT_SIF_ROWS | GIFT_SIF_SORT)) == 0 &&
+                   flags != (GIFT_SIF_ROWS | GIFT_SIF_SORT),
+               GIFT_ERR_INVALID, "bad S-IF query flags 0x%x", flags);
   GIFT_REQUIRE(k >= 1 && k <= 256, GIFT_ERR_UNSUPPORTED, "k = %d outside [1, 256]", k);
   GIFT_REQUIRE(n_acc_rows >= 1 && acc_rows != nullptr && order != nullptr, GIFT_ERR_INVALID,
                "sparse S-IF query needs accumulator rows and the id-rank order");
@@ -658,7 +661,7 @@ extern "C" int gift_sif_query_topk(const int64_t* e_off, const int32_t* e_ord, c
   int bbits = 1, jbits = 1;
   while ((1LL << bbits) < B) ++bbits;
   while ((1LL << jbits) < n_local) ++jbits;
-  const bool sorted = sif_sorted_mode(B, max_touched, n_local);
+  const bool sorted = sif_sorted_mode(B, max_touched, n_local, flags);
   if (!sorted) {
     const int grid = min(B, n_acc_rows);
     sif_query_sparse_kernel<<<static_cast<unsigned>(grid), 256, 0, st>>>(
@@ -727,10 +730,10 @@ extern "C" int gift_sif_query_topk(const int64_t* e_off, const int32_t* e_ord, c
 }
 
 extern "C" size_t gift_sif_query_topk_ws_bytes(int32_t B, int64_t n_local, int32_t k,
-                                               int64_t max_touched) {
+                                               int64_t max_touched, int32_t flags) {
   const int64_t m = min64(max_touched, n_local) + k + 1;
   size_t bytes = static_cast<size_t>(B) * m * 16 + static_cast<size_t>(B) * 4 + 4096;
-  if (sif_sorted_mode(B, max_touched, n_local)) {  // sort-based path: pairs + radix scratch
+  if (sif_sorted_mode(B, max_touched, n_local, flags)) {  // sort-based path: pairs + radix scratch
     const int64_t tmax = static_cast<int64_t>(B) * max_touched;
     bytes += static_cast<size_t>(B) * 12 + 1024 + static_cast<size_t>(tmax) * 44 + 8 +
              scan_ws_bytes(B) + scan_ws_bytes(tmax) + gift_radix_sort_ws_bytes(tmax) + 8192;

@@ -329,127 +329,3 @@ extern "C" int gift_fif_tiles(const int64_t* cell_off, const int64_t* seg_off,
   }
   return GIFT_OK;
 }
-
-namespace gift {
-
-// ---------------------------------------------------------------------------
-// Compressed tile store (CTS) of the tensor-core planes.
-//
-// The f32 view features are ReLU outputs (configs 2/3: ~60% exact zeros) and
-// the f32 scan is HBM-bound, so the scan reads the planes in a lossless sparse
-// form and expands them in shared memory.  One block per (scan tile t,
-// 64-wide k-block kb), 128 rows (tile rows past the tile's end are empty):
-//   [0, 1024)     u64 mask per row: bit c <=> element kb*64+c of the row is
-//                 non-zero in the hi or the lo plane
-//   [1024, 1280)  u16 per row: start of the row's values, in 16-byte units
-//                 from the values area
-//   [1280, ...)   per row, its non-zero elements in ascending column order as
-//                 (hi, lo) half2 pairs, each row padded to 16 bytes
-// Blocks are 128-byte aligned; block_off[t * nkb + kb] is the byte offset,
-// block_off[T * nkb] the total.  Decompression reproduces the dense planes
-// bit for bit (zeros are +0 in both planes of a dense zero element).
-constexpr int CTS_ROWS = 128;
-constexpr int CTS_HDR = CTS_ROWS * 8 + CTS_ROWS * 2;  // 1280
-
-__device__ __forceinline__ uint64_t cts_row_mask(const __half* __restrict__ hi,
-                                                 const __half* __restrict__ lo, int64_t row,
-                                                 int d, int kb) {
-  const uint4* h4 = reinterpret_cast<const uint4*>(hi + row * d + kb * 64);
-  const uint4* l4 = reinterpret_cast<const uint4*>(lo + row * d + kb * 64);
-  uint64_t m = 0;
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const uint4 a = h4[q], b = l4[q];
-    const uint32_t w[4] = {a.x | b.x, a.y | b.y, a.z | b.z, a.w | b.w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      // two halves per word; -0.0 (0x8000) counts as non-zero: bit-exact planes
-      if (w[e] & 0xffffu) m |= 1ull << (q * 8 + e * 2);
-      if (w[e] >> 16) m |= 1ull << (q * 8 + e * 2 + 1);
-    }
-  }
-  return m;
-}
-
-// Pass 1 (emit == false): block sizes.  Pass 2: the blocks.  One CTA of 128
-// threads per (tile, kb); thread r = row r.
-__global__ void __launch_bounds__(CTS_ROWS)
-    cts_build_kernel(const __half* __restrict__ hi, const __half* __restrict__ lo, int d,
-                     int nkb, const int32_t* __restrict__ t_pstart,
-                     const int32_t* __restrict__ t_pend, int64_t* __restrict__ block_size_or_off,
-                     bool emit, uint8_t* __restrict__ out) {
-  __shared__ int s_units[CTS_ROWS];
-  const int64_t blk = blockIdx.x;
-  const int64_t t = blk / nkb;
-  const int kb = static_cast<int>(blk - t * nkb);
-  const int r = threadIdx.x;
-  const int64_t p0 = t_pstart[t], p1 = t_pend[t];
-  const int64_t row = p0 + r;
-  const uint64_t m = row < p1 ? cts_row_mask(hi, lo, row, d, kb) : 0ull;
-  const int units = (__popcll(m) * 4 + 15) / 16;
-  // exclusive scan of the rows' 16-byte units (128 threads)
-  s_units[r] = units;
-  __syncthreads();
-  for (int o = 1; o < CTS_ROWS; o <<= 1) {
-    const int v = r >= o ? s_units[r - o] : 0;
-    __syncthreads();
-    s_units[r] += v;
-    __syncthreads();
-  }
-  const int incl = s_units[r];
-  const int total = s_units[CTS_ROWS - 1];
-  if (!emit) {
-    if (r == 0) block_size_or_off[blk] = (CTS_HDR + 16 * total + 127) / 128 * 128;
-    return;
-  }
-  uint8_t* b = out + block_size_or_off[blk];
-  reinterpret_cast<uint64_t*>(b)[r] = m;
-  reinterpret_cast<uint16_t*>(b + CTS_ROWS * 8)[r] = static_cast<uint16_t>(incl - units);
-  uint32_t* v = reinterpret_cast<uint32_t*>(b + CTS_HDR + 16 * (incl - units));
-  const __half* h = hi + row * d + kb * 64;
-  const __half* l = lo + row * d + kb * 64;
-  int n = 0;
-  for (int c = 0; c < 64; ++c) {
-    if ((m >> c) & 1ull) {
-      const uint32_t hv = __half_as_ushort(h[c]), lv = __half_as_ushort(l[c]);
-      v[n++] = hv | (lv << 16);
-    }
-  }
-  for (; n < units * 4; ++n) v[n] = 0u;  // row padding
-}
-
-}  // namespace gift
-
-using namespace gift;
-
-extern "C" int gift_cts_build(const void* feat_hi, const void* feat_lo, int64_t n_postings,
-                              int32_t d, const int32_t* tile_pstart, const int32_t* tile_pend,
-                              int64_t n_tiles, int64_t* block_off, void* out, void* ws,
-                              size_t ws_bytes, void* stream) {
-  cudaStream_t st = as_stream(stream);
-  GIFT_REQUIRE(d % 64 == 0, GIFT_ERR_UNSUPPORTED, "compressed tiles need d %% 64 == 0");
-  GIFT_REQUIRE(feat_hi != nullptr && feat_lo != nullptr, GIFT_ERR_INVALID, "planes required");
-  (void)n_postings;
-  const int nkb = d / 64;
-  const int64_t nblk = n_tiles * nkb;
-  if (nblk <= 0) {
-    GIFT_CUDA_TRY(cudaMemsetAsync(block_off, 0, sizeof(int64_t), st));
-    return GIFT_OK;
-  }
-  const __half* hi = static_cast<const __half*>(feat_hi);
-  const __half* lo = static_cast<const __half*>(feat_lo);
-  if (out == nullptr) {  // sizes -> offsets (block_off[nblk] = total bytes)
-    cts_build_kernel<<<static_cast<unsigned>(nblk), CTS_ROWS, 0, st>>>(
-        hi, lo, d, nkb, tile_pstart, tile_pend, block_off, false, nullptr);
-    GIFT_LAUNCH_CHECK();
-    return scan_exclusive_i64(block_off, block_off, nblk, true, ws, ws_bytes, st);
-  }
-  cts_build_kernel<<<static_cast<unsigned>(nblk), CTS_ROWS, 0, st>>>(
-      hi, lo, d, nkb, tile_pstart, tile_pend, block_off, true, static_cast<uint8_t*>(out));
-  GIFT_LAUNCH_CHECK();
-  return GIFT_OK;
-}
-
-extern "C" size_t gift_cts_ws_bytes(int64_t n_tiles, int32_t d) {
-  return scan_ws_bytes(n_tiles * (d / 64) + 1) + 4096;
-}

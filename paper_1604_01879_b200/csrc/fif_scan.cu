@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(PLAN_THREADS)
     meta[M_OUT_TOTAL] = tot_out;
     meta[M_OVERFLOW] = tot_out > capacity ? 1 : 0;
     meta[M_WORK] = 0;
+    meta[M_QLO] = 0;  // set by the probe gather when a query lo plane is non-zero
   }
 }
 
@@ -1058,8 +1059,7 @@ struct ScoreWs {
 };
 
 bool use_tc(const gift_fif_view* f) {
-  const char* e = getenv("GIFT_SCAN");
-  if (e != nullptr && e[0] == 's') return false;  // GIFT_SCAN=simt forces the CUDA-core scan
+  if (f->flags & GIFT_FIF_SCAN_SIMT) return false;  // the CUDA-core scan, by request
   return tc_supported(f);
 }
 
@@ -1082,7 +1082,7 @@ int gather_words(const gift_fif_view* f, int V, int ma) {
   return slots <= 32 ? 1 : slots <= 64 ? 2 : 4;
 }
 
-// GIFT_REDUCE=range|gather|owner forces one reduce.  Default: the owner
+// GIFT_FIF_REDUCE(m) in the view flags forces one reduce.  Default: the owner
 // reduce (touched pairs only) on large shards, whose per-range [V x rs]
 // tiles cost B * N * V: measured 4.1 vs 28 ms on config 4 (1M shapes),
 // 1.2 vs 3.1 ms on config 3 (100k); the per-range reduce on small shards
@@ -1092,10 +1092,12 @@ constexpr int64_t OWNER_MIN_SHAPES = 32768;
 int reduce_mode(const gift_fif_view* f, int V, int ma) {
   const int W = gather_words(f, V, ma);
   if (W == 0) return RM_RANGE;
-  const char* e = getenv("GIFT_REDUCE");
-  if (e != nullptr && e[0] == 'r') return RM_RANGE;
-  if (e != nullptr && e[0] == 'g') return RM_GATHER;
-  if (e != nullptr && e[0] == 'o') return RM_OWNER;
+  switch ((f->flags >> GIFT_FIF_REDUCE_SHIFT) & 3) {
+    case GIFT_FIF_REDUCE_RANGE: return RM_RANGE;
+    case GIFT_FIF_REDUCE_GATHER: return RM_GATHER;
+    case GIFT_FIF_REDUCE_OWNER: return RM_OWNER;
+    default: break;
+  }
   return f->n_local >= OWNER_MIN_SHAPES ? RM_OWNER : RM_RANGE;
 }
 
@@ -1205,6 +1207,8 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
                "out_scores may be NULL only with cand_k > 0");
   cudaStream_t st = as_stream(stream);
   GIFT_REQUIRE(f != nullptr, GIFT_ERR_INVALID, "null index");
+  GIFT_REQUIRE(((f->flags >> GIFT_FIF_DRAIN_SHIFT) & 7) <= 4, GIFT_ERR_INVALID,
+               "drain interval %d > 4 k-blocks", (f->flags >> GIFT_FIF_DRAIN_SHIFT) & 7);
   GIFT_REQUIRE(ma >= 1 && ma <= f->K, GIFT_ERR_INVALID, "ma must be in [1, %d]", f->K);
   GIFT_REQUIRE(mode == GIFT_SIM_COSINE || mode == GIFT_SIM_GAUSSIAN, GIFT_ERR_INVALID, "bad mode");
   GIFT_REQUIRE(mode != GIFT_SIM_GAUSSIAN || sigma > 0, GIFT_ERR_INVALID, "sigma must be > 0");
@@ -1224,7 +1228,8 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
   int rc = gift_view_prep(Q, GIFT_F32, nviews, d, w.nz, w.qn2, stream);
   if (rc) return rc;
   rc = quantize_impl(Q, GIFT_F32, nviews, d, f->centroids, f->cnorm2, K, f->cmax_norm, ma, w.nz,
-                     -1, w.cells, w.qws, w.qws_bytes, stream, false, w.qn2);
+                     -1, w.cells, w.qws, w.qws_bytes, stream, false, w.qn2,
+                     !(f->flags & GIFT_FIF_QUANT_SIMT));
   if (rc) return rc;
   GIFT_CUDA_TRY(cudaMemsetAsync(w.counts, 0, sizeof(int32_t) * K, st));
   probe_count_kernel<<<static_cast<unsigned>(cdiv(nprobes, 256)), 256, 0, st>>>(w.cells, nprobes,
@@ -1268,18 +1273,11 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
     ta.mode = mode;
     ta.inv_sigma2 = mode == GIFT_SIM_GAUSSIAN ? static_cast<float>(1.0 / (sigma * sigma)) : 0.f;
     ta.has_lo = 0;
-    const char* ck = getenv("GIFT_TC_CHUNK_KB");
-    ta.chunk_kb = ck ? atoi(ck) : 4;
-    const char* mo = getenv("GIFT_TC_ORDER");
-    ta.mt_major = (mo != nullptr && mo[0] == 'm') ? 1 : 0;
-    const char* sched = getenv("GIFT_TC_SCHED");
-    ta.dyn = (sched != nullptr && sched[0] == 's') ? 0 : 1;
-    const char* dbg = getenv("GIFT_TC_DBG");
-    ta.dbg = dbg ? atoi(dbg) : 0;
-    const bool cts_ok = cts_enabled(f);
-    ta.cts = cts_ok ? f->cts : nullptr;
-    ta.cts_off = cts_ok ? f->cts_off : nullptr;
-    if (ta.chunk_kb < 1) ta.chunk_kb = 1;
+    // D1 drain interval (k-blocks): short tensor-core accumulation chains
+    // hold the 1e-5 contract; at most 4
+    const int dkb = (f->flags >> GIFT_FIF_DRAIN_SHIFT) & 7;
+    ta.chunk_kb = dkb == 0 ? 4 : dkb;
+    ta.dyn = (f->flags & GIFT_FIF_SCHED_STATIC) ? 0 : 1;
     int rc2 = launch_scan_tc(f, Q, nprobes, ta, w.g1, w.g2, st, ev_scan_begin, ev_scan_end);
     if (rc2) return rc2;
   } else {

@@ -41,8 +41,6 @@ constexpr int B_TILE = TC_NMAX * TC_BK * 2;  // 16 KB
 constexpr int STAGE_LO = 2 * A_TILE + 2 * B_TILE;
 constexpr int RING_BYTES = 3 * STAGE_LO;  // 192 KB
 constexpr int EPI_COLS = 32;  // epilogue stages 32 probe columns at a time
-constexpr int EPI_STRIDE = EPI_COLS + 1;
-constexpr int EPI_BYTES = TC_M * EPI_STRIDE * 4;
 constexpr int ITEM_RING = 8;     // decoded work items in flight (scheduler -> roles)
 // TMEM: D1 (hi x hi) double-buffered per k-chunk, drained every chunk_kb
 // k-blocks (short tensor-core accumulation chains: the fp32 accumulate is
@@ -93,10 +91,6 @@ __device__ __forceinline__ ItemInfo decode_item(const TcArgs& p, int64_t item, i
     I.mt = static_cast<int>(rem % nm);
     I.live = tt < T;
     if (!I.live) tt -= 1;  // odd tile count: the second CTA recomputes the first tile
-  } else if (p.mt_major) {  // neighbouring CTAs share a probe tile (B)
-    tt = rem % T;
-    I.mt = static_cast<int>(rem / T);
-    I.live = true;
   } else {  // neighbouring CTAs share a posting tile (A)
     tt = rem / nm;
     I.mt = static_cast<int>(rem % nm);
@@ -110,7 +104,7 @@ __device__ __forceinline__ ItemInfo decode_item(const TcArgs& p, int64_t item, i
   I.seg1 = p.tile_seg1[t];
   I.nb = min(TC_NMAX, cnt - I.mt * TC_NMAX);
   I.pb0 = p.probe_off[lo] + I.mt * TC_NMAX;
-  I.n = (I.nb > 64 || (p.dbg & 16)) ? 128 : 64;  // dbg 16: timing experiment, N = 128 always
+  I.n = I.nb > 64 ? 128 : 64;
   return I;
 }
 
@@ -190,6 +184,10 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (p.meta[M_OVERFLOW]) return;  // uniform over the grid (both CTAs of a pair)
   const int64_t n_items = p.meta[M_ITEMS];
+  // every query lo plane is zero (fp16-exact queries): the single-CTA kernel
+  // drops the b2 operand -- one N = n MMA per k-step instead of N = 2n, no b2
+  // loads, no D2 drains (b2 = 0 contributes exactly 0: bit-identical)
+  const bool qz = !PAIR && p.meta[M_QLO] == 0;
   const int nkb = (p.d + TC_BK - 1) / TC_BK;
   const int chunk_kb = p.chunk_kb;
 
@@ -246,15 +244,12 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
         const uint32_t a_bytes = has_lo ? 2 * A_TILE : A_TILE;
         // this CTA's B bytes: both planes (single), one whole plane (pair, cb),
         // half of each plane (pair, lo)
-        const uint32_t bytes = a_bytes + (PAIR && cb ? I.n : 2 * brows) * TC_BK * 2;
+        const uint32_t bytes = a_bytes + (PAIR && cb ? I.n : (qz ? 1 : 2) * brows) * TC_BK * 2;
         for (int kb = 0; kb < nkb; ++kb) {
-          if (p.dbg & 32) break;  // timing experiment: no smem ring at all
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * stage_bytes;
           if (!tc::elect_one()) {
             // other lanes: nothing to issue
-          } else if (p.dbg & 8) {  // timing experiment: MMA pipeline without loads
-            if (!PAIR || leader) tc::mbar_arrive(&full[stage]);
           } else if (PAIR) {
             // both CTAs' bytes complete on the leader's full barrier
             const uint32_t lbar = tc::mapa(&full[stage], 0);
@@ -282,8 +277,9 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
             for (int x = 0; x < I.n / 64; ++x) {
               tc::tma_load_2d(st + b_off + x * B_BOX, &tmB1, &full[stage], kb * TC_BK,
                               I.pb0 + 64 * x);
-              tc::tma_load_2d(st + b_off + I.n * TC_BK * 2 + x * B_BOX, &tmB2, &full[stage],
-                              kb * TC_BK, I.pb0 + 64 * x);
+              if (!qz)
+                tc::tma_load_2d(st + b_off + I.n * TC_BK * 2 + x * B_BOX, &tmB2, &full[stage],
+                                kb * TC_BK, I.pb0 + 64 * x);
             }
           }
           __syncwarp();
@@ -327,7 +323,7 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
           const uint32_t d1 = tmem_base + buf * (cb ? 2 * TC_NMAX : TC_NMAX);
           const int kend = min(kb0 + chunk_kb, nkb);
           for (int kb = kb0; kb < kend; ++kb) {
-            if (!(p.dbg & 32)) tc::mbar_wait(&full[stage], phase);
+            tc::mbar_wait(&full[stage], phase);
             tc::tc_fence_after();
             uint8_t* st = smem + stage * stage_bytes;
             const uint64_t a1 = tc::smem_desc_sw128(st);
@@ -337,7 +333,6 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
             if (tc::elect_one()) {
 #pragma unroll
               for (int k = 0; k < TC_BK / 16; ++k) {
-                if (p.dbg & 4) break;  // timing experiment: load pipeline without MMAs
                 const uint32_t acc1 = (kb > kb0 || k > 0) ? 1u : 0u;
                 const uint32_t acc2 = (kb > 0 || k > 0) ? 1u : 0u;
                 const uint64_t adv = static_cast<uint64_t>(k * 2);  // 32 B in 16-B units
@@ -347,15 +342,16 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
                   tc::mma_f16_2sm(d1, a1 + adv, b1 + adv, idesc, acc1);
                   tc::mma_f16_2sm(d2, a1 + adv, b2 + adv, idesc, acc2);
                   tc::mma_f16_2sm(d2, a2 + adv, b1 + adv, idesc, 1u);
+                } else if (qz) {  // b2 = 0: D1 = a1 . b1 [, D2 = a2 . b1]
+                  tc::mma_f16(d1, a1 + adv, b1 + adv, idesc, acc1);
+                  if (has_lo) tc::mma_f16(d1 + I.n, a2 + adv, b1 + adv, idesc, acc1);
                 } else {
                   // a1 . [b1 | b2] -> [D1 | D2] (A read once), then D2 += a2 . b1
                   tc::mma_f16(d1, a1 + adv, b1 + adv, idesc2, acc1);
                   if (has_lo) tc::mma_f16(d1 + I.n, a2 + adv, b1 + adv, idesc, 1u);
                 }
               }
-              if (!(p.dbg & 32)) {
-                if (PAIR) tc::mma_commit_2sm(&empty[stage], 0x3); else tc::mma_commit(&empty[stage]);
-              }
+              if (PAIR) tc::mma_commit_2sm(&empty[stage], 0x3); else tc::mma_commit(&empty[stage]);
             }
             __syncwarp();
             if (++stage == nstages) {
@@ -383,7 +379,7 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
     // plan kernel) as CTAs become free, so the probe tiles of one posting
     // tile (consecutive items) run at the same time on neighbouring SMs and
     // the posting tile's re-reads hit L2 (a static stride lets the CTAs drift
-    // apart); GIFT_TC_SCHED=static restores the stride.  Pair: the leader
+    // apart); GIFT_FIF_SCHED_STATIC restores the stride.  Pair: the leader
     // fetches and pushes each index into the peer's s_next ring.
     if (lane == 0) {
       int hint = 0;
@@ -476,7 +472,23 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
           const uint32_t base = tmem_base + lane_off + buf * TC_NMAX + c0;
 #pragma unroll
           for (int j = 0; j < NA / 16; j += 2) {
-            if (j < ng && !(p.dbg & 2)) {
+            if (j < ng) {
+              float v1[16], v2[16];
+              tc::tmem_ld_x16(base + j * 16, v1);
+              tc::tmem_ld_x16(base + (j + 1) * 16, v2);  // ng is even
+              tc::tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                acc[j * 16 + i] += v1[i];
+                acc[(j + 1) * 16 + i] += v2[i];
+              }
+            }
+          }
+        } else if (qz && !has_lo) {  // D1 only: acc += D1
+          const uint32_t base = tmem_base + lane_off + buf * 2 * TC_NMAX + c0;
+#pragma unroll
+          for (int j = 0; j < NA / 16; j += 2) {
+            if (j < ng) {
               float v1[16], v2[16];
               tc::tmem_ld_x16(base + j * 16, v1);
               tc::tmem_ld_x16(base + (j + 1) * 16, v2);  // ng is even
@@ -492,7 +504,7 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
           const uint32_t base = tmem_base + lane_off + buf * 2 * TC_NMAX + c0;
 #pragma unroll
           for (int j = 0; j < NA / 16; ++j) {
-            if (j < ng && !(p.dbg & 2)) {
+            if (j < ng) {
               float v1[16], v2[16];
               tc::tmem_ld_x16(base + j * 16, v1);
               tc::tmem_ld_x16(base + I.n + j * 16, v2);
@@ -537,7 +549,7 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
           tc::mbar_arrive(&dempty[ib]);
         ++item_ctr;
       }
-      if (!I.live || (p.dbg & 1)) {  // pair: duplicate tile, nothing to write
+      if (!I.live) {  // pair: duplicate tile, nothing to write
         named_bar(bar_tail, TC_M);
         continue;
       }
@@ -571,9 +583,7 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
               sim = fminf(fmaxf(mx, 0.f), 1.f);
             const int64_t o = obase + static_cast<int64_t>(I.mt * TC_NMAX + m) * S_c +
                               (I.seg0 + sl - seg_base);
-            if (p.dbg & 64) {  // timing experiment: no compact stores
-              if (sim == -1.f) p.out[o] = sim;
-            } else if (sp0 < I.p0 || sp1 > I.p1) {
+            if (sp0 < I.p0 || sp1 > I.p1) {
               atomicMax(reinterpret_cast<int*>(p.out + o), __float_as_int(sim));
             } else {
               p.out[o] = sim;
@@ -592,331 +602,6 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
       tc::tmem_dealloc_2sm<TMEM_COLS>(tmem_base);
     else
       tc::tmem_dealloc<TMEM_COLS>(tmem_base);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Scan over the compressed tile store (f32 planes; experimental, built only
-// with GIFT_CTS=1).
-//
-// Same items, MMAs and epilogue as fif_scan_tc_kernel (single CTA, combined
-// [b1 | b2] operand, D2 += a2 . b1), but the posting planes arrive as the
-// sparse blocks of fif_build.cu (one cp.async.bulk per (tile, k-block) into a
-// 3-slot staging ring) and 4 expander warps rebuild the dense 128B-swizzled
-// tiles (thread = tile row: mask walk, predicated half2 loads, 16-byte
-// stores), then issue the probe planes' TMA into the same stage.  Bit-identical
-// to the dense single-CTA scan (tested); measured slower than the dense scan
-// on config 2 (1.99 vs 1.38 ms): the expansion's shared-memory traffic, not
-// HBM, becomes the bound.
-//   warp 0 bulk producer | 1 MMA | 2 scheduler | 3-6 epilogue | 7-10 expand
-constexpr int CTS_THREADS = 352;
-constexpr int CTS_STAGES = 2;                        // dense stages: A1 A2 B (64 KB)
-constexpr int CTS_STAGE = STAGE_LO;
-constexpr int CTS_NSTG = 3;                          // staging slots
-constexpr int CTS_STG_BYTES = 25 * 1024;
-constexpr int CTS_RING = CTS_STAGES * CTS_STAGE + CTS_NSTG * CTS_STG_BYTES;
-constexpr int SMEM_CTS = CTS_RING + EPI_BYTES + 256;
-constexpr int CTS_HDR_BYTES = 128 * 8 + 128 * 2;
-
-bool cts_enabled(const gift_fif_view* f) {
-  const char* ce = getenv("GIFT_CTS");
-  return f->cts != nullptr && f->cts_off != nullptr && f->feat_lo != nullptr && f->d % 64 == 0 &&
-         !(ce != nullptr && ce[0] == '0');
-}
-
-__global__ void __launch_bounds__(CTS_THREADS, 1)
-    fif_scan_cts_kernel(const __grid_constant__ CUtensorMap tmB1,
-                        const __grid_constant__ CUtensorMap tmB2, const TcArgs p) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ int32_t s_sp[TC_M + 2];
-  __shared__ float s_qn2[TC_NMAX];
-  __shared__ ItemInfo s_item[ITEM_RING];
-  __shared__ __align__(8) uint64_t ifull[ITEM_RING], iempty[ITEM_RING];
-  uint8_t* stg = smem + CTS_STAGES * CTS_STAGE;
-  float* Ds = reinterpret_cast<float*>(smem + CTS_RING);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + CTS_RING + EPI_BYTES);
-  uint64_t* full = bars;                    // dense stages
-  uint64_t* empty = full + CTS_STAGES;
-  uint64_t* sfull = empty + CTS_STAGES;     // staging slots
-  uint64_t* sempty = sfull + CTS_NSTG;
-  uint64_t* tfull = sempty + CTS_NSTG;      // D chunk buffers
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
-  const int64_t first = blockIdx.x, stride = gridDim.x;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (p.meta[M_OVERFLOW]) return;
-  const int64_t n_items = p.meta[M_ITEMS];
-  const int nkb = p.d / TC_BK;
-  const int chunk_kb = p.chunk_kb;
-
-  if (warp == 0 && lane == 0) {
-    for (int r = 0; r < ITEM_RING; ++r) {
-      tc::mbar_init(&ifull[r], 1);
-      tc::mbar_init(&iempty[r], 4);  // producer, MMA, epilogue, expander
-    }
-    for (int s = 0; s < CTS_STAGES; ++s) {
-      tc::mbar_init(&full[s], TC_M);  // the 128 expander threads (one with B's bytes)
-      tc::mbar_init(&empty[s], 1);
-    }
-    for (int s = 0; s < CTS_NSTG; ++s) {
-      tc::mbar_init(&sfull[s], 1);
-      tc::mbar_init(&sempty[s], TC_M);
-    }
-    for (int b = 0; b < 2; ++b) {
-      tc::mbar_init(&tfull[b], 1);
-      tc::mbar_init(&tempty[b], TC_M);
-    }
-    tc::fence_barrier_init();
-    tc::tma_prefetch(&tmB1);
-    tc::tma_prefetch(&tmB2);
-  }
-  if (warp == 1) tc::tmem_alloc<TMEM_COLS>(tmem_holder);
-  tc::tc_fence_before();
-  __syncthreads();
-  tc::tc_fence_after();
-  const uint32_t tmem_base = *tmem_holder;
-
-  if (warp == 0) {
-    // ------------------------------------------------ bulk producer (staging)
-    int slot = 0;
-    uint32_t sph = 0, it = 0;
-    for (int64_t item = first; item < n_items; item += stride, ++it) {
-      const uint32_t rs = it % ITEM_RING, rph = (it / ITEM_RING) & 1;
-      tc::mbar_wait(&ifull[rs], rph);
-      const ItemInfo I = s_item[rs];
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&iempty[rs]);
-      for (int kb = 0; kb < nkb; ++kb) {
-        tc::mbar_wait(&sempty[slot], sph ^ 1);
-        if (tc::elect_one()) {
-          const int64_t bi = static_cast<int64_t>(I.t) * nkb + kb;
-          const int64_t o0 = p.cts_off[bi];
-          const uint32_t bytes = static_cast<uint32_t>(p.cts_off[bi + 1] - o0);
-          tc::mbar_arrive_expect_tx(&sfull[slot], bytes);
-          tc::bulk_load(stg + slot * CTS_STG_BYTES, p.cts + o0, bytes, &sfull[slot]);
-        }
-        __syncwarp();
-        if (++slot == CTS_NSTG) {
-          slot = 0;
-          sph ^= 1;
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer (whole warp)
-    int stage = 0;
-    uint32_t phase = 0, chunk_ctr = 0, it = 0;
-    for (int64_t item = first; item < n_items; item += stride, ++it) {
-      const uint32_t rs = it % ITEM_RING, rph = (it / ITEM_RING) & 1;
-      tc::mbar_wait(&ifull[rs], rph);
-      const ItemInfo I = s_item[rs];
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&iempty[rs]);
-      const uint32_t idesc = tc::idesc_f16_f32(TC_M, I.n);
-      const uint32_t idesc2 = tc::idesc_f16_f32(TC_M, 2 * I.n);
-      for (int kb0 = 0; kb0 < nkb; kb0 += chunk_kb) {
-        const uint32_t buf = chunk_ctr & 1, aph = (chunk_ctr >> 1) & 1;
-        tc::mbar_wait(&tempty[buf], aph ^ 1);
-        tc::tc_fence_after();
-        const uint32_t d1 = tmem_base + buf * 2 * TC_NMAX;
-        const int kend = min(kb0 + chunk_kb, nkb);
-        for (int kb = kb0; kb < kend; ++kb) {
-          tc::mbar_wait(&full[stage], phase);
-          tc::tc_fence_after();
-          uint8_t* st = smem + stage * CTS_STAGE;
-          const uint64_t a1 = tc::smem_desc_sw128(st);
-          const uint64_t a2 = tc::smem_desc_sw128(st + A_TILE);
-          const uint64_t b1 = tc::smem_desc_sw128(st + 2 * A_TILE);
-          if (tc::elect_one()) {
-#pragma unroll
-            for (int k = 0; k < TC_BK / 16; ++k) {
-              const uint32_t acc1 = (kb > kb0 || k > 0) ? 1u : 0u;
-              const uint64_t adv = static_cast<uint64_t>(k * 2);
-              tc::mma_f16(d1, a1 + adv, b1 + adv, idesc2, acc1);
-              tc::mma_f16(d1 + I.n, a2 + adv, b1 + adv, idesc, 1u);
-            }
-            tc::mma_commit(&empty[stage]);
-          }
-          __syncwarp();
-          if (++stage == CTS_STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-        if (tc::elect_one()) tc::mma_commit(&tfull[buf]);
-        __syncwarp();
-        ++chunk_ctr;
-      }
-    }
-  } else if (warp == 2) {
-    // ------------------------------------------------ scheduler
-    if (lane == 0) {
-      int hint = 0;
-      uint32_t it = 0;
-      for (int64_t item = first; item < n_items; item += stride, ++it) {
-        const uint32_t rs = it % ITEM_RING, rph = (it / ITEM_RING) & 1;
-        const ItemInfo I = decode_item<false>(p, item, hint, 0);
-        tc::mbar_wait(&iempty[rs], rph ^ 1);
-        s_item[rs] = I;
-        tc::mbar_arrive(&ifull[rs]);
-      }
-    }
-  } else if (warp >= 7) {
-    // ------------------------------------------------ expanders (thread = row)
-    const int r = threadIdx.x - 7 * 32;  // 0..127
-    int stage = 0, slot = 0;
-    uint32_t phase = 0, sph = 0, it = 0;
-    const uint32_t sw = static_cast<uint32_t>(r & 7);
-    const int row_off = (r >> 3) * 1024 + (r & 7) * 128;
-    for (int64_t item = first; item < n_items; item += stride, ++it) {
-      const uint32_t rs = it % ITEM_RING, rph = (it / ITEM_RING) & 1;
-      tc::mbar_wait(&ifull[rs], rph);
-      const ItemInfo I = s_item[rs];
-      named_bar(3, TC_M);
-      if (r == 0) tc::mbar_arrive(&iempty[rs]);
-      const uint32_t bbytes = 2u * I.n * TC_BK * 2;
-      for (int kb = 0; kb < nkb; ++kb) {
-        tc::mbar_wait(&empty[stage], phase ^ 1);  // MMA done with this stage
-        uint8_t* st = smem + stage * CTS_STAGE;
-        if (r == 0) {  // probe planes [b1 | b2] of this k-block (bytes registered below)
-          for (int x = 0; x < I.n / 64; ++x) {
-            tc::tma_load_2d(st + 2 * A_TILE + x * B_BOX, &tmB1, &full[stage], kb * TC_BK,
-                            I.pb0 + 64 * x);
-            tc::tma_load_2d(st + 2 * A_TILE + I.n * TC_BK * 2 + x * B_BOX, &tmB2, &full[stage],
-                            kb * TC_BK, I.pb0 + 64 * x);
-          }
-        }
-        tc::mbar_wait(&sfull[slot], sph);
-        if (!(p.dbg & 64)) {  // dbg 64: timing experiment without the expansion
-          const uint8_t* blk = stg + slot * CTS_STG_BYTES;
-          const uint64_t m = reinterpret_cast<const uint64_t*>(blk)[r];
-          const uint32_t* vals = reinterpret_cast<const uint32_t*>(
-              blk + CTS_HDR_BYTES + 16 * reinterpret_cast<const uint16_t*>(blk + 1024)[r]);
-          int cnt = 0;
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {  // 16-byte chunk q = elements 8q .. 8q+7
-            uint32_t hw[4], lw[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int c0 = q * 8 + e * 2;
-              const bool b0 = (m >> c0) & 1ull, b1 = (m >> (c0 + 1)) & 1ull;
-              const uint32_t v0 = b0 ? vals[cnt] : 0u;
-              cnt += b0;
-              const uint32_t v1 = b1 ? vals[cnt] : 0u;
-              cnt += b1;
-              hw[e] = (v0 & 0xffffu) | (v1 << 16);
-              lw[e] = (v0 >> 16) | (v1 & 0xffff0000u);
-            }
-            const int cpos = row_off + static_cast<int>((static_cast<uint32_t>(q) ^ sw) * 16);
-            *reinterpret_cast<uint4*>(st + cpos) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-            *reinterpret_cast<uint4*>(st + A_TILE + cpos) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
-          }
-        }
-        tc::mbar_arrive(&sempty[slot]);     // staging slot read
-        tc::fence_proxy_async_smem();       // expanded tile -> tensor-core proxy
-        if (r == 0)  // the TMA bytes may land before this: tx-count goes transiently negative
-          tc::mbar_arrive_expect_tx(&full[stage], bbytes);
-        else
-          tc::mbar_arrive(&full[stage]);
-        if (++stage == CTS_STAGES) {
-          stage = 0;
-          phase ^= 1;
-        }
-        if (++slot == CTS_NSTG) {
-          slot = 0;
-          sph ^= 1;
-        }
-      }
-    }
-  } else {
-    // ------------------------------------------------ epilogue (warps 3..6)
-    const int et = threadIdx.x - 96;
-    const int lb = 32 * (warp & 3);
-    const int row = lb + lane;
-    const bool gauss = p.mode == GIFT_SIM_GAUSSIAN;
-    uint32_t chunk_ctr = 0, it = 0;
-    for (int64_t item = first; item < n_items; item += stride, ++it) {
-      const uint32_t rs = it % ITEM_RING, rph = (it / ITEM_RING) & 1;
-      tc::mbar_wait(&ifull[rs], rph);
-      const ItemInfo I = s_item[rs];
-      named_bar(2, TC_M);
-      if (et == 0) tc::mbar_arrive(&iempty[rs]);
-      const int nseg = I.seg1 - I.seg0;
-      const int ng = I.n / 16;
-      const int sp_a = et <= nseg ? p.seg_pstart[I.seg0 + et] : 0;
-      const int sp_b = et + TC_M <= nseg ? p.seg_pstart[I.seg0 + et + TC_M] : 0;
-      const float qn_r = et < I.nb ? p.qn2s[I.pb0 + et] : 0.f;
-      float acc[TC_NMAX];
-#pragma unroll
-      for (int n = 0; n < TC_NMAX; ++n) acc[n] = 0.f;
-      const uint32_t lane_off = static_cast<uint32_t>(lb) << 16;
-      for (int kb0 = 0; kb0 < nkb; kb0 += chunk_kb) {
-        const uint32_t buf = chunk_ctr & 1, aph = (chunk_ctr >> 1) & 1;
-        tc::mbar_wait(&tfull[buf], aph);
-        tc::tc_fence_after();
-        const uint32_t base = tmem_base + lane_off + buf * 2 * TC_NMAX;
-#pragma unroll
-        for (int j = 0; j < TC_NMAX / 16; ++j) {
-          if (j < ng) {
-            float v1[16], v2[16];
-            tc::tmem_ld_x16(base + j * 16, v1);
-            tc::tmem_ld_x16(base + I.n + j * 16, v2);
-            tc::tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 16; ++i) acc[j * 16 + i] += fmaf(v2[i], SPLIT_INV, v1[i]);
-          }
-        }
-        tc::tc_fence_before();
-        tc::mbar_arrive(&tempty[buf]);
-        ++chunk_ctr;
-      }
-      if (et <= nseg) s_sp[et] = sp_a;
-      if (et + TC_M <= nseg) s_sp[et + TC_M] = sp_b;
-      s_qn2[et] = qn_r;
-      const float pn = (I.p0 + row < I.p1) ? p.pnorm2[I.p0 + row] : 0.f;
-      const int64_t S_c = p.seg_off[I.c + 1] - p.seg_off[I.c];
-      const int64_t seg_base = p.seg_off[I.c];
-      const int64_t obase = p.outbase[I.c];
-      const int mc = et & (EPI_COLS - 1), sg0 = et >> 5;
-#pragma unroll
-      for (int sl0 = 0; sl0 < TC_NMAX; sl0 += EPI_COLS) {
-        if (sl0 < I.nb) {
-#pragma unroll
-          for (int c = 0; c < EPI_COLS; ++c) {
-            float v = acc[sl0 + c];
-            if (gauss) v = 2.0f * v - pn;
-            Ds[row * EPI_STRIDE + c] = v;
-          }
-          named_bar(1, TC_M);
-          const int ncol = min(EPI_COLS, I.nb - sl0);
-          const int m = sl0 + mc;
-          for (int sl = sg0; mc < ncol && sl < nseg; sl += TC_M / EPI_COLS) {
-            const int sp0 = s_sp[sl], sp1 = s_sp[sl + 1];
-            const int r0 = max(sp0, I.p0) - I.p0, r1 = min(sp1, I.p1) - I.p0;
-            float mx = -INFINITY;
-            for (int rr = r0; rr < r1; ++rr) mx = fmaxf(mx, Ds[rr * EPI_STRIDE + mc]);
-            float sim;
-            if (gauss)
-              sim = expf(-fmaxf(s_qn2[m] - mx, 0.f) * p.inv_sigma2);
-            else
-              sim = fminf(fmaxf(mx, 0.f), 1.f);
-            const int64_t o = obase + static_cast<int64_t>(I.mt * TC_NMAX + m) * S_c +
-                              (I.seg0 + sl - seg_base);
-            if (sp0 < I.p0 || sp1 > I.p1)
-              atomicMax(reinterpret_cast<int*>(p.out + o), __float_as_int(sim));
-            else
-              p.out[o] = sim;
-          }
-          named_bar(1, TC_M);
-        }
-      }
-    }
-  }
-  tc::tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc::tc_fence_after();
-    tc::tmem_dealloc<TMEM_COLS>(tmem_base);
   }
 }
 
@@ -948,6 +633,7 @@ __global__ void probe_gather_split_kernel(const float* __restrict__ Q, int d, in
   const float* q = Q + view * d;
   __half* o1 = g1 + static_cast<int64_t>(s) * d;
   __half* o2 = g2 + static_cast<int64_t>(s) * d;
+  bool lo = false;
   for (int k = threadIdx.x * 4; k < d; k += blockDim.x * 4) {
     const float4 v = *reinterpret_cast<const float4*>(q + k);
     __half a0, a1, a2, a3, b0, b1, b2, b3;
@@ -959,7 +645,11 @@ __global__ void probe_gather_split_kernel(const float* __restrict__ Q, int d, in
     reinterpret_cast<__half2*>(o1 + k)[1] = __halves2half2(a2, a3);
     reinterpret_cast<__half2*>(o2 + k)[0] = __halves2half2(b0, b1);
     reinterpret_cast<__half2*>(o2 + k)[1] = __halves2half2(b2, b3);
+    lo |= (__half_as_ushort(b0) | __half_as_ushort(b1) | __half_as_ushort(b2) |
+           __half_as_ushort(b3)) & 0x7fff;
   }
+  if (__syncthreads_or(lo) && threadIdx.x == 0)
+    atomicOr(reinterpret_cast<unsigned long long*>(const_cast<int64_t*>(meta) + M_QLO), 1ull);
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -1001,19 +691,16 @@ bool tc_supported(const gift_fif_view* f) {
 // traffic per SM; config 3 scan 16.3 -> 15.1 ms, config 2 unchanged), single
 // CTAs for fp16 storage (config 4: the pair is ~7% slower there)
 // persistent scan CTAs: one per SM minus the view's GIFT_FIF_RESERVE_SMS
-// (left to the kernels of other batches in flight); GIFT_SCAN_CTAS=n overrides
+// (left to the kernels of other batches in flight)
 static int scan_ctas(const gift_fif_view* f) {
-  const char* e = getenv("GIFT_SCAN_CTAS");
-  const int n = e != nullptr ? atoi(e) : 0;
-  if (n > 0) return min(n, sm_count());
   const int reserve = (f->flags >> 8) & 255;
   return max(2, sm_count() - reserve);
 }
 
 bool tc_pair_enabled(const gift_fif_view* f) {
-  if (cts_enabled(f)) return false;  // the compressed-store scan runs on single CTAs
-  const char* e = getenv("GIFT_TC_PAIR");
-  if (e != nullptr && (e[0] == '0' || e[0] == '1')) return e[0] == '1' && sm_count() >= 2;
+  const int m = (f->flags >> GIFT_FIF_PAIR_SHIFT) & 3;
+  if (m == GIFT_FIF_PAIR_OFF) return false;
+  if (m == GIFT_FIF_PAIR_ON) return sm_count() >= 2;
   return f->feat_lo != nullptr && sm_count() >= 2;
 }
 
@@ -1063,11 +750,7 @@ int launch_scan_tc(const gift_fif_view* f, const float* Q, int64_t nprobes_max, 
   if (rc) return rc;
   a.has_lo = f->feat_lo != nullptr ? 1 : 0;
   if (ev0) GIFT_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(ev0), st));
-  if (a.cts != nullptr) {
-    GIFT_CUDA_TRY(cudaFuncSetAttribute(fif_scan_cts_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_CTS));
-    fif_scan_cts_kernel<<<scan_ctas(f), CTS_THREADS, SMEM_CTS, st>>>(mB1, mB2, a);
-  } else if (pair && a.has_lo) {
+  if (pair && a.has_lo) {
     GIFT_CUDA_TRY((launch_pair<1, true>(scan_ctas(f), st, mA1, mA2, mB1, mB2, mB1h, mB2h, a)));
   } else if (pair) {  // fp16 storage: tensor-bound, two epilogue groups
     GIFT_CUDA_TRY((launch_pair<2, false>(scan_ctas(f), st, mA1, mA2, mB1, mB2, mB1h, mB2h, a)));
@@ -1102,4 +785,3 @@ extern "C" int gift_split_planes(const float* x, int64_t n, void* h1, void* h2, 
   return GIFT_OK;
 }
 
-extern "C" int gift_cts_stage_limit(void) { return gift::CTS_STG_BYTES; }

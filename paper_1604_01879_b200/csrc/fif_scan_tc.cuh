@@ -5,7 +5,10 @@
 
 namespace gift {
 
-enum Meta { M_ITEMS = 0, M_OUT_TOTAL = 1, M_OVERFLOW = 2, M_WORK = 3 };
+// meta[M_QLO] != 0: some probe's query lo plane (b2) is non-zero.  Queries
+// whose values are exactly fp16 (config 4's fp16-rounded views) leave it 0 and
+// the single-CTA scan then skips the b2 operand (half the MMA work, bit-identical).
+enum Meta { M_ITEMS = 0, M_OUT_TOTAL = 1, M_OVERFLOW = 2, M_WORK = 3, M_QLO = 4 };
 
 struct TcArgs {
   const int64_t* item_off;
@@ -29,28 +32,22 @@ struct TcArgs {
   float inv_sigma2;
   int has_lo;
   int chunk_kb;
-  int mt_major;  // item order within a cell: probe-tile-major (1) or posting-tile-major (0)
   int dyn;       // items from the meta[M_WORK] counter (1) or a static CTA stride (0)
-  const uint8_t* cts;      // compressed tile store of the planes (fif_build.cu) or null
-  const int64_t* cts_off;  // [T * nkb + 1] block byte offsets
-  int dbg;       // timing experiments only (GIFT_TC_DBG bits; outputs invalid): 1 = skip
-                 // the epilogue tail, 2 = skip the TMEM drains, 4 = no MMAs, 8 = no loads
 };
 
 bool tc_supported(const gift_fif_view* f);
 // The scan on CTA pairs (cta_group::2, M = 256): a work item is two
-// consecutive posting tiles of a cell x one probe tile.  GIFT_TC_PAIR=0|1
-// overrides the default (pairs with the f32 lo plane).
+// consecutive posting tiles of a cell x one probe tile.  GIFT_FIF_PAIR(m) in
+// the view flags overrides the default (pairs with the f32 lo plane).
 bool tc_pair_enabled(const gift_fif_view* f);
-// the index carries a compressed tile store and GIFT_CTS != 0
-bool cts_enabled(const gift_fif_view* f);
 // quantize with need_order = false: when exactly ma candidates survive the
 // margin test their order is not resolved (the F-IF scan takes a max over
 // the ma cells, matching.py:153-159, so only the set matters)
 int quantize_impl(const void* X, int32_t xdtype, int64_t n, int32_t d, const float* C,
                   const double* cnorm2, int32_t K, double cmax_norm, int32_t ma,
                   const uint8_t* nz, int32_t zero_key, int32_t* out_idx, void* ws,
-                  size_t ws_bytes, void* stream, bool need_order, const float* xnorm2);
+                  size_t ws_bytes, void* stream, bool need_order, const float* xnorm2,
+                  bool allow_tc);
 size_t tc_probe_plane_bytes(int64_t nprobes, int d);
 int launch_scan_tc(const gift_fif_view* f, const float* Q, int64_t nprobes_max, TcArgs a,
                    __half* g1, __half* g2, cudaStream_t st, void* ev0, void* ev1);

@@ -255,8 +255,6 @@ double tc_dot_eps(int d) {
 }
 
 bool quant_tc_supported(int d, int xdtype) {
-  const char* e = getenv("GIFT_QUANT");
-  if (e != nullptr && e[0] == 's') return false;  // GIFT_QUANT=simt
   return d % 8 == 0 && d >= 8 && (xdtype == GIFT_F32 || xdtype == GIFT_F16);
 }
 

@@ -641,7 +641,8 @@ namespace gift {
 int quantize_impl(const void* X, int32_t xdtype, int64_t n, int32_t d, const float* C,
                   const double* cnorm2, int32_t K, double cmax_norm, int32_t ma,
                   const uint8_t* nz, int32_t zero_key, int32_t* out_idx, void* ws,
-                  size_t ws_bytes, void* stream, bool need_order, const float* xnorm2) {
+                  size_t ws_bytes, void* stream, bool need_order, const float* xnorm2,
+                  bool allow_tc) {
   cudaStream_t st = as_stream(stream);
   GIFT_REQUIRE(K >= 1 && d >= 1, GIFT_ERR_EMPTY, "empty codebook");
   GIFT_REQUIRE(ma >= 1 && ma <= K, GIFT_ERR_INVALID, "ma must be in [1, %d]", K);
@@ -680,7 +681,7 @@ int quantize_impl(const void* X, int32_t xdtype, int64_t n, int32_t d, const flo
   float* xconv = xdtype == GIFT_F64 ? ar.take<float>(rows * static_cast<int64_t>(d)) : nullptr;
   GIFT_REQUIRE(approx != nullptr && (xdtype != GIFT_F64 || xconv != nullptr), GIFT_ERR_CAPACITY,
                "quantize workspace too small");
-  const bool use_tc = quant_tc_supported(d, xdtype);
+  const bool use_tc = allow_tc && quant_tc_supported(d, xdtype);
   // views left for the CTA kernel by the warp kernel (+ their count)
   int32_t* list = ma <= 8 ? ar.take<int32_t>(rows + 1) : nullptr;
   GIFT_REQUIRE(ma > 8 || list != nullptr, GIFT_ERR_CAPACITY, "quantize workspace too small");
@@ -755,6 +756,17 @@ extern "C" int gift_quantize(const void* X, int32_t xdtype, int64_t n, int32_t d
                              const double* cnorm2, int32_t K, double cmax_norm, int32_t ma,
                              const uint8_t* nz, int32_t zero_key, int32_t* out_idx, void* ws,
                              size_t ws_bytes, void* stream) {
+  return gift_quantize_ex(X, xdtype, n, d, C, cnorm2, K, cmax_norm, ma, nz, zero_key, out_idx, ws,
+                          ws_bytes, 0, stream);
+}
+
+extern "C" int gift_quantize_ex(const void* X, int32_t xdtype, int64_t n, int32_t d,
+                                const float* C, const double* cnorm2, int32_t K,
+                                double cmax_norm, int32_t ma, const uint8_t* nz,
+                                int32_t zero_key, int32_t* out_idx, void* ws, size_t ws_bytes,
+                                int32_t flags, void* stream) {
+  GIFT_REQUIRE((flags & ~GIFT_QUANT_SIMT) == 0, GIFT_ERR_INVALID, "unknown quantize flags 0x%x",
+               flags);
   return quantize_impl(X, xdtype, n, d, C, cnorm2, K, cmax_norm, ma, nz, zero_key, out_idx, ws,
-                       ws_bytes, stream, true, nullptr);
+                       ws_bytes, stream, true, nullptr, !(flags & GIFT_QUANT_SIMT));
 }

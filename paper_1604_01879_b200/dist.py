@@ -24,6 +24,7 @@ import torch
 import torch.distributed as dist
 
 from . import engine as eg
+from .index import CAND_K_MAX
 
 
 def shard_bounds(n: int, world: int, rank: int):
@@ -170,11 +171,14 @@ class ShardedEngine:
         loc_self = torch.where((loc_self >= 0) & (loc_self < self.fif.n_local), loc_self,
                                torch.full_like(loc_self, -1)).to(torch.int32)
         if rerank:
-            # local top-k2 straight from the reduce's candidates (no dense row)
             k2 = min(cfg.k2, self.n_global)
-            _, cs, ci = self.runner.score(self.fif, Q, cfg.ma, self.mode, cfg.sigma, cand_k=k2,
-                                          dense=False)
-            li, lv = eg.topk_candidates(cs, ci, k2, positive_only=True)
+            if k2 <= CAND_K_MAX:  # local top-k2 straight from the reduce's candidates
+                _, cs, ci = self.runner.score(self.fif, Q, cfg.ma, self.mode, cfg.sigma,
+                                              cand_k=k2, dense=False)
+                li, lv = eg.topk_candidates(cs, ci, k2, positive_only=True)
+            else:
+                s = self.runner.score(self.fif, Q, cfg.ma, self.mode, cfg.sigma)
+                li, lv = eg.topk_rows(s, k2, positive_only=True, ord_base=base)
             nbr, _ = all_gather_topk(lv, li, ordinal_tiebreak(li), k2, self.group)
             fa = eg.act_mean(self.raw, nbr.to(torch.int32).contiguous())
             if k <= 256:

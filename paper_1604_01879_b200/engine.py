@@ -66,8 +66,9 @@ class DeviceCodebook:
 
 
 def quantize_rows(cb: DeviceCodebook, X: torch.Tensor, ma: int, nz: torch.Tensor | None = None,
-                  zero_key: int = -1, stream=None) -> torch.Tensor:
-    """K1: [n, d] (f32/f16/f64, device) -> [n, ma] int32 nearest centroids."""
+                  zero_key: int = -1, stream=None, flags: int = 0) -> torch.Tensor:
+    """K1: [n, d] (f32/f16/f64, device) -> [n, ma] int32 nearest centroids.
+    flags: nat.QUANT_SIMT selects the CUDA-core stage 1 (same results)."""
     X = X.contiguous()
     n, d = X.shape
     if d != cb.d:
@@ -77,9 +78,9 @@ def quantize_rows(cb: DeviceCodebook, X: torch.Tensor, ma: int, nz: torch.Tensor
     out = torch.empty((n, ma), dtype=torch.int32, device=X.device)
     wsb = nat.lib().gift_quantize_ws_bytes(n, d, cb.K, _DTYPE_CODE[X.dtype])
     ws = nat.workspace("quantize", stream).get(wsb)
-    nat.call("gift_quantize", nat.ptr(X), _DTYPE_CODE[X.dtype], n, d, nat.ptr(cb.centroids),
+    nat.call("gift_quantize_ex", nat.ptr(X), _DTYPE_CODE[X.dtype], n, d, nat.ptr(cb.centroids),
              nat.ptr(cb.cnorm2), cb.K, cb.cmax, ma, nat.ptr(nz), zero_key, nat.ptr(out),
-             nat.ptr(ws), ws.numel(), _sp(stream))
+             nat.ptr(ws), ws.numel(), int(flags), _sp(stream))
     return out
 
 
@@ -121,6 +122,21 @@ class DeviceFif:
         self.view = None
         self.feat = None
         self.feat_hi = self.feat_lo = None
+        self.variant = 0  # kernel-variant bits of gift_fif_view.flags (set_variant)
+
+    def set_variant(self, scan: str = "tc", quant: str = "tc", reduce: str = "auto",
+                    pair: str = "auto", sched: str = "dynamic", drain_kb: int = 0):
+        """Select kernel variants through the view flags (include/gift.h):
+        scan/quant "tc" | "simt", reduce "auto" | "range" | "gather" | "owner",
+        pair "auto" | "on" | "off", sched "dynamic" | "static", drain_kb 0..4
+        (0 = default).  Defaults reproduce the measured-fastest choice."""
+        v = (nat.FIF_SCAN_SIMT if scan == "simt" else 0) | \
+            (nat.FIF_QUANT_SIMT if quant == "simt" else 0) | nat.FIF_REDUCE[reduce] | \
+            nat.FIF_PAIR[pair] | (nat.FIF_SCHED_STATIC if sched == "static" else 0) | \
+            nat.fif_drain_kb(drain_kb)
+        self.variant = v
+        self.bind()
+        return self
 
     @property
     def storage_dtype(self):
@@ -157,9 +173,8 @@ class DeviceFif:
         v.shape_seg = self.shape_seg.data_ptr()
         v.shape_seg_cell = self.shape_seg_cell.data_ptr()
         v.max_cell_segments = self.smax
-        v.cts = None if getattr(self, "cts", None) is None else self.cts.data_ptr()
-        v.cts_off = None if getattr(self, "cts_off", None) is None else self.cts_off.data_ptr()
-        v.flags = nat.FIF_TILED_SEGMENTS if self.seg_len_max <= nat.lib().gift_fif_tile_n() else 0
+        v.flags = (nat.FIF_TILED_SEGMENTS if self.seg_len_max <= nat.lib().gift_fif_tile_n()
+                   else 0) | self.variant
         self.view = v
         return v
 
@@ -331,7 +346,6 @@ class DeviceFif:
         radix_sort_pairs(k2, v2, _bits(n_local), stream)
         self.shape_off = offsets_from_sorted(k2, n_local, stream)  # [n_local+1]
         self.shape_post = v2.to(torch.int64)
-        self._build_cts(stream)
         seg_sizes = self.seg_off[1:] - self.seg_off[:-1]
         self.seg_len_max = int((self.seg_pstart[1:S + 1] - self.seg_pstart[:S]).max().item()) if S else 0
         self.smax = int(seg_sizes.max().item()) if K else 0
@@ -350,37 +364,6 @@ class DeviceFif:
             self.shape_seg = torch.zeros(1, dtype=torch.int32, device=dev)
             self.shape_seg_cell = torch.zeros(1, dtype=torch.int32, device=dev)
         self.bind()
-
-    def _build_cts(self, stream=None):
-        """Compressed tile store of the f32 planes (lossless sparse blocks per
-        (scan tile, 64-wide k-block), read by the experimental compressed
-        scan).  Built only with GIFT_CTS=1 (the expansion measured slower than
-        the dense-plane scan); skipped for fp16 storage, d % 64 != 0, blocks
-        over the scan's staging slot or not enough free HBM."""
-        import os
-
-        self.cts = self.cts_off = None
-        if (self.feat_lo is None or self.d % 64 != 0 or self.T == 0
-                or os.environ.get("GIFT_CTS", "0") != "1"):
-            return
-        lib = nat.lib()
-        dev = self.post_ord.device
-        nkb = self.d // 64
-        off = torch.empty(self.T * nkb + 1, dtype=torch.int64, device=dev)
-        ws = nat.workspace("build", stream).get(lib.gift_cts_ws_bytes(self.T, self.d))
-        nat.call("gift_cts_build", nat.ptr(self.feat_hi), nat.ptr(self.feat_lo), self.P, self.d,
-                 nat.ptr(self.tile_pstart), nat.ptr(self.tile_pend), self.T, nat.ptr(off), None,
-                 nat.ptr(ws), ws.numel(), _sp(stream))
-        total = int(off[-1].item())
-        biggest = int((off[1:] - off[:-1]).max().item())
-        free, _ = torch.cuda.mem_get_info(dev)
-        if biggest > lib.gift_cts_stage_limit() or total + (8 << 30) > free:
-            return
-        self.cts = torch.empty(max(total, 16), dtype=torch.uint8, device=dev)
-        nat.call("gift_cts_build", nat.ptr(self.feat_hi), nat.ptr(self.feat_lo), self.P, self.d,
-                 nat.ptr(self.tile_pstart), nat.ptr(self.tile_pend), self.T, nat.ptr(off),
-                 nat.ptr(self.cts), nat.ptr(ws), ws.numel(), _sp(stream))
-        self.cts_off = off
 
     # -- host views (reference container attributes) ---------------------
     def host_lists(self):
@@ -423,13 +406,21 @@ class DeviceFif:
 
 
 class ScoreRunner:
-    """K3 launcher with a grow-on-overflow compact workspace."""
+    """K3 launcher with a pre-sized (or grow-on-overflow) compact workspace.
 
-    MAX_BOUND = 1 << 30  # compact floats we are willing to pre-size for
+    The compact (probe x segment) buffer is sized for its worst case
+    B V ma max_cell_segments whenever that fits the budget (a quarter of the
+    HBM free at first use, at most 16 GiB per stream): the batch then never
+    needs the host to read the plan's overflow word, so nothing in the query
+    path synchronises (config 4's Zipf head cells: ~8 GiB).  Larger bounds
+    fall back to a capacity that grows on overflow, checked per batch."""
+
+    MAX_BOUND_BYTES = 16 << 30
 
     def __init__(self):
         self.capacity = 1 << 22
         self._ws = {}  # stream handle -> Workspace (batches in flight on two streams)
+        self._budget = None  # compact floats we are willing to pre-size for
 
     def score(self, fif: DeviceFif, Q: torch.Tensor, ma: int, mode: int = nat.SIM_COSINE,
               sigma: float = 0.5, vq: torch.Tensor | None = None, out: torch.Tensor | None = None,
@@ -465,7 +456,10 @@ class ScoreRunner:
         # upper bound of the compact (probe x segment) buffer: if it fits the
         # budget, size for it and skip the host round trip on the overflow flag
         bound = B * V * ma * max(fif.smax, 1)
-        checked = bound > self.MAX_BOUND
+        if self._budget is None:
+            free, _ = torch.cuda.mem_get_info(Q.device)
+            self._budget = min(self.MAX_BOUND_BYTES, free // 4) // 4
+        checked = bound > self._budget
         if not checked:
             self.capacity = max(self.capacity, bound)
         cs = ci = None
@@ -537,10 +531,12 @@ class ActRows:
 
     @classmethod
     def empty(cls, n: int, cap: int, device) -> "ActRows":
-        return cls(torch.full((n, cap), -1, dtype=torch.int32, device=device),
-                   torch.zeros((n, cap), dtype=torch.float64, device=device),
-                   torch.zeros(n, dtype=torch.int32, device=device),
-                   torch.zeros(n, dtype=torch.float64, device=device))
+        """Uninitialised rows: every libgift producer (act_from_topk, act_mean,
+        act_aggregate) writes all cap slots of a row plus cnt and norm."""
+        return cls(torch.empty((n, cap), dtype=torch.int32, device=device),
+                   torch.empty((n, cap), dtype=torch.float64, device=device),
+                   torch.empty(n, dtype=torch.int32, device=device),
+                   torch.empty(n, dtype=torch.float64, device=device))
 
     def rows(self, a: int, b: int) -> "ActRows":
         return ActRows(self.idx[a:b], self.val[a:b], self.cnt[a:b], self.norm[a:b])
@@ -668,10 +664,12 @@ class DeviceSif:
         return acc
 
     def query_topk(self, q: ActRows, k: int, order: torch.Tensor, idrank: torch.Tensor | None,
-                   self_local: torch.Tensor | None = None, stream=None):
+                   self_local: torch.Tensor | None = None, stream=None, flags: int | None = None):
         """Sparse query_sif + final top-k (index.py:290-294): identical to
         topk_rows(self.query(q), k, idrank=..., self_local=...) without the
-        dense [B, n] rows."""
+        dense [B, n] rows.  flags: nat.SIF_ROWS / nat.SIF_SORT force one of the
+        two implementations (default: `self.query_flags`, 0 = by batch size)."""
+        flags = int(getattr(self, "query_flags", 0) if flags is None else flags)
         B = q.n
         dev = q.idx.device
         idx = torch.empty((B, k), dtype=torch.int32, device=dev)
@@ -681,14 +679,14 @@ class DeviceSif:
         bound = q.cap * self.max_list
         lib = nat.lib()
         ws = nat.workspace("sif_topk", stream).get(
-            lib.gift_sif_query_topk_ws_bytes(B, self.n_local, k, bound))
+            lib.gift_sif_query_topk_ws_bytes(B, self.n_local, k, bound, flags))
         acc = self._acc_rows(B, stream)
         nat.call("gift_sif_query_topk", nat.ptr(self.e_off), nat.ptr(self.e_ord),
                  nat.ptr(self.e_val), nat.ptr(self.norms), self.n_global, self.n_local,
                  nat.ptr(q.idx), nat.ptr(q.val), nat.ptr(q.cnt), nat.ptr(q.norm), B, q.cap,
                  nat.ptr(acc), acc.shape[0], acc.shape[1], nat.ptr(order), nat.ptr(idrank),
                  nat.ptr(self_local), self.ord_base, k, bound, nat.ptr(idx), nat.ptr(val),
-                 nat.ptr(ws), ws.numel(), _sp(stream))
+                 nat.ptr(ws), ws.numel(), flags, _sp(stream))
         return idx, val
 
     def query(self, q: ActRows, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:

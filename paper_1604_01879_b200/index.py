@@ -34,6 +34,9 @@ log = logging.getLogger(__name__)
 
 FORMAT_VERSION = "shapesearch-index-1"
 CHANNELS = ("A", "B")
+CAND_K_MAX = 8  # the reduce's per-range candidates (fif_scan.cu RED_MAXK); larger k2 -> dense path
+ACT_MAX_K2 = 64  # act.cu MAX_NBR: neighbours per mean activation
+ACT_MAX_E = 1024  # act.cu AM_MAX_E: k1 * k2 staged entries per mean activation
 _REFERENCE_FIELDS = ("n_views", "resolution", "grid", "cells", "bins", "codebook_size", "ma",
                      "k1", "k2", "alpha", "seed", "imported")
 
@@ -74,6 +77,11 @@ class IndexConfig:
             raise ValueError("storage_dtype must be 'float32' or 'float16'")
         if self.batch_size < 1:
             raise ValueError("batch_size must be >= 1")
+        # the device mean activation stages k2 lists of <= k1 entries per row
+        if self.k2 > ACT_MAX_K2 or self.k1 * self.k2 > ACT_MAX_E:
+            raise Unsupported(f"k2 = {self.k2} (max {ACT_MAX_K2}) and k1 * k2 = "
+                              f"{self.k1 * self.k2} (max {ACT_MAX_E}) exceed the device "
+                              "mean-activation kernel")
 
     @property
     def torch_storage(self):
@@ -198,7 +206,7 @@ class QueryEngine:
             final = sa if sb is sa else (sa + sb) / 2.0
             return eg.topk_rows(final, min(top_k, self.n), idrank=self.idrank,
                                 self_local=self_local, stream=stream)
-        if rerank and Qb is None and self.dup and self.raw_dup:
+        if rerank and Qb is None and self.dup and self.raw_dup and self.cfg.k2 <= CAND_K_MAX:
             # single-channel fast path: the reduce emits per-range top-k2
             # candidates, merged into the neighbour lists (rerank.py:78-87)
             k2 = min(self.cfg.k2, self.n)

@@ -69,6 +69,22 @@ EVAL_CASES = [
 ]
 
 
+# BASELINE.json config 1, exactly: N=1,000 shapes x V=64 views x d=256, a
+# 40-class isotropic mixture (means ~ N(0, 1), sigma 0.3, ReLU, L2), K=64
+# sampled centroids, ma=1, gaussian sigma=0.5 (cosine for the reference
+# goldens), S-IF top-10 neighbour sets (k1=10, k2=4), 100 queries, top-50.
+C1 = dict(N=1000, V=64, d=256, classes=40, K=64, ma=1, k1=10, k2=4, n_queries=100, top_k=50,
+          sigma=0.5, seed=2016)
+
+
+def c1_inputs():
+    """(db [1000, 64, 256] f32, queries [100, 64, 256] f32, centroids, ids)."""
+    views, _ = mixture_views(C1["seed"], C1["N"], C1["V"], C1["d"], C1["classes"],
+                             n_queries=C1["n_queries"])
+    db, qs = views[:C1["N"]], views[C1["N"]:]
+    return db, qs, sampled_codebook(db, C1["K"], C1["seed"] + 1), shape_ids(C1["N"])
+
+
 def kmeans_inputs(name):
     """Seeded training sets for codebook training (codebook.py:64-108):
     (features, k, seed, max_iters)."""

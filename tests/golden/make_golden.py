@@ -218,6 +218,53 @@ def golden_e2e():
         print(name, "done")
 
 
+def golden_c1():
+    """BASELINE.json config 1 exactly (N=1,000 x V=64 x d=256, 40 classes,
+    sigma 0.3, K=64 sampled centroids, ma=1, k1=10, k2=4, 100 queries,
+    top-50), cosine mode, built and queried by the reference itself (both
+    channels computed, as the reference does).  Inputs are regenerated from
+    cases.c1_inputs() on the GPU box."""
+    from cases import C1, c1_inputs
+
+    db, qs, C, ids = c1_inputs()
+    cfg = rix.IndexConfig(n_views=C1["V"], codebook_size=C1["K"], ma=C1["ma"], k1=C1["k1"],
+                          k2=C1["k2"], imported=True)
+    bundle, scores, raw, nbr, final = reference_bundle(db, ids, C, cfg)
+    out = {"C": C}
+    out["raw_len"] = np.array([a.support for a in raw["A"]])
+    out["raw_idx"] = np.concatenate([a.indices for a in raw["A"]])
+    out["raw_val"] = np.concatenate([a.values for a in raw["A"]])
+    out["raw_norm"] = np.array([a.norm for a in raw["A"]])
+    out["final_len"] = np.array([a.support for a in final])
+    out["final_idx"] = np.concatenate([a.indices for a in final])
+    out["final_val"] = np.concatenate([a.values for a in final])
+    out["final_norm"] = np.array([a.norm for a in final])
+    top_k = C1["top_k"]
+    for rerank in (True, False):
+        tag = "rr" if rerank else "nr"
+        rid, rsc = [], []
+        for q in qs:
+            res, _t = rix.query(bundle, as_viewset("query", q), top_k=top_k, rerank=rerank)
+            rid.append([ids.index(r[0]) for r in res])
+            rsc.append([r[1] for r in res])
+        out[f"q_{tag}_ids"] = np.array(rid, dtype=np.int64)
+        out[f"q_{tag}_scores"] = np.array(rsc)
+        bid, bsc = [], []
+        for i in range(0, len(ids), 125):
+            res, _t = rix.query_by_id(bundle, ids[i], top_k=top_k, rerank=rerank)
+            bid.append([ids.index(r[0]) for r in res])
+            bsc.append([r[1] for r in res])
+        out[f"id_{tag}_ids"] = np.array(bid, dtype=np.int64)
+        out[f"id_{tag}_scores"] = np.array(bsc)
+    out["q_fif_scores"] = np.stack([rmt.query_fif(bundle.fifs["A"], q, ma=C1["ma"]) for q in qs])
+    out["q_rerank_scores"] = np.stack([rix.rerank_scores(bundle, {"A": s, "B": s})
+                                       for s in out["q_fif_scores"]])
+    out["fif_len"] = np.array([len(o) for o in bundle.fifs["A"].entry_ordinals])
+    out["fif_ord"] = np.concatenate(bundle.fifs["A"].entry_ordinals)
+    np.savez_compressed(os.path.join(HERE, "c1.npz"), **out)
+    print("c1 done")
+
+
 def golden_bundles():
     """The reference's own `save_bundle` directory (index.py:360-375) for the
     tiny and small end-to-end cases, every file's bytes kept verbatim: the
@@ -360,11 +407,15 @@ def golden_ingest():
 
 
 if __name__ == "__main__":
+    if sys.argv[1:] == ["c1"]:
+        golden_c1()
+        sys.exit(0)
     if sys.argv[1:] == ["ingest"]:
         golden_ingest()
         sys.exit(0)
     if sys.argv[1:] == ["kmeans"]:
         golden_kmeans()
+    golden_c1()
         sys.exit(0)
     if sys.argv[1:] == ["trained"]:
         golden_trained_bundle()
@@ -390,4 +441,5 @@ if __name__ == "__main__":
     golden_eval()
     golden_ingest()
     golden_kmeans()
+    golden_c1()
     golden_trained_bundle()

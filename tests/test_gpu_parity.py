@@ -18,6 +18,7 @@ from helpers import RTOL, assert_act_close, assert_ranking_close, unpack_acts, u
 pytestmark = pytest.mark.gpu
 
 import paper_1604_01879_b200 as gift  # noqa: E402
+from paper_1604_01879_b200 import _native as nat  # noqa: E402
 from paper_1604_01879_b200 import engine as eg  # noqa: E402
 from paper_1604_01879_b200 import matching as mt  # noqa: E402
 from paper_1604_01879_b200 import rerank as rr  # noqa: E402
@@ -299,20 +300,18 @@ def test_persistence_round_trip_and_bytes():
 
 
 @pytest.mark.parametrize("variant", ["default", "pair", "static"])
-def test_fp16_storage_matches_widened_oracle(variant, monkeypatch):
+def test_fp16_storage_matches_widened_oracle(variant):
     """Config 4 storage (D5): fp16 features, fp32 accumulation; the oracle
-    sees the same fp16 values widened to f32.  Variants: the single-CTA scan
-    with two epilogue groups (default), CTA pairs (GIFT_TC_PAIR=1) and the
-    static item stride (GIFT_TC_SCHED=static)."""
-    if variant == "pair":
-        monkeypatch.setenv("GIFT_TC_PAIR", "1")
-    if variant == "static":
-        monkeypatch.setenv("GIFT_TC_SCHED", "static")
+    sees the same fp16 values widened to f32.  Variants (view flags): the
+    single-CTA scan with two epilogue groups (default), CTA pairs
+    (GIFT_FIF_PAIR_ON) and the static item stride (GIFT_FIF_SCHED_STATIC)."""
     views, _ = mixture_views(21, 200, 20, 1024, 16, n_queries=4)
     v16 = views.astype(np.float16)
     db, qs = v16[:200], v16[200:].astype(np.float32)
     C = sampled_codebook(db.astype(np.float32), 32, 1)
     fif = mt.build_fif_from_tensor(torch.from_numpy(db).to(dev()), Codebook(C), shape_ids(200))
+    fif.dev.set_variant(pair="on" if variant == "pair" else "auto",
+                        sched="static" if variant == "static" else "dynamic")
     dbw = db.astype(np.float32)
     assign = oracle.quantize_many(C, dbw.reshape(-1, 1024), 1).reshape(200, 20)
     ref = oracle.build_fif(list(dbw), C, assign=assign)
@@ -355,7 +354,7 @@ def test_query_many_pipelined_equals_batch(lanes, reserve):
 
 
 @pytest.mark.parametrize("similarity", ["gaussian", "cosine"])
-def test_tensor_core_scan_matches_oracle_at_c2_dims(similarity, monkeypatch):
+def test_tensor_core_scan_matches_oracle_at_c2_dims(similarity):
     """The tcgen05 scan (default for d % 8 == 0) and the CUDA-core scan both
     match the f64 oracle at config-2 dimensions (d = 4096, K = 256, ma = 2)."""
     views, _ = mixture_views(55, 300, 16, 4096, 55, mu0=-0.26, n_queries=8)
@@ -368,14 +367,11 @@ def test_tensor_core_scan_matches_oracle_at_c2_dims(similarity, monkeypatch):
     got = {}
     # tc: CTA pairs (default with the f32 lo plane); tc_single: one CTA, two
     # epilogue groups; tc_static: static item stride instead of the counter
-    for impl, env in (("tc", {}), ("tc_single", {"GIFT_TC_PAIR": "0"}),
-                      ("tc_static", {"GIFT_TC_SCHED": "static"}), ("simt", {})):
-        monkeypatch.setenv("GIFT_SCAN", "simt" if impl == "simt" else "tc")
-        for k, v in env.items():
-            monkeypatch.setenv(k, v)
+    for impl, kw in (("tc", {}), ("tc_single", {"pair": "off"}),
+                     ("tc_static", {"sched": "static"}), ("simt", {"scan": "simt"})):
+        fif.dev.set_variant(**kw)
         got[impl] = mt.query_fif_batch(fif, qs, 2, similarity).cpu().numpy()
-        for k in env:
-            monkeypatch.delenv(k)
+    fif.dev.set_variant()
     np.testing.assert_array_equal(got["tc_static"], got["tc"])  # same items, same order
     worst = 0.0
     for i, q in enumerate(qs):
@@ -391,11 +387,10 @@ def test_tensor_core_scan_matches_oracle_at_c2_dims(similarity, monkeypatch):
 
 
 @pytest.mark.parametrize("impl", ["tc", "simt"])
-def test_quantize_near_ties_and_scale(impl, monkeypatch):
+def test_quantize_near_ties_and_scale(impl):
     """Bit-exact assignment under stress: midpoints of centroid pairs (d2 ties
     up to rounding), exact duplicates (ties -> lower index), and 8k config-2
     views, on both stage-1 implementations (tensor cores / CUDA cores)."""
-    monkeypatch.setenv("GIFT_QUANT", impl)
     views, _ = mixture_views(321, 200, 16, 4096, 55, mu0=-0.26)
     C = sampled_codebook(views, 256, 9)
     C[200] = C[17]  # exact duplicate centroids
@@ -406,12 +401,13 @@ def test_quantize_near_ties_and_scale(impl, monkeypatch):
                         .reshape(-1, 4096)]).astype(np.float32)
     cb = Codebook(C)
     for ma in (1, 2, 3):
-        got = quantize_batch(cb, X, ma)
+        got = eg.quantize_rows(cb.device(), torch.from_numpy(X).to(dev()), ma,
+                               flags=nat.QUANT_SIMT if impl == "simt" else 0).cpu().numpy()
         np.testing.assert_array_equal(got, oracle.quantize_many(C, X.astype(np.float64), ma))
 
 
 @pytest.mark.parametrize("V,ma,K", [(16, 1, 32), (16, 2, 32), (20, 3, 16), (64, 2, 64), (70, 2, 64)])
-def test_gather_reduce_equals_range_reduce(V, ma, K, monkeypatch):
+def test_gather_reduce_equals_range_reduce(V, ma, K):
     """The shape-centric gather and owner reduces (available when the index
     has its shape -> segment map and V * ma <= 128) are bit-identical to the
     per-range reduce: same per-view maxima, same ascending-view f64 sum.  Uniform
@@ -429,7 +425,7 @@ def test_gather_reduce_equals_range_reduce(V, ma, K, monkeypatch):
     run = eg.ScoreRunner()
     got = {}
     for impl in ("gather", "range", "owner"):
-        monkeypatch.setenv("GIFT_REDUCE", impl)
+        fif.dev.set_variant(reduce=impl)
         for sim in ("cosine", "gaussian"):
             s, cs, ci = run.score(fif.dev, Q, ma, mt.sim_mode(sim), 0.5, cand_k=4)
             nbr, val = eg.topk_candidates(cs, ci, 4, positive_only=True)
@@ -443,7 +439,7 @@ def test_gather_reduce_equals_range_reduce(V, ma, K, monkeypatch):
         np.testing.assert_array_equal(got["gather", sim][1], ref)
     # candidates-only mode (no dense scores) gives the same neighbour lists
     for impl in ("gather", "range", "owner"):
-        monkeypatch.setenv("GIFT_REDUCE", impl)
+        fif.dev.set_variant(reduce=impl)
         s, cs, ci = run.score(fif.dev, Q, ma, mt.sim_mode("cosine"), 0.5, cand_k=4, dense=False)
         assert s is None
         nbr, _ = eg.topk_candidates(cs, ci, 4, positive_only=True)
@@ -452,15 +448,14 @@ def test_gather_reduce_equals_range_reduce(V, ma, K, monkeypatch):
 
 @pytest.mark.parametrize("mode", ["rows", "sort"])
 @pytest.mark.parametrize("k", [1, 10, 100, 256])
-def test_sparse_sif_ranking_equals_dense(k, mode, monkeypatch):
+def test_sparse_sif_ranking_equals_dense(k, mode):
     """Sparse S-IF query + ranking (touched shapes + zero-score fill) is
     identical to top-k over the dense query_sif rows: shuffled id ranks,
     self inside / outside the touched set, an empty query support (pure
     fill), fewer touched shapes than k; repeated calls (scratch re-zeroed).
     Both implementations: per-query accumulator rows, and the sort-based one
-    (GIFT_SIF=sort: (query, shape) pairs radix-sorted, runs summed in order)."""
-    if mode == "sort":
-        monkeypatch.setenv("GIFT_SIF", "sort")
+    (GIFT_SIF_SORT: (query, shape) pairs radix-sorted, runs summed in order)."""
+    flags = nat.SIF_SORT if mode == "sort" else nat.SIF_ROWS
     rng = np.random.default_rng(k)
     N, B = 500, 37
     acts = []
@@ -481,39 +476,10 @@ def test_sparse_sif_ranking_equals_dense(k, mode, monkeypatch):
     kk = min(k, N)
     di, dv = eg.topk_rows(sif.query(q), kk, idrank=idrank, self_local=self_local)
     for _ in range(2):
-        si, sv = sif.query_topk(q, kk, order, idrank, self_local)
+        si, sv = sif.query_topk(q, kk, order, idrank, self_local, flags=flags)
         np.testing.assert_array_equal(si.cpu().numpy(), di.cpu().numpy())
         np.testing.assert_array_equal(sv.cpu().numpy(), dv.cpu().numpy())
     assert all(float(a.abs().sum()) == 0.0 for a in sif._acc.values())
-
-
-@pytest.mark.parametrize("similarity", ["gaussian", "cosine"])
-def test_compressed_tile_store_scan_bit_identical(similarity, monkeypatch):
-    """The (experimental, opt-in) scan over the compressed tile store (sparse
-    (hi, lo) blocks expanded in shared memory) gives exactly the scores of the
-    single-CTA dense-plane scan (same MMAs on the same operands), and matches
-    the oracle."""
-    views, _ = mixture_views(77, 300, 16, 4096, 55, mu0=-0.26, n_queries=8)
-    views[5, 3] = 0.0  # an empty view
-    db, qs = views[:300], views[300:]
-    C = sampled_codebook(db, 64, 4)
-    monkeypatch.setenv("GIFT_CTS", "1")  # the store is opt-in
-    fif = mt.build_fif_from_tensor(torch.from_numpy(db).to(dev()), Codebook(C), shape_ids(300))
-    assert fif.dev.cts is not None, "compressed tile store not built"
-    dense = fif.dev.P * 4096 * 4
-    assert fif.dev.cts.numel() < 0.7 * dense  # ReLU-sparse: well under the dense bytes
-    got = {}
-    for mode in ("cts", "dense"):
-        monkeypatch.setenv("GIFT_CTS", "1" if mode == "cts" else "0")
-        monkeypatch.setenv("GIFT_TC_PAIR", "0")
-        got[mode] = mt.query_fif_batch(fif, qs, 2, similarity).cpu().numpy()
-    np.testing.assert_array_equal(got["cts"], got["dense"])
-    assign = oracle.quantize_many(C, db.reshape(-1, 4096), 1).reshape(300, 16)
-    ref = oracle.build_fif(list(db), C, assign=assign)
-    for q, g in zip(qs, got["cts"]):
-        e = oracle.query_fif(ref, q, 2, similarity,
-                             cells=oracle.quantize_many(C, q.astype(np.float64), 2))
-        np.testing.assert_allclose(g, e, rtol=RTOL, atol=1e-12)
 
 
 @pytest.mark.parametrize("case", E2E_CASES[:2], ids=[c[0] for c in E2E_CASES[:2]])

@@ -1,0 +1,98 @@
+"""GPU: kernel-variant selection through explicit flags, the fp16-exact query
+shortcut of the scan, and the k2 edge cases of the re-rank (k2 > 8 takes the
+dense neighbour path; k2 = 64 fills the mean activation's neighbour table)."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from cases import mixture_views, sampled_codebook, shape_ids
+from helpers import RTOL, assert_ranking_close
+
+pytestmark = pytest.mark.gpu
+
+import paper_1604_01879_b200 as gift  # noqa: E402
+from paper_1604_01879_b200 import engine as eg  # noqa: E402
+from paper_1604_01879_b200 import matching as mt  # noqa: E402
+from paper_1604_01879_b200.codebook import Codebook  # noqa: E402
+from paper_1604_01879_b200.errors import Unsupported  # noqa: E402
+
+
+def dev():
+    return torch.device("cuda", 0)
+
+
+@pytest.mark.parametrize("storage", ["float16", "float32"])
+def test_fp16_exact_queries_skip_lo_plane_bit_identical(storage):
+    """Queries whose values are exactly fp16 have an all-zero lo plane: the
+    single-CTA scan then issues one N = n MMA per k-step (no b2 operand).  A
+    batch with one non-fp16 value elsewhere takes the full [b1 | b2] path; the
+    fp16-exact queries must score bit-identically in both batches, and match
+    the widened oracle."""
+    views, _ = mixture_views(31, 240, 20, 256, 12, n_queries=5)
+    db = views[:240].astype(np.float16 if storage == "float16" else np.float32)
+    q16 = views[240:].astype(np.float16).astype(np.float32)  # fp16-exact
+    C = sampled_codebook(db.astype(np.float32), 24, 2)
+    fif = mt.build_fif_from_tensor(torch.from_numpy(db).to(dev()), Codebook(C), shape_ids(240))
+    fif.dev.set_variant(pair="off")  # the single-CTA kernel (default for fp16 storage)
+    other = views[240:241].copy()
+    other[0, 0, 7] += np.float32(1e-6)  # not representable in fp16: lo plane non-zero
+    for sim in ("gaussian", "cosine"):
+        a = mt.query_fif_batch(fif, q16, 1, sim).cpu().numpy()
+        b = mt.query_fif_batch(fif, np.concatenate([q16, other]), 1, sim).cpu().numpy()[:5]
+        np.testing.assert_array_equal(a, b)
+        dbw = db.astype(np.float32)
+        assign = oracle.quantize_many(C, dbw.reshape(-1, 256), 1).reshape(240, 20)
+        ref = oracle.build_fif(list(dbw), C, assign=assign)
+        for q, g in zip(q16, a):
+            e = oracle.query_fif(ref, q, 1, sim, cells=oracle.quantize_many(C, q.astype(np.float64), 1))
+            np.testing.assert_allclose(g, e, rtol=RTOL, atol=1e-9)
+    fif.dev.set_variant()
+
+
+def _oracle_rank(db, qs, C, ids, ma, k1, k2, top_k):
+    ref = oracle.OracleIndex(list(db), C, ids, ma=ma, k1=k1, k2=k2)
+    return [ref.query(q, top_k=top_k, rerank=True)[0] for q in qs]
+
+
+@pytest.mark.parametrize("k1,k2", [(10, 10), (12, 64), (3, 9)])
+def test_large_k2_against_oracle(k1, k2):
+    """k2 above the reduce's candidate limit (8) runs through the dense
+    scores; k2 = 64 = the mean kernel's neighbour-table size."""
+    N, V, d, K = 180, 6, 32, 10
+    views, _ = mixture_views(41 + k2, N, V, d, 5, n_queries=4)
+    db, qs = views[:N], views[N:]
+    ids = shape_ids(N)
+    C = sampled_codebook(db, K, 3)
+    cfg = gift.IndexConfig(n_views=V, codebook_size=K, ma=2, k1=k1, k2=k2, imported=True)
+    bundle = gift.build_index_from_views(db, ids, cfg,
+                                         codebooks={"A": Codebook(C, "A"), "B": Codebook(C, "B")})
+    got = gift.query_batch(bundle, qs, top_k=25)
+    exp = _oracle_rank(db, qs, C, ids, 2, k1, k2, 25)
+    for g, e in zip(got, exp):
+        assert_ranking_close([ids.index(r[0]) for r in g], [r[1] for r in g],
+                             [ids.index(r[0]) for r in e], [r[1] for r in e])
+
+
+def test_kernel_limits_rejected_at_config():
+    with pytest.raises(Unsupported):
+        gift.IndexConfig(k1=20, k2=65)
+    with pytest.raises(Unsupported):
+        gift.IndexConfig(k1=100, k2=11)
+
+
+def test_drain_interval_flag_validated():
+    views, _ = mixture_views(5, 40, 4, 64, 3, n_queries=2)
+    C = sampled_codebook(views[:40], 8, 1)
+    fif = mt.build_fif_from_tensor(torch.from_numpy(views[:40]).to(dev()), Codebook(C),
+                                   shape_ids(40))
+    base = mt.query_fif_batch(fif, views[40:], 2, "gaussian").cpu().numpy()
+    for kb in (1, 2, 3):
+        fif.dev.set_variant(drain_kb=kb)
+        np.testing.assert_allclose(mt.query_fif_batch(fif, views[40:], 2, "gaussian").cpu().numpy(),
+                                   base, rtol=RTOL)
+    fif.dev.set_variant(drain_kb=6)
+    with pytest.raises(ValueError):
+        mt.query_fif_batch(fif, views[40:], 2, "gaussian")
+    fif.dev.set_variant()
