@@ -304,6 +304,14 @@ int gift_topk_rows_ex(const double* scores, int32_t B, int64_t n, int32_t k,
 int gift_topk_cand(const double* cs, const int32_t* ci, int32_t B, int64_t m,
                    int32_t k, int32_t positive_only, int32_t* out_idx,
                    double* out_val, void* stream);
+/* gift_topk_cand with an explicit tiebreak per candidate (ct, uint32: the
+ * key is (score desc, tiebreak asc)); candidates with ci < 0 are absent.
+ * Merges the per-shard candidates of the sharded engine (one all-gather per
+ * exchange): tiebreak = ordinal for the neighbour lists (rerank.py:86),
+ * 0 (own entry) / 1 + id rank for the final ranking (index.py:290-294). */
+int gift_topk_cand_tb(const double* cs, const int32_t* ci, const uint32_t* ct, int32_t B,
+                      int64_t m, int32_t k, int32_t positive_only, int32_t* out_idx,
+                      double* out_val, void* stream);
 
 /* ---- K5 activations (fixed-capacity rows: idx[B,cap] asc, val, cnt, norm) */
 /* build_activation (rerank.py:64-75) from a top-k result: first k1 positive

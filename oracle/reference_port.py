@@ -416,15 +416,17 @@ class OracleIndex:
 
     @classmethod
     def from_parts(cls, shape_ids, centroids, entry_ordinals, entry_features, raw, sif, *,
-                   ma, k1, k2, alpha=0.5, similarity="cosine", sigma=0.5):
-        """Assemble a single-channel (duplicated) oracle index from given
-        lists (e.g. parity-verified GPU-built lists; the CPU build of the
-        large configs takes hours)."""
+                   ma, k1, k2, alpha=0.5, similarity="cosine", sigma=0.5, single_channel=True):
+        """Assemble an oracle index over one feature set (duplicated channel,
+        D4) from given lists (oracle.scale's host build, or parity-verified
+        GPU-built lists).  single_channel=False scores channel B again, as
+        the reference does with two identical channels ("as-is")."""
         self = cls.__new__(cls)
         self.shape_ids = list(shape_ids)
         self.ma, self.k1, self.k2, self.alpha = ma, k1, k2, alpha
         self.similarity, self.sigma = similarity, sigma
-        self.dup = self.single = True
+        self.dup = True
+        self.single = single_channel
         fif = Fif(centroids=np.asarray(centroids, dtype=np.float32), n_shapes=len(shape_ids),
                   entry_ordinals=list(entry_ordinals), entry_features=list(entry_features))
         self.fifs = {"A": fif, "B": fif}

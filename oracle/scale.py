@@ -59,7 +59,9 @@ def quantize_many_mt(centroids, X, ma: int = 1, chunk: int = 8192, threads: int 
         for p in parts:
             run(p)
     else:
-        with ThreadPoolExecutor(threads) as ex:
+        from threadpoolctl import threadpool_limits
+
+        with threadpool_limits(1), ThreadPoolExecutor(threads) as ex:
             list(ex.map(run, parts))
     return out
 

@@ -108,6 +108,8 @@ _SIGS = {
                                     _c_i32, _c_dbl, _c_p, _c_p, _c_sz, _c_p, _c_p, _c_p, _c_i32,
                                     _c_p, _c_p]),
     "gift_topk_cand": (_c_i32, [_c_p, _c_p, _c_i32, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_p]),
+    "gift_topk_cand_tb": (_c_i32, [_c_p, _c_p, _c_p, _c_i32, _c_i64, _c_i32, _c_i32, _c_p, _c_p,
+                                   _c_p]),
     "gift_topk_rows": (_c_i32, [_c_p, _c_i32, _c_i64, _c_i32, _c_p, _c_p, _c_i64, _c_i32, _c_p,
                                 _c_p, _c_p]),
     "gift_topk_ws_bytes": (_c_sz, [_c_i32, _c_i64, _c_i32]),

@@ -160,9 +160,9 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + RING_BYTES + G * Epi<G>::DS * 4);
   uint64_t* full = bars;
   uint64_t* empty = bars + MAX_RING_STAGES;
-  uint64_t* tfull = bars + 2 * MAX_RING_STAGES;  // D1 chunk buffers
-  uint64_t* tempty = tfull + 2;
-  uint64_t* dfull = tempty + 2;                  // D2 item buffers
+  uint64_t* tfull = bars + 2 * MAX_RING_STAGES;  // D1 chunk buffers (2, or 4 when qz4)
+  uint64_t* tempty = tfull + 4;
+  uint64_t* dfull = tempty + 4;                  // D2 item buffers
   uint64_t* dempty = dfull + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(dempty + 2);
   constexpr bool has_lo = LO;  // the f32 storage's lo plane (compile time: lean MMA loop)
@@ -188,6 +188,12 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
   // drops the b2 operand -- one N = n MMA per k-step instead of N = 2n, no b2
   // loads, no D2 drains (b2 = 0 contributes exactly 0: bit-identical)
   const bool qz = !PAIR && p.meta[M_QLO] == 0;
+  // qz without the lo plane needs D1 only (128 TMEM columns per chunk): four
+  // chunk buffers instead of two, so the MMAs run a whole item ahead of the
+  // epilogue's per-item tail instead of stalling on the accumulators
+  const bool qz4 = qz && !LO;
+  const uint32_t nbuf = qz4 ? 4u : 2u;
+  const uint32_t buf_cols = qz4 ? TC_NMAX : ((!PAIR || !LO) ? 2 * TC_NMAX : TC_NMAX);
   const int nkb = (p.d + TC_BK - 1) / TC_BK;
   const int chunk_kb = p.chunk_kb;
 
@@ -202,9 +208,11 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
       tc::mbar_init(&ifull[r], 1);
       tc::mbar_init(&iempty[r], (PAIR && !leader) ? 1 + G : 2 + G);  // producer, [MMA,] epilogues
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < 4; ++b) {
       tc::mbar_init(&tfull[b], 1);
       tc::mbar_init(&tempty[b], (PAIR ? 2 : 1) * G * TC_M);  // pair: both CTAs' epilogues
+    }
+    for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&dfull[b], 1);
       tc::mbar_init(&dempty[b], (PAIR ? 2 : 1) * G * TC_M);
     }
@@ -316,11 +324,12 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
           d2 = tmem_base + 256 + ib * TC_NMAX;
         }
         for (int kb0 = 0; kb0 < nkb; kb0 += chunk_kb) {
-          const uint32_t buf = chunk_ctr & 1, aph = (chunk_ctr >> 1) & 1;
+          const uint32_t buf = chunk_ctr % nbuf, aph = (chunk_ctr / nbuf) & 1;
           tc::mbar_wait(&tempty[buf], aph ^ 1);
           tc::tc_fence_after();
-          // pair: D1 per chunk buffer, D2 per item; single: [D1 | D2] per chunk buffer
-          const uint32_t d1 = tmem_base + buf * (cb ? 2 * TC_NMAX : TC_NMAX);
+          // pair: D1 per chunk buffer, D2 per item; single: [D1 | D2] per chunk
+          // buffer; qz4: D1 per chunk buffer
+          const uint32_t d1 = tmem_base + buf * buf_cols;
           const int kend = min(kb0 + chunk_kb, nkb);
           for (int kb = kb0; kb < kend; ++kb) {
             tc::mbar_wait(&full[stage], phase);
@@ -465,7 +474,7 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
       for (int n = 0; n < NA; ++n) acc[n] = 0.f;
       const uint32_t lane_off = static_cast<uint32_t>(lb) << 16;
       for (int kb0 = 0; kb0 < nkb; kb0 += chunk_kb) {
-        const uint32_t buf = chunk_ctr & 1, aph = (chunk_ctr >> 1) & 1;
+        const uint32_t buf = chunk_ctr % nbuf, aph = (chunk_ctr / nbuf) & 1;
         tc::mbar_wait(&tfull[buf], aph);
         tc::tc_fence_after();
         if (!cb) {
@@ -484,8 +493,8 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
               }
             }
           }
-        } else if (qz && !has_lo) {  // D1 only: acc += D1
-          const uint32_t base = tmem_base + lane_off + buf * 2 * TC_NMAX + c0;
+        } else if (qz4) {  // D1 only: acc += D1
+          const uint32_t base = tmem_base + lane_off + buf * TC_NMAX + c0;
 #pragma unroll
           for (int j = 0; j < NA / 16; j += 2) {
             if (j < ng) {

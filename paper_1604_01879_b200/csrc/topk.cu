@@ -425,6 +425,12 @@ extern "C" int gift_topk_rows(const double* scores, int32_t B, int64_t n, int32_
 extern "C" int gift_topk_cand(const double* cs, const int32_t* ci, int32_t B, int64_t m, int32_t k,
                               int32_t positive_only, int32_t* out_idx, double* out_val,
                               void* stream) {
+  return gift_topk_cand_tb(cs, ci, nullptr, B, m, k, positive_only, out_idx, out_val, stream);
+}
+
+extern "C" int gift_topk_cand_tb(const double* cs, const int32_t* ci, const uint32_t* ct, int32_t B,
+                                 int64_t m, int32_t k, int32_t positive_only, int32_t* out_idx,
+                                 double* out_val, void* stream) {
   cudaStream_t st = as_stream(stream);
   GIFT_REQUIRE(k >= 1 && k <= 256, GIFT_ERR_UNSUPPORTED, "k = %d outside [1, 256]", k);
   if (B <= 0) return GIFT_OK;
@@ -433,7 +439,7 @@ extern "C" int gift_topk_cand(const double* cs, const int32_t* ci, int32_t B, in
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   TopkIn in{};
   in.cs = cs;
-  in.ct = nullptr;
+  in.ct = ct;
   in.ci = ci;
   in.m = m;
   TopkOut out{};

@@ -415,7 +415,6 @@ if __name__ == "__main__":
         sys.exit(0)
     if sys.argv[1:] == ["kmeans"]:
         golden_kmeans()
-    golden_c1()
         sys.exit(0)
     if sys.argv[1:] == ["trained"]:
         golden_trained_bundle()
@@ -441,5 +440,5 @@ if __name__ == "__main__":
     golden_eval()
     golden_ingest()
     golden_kmeans()
-    golden_c1()
     golden_trained_bundle()
+    golden_c1()

@@ -55,3 +55,50 @@ def assert_act_close(got, ref, rtol=RTOL, atol=1e-12):
     np.testing.assert_array_equal(np.asarray(gi), np.asarray(ri))
     np.testing.assert_allclose(gv, rv, rtol=rtol, atol=atol)
     assert abs(gn - rn) <= rtol * abs(rn) + atol
+
+
+def rel_err_stats(got, ref):
+    """Relative-error summary over the scores the reference makes positive
+    (max, p99.99, p99, count), plus how many zero / non-zero patterns differ."""
+    got = np.asarray(got, dtype=np.float64).ravel()
+    ref = np.asarray(ref, dtype=np.float64).ravel()
+    m = ref > 0
+    r = np.abs(got[m] - ref[m]) / ref[m] if m.any() else np.zeros(1)
+    return {"n": int(m.sum()), "max": float(r.max()), "p9999": float(np.quantile(r, 0.9999)),
+            "p99": float(np.quantile(r, 0.99)), "zero_mismatch": int(((got == 0) != (ref == 0)).sum())}
+
+
+def record_parity(config, check, stats):
+    """Append one parity measurement to $GIFT_PARITY_OUT (JSON lines; the GPU
+    runs copy it under profiles/) and print it."""
+    import json
+    import os
+
+    line = {"config": config, "check": check, **stats}
+    print("PARITY", json.dumps(line))
+    path = os.environ.get("GIFT_PARITY_OUT")
+    if path:
+        with open(path, "a") as fh:
+            fh.write(json.dumps(line) + "\n")
+
+
+def assert_topk_rows_close(got, ref, rtol=RTOL, atol=1e-12):
+    """Top-k activation rows (indices ascending, values): identical supports
+    with values within rtol, except members whose scores tie the row's
+    boundary (its smallest kept score) within rtol, which may be exchanged
+    (north_star: swaps among scores tied within the tolerance).  got/ref:
+    lists of (indices, values).  Returns the number of exchanged entries."""
+    swaps = 0
+    for r, ((gi, gv), (ri, rv)) in enumerate(zip(got, ref)):
+        gd = dict(zip(np.asarray(gi).tolist(), np.asarray(gv).tolist()))
+        rd = dict(zip(np.asarray(ri).tolist(), np.asarray(rv).tolist()))
+        for k in gd.keys() & rd.keys():
+            assert abs(gd[k] - rd[k]) <= rtol * abs(rd[k]) + atol, (r, k, gd[k], rd[k])
+        diff = (gd.keys() ^ rd.keys())
+        if diff:
+            edge = min(rd.values())
+            for k in diff:
+                v = gd.get(k, rd.get(k))
+                assert abs(v - edge) <= rtol * abs(edge) + atol, (r, k, v, edge)
+            swaps += len(diff)
+    return swaps

@@ -12,8 +12,32 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1604_01879_b200.dist import (all_gather_topk, merge_candidates, ordinal_tiebreak,
-                                        ranking_tiebreak, shard_bounds)
+from paper_1604_01879_b200.dist import (exchange_topk, ordinal_tiebreak, pack_candidates,
+                                        ranking_tiebreak, shard_bounds, unpack_candidates)
+
+
+def host_merge(v, o, t, k, positive_only):
+    """Reference merge of the exchanged candidates (the device kernel's
+    contract, gift_topk_cand_tb): best k by (score desc, uint32 tiebreak
+    asc), absent entries (ordinal < 0) skipped, -1 / 0.0 padded."""
+    B = v.shape[0]
+    out_i = torch.full((B, k), -1, dtype=torch.int32)
+    out_v = torch.zeros((B, k), dtype=torch.float64)
+    for b in range(B):
+        vv, oo = v[b].numpy(), o[b].numpy()
+        tt = t[b].numpy().astype(np.int64) & 0xFFFFFFFF
+        keep = np.flatnonzero(oo >= 0)
+        order = keep[np.lexsort((tt[keep], -vv[keep]))][:k]
+        for j, x in enumerate(order):
+            if positive_only and not vv[x] > 0:
+                continue
+            out_i[b, j] = int(oo[x])
+            out_v[b, j] = vv[x]
+    return out_i, out_v
+
+
+def all_gather_topk(vals, idx, tb, k, positive_only=False):
+    return exchange_topk(vals, idx, tb, k, positive_only, merge=host_merge)
 
 
 def _free_port():
@@ -100,11 +124,13 @@ def test_shard_bounds_partition(n, world):
     assert cover == list(range(n))
 
 
-def test_merge_candidates_missing_entries():
-    vals = torch.tensor([[[0.5, 0.0]], [[0.5, 0.2]]], dtype=torch.float64)
-    idx = torch.tensor([[[3, -1]], [[7, 9]]])
-    i, v = merge_candidates(vals, idx, ordinal_tiebreak(idx), 3)
-    assert i.tolist() == [[3, 7, 9]]
-    assert v.tolist() == [[0.5, 0.5, 0.2]]
-    i, v = merge_candidates(vals, idx, ordinal_tiebreak(idx), 4)
-    assert i.tolist() == [[3, 7, 9, -1]]
+def test_pack_round_trip_and_missing_entries():
+    vals = torch.tensor([[0.5, 0.0, 1e-300, -2.5]], dtype=torch.float64)
+    idx = torch.tensor([[3, -1, 2**31 - 1, 0]])
+    tb = torch.tensor([[3, 7, 0xFFFFFFFE, 0]])
+    v, o, t = unpack_candidates(pack_candidates(vals, idx, tb))
+    assert torch.equal(v, vals)
+    assert o.tolist() == [[3, -1, 2**31 - 1, 0]]
+    assert (t.to(torch.int64) & 0xFFFFFFFF).tolist() == [[3, 0xFFFFFFFF, 0xFFFFFFFE, 0]]
+    i, val = host_merge(v, o, t, 3, False)
+    assert i.tolist() == [[3, 2**31 - 1, 0]]
