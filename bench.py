@@ -2,21 +2,25 @@
 queries/sec, F-IF match + S-IF re-rank; F-IF scan HBM GB/s).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl gift|reference]
-                    [--config c2]
+                    [--config c1|c2|c3|c4|c5|...] [--shard]
 
 A step = one batch of queries (config 2: 64 queries x 64 views x d=4096)
 through quantize -> F-IF scan -> top-k2 -> query activation -> S-IF ->
 top-100, against a 10,000-shape database resident in HBM.  `value` is
 device-timed (CUDA events, inputs resident); `e2e` runs the public API
-`query_many` from pinned host memory (H2D of every batch and D2H of its
-results inside the timed region).  Under torchrun (N > 1) every rank serves
-an index replica and a disjoint query stream ("replicas": the 10 GB
-database of config 2 fits one GPU; sharding is for configs 3-5).
+(`query_many`, or the sharded engine) from pinned host memory, the H2D copy
+of every batch and the D2H of its results inside the timed region.
 
---impl reference times the reference's CPU path (oracle/ numpy port of
-shapesearch's query_fif + rerank_scores, single-channel variant) on all host
-cores; its index lists come from the parity-verified GPU build (the CPU
-build of config 2 would take hours).
+--gpus N: under torchrun WORLD_SIZE must equal N; without torchrun, N > 1
+re-launches this script with `torch.distributed.run` (one rank per GPU).
+At N > 1 configs 1-2 serve one index replica per rank (the database fits
+one GPU; disjoint query streams, no collective), configs 3-5 shard the
+database by shape (dist.py: two packed all-gathers per batch).
+
+--impl reference times the reference's own CPU path (the oracle/ port of
+shapesearch's query_fif + rerank_scores + ranking) on all host cores, over
+an index the ORACLE builds on the host (bit-exact quantize, f64 self-join):
+this arm never imports the product package nor maps libgift.so.
 """
 
 from __future__ import annotations
@@ -24,6 +28,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -37,15 +42,26 @@ import torch.distributed as dist
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from paper_1604_01879_b200 import IndexConfig, build_index_from_views, query_many  # noqa: E402
-from paper_1604_01879_b200.index import LANE_RESERVE_SMS, lane_streams  # noqa: E402
-from paper_1604_01879_b200 import engine as eg  # noqa: E402
-from paper_1604_01879_b200 import synth  # noqa: E402
-from paper_1604_01879_b200.codebook import Codebook  # noqa: E402
-
 METRIC = "queries/sec (F-IF match + S-IF rerank)"
 UNIT = "queries/s"
 SEED = 20160407
+
+
+def _load_synth():
+    """The workload generators (paper_1604_01879_b200/synth.py, torch only),
+    loaded by path: the reference arm must not import the product package
+    (nor map libgift.so)."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location(
+        "gift_workloads", os.path.join(ROOT, "paper_1604_01879_b200", "synth.py"))
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules["gift_workloads"] = mod  # dataclasses resolve their module by name
+    spec.loader.exec_module(mod)
+    return mod
+
+
+synth = _load_synth()
 
 
 # ------------------------------------------------------------------ helpers
@@ -70,13 +86,10 @@ class ClockSampler:
         self.lines = []
 
     def __enter__(self):
-        if os.environ.get("GIFT_BENCH_NO_SMI") == "1":  # diagnostics: no sampler
-            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms",
-                 os.environ.get("GIFT_SMI_MS", str(self.period_ms))],
+                 "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -121,13 +134,6 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
-# (batches in flight, SMs the scan leaves to the other lanes) per config:
-# config 2's non-scan kernels are ~20% of a step and overlap the next
-# batches' scans; config 3 (owner reduce, 105 GB) and config 4 (tensor-bound
-# scan) measured no gain
-DEFAULT_LANES = {"c1": (4, LANE_RESERVE_SMS), "c2": (4, LANE_RESERVE_SMS)}
-
-
 def warm(fn, iters: int, min_s: float = 0.25):
     """Untimed warm-up: at least `iters` calls and `min_s` seconds of
     back-to-back GPU work, ending with a synchronize.  Runs inside the clock
@@ -143,13 +149,25 @@ def warm(fn, iters: int, min_s: float = 0.25):
     torch.cuda.synchronize()
 
 
-def measured_peaks():
+def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            p = json.load(fh)
+            return json.load(fh)
+    except (OSError, ValueError):
+        return {}
+
+
+def measured_peaks():
+    p = _peaks()
+    if "hbm_gbs" in p:
         return float(p["hbm_gbs"]), "measured"
-    except (OSError, KeyError, ValueError):
-        return 6650.0, "fallback"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def measured_tensor_peak():
+    """Dense bf16/fp16 tensor peak (TFLOP/s): MEASURED_PEAKS.json burst figure
+    (the scan is timed per launch), else the profiling recipe's fallback."""
+    return float(_peaks().get("bf16_tflops", 1590.0))
 
 
 def count_launches(fn) -> int:
@@ -165,21 +183,80 @@ def count_launches(fn) -> int:
                if e.device_type.name == "CUDA" and "gift::" in e.name)
 
 
-def measured_tensor_peak():
-    """Dense bf16/fp16 tensor peak (TFLOP/s): MEASURED_PEAKS.json burst figure
-    (the scan is timed per launch), else the profiling recipe's fallback."""
+def host_cores():
     try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            return float(json.load(fh)["bf16_tflops"])
-    except (OSError, KeyError, ValueError):
-        return 1590.0
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
 
 
-def scan_work(eng, Q, w, top_k):
+def host_info():
+    """CPU model, cores and RAM of the host the CPU baseline runs on."""
+    model, phys = None, set()
+    try:
+        with open("/proc/cpuinfo") as fh:
+            cur = {}
+            for line in fh:
+                if ":" in line:
+                    k, v = (x.strip() for x in line.split(":", 1))
+                    cur[k] = v
+                    if k == "model name":
+                        model = v
+                elif cur:
+                    phys.add((cur.get("physical id"), cur.get("core id")))
+                    cur = {}
+    except OSError:
+        pass
+    ram = None
+    try:
+        with open("/proc/meminfo") as fh:
+            for line in fh:
+                if line.startswith("MemTotal:"):
+                    ram = round(int(line.split()[1]) / 2**20, 1)
+    except OSError:
+        pass
+    return {"cpu_model": model, "physical_cores": len(phys) or None,
+            "threads_available": host_cores(), "ram_gib": ram}
+
+
+def workload_config(w, parallelism: str) -> dict:
+    """The workload keys both arms report (the driver compares them)."""
+    return {"workload": w.name, "n_shapes": w.n_shapes, "n_views": w.n_views, "dim": w.dim,
+            "K": w.K, "ma": w.ma, "similarity": "gaussian", "sigma": w.sigma, "k1": w.k1,
+            "k2": w.k2, "top_k": w.top_k, "batch": w.batch, "n_queries": w.n_queries,
+            "storage": w.storage, "parallelism": parallelism,
+            "l2": "inputs larger than L2 (database >= 65 MB per GPU, batch inputs streamed)"}
+
+
+def c5_communities(n):
+    return synth.C5["communities"] if n >= synth.C5["n_shapes"] else max(1, n // 500)
+
+
+def c5_config(c, n, parallelism):
+    return {"workload": "c5", "n_shapes": n, "list_len": c["list_len"],
+            "communities": c5_communities(n), "k1": c["list_len"], "k2": c["k2"],
+            "top_k": c["top_k"], "batch": c["batch"], "n_queries": c["n_queries"],
+            "parallelism": parallelism,
+            "l2": "inputs larger than L2 (S-IF of 1M shapes ~2.2 GB)"}
+
+
+# ------------------------------------------------------------------ GPU arm
+def default_lanes(name):
+    """(batches in flight, SMs the scan leaves to the other lanes) per config:
+    config 2's non-scan kernels are ~20% of a step and overlap the next
+    batches' scans; config 3 (owner reduce, 105 GB) and config 4 (tensor-bound
+    scan) measured no gain."""
+    from paper_1604_01879_b200.index import LANE_RESERVE_SMS
+
+    return {"c1": (4, LANE_RESERVE_SMS), "c2": (4, LANE_RESERVE_SMS)}.get(name, (1, 0))
+
+
+def scan_work(fif, Q, w, top_k, similarity="gaussian"):
     """Algorithmic bytes / flops of one scan launch:
     bytes = sum_{c in U} |c| (d s_feat + 4 [+4 |p|^2]) + B V d 4 + B k 8,
     flops = sum_c M_c |c| 2 d."""
-    fif = eng.fa
+    from paper_1604_01879_b200 import engine as eg
+
     B, V, d = Q.shape
     flat = Q.reshape(-1, d)
     nz, _ = eg.view_prep(flat)
@@ -188,7 +265,7 @@ def scan_work(eng, Q, w, top_k):
     counts = torch.bincount(cells, minlength=fif.cb.K).double()
     sizes = (fif.cell_off[1:] - fif.cell_off[:-1]).double()
     s_feat = 2 if w.storage == "float16" else 4
-    per_post = d * s_feat + 4 + (4 if eng.cfg.similarity == "gaussian" else 0)
+    per_post = d * s_feat + 4 + (4 if similarity == "gaussian" else 0)
     used = counts > 0
     nbytes = float((sizes[used] * per_post).sum()) + B * V * d * 4 + B * top_k * 8
     flops = float((counts * sizes).sum()) * 2 * d
@@ -198,9 +275,8 @@ def scan_work(eng, Q, w, top_k):
 def load_ncu(config):
     """ncu --set full summary of this workload's scan / quantizer launch
     (profiles/ncu_summary.json, captured on one timed-path batch)."""
-    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
-        with open(path) as fh:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as fh:
             return json.load(fh).get(config) or {}
     except (OSError, ValueError):
         return {}
@@ -213,13 +289,40 @@ def load_traffic(config):
     return n["scan_dram_read_bytes"] + n.get("scan_dram_write_bytes", 0)
 
 
-# ------------------------------------------------------------------ setup
+def roofline_of(nbytes, flops, scan_ms, w, kernel, measured):
+    """The slower of the HBM time and the tensor time of the algorithmic
+    work; the fp32 split runs 2 (fp16 storage) or 3 (f32)
+    fp16 MMA products per algorithmic product on the tensor cores."""
+    peak, peak_kind = measured_peaks()
+    tpeak = measured_tensor_peak()
+    scan_s = scan_ms / 1000.0
+    achieved = nbytes / scan_s / 1e9
+    achieved_tf = flops / scan_s / 1e12
+    t_hbm = nbytes / (peak * 1e9)
+    t_tc = flops / (tpeak * 1e12)
+    split = 2 if w.storage == "float16" else 3
+    if t_tc > t_hbm:
+        r = {"bound": "tensor", "achieved": achieved_tf, "peak": tpeak, "unit": "TFLOP/s",
+             "frac": achieved_tf / tpeak}
+    else:
+        r = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+             "frac": achieved / peak}
+    r.update({"kernel": kernel, "peak_source": peak_kind, "traffic": load_traffic(w.name),
+              "alg_bytes_per_launch": nbytes, "alg_flops_per_launch": flops,
+              "scan_ms_avg": scan_ms, "scan_ms_measured": measured,
+              "achieved_gbs": achieved, "hbm_frac": achieved / peak,
+              "achieved_tflops": achieved_tf, "tensor_frac": achieved_tf / tpeak,
+              "fp16_mma_products_per_alg_product": split})
+    return r
+
+
 def build_streamed(w, device):
     """Config 3: 105 GB of f32 views on one GPU.  The database is generated
     block by block on the device and streamed through the chunked build
     (quantize pass, scatter into the tensor-core planes, self-join); the index
     keeps only the planes (52 GB hi + 52 GB lo)."""
-    from paper_1604_01879_b200 import build_index_streamed
+    from paper_1604_01879_b200 import IndexConfig, build_index_streamed
+    from paper_1604_01879_b200.codebook import Codebook
 
     mix = synth.BlockMixture(w, SEED, device)
     C = synth.sample_centroids_rows(mix, w.K, SEED + 1).cpu().numpy()
@@ -235,15 +338,22 @@ def build_streamed(w, device):
     return bundle, qs, time.perf_counter() - t0
 
 
-def build(w, device):
-    if w.name == "c3":
-        return build_streamed(w, device)
+def generate(w, device):
+    """(db [N, V, d] on device, queries [Q, V, d] f32 on device, centroids)."""
     if w.storage == "float16":  # config 4: Zipf-skewed cells, fp16 storage
         db, qs, Ct = synth.zipf_mixture(w, SEED, device)
-        C = Ct.cpu().numpy()
-    else:
-        db, qs, _labels = synth.mixture(w, SEED, device)
-        C = synth.sample_centroids(db, w.K, SEED + 1).cpu().numpy()
+        return db, qs, Ct.cpu().numpy()
+    db, qs, _labels = synth.mixture(w, SEED, device)
+    return db, qs, synth.sample_centroids(db, w.K, SEED + 1).cpu().numpy()
+
+
+def build(w, device):
+    from paper_1604_01879_b200 import IndexConfig, build_index_from_views
+    from paper_1604_01879_b200.codebook import Codebook
+
+    if w.name == "c3":
+        return build_streamed(w, device)
+    db, qs, C = generate(w, device)
     cfg = IndexConfig(n_views=w.n_views, codebook_size=w.K, ma=w.ma, k1=w.k1, k2=w.k2,
                       similarity="gaussian", sigma=w.sigma, storage_dtype=w.storage,
                       batch_size=w.batch, imported=True)
@@ -258,8 +368,9 @@ def build(w, device):
     return bundle, qs, build_s
 
 
-def host_oracle(bundle, w):
-    """oracle.OracleIndex over the (parity-verified) GPU-built lists."""
+def host_oracle(bundle, w, single_channel=True):
+    """oracle.OracleIndex over the (parity-verified) GPU-built lists: the CPU
+    baseline inside the GPU arm (the reference arm builds its own index)."""
     import oracle
 
     fif = bundle.fifs["A"]
@@ -269,30 +380,40 @@ def host_oracle(bundle, w):
                      entry_values=bundle.sif.entry_values)
     orc = oracle.OracleIndex.from_parts(
         bundle.shape_ids, fif.codebook.centroids, ords, feats, raw, sif, ma=w.ma, k1=w.k1,
-        k2=w.k2, alpha=0.5, similarity="gaussian_expanded", sigma=w.sigma)
+        k2=w.k2, alpha=0.5, similarity="gaussian_expanded", sigma=w.sigma,
+        single_channel=single_channel)
     for e in range(len(ords)):  # |p|^2 per cell, computed once before forking
         orc.fifs["A"].pnorm2(e)
     return orc
 
 
+# forked CPU workers (oracle port of the reference path, one BLAS thread each)
 _ORACLE = None
 _QUERIES = None
+_TOPK = 10
 
 
 def _cpu_query(i):
     from threadpoolctl import threadpool_limits
 
     with threadpool_limits(1):
-        res, _ = _ORACLE.query(_QUERIES[i], top_k=100, rerank=True)
+        res, _ = _ORACLE.query(_QUERIES[i], top_k=_TOPK, rerank=True)
     return len(res)
 
 
-def cpu_sample(orc, queries_host, n_procs, n_queries):
-    """Wall time of n_queries oracle queries on n_procs forked workers."""
+def cpu_sample(orc, queries_host, n_procs, n_queries, top_k):
+    """Wall time of n_queries oracle queries on n_procs forked workers (or
+    in this process, one BLAS thread, for n_procs = 1)."""
     import multiprocessing as mp
 
-    global _ORACLE, _QUERIES
-    _ORACLE, _QUERIES = orc, queries_host
+    global _ORACLE, _QUERIES, _TOPK
+    _ORACLE, _QUERIES, _TOPK = orc, queries_host, top_k
+    if n_procs == 1:
+        _cpu_query(0)  # warm
+        t0 = time.perf_counter()
+        for i in range(n_queries):
+            _cpu_query(i % len(queries_host))
+        return time.perf_counter() - t0
     ctx = mp.get_context("fork")
     with ctx.Pool(n_procs) as pool:
         pool.map(_cpu_query, [0] * min(n_procs, 2))  # warm the forked workers
@@ -301,164 +422,22 @@ def cpu_sample(orc, queries_host, n_procs, n_queries):
         return time.perf_counter() - t0
 
 
-def host_cores():
-    try:
-        return len(os.sched_getaffinity(0))
-    except AttributeError:
-        return os.cpu_count() or 1
-
-
-# ------------------------------------------------------------------ arms
-def run_reference(args, w):
-    ws, rank, local = dist_env()
-    if ws > 1 and rank != 0:
-        return
-    torch.cuda.set_device(local)
-    bundle, qs, _ = build(w, torch.device("cuda", local))  # setup only (not timed)
-    orc = host_oracle(bundle, w)
-    qh = qs[: max(64, w.batch)].cpu().numpy()
-    del bundle
-    torch.cuda.empty_cache()
-    cores = host_cores()
-    per_step = cores  # one query per worker per step
-    for _ in range(args.warmup):
-        cpu_sample(orc, qh, cores, min(cores, 4))
-    times = [cpu_sample(orc, qh, cores, per_step) for _ in range(args.steps)]
-    qps = per_step * len(times) / sum(times)
-    sample = (f"{per_step} queries/step x {len(times)} steps of config {w.name} "
-              f"(single-channel oracle port of query_fif+rerank_scores, gaussian via GEMV)")
-    line = {"impl": "reference", "metric": METRIC, "value": qps, "unit": UNIT, "n_gpus": ws,
-            "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000 * sum(times) / len(times), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": w.name, "n_shapes": w.n_shapes, "n_views": w.n_views,
-                       "dim": w.dim, "K": w.K, "ma": w.ma, "sigma": w.sigma, "top_k": w.top_k},
-            "cpu_baseline": {"value": qps, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": sample},
-            "e2e": {"value": qps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
-
-
-def run_c5(args):
-    """Config 5 (re-rank dominated): given top-50 lists for 1M shapes, S-IF
-    over all shapes, queries re-ranked with k = 50 neighbour-set Jaccard."""
-    from paper_1604_01879_b200 import build_index_from_lists
-
-    ws, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    device = torch.device("cuda", local)
-    c = synth.C5
-    n = args.c5_shapes or c["n_shapes"]
-    idx, val = synth.community_lists(SEED, device, n_shapes=n)
-    cfg = IndexConfig(k1=c["list_len"], k2=c["k2"], imported=True, batch_size=c["batch"])
-    t0 = time.perf_counter()
-    bundle = build_index_from_lists(idx, val, synth.shape_ids(n), cfg)
-    torch.cuda.synchronize()
-    build_s = time.perf_counter() - t0
-    eng = bundle.engine
-    g = torch.Generator(device=device)
-    g.manual_seed(SEED + 5)
-    B = c["batch"]
-    qrows = torch.randint(0, n, (B * (args.steps + args.warmup),), generator=g, device=device)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-
-    def step(i):
-        r = qrows[(i % args.warmup) * B:(i % args.warmup + 1) * B]
-        eng.rerank_lists(idx[r], val[r], top_k=c["top_k"], self_local=r.to(torch.int32))
-
-    with ClockSampler(local) as clk:
-        warm(step, args.warmup)
-        ev[0].record()
-        for i in range(args.warmup, args.warmup + args.steps):
-            r = qrows[i * B:(i + 1) * B]
-            eng.rerank_lists(idx[r], val[r], top_k=c["top_k"], self_local=r.to(torch.int32))
-        ev[1].record()
-        torch.cuda.synchronize()
-    ms = ev[0].elapsed_time(ev[1])
-    per_step = count_launches(lambda: step(0))
-    line = {"metric": METRIC, "value": B * args.steps / (ms / 1000), "unit": UNIT, "n_gpus": ws,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic",
-            "config": {"workload": "c5", "n_shapes": n, "list_len": c["list_len"],
-                       "communities": c["communities"], "k2": c["k2"], "top_k": c["top_k"],
-                       "batch": B, "sif_postings": int(bundle.sif.dev.e_ord.numel()),
-                       "build_s": build_s},
-            "e2e": None, "gpu_launches": per_step * args.steps, "roofline": None,
-            "cpu_baseline": None,
-            "clocks": clk.summary()}
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-
-
-def run_sharded(args, w):
-    """Database sharded by shape over the ranks (dist.py): every rank holds
-    N / G shapes (all cells), queries are replicated, per-shard top-k2 and
-    top-k candidates are merged with NCCL all_gather_into_tensor."""
-    from paper_1604_01879_b200 import engine as eg2
-    from paper_1604_01879_b200.dist import ShardedEngine, build_sharded, shard_bounds
-
-    ws, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    device = torch.device("cuda", local)
-    if ws > 1:
-        dist.init_process_group("nccl", device_id=device)
-    else:
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        os.environ.setdefault("MASTER_PORT", "29533")
-        dist.init_process_group("gloo", rank=0, world_size=1)
-    if w.storage == "float16":
-        db, qs, Ct = synth.zipf_mixture(w, SEED, device)
-        C = Ct.cpu().numpy()
-    else:
-        db, qs, _ = synth.mixture(w, SEED, device)
-        C = synth.sample_centroids(db, w.K, SEED + 1).cpu().numpy()
-    lo, hi = shard_bounds(w.n_shapes, ws, rank)
-    X = db[lo:hi].contiguous()
-    del db
-    torch.cuda.empty_cache()
-    cfg = IndexConfig(n_views=w.n_views, codebook_size=w.K, ma=w.ma, k1=w.k1, k2=w.k2,
-                      similarity="gaussian", sigma=w.sigma, storage_dtype=w.storage,
-                      batch_size=w.batch, imported=True)
-    t0 = time.perf_counter()
-    fif, raw, sif = build_sharded(X, eg2.DeviceCodebook.from_numpy(C), cfg, w.n_shapes)
-    torch.cuda.synchronize()
-    build_s = time.perf_counter() - t0
-    del X
-    idrank = torch.arange(w.n_shapes, dtype=torch.int32, device=device)  # zero-padded ids
-    eng = ShardedEngine(fif, raw, sif, idrank, cfg, w.n_shapes)
-    B = w.batch
-    nb = max(1, qs.shape[0] // B)
-    batches = [qs[j * B:(j + 1) * B].contiguous() for j in range(nb)]
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    with ClockSampler(local) as clk:
-        warm(lambda i: eng.run(batches[i % nb], w.top_k), args.warmup)
-        dist.barrier()
-        torch.cuda.synchronize()
-        ev[0].record()
-        for i in range(args.steps):
-            eng.run(batches[(args.warmup + i) % nb], w.top_k)
-        ev[1].record()
-        torch.cuda.synchronize()
-        dist.barrier()
-    t = torch.tensor([ev[0].elapsed_time(ev[1])], dtype=torch.float64, device=device)
-    if ws > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    if rank == 0:
-        line = {"metric": METRIC, "value": B * args.steps / (ms / 1000.0), "unit": UNIT,
-                "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
-                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": {"workload": w.name, "n_shapes": w.n_shapes, "parallelism":
-                           f"shard{ws}", "batch": B, "top_k": w.top_k, "build_s": build_s},
-                "e2e": None, "gpu_launches": None, "roofline": None, "cpu_baseline": None,
-                "clocks": clk.summary()}
-        print(json.dumps(line), flush=True)
-    dist.destroy_process_group()
+def _gpu_line(args, config, value, ms, scaling, e2e, launches, roofline, cpu, clk, run,
+              dtype="f32"):
+    ws, _, _ = dist_env()
+    return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": scaling, "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+            "config": config, "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
+            "cpu_baseline": cpu, "clocks": clk, "run": run}
 
 
 def run_gift(args, w):
+    """One index per rank: configs 1-2 at any N (replicas: disjoint query
+    streams, no collective), other configs at N = 1."""
+    from paper_1604_01879_b200 import query_many
+    from paper_1604_01879_b200.index import lane_streams
+
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
@@ -473,7 +452,7 @@ def run_gift(args, w):
     stream = torch.cuda.current_stream()
     # batch i runs on lane i % L: its own stream and scratch, so one batch's
     # quantize / reduce / re-rank kernels overlap the other batch's scan
-    lanes_default, reserve_default = DEFAULT_LANES.get(w.name, (1, 0))
+    lanes_default, reserve_default = default_lanes(w.name)
     L = max(1, args.lanes if args.lanes is not None else lanes_default)
     lanes = [stream] if L == 1 else lane_streams(L)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -482,12 +461,9 @@ def run_gift(args, w):
     for i, (a, b) in enumerate(scan_ev):  # torch creates CUDA events lazily, on first record
         a.record(lanes[i % L])
         b.record(lanes[i % L])
-
-    # SMs the scan leaves to the other lanes' kernels (DEFAULT_LANES)
-    if args.reserve_sms is not None:
-        eng.reserve_sms = args.reserve_sms
-    else:
-        eng.reserve_sms = reserve_default if L > 1 else 0
+    # SMs the scan leaves to the other lanes' kernels
+    eng.reserve_sms = (args.reserve_sms if args.reserve_sms is not None
+                       else (reserve_default if L > 1 else 0))
 
     def step(i, bi, sev=None):
         s = lanes[i % L]
@@ -514,30 +490,28 @@ def run_gift(args, w):
         torch.cuda.synchronize()
         if ws > 1:
             dist.barrier()
-        # the scan's own duration: with batches in flight a scan's events also
-        # span its wait behind the previous batch's scan, so the kernel time
-        # for the roofline comes from the same batches run one at a time
-        # right after (CUDA events on the launching stream, inside the sampler)
-        if L > 1:
-            reserve, eng.reserve_sms = eng.reserve_sms, 0
-            serial_ev = [(torch.cuda.Event(enable_timing=True),
-                          torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-            for a, b in serial_ev:
-                a.record(stream)
-                b.record(stream)
-            torch.cuda.synchronize()
-            for i in range(args.steps):
-                eng.run(batches[order[args.warmup + i]], top_k=w.top_k, rerank=True,
-                        scan_events=serial_ev[i])
-            torch.cuda.synchronize()
-            eng.reserve_sms = reserve
-        else:
-            serial_ev = scan_ev
     ms = ev[0].elapsed_time(ev[1])
     launches_per_step = count_launches(
         lambda: eng.run(batches[order[args.warmup]], top_k=w.top_k, rerank=True))
-    scan_ms = [a.elapsed_time(b) for a, b in serial_ev]
-    scan_ms_overlapped = [a.elapsed_time(b) for a, b in scan_ev]
+    # with batches in flight a scan's events also span its wait behind another
+    # lane's scan: the kernel's own duration comes from the same batches run
+    # one at a time right after, with the timed run's configuration (the same
+    # SMs left to other lanes), inside the clock sampler's run
+    scan_in_flight = [a.elapsed_time(b) for a, b in scan_ev]
+    if L > 1:
+        serial_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                     for _ in range(args.steps)]
+        for a, b in serial_ev:
+            a.record(stream)
+            b.record(stream)
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            eng.run(batches[order[args.warmup + i]], top_k=w.top_k, rerank=True,
+                    scan_events=serial_ev[i])
+        torch.cuda.synchronize()
+        scan_ms = [a.elapsed_time(b) for a, b in serial_ev]
+    else:
+        scan_ms = scan_in_flight
     t = torch.tensor([ms], dtype=torch.float64, device=device)
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -549,8 +523,7 @@ def run_gift(args, w):
     host = torch.empty((args.steps * B, w.n_views, w.dim), dtype=torch.float32, pin_memory=True)
     for i in range(args.steps):
         host[i * B:(i + 1) * B].copy_(batches[order[args.warmup + i]])
-    query_many(bundle, host[:L * B], top_k=w.top_k, lanes=L,
-               reserve_sms=eng.reserve_sms)  # warm
+    query_many(bundle, host[:L * B], top_k=w.top_k, lanes=L, reserve_sms=eng.reserve_sms)  # warm
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -562,39 +535,22 @@ def run_gift(args, w):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_value = total_q / float(t.item())
 
-    # ---- roofline of the dominant kernel (F-IF scan)
-    work = [scan_work(eng, batches[order[args.warmup + i]], w, w.top_k) for i in range(args.steps)]
+    # ---- roofline of the dominant kernel (F-IF scan), per launch
+    work = [scan_work(eng.fa, batches[order[args.warmup + i]], w, w.top_k)
+            for i in range(args.steps)]
     nbytes = sum(x[0] for x in work) / len(work)
     flops = sum(x[1] for x in work) / len(work)
-    scan_avg_ms = sum(scan_ms) / len(scan_ms)
-    peak, peak_kind = measured_peaks()
-    tpeak = measured_tensor_peak()
-    scan_s = scan_avg_ms / 1000.0
-    achieved = nbytes / scan_s / 1e9
-    achieved_tf = flops / scan_s / 1e12
-    # roofline: the slower of the HBM time and the tensor time of the
-    # algorithmic work; the fp32 split runs 2 (fp16 storage)
-    # or 3 (f32) fp16 MMA products per algorithmic product on the tensor cores
-    t_hbm = nbytes / (peak * 1e9)
-    t_tc = flops / (tpeak * 1e12)
-    split = 2 if w.storage == "float16" else 3
-    if t_tc > t_hbm:
-        roofline = {"bound": "tensor", "achieved": achieved_tf, "peak": tpeak, "unit": "TFLOP/s",
-                    "frac": achieved_tf / tpeak}
-    else:
-        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": achieved / peak}
-    roofline.update({"kernel": "fif_scan_tc_kernel", "peak_source": peak_kind,
-                     "traffic": load_traffic(w.name), "alg_bytes_per_launch": nbytes,
-                     "alg_flops_per_launch": flops, "scan_ms_avg": scan_avg_ms,
-                     "scan_ms_measured": ("serial pass over the timed batches" if L > 1
-                                          else "timed region"),
-                     "scan_ms_avg_in_flight": sum(scan_ms_overlapped) / len(scan_ms_overlapped),
-                     "scan_share_of_step": scan_avg_ms * args.steps / ms,
-                     "achieved_gbs": achieved, "hbm_frac": achieved / peak,
-                     "achieved_tflops": achieved_tf, "tensor_frac": achieved_tf / tpeak,
-                     "fp16_mma_products_per_alg_product": split,
-                     "tensor_pipe_frac_incl_split": achieved_tf * split / tpeak})
+    scan_avg = sum(scan_ms) / len(scan_ms)
+    roof = roofline_of(nbytes, flops, scan_avg, w, "fif_scan_tc_kernel",
+                       ("CUDA events around each scan launch, the timed batches re-run one "
+                        f"at a time with the timed configuration ({eng.reserve_sms} SMs left "
+                        "to other lanes)") if L > 1 else
+                       "CUDA events around each scan launch inside the timed region")
+    roof["scan_ms_in_flight_avg"] = sum(scan_in_flight) / len(scan_in_flight)
+    roof["scan_share_of_step"] = scan_avg * args.steps / ms
+    # lower bound independent of overlap: the scan's algorithmic bytes per
+    # timed step (every step runs one scan) over the whole step time
+    roof["achieved_gbs_per_step_lower_bound"] = nbytes / (ms / args.steps / 1000.0) / 1e9
     ncu = load_ncu(w.name)
     quant_ncu = ({"kernel": ncu["quantize_kernel"], "tensor_hmma_active_pct":
                   ncu["quantize_tensor_hmma_active_pct"], "source": "ncu --set full"}
@@ -605,35 +561,377 @@ def run_gift(args, w):
         orc = host_oracle(bundle, w)
         qh = batches[0].cpu().numpy()
         cores = host_cores()
-        n = cores
-        wall = cpu_sample(orc, qh, cores, n)
-        cpu = {"value": n / wall, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"{n} config-{w.name} queries on {cores} forked workers "
-                         f"(oracle port of query_fif+rerank_scores, single channel)"}
+        wall = cpu_sample(orc, qh, cores, cores, w.top_k)
+        cpu = {"value": cores / wall, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{cores} config-{w.name} queries on {cores} forked workers, one BLAS "
+                         f"thread each (oracle port of query_fif + rerank_scores + ranking, "
+                         f"single channel, over the GPU-built lists)", "host": host_info()}
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                "dtype": "f32", "data": "synthetic",
-                "config": {"workload": w.name, "n_shapes": w.n_shapes, "n_views": w.n_views,
-                           "dim": w.dim, "K": w.K, "ma": w.ma, "similarity": "gaussian",
-                           "sigma": w.sigma, "k1": w.k1, "k2": w.k2, "top_k": w.top_k,
-                           "batch": B, "parallelism": f"replicas{ws}",
-                           "lanes": L, "scan_reserved_sms": eng.reserve_sms,
-                           "storage": w.storage, "n_queries": w.n_queries,
-                           "l2": "inputs larger than L2 (database >= 10.5 GB)",
-                           "features": "planes only (streamed build)" if eng.fa.feat is None
-                           else "storage copy + planes",
-                           "build_s": build_s},
-                "e2e": {"value": e2e_value, "unit": UNIT,
-                        "h2d_bytes_per_step": B * w.n_views * w.dim * 4,
-                        "d2h_bytes_per_step": B * w.top_k * 12},
-                "gpu_launches": launches_per_step * args.steps,
-                "roofline": roofline, "quantize": quant_ncu, "cpu_baseline": cpu,
-                "clocks": clk.summary()}
+        run = {"lanes": L, "scan_reserved_sms": eng.reserve_sms, "build_s": build_s,
+               "features": ("planes only (streamed build)" if eng.fa.feat is None
+                            else "storage copy + planes"), "quantize": quant_ncu}
+        line = _gpu_line(args, workload_config(w, f"replicas{ws}" if ws > 1 else "single"),
+                         value, ms_max / args.steps, "weak",
+                         {"value": e2e_value, "unit": UNIT,
+                          "h2d_bytes_per_step": B * w.n_views * w.dim * 4,
+                          "d2h_bytes_per_step": B * w.top_k * 12},
+                         launches_per_step * args.steps, roof, cpu, clk.summary(), run)
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _init_dist(device):
+    ws, _, _ = dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=device)
+    else:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(_free_port()))
+        dist.init_process_group("gloo", rank=0, world_size=1)
+
+
+def _timed_sharded(args, device, run_batch, n_batches, local):
+    """Warm-up, then K steps bracketed by barrier + synchronize, device
+    events; returns (max-over-ranks ms, clocks)."""
+    ws, _, _ = dist_env()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    with ClockSampler(local) as clk:
+        warm(lambda i: run_batch(i % n_batches), args.warmup)
+        dist.barrier()
+        torch.cuda.synchronize()
+        ev[0].record()
+        for i in range(args.steps):
+            run_batch((args.warmup + i) % n_batches)
+        ev[1].record()
+        torch.cuda.synchronize()
+        dist.barrier()
+    t = torch.tensor([ev[0].elapsed_time(ev[1])], dtype=torch.float64, device=device)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item()), clk.summary()
+
+
+def _e2e_sharded(device, host_batches, run_dev):
+    """End to end through the sharded engine: every step copies its pinned
+    host batch in, runs, and copies the merged top-k out (all inside)."""
+    ws, _, _ = dist_env()
+    bufs = [torch.empty_like(host_batches[0], device=device) for _ in range(2)]
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    outs = []
+    for i, hb in enumerate(host_batches):
+        buf = bufs[i % 2]
+        buf.copy_(hb, non_blocking=True)
+        idx, val = run_dev(buf)
+        outs.append((idx.to("cpu", non_blocking=True), val.to("cpu", non_blocking=True)))
+    torch.cuda.synchronize()
+    dist.barrier()
+    e2e = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=device)
+    if ws > 1:
+        dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
+    return float(e2e.item())
+
+
+def run_sharded(args, w):
+    """Database sharded by shape over the ranks (dist.py): every rank holds
+    N / G shapes (all cells), queries are replicated, per-shard top-k2 and
+    top-k candidates are merged with one packed NCCL all_gather each.  Every
+    rank generates the seeded database itself (no broadcast of the
+    self-join's query blocks)."""
+    from paper_1604_01879_b200 import IndexConfig
+    from paper_1604_01879_b200 import engine as eg
+    from paper_1604_01879_b200.dist import ShardedEngine, build_sharded, shard_bounds
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    _init_dist(device)
+    cfg = IndexConfig(n_views=w.n_views, codebook_size=w.K, ma=w.ma, k1=w.k1, k2=w.k2,
+                      similarity="gaussian", sigma=w.sigma, storage_dtype=w.storage,
+                      batch_size=w.batch, imported=True)
+    lo, hi = shard_bounds(w.n_shapes, ws, rank)
+    t0 = time.perf_counter()
+    db = None
+    if w.name.startswith("c3"):
+        mix = synth.BlockMixture(w, SEED, device)
+        C = synth.sample_centroids_rows(mix, w.K, SEED + 1).cpu().numpy()
+        qs = mix.queries()
+        X = mix.rows(lo, hi).to(cfg.torch_storage)
+        query_views = mix.rows
+    else:
+        db, qs, C = generate(w, device)
+        X = db[lo:hi].contiguous()
+        query_views = lambda s0, s1: db[s0:s1]  # noqa: E731
+    fif, raw, sif = build_sharded(X, eg.DeviceCodebook.from_numpy(C), cfg, w.n_shapes,
+                                  batch=w.batch, query_views=query_views)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    del X, query_views, db
+    torch.cuda.empty_cache()
+    idrank = torch.arange(w.n_shapes, dtype=torch.int32, device=device)  # zero-padded ids
+    eng = ShardedEngine(fif, raw, sif, idrank, cfg, w.n_shapes)
+    B = w.batch
+    nb = max(1, qs.shape[0] // B)
+    batches = [qs[j * B:(j + 1) * B].contiguous() for j in range(nb)]
+    ms, clk = _timed_sharded(args, device, lambda j: eng.run(batches[j], w.top_k), nb, local)
+    launches = count_launches(lambda: eng.run(batches[0], w.top_k))
+    steps = [batches[(args.warmup + i) % nb].cpu().pin_memory() for i in range(args.steps)]
+    e2e_s = _e2e_sharded(device, steps, lambda q: eng.run(q, w.top_k))
+    ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    for e in ev:  # torch creates CUDA events lazily, on first record
+        e.record()
+    sms = []
+    for i in range(min(args.steps, 4)):
+        eng.runner.score(fif, batches[i % nb], w.ma, eng.mode, w.sigma, cand_k=min(w.k2, 8),
+                         dense=False, scan_events=ev)
+        torch.cuda.synchronize()
+        sms.append(ev[0].elapsed_time(ev[1]))
+    work = [scan_work(fif, batches[i % nb], w, w.top_k) for i in range(min(args.steps, 4))]
+    roof = roofline_of(sum(x[0] for x in work) / len(work), sum(x[1] for x in work) / len(work),
+                       sum(sms) / len(sms), w, "fif_scan_tc_kernel (this rank's shard)",
+                       "CUDA events around the shard's scan, batches run one at a time")
+    if rank == 0:
+        total_q = B * args.steps
+        line = _gpu_line(args, workload_config(w, f"shard{ws}"), total_q / (ms / 1000.0),
+                         ms / args.steps, "strong",
+                         {"value": total_q / e2e_s, "unit": UNIT,
+                          "h2d_bytes_per_step": B * w.n_views * w.dim * 4,
+                          "d2h_bytes_per_step": B * w.top_k * 12},
+                         launches * args.steps, roof, None, clk,
+                         {"build_s": build_s, "shard_shapes": hi - lo,
+                          "collectives_per_step": 2 if ws > 1 else 0,
+                          "exchange": "packed all_gather_into_tensor (score bits, "
+                                      "ordinal << 32 | tiebreak) + gift_topk_cand_tb merge"})
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
+def run_c5(args):
+    """Config 5 (re-rank dominated): given top-50 lists for 1M shapes, S-IF
+    over all shapes, queries re-ranked with k = 50 neighbour-set Jaccard.
+    N > 1 (or --shard): the S-IF sharded by shape, one packed all-gather of
+    the per-shard top-100 per batch."""
+    from paper_1604_01879_b200 import IndexConfig, build_index_from_lists
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    c = synth.C5
+    n = args.c5_shapes or c["n_shapes"]
+    idx, val = synth.community_lists(SEED, device, n_shapes=n, communities=c5_communities(n))
+    cfg = IndexConfig(k1=c["list_len"], k2=c["k2"], imported=True, batch_size=c["batch"])
+    g = torch.Generator(device=device)
+    g.manual_seed(SEED + 5)
+    B = c["batch"]
+    nsteps = args.steps + args.warmup
+    qrows = torch.randint(0, n, (B * nsteps,), generator=g, device=device)
+    sharded = ws > 1 or args.shard
+    bundle = None
+    t0 = time.perf_counter()
+    if sharded:
+        from paper_1604_01879_b200.dist import ShardedEngine, build_sharded_from_lists
+
+        _init_dist(device)
+        raw, sif = build_sharded_from_lists(idx, val, cfg)
+        eng = ShardedEngine(None, raw, sif, torch.arange(n, dtype=torch.int32, device=device),
+                            cfg, n)
+
+        def run_q(qi, qv, r):
+            return eng.rerank_lists(qi, qv, c["top_k"], self_global=r)
+        postings = int(sif.e_ord.numel())
+    else:
+        bundle = build_index_from_lists(idx, val, synth.shape_ids(n), cfg)
+        eng = bundle.engine
+
+        def run_q(qi, qv, r):
+            return eng.rerank_lists(qi, qv, top_k=c["top_k"], self_local=r.to(torch.int32))
+        postings = int(bundle.sif.dev.e_ord.numel())
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    rows = [qrows[i * B:(i + 1) * B] for i in range(nsteps)]
+    step = lambda j: run_q(idx[rows[j]], val[rows[j]], rows[j])  # noqa: E731
+    if sharded:
+        ms, clk = _timed_sharded(args, device, step, nsteps, local)
+    else:
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        with ClockSampler(local) as clk_s:
+            warm(lambda i: step(i % args.warmup), args.warmup)
+            ev[0].record()
+            for i in range(args.warmup, nsteps):
+                step(i)
+            ev[1].record()
+            torch.cuda.synchronize()
+        ms, clk = ev[0].elapsed_time(ev[1]), clk_s.summary()
+    launches = count_launches(lambda: step(0))
+    # e2e: each step's given lists come from pinned host memory, results go back
+    host = [(idx[r].cpu().pin_memory(), val[r].cpu().pin_memory(), r.cpu().pin_memory())
+            for r in rows[args.warmup:]]
+    if sharded:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for hi_, hv, hr in host:
+        oi, ov = run_q(hi_.to(device, non_blocking=True), hv.to(device, non_blocking=True),
+                       hr.to(device, non_blocking=True))
+        oi.to("cpu", non_blocking=True)
+        ov.to("cpu", non_blocking=True)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if sharded:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    cpu = None
+    if rank == 0 and bundle is not None and not args.no_cpu_baseline:
+        cpu = c5_cpu_baseline(bundle, idx, val, rows[args.warmup], c)
+    if rank == 0:
+        L = c["list_len"]
+        line = _gpu_line(args, c5_config(c, n, f"shard{ws}" if sharded else "single"),
+                         B * args.steps / (ms / 1000.0), ms / args.steps,
+                         "strong" if sharded else "weak",
+                         {"value": B * args.steps / e2e_s, "unit": UNIT,
+                          "h2d_bytes_per_step": B * (L * 12 + 8),
+                          "d2h_bytes_per_step": B * c["top_k"] * 12},
+                         launches * args.steps, None, cpu, clk,
+                         {"build_s": build_s, "sif_postings": postings}, dtype="f64")
+        print(json.dumps(line), flush=True)
+    if sharded:
+        dist.destroy_process_group()
+
+
+_C5 = None
+
+
+def _c5_query(i):
+    import oracle
+
+    raw, sif, ids, qi, qv, r, n, c = _C5
+    scores = np.zeros(n)
+    scores[qi[i]] = qv[i]
+    nb = oracle.top_neighbors(scores, c["k2"])
+    f = oracle.mean_activation(raw, nb)
+    fin = oracle.query_sif(sif, oracle.aggregate(f, f, 0.5))
+    return oracle.lexsort_rank(fin, ids, ids[r[i]], c["top_k"])[:1].tolist()
+
+
+def c5_cpu_baseline(bundle, idx, val, rows, c):
+    """The reference's query-time path for config 5 (index.py:249-299 from
+    given lists: top_neighbors over the dense score row, mean_activation,
+    aggregate, query_sif, lexsort ranking over all shapes) on the host cores,
+    over the GPU-built raw activations and S-IF (oracle port, forked
+    workers)."""
+    import multiprocessing as mp
+
+    import oracle
+
+    global _C5
+    raw = [oracle.Act(a.indices, a.values, a.norm) for a in bundle.raw_activations["A"]]
+    sif = oracle.Sif(norms=bundle.sif.norms, entry_ordinals=bundle.sif.entry_ordinals,
+                     entry_values=bundle.sif.entry_values)
+    ids = np.asarray(bundle.shape_ids)
+    r = rows.cpu().numpy()
+    _C5 = (raw, sif, ids, idx[rows].cpu().numpy(), val[rows].cpu().numpy(), r, len(raw), c)
+    cores = host_cores()
+    nq = 2 * cores
+    with mp.get_context("fork").Pool(cores) as pool:
+        pool.map(_c5_query, [0] * cores)
+        t0 = time.perf_counter()
+        pool.map(_c5_query, [i % len(r) for i in range(nq)], chunksize=1)
+        wall = time.perf_counter() - t0
+    return {"value": nq / wall, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{nq} config-5 queries on {cores} forked workers (oracle port of "
+                      f"rerank_scores + ranking over dense rows of all shapes, GPU-built S-IF)",
+            "host": host_info()}
+
+
+# ------------------------------------------------------------------ reference arm
+def reference_index(w, device):
+    """The index of configs 1-2 built on the HOST by the oracle: the seeded
+    workload (the GPU arm's own generator; torch only), every view quantized
+    bit-exactly, the lists laid out, the full f64 self-join, co-augment and
+    the S-IF (oracle/scale.py).  No product code runs."""
+    import oracle
+    from oracle import scale
+
+    db, qs, C = generate(w, device)
+    db_h = db.cpu().numpy()
+    qs_h = qs.cpu().numpy()
+    del db, qs
+    torch.cuda.empty_cache()
+    t0 = time.perf_counter()
+    idx = scale.OracleCsrIndex.from_views(db_h, C, w.ma, w.k1, w.k2, "gaussian", w.sigma)
+    build_s = time.perf_counter() - t0
+    off = idx.cell_off
+    ords = [idx.post_ord[off[c]:off[c + 1]] for c in range(w.K)]
+    feats = [idx.feat[off[c]:off[c + 1]] for c in range(w.K)]
+    ids = synth.shape_ids(w.n_shapes)
+    per = {}
+    for single in (True, False):
+        per[single] = oracle.OracleIndex.from_parts(
+            ids, C, ords, feats, idx.raw, idx.sif, ma=w.ma, k1=w.k1, k2=w.k2,
+            similarity="gaussian_expanded", sigma=w.sigma, single_channel=single)
+    for e in range(w.K):  # |p|^2 per cell, once, before forking (shared Fif)
+        per[True].fifs["A"].pnorm2(e)
+    return per, qs_h, build_s
+
+
+def run_reference(args, w):
+    ws, rank, local = dist_env()
+    if ws > 1 and rank != 0:
+        return
+    if w.name not in ("c1", "c2"):
+        print(json.dumps({"impl": "reference", "unavailable":
+                          f"config {w.name}: the host build of the reference index (bit-exact "
+                          "quantize of every view + the f64 self-join) takes hours; its CPU "
+                          "baseline is the GPU arm's cpu_baseline over GPU-built lists"}))
+        return
+    torch.cuda.set_device(local)
+    per, qh, build_s = reference_index(w, torch.device("cuda", local))
+    cores = host_cores()
+    orc = per[True]
+    for _ in range(args.warmup):
+        cpu_sample(orc, qh, cores, cores, w.top_k)
+    times = [cpu_sample(orc, qh, cores, cores, w.top_k) for _ in range(args.steps)]
+    qps = cores * len(times) / sum(times)
+    as_is_s = cpu_sample(per[False], qh, cores, cores, w.top_k)
+    lat_q = 2
+    lat_s = cpu_sample(orc, qh, 1, lat_q, w.top_k)
+    sample = (f"{cores} queries/step x {len(times)} steps of config {w.name} on {cores} forked "
+              f"workers, one BLAS thread each: the oracle port of the reference's query "
+              f"(quantize, query_fif with one f64 GEMV per probed cell, rerank_scores, lexsort "
+              f"ranking), single channel; over an index the oracle built on the host in "
+              f"{build_s:.0f} s")
+    line = {"impl": "reference", "metric": METRIC, "value": qps, "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000 * sum(times) / len(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(w, f"replicas{ws}" if ws > 1 else "single"),
+            "cpu_baseline": {"value": qps, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": sample, "host": host_info(),
+                             "as_is_two_channel_qps": cores / as_is_s,
+                             "latency_1core_ms": 1000 * lat_s / lat_q,
+                             "index_build_s": build_s},
+            "e2e": {"value": qps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ main
+def _relaunch(n):
+    """--gpus N without torchrun: one rank per GPU via torch.distributed.run."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
 
 
 def main():
@@ -646,26 +944,32 @@ def main():
     ap.add_argument("--c5-shapes", type=int, default=0, help="override config-5 N (smoke runs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--reserve-sms", type=int, default=None,
-                    help="SMs the scan leaves to other lanes (default per config, "
-                         "DEFAULT_LANES)")
+                    help="SMs the scan leaves to other lanes (default per config)")
     ap.add_argument("--lanes", type=int, default=None,
-                    help="batches in flight on separate streams (1 = serial; default "
-                         "per config, DEFAULT_LANES)")
+                    help="batches in flight on separate streams (1 = serial; default per config)")
     ap.add_argument("--shard", action="store_true",
-                    help="shard the database by shape over the ranks (configs 3/4)")
+                    help="shard the database by shape over the ranks (default for configs "
+                         "3-5 at N > 1)")
     args = ap.parse_args()
+    ws = int(os.environ.get("WORLD_SIZE", "0"))
+    if ws == 0 and args.gpus > 1:
+        _relaunch(args.gpus)
+    if ws and ws != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
     args.warmup = max(args.warmup, 3) if args.impl == "gift" else args.warmup
     if args.config == "c5":
         if args.impl == "reference":
-            print(json.dumps({"impl": "reference", "unavailable": "config 5 reference arm not "
-                              "provided (oracle S-IF build of 1M shapes takes hours)"}))
+            print(json.dumps({"impl": "reference", "unavailable":
+                              "config 5: the host build of the reference S-IF over 1M shapes "
+                              "(dict loops) takes tens of minutes; its CPU baseline is the GPU "
+                              "arm's cpu_baseline over the GPU-built S-IF"}))
             return
         run_c5(args)
         return
     w = synth.WORKLOADS[args.config]
     if args.impl == "reference":
         run_reference(args, w)
-    elif args.shard:
+    elif args.shard or (args.gpus > 1 and w.name not in ("c1", "c2")):
         run_sharded(args, w)
     else:
         run_gift(args, w)

@@ -71,9 +71,12 @@ extern "C" {
 #define GIFT_FIF_PAIR_OFF 1
 #define GIFT_FIF_PAIR_ON 2
 #define GIFT_FIF_PAIR(m) (((m) & 3) << GIFT_FIF_PAIR_SHIFT)
-#define GIFT_FIF_DRAIN_SHIFT 24         /* bits 24-26: D1 drain interval in    */
-#define GIFT_FIF_DRAIN_KB(n) (((n) & 7) << GIFT_FIF_DRAIN_SHIFT) /* k-blocks, */
-                                        /* 1..4 (0 = 4); > 4 is rejected       */
+#define GIFT_FIF_DRAIN_SHIFT 24         /* bits 24-28: D1 drain interval in    */
+#define GIFT_FIF_DRAIN_KB(n) (((n) & 31) << GIFT_FIF_DRAIN_SHIFT) /* 64-wide */
+                                        /* k-blocks, 1..16 (0 = the default:   */
+                                        /* 4, the 1e-5 contract at d = 4096)   */
+#define GIFT_FIF_RAW_ACCUM (1 << 29)    /* no truncation compensation of the   */
+                                        /* tensor-core accumulators (tests)    */
 
 typedef struct gift_fif_view {
   int32_t K;                 /* codebook size                                 */
@@ -385,6 +388,26 @@ int gift_sif_query_topk(const int64_t* e_off, const int32_t* e_ord,
                         const int32_t* self_local, int64_t ord_base, int32_t k,
                         int64_t max_touched, int32_t* out_idx, double* out_val,
                         void* ws, size_t ws_bytes, int32_t flags, void* stream);
+
+/* ---- exact set matching: replaces matching.exact_hausdorff_distance and
+ * matching.exact_similarity (matching.py:39-61).  For every (query set b,
+ * target set n): out[(b N + n) 3 + 0] = robust Hausdorff mean_v(1 - max_u
+ * q_v.p_u), [1] = standard max_v(1 - max_u q_v.p_u), [2] = exact similarity
+ * mean_v clip(max_u q_v.p_u, 0, 1), dots in f64.  Q [B, Vq, d], P [N, Vp,
+ * d] (dtype f32 or f64); q_cnt / p_cnt (optional) = views per set. */
+int gift_exact_sets(const void* Q, int32_t qdtype, const int32_t* q_cnt, int32_t B,
+                    int32_t Vq, const void* P, int32_t pdtype, const int32_t* p_cnt,
+                    int32_t N, int32_t Vp, int32_t d, double* out, void* stream);
+
+/* ---- evaluation ranks: the 1-based positions evaluate_index /
+ * exact_baseline_report give each relevant shape (index.py:317-357): for
+ * each query row b of scores [B, N] and each rel[b, r] >= 0,
+ * out_rank[b, r] = 1 + #{i != self_local[b] : key_i before key_j}, key =
+ * (score desc, idrank asc); NaN scores are excluded; -1 where rel is -1.
+ * R <= 4096. */
+int gift_eval_ranks(const double* scores, int32_t B, int64_t N, const int32_t* idrank,
+                    const int32_t* self_local, const int32_t* rel, int32_t R,
+                    int32_t* out_rank, void* stream);
 
 #ifdef __cplusplus
 }

@@ -16,6 +16,7 @@ from .index import (
     build_index_from_views,
     build_index_streamed,
     evaluate_index,
+    exact_baseline_report,
     load_bundle,
     query,
     query_batch,
@@ -37,6 +38,7 @@ __all__ = [
     "build_index_from_views",
     "build_index_streamed",
     "evaluate_index",
+    "exact_baseline_report",
     "load_bundle",
     "query",
     "query_batch",

@@ -27,7 +27,9 @@ FIF_QUANT_SIMT = 1 << 17
 FIF_REDUCE = {"auto": 0, "range": 1 << 18, "gather": 2 << 18, "owner": 3 << 18}
 FIF_SCHED_STATIC = 1 << 20
 FIF_PAIR = {"auto": 0, "off": 1 << 21, "on": 2 << 21}
-FIF_VARIANT_MASK = (1 << 16) | (1 << 17) | (3 << 18) | (1 << 20) | (3 << 21) | (7 << 24)
+FIF_RAW_ACCUM = 1 << 29
+FIF_VARIANT_MASK = ((1 << 16) | (1 << 17) | (3 << 18) | (1 << 20) | (3 << 21) | (31 << 24)
+                    | FIF_RAW_ACCUM)
 QUANT_SIMT = 1        # gift_quantize_ex flags
 SIF_ROWS, SIF_SORT = 1, 2  # gift_sif_query_topk flags
 
@@ -38,8 +40,8 @@ def fif_reserve_sms(n: int) -> int:
 
 
 def fif_drain_kb(n: int) -> int:
-    """GIFT_FIF_DRAIN_KB(n): flags bits 24-26 (1..4; 0 = the default 4)."""
-    return (int(n) & 7) << 24
+    """GIFT_FIF_DRAIN_KB(n): flags bits 24-28 (1..16; 0 = the default 4)."""
+    return (int(n) & 31) << 24
 
 _c_i32 = ctypes.c_int32
 _c_i64 = ctypes.c_int64
@@ -131,6 +133,9 @@ _SIGS = {
                                      _c_p, _c_i32, _c_i32, _c_p, _c_i32, _c_i64, _c_p, _c_p, _c_p,
                                      _c_i64, _c_i32, _c_i64, _c_p, _c_p, _c_p, _c_sz, _c_i32,
                                      _c_p]),
+    "gift_exact_sets": (_c_i32, [_c_p, _c_i32, _c_p, _c_i32, _c_i32, _c_p, _c_i32, _c_p, _c_i32,
+                                 _c_i32, _c_i32, _c_p, _c_p]),
+    "gift_eval_ranks": (_c_i32, [_c_p, _c_i32, _c_i64, _c_p, _c_p, _c_p, _c_i32, _c_p, _c_p]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -1207,8 +1207,8 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
                "out_scores may be NULL only with cand_k > 0");
   cudaStream_t st = as_stream(stream);
   GIFT_REQUIRE(f != nullptr, GIFT_ERR_INVALID, "null index");
-  GIFT_REQUIRE(((f->flags >> GIFT_FIF_DRAIN_SHIFT) & 7) <= 4, GIFT_ERR_INVALID,
-               "drain interval %d > 4 k-blocks", (f->flags >> GIFT_FIF_DRAIN_SHIFT) & 7);
+  GIFT_REQUIRE(((f->flags >> GIFT_FIF_DRAIN_SHIFT) & 31) <= 16, GIFT_ERR_INVALID,
+               "drain interval %d > 16 k-blocks", (f->flags >> GIFT_FIF_DRAIN_SHIFT) & 31);
   GIFT_REQUIRE(ma >= 1 && ma <= f->K, GIFT_ERR_INVALID, "ma must be in [1, %d]", f->K);
   GIFT_REQUIRE(mode == GIFT_SIM_COSINE || mode == GIFT_SIM_GAUSSIAN, GIFT_ERR_INVALID, "bad mode");
   GIFT_REQUIRE(mode != GIFT_SIM_GAUSSIAN || sigma > 0, GIFT_ERR_INVALID, "sigma must be > 0");
@@ -1275,9 +1275,10 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
     ta.has_lo = 0;
     // D1 drain interval (k-blocks): short tensor-core accumulation chains
     // hold the 1e-5 contract; at most 4
-    const int dkb = (f->flags >> GIFT_FIF_DRAIN_SHIFT) & 7;
+    const int dkb = (f->flags >> GIFT_FIF_DRAIN_SHIFT) & 31;
     ta.chunk_kb = dkb == 0 ? 4 : dkb;
     ta.dyn = (f->flags & GIFT_FIF_SCHED_STATIC) ? 0 : 1;
+    ta.tcomp = (f->flags & GIFT_FIF_RAW_ACCUM) ? 0 : 1;
     int rc2 = launch_scan_tc(f, Q, nprobes, ta, w.g1, w.g2, st, ev_scan_begin, ev_scan_end);
     if (rc2) return rc2;
   } else {

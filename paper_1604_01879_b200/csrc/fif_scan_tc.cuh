@@ -33,6 +33,7 @@ struct TcArgs {
   int has_lo;
   int chunk_kb;
   int dyn;       // items from the meta[M_WORK] counter (1) or a static CTA stride (0)
+  int tcomp;     // add back the expected truncation loss of each drained D1 chunk
 };
 
 bool tc_supported(const gift_fif_view* f);

@@ -125,15 +125,17 @@ class DeviceFif:
         self.variant = 0  # kernel-variant bits of gift_fif_view.flags (set_variant)
 
     def set_variant(self, scan: str = "tc", quant: str = "tc", reduce: str = "auto",
-                    pair: str = "auto", sched: str = "dynamic", drain_kb: int = 0):
+                    pair: str = "auto", sched: str = "dynamic", drain_kb: int = 0,
+                    raw_accum: bool = False):
         """Select kernel variants through the view flags (include/gift.h):
         scan/quant "tc" | "simt", reduce "auto" | "range" | "gather" | "owner",
-        pair "auto" | "on" | "off", sched "dynamic" | "static", drain_kb 0..4
-        (0 = default).  Defaults reproduce the measured-fastest choice."""
+        pair "auto" | "on" | "off", sched "dynamic" | "static", drain_kb 0..16
+        (0 = default), raw_accum (no truncation compensation; measurement
+        only).  Defaults reproduce the measured-fastest choice."""
         v = (nat.FIF_SCAN_SIMT if scan == "simt" else 0) | \
             (nat.FIF_QUANT_SIMT if quant == "simt" else 0) | nat.FIF_REDUCE[reduce] | \
             nat.FIF_PAIR[pair] | (nat.FIF_SCHED_STATIC if sched == "static" else 0) | \
-            nat.fif_drain_kb(drain_kb)
+            nat.fif_drain_kb(drain_kb) | (nat.FIF_RAW_ACCUM if raw_accum else 0)
         self.variant = v
         self.bind()
         return self

@@ -392,6 +392,10 @@ def build_index_from_lists(list_idx, list_scores, shape_ids, config: IndexConfig
     if n != len(shape_ids):
         raise ValueError("lists and shape_ids disagree on the number of shapes")
     k1, k2 = min(config.k1, L), min(config.k2, L)
+    srt = torch.sort(idx, dim=1).values  # a score row lists each shape once (rerank.py:64-75)
+    if bool(((srt[:, 1:] == srt[:, :-1]) & (srt[:, 1:] >= 0)).any()):
+        raise ValueError("neighbour lists must not repeat a shape within a row")
+    del srt
     raw = eg.act_from_topk(idx, val, k1)
     nbr = torch.where(val[:, :k2] > 0, idx[:, :k2], torch.full_like(idx[:, :k2], -1)).contiguous()
     final = eg.act_mean(raw, nbr)
@@ -648,55 +652,93 @@ def query_many(bundle: IndexBundle, views_host: torch.Tensor, top_k: int = 10,
 
 
 # ------------------------------------------------------------------ evaluation
+def _eval_ranks(eng, final: torch.Tensor, rows: torch.Tensor, rel_host: list) -> list:
+    """Ranks of each query's relevant shapes in its ranking (key: score desc,
+    shape id asc; the query itself excluded) -- libgift gift_eval_ranks."""
+    B = final.shape[0]
+    R = max(1, max(len(r) for r in rel_host))
+    rel = np.full((B, R), -1, dtype=np.int32)
+    for b, r in enumerate(rel_host):
+        rel[b, :len(r)] = r
+    rel_d = torch.from_numpy(rel).to(final.device)
+    out = torch.empty((B, R), dtype=torch.int32, device=final.device)
+    nat.call("gift_eval_ranks", nat.ptr(final.contiguous()), B, final.shape[1],
+             nat.ptr(eng.idrank), nat.ptr(rows.to(torch.int32).contiguous()), nat.ptr(rel_d), R,
+             nat.ptr(out), nat.stream_ptr())
+    ranks = out.cpu().numpy()
+    return [np.sort(ranks[b, :len(r)]) for b, r in enumerate(rel_host)]
+
+
+def _labelled_queries(bundle):
+    """index.py:320-327: class sizes; shapes of classes with >= 2 members are
+    queries, the others are skipped; relevant shapes = same class, not self."""
+    ids, labels = bundle.shape_ids, bundle.labels
+    lab = [labels.get(s, "") for s in ids]
+    groups = {}
+    for i, x in enumerate(lab):
+        groups.setdefault(x, []).append(i)
+    sizes = {x: len(g) for x, g in groups.items()}
+    keep = [i for i in range(len(ids)) if sizes[lab[i]] >= 2]
+    return lab, groups, sizes, keep, len(ids) - len(keep)
+
+
+def _device_report(bundle, scores_of, batch_size=None):
+    from . import evaluation as ev
+
+    eng = bundle.engine
+    lab, groups, sizes, keep, skipped = _labelled_queries(bundle)
+    dev = nat.device()
+    bs = batch_size or bundle.config.batch_size
+    per_query = []
+    for b0 in range(0, len(keep), bs):
+        sel = keep[b0:b0 + bs]
+        rows = torch.tensor(sel, dtype=torch.int64, device=dev)
+        final = scores_of(rows)
+        rel = [[j for j in groups[lab[i]] if j != i] for i in sel]
+        for i, ranks in zip(sel, _eval_ranks(eng, final, rows, rel)):
+            per_query.append(ev.metrics_from_ranks(ranks, sizes[lab[i]], lab[i]))
+    return ev.aggregate_report(per_query, n_skipped=skipped)
+
+
 def evaluate_index(bundle: IndexBundle, exact: bool = False, rerank: bool = True,
                    batch_size: int | None = None):
     """Every labelled database shape (class of >= 2) queried with its stored
     views, excluded from its own ranking, scored (index.py:317-333).  The
     queries run through the device pipeline in batches; each query's ranking
-    key (score desc, shape id asc) is resolved on the device as the 1-based
-    ranks of its relevant shapes: rank(j) = 1 + #{i != self : key_i < key_j}."""
-    from . import evaluation as ev
-
+    (score desc, shape id asc) is resolved on the device as the 1-based ranks
+    of its relevant shapes (gift_eval_ranks)."""
     eng = bundle.engine
     if eng.fa is None:
         raise Unsupported("evaluation needs the stored view features (F-IF)")
-    ids, labels = bundle.shape_ids, bundle.labels
-    lab = [labels.get(s, "") for s in ids]
-    sizes = {}
-    for x in lab:
-        sizes[x] = sizes.get(x, 0) + 1
-    keep = [i for i in range(eng.n) if sizes[lab[i]] >= 2]
-    skipped = eng.n - len(keep)
-    dev = nat.device()
-    codes = {x: c for c, x in enumerate(sorted(sizes))}
-    lab_dev = torch.tensor([codes[x] for x in lab], dtype=torch.int32, device=dev)
-    rank_dev = eng.idrank.to(torch.int64)
-    bs = batch_size or bundle.config.batch_size
-    per_query = []
-    for b0 in range(0, len(keep), bs):
-        rows = torch.tensor(keep[b0:b0 + bs], dtype=torch.int64, device=dev)
+
+    def scores_of(rows):
         Q, vq = eng.fa.shape_views(rows)  # query_by_id: stored views, cell-major
-        # the reference's query_by_id passes every stored view (no zero views)
         sa, sb = eng.scores(Q, None, vq=vq, ma=eng.fa.cb.K if exact else None)
-        final = eng.rerank(sa, sb) if rerank else (sa if sb is sa else (sa + sb) / 2.0)
-        B = rows.numel()
-        ar = torch.arange(B, device=dev)
-        final = final.clone()
-        final[ar, rows] = float("nan")  # the query itself leaves the ranking
-        own = lab_dev[rows]
-        for r in range(B):
-            s = final[r]
-            rel = torch.nonzero((lab_dev == own[r]) & (torch.arange(eng.n, device=dev) !=
-                                                       rows[r])).view(-1)
-            sv = s[rel][:, None]
-            rv = rank_dev[rel][:, None]
-            valid = ~torch.isnan(s)
-            better = (s[None, :] > sv) | ((s[None, :] == sv) & (rank_dev[None, :] < rv))
-            ranks = 1 + (better & valid[None, :]).sum(dim=1)
-            ranks = torch.sort(ranks).values.cpu().numpy()
-            i = keep[b0 + r]
-            per_query.append(ev.metrics_from_ranks(ranks, sizes[lab[i]], lab[i]))
-    return ev.aggregate_report(per_query, n_skipped=skipped)
+        return eng.rerank(sa, sb) if rerank else (sa if sb is sa else (sa + sb) / 2.0)
+
+    return _device_report(bundle, scores_of, batch_size)
+
+
+def exact_baseline_report(bundle: IndexBundle, channel: str = "B", variant: str = "robust",
+                          batch_size: int | None = None):
+    """Single-channel exact ranking over the database, scored (index.py:
+    336-357): each labelled shape's stored views of `channel` against every
+    shape's by exact_similarity (the scan with every view probing every cell:
+    mean over the query views of the best clamped cosine), ranked by (score
+    desc, id asc) without the query itself.  `variant` is accepted and, as in
+    the reference, does not change the similarity used."""
+    eng = bundle.engine
+    if channel not in CHANNELS:
+        raise ChannelMismatch(f"unknown channel {channel!r}")
+    fif = eng.fa if channel == "A" else eng.fb
+    if fif is None:
+        raise Unsupported("the exact baseline needs the stored view features (F-IF)")
+
+    def scores_of(rows):
+        Q, vq = fif.shape_views(rows)
+        return eng.runner.score(fif, Q, fif.cb.K, nat.SIM_COSINE, 0.5, vq=vq)
+
+    return _device_report(bundle, scores_of, batch_size)
 
 
 # ------------------------------------------------------------------ persistence

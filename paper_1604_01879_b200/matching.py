@@ -1,8 +1,8 @@
 """First inverted file: GPU build and batched scoring.
 
-Mirrors `shapesearch.matching` (matching.py:64-211): FirstInvertedFile,
-build_fif, query_fif, save_fif/load_fif.  The exact-Hausdorff helpers
-(matching.py:22-61) are outside the GPU path.
+Mirrors `shapesearch.matching` (matching.py:22-211): the exact set matching
+functions (exact_hausdorff_distance, exact_similarity, on libgift's f64
+gift_exact_sets), FirstInvertedFile, build_fif, query_fif, save_fif/load_fif.
 """
 
 from __future__ import annotations
@@ -87,6 +87,74 @@ class FirstInvertedFile:
             raise EmptySet(f"shape ordinal {ordinal} has no stored views")
         Q, _vq = self.dev.shape_views(torch.tensor([loc], device=self.dev.device))
         return Q[0].cpu().numpy()
+
+
+# ------------------------------------------------------------------ exact
+def _exact_operand(views):
+    """matching.py:22-26 `_as_matrix`: a non-empty 2-D view set (f32 values
+    keep f32 storage; anything else is widened to f64 like the reference)."""
+    if torch.is_tensor(views):
+        views = views.detach().cpu().numpy()
+    arr = np.asarray(views)
+    if arr.dtype != np.float32:
+        arr = arr.astype(np.float64)
+    if arr.ndim != 2 or arr.shape[0] == 0:
+        raise EmptySet("view set is empty")
+    return np.ascontiguousarray(arr)
+
+
+def exact_set_scores(query_sets, target_sets, q_counts=None, t_counts=None) -> torch.Tensor:
+    """Batched exact matching (new): query_sets [B, Vq, d], target_sets [N,
+    Vp, d] (host or device, f32/f64; the first q_counts[b] / t_counts[n]
+    views of each set are used) -> device f64 [B, N, 3] = (robust Hausdorff,
+    standard Hausdorff, exact similarity), matching.py:39-61 for every pair."""
+    dev = nat.device()
+
+    def prep(x):
+        t = x if torch.is_tensor(x) else torch.from_numpy(np.ascontiguousarray(x))
+        if t.dtype not in (torch.float32, torch.float64):
+            t = t.double()
+        return t.to(dev).contiguous()
+
+    Q, P = prep(query_sets), prep(target_sets)
+    if Q.dim() != 3 or P.dim() != 3:
+        raise ValueError("view sets must be [n_sets, n_views, d]")
+    if Q.shape[2] != P.shape[2]:
+        raise DimensionMismatch(f"view dims differ: {Q.shape[2]} vs {P.shape[2]}")
+    qc = None if q_counts is None else torch.as_tensor(q_counts, dtype=torch.int32).to(dev)
+    pc = None if t_counts is None else torch.as_tensor(t_counts, dtype=torch.int32).to(dev)
+    B, N = Q.shape[0], P.shape[0]
+    out = torch.empty((B, N, 3), dtype=torch.float64, device=dev)
+    code = {torch.float32: nat.GIFT_F32, torch.float64: nat.GIFT_F64}
+    nat.call("gift_exact_sets", nat.ptr(Q), code[Q.dtype], nat.ptr(qc), B, Q.shape[1],
+             nat.ptr(P), code[P.dtype], nat.ptr(pc), N, P.shape[1], Q.shape[2], nat.ptr(out),
+             nat.stream_ptr())
+    return out
+
+
+def _exact_pair(query_views, target_views):
+    q = _exact_operand(query_views)
+    p = _exact_operand(target_views)
+    if q.shape[1] != p.shape[1]:
+        raise DimensionMismatch(f"view dims differ: {q.shape[1]} vs {p.shape[1]}")
+    return exact_set_scores(q[None], p[None])[0, 0].cpu().numpy()
+
+
+def exact_hausdorff_distance(query_views, target_views, variant: str = "robust") -> float:
+    """Exact Hausdorff distance between two view sets with d = 1 - cosine
+    (matching.py:39-52): "standard" = max over query views of the min
+    distance, "robust" = their mean."""
+    if variant not in ("standard", "robust"):
+        _exact_pair(query_views, target_views)  # the reference validates the sets first
+        raise ValueError(f"unknown variant {variant!r}")
+    r = _exact_pair(query_views, target_views)
+    return float(r[1] if variant == "standard" else r[0])
+
+
+def exact_similarity(query_views, target_views) -> float:
+    """Mean over query views of the best clamped cosine in the target set
+    (matching.py:55-61)."""
+    return float(_exact_pair(query_views, target_views)[2])
 
 
 def _stack_views(viewsets, channel, dim):

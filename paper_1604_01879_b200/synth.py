@@ -221,6 +221,9 @@ def community_lists(seed: int, device, n_shapes=C5["n_shapes"], list_len=C5["lis
     without duplicates — with scores U(0, 1) sorted descending (assigned to a
     random permutation of the list).  Returns (idx [N, L] i32, scores [N, L]
     f64), best first."""
+    if n_shapes < 4 * communities * list_len:
+        raise ValueError("communities too small for duplicate-free lists: use about "
+                         f"{n_shapes // (4 * list_len)} or fewer for {n_shapes} shapes")
     g = torch.Generator(device=device)
     g.manual_seed(seed)
     comm = torch.randint(0, communities, (n_shapes,), generator=g, device=device)

@@ -338,6 +338,53 @@ def golden_eval():
         print("eval", name, "done")
 
 
+def golden_exact_sets():
+    """Reference exact_hausdorff_distance (both variants) and exact_similarity
+    (matching.py:39-61) on seeded view-set pairs: unit non-negative rows,
+    signed rows (negative cosines), unequal set sizes, identical sets; and
+    exact_baseline_report (index.py:336-357) on the evaluation corpora."""
+    import dataclasses
+
+    rng = np.random.default_rng(606)
+    out = {}
+    pairs = []
+    for i in range(24):
+        d = int(rng.choice([3, 16, 64, 257]))
+        vq, vp = int(rng.integers(1, 12)), int(rng.integers(1, 12))
+        if i % 3 == 0:
+            q, p = unit_nonneg_rows(rng, vq, d), unit_nonneg_rows(rng, vp, d)
+        elif i % 3 == 1:
+            q = rng.standard_normal((vq, d))
+            p = rng.standard_normal((vp, d))
+            q /= np.linalg.norm(q, axis=1, keepdims=True)
+            p /= np.linalg.norm(p, axis=1, keepdims=True)
+        else:
+            q = unit_nonneg_rows(rng, vq, d)
+            p = q.copy()
+        pairs.append((q, p))
+    for i, (q, p) in enumerate(pairs):
+        out[f"p{i}_q"], out[f"p{i}_p"] = q, p
+        out[f"p{i}_out"] = np.array([rmt.exact_hausdorff_distance(q, p, "robust"),
+                                     rmt.exact_hausdorff_distance(q, p, "standard"),
+                                     rmt.exact_similarity(q, p)])
+    out["n_pairs"] = np.array(len(pairs))
+    for case in EVAL_CASES:
+        (name, seed, N, V, d, classes, K, ma, k1, k2, sigma) = case
+        views, labels = mixture_views(seed, N, V, d, classes, sigma=sigma, zero_views=3)
+        db = views[:N]
+        ids = shape_ids(N)
+        C = sampled_codebook(db, K, seed + 1)
+        cfg = rix.IndexConfig(n_views=V, codebook_size=K, ma=ma, k1=k1, k2=k2, imported=True)
+        bundle = reference_bundle(db, ids, C, cfg)[0]
+        bundle = dataclasses.replace(bundle, labels={ids[i]: f"c{labels[i]}" for i in range(N)})
+        rep = rix.exact_baseline_report(bundle, channel="B")
+        out[f"{name}_metrics"] = np.array([rep.nn, rep.ft, rep.st, rep.map, rep.auc])
+        out[f"{name}_pr11"] = rep.pr11
+        out[f"{name}_counts"] = np.array([rep.n_queries, rep.n_skipped])
+    np.savez_compressed(os.path.join(HERE, "exact_sets.npz"), **out)
+    print("exact sets done")
+
+
 def golden_kmeans():
     """Reference train_codebook (codebook.py:64-108: k-means++ seeding, Lloyd
     iterations, empty-cluster repair) on the seeded sets of cases.py."""
@@ -407,6 +454,9 @@ def golden_ingest():
 
 
 if __name__ == "__main__":
+    if sys.argv[1:] == ["exact_sets"]:
+        golden_exact_sets()
+        sys.exit(0)
     if sys.argv[1:] == ["c1"]:
         golden_c1()
         sys.exit(0)
@@ -442,3 +492,4 @@ if __name__ == "__main__":
     golden_kmeans()
     golden_trained_bundle()
     golden_c1()
+    golden_exact_sets()

@@ -231,7 +231,9 @@ def _c5_oracle(idx_h, val_h, k1, k2):
 @pytest.mark.parametrize("n_shapes", [50_000])
 def test_c5_given_lists_against_oracle(n_shapes):
     c = synth.C5
-    idx, val = synth.community_lists(SEED, dev(), n_shapes=n_shapes)
+    # communities of ~500 members as at N = 1M (45 in-community picks per list)
+    idx, val = synth.community_lists(SEED, dev(), n_shapes=n_shapes,
+                                     communities=max(1, n_shapes // 500))
     ids = synth.shape_ids(n_shapes)
     cfg = gift.IndexConfig(k1=c["list_len"], k2=c["k2"], imported=True, batch_size=c["batch"])
     b = gift.build_index_from_lists(idx, val, ids, cfg)

@@ -92,7 +92,7 @@ def test_drain_interval_flag_validated():
         fif.dev.set_variant(drain_kb=kb)
         np.testing.assert_allclose(mt.query_fif_batch(fif, views[40:], 2, "gaussian").cpu().numpy(),
                                    base, rtol=RTOL)
-    fif.dev.set_variant(drain_kb=6)
+    fif.dev.set_variant(drain_kb=17)
     with pytest.raises(ValueError):
         mt.query_fif_batch(fif, views[40:], 2, "gaussian")
     fif.dev.set_variant()
