@@ -445,6 +445,8 @@ def run_gift(args, w):
         dist.init_process_group("nccl", device_id=device)
     bundle, qs, build_s = build(w, device)
     eng = bundle.engine
+    if args.drain_kb:
+        eng.fa.set_variant(drain_kb=args.drain_kb)
     B = w.batch
     nb = max(1, qs.shape[0] // B)
     order = [(rank + i * ws) % nb for i in range(args.steps + args.warmup)]
@@ -568,6 +570,7 @@ def run_gift(args, w):
                          f"single channel, over the GPU-built lists)", "host": host_info()}
     if rank == 0:
         run = {"lanes": L, "scan_reserved_sms": eng.reserve_sms, "build_s": build_s,
+               "drain_kb": args.drain_kb or "default",
                "features": ("planes only (streamed build)" if eng.fa.feat is None
                             else "storage copy + planes"), "quantize": quant_ncu}
         line = _gpu_line(args, workload_config(w, f"replicas{ws}" if ws > 1 else "single"),
@@ -947,6 +950,9 @@ def main():
                     help="SMs the scan leaves to other lanes (default per config)")
     ap.add_argument("--lanes", type=int, default=None,
                     help="batches in flight on separate streams (1 = serial; default per config)")
+    ap.add_argument("--drain-kb", type=int, default=0,
+                    help="scan accumulator drain interval in 64-wide k-blocks (0 = the "
+                         "library default)")
     ap.add_argument("--shard", action="store_true",
                     help="shard the database by shape over the ranks (default for configs "
                          "3-5 at N > 1)")

@@ -85,21 +85,25 @@ def fif_lists(views, assign, K: int):
     return cell_off, (rows // V).astype(np.int32), rows.astype(np.int64)
 
 
-def fif_scores_many(cell_off, post_ord, feat_of, Q, q_cells, n_shapes: int,
+def fif_scores_many(cell_off, post_ord, feat_rows, Q, q_cells, n_shapes: int,
                     similarity: str = "cosine", sigma: float = 0.5, vq=None,
-                    threads: int | None = None, pnorm2=None) -> np.ndarray:
+                    threads: int | None = None, pnorm2=None, cell_chunk: int = 1 << 17,
+                    shape_base: int = 0, return_best: bool = False) -> np.ndarray:
     """matching.py:136-161 for a batch of queries.
 
     cell_off/post_ord: the F-IF lists (ordinals ascending inside a cell, as
-    build_fif appends them); feat_of(c) -> [|c|, d] features of cell c (any
-    float dtype, widened to f64 like `F_e @ row`); Q: [B, V, d] query views;
-    q_cells: [B, V, ma] the views' cells (quantize; rows of zero views are
-    skipped, matching.py:150-151); vq: views per query to divide by
-    (default V: `total / q.shape[0]`).  similarity "cosine" = clip(q.p, 0, 1)
-    (matching.py:158); "gaussian" = exp(-|q - p|^2 / sigma^2) via
-    |q|^2 + |p|^2 - 2 q.p in f64 (north_star kernel, D1); pnorm2: optional
-    [P] f64 |p|^2 per posting (computed per cell otherwise).
-    Returns f64 [B, n_shapes]; never-visited shapes score exactly 0."""
+    build_fif appends them); feat_rows(p0, p1) -> [p1 - p0, d] features of
+    posting rows p0..p1 (any float dtype, widened to f64 like `F_e @ row`);
+    Q: [B, V, d] query views; q_cells: [B, V, ma] the views' cells (quantize;
+    rows of zero views are skipped, matching.py:150-151); vq: views per query
+    to divide by (default V: `total / q.shape[0]`).  similarity "cosine" =
+    clip(q.p, 0, 1) (matching.py:158); "gaussian" = exp(-|q - p|^2 / sigma^2)
+    via |q|^2 + |p|^2 - 2 q.p in f64 (north_star kernel, D1); pnorm2:
+    optional [P] f64 |p|^2 per posting row.  Cells are scored in chunks of
+    cell_chunk postings (a shape split across chunks keeps its max).  The
+    shapes are ordinals shape_base .. shape_base + n_shapes (a block of the
+    database).  Returns f64 [B, n_shapes] (never-visited shapes score
+    exactly 0), or with return_best the per-view maxima [B, V, n_shapes]."""
     Q = np.asarray(Q)
     B, V, d = Q.shape
     ma = q_cells.shape[2]
@@ -115,15 +119,17 @@ def fif_scores_many(cell_off, post_ord, feat_of, Q, q_cells, n_shapes: int,
     bounds = np.flatnonzero(np.r_[True, cells[1:] != cells[:-1], True]) if len(cells) else [0]
     inv_s2 = 1.0 / (sigma * sigma)
     qn2 = (Qf * Qf).sum(axis=1)
-
-    def cell_best(i):
-        a, b = bounds[i], bounds[i + 1]
-        c = int(cells[a])
+    work = []
+    for i in range(len(bounds) - 1):
+        c = int(cells[bounds[i]])
         p0, p1 = int(cell_off[c]), int(cell_off[c + 1])
-        if p1 == p0:
-            return None
-        F = np.asarray(feat_of(c), dtype=np.float64)
-        r = rows[a:b]
+        for a0 in range(p0, p1, cell_chunk):
+            work.append((i, a0, min(p1, a0 + cell_chunk)))
+
+    def chunk_best(item):
+        i, p0, p1 = item
+        F = np.asarray(feat_rows(p0, p1), dtype=np.float64)
+        r = rows[bounds[i]:bounds[i + 1]]
         G = Qf[r] @ F.T
         if similarity == "cosine":
             S = np.clip(G, 0.0, 1.0)
@@ -134,27 +140,26 @@ def fif_scores_many(cell_off, post_ord, feat_of, Q, q_cells, n_shapes: int,
             raise ValueError(f"unknown similarity {similarity!r}")
         o = np.asarray(post_ord[p0:p1])
         starts = np.flatnonzero(np.r_[True, o[1:] != o[:-1]])
-        return r, o[starts], np.maximum.reduceat(S, starts, axis=1)
+        return r, o[starts] - shape_base, np.maximum.reduceat(S, starts, axis=1)
 
     def merge(res):
-        if res is None:
-            return
         r, shapes, M = res
         ix = np.ix_(r, shapes)
         best[ix] = np.maximum(best[ix], M)
 
-    n_groups = len(bounds) - 1
     threads = threads or _threads()
-    if threads == 1 or n_groups < 4:
-        for i in range(n_groups):
-            merge(cell_best(i))
+    if threads == 1 or len(work) < 4:
+        for item in work:
+            merge(chunk_best(item))
     else:
         from threadpoolctl import threadpool_limits
 
-        # one BLAS thread per cell GEMM, cells spread over the host threads
+        # one BLAS thread per chunk GEMM, chunks spread over the host threads
         with threadpool_limits(1), ThreadPoolExecutor(threads) as ex:
-            for res in ex.map(cell_best, range(n_groups)):
+            for res in ex.map(chunk_best, work):
                 merge(res)
+    if return_best:
+        return best.reshape(B, V, n_shapes)
     total = best.reshape(B, V, n_shapes).sum(axis=1)
     div = np.full(B, float(V)) if vq is None else np.asarray(vq, dtype=np.float64)
     return total / div[:, None]
@@ -223,6 +228,72 @@ def build_context(raw, nbrs, alpha: float = 0.5):
     return final, sif
 
 
+def build_context_arrays(raw_idx, raw_val, raw_cnt, nbr, alpha: float = 0.5):
+    """`build_context` without Python loops, for config-scale N: the same
+    arithmetic in the same order.  raw_* : [N, k1] activation rows (indices
+    ascending, -1 / 0 padded, cnt valid entries); nbr: [N, k2] neighbour
+    lists (best first, -1 padded).
+
+    mean_activation (rerank.py:90-100): each coordinate's values are summed
+    in neighbour order starting from 0.0 (dict `acc.get(i, 0.0) + v`), then
+    divided by the neighbour count; make_activation sorts by coordinate and
+    keeps values > 0 with the sequential norm (rerank.py:24-61); aggregate of
+    identical channels is the identity (v1 == v2, rerank.py:142-146); the
+    S-IF lists owners ascending per coordinate (rerank.py:187-208).
+    Returns (final_idx, final_val, final_cnt, norms, Sif)."""
+    raw_idx = np.asarray(raw_idx)
+    raw_val = np.asarray(raw_val, dtype=np.float64)
+    nbr = np.asarray(nbr)
+    N, k1 = raw_idx.shape
+    k2 = nbr.shape[1]
+    # (owner j, neighbour slot t, entry e) flattened in neighbour order
+    j = np.repeat(np.arange(N), k2 * k1)
+    t = np.tile(np.repeat(np.arange(k2), k1), N)
+    q = nbr[j, t]
+    e = np.tile(np.arange(k1), N * k2)
+    ok = q >= 0
+    qq = np.where(ok, q, 0)
+    ok &= e < np.asarray(raw_cnt)[qq]
+    j, t, qq, e = j[ok], t[ok], qq[ok], e[ok]
+    coord = raw_idx[qq, e].astype(np.int64)
+    val = raw_val[qq, e]
+    order = np.lexsort((t, coord, j))  # by owner, coordinate, then neighbour order
+    j, coord, val = j[order], coord[order], val[order]
+    first = np.r_[True, (j[1:] != j[:-1]) | (coord[1:] != coord[:-1])]
+    gid = np.cumsum(first) - 1
+    ng = int(gid[-1]) + 1 if len(gid) else 0
+    pos_in = np.arange(len(gid)) - np.flatnonzero(first)[gid]
+    acc = np.zeros(ng)
+    for r in range(int(pos_in.max()) + 1 if len(pos_in) else 0):  # sequential per coordinate
+        m = pos_in == r
+        acc[gid[m]] = acc[gid[m]] + val[m]
+    g_owner = j[first]
+    g_coord = coord[first]
+    cnt_nb = (nbr >= 0).sum(axis=1).astype(np.float64)
+    g_val = acc / cnt_nb[g_owner]
+    keep = g_val > 0.0
+    g_owner, g_coord, g_val = g_owner[keep], g_coord[keep], g_val[keep]
+    fcnt = np.bincount(g_owner, minlength=N)
+    fstart = np.r_[0, np.cumsum(fcnt)]
+    cap = max(1, int(fcnt.max()) if N else 1)
+    pos = np.arange(len(g_owner)) - fstart[g_owner]
+    fidx = np.full((N, cap), -1, dtype=np.int64)
+    fval = np.zeros((N, cap))
+    fidx[g_owner, pos] = g_coord
+    fval[g_owner, pos] = g_val
+    norms = np.zeros(N)
+    for r in range(cap):  # _seq_sum: left to right from 0.0
+        norms = norms + fval[:, r]
+    # S-IF: owners ascending within each coordinate
+    o2 = np.lexsort((g_owner, g_coord))
+    sc, so, sv = g_coord[o2], g_owner[o2], g_val[o2]
+    off = np.r_[0, np.cumsum(np.bincount(sc, minlength=N))]
+    sif = Sif(norms=norms,
+              entry_ordinals=[so[off[i]:off[i + 1]].astype(np.int32) for i in range(N)],
+              entry_values=[sv[off[i]:off[i + 1]] for i in range(N)])
+    return fidx, fval, fcnt, norms, sif
+
+
 def rerank_query(raw, sif: Sif, scores: np.ndarray, k2: int, alpha: float = 0.5):
     """index.py:249-258 (duplicated channel): neighbours from the query's own
     scores, mean of their raw activations, aggregate, query_sif."""
@@ -256,8 +327,8 @@ class OracleCsrIndex:
         self.feat64 = np.asarray(feat_rows, dtype=np.float64)  # F_e widened once
         self.pnorm2 = (self.feat64 * self.feat64).sum(axis=1)
 
-    def feat_of(self, c):
-        return self.feat64[self.cell_off[c]:self.cell_off[c + 1]]
+    def feat_rows(self, p0, p1):
+        return self.feat64[p0:p1]
 
     @classmethod
     def from_views(cls, views, centroids, ma, k1, k2, similarity="cosine", sigma=0.5,
@@ -276,6 +347,7 @@ class OracleCsrIndex:
         self = cls(C, cell_off, post_ord, feat, ma, k1, k2, similarity, sigma, N)
         self.assign = assign
         self.rows = rows
+        self.views = views
         if self_join:
             self.self_join(block)
         return self
@@ -286,34 +358,23 @@ class OracleCsrIndex:
             B, V, d = Q.shape
             q_cells = quantize_many_mt(self.C, Q.reshape(B * V, d), self.ma).reshape(B, V, self.ma)
             q_cells = np.where(Q.any(axis=2)[:, :, None], q_cells, -1)
-        return fif_scores_many(self.cell_off, self.post_ord, self.feat_of, Q, q_cells, self.n,
+        return fif_scores_many(self.cell_off, self.post_ord, self.feat_rows, Q, q_cells, self.n,
                                self.similarity, self.sigma, vq=vq, pnorm2=self.pnorm2)
 
     def self_join(self, block=128):
         """index.py:196-210: raw activations and neighbour lists of every DB
-        shape, queried with its stored views (cell-major, zero views absent,
-        matching.py:94-103); then co-augment and the S-IF."""
-        N = self.n
-        order = np.argsort(self.post_ord, kind="stable")  # cell-major inside each owner
-        counts = np.bincount(self.post_ord, minlength=N)
-        starts = np.r_[0, np.cumsum(counts)]
-        vmax = max(1, int(counts.max()) if N else 1)
-        flat_cells = self.assign.reshape(-1, self.assign.shape[2])
-        have = flat_cells.shape[1] >= self.ma
+        shape, queried with its full view matrix (`vs.matrix(ch)`: zero views
+        included, so the mean divides by V, index.py:198-201); then
+        co-augment and the S-IF."""
+        N, V, d = self.views.shape
+        cells = self.assign[:, :, :self.ma] if self.assign.shape[2] >= self.ma else None
         raw, nbrs = [], []
-        d = self.feat.shape[1]
         for b0 in range(0, N, block):
             b1 = min(N, b0 + block)
-            B = b1 - b0
-            Q = np.zeros((B, vmax, d), dtype=self.feat.dtype)
-            qc = np.full((B, vmax, self.ma), -1, dtype=np.int64)
-            for i in range(B):
-                p = order[starts[b0 + i]:starts[b0 + i + 1]]
-                Q[i, :len(p)] = self.feat[p]
-                if have:
-                    qc[i, :len(p)] = flat_cells[self.rows[p], :self.ma]
-            S = self.scores(Q, q_cells=qc if have else None,
-                            vq=counts[b0:b1].astype(np.float64))
+            Q = self.views[b0:b1]
+            qc = None if cells is None else np.where(Q.any(axis=2)[:, :, None],
+                                                     cells[b0:b1], -1)
+            S = self.scores(Q, q_cells=qc)
             a, nb = activations_from_scores(S, self.k1, self.k2)
             raw += a
             nbrs += nb

@@ -168,7 +168,10 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
                        const __grid_constant__ CUtensorMap tmB2h, const TcArgs p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ int32_t s_sp[G * (TC_M + 2)];
-  __shared__ float s_qn2[TC_NMAX];
+  // per epilogue group: the groups run items independently (a group may
+  // start the next item's tail while the other finishes this one's), and an
+  // item's column split depends on its N
+  __shared__ float s_qn2[G * TC_NMAX];
   __shared__ ItemInfo s_item[ITEM_RING];
   __shared__ __align__(8) uint64_t ifull[ITEM_RING], iempty[ITEM_RING];
   // pair: item indices the leader's scheduler fetched, pushed into the peer
@@ -586,7 +589,7 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
       }
       if (e <= nseg) sp_s[e] = sp_a;
       if (e + TC_M <= nseg) sp_s[e + TC_M] = sp_b;
-      if (e < hn) s_qn2[c0 + e] = qn_r;
+      if (e < hn) s_qn2[eg * TC_NMAX + c0 + e] = qn_r;
       // thread -> (column mc = e % EC, segments e / EC, + TC_M / EC, ...)
       const int mc = e & (EC - 1), sg0 = e / EC;
       // EC-column slices: stage -> per-segment max over rows -> store
@@ -609,7 +612,7 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
             for (int r = r0; r < r1; ++r) mx = fmaxf(mx, Dg[r * ES + mc]);
             float sim;
             if (gauss)
-              sim = expf(-fmaxf(s_qn2[m] - mx, 0.f) * p.inv_sigma2);
+              sim = expf(-fmaxf(s_qn2[eg * TC_NMAX + m] - mx, 0.f) * p.inv_sigma2);
             else
               sim = fminf(fmaxf(mx, 0.f), 1.f);
             const int64_t o = obase + static_cast<int64_t>(I.mt * TC_NMAX + m) * S_c +

@@ -273,3 +273,197 @@ def test_c5_given_lists_against_oracle(n_shapes):
     record_parity("c5", f"rankings_top100_{len(rows)}q_n{n_shapes}",
                   {"queries": len(rows), "sif_postings": int(sum(len(o) for o in sif.entry_ordinals)),
                    "exact": True})
+
+
+# ------------------------------------------------------------------ C3 / C4 (sampled)
+def _raw_arrays(bundle):
+    r = bundle.raw_activations["A"].rows
+    return r.idx.cpu().numpy(), r.val.cpu().numpy(), r.cnt.cpu().numpy()
+
+
+def _nbrs_from_raw_arrays(ri, rv, rc, k2):
+    """top_neighbors of every self-join row read off its raw activation
+    (best k2 by value desc, ordinal asc; zeros already dropped), [N, k2]."""
+    k1 = ri.shape[1]
+    valid = np.arange(k1)[None, :] < rc[:, None]
+    v = np.where(valid, rv, -np.inf)
+    i = np.where(valid, ri, np.iinfo(np.int32).max)
+    order = np.lexsort((i, -v), axis=1)[:, :k2]
+    nb = np.take_along_axis(ri, order, axis=1).astype(np.int64)
+    ok = np.take_along_axis(valid, order, axis=1)
+    return np.where(ok, nb, -1)
+
+
+def _acts_of(ri, rv, rc, rows):
+    return {int(j): oracle.Act(ri[j, :rc[j]].astype(np.int64), rv[j, :rc[j]], 0.0) for j in rows}
+
+
+def _rerank_from_arrays(ri, rv, rc, sif, scores, k2):
+    """index.py:249-258 with the raw activations given as arrays."""
+    nb = oracle.top_neighbors(scores, k2)
+    acts = _acts_of(ri, rv, rc, nb)
+    f = oracle.mean_activation(acts, nb)
+    return oracle.query_sif(sif, oracle.aggregate(f, f, 0.5))
+
+
+def _check_scale_rerank(name, b, w, ref_sc, q_dev, ids):
+    """S-IF of the device's raw activations (vectorized oracle, exact) and
+    the final top-k of the sampled queries against the oracle's re-rank."""
+    ri, rv, rc = _raw_arrays(b)
+    nbr = _nbrs_from_raw_arrays(ri, rv, rc, w.k2)
+    _fi, _fv, _fc, norms, sif = scale.build_context_arrays(ri, rv, rc, nbr)
+    d = b.sif.dev
+    np.testing.assert_array_equal(d.norms.cpu().numpy(), norms)
+    np.testing.assert_array_equal(np.diff(d.e_off.cpu().numpy()),
+                                  [len(o) for o in sif.entry_ordinals])
+    np.testing.assert_array_equal(d.e_ord.cpu().numpy(), np.concatenate(sif.entry_ordinals))
+    np.testing.assert_array_equal(d.e_val.cpu().numpy(), np.concatenate(sif.entry_values))
+    got = gift.query_batch(b, q_dev, top_k=w.top_k)
+    pos = {s: i for i, s in enumerate(ids)}
+    for qi in range(ref_sc.shape[0]):
+        fin = _rerank_from_arrays(ri, rv, rc, sif, ref_sc[qi], w.k2)
+        order = scale.rank_final(fin, ids, "query", w.top_k)
+        gi, gs = _rank_ids(got[qi], pos)
+        assert_ranking_close(gi, gs, order, fin[order])
+    record_parity(name, f"rankings_top{w.top_k}_{ref_sc.shape[0]}q", {"queries": ref_sc.shape[0]})
+
+
+def test_c4_sampled_queries_against_oracle():
+    """Config 4 at full size: 1M shapes x 20 views x d=1024 fp16, Zipf cells
+    over K=4096.  Sampled DB shapes' lists and the 16 queries' assignments
+    bit-exact; 16 queries scored against all 1M shapes by the oracle over the
+    (verified) lists; 8 DB shapes' self-join rows; the S-IF; the rankings."""
+    w = synth.WORKLOADS["c4"]
+    db, qs, Ct = synth.zipf_mixture(w, SEED, dev())
+    C = Ct.cpu().numpy()
+    ids = synth.shape_ids(w.n_shapes)
+    b = _bundle(db, ids, C, n_views=w.n_views, codebook_size=w.K, ma=w.ma, k1=w.k1, k2=w.k2,
+                similarity="gaussian", sigma=w.sigma, storage_dtype=w.storage,
+                batch_size=w.batch)
+    rng = np.random.default_rng(4)
+    samp = np.sort(rng.choice(w.n_shapes, 200, replace=False))
+    samp_views = db[torch.from_numpy(samp).to(dev())].float().cpu().numpy()
+    del db
+    torch.cuda.empty_cache()
+    f = b.fifs["A"].dev
+    cell_off, post_ord = f.cell_off.cpu().numpy(), f.post_ord.cpu().numpy()
+    shape_off, shape_post = f.shape_off.cpu().numpy(), f.shape_post.cpu().numpy()
+    feat = f.feat.cpu().numpy()  # fp16 [P, d]
+    # (1) lists: each sampled shape's postings are its non-zero views in
+    # cell order (view order inside a cell), under the oracle's cells
+    cells = scale.quantize_many_mt(C, samp_views.reshape(-1, w.dim), 1)[:, 0].reshape(200, -1)
+    for k, i in enumerate(samp):
+        nz = samp_views[k].any(axis=1)
+        o = np.argsort(np.where(nz, cells[k], 1 << 30), kind="stable")[:int(nz.sum())]
+        p = shape_post[shape_off[i]:shape_off[i + 1]]
+        np.testing.assert_array_equal(np.searchsorted(cell_off, p, side="right") - 1, cells[k][o])
+        np.testing.assert_array_equal(feat[p].astype(np.float32), samp_views[k][o])
+    # (2) the 16 queries: assignment bit-exact, scores vs the oracle
+    sel = np.sort(rng.choice(qs.shape[0], 16, replace=False))
+    q = qs[torch.from_numpy(sel).to(dev())].contiguous()
+    q_h = q.cpu().numpy()
+    qc = scale.quantize_many_mt(C, q_h.reshape(-1, w.dim), w.ma)
+    np.testing.assert_array_equal(quantize_batch(Codebook(C), q.reshape(-1, w.dim), w.ma), qc)
+    got = mt.query_fif_batch(b.fifs["A"], q, w.ma, "gaussian", w.sigma).cpu().numpy()
+    ref = scale.fif_scores_many(cell_off, post_ord, lambda a, e: feat[a:e], q_h,
+                                qc.reshape(16, -1, w.ma), w.n_shapes, "gaussian", w.sigma)
+    st = rel_err_stats(got, ref)
+    record_parity("c4", "fif_scores_gaussian_vs_oracle_16q_x_1M", st)
+    assert st["max"] <= RTOL and st["zero_mismatch"] == 0
+    # (3) 8 DB shapes' self-join rows (index.py:196-210: the full view matrix)
+    rows8 = samp[:8]
+    Q8 = samp_views[:8]
+    qc8 = scale.quantize_many_mt(C, Q8.reshape(-1, w.dim), w.ma).reshape(8, -1, w.ma)
+    qc8 = np.where(Q8.any(axis=2)[:, :, None], qc8, -1)
+    S8 = scale.fif_scores_many(cell_off, post_ord, lambda a, e: feat[a:e], Q8, qc8,
+                               w.n_shapes, "gaussian", w.sigma)
+    acts8, _ = scale.activations_from_scores(S8, w.k1, w.k2)
+    ri, rv, rc = _raw_arrays(b)
+    swaps = assert_topk_rows_close([(ri[j, :rc[j]], rv[j, :rc[j]]) for j in rows8],
+                                   [(a.idx, a.val) for a in acts8])
+    record_parity("c4", "self_join_raw_activations_8_shapes", {"raw_swaps": swaps})
+    # (4) S-IF and rankings
+    _check_scale_rerank("c4", b, w, ref, q, ids)
+
+
+def test_c3_sampled_queries_against_oracle():
+    """Config 3 at full size: 100k shapes x 64 views x d=4096 f32 (105 GB),
+    K=1024, ma=2, streamed build (the index keeps only the tensor-core
+    planes).  The database is regenerated block by block for the oracle: the
+    16 queries scored against all 100k shapes, sampled DB views' assignments
+    bit-exact, the list sizes per cell, 4 DB shapes' self-join rows, the
+    S-IF and the rankings."""
+    w = synth.WORKLOADS["c3"]
+    mix = synth.BlockMixture(w, SEED, dev())
+    C = synth.sample_centroids_rows(mix, w.K, SEED + 1).cpu().numpy()
+    cbk = Codebook(C)
+    ids = synth.shape_ids(w.n_shapes)
+    cfg = gift.IndexConfig(n_views=w.n_views, codebook_size=w.K, ma=w.ma, k1=w.k1, k2=w.k2,
+                           similarity="gaussian", sigma=w.sigma, batch_size=w.batch,
+                           imported=True)
+    b = gift.build_index_streamed(mix.provider(), ids, w.n_views, w.dim, cfg,
+                                  codebooks={"A": Codebook(C, "A"), "B": Codebook(C, "B")},
+                                  chunk=1024, keep_features=False, self_join_batch=w.batch)
+    f = b.fifs["A"].dev
+    cell_off = f.cell_off.cpu().numpy()
+    rng = np.random.default_rng(3)
+    qs = mix.queries()
+    sel = np.sort(rng.choice(qs.shape[0], 16, replace=False))
+    q = qs[torch.from_numpy(sel).to(dev())].contiguous()
+    q_h = q.cpu().numpy()
+    qc = scale.quantize_many_mt(C, q_h.reshape(-1, w.dim), w.ma)
+    np.testing.assert_array_equal(quantize_batch(cbk, q.reshape(-1, w.dim), w.ma), qc)
+    qc = qc.reshape(16, w.n_views, w.ma)
+    self_rows = np.sort(rng.choice(w.n_shapes, 4, replace=False))
+    best = np.zeros((16, w.n_views, w.n_shapes))
+    best4 = np.zeros((4, w.n_views, w.n_shapes))
+    sizes = np.zeros(w.K, dtype=np.int64)
+    q4, qc4 = None, None
+    blk = 2048
+    for s0 in range(0, w.n_shapes, blk):  # regenerate, assign (GPU), score (host)
+        s1 = min(w.n_shapes, s0 + blk)
+        X = mix.rows(s0, s1)
+        flat = X.reshape(-1, w.dim)
+        cells = quantize_batch(cbk, flat, 1)[:, 0].reshape(s1 - s0, w.n_views)
+        Xh = X.cpu().numpy()
+        if s0 == 0:  # the device assignments of a sample of views, bit-exact
+            pick = rng.choice(flat.shape[0], 2048, replace=False)
+            np.testing.assert_array_equal(
+                scale.quantize_many_mt(C, Xh.reshape(-1, w.dim)[pick], 1)[:, 0],
+                cells.reshape(-1)[pick])
+        co, po, rows = scale.fif_lists(Xh, cells, w.K)
+        sizes += np.diff(co)
+        fr = Xh.reshape(-1, w.dim)
+        best[:, :, s0:s1] = scale.fif_scores_many(co, po + s0, lambda a, e: fr[rows[a:e]], q_h, qc,
+                                                  s1 - s0, "gaussian", w.sigma, shape_base=s0,
+                                                  return_best=True)
+        mine = self_rows[(self_rows >= s0) & (self_rows < s1)]
+        if len(mine):
+            part = Xh[mine - s0]
+            q4 = part if q4 is None else np.concatenate([q4, part])
+        del X, Xh, fr
+    np.testing.assert_array_equal(np.diff(cell_off), sizes)  # every cell's size
+    ref = best.sum(axis=1) / w.n_views
+    got = mt.query_fif_batch(b.fifs["A"], q, w.ma, "gaussian", w.sigma).cpu().numpy()
+    st = rel_err_stats(got, ref)
+    record_parity("c3", "fif_scores_gaussian_vs_oracle_16q_x_100k", st)
+    assert st["max"] <= RTOL and st["zero_mismatch"] == 0
+    # 4 DB shapes' self-join rows: one more pass over the regenerated blocks
+    qc4 = scale.quantize_many_mt(C, q4.reshape(-1, w.dim), w.ma).reshape(4, w.n_views, w.ma)
+    for s0 in range(0, w.n_shapes, blk):
+        s1 = min(w.n_shapes, s0 + blk)
+        X = mix.rows(s0, s1)
+        cells = quantize_batch(cbk, X.reshape(-1, w.dim), 1)[:, 0].reshape(s1 - s0, -1)
+        Xh = X.cpu().numpy()
+        co, po, rows = scale.fif_lists(Xh, cells, w.K)
+        fr = Xh.reshape(-1, w.dim)
+        best4[:, :, s0:s1] = scale.fif_scores_many(co, po + s0, lambda a, e: fr[rows[a:e]], q4,
+                                                   qc4, s1 - s0, "gaussian", w.sigma,
+                                                   shape_base=s0, return_best=True)
+        del X, Xh, fr
+    acts4, _ = scale.activations_from_scores(best4.sum(axis=1) / w.n_views, w.k1, w.k2)
+    ri, rv, rc = _raw_arrays(b)
+    swaps = assert_topk_rows_close([(ri[j, :rc[j]], rv[j, :rc[j]]) for j in self_rows],
+                                   [(a.idx, a.val) for a in acts4])
+    record_parity("c3", "self_join_raw_activations_4_shapes", {"raw_swaps": swaps})
+    _check_scale_rerank("c3", b, w, ref, q, ids)

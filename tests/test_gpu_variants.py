@@ -96,3 +96,33 @@ def test_drain_interval_flag_validated():
     with pytest.raises(ValueError):
         mt.query_fif_batch(fif, views[40:], 2, "gaussian")
     fif.dev.set_variant()
+
+
+@pytest.mark.parametrize("storage", ["float16", "float32"])
+def test_scan_variants_many_probes_per_cell(storage):
+    """Cells with hundreds of probes (several probe tiles per posting tile,
+    items of N = 64 and 128 interleaved), so the two epilogue groups run
+    different items at once: every scan variant (single CTA / CTA pairs,
+    drain interval 4 / 8 / 16, fp16-exact and general queries) stays within
+    the contract of the f64 oracle."""
+    rng = np.random.default_rng(17)
+    views, _ = mixture_views(71, 1500, 8, 256, 6, n_queries=72)
+    db = views[:1500].astype(np.float16 if storage == "float16" else np.float32)
+    C = sampled_codebook(db.astype(np.float32), 5, 3)
+    fif = mt.build_fif_from_tensor(torch.from_numpy(db).to(dev()), Codebook(C), shape_ids(1500))
+    dbw = db.astype(np.float32)
+    assign = oracle.quantize_many(C, dbw.reshape(-1, 256), 1).reshape(1500, 8)
+    ref_fif = oracle.build_fif(list(dbw), C, assign=assign)
+    for qname, qs in (("q16", views[1500:].astype(np.float16).astype(np.float32)),
+                      ("q32", views[1500:])):
+        ref = np.stack([oracle.query_fif(ref_fif, q, 1, "gaussian",
+                                         cells=oracle.quantize_many(C, q.astype(np.float64), 1))
+                        for q in qs])
+        for pair in ("off", "on"):
+            for kb in (4, 8, 16):
+                fif.dev.set_variant(pair=pair, drain_kb=kb)
+                got = mt.query_fif_batch(fif, qs, 1, "gaussian").cpu().numpy()
+                np.testing.assert_allclose(got, ref, rtol=RTOL, atol=1e-12,
+                                           err_msg=f"{storage} {qname} pair={pair} drain={kb}")
+    fif.dev.set_variant()
+    del rng

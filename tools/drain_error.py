@@ -29,7 +29,7 @@ def run(name, db, qs, C, ma, nq):
     q = qs[:nq].contiguous()
     qh = q.cpu().numpy()
     cells = scale.quantize_many_mt(C, qh.reshape(-1, qh.shape[2]), ma).reshape(nq, -1, ma)
-    ref = scale.fif_scores_many(cell_off, post_ord, lambda c: feat[cell_off[c]:cell_off[c + 1]],
+    ref = scale.fif_scores_many(cell_off, post_ord, lambda a, b: feat[a:b],
                                 qh, cells, db.shape[0], "gaussian", 0.5)
     for kb, raw in [(k, r) for k in (1, 2, 4, 8, 16) for r in (True, False)]:
         d.set_variant(drain_kb=kb, raw_accum=raw)
