@@ -1278,7 +1278,17 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
     const int dkb = (f->flags >> GIFT_FIF_DRAIN_SHIFT) & 31;
     ta.chunk_kb = dkb == 0 ? 4 : dkb;
     ta.dyn = (f->flags & GIFT_FIF_SCHED_STATIC) ? 0 : 1;
-    ta.tcomp = (f->flags & GIFT_FIF_RAW_ACCUM) ? 0 : 1;
+    {  // the truncation compensation of this launch's chunking
+      const int nkb = (d + 63) / 64;
+      double s1 = 0, s2 = 0;
+      for (int kb0 = 0; kb0 < nkb; kb0 += ta.chunk_kb) {
+        const double n = 4.0 * min(ta.chunk_kb, nkb - kb0);  // K = 16 steps per 64-wide block
+        s1 += n;
+        s2 += n * n;
+      }
+      ta.tcomp_scale = (f->flags & GIFT_FIF_RAW_ACCUM) ? 0.f
+                                                       : static_cast<float>(TCOMP_PER_STEP * s2 / s1);
+    }
     int rc2 = launch_scan_tc(f, Q, nprobes, ta, w.g1, w.g2, st, ev_scan_begin, ev_scan_end);
     if (rc2) return rc2;
   } else {

@@ -49,24 +49,6 @@ constexpr int ITEM_RING = 8;     // decoded work items in flight (scheduler -> r
 constexpr uint32_t TMEM_COLS = 512;  // D1[2][128] | D2[2][128]
 constexpr float SPLIT_INV = 1.0f / 2048.0f;
 
-// Truncation compensation.  The tensor cores' fp32 accumulation truncates
-// (measured: every scan score low, the bias linear in the MMA steps per
-// drain, e.g. -3.4e-6 relative on gaussian scores at 16 steps; std ~0.2e-6;
-// tools/drain_error.py).  Each K = 16 step loses on average half an ulp of
-// the running accumulator; for a drained chunk value v = m 2^e (m in [1, 2))
-// reached by n steps of roughly even increments, the expected loss is
-//   0.5 n ulp(v) (1 - 2 / (3 m))
-// (the running sum spends the fraction 1 - 1/m of the steps in v's binade,
-// and halves its ulp per binade below).  Added back per drained chunk.
-__device__ __forceinline__ float trunc_comp(float v, float half_n) {
-  const uint32_t b = __float_as_uint(v) & 0x7fffffffu;
-  const uint32_t e = b >> 23;
-  if (e <= 23u || e == 255u) return 0.f;  // zero / subnormal-scale / non-finite: nothing to add
-  const float ulp = __uint_as_float((e - 23u) << 23);
-  const float m = __uint_as_float((b & 0x7fffffu) | 0x3f800000u);
-  return copysignf(half_n * ulp * (1.f - __fdividef(2.f / 3.f, m)), v);
-}
-
 struct ItemInfo {
   int c, mt, p0, p1, seg0, seg1, nb, pb0, n;  // n: MMA N of the item (64 | 128)
   int t;      // global scan tile index
@@ -496,9 +478,6 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
       const uint32_t lane_off = static_cast<uint32_t>(lb) << 16;
       for (int kb0 = 0; kb0 < nkb; kb0 += chunk_kb) {
         const uint32_t buf = chunk_ctr % nbuf, aph = (chunk_ctr / nbuf) & 1;
-        // half the K = 16 MMA steps accumulated into this chunk (0: no compensation)
-        const float hn_steps = p.tcomp ? 0.5f * (TC_BK / 16) * (min(kb0 + chunk_kb, nkb) - kb0)
-                                       : 0.f;
         tc::mbar_wait(&tfull[buf], aph);
         tc::tc_fence_after();
         if (!cb) {
@@ -512,8 +491,8 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
               tc::tmem_ld_wait();
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
-                acc[j * 16 + i] += v1[i] + trunc_comp(v1[i], hn_steps);
-                acc[(j + 1) * 16 + i] += v2[i] + trunc_comp(v2[i], hn_steps);
+                acc[j * 16 + i] += v1[i];
+                acc[(j + 1) * 16 + i] += v2[i];
               }
             }
           }
@@ -528,8 +507,8 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
               tc::tmem_ld_wait();
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
-                acc[j * 16 + i] += v1[i] + trunc_comp(v1[i], hn_steps);
-                acc[(j + 1) * 16 + i] += v2[i] + trunc_comp(v2[i], hn_steps);
+                acc[j * 16 + i] += v1[i];
+                acc[(j + 1) * 16 + i] += v2[i];
               }
             }
           }
@@ -543,8 +522,7 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
               tc::tmem_ld_x16(base + I.n + j * 16, v2);
               tc::tmem_ld_wait();
 #pragma unroll
-              for (int i = 0; i < 16; ++i)
-                acc[j * 16 + i] += fmaf(v2[i], SPLIT_INV, v1[i] + trunc_comp(v1[i], hn_steps));
+              for (int i = 0; i < 16; ++i) acc[j * 16 + i] += fmaf(v2[i], SPLIT_INV, v1[i]);
             }
           }
         }
@@ -582,6 +560,10 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
         else
           tc::mbar_arrive(&dempty[ib]);
         ++item_ctr;
+      }
+      if (p.tcomp_scale != 0.f) {  // add back the expected truncation loss
+#pragma unroll
+        for (int n = 0; n < NA; ++n) acc[n] = fmaf(acc[n], p.tcomp_scale, acc[n]);
       }
       if (!I.live) {  // pair: duplicate tile, nothing to write
         named_bar(bar_tail, TC_M);

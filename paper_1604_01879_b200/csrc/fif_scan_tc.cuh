@@ -33,8 +33,20 @@ struct TcArgs {
   int has_lo;
   int chunk_kb;
   int dyn;       // items from the meta[M_WORK] counter (1) or a static CTA stride (0)
-  int tcomp;     // add back the expected truncation loss of each drained D1 chunk
+  float tcomp_scale;  // acc *= 1 + tcomp_scale after the drains (0: no compensation)
 };
+
+// Truncation compensation.  The tensor cores' fp32 accumulation truncates
+// (measured: every scan score low, the bias linear in the MMA steps per
+// drain: -3.4e-6 relative on gaussian scores at 16 steps, std ~0.2e-6;
+// tools/drain_error.py).  A K = 16 step loses on average half an ulp of the
+// running accumulator; a drained chunk v = m 2^e (m in [1, 2)) reached by n
+// steps of roughly even increments has lost about 0.5 n ulp(v) (1 - 2/(3m)),
+// i.e. a fraction 0.5 n 2^-23 (1/m)(1 - 2/(3m)) of v, whose mean over
+// log-uniform mantissas is 0.5 n 2^-23 / (4 ln 2).  The chunks' shares of a
+// dot scale with their lengths, so each item's dots are scaled once by
+//   1 + TCOMP_PER_STEP * sum_c n_c^2 / sum_c n_c.
+constexpr double TCOMP_PER_STEP = 0.5 * 0x1p-23 / (4.0 * 0.6931471805599453);
 
 bool tc_supported(const gift_fif_view* f);
 // The scan on CTA pairs (cta_group::2, M = 256): a work item is two

@@ -131,6 +131,52 @@ def read_manifest(path) -> list:
     return rows
 
 
+# ------------------------------------------------------------------ rendering hook
+class _Renderer:
+    """Mesh rendering + depth descriptors (index.py:106-139) are outside the
+    GPU path.  The `shapesearch` shim plugs the reference's own CPU renderer
+    in here, so mesh manifests and mesh queries work through this package."""
+
+    compute_viewset = None  # (mesh, config) -> ViewSet
+    load_mesh = None        # path -> mesh
+    mesh_type = None        # type of mesh query targets
+
+
+def set_renderer(compute_viewset, load_mesh, mesh_type) -> None:
+    _Renderer.compute_viewset = staticmethod(compute_viewset)
+    _Renderer.load_mesh = staticmethod(load_mesh)
+    _Renderer.mesh_type = mesh_type
+
+
+def _gather_viewsets(rows, config, jobs: int = 1):
+    """index.py:117-139: render every manifest row (in manifest order for any
+    job count); rows that fail with a ShapeSearchError / OSError are skipped
+    with a warning."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from .errors import ShapeSearchError
+
+    def one(row):
+        return _Renderer.compute_viewset(_Renderer.load_mesh(row[0]), config)
+
+    out = []
+    if jobs > 1:
+        with ThreadPoolExecutor(max_workers=jobs) as pool:
+            futs = [pool.submit(one, row) for row in rows]
+            for row, fut in zip(rows, futs):
+                try:
+                    out.append((row, fut.result()))
+                except (ShapeSearchError, OSError) as exc:
+                    log.warning("skipping shape %s: %s", row[0], exc)
+    else:
+        for row in rows:
+            try:
+                out.append((row, one(row)))
+            except (ShapeSearchError, OSError) as exc:
+                log.warning("skipping shape %s: %s", row[0], exc)
+    return out
+
+
 # ------------------------------------------------------------------ engine
 class QueryEngine:
     """Batched device pipeline over one bundle (single GPU or one shard):
@@ -421,8 +467,7 @@ def build_index(manifest, config: IndexConfig = IndexConfig(), jobs: int = 1,
     if not rows:
         raise EmptyManifest("no shapes listed")
     if not feature_files:
-        raise Unsupported("mesh rendering is outside the GPU path: pass feature_files "
-                          "or use build_index_from_views")
+        return _build_index_rendered(rows, config, jobs, codebooks)
     if set(feature_files) != set(CHANNELS):
         raise ChannelMismatch(f"feature files required for channels {CHANNELS}")
     config = replace(config, imported=True)
@@ -451,15 +496,42 @@ def build_index(manifest, config: IndexConfig = IndexConfig(), jobs: int = 1,
         if vb.shape == va.shape and torch.equal(va, vb):
             vb = None
     if codebooks is None:
-        # index.py:186-193: k-means per channel over the non-zero views, on the device
-        codebooks = {}
-        for ch, v in (("A", va), ("B", va if vb is None else vb)):
-            if ch == "B" and vb is None:  # same rows, same seed: the same centroids
-                codebooks["B"] = cb.Codebook(codebooks["A"].centroids, "B", config.seed)
-                continue
-            rows = v.reshape(-1, v.shape[-1])
-            codebooks[ch] = cb.train_codebook(rows[rows.any(dim=1)], k=config.codebook_size,
-                                              seed=config.seed, channel=ch)
+        codebooks = _train_codebooks(va, vb, config)
+    return build_index_from_views(va, ids, config, views_b=vb, labels=labels,
+                                  codebooks=codebooks)
+
+
+def _train_codebooks(va, vb, config):
+    """index.py:186-193: k-means per channel over the non-zero views, on the
+    device (channel B reuses A's centroids when the features are the same)."""
+    codebooks = {}
+    for ch, v in (("A", va), ("B", va if vb is None else vb)):
+        if ch == "B" and vb is None:
+            codebooks["B"] = cb.Codebook(codebooks["A"].centroids, "B", config.seed)
+            continue
+        rows = v.reshape(-1, v.shape[-1])
+        codebooks[ch] = cb.train_codebook(rows[rows.any(dim=1)], k=config.codebook_size,
+                                          seed=config.seed, channel=ch)
+    return codebooks
+
+
+def _build_index_rendered(rows, config, jobs, codebooks):
+    """index.py:146-227 from meshes: the plugged-in CPU renderer gives the
+    view sets (`set_renderer`), everything after them runs on the device."""
+    if _Renderer.compute_viewset is None:
+        raise Unsupported("mesh rendering is outside the GPU path: pass feature_files, use "
+                          "build_index_from_views, or plug a renderer (set_renderer)")
+    built = _gather_viewsets(rows, config, jobs)
+    if not built:
+        raise AllShapesFailed("every shape in the manifest failed to build")
+    ids = [vs.shape_id for _row, vs in built]
+    labels = {vs.shape_id: row[1] for row, vs in built}
+    dev = nat.device()
+    va = torch.from_numpy(np.stack([vs.matrix("A") for _r, vs in built]).astype(np.float32))
+    vb = torch.from_numpy(np.stack([vs.matrix("B") for _r, vs in built]).astype(np.float32))
+    va, vb = va.to(dev), vb.to(dev)
+    if codebooks is None:
+        codebooks = _train_codebooks(va, vb, config)
     return build_index_from_views(va, ids, config, views_b=vb, labels=labels,
                                   codebooks=codebooks)
 
@@ -504,6 +576,13 @@ def query(bundle: IndexBundle, target, top_k: int = 10, exact: bool = False,
     eng = bundle.engine
     if exact and eng.fa is None:
         raise Unsupported("exact ranking needs the stored view features (F-IF)")
+    render_s = 0.0
+    if _Renderer.mesh_type is not None and isinstance(target, _Renderer.mesh_type):
+        if bundle.config.imported:  # index.py:273-275
+            raise ChannelMismatch("index was built from imported features; query by id instead")
+        t0 = time.perf_counter()
+        target = _Renderer.compute_viewset(target, bundle.config)
+        render_s = time.perf_counter() - t0
     ma_, mb_, sid = _viewset_mats(bundle, target)
     t0 = time.perf_counter()
     qa = mt._as_query_tensor(ma_, bundle.fifs["A"].dim)[None]
@@ -514,7 +593,7 @@ def query(bundle: IndexBundle, target, top_k: int = 10, exact: bool = False,
     idx, val = eng.run(qa, qb, top_k=top_k, rerank=rerank, self_local=self_local, exact=exact)
     idx, val = idx.cpu().numpy(), val.cpu().numpy()
     t1 = time.perf_counter()
-    return eng.results(idx[0], val[0]), {"render": 0.0, "match": t1 - t0}
+    return eng.results(idx[0], val[0]), {"render": render_s, "match": t1 - t0}
 
 
 def query_by_id(bundle: IndexBundle, shape_id: str, top_k: int = 10, exact: bool = False,
@@ -713,7 +792,10 @@ def evaluate_index(bundle: IndexBundle, exact: bool = False, rerank: bool = True
 
     def scores_of(rows):
         Q, vq = eng.fa.shape_views(rows)  # query_by_id: stored views, cell-major
-        sa, sb = eng.scores(Q, None, vq=vq, ma=eng.fa.cb.K if exact else None)
+        Qb = vqb = None
+        if not eng.dup:  # channel B's own stored views (its own dimension)
+            Qb, vqb = eng.fb.shape_views(rows)
+        sa, sb = eng.scores(Q, Qb, vq=vq, vqb=vqb, ma=eng.fa.cb.K if exact else None)
         return eng.rerank(sa, sb) if rerank else (sa if sb is sa else (sa + sb) / 2.0)
 
     return _device_report(bundle, scores_of, batch_size)
