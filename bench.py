@@ -170,17 +170,27 @@ def measured_tensor_peak():
     return float(_peaks().get("bf16_tflops", 1590.0))
 
 
-def count_launches(fn) -> int:
+_SYNC_APIS = ("cudaStreamSynchronize", "cudaDeviceSynchronize", "cudaEventSynchronize",
+              "cudaMemcpy", "cudaMemcpy2D", "cudaMemset")  # host-blocking runtime calls
+
+
+def count_launches(fn, syncs: dict | None = None) -> int:
     """Kernels of libgift.so one call of fn launches (CUPTI via torch.profiler,
-    names in namespace gift::), measured outside the timed region."""
+    names in namespace gift::), measured outside the timed region; with
+    `syncs`, also counts the host-blocking CUDA runtime calls fn makes (the
+    query path should make none)."""
     from torch.profiler import ProfilerActivity, profile
 
     torch.cuda.synchronize()
-    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
         fn()
-        torch.cuda.synchronize()
-    return sum(1 for e in prof.events()
-               if e.device_type.name == "CUDA" and "gift::" in e.name)
+    evs = prof.events()
+    if syncs is not None:
+        for e in evs:
+            if e.device_type.name == "CPU" and e.name in _SYNC_APIS:
+                syncs[e.name] = syncs.get(e.name, 0) + 1
+    torch.cuda.synchronize()
+    return sum(1 for e in evs if e.device_type.name == "CUDA" and "gift::" in e.name)
 
 
 def host_cores():
@@ -445,8 +455,8 @@ def run_gift(args, w):
         dist.init_process_group("nccl", device_id=device)
     bundle, qs, build_s = build(w, device)
     eng = bundle.engine
-    if args.drain_kb:
-        eng.fa.set_variant(drain_kb=args.drain_kb)
+    if args.drain_kb or args.pair != "auto":
+        eng.fa.set_variant(drain_kb=args.drain_kb, pair=args.pair)
     B = w.batch
     nb = max(1, qs.shape[0] // B)
     order = [(rank + i * ws) % nb for i in range(args.steps + args.warmup)]
@@ -493,8 +503,9 @@ def run_gift(args, w):
         if ws > 1:
             dist.barrier()
     ms = ev[0].elapsed_time(ev[1])
+    syncs = {}
     launches_per_step = count_launches(
-        lambda: eng.run(batches[order[args.warmup]], top_k=w.top_k, rerank=True))
+        lambda: eng.run(batches[order[args.warmup]], top_k=w.top_k, rerank=True), syncs)
     # with batches in flight a scan's events also span its wait behind another
     # lane's scan: the kernel's own duration comes from the same batches run
     # one at a time right after, with the timed run's configuration (the same
@@ -570,7 +581,8 @@ def run_gift(args, w):
                          f"single channel, over the GPU-built lists)", "host": host_info()}
     if rank == 0:
         run = {"lanes": L, "scan_reserved_sms": eng.reserve_sms, "build_s": build_s,
-               "drain_kb": args.drain_kb or "default",
+               "drain_kb": args.drain_kb or "default", "pair": args.pair,
+               "host_blocking_cuda_calls_per_step": syncs,
                "features": ("planes only (streamed build)" if eng.fa.feat is None
                             else "storage copy + planes"), "quantize": quant_ncu}
         line = _gpu_line(args, workload_config(w, f"replicas{ws}" if ws > 1 else "single"),
@@ -631,12 +643,17 @@ def _e2e_sharded(device, host_batches, run_dev):
     dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    outs = []
+    outs = None
     for i, hb in enumerate(host_batches):
         buf = bufs[i % 2]
         buf.copy_(hb, non_blocking=True)
         idx, val = run_dev(buf)
-        outs.append((idx.to("cpu", non_blocking=True), val.to("cpu", non_blocking=True)))
+        if outs is None:  # pinned result buffers (a pageable D2H would block)
+            outs = [(torch.empty(idx.shape, dtype=idx.dtype, pin_memory=True),
+                     torch.empty(val.shape, dtype=val.dtype, pin_memory=True))
+                    for _ in host_batches]
+        outs[i][0].copy_(idx, non_blocking=True)
+        outs[i][1].copy_(val, non_blocking=True)
     torch.cuda.synchronize()
     dist.barrier()
     e2e = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=device)
@@ -687,7 +704,8 @@ def run_sharded(args, w):
     nb = max(1, qs.shape[0] // B)
     batches = [qs[j * B:(j + 1) * B].contiguous() for j in range(nb)]
     ms, clk = _timed_sharded(args, device, lambda j: eng.run(batches[j], w.top_k), nb, local)
-    launches = count_launches(lambda: eng.run(batches[0], w.top_k))
+    syncs = {}
+    launches = count_launches(lambda: eng.run(batches[0], w.top_k), syncs)
     steps = [batches[(args.warmup + i) % nb].cpu().pin_memory() for i in range(args.steps)]
     e2e_s = _e2e_sharded(device, steps, lambda q: eng.run(q, w.top_k))
     ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -712,6 +730,7 @@ def run_sharded(args, w):
                           "d2h_bytes_per_step": B * w.top_k * 12},
                          launches * args.steps, roof, None, clk,
                          {"build_s": build_s, "shard_shapes": hi - lo,
+                          "host_blocking_cuda_calls_per_step": syncs,
                           "collectives_per_step": 2 if ws > 1 else 0,
                           "exchange": "packed all_gather_into_tensor (score bits, "
                                       "ordinal << 32 | tiebreak) + gift_topk_cand_tb merge"})
@@ -775,19 +794,23 @@ def run_c5(args):
             ev[1].record()
             torch.cuda.synchronize()
         ms, clk = ev[0].elapsed_time(ev[1]), clk_s.summary()
-    launches = count_launches(lambda: step(0))
+    syncs = {}
+    launches = count_launches(lambda: step(0), syncs)
     # e2e: each step's given lists come from pinned host memory, results go back
     host = [(idx[r].cpu().pin_memory(), val[r].cpu().pin_memory(), r.cpu().pin_memory())
             for r in rows[args.warmup:]]
     if sharded:
         dist.barrier()
     torch.cuda.synchronize()
+    k_out = c["top_k"]
+    res = [(torch.empty((B, k_out), dtype=torch.int32, pin_memory=True),
+            torch.empty((B, k_out), dtype=torch.float64, pin_memory=True)) for _ in host]
     t0 = time.perf_counter()
-    for hi_, hv, hr in host:
+    for (hi_, hv, hr), (ri, rv) in zip(host, res):
         oi, ov = run_q(hi_.to(device, non_blocking=True), hv.to(device, non_blocking=True),
                        hr.to(device, non_blocking=True))
-        oi.to("cpu", non_blocking=True)
-        ov.to("cpu", non_blocking=True)
+        ri.copy_(oi, non_blocking=True)
+        rv.copy_(ov, non_blocking=True)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     if sharded:
@@ -806,7 +829,8 @@ def run_c5(args):
                           "h2d_bytes_per_step": B * (L * 12 + 8),
                           "d2h_bytes_per_step": B * c["top_k"] * 12},
                          launches * args.steps, None, cpu, clk,
-                         {"build_s": build_s, "sif_postings": postings}, dtype="f64")
+                         {"build_s": build_s, "sif_postings": postings,
+                          "host_blocking_cuda_calls_per_step": syncs}, dtype="f64")
         print(json.dumps(line), flush=True)
     if sharded:
         dist.destroy_process_group()
@@ -953,6 +977,8 @@ def main():
     ap.add_argument("--drain-kb", type=int, default=0,
                     help="scan accumulator drain interval in 64-wide k-blocks (0 = the "
                          "library default)")
+    ap.add_argument("--pair", default="auto", choices=["auto", "on", "off"],
+                    help="F-IF scan on CTA pairs (cta_group::2): default per storage")
     ap.add_argument("--shard", action="store_true",
                     help="shard the database by shape over the ranks (default for configs "
                          "3-5 at N > 1)")

@@ -190,7 +190,8 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
   // every query lo plane is zero (fp16-exact queries): the single-CTA kernel
   // drops the b2 operand -- one N = n MMA per k-step instead of N = 2n, no b2
   // loads, no D2 drains (b2 = 0 contributes exactly 0: bit-identical)
-  const bool qz = !PAIR && p.meta[M_QLO] == 0;
+  // (pairs without the lo plane too: each CTA then holds half of b1's rows)
+  const bool qz = (!PAIR || !LO) && p.meta[M_QLO] == 0;
   // qz without the lo plane needs D1 only (128 TMEM columns per chunk): four
   // chunk buffers instead of two, so the MMAs run a whole item ahead of the
   // epilogue's per-item tail instead of stalling on the accumulators
@@ -255,7 +256,8 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
         const uint32_t a_bytes = has_lo ? 2 * A_TILE : A_TILE;
         // this CTA's B bytes: both planes (single), one whole plane (pair, cb),
         // half of each plane (pair, lo)
-        const uint32_t bytes = a_bytes + (PAIR && cb ? I.n : (qz ? 1 : 2) * brows) * TC_BK * 2;
+        const uint32_t bytes =
+            a_bytes + (PAIR && qz ? brows : PAIR && cb ? I.n : (qz ? 1 : 2) * brows) * TC_BK * 2;
         for (int kb = 0; kb < nkb; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * stage_bytes;
@@ -268,7 +270,9 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
             tc::tma_load_2d_2sm(st, &tmA1, lbar, kb * TC_BK, I.p0);
             if (has_lo) tc::tma_load_2d_2sm(st + A_TILE, &tmA2, lbar, kb * TC_BK, I.p0);
             const int r0 = I.pb0 + static_cast<int>(rank) * brows;
-            if (cb) {  // CTA r: plane r, all n probe rows
+            if (qz) {  // fp16-exact queries: CTA r holds its half of b1's rows
+              tc::tma_load_2d_2sm(st + b_off, brows == 64 ? &tmB1 : &tmB1h, lbar, kb * TC_BK, r0);
+            } else if (cb) {  // CTA r: plane r, all n probe rows
               const CUtensorMap* pm = rank == 0 ? &tmB1 : &tmB2;
               for (int x = 0; x < I.n / 64; ++x)
                 tc::tma_load_2d_2sm(st + b_off + x * B_BOX, pm, lbar, kb * TC_BK,
@@ -348,7 +352,9 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
                 const uint32_t acc1 = (kb > kb0 || k > 0) ? 1u : 0u;
                 const uint32_t acc2 = (kb > 0 || k > 0) ? 1u : 0u;
                 const uint64_t adv = static_cast<uint64_t>(k * 2);  // 32 B in 16-B units
-                if (PAIR && cb) {  // [D1 | D2] = a1 . [b1 | b2], M = 256
+                if (PAIR && qz) {  // D1 = a1 . b1, M = 256, b1 split over the pair
+                  tc::mma_f16_2sm(d1, a1 + adv, b1 + adv, idesc, acc1);
+                } else if (PAIR && cb) {  // [D1 | D2] = a1 . [b1 | b2], M = 256
                   tc::mma_f16_2sm(d1, a1 + adv, b1 + adv, idesc2, acc1);
                 } else if (PAIR) {
                   tc::mma_f16_2sm(d1, a1 + adv, b1 + adv, idesc, acc1);
@@ -444,8 +450,6 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
     const bool gauss = p.mode == GIFT_SIM_GAUSSIAN;
     uint32_t chunk_ctr = 0, item_ctr = 0;
     // accumulator release: own barrier, or the pair leader's (remote arrive)
-    const uint32_t rel_t0 = PAIR ? tc::mapa(&tempty[0], 0) : 0u;
-    const uint32_t rel_t1 = PAIR ? tc::mapa(&tempty[1], 0) : 0u;
     const uint32_t rel_d0 = PAIR ? tc::mapa(&dempty[0], 0) : 0u;
     const uint32_t rel_d1 = PAIR ? tc::mapa(&dempty[1], 0) : 0u;
     for (;;) {
@@ -528,7 +532,7 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
         }
         tc::tc_fence_before();
         if (PAIR)
-          tc::mbar_arrive_cluster(buf ? rel_t1 : rel_t0);
+          tc::mbar_arrive_cluster(tc::mapa(&tempty[buf], 0));  // the leader's barrier
         else
           tc::mbar_arrive(&tempty[buf]);
         ++chunk_ctr;

@@ -87,6 +87,11 @@ def exchange_topk(vals, idx, tb, k: int, positive_only: bool = False, group=None
     each rank) and the merge into the global best k: returns (idx [B, k] i32,
     -1 padded, vals [B, k] f64).  `merge` defaults to the device kernel (the
     CPU tests pass a host reference merge)."""
+    if dist.get_world_size(group) == 1:  # nothing to exchange: merge in place
+        return (merge or device_merge)(vals.to(torch.float64).contiguous(),
+                                       idx.to(torch.int32).contiguous(),
+                                       (tb.to(torch.int64) & _MISSING_TB).to(torch.int32),
+                                       k, positive_only)
     packed = _all_gather(pack_candidates(vals, idx, tb), group)  # [G, B, k', 2]
     G, B, kk, _ = packed.shape
     v, o, t = unpack_candidates(packed.permute(1, 0, 2, 3).reshape(B, G * kk, 2))
