@@ -452,6 +452,7 @@ def run_gift(args, w):
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if ws > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # init lines let the driver count the ranks
         dist.init_process_group("nccl", device_id=device)
     bundle, qs, build_s = build(w, device)
     eng = bundle.engine
@@ -607,6 +608,7 @@ def _free_port():
 def _init_dist(device):
     ws, _, _ = dist_env()
     if ws > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # init lines let the driver count the ranks
         dist.init_process_group("nccl", device_id=device)
     else:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")

@@ -1030,6 +1030,12 @@ __global__ void __launch_bounds__(GR_THREADS, W >= 2 ? 3 : 4) fif_owner_reduce_k
 
 using namespace gift;
 
+#ifdef GIFT_SCAN_EXPERIMENT
+namespace gift {
+extern int g_scan_experiment;
+}
+#endif
+
 namespace {
 struct ScoreWs {
   int64_t* meta;
@@ -1278,6 +1284,9 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
     const int dkb = (f->flags >> GIFT_FIF_DRAIN_SHIFT) & 31;
     ta.chunk_kb = dkb == 0 ? 4 : dkb;
     ta.dyn = (f->flags & GIFT_FIF_SCHED_STATIC) ? 0 : 1;
+#ifdef GIFT_SCAN_EXPERIMENT
+    ta.exp = g_scan_experiment;
+#endif
     {  // the truncation compensation of this launch's chunking
       const int nkb = (d + 63) / 64;
       double s1 = 0, s2 = 0;

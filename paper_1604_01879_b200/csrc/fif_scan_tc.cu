@@ -31,6 +31,12 @@
 
 namespace gift {
 
+#ifdef GIFT_SCAN_EXPERIMENT
+#define GIFT_EXP(p, bit) (((p).exp & (bit)) != 0)
+#else
+#define GIFT_EXP(p, bit) false
+#endif
+
 constexpr int TC_M = 128;
 constexpr int TC_NMAX = 128;  // probes per item: N = 64 or 128 (per item)
 constexpr int TC_BK = 64;     // fp16 per k-block = 128-byte rows
@@ -263,6 +269,8 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
           uint8_t* st = smem + stage * stage_bytes;
           if (!tc::elect_one()) {
             // other lanes: nothing to issue
+          } else if (GIFT_EXP(p, 8)) {
+            if (!PAIR || leader) tc::mbar_arrive(&full[stage]);
           } else if (PAIR) {
             // both CTAs' bytes complete on the leader's full barrier
             const uint32_t lbar = tc::mapa(&full[stage], 0);
@@ -349,6 +357,7 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
             if (tc::elect_one()) {
 #pragma unroll
               for (int k = 0; k < TC_BK / 16; ++k) {
+                if (GIFT_EXP(p, 4)) break;
                 const uint32_t acc1 = (kb > kb0 || k > 0) ? 1u : 0u;
                 const uint32_t acc2 = (kb > 0 || k > 0) ? 1u : 0u;
                 const uint64_t adv = static_cast<uint64_t>(k * 2);  // 32 B in 16-B units
@@ -488,7 +497,7 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
           const uint32_t base = tmem_base + lane_off + buf * TC_NMAX + c0;
 #pragma unroll
           for (int j = 0; j < NA / 16; j += 2) {
-            if (j < ng) {
+            if (j < ng && !GIFT_EXP(p, 2)) {
               float v1[16], v2[16];
               tc::tmem_ld_x16(base + j * 16, v1);
               tc::tmem_ld_x16(base + (j + 1) * 16, v2);  // ng is even
@@ -504,7 +513,7 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
           const uint32_t base = tmem_base + lane_off + buf * TC_NMAX + c0;
 #pragma unroll
           for (int j = 0; j < NA / 16; j += 2) {
-            if (j < ng) {
+            if (j < ng && !GIFT_EXP(p, 2)) {
               float v1[16], v2[16];
               tc::tmem_ld_x16(base + j * 16, v1);
               tc::tmem_ld_x16(base + (j + 1) * 16, v2);  // ng is even
@@ -520,7 +529,7 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
           const uint32_t base = tmem_base + lane_off + buf * 2 * TC_NMAX + c0;
 #pragma unroll
           for (int j = 0; j < NA / 16; ++j) {
-            if (j < ng) {
+            if (j < ng && !GIFT_EXP(p, 2)) {
               float v1[16], v2[16];
               tc::tmem_ld_x16(base + j * 16, v1);
               tc::tmem_ld_x16(base + I.n + j * 16, v2);
@@ -569,7 +578,7 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
 #pragma unroll
         for (int n = 0; n < NA; ++n) acc[n] = fmaf(acc[n], p.tcomp_scale, acc[n]);
       }
-      if (!I.live) {  // pair: duplicate tile, nothing to write
+      if (!I.live || GIFT_EXP(p, 1)) {  // pair: duplicate tile, nothing to write
         named_bar(bar_tail, TC_M);
         continue;
       }
@@ -805,3 +814,9 @@ extern "C" int gift_split_planes(const float* x, int64_t n, void* h1, void* h2, 
   return GIFT_OK;
 }
 
+#ifdef GIFT_SCAN_EXPERIMENT
+namespace gift {
+int g_scan_experiment = 0;
+}
+extern "C" void gift_scan_experiment(int bits) { gift::g_scan_experiment = bits; }
+#endif

@@ -34,6 +34,10 @@ struct TcArgs {
   int chunk_kb;
   int dyn;       // items from the meta[M_WORK] counter (1) or a static CTA stride (0)
   float tcomp_scale;  // acc *= 1 + tcomp_scale after the drains (0: no compensation)
+#ifdef GIFT_SCAN_EXPERIMENT
+  int exp;  // timing experiments only (tools/scan_experiment.py): 1 = no epilogue tail,
+            // 2 = no TMEM drains, 4 = no MMAs, 8 = no loads; outputs invalid
+#endif
 };
 
 // Truncation compensation.  The tensor cores' fp32 accumulation truncates

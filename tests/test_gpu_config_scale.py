@@ -415,10 +415,12 @@ def test_c3_sampled_queries_against_oracle():
     np.testing.assert_array_equal(quantize_batch(cbk, q.reshape(-1, w.dim), w.ma), qc)
     qc = qc.reshape(16, w.n_views, w.ma)
     self_rows = np.sort(rng.choice(w.n_shapes, 4, replace=False))
-    best = np.zeros((16, w.n_views, w.n_shapes))
-    best4 = np.zeros((4, w.n_views, w.n_shapes))
+    q4 = np.concatenate([mix.rows(int(r), int(r) + 1).cpu().numpy() for r in self_rows])
+    qc4 = scale.quantize_many_mt(C, q4.reshape(-1, w.dim), w.ma).reshape(4, w.n_views, w.ma)
+    qall = np.concatenate([q_h, q4])  # the 16 queries and 4 DB shapes' self-join rows
+    qcall = np.concatenate([qc, qc4])
+    best = np.zeros((20, w.n_views, w.n_shapes))
     sizes = np.zeros(w.K, dtype=np.int64)
-    q4, qc4 = None, None
     blk = 2048
     for s0 in range(0, w.n_shapes, blk):  # regenerate, assign (GPU), score (host)
         s1 = min(w.n_shapes, s0 + blk)
@@ -434,33 +436,17 @@ def test_c3_sampled_queries_against_oracle():
         co, po, rows = scale.fif_lists(Xh, cells, w.K)
         sizes += np.diff(co)
         fr = Xh.reshape(-1, w.dim)
-        best[:, :, s0:s1] = scale.fif_scores_many(co, po + s0, lambda a, e: fr[rows[a:e]], q_h, qc,
-                                                  s1 - s0, "gaussian", w.sigma, shape_base=s0,
-                                                  return_best=True)
-        mine = self_rows[(self_rows >= s0) & (self_rows < s1)]
-        if len(mine):
-            part = Xh[mine - s0]
-            q4 = part if q4 is None else np.concatenate([q4, part])
+        best[:, :, s0:s1] = scale.fif_scores_many(co, po + s0, lambda a, e: fr[rows[a:e]], qall,
+                                                  qcall, s1 - s0, "gaussian", w.sigma,
+                                                  shape_base=s0, return_best=True)
         del X, Xh, fr
     np.testing.assert_array_equal(np.diff(cell_off), sizes)  # every cell's size
-    ref = best.sum(axis=1) / w.n_views
+    ref = best[:16].sum(axis=1) / w.n_views
     got = mt.query_fif_batch(b.fifs["A"], q, w.ma, "gaussian", w.sigma).cpu().numpy()
     st = rel_err_stats(got, ref)
     record_parity("c3", "fif_scores_gaussian_vs_oracle_16q_x_100k", st)
     assert st["max"] <= RTOL and st["zero_mismatch"] == 0
-    # 4 DB shapes' self-join rows: one more pass over the regenerated blocks
-    qc4 = scale.quantize_many_mt(C, q4.reshape(-1, w.dim), w.ma).reshape(4, w.n_views, w.ma)
-    for s0 in range(0, w.n_shapes, blk):
-        s1 = min(w.n_shapes, s0 + blk)
-        X = mix.rows(s0, s1)
-        cells = quantize_batch(cbk, X.reshape(-1, w.dim), 1)[:, 0].reshape(s1 - s0, -1)
-        Xh = X.cpu().numpy()
-        co, po, rows = scale.fif_lists(Xh, cells, w.K)
-        fr = Xh.reshape(-1, w.dim)
-        best4[:, :, s0:s1] = scale.fif_scores_many(co, po + s0, lambda a, e: fr[rows[a:e]], q4,
-                                                   qc4, s1 - s0, "gaussian", w.sigma,
-                                                   shape_base=s0, return_best=True)
-        del X, Xh, fr
+    best4 = best[16:]
     acts4, _ = scale.activations_from_scores(best4.sum(axis=1) / w.n_views, w.k1, w.k2)
     ri, rv, rc = _raw_arrays(b)
     swaps = assert_topk_rows_close([(ri[j, :rc[j]], rv[j, :rc[j]]) for j in self_rows],
