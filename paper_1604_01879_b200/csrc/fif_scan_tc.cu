@@ -202,6 +202,12 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
   // chunk buffers instead of two, so the MMAs run a whole item ahead of the
   // epilogue's per-item tail instead of stalling on the accumulators
   const bool qz4 = qz && !LO;
+  // a single CTA with fp16-exact queries stages A + b1 only: 32 KB stages, six
+  // in the ring instead of four (more k-blocks in flight; measured neutral on
+  // config 4, whose scan is paced by its per-item latencies)
+  const bool small_st = qz && !PAIR && !LO;
+  const int st_bytes = small_st ? A_TILE + B_TILE : stage_bytes;
+  const int n_st = small_st ? RING_BYTES / (A_TILE + B_TILE) : nstages;
   const uint32_t nbuf = qz4 ? 4u : 2u;
   const uint32_t buf_cols = qz4 ? TC_NMAX : ((!PAIR || !LO) ? 2 * TC_NMAX : TC_NMAX);
   const int nkb = (p.d + TC_BK - 1) / TC_BK;
@@ -266,7 +272,7 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
             a_bytes + (PAIR && qz ? brows : PAIR && cb ? I.n : (qz ? 1 : 2) * brows) * TC_BK * 2;
         for (int kb = 0; kb < nkb; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* st = smem + stage * stage_bytes;
+          uint8_t* st = smem + stage * st_bytes;
           if (!tc::elect_one()) {
             // other lanes: nothing to issue
           } else if (GIFT_EXP(p, 8)) {
@@ -306,7 +312,7 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
             }
           }
           __syncwarp();
-          if (++stage == nstages) {
+          if (++stage == n_st) {
             stage = 0;
             phase ^= 1;
           }
@@ -349,7 +355,7 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
           for (int kb = kb0; kb < kend; ++kb) {
             tc::mbar_wait(&full[stage], phase);
             tc::tc_fence_after();
-            uint8_t* st = smem + stage * stage_bytes;
+            uint8_t* st = smem + stage * st_bytes;
             const uint64_t a1 = tc::smem_desc_sw128(st);
             const uint64_t a2 = tc::smem_desc_sw128(st + A_TILE);
             const uint64_t b1 = tc::smem_desc_sw128(st + b_off);
@@ -381,7 +387,7 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
               if (PAIR) tc::mma_commit_2sm(&empty[stage], 0x3); else tc::mma_commit(&empty[stage]);
             }
             __syncwarp();
-            if (++stage == nstages) {
+            if (++stage == n_st) {
               stage = 0;
               phase ^= 1;
             }
