@@ -637,6 +637,28 @@ def _timed_sharded(args, device, run_batch, n_batches, local):
     return float(t.item()), clk.summary()
 
 
+def _timed_sharded_many(args, device, eng, batches, top_k, lanes, local):
+    """Like _timed_sharded, the K steps issued as batches in flight."""
+    ws, _, _ = dist_env()
+    nb = len(batches)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    with ClockSampler(local) as clk:
+        warm(lambda i: eng.run_many([batches[(i + j) % nb] for j in range(lanes)], top_k,
+                                    lanes=lanes), args.warmup)  # every lane's scratch
+        dist.barrier()
+        torch.cuda.synchronize()
+        ev[0].record()
+        eng.run_many([batches[(args.warmup + i) % nb] for i in range(args.steps)], top_k,
+                     lanes=lanes)
+        ev[1].record()
+        torch.cuda.synchronize()
+        dist.barrier()
+    t = torch.tensor([ev[0].elapsed_time(ev[1])], dtype=torch.float64, device=device)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item()), clk.summary()
+
+
 def _e2e_sharded(device, host_batches, run_dev):
     """End to end through the sharded engine: every step copies its pinned
     host batch in, runs, and copies the merged top-k out (all inside)."""
@@ -705,7 +727,10 @@ def run_sharded(args, w):
     B = w.batch
     nb = max(1, qs.shape[0] // B)
     batches = [qs[j * B:(j + 1) * B].contiguous() for j in range(nb)]
-    ms, clk = _timed_sharded(args, device, lambda j: eng.run(batches[j], w.top_k), nb, local)
+    # two batches in flight: batch i+1's quantize and scan overlap batch i's
+    # exchanges (ShardedEngine.run_many); every rank issues the same order
+    lanes = max(1, args.lanes or 2)
+    ms, clk = _timed_sharded_many(args, device, eng, batches, w.top_k, lanes, local)
     syncs = {}
     launches = count_launches(lambda: eng.run(batches[0], w.top_k), syncs)
     steps = [batches[(args.warmup + i) % nb].cpu().pin_memory() for i in range(args.steps)]
@@ -731,7 +756,7 @@ def run_sharded(args, w):
                           "h2d_bytes_per_step": B * w.n_views * w.dim * 4,
                           "d2h_bytes_per_step": B * w.top_k * 12},
                          launches * args.steps, roof, None, clk,
-                         {"build_s": build_s, "shard_shapes": hi - lo,
+                         {"build_s": build_s, "shard_shapes": hi - lo, "lanes": lanes,
                           "host_blocking_cuda_calls_per_step": syncs,
                           "collectives_per_step": 2 if ws > 1 else 0,
                           "exchange": "packed all_gather_into_tensor (score bits, "

@@ -252,6 +252,27 @@ class ShardedEngine:
         tb = ranking_tiebreak(li, self.idrank, self_global)
         return exchange_topk(lv, li, tb, k, False, self.group)
 
+    def run_many(self, batches, top_k: int, rerank: bool = True, lanes: int = 2):
+        """Query batches in flight on `lanes` streams: batch i runs on stream
+        i % lanes (its own scratch), so batch i+1's quantize and scan overlap
+        batch i's exchanges and S-IF.  Every rank issues the same batches in
+        the same order, so the collectives match.  Returns the per-batch
+        (idx, val) on the device."""
+        from .index import lane_streams
+
+        main = torch.cuda.current_stream()
+        streams = lane_streams(max(1, lanes))
+        for st in streams:
+            st.wait_stream(main)
+        out = []
+        for i, Q in enumerate(batches):
+            st = streams[i % len(streams)]
+            with torch.cuda.stream(st):
+                out.append(self.run(Q, top_k, rerank=rerank))
+        for st in streams:
+            main.wait_stream(st)
+        return out
+
     def rerank_lists(self, q_idx, q_val, top_k: int, self_global=None):
         """Config 5 re-rank from given best-first lists (index.py:249-299):
         the neighbours (first k2 positive entries) are global already, so the

@@ -50,7 +50,16 @@ def _sharded(rank, world, db, qs, C, cfgkw, top_k):
     fif, raw, sif = build_sharded(X, eg.DeviceCodebook.from_numpy(C), cfg, N)
     idrank = torch.arange(N, dtype=torch.int32, device="cuda")  # zero-padded ids: rank == ordinal
     eng = ShardedEngine(fif, raw, sif, idrank, cfg, N)
-    i, v = eng.run(torch.from_numpy(qs).cuda(), top_k, rerank=True)
+    Q = torch.from_numpy(qs).cuda()
+    i, v = eng.run(Q, top_k, rerank=True)
+    # batches in flight on two streams give the same rankings
+    half = (Q.shape[0] + 1) // 2
+    outs = eng.run_many([Q[:half].contiguous(), Q[half:].contiguous()], top_k, lanes=2)
+    torch.cuda.synchronize()
+    i2 = torch.cat([o[0] for o in outs]).cpu().numpy()
+    v2 = torch.cat([o[1] for o in outs]).cpu().numpy()
+    np.testing.assert_array_equal(i2, i.cpu().numpy())
+    np.testing.assert_array_equal(v2, v.cpu().numpy())
     return i.cpu().numpy().astype(np.int64), v.cpu().numpy()
 
 
