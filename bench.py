@@ -189,6 +189,13 @@ def count_launches(fn, syncs: dict | None = None) -> int:
         for e in evs:
             if e.device_type.name == "CPU" and e.name in _SYNC_APIS:
                 syncs[e.name] = syncs.get(e.name, 0) + 1
+        with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as base:
+            pass  # the profiler's own calls (its stop synchronizes the device)
+        for e in base.events():
+            if e.device_type.name == "CPU" and e.name in syncs:
+                syncs[e.name] -= 1
+        for k in [k for k, v in syncs.items() if v <= 0]:
+            del syncs[k]
     torch.cuda.synchronize()
     return sum(1 for e in evs if e.device_type.name == "CUDA" and "gift::" in e.name)
 

@@ -206,8 +206,13 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
   // in the ring instead of four (more k-blocks in flight; measured neutral on
   // config 4, whose scan is paced by its per-item latencies)
   const bool small_st = qz && !PAIR && !LO;
-  const int st_bytes = small_st ? A_TILE + B_TILE : stage_bytes;
-  const int n_st = small_st ? RING_BYTES / (A_TILE + B_TILE) : nstages;
+  // ... and two k-blocks per stage (one producer / MMA hand-off per two
+  // k-blocks: the per-k-block hand-off paced this scan), when
+  // the drain chunks are whole stages
+  const int kps = (small_st && p.chunk_kb % 2 == 0) ? 2 : 1;  // k-blocks per stage
+  constexpr int SUB = A_TILE + B_TILE;  // one k-block's A + b1 in a small stage
+  const int st_bytes = small_st ? kps * SUB : stage_bytes;
+  const int n_st = small_st ? RING_BYTES / (kps * SUB) : nstages;
   const uint32_t nbuf = qz4 ? 4u : 2u;
   const uint32_t buf_cols = qz4 ? TC_NMAX : ((!PAIR || !LO) ? 2 * TC_NMAX : TC_NMAX);
   const int nkb = (p.d + TC_BK - 1) / TC_BK;
@@ -270,9 +275,10 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
         // half of each plane (pair, lo)
         const uint32_t bytes =
             a_bytes + (PAIR && qz ? brows : PAIR && cb ? I.n : (qz ? 1 : 2) * brows) * TC_BK * 2;
-        for (int kb = 0; kb < nkb; ++kb) {
+        for (int kb = 0; kb < nkb; kb += kps) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * st_bytes;
+          const int nk = min(kps, nkb - kb);  // k-blocks in this stage
           if (!tc::elect_one()) {
             // other lanes: nothing to issue
           } else if (GIFT_EXP(p, 8)) {
@@ -297,6 +303,15 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
             } else {
               tc::tma_load_2d_2sm(st + b_off, &tmB1h, lbar, kb * TC_BK, r0);
               tc::tma_load_2d_2sm(st + b_off + B_PART, &tmB2h, lbar, kb * TC_BK, r0);
+            }
+          } else if (small_st) {  // [A(kb) | b1(kb)] [A(kb+1) | b1(kb+1)]
+            tc::mbar_arrive_expect_tx(&full[stage], nk * bytes);
+            for (int j = 0; j < nk; ++j) {
+              uint8_t* sj = st + j * SUB;
+              tc::tma_load_2d(sj, &tmA1, &full[stage], (kb + j) * TC_BK, I.p0);
+              for (int x = 0; x < I.n / 64; ++x)
+                tc::tma_load_2d(sj + A_TILE + x * B_BOX, &tmB1, &full[stage], (kb + j) * TC_BK,
+                                I.pb0 + 64 * x);
             }
           } else {
             tc::mbar_arrive_expect_tx(&full[stage], bytes);
@@ -352,10 +367,35 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
           // buffer; qz4: D1 per chunk buffer
           const uint32_t d1 = tmem_base + buf * buf_cols;
           const int kend = min(kb0 + chunk_kb, nkb);
-          for (int kb = kb0; kb < kend; ++kb) {
+          for (int kb = kb0; kb < kend; kb += kps) {
             tc::mbar_wait(&full[stage], phase);
             tc::tc_fence_after();
             uint8_t* st = smem + stage * st_bytes;
+            if (small_st) {  // fp16-exact queries, single CTA: D1 = a1 . b1, kps k-blocks
+              const int nk = min(kps, kend - kb);
+              if (tc::elect_one()) {
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                  if (j >= nk) break;
+                  const uint64_t a1 = tc::smem_desc_sw128(st + j * SUB);
+                  const uint64_t b1 = tc::smem_desc_sw128(st + j * SUB + A_TILE);
+#pragma unroll
+                  for (int k = 0; k < TC_BK / 16; ++k) {
+                    if (GIFT_EXP(p, 4)) break;
+                    const uint32_t acc1 = (kb + j > kb0 || k > 0) ? 1u : 0u;
+                    const uint64_t adv = static_cast<uint64_t>(k * 2);
+                    tc::mma_f16(d1, a1 + adv, b1 + adv, idesc, acc1);
+                  }
+                }
+                tc::mma_commit(&empty[stage]);
+              }
+              __syncwarp();
+              if (++stage == n_st) {
+                stage = 0;
+                phase ^= 1;
+              }
+              continue;
+            }
             const uint64_t a1 = tc::smem_desc_sw128(st);
             const uint64_t a2 = tc::smem_desc_sw128(st + A_TILE);
             const uint64_t b1 = tc::smem_desc_sw128(st + b_off);

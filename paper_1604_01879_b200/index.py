@@ -240,6 +240,15 @@ class QueryEngine:
 
     def run(self, Qa, Qb=None, top_k=10, rerank=True, self_local=None, vq=None, vqb=None,
             stream=None, scan_events=None, exact=False):
+        torch.cuda.nvtx.range_push("gift.query_batch")  # timeline marker (nsys / CUPTI)
+        try:
+            return self._run(Qa, Qb, top_k, rerank, self_local, vq, vqb, stream, scan_events,
+                             exact)
+        finally:
+            torch.cuda.nvtx.range_pop()
+
+    def _run(self, Qa, Qb=None, top_k=10, rerank=True, self_local=None, vq=None, vqb=None,
+             stream=None, scan_events=None, exact=False):
         """Device batch -> (idx [B, k] i32 global ordinals, val [B, k] f64).
         exact: every query view probes every cell (ma = K), which is the
         reference's exact set similarity (index.py:230-243, matching.py:55-61:

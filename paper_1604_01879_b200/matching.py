@@ -8,6 +8,7 @@ gift_exact_sets), FirstInvertedFile, build_fif, query_fif, save_fif/load_fif.
 from __future__ import annotations
 
 import struct
+import threading
 
 import numpy as np
 import torch
@@ -18,14 +19,16 @@ from .codebook import Codebook
 from .errors import DimensionMismatch, EmptySet, FormatError
 
 DEFAULT_MA = 2
-_RUNNER = None
+_TLS = threading.local()
 
 
 def runner() -> eg.ScoreRunner:
-    global _RUNNER
-    if _RUNNER is None:
-        _RUNNER = eg.ScoreRunner()
-    return _RUNNER
+    """The calling thread's scan launcher (its grow-only workspaces are per
+    stream; one per thread keeps concurrent callers independent)."""
+    r = getattr(_TLS, "runner", None)
+    if r is None:
+        r = _TLS.runner = eg.ScoreRunner()
+    return r
 
 
 def sim_mode(similarity: str) -> int:
