@@ -261,11 +261,13 @@ def c5_config(c, n, parallelism):
 def default_lanes(name):
     """(batches in flight, SMs the scan leaves to the other lanes) per config:
     config 2's non-scan kernels are ~20% of a step and overlap the next
-    batches' scans; config 3 (owner reduce, 105 GB) and config 4 (tensor-bound
-    scan) measured no gain."""
+    batches' scans (profiles/r02/c2_lanes_reserve_sweep.json); configs 3 and 4
+    (no host synchronisation left in the query path) gain 3% / 2% from two
+    lanes with 20 SMs left to the other lane."""
     from paper_1604_01879_b200.index import LANE_RESERVE_SMS
 
-    return {"c1": (4, LANE_RESERVE_SMS), "c2": (4, LANE_RESERVE_SMS)}.get(name, (1, 0))
+    return {"c1": (4, LANE_RESERVE_SMS), "c2": (4, LANE_RESERVE_SMS),
+            "c3": (2, 20), "c4": (2, 20)}.get(name, (1, 0))
 
 
 def scan_work(fif, Q, w, top_k, similarity="gaussian"):

@@ -1,0 +1,5 @@
+# C3 with batches in flight
+set -x
+for cfg in "1 0" "2 20" "2 36"; do set -- $cfg
+timeout 1500 python bench.py --config c3 --steps 8 --warmup 3 --no-cpu-baseline --lanes $1 --reserve-sms $2 > gpurun_out/r2u_c3_l$1_r$2.json 2> gpurun_out/r2u_c3_l$1_r$2.err; echo c3_$1_$2=$?
+done
