@@ -33,9 +33,15 @@ run = eg.ScoreRunner()
 ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
 for e in ev:
     e.record()
+run.score(fif.dev, q, w.ma, nat.SIM_GAUSSIAN, 0.5, cand_k=4, dense=False)
+torch.cuda.synchronize()
+meta = next(iter(run._ws.values())).get(64)[:64].view(torch.int64).cpu().tolist()
+print(f"{name} items {meta[0]} compact {meta[1]} tiles {fif.dev.T} postings {fif.dev.P} "
+      f"segments {fif.dev.S} queries {q.shape[0]}", flush=True)
 for bits, label in ((0, "full"), (1, "no tail"), (2, "no drains"), (3, "no drains, no tail"),
                     (4, "no MMAs"), (5, "no MMAs, no tail"), (8, "no loads"),
-                    (9, "no loads, no tail"), (15, "nothing (scheduling only)")):
+                    (9, "no loads, no tail"), (11, "MMAs only"), (7, "loads only"),
+                    (13, "drains only"), (14, "tail only"), (15, "nothing (scheduling only)")):
     lib.gift_scan_experiment(bits)
     ts = []
     for i in range(6):
