@@ -467,6 +467,7 @@ def run_gift(args, w):
     eng = bundle.engine
     if args.drain_kb or args.pair != "auto":
         eng.fa.set_variant(drain_kb=args.drain_kb, pair=args.pair)
+    _set_sif_mode(eng.sif, args)
     B = w.batch
     nb = max(1, qs.shape[0] // B)
     order = [(rank + i * ws) % nb for i in range(args.steps + args.warmup)]
@@ -774,6 +775,14 @@ def run_sharded(args, w):
     dist.destroy_process_group()
 
 
+def _set_sif_mode(sif, args):
+    """--sif: force one S-IF query implementation (default: by batch size)."""
+    from paper_1604_01879_b200 import _native as nat
+
+    sif.query_flags = {"auto": 0, "rows": nat.SIF_ROWS, "sort": nat.SIF_SORT,
+                       "bucket": nat.SIF_BUCKET}[args.sif]
+
+
 def run_c5(args):
     """Config 5 (re-rank dominated): given top-50 lists for 1M shapes, S-IF
     over all shapes, queries re-ranked with k = 50 neighbour-set Jaccard.
@@ -801,6 +810,7 @@ def run_c5(args):
 
         _init_dist(device)
         raw, sif = build_sharded_from_lists(idx, val, cfg)
+        _set_sif_mode(sif, args)
         eng = ShardedEngine(None, raw, sif, torch.arange(n, dtype=torch.int32, device=device),
                             cfg, n)
 
@@ -810,6 +820,7 @@ def run_c5(args):
     else:
         bundle = build_index_from_lists(idx, val, synth.shape_ids(n), cfg)
         eng = bundle.engine
+        _set_sif_mode(eng.sif, args)
 
         def run_q(qi, qv, r):
             return eng.rerank_lists(qi, qv, top_k=c["top_k"], self_local=r.to(torch.int32))
@@ -1015,6 +1026,8 @@ def main():
                          "library default)")
     ap.add_argument("--pair", default="auto", choices=["auto", "on", "off"],
                     help="F-IF scan on CTA pairs (cta_group::2): default per storage")
+    ap.add_argument("--sif", default="auto", choices=["auto", "rows", "sort", "bucket"],
+                    help="S-IF query implementation (default: by batch size)")
     ap.add_argument("--shard", action="store_true",
                     help="shard the database by shape over the ranks (default for configs "
                          "3-5 at N > 1)")

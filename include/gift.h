@@ -370,12 +370,17 @@ int gift_sif_query(const int64_t* e_off, const int32_t* e_ord,
  * power of two keeps the rows' hot entries on different DRAM channels).  order[r] = local shape of id rank r (inverse of idrank).
  * max_touched: an upper bound of the shapes one query can touch (support cap
  * x the longest S-IF entry). */
-/* flags: 0 = by batch size (the sort-based path for B x max_touched >= 2^24),
- * GIFT_SIF_ROWS = per-query accumulator rows, GIFT_SIF_SORT = sort-based
- * (identical results) */
+/* flags: 0 = by batch size (B x max_touched >= 2^24: the bucketed path, or
+ * the sort-based one beyond the bucketed limits -- cap <= 1024 support
+ * entries, n_local <= 2^24), GIFT_SIF_ROWS = per-query accumulator rows,
+ * GIFT_SIF_SORT = (query, shape) pairs radix-sorted, GIFT_SIF_BUCKET = pairs
+ * split by shape range and reduced in shared memory (no host
+ * synchronisation).  All give identical results; a forced mode outside its
+ * limits falls back to the rows path. */
 #define GIFT_SIF_ROWS 1
 #define GIFT_SIF_SORT 2
-size_t gift_sif_query_topk_ws_bytes(int32_t B, int64_t n_local, int32_t k,
+#define GIFT_SIF_BUCKET 4
+size_t gift_sif_query_topk_ws_bytes(int32_t B, int32_t cap, int64_t n_local, int32_t k,
                                     int64_t max_touched, int32_t flags);
 int gift_sif_query_topk(const int64_t* e_off, const int32_t* e_ord,
                         const double* e_val, const double* norms,

@@ -31,7 +31,7 @@ FIF_RAW_ACCUM = 1 << 29
 FIF_VARIANT_MASK = ((1 << 16) | (1 << 17) | (3 << 18) | (1 << 20) | (3 << 21) | (31 << 24)
                     | FIF_RAW_ACCUM)
 QUANT_SIMT = 1        # gift_quantize_ex flags
-SIF_ROWS, SIF_SORT = 1, 2  # gift_sif_query_topk flags
+SIF_ROWS, SIF_SORT, SIF_BUCKET = 1, 2, 4  # gift_sif_query_topk flags
 
 
 def fif_reserve_sms(n: int) -> int:
@@ -128,7 +128,7 @@ _SIGS = {
     "gift_sif_permute": (_c_i32, [_c_p, _c_p, _c_p, _c_i64, _c_p, _c_p, _c_p]),
     "gift_sif_query": (_c_i32, [_c_p, _c_p, _c_p, _c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p,
                                 _c_i32, _c_i32, _c_p, _c_p]),
-    "gift_sif_query_topk_ws_bytes": (_c_sz, [_c_i32, _c_i64, _c_i32, _c_i64, _c_i32]),
+    "gift_sif_query_topk_ws_bytes": (_c_sz, [_c_i32, _c_i32, _c_i64, _c_i32, _c_i64, _c_i32]),
     "gift_sif_query_topk": (_c_i32, [_c_p, _c_p, _c_p, _c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p,
                                      _c_p, _c_i32, _c_i32, _c_p, _c_i32, _c_i64, _c_p, _c_p, _c_p,
                                      _c_i64, _c_i32, _c_i64, _c_p, _c_p, _c_p, _c_sz, _c_i32,

@@ -534,6 +534,517 @@ __global__ void sif_fill_kernel(const uint32_t* __restrict__ keys, const int64_t
   if (lane == 0) row_cnt[b] = static_cast<int32_t>(pos + nf);
 }
 
+// ---- bucketed S-IF query (no sort, no host synchronisation) ----------------
+// The same result again, from a stable split of each query's pairs into
+// buckets of 2^rb consecutive local shapes: one CTA per query counts its
+// pairs per (warp, bucket) and scatters them warp-ordered, so every bucket
+// holds its (shape, contribution) pairs in the query's entry order.  One warp
+// then reduces a bucket in a dense f64 shared-memory accumulator; lanes of a
+// 32-pair chunk that hit the same shape (two entries) take turns in lane
+// order, so every sum is the reference's left-to-right acc[j] += ... order
+// (rerank.py:219-230), bit-equal to the other two paths.
+constexpr int SB_WARPS = 8;
+constexpr int SB_MAX_R = 2048;  // buckets per query (split kernel counters)
+constexpr int SB_MAX_E = 1024;  // query support entries staged in shared memory
+constexpr int SB_MIN_RB = 11;   // 2^11 shapes (16 KB of f64) per reducing warp
+constexpr int SB_MAX_RB = 13;
+constexpr int SB_U = 4;        // chunks of 32 pairs in flight per lane
+
+// exclusive scan of a[0, n) in place (all threads of the CTA); returns the total
+__device__ int32_t block_scan_excl(int32_t* a, int n, int32_t* wsum) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int i0 = min(n, tid * per), i1 = min(n, i0 + per);
+  int32_t own = 0;
+  for (int i = i0; i < i1; ++i) own += a[i];
+  int32_t x = own;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  int32_t before = 0, total = 0;
+  for (int w = 0; w < nw; ++w) {
+    if (w < warp) before += wsum[w];
+    total += wsum[w];
+  }
+  int32_t run = before + x - own;
+  for (int i = i0; i < i1; ++i) {
+    const int32_t t = a[i];
+    a[i] = run;
+    run += t;
+  }
+  __syncthreads();
+  return total;
+}
+
+__device__ __forceinline__ int entry_of(const int32_t* pre, int ne, int32_t t) {
+  int lo = 0, hi = ne;  // last e with pre[e] <= t
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (pre[mid] <= t) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__host__ __device__ constexpr size_t sif_pre_bytes(int cap) {
+  return (sizeof(int32_t) * (cap + 1) + 15) / 16 * 16;
+}
+
+size_t sif_split_smem(int cap, int R) {
+  return static_cast<size_t>(cap) * 16 + sif_pre_bytes(cap) +
+         sizeof(int32_t) * static_cast<size_t>(SB_WARPS + 1) * R;
+}
+
+// One CTA per query b: pairs of the query support, flattened in entry order
+// (t = pre[e] + posting), warp w owning t in [w per, (w + 1) per).
+__global__ void __launch_bounds__(SB_WARPS * 32)
+    sif_split_kernel(const int32_t* __restrict__ q_idx, const double* __restrict__ q_val,
+                     const int32_t* __restrict__ q_cnt, int cap, const int64_t* __restrict__ e_off,
+                     const int32_t* __restrict__ e_ord, const double* __restrict__ e_val,
+                     int64_t n_global, int rb, int R, const int64_t* __restrict__ off,
+                     int32_t* __restrict__ bstart, uint16_t* __restrict__ pj,
+                     double* __restrict__ pc) {
+  extern __shared__ __align__(16) char sb_smem[];
+  int64_t* s_p0 = reinterpret_cast<int64_t*>(sb_smem);
+  double* s_v = reinterpret_cast<double*>(sb_smem + static_cast<size_t>(cap) * 8);
+  int32_t* s_pre = reinterpret_cast<int32_t*>(sb_smem + static_cast<size_t>(cap) * 16);
+  int32_t* s_cnt =
+      reinterpret_cast<int32_t*>(sb_smem + static_cast<size_t>(cap) * 16 + sif_pre_bytes(cap));
+  int32_t* s_tot = s_cnt + SB_WARPS * R;
+  __shared__ int32_t s_wsum[SB_WARPS];
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const int ne = min(q_cnt[b], cap);
+  for (int e = tid; e < ne; e += blockDim.x) {
+    const int64_t i = q_idx[static_cast<int64_t>(b) * cap + e];
+    const bool ok = i >= 0 && i < n_global;
+    const int64_t a = ok ? e_off[i] : 0;
+    s_p0[e] = a;
+    s_v[e] = q_val[static_cast<int64_t>(b) * cap + e];
+    s_pre[e] = ok ? static_cast<int32_t>(e_off[i + 1] - a) : 0;
+  }
+  for (int x = tid; x < SB_WARPS * R; x += blockDim.x) s_cnt[x] = 0;
+  __syncthreads();
+  const int32_t Tb = block_scan_excl(s_pre, ne, s_wsum);
+  if (tid == 0) s_pre[ne] = Tb;
+  __syncthreads();
+  const int32_t per = (Tb + SB_WARPS - 1) / SB_WARPS;
+  const int32_t t0w = min(Tb, warp * per), t1w = min(Tb, t0w + per);
+  int32_t* my = s_cnt + warp * R;
+  // pass 1: per-(warp, bucket) counts; SB_U chunks' loads in flight per lane,
+  // one counter update per run of equal buckets in a chunk (leader lane; the
+  // counters are warp-private, leaders of one chunk hold distinct buckets)
+  {
+    int e = entry_of(s_pre, ne, t0w + lane);
+    for (int32_t c0 = t0w; c0 < t1w; c0 += 32 * SB_U) {
+      int32_t jj[SB_U];
+#pragma unroll
+      for (int u = 0; u < SB_U; ++u) {
+        const int32_t t = c0 + u * 32 + lane;
+        jj[u] = -1;
+        if (t < t1w) {
+          while (s_pre[e + 1] <= t) ++e;
+          jj[u] = e_ord[s_p0[e] + (t - s_pre[e])];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < SB_U; ++u) {
+        const uint32_t key = jj[u] >= 0 ? static_cast<uint32_t>(jj[u]) >> rb : 0x80000000u | lane;
+        const unsigned peers = __match_any_sync(0xffffffffu, key);
+        if (jj[u] >= 0 && __ffs(peers) - 1 == lane) my[key] += __popc(peers);
+        __syncwarp();
+      }
+    }
+  }
+  __syncthreads();
+  for (int r = tid; r < R; r += blockDim.x) {  // bucket totals; warp prefix within a bucket
+    int32_t run = 0;
+    for (int w = 0; w < SB_WARPS; ++w) {
+      const int32_t c = s_cnt[w * R + r];
+      s_cnt[w * R + r] = run;
+      run += c;
+    }
+    s_tot[r] = run;
+  }
+  __syncthreads();
+  block_scan_excl(s_tot, R, s_wsum);
+  int32_t* bs = bstart + static_cast<int64_t>(b) * (R + 1);
+  for (int r = tid; r < R; r += blockDim.x) {
+    bs[r] = s_tot[r];
+    for (int w = 0; w < SB_WARPS; ++w) s_cnt[w * R + r] += s_tot[r];
+  }
+  if (tid == 0) bs[R] = Tb;
+  __syncthreads();
+  // pass 2: warp-ordered stable scatter (a lane's slot = its warp's bucket
+  // cursor + the lanes before it in the chunk with the same bucket)
+  const int64_t base = off[b];
+  const uint32_t mask = (1u << rb) - 1u;
+  int e = entry_of(s_pre, ne, t0w + lane);
+  for (int32_t c0 = t0w; c0 < t1w; c0 += 32 * SB_U) {
+    int32_t jj[SB_U];
+    double cc[SB_U], vq[SB_U];
+#pragma unroll
+    for (int u = 0; u < SB_U; ++u) {  // loads only: the uses below wait for them
+      const int32_t t = c0 + u * 32 + lane;
+      jj[u] = -1;
+      cc[u] = vq[u] = 0.0;
+      if (t < t1w) {
+        while (s_pre[e + 1] <= t) ++e;
+        const int64_t p = s_p0[e] + (t - s_pre[e]);
+        jj[u] = e_ord[p];
+        cc[u] = e_val[p];
+        vq[u] = s_v[e];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < SB_U; ++u) {
+      const bool valid = jj[u] >= 0;
+      const uint32_t j = static_cast<uint32_t>(jj[u]);
+      const uint32_t key = valid ? j >> rb : 0x80000000u | lane;
+      const unsigned peers = __match_any_sync(0xffffffffu, key);
+      const int leader = __ffs(peers) - 1;
+      int32_t pos = 0;
+      if (valid && lane == leader) {
+        pos = my[key];
+        my[key] = pos + __popc(peers);
+      }
+      pos = __shfl_sync(0xffffffffu, pos, leader) + __popc(peers & lt);
+      if (valid) {
+        pj[base + pos] = static_cast<uint16_t>(j & mask);
+        pc[base + pos] = fmin(vq[u], cc[u]);
+      }
+    }
+  }
+}
+
+// Persistent: warp w reduces the contiguous bucket range [w per, (w + 1) per)
+// (bucket g = query g / R, shape range g % R) in its shared f64 row
+// acc[2^rb], zero between buckets.  The touched shapes' sums are compacted in
+// place to the front of the bucket's pair region (pc = sum, pj = shape;
+// count ntb[g]) -- the ranking kernel scores and selects them.  Bounds of 32
+// buckets come in one load per lane; the next bucket's first chunk is loaded
+// before the current one is reduced.
+__global__ void sif_bucket_reduce_kernel(uint16_t* __restrict__ pj, double* __restrict__ pc,
+                                         const int64_t* __restrict__ off,
+                                         const int32_t* __restrict__ bstart, int B, int R, int rb,
+                                         int32_t* __restrict__ ntb) {
+  extern __shared__ double s_acc[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const int W = 1 << rb;
+  for (int x = tid; x < nw * W; x += blockDim.x) s_acc[x] = 0.0;
+  __syncthreads();
+  double* acc = s_acc + warp * W;
+  const int64_t nb = static_cast<int64_t>(B) * R;
+  const int64_t totw = static_cast<int64_t>(gridDim.x) * nw;
+  const int64_t per = (nb + totw - 1) / totw;
+  const int64_t g0 = (static_cast<int64_t>(blockIdx.x) * nw + warp) * per;
+  const int64_t g1 = min64(nb, g0 + per);
+  for (int64_t gb = g0; gb < g1; gb += 32) {
+    int64_t sL = 0, eL = 0;
+    if (gb + lane < g1) {
+      const int64_t g = gb + lane;
+      const int64_t b = g / R, r = g % R;
+      const int64_t q0 = off[b];
+      const int32_t* bs = bstart + b * (R + 1);
+      sL = q0 + bs[r];
+      eL = q0 + bs[r + 1];
+    }
+    const int nbk = static_cast<int>(min64(32, g1 - gb));
+    int64_t s = __shfl_sync(0xffffffffu, sL, 0), e = __shfl_sync(0xffffffffu, eL, 0);
+    uint32_t jn = s + lane < e ? pj[s + lane] : 0x10000u + lane;
+    double cn = s + lane < e ? pc[s + lane] : 0.0;
+    for (int i = 0; i < nbk; ++i) {
+      // next bucket's bounds and first chunk
+      const int64_t s2 = __shfl_sync(0xffffffffu, sL, (i + 1) & 31);
+      const int64_t e2 = __shfl_sync(0xffffffffu, eL, (i + 1) & 31);
+      const bool more = i + 1 < nbk;
+      const uint32_t jn2 = more && s2 + lane < e2 ? pj[s2 + lane] : 0x10000u + lane;
+      const double cn2 = more && s2 + lane < e2 ? pc[s2 + lane] : 0.0;
+      int nt = 0;
+      for (int64_t c0 = s; c0 < e; c0 += 32) {  // pass 1: accumulate in lane turns
+        const uint32_t jl = jn;
+        const double c = cn;
+        const bool valid = c0 + lane < e;
+        const int64_t tn = c0 + 32 + lane;
+        jn = tn < e ? pj[tn] : 0x10000u + lane;
+        cn = tn < e ? pc[tn] : 0.0;
+        const unsigned peers = __match_any_sync(0xffffffffu, jl);
+        const int rank = __popc(peers & lt);
+        const int mr = __reduce_max_sync(0xffffffffu, rank);
+        for (int rr = 0; rr <= mr; ++rr) {
+          if (valid && rank == rr) acc[jl] = __dadd_rn(acc[jl], c);
+          __syncwarp();
+        }
+      }
+      for (int64_t c0 = s; c0 < e; c0 += 32) {  // pass 2: each shape once, compacted
+        const int64_t t = c0 + lane;
+        const bool valid = t < e;
+        const uint32_t jl = valid ? pj[t] : 0x10000u + lane;
+        const unsigned peers = __match_any_sync(0xffffffffu, jl);
+        const bool lead = valid && __ffs(peers) - 1 == lane;
+        const double a = lead ? acc[jl] : 0.0;
+        const bool fin = lead && a != 0.0;  // contributions are > 0
+        if (fin) acc[jl] = 0.0;
+        const unsigned fb = __ballot_sync(0xffffffffu, fin);
+        if (fin) {  // slot <= t: pairs at or before this chunk, already read
+          const int64_t at = s + nt + __popc(fb & lt);
+          pc[at] = a;
+          pj[at] = static_cast<uint16_t>(jl);
+        }
+        nt += __popc(fb);
+        __syncwarp();
+      }
+      if (lane == 0) ntb[gb + i] = nt;
+      s = s2;
+      e = e2;
+      jn = jn2;
+      cn = cn2;
+    }
+  }
+}
+
+// Ranking of the bucketed query (index.py:290-294), one CTA per query: the
+// touched shapes' (score, tiebreak, ordinal) -- the accumulator-row kernel's
+// finalisation -- go to the query's candidate row at off[b] + b (k + 1),
+// with the zero-score fill appended when fewer than k are touched.  Rows
+// that fit the sort buffer are bitonic-sorted whole; longer rows are
+// filtered by the k-th best of a strided sample (a lower bound of the row's
+// k-th best key), survivors collected into the buffer in rounds that cannot
+// overflow it and sorted with the running best.  Keys are unique per row, so
+// the first k are the dense ranking's.
+constexpr int RK_THREADS = 256;
+constexpr int RK_BUF = 2048;  // sort buffer: [0, RK_BEST) best so far, then survivors
+constexpr int RK_BEST = 256;  // >= k
+
+__device__ void bitonic_sort_desc_n(double* s, uint32_t* t, int32_t* j, int N) {
+  for (int size = 2; size <= N; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < N / 2; i += blockDim.x) {
+        const int lo = 2 * stride * (i / stride) + (i % stride);
+        const int hi = lo + stride;
+        const bool desc = (lo & size) == 0;
+        if (key_better(s[hi], t[hi], s[lo], t[lo]) == desc) {
+          const double ts = s[lo]; s[lo] = s[hi]; s[hi] = ts;
+          const uint32_t tt = t[lo]; t[lo] = t[hi]; t[hi] = tt;
+          const int32_t tj = j[lo]; j[lo] = j[hi]; j[hi] = tj;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+size_t sif_rank_smem(int R) { return static_cast<size_t>(RK_BUF) * 16 + sizeof(int32_t) * 2 * (R + 1); }
+
+__global__ void __launch_bounds__(RK_THREADS)
+    sif_bucket_rank_kernel(const uint16_t* __restrict__ pj, const double* __restrict__ pc,
+                           const int64_t* __restrict__ off, const int32_t* __restrict__ bstart,
+                           const int32_t* __restrict__ ntb, int R, int rb,
+                           const double* __restrict__ norms, const double* __restrict__ q_norm,
+                           const int32_t* __restrict__ order, const int32_t* __restrict__ idrank,
+                           const int32_t* __restrict__ self_local, int64_t ord_base,
+                           int64_t n_local, int k, double* __restrict__ cs,
+                           uint32_t* __restrict__ ct, int32_t* __restrict__ ci,
+                           int32_t* __restrict__ out_idx, double* __restrict__ out_val) {
+  extern __shared__ __align__(16) char rk_smem[];
+  double* xs = reinterpret_cast<double*>(rk_smem);
+  uint32_t* xt = reinterpret_cast<uint32_t*>(rk_smem + RK_BUF * 8);
+  int32_t* xj = reinterpret_cast<int32_t*>(rk_smem + RK_BUF * 12);
+  int32_t* s_ps = reinterpret_cast<int32_t*>(rk_smem + RK_BUF * 16);  // pair starts
+  int32_t* s_cs = s_ps + R + 1;                                         // candidate starts
+  __shared__ int32_t s_wsum[RK_THREADS / 32];
+  __shared__ int s_cnt, s_nfill;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const int64_t q0 = off[b];
+  const int64_t row = q0 + static_cast<int64_t>(b) * (k + 1);
+  for (int r = tid; r <= R; r += RK_THREADS) {
+    s_ps[r] = bstart[static_cast<int64_t>(b) * (R + 1) + r];
+    s_cs[r] = r < R ? ntb[static_cast<int64_t>(b) * R + r] : 0;
+  }
+  if (tid == 0) s_nfill = 0;
+  __syncthreads();
+  const int32_t n = block_scan_excl(s_cs, R, s_wsum);
+  if (tid == 0) s_cs[R] = n;
+  __syncthreads();
+  const double qn = q_norm[b];
+  const int64_t sl = self_local ? static_cast<int64_t>(self_local[b]) : -1;
+  const int32_t stride = n > RK_BUF ? (n + RK_BUF - 1) / RK_BUF : 1;
+  // pass 1: score every touched shape (4 candidates' loads in flight per thread)
+  for (int32_t t0 = 0; t0 < n; t0 += 4 * RK_THREADS) {
+    double a[4], nr[4];
+    int32_t jg[4], rk[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int32_t t = t0 + u * RK_THREADS + tid;
+      jg[u] = -1;
+      if (t < n) {
+        int lo = 0, hi = R - 1;  // bucket: last r with s_cs[r] <= t
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (s_cs[mid] <= t) lo = mid; else hi = mid - 1;
+        }
+        const int64_t pos = q0 + s_ps[lo] + (t - s_cs[lo]);
+        a[u] = pc[pos];
+        jg[u] = (lo << rb) + pj[pos];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (jg[u] >= 0) {
+        nr[u] = norms[jg[u]];
+        rk[u] = idrank ? idrank[jg[u]] : 0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int32_t t = t0 + u * RK_THREADS + tid;
+      if (jg[u] < 0) continue;
+      const int64_t j = jg[u];
+      const double sc = __ddiv_rn(a[u], __dsub_rn(__dadd_rn(qn, nr[u]), a[u]));
+      const uint32_t tb =
+          j == sl ? 0u : 1u + static_cast<uint32_t>(idrank ? static_cast<int64_t>(rk[u]) : ord_base + j);
+      const int32_t jj = static_cast<int32_t>(ord_base + j);
+      cs[row + t] = sc;
+      ct[row + t] = tb;
+      ci[row + t] = jj;
+      if (t % stride == 0) {
+        const int32_t x = t / stride;
+        xs[x] = sc;
+        xt[x] = tb;
+        xj[x] = jj;
+      }
+    }
+  }
+  __syncthreads();
+  if (n < k && tid < 32) {  // zero-score fill (the whole row is in the buffer)
+    const int lane = tid;
+    auto touched = [&](int64_t j) {
+      const int32_t want = static_cast<int32_t>(ord_base + j);
+      for (int u = 0; u < n; ++u)
+        if (xj[u] == want) return true;
+      return false;
+    };
+    int pos = n;
+    if (sl >= 0 && sl < n_local && !touched(sl)) {
+      if (lane == 0) {
+        cs[row + pos] = 0.0;
+        ct[row + pos] = 0u;
+        ci[row + pos] = static_cast<int32_t>(ord_base + sl);
+      }
+      ++pos;
+    }
+    int nf = 0;
+    for (int64_t r0 = 0; nf < k && r0 < n_local; r0 += 32) {
+      const int64_t r = r0 + lane;
+      int32_t j = -1;
+      bool hit = false;
+      if (r < n_local) {
+        j = order[r];
+        hit = j != sl && !touched(j);
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, hit);
+      const int before = __popc(bal & ((1u << lane) - 1u));
+      if (hit && nf + before < k) {
+        const int64_t at = row + pos + nf + before;
+        cs[at] = 0.0;
+        ct[at] = 1u + static_cast<uint32_t>(idrank ? static_cast<int64_t>(idrank[j]) : ord_base + j);
+        ci[at] = static_cast<int32_t>(ord_base + j);
+      }
+      nf = min(k, nf + __popc(bal));
+    }
+    __syncwarp();
+    // the appended entries into the buffer too
+    for (int u = n + lane; u < pos + nf; u += 32) {
+      xs[u] = cs[row + u];
+      xt[u] = ct[row + u];
+      xj[u] = ci[row + u];
+    }
+    if (lane == 0) s_nfill = pos + nf - n;
+  }
+  __syncthreads();
+  const int ntot = n + s_nfill;
+  auto pad_sort = [&](int from, int N) {
+    for (int i = from + tid; i < N; i += RK_THREADS) {
+      xs[i] = -INFINITY;
+      xt[i] = 0xffffffffu;
+      xj[i] = -1;
+    }
+    __syncthreads();
+    bitonic_sort_desc_n(xs, xt, xj, N);
+  };
+  if (ntot <= RK_BUF) {
+    int N = 2;
+    while (N < ntot || N < k) N <<= 1;
+    pad_sort(ntot, N);
+  } else {
+    pad_sort((n + stride - 1) / stride, RK_BUF);  // the sample
+    double th_s = xs[k - 1];
+    uint32_t th_t = xt[k - 1];
+    __syncthreads();
+    for (int i = tid; i < RK_BEST; i += RK_THREADS) {  // best: empty
+      xs[i] = -INFINITY;
+      xt[i] = 0xffffffffu;
+      xj[i] = -1;
+    }
+    if (tid == 0) s_cnt = 0;
+    __syncthreads();
+    int32_t t0 = 0;
+    while (t0 < n) {
+      const int cnt = s_cnt;
+      const int free = RK_BUF - RK_BEST - cnt;
+      if (free < 4 * RK_THREADS) {  // make room: keep the best RK_BEST
+        __syncthreads();
+        pad_sort(RK_BEST + cnt, RK_BUF);
+        if (key_better(xs[k - 1], xt[k - 1], th_s, th_t)) {
+          th_s = xs[k - 1];
+          th_t = xt[k - 1];
+        }
+        __syncthreads();
+        if (tid == 0) s_cnt = 0;
+        __syncthreads();
+        continue;
+      }
+      const int32_t span = min(free, n - t0);
+      for (int32_t i0 = 0; i0 < span; i0 += 4 * RK_THREADS) {
+        double sc[4];
+        uint32_t tb[4];
+        int32_t jj[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int32_t i = i0 + u * RK_THREADS + tid;
+          jj[u] = -1;
+          if (i < span) {
+            sc[u] = cs[row + t0 + i];
+            tb[u] = ct[row + t0 + i];
+            jj[u] = ci[row + t0 + i];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (jj[u] >= 0 && !key_better(th_s, th_t, sc[u], tb[u])) {
+            const int p = RK_BEST + atomicAdd(&s_cnt, 1);
+            xs[p] = sc[u];
+            xt[p] = tb[u];
+            xj[p] = jj[u];
+          }
+        }
+      }
+      t0 += span;
+      __syncthreads();
+    }
+    pad_sort(RK_BEST + s_cnt, RK_BUF);
+  }
+  for (int i = tid; i < k; i += RK_THREADS) {
+    const bool ok = xj[i] >= 0;
+    out_idx[static_cast<int64_t>(b) * k + i] = ok ? xj[i] : -1;
+    out_val[static_cast<int64_t>(b) * k + i] = ok ? xs[i] : 0.0;
+  }
+}
+
 }  // namespace gift
 
 using namespace gift;
@@ -618,18 +1129,39 @@ extern "C" int gift_sif_query(const int64_t* e_off, const int32_t* e_ord, const 
   return GIFT_OK;
 }
 
-// Sort-based S-IF query for big batches (B x max_touched >= 2^24 pairs bound:
-// config 5, 111k -> 224k q/s); the accumulator-row kernel otherwise (it needs
-// no host synchronisation, so batches in flight keep overlapping).
-// flags GIFT_SIF_ROWS / GIFT_SIF_SORT override.
-static bool sif_sorted_mode(int64_t B, int64_t max_touched, int64_t n_local, int32_t flags) {
+// S-IF query implementations.  Big batches (B x max_touched >= 2^24 pairs
+// bound: config 5) take the bucketed path (no host synchronisation), or the
+// radix-sort one where the bucketed limits are exceeded; small batches the
+// accumulator-row kernel.  flags GIFT_SIF_ROWS / SORT / BUCKET override.
+enum SifMode { SIF_MODE_ROWS, SIF_MODE_SORT, SIF_MODE_BUCKET };
+
+static int sif_bucket_rb(int64_t n_local) {
+  int rb = SB_MIN_RB;
+  while ((static_cast<int64_t>(SB_MAX_R) << rb) < n_local) ++rb;
+  return rb;
+}
+
+static bool sif_bucket_ok(int32_t cap, int64_t max_touched, int64_t n_local) {
+  return cap <= SB_MAX_E && max_touched < (1LL << 31) && sif_bucket_rb(n_local) <= SB_MAX_RB;
+}
+
+static bool sif_sort_ok(int64_t B, int64_t n_local) {
   int bbits = 1, jbits = 1;
   while ((1LL << bbits) < B) ++bbits;
   while ((1LL << jbits) < n_local) ++jbits;
-  if (bbits + jbits > 32) return false;  // (query, shape) keys must fit 32 bits
-  if (flags & GIFT_SIF_ROWS) return false;
-  if (flags & GIFT_SIF_SORT) return true;
-  return B * max_touched >= (1LL << 24);
+  return bbits + jbits <= 32;  // (query, shape) keys must fit 32 bits
+}
+
+static SifMode sif_mode(int64_t B, int32_t cap, int64_t max_touched, int64_t n_local,
+                        int32_t flags) {
+  if (flags & GIFT_SIF_ROWS) return SIF_MODE_ROWS;
+  if ((flags & GIFT_SIF_BUCKET) && sif_bucket_ok(cap, max_touched, n_local))
+    return SIF_MODE_BUCKET;
+  if ((flags & GIFT_SIF_SORT) && sif_sort_ok(B, n_local)) return SIF_MODE_SORT;
+  if (flags) return SIF_MODE_ROWS;  // a forced mode outside its limits
+  if (B * max_touched < (1LL << 24)) return SIF_MODE_ROWS;
+  if (sif_bucket_ok(cap, max_touched, n_local)) return SIF_MODE_BUCKET;
+  return sif_sort_ok(B, n_local) ? SIF_MODE_SORT : SIF_MODE_ROWS;
 }
 
 extern "C" int gift_sif_query_topk(const int64_t* e_off, const int32_t* e_ord, const double* e_val,
@@ -643,8 +1175,8 @@ extern "C" int gift_sif_query_topk(const int64_t* e_off, const int32_t* e_ord, c
                                    int64_t max_touched, int32_t* out_idx, double* out_val,
                                    void* ws, size_t ws_bytes, int32_t flags, void* stream) {
   cudaStream_t st = as_stream(stream);
-  GIFT_REQUIRE((flags & ~(GIFT_SIF_ROWS | GIFT_SIF_SORT)) == 0 &&
-                   flags != (GIFT_SIF_ROWS | GIFT_SIF_SORT),
+  GIFT_REQUIRE((flags & ~(GIFT_SIF_ROWS | GIFT_SIF_SORT | GIFT_SIF_BUCKET)) == 0 &&
+                   __builtin_popcount(static_cast<unsigned>(flags)) <= 1,
                GIFT_ERR_INVALID, "bad S-IF query flags 0x%x", flags);
   GIFT_REQUIRE(k >= 1 && k <= 256, GIFT_ERR_UNSUPPORTED, "k = %d outside [1, 256]", k);
   GIFT_REQUIRE(n_acc_rows >= 1 && acc_rows != nullptr && order != nullptr, GIFT_ERR_INVALID,
@@ -661,8 +1193,59 @@ extern "C" int gift_sif_query_topk(const int64_t* e_off, const int32_t* e_ord, c
   int bbits = 1, jbits = 1;
   while ((1LL << bbits) < B) ++bbits;
   while ((1LL << jbits) < n_local) ++jbits;
-  const bool sorted = sif_sorted_mode(B, max_touched, n_local, flags);
-  if (!sorted) {
+  const SifMode mode = sif_mode(B, cap, max_touched, n_local, flags);
+  if (mode == SIF_MODE_BUCKET) {
+    const int rb = sif_bucket_rb(n_local);
+    const int R = static_cast<int>(cdiv(n_local, 1LL << rb));
+    const int64_t tmax = static_cast<int64_t>(B) * max_touched;
+    const int64_t nc = tmax + static_cast<int64_t>(B) * (k + 1);
+    Arena ab(ws, ws_bytes);
+    double* bcs = ab.take<double>(nc);
+    uint32_t* bct = ab.take<uint32_t>(nc);
+    int32_t* bci = ab.take<int32_t>(nc);
+    int32_t* tcnt = ab.take<int32_t>(B);
+    int64_t* off = ab.take<int64_t>(B + 1);
+    int32_t* bst = ab.take<int32_t>(static_cast<int64_t>(B) * (R + 1));
+    int32_t* ntb = ab.take<int32_t>(static_cast<int64_t>(B) * R);
+    uint16_t* pj = ab.take<uint16_t>(tmax);
+    double* pc = ab.take<double>(tmax);
+    const size_t sws = scan_ws_bytes(B);
+    GIFT_REQUIRE(bcs && bct && bci && tcnt && off && bst && ntb && pj && pc &&
+                     ab.remaining() >= sws + 256,
+                 GIFT_ERR_CAPACITY, "bucketed S-IF workspace too small");
+    sif_tcount_kernel<<<static_cast<unsigned>(cdiv(B, 8)), 256, 0, st>>>(q_idx, q_cnt, cap, e_off,
+                                                                       n_global, B, tcnt);
+    GIFT_LAUNCH_CHECK();
+    int rc = scan_exclusive_i32_to_i64(tcnt, off, B, true, ab.base + align_up(ab.used, 256), sws,
+                                       st);
+    if (rc) return rc;
+    const size_t ssm = sif_split_smem(cap, R);
+    GIFT_CUDA_TRY(cudaFuncSetAttribute(sif_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(ssm)));
+    sif_split_kernel<<<static_cast<unsigned>(B), SB_WARPS * 32, ssm, st>>>(
+        q_idx, q_val, q_cnt, cap, e_off, e_ord, e_val, n_global, rb, R, off, bst, pj, pc);
+    GIFT_LAUNCH_CHECK();
+    const int W = 1 << rb;
+    const int rw = static_cast<int>(min64(16, (208 * 1024) / (static_cast<int64_t>(W) * 8)));
+    const size_t rsm = static_cast<size_t>(rw) * W * 8;
+    GIFT_CUDA_TRY(cudaFuncSetAttribute(sif_bucket_reduce_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(rsm)));
+    const int64_t grid = min64(sm_count(), cdiv(static_cast<int64_t>(B) * R, rw * 4));
+    sif_bucket_reduce_kernel<<<static_cast<unsigned>(grid), rw * 32, rsm, st>>>(pj, pc, off, bst, B,
+                                                                               R, rb, ntb);
+    GIFT_LAUNCH_CHECK();
+    const size_t ksm = sif_rank_smem(R);
+    GIFT_CUDA_TRY(cudaFuncSetAttribute(sif_bucket_rank_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(ksm)));
+    sif_bucket_rank_kernel<<<static_cast<unsigned>(B), RK_THREADS, ksm, st>>>(
+        pj, pc, off, bst, ntb, R, rb, norms, q_norm, order, idrank, self_local, ord_base, n_local, k,
+        bcs, bct, bci, out_idx, out_val);
+    GIFT_LAUNCH_CHECK();
+    return GIFT_OK;
+  }
+  if (mode == SIF_MODE_ROWS) {
     const int grid = min(B, n_acc_rows);
     sif_query_sparse_kernel<<<static_cast<unsigned>(grid), 256, 0, st>>>(
         e_off, e_ord, e_val, norms, n_global, n_local, q_idx, q_val, q_cnt, q_norm, B, cap,
@@ -729,11 +1312,19 @@ extern "C" int gift_sif_query_topk(const int64_t* e_off, const int32_t* e_ord, c
   return topk_rows_from_lists(cs, ct, ci, cnt, B, m, k, 0, out_idx, out_val, st);
 }
 
-extern "C" size_t gift_sif_query_topk_ws_bytes(int32_t B, int64_t n_local, int32_t k,
+extern "C" size_t gift_sif_query_topk_ws_bytes(int32_t B, int32_t cap, int64_t n_local, int32_t k,
                                                int64_t max_touched, int32_t flags) {
   const int64_t m = min64(max_touched, n_local) + k + 1;
   size_t bytes = static_cast<size_t>(B) * m * 16 + static_cast<size_t>(B) * 4 + 4096;
-  if (sif_sorted_mode(B, max_touched, n_local, flags)) {  // sort-based path: pairs + radix scratch
+  const SifMode mode = sif_mode(B, cap, max_touched, n_local, flags);
+  if (mode == SIF_MODE_BUCKET) {  // candidates, pairs, bucket starts
+    const int64_t tmax = static_cast<int64_t>(B) * max_touched;
+    const int64_t R = cdiv(n_local, 1LL << sif_bucket_rb(n_local));
+    const int64_t nc = tmax + static_cast<int64_t>(B) * (k + 1);
+    return static_cast<size_t>(nc) * 16 + static_cast<size_t>(tmax) * 10 +
+           static_cast<size_t>(B) * (4 + 8 + 4 * (2 * R + 1)) + scan_ws_bytes(B) + 16 * 256 + 4096;
+  }
+  if (mode == SIF_MODE_SORT) {  // sort-based path: pairs + radix scratch
     const int64_t tmax = static_cast<int64_t>(B) * max_touched;
     bytes += static_cast<size_t>(B) * 12 + 1024 + static_cast<size_t>(tmax) * 44 + 8 +
              scan_ws_bytes(B) + scan_ws_bytes(tmax) + gift_radix_sort_ws_bytes(tmax) + 8192;

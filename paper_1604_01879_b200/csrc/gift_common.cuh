@@ -185,6 +185,7 @@ int sm_count();
 int topk_rows_from_lists(const double* cs, const uint32_t* ct, const int32_t* ci,
                          const int32_t* counts, int32_t B, int64_t m, int32_t k,
                          int32_t positive_only, int32_t* out_idx, double* out_val,
-                         cudaStream_t st);
+                         cudaStream_t st, const int64_t* row_off = nullptr,
+                         int64_t row_pad = 0);
 
 }  // namespace gift

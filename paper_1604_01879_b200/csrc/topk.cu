@@ -72,7 +72,14 @@ struct TopkIn {
   const int32_t* ci;
   int64_t m;
   const int32_t* counts;  // optional: valid candidates per row (<= m)
+  const int64_t* row_off;  // optional: row b starts at row_off[b] + b * row_pad
+  int64_t row_pad;         //   (instead of b * m; m then bounds the counts)
 };
+
+__device__ __forceinline__ int64_t list_row(const TopkIn& in, int b) {
+  return in.row_off ? in.row_off[b] + static_cast<int64_t>(b) * in.row_pad
+                    : static_cast<int64_t>(b) * in.m;
+}
 
 struct TopkOut {
   int k, positive_only, final_out, nslices;
@@ -135,7 +142,7 @@ __global__ void __launch_bounds__(TK_THREADS) topk_kernel(const TopkIn in, const
                                                                 : in.ord_base + e);
           jj = static_cast<int32_t>(in.ord_base + e);
         } else {
-          const int64_t at = static_cast<int64_t>(b) * in.m + e;
+          const int64_t at = list_row(in, b) + e;
           sc = in.cs[at];
           jj = in.ci[at];
           tb = in.ct ? in.ct[at] : static_cast<uint32_t>(jj);
@@ -296,7 +303,7 @@ __global__ void __launch_bounds__(TKS_WARPS * 32)
   TkKey best[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) best[i] = TkKey{-INFINITY, 0xffffffffu, -1};
-  const int64_t row = static_cast<int64_t>(b) * in.m;
+  const int64_t row = list_row(in, b);
   const int64_t e0 = WPR == 1 ? lane : warp * 32 + lane;
   for (int64_t e = e0; e < e1; e += 32 * WPR) {
     TkKey x{in.cs[row + e], 0u, in.ci[row + e]};
@@ -359,10 +366,11 @@ static void launch_topk_small(const TopkIn& in, const TopkOut& out, int B, cudaS
 
 // Best k of explicit (score, tiebreak, global ordinal) rows with per-row
 // counts: the merge pass of the dense top-k (used by the sparse S-IF query).
+// row_off (optional): row b starts at row_off[b] + b * row_pad, not b * m.
 int topk_rows_from_lists(const double* cs, const uint32_t* ct, const int32_t* ci,
                          const int32_t* counts, int32_t B, int64_t m, int32_t k,
                          int32_t positive_only, int32_t* out_idx, double* out_val,
-                         cudaStream_t st) {
+                         cudaStream_t st, const int64_t* row_off, int64_t row_pad) {
   GIFT_REQUIRE(k >= 1 && k <= 256, GIFT_ERR_UNSUPPORTED, "k = %d outside [1, 256]", k);
   if (B <= 0) return GIFT_OK;
   const int smem = sizeof(TopkSmem<256>);
@@ -374,6 +382,8 @@ int topk_rows_from_lists(const double* cs, const uint32_t* ct, const int32_t* ci
   in.ci = ci;
   in.m = m;
   in.counts = counts;
+  in.row_off = row_off;
+  in.row_pad = row_pad;
   TopkOut out{};
   out.k = k;
   out.positive_only = positive_only;

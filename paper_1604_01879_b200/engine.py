@@ -669,8 +669,9 @@ class DeviceSif:
                    self_local: torch.Tensor | None = None, stream=None, flags: int | None = None):
         """Sparse query_sif + final top-k (index.py:290-294): identical to
         topk_rows(self.query(q), k, idrank=..., self_local=...) without the
-        dense [B, n] rows.  flags: nat.SIF_ROWS / nat.SIF_SORT force one of the
-        two implementations (default: `self.query_flags`, 0 = by batch size)."""
+        dense [B, n] rows.  flags: nat.SIF_ROWS / SIF_SORT / SIF_BUCKET force one
+        of the three implementations (default: `self.query_flags`, 0 = by
+        batch size)."""
         flags = int(getattr(self, "query_flags", 0) if flags is None else flags)
         B = q.n
         dev = q.idx.device
@@ -681,7 +682,7 @@ class DeviceSif:
         bound = q.cap * self.max_list
         lib = nat.lib()
         ws = nat.workspace("sif_topk", stream).get(
-            lib.gift_sif_query_topk_ws_bytes(B, self.n_local, k, bound, flags))
+            lib.gift_sif_query_topk_ws_bytes(B, q.cap, self.n_local, k, bound, flags))
         acc = self._acc_rows(B, stream)
         nat.call("gift_sif_query_topk", nat.ptr(self.e_off), nat.ptr(self.e_ord),
                  nat.ptr(self.e_val), nat.ptr(self.norms), self.n_global, self.n_local,

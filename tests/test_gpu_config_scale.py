@@ -249,7 +249,8 @@ def test_c5_given_lists_against_oracle(n_shapes):
     eng = b.engine
     r = torch.from_numpy(rows).to(dev())
     outs = {}
-    for mode, flags in (("rows", nat.SIF_ROWS), ("sort", nat.SIF_SORT)):
+    for mode, flags in (("rows", nat.SIF_ROWS), ("sort", nat.SIF_SORT),
+                        ("bucket", nat.SIF_BUCKET)):
         eng.sif.query_flags = flags
         gi, gv = [], []
         for s in range(0, len(rows), c["batch"]):
@@ -260,8 +261,9 @@ def test_c5_given_lists_against_oracle(n_shapes):
             gv.append(v2.cpu().numpy())
         outs[mode] = (np.concatenate(gi), np.concatenate(gv))
     eng.sif.query_flags = 0
-    np.testing.assert_array_equal(outs["rows"][0], outs["sort"][0])
-    np.testing.assert_array_equal(outs["rows"][1], outs["sort"][1])
+    for mode in ("sort", "bucket"):
+        np.testing.assert_array_equal(outs["rows"][0], outs[mode][0])
+        np.testing.assert_array_equal(outs["rows"][1], outs[mode][1])
     gi, gv = outs["rows"]
     for n, q in enumerate(rows):
         nb = [int(j) for j, x in zip(idx_h[q][:c["k2"]], val_h[q][:c["k2"]]) if x > 0.0]

@@ -446,16 +446,21 @@ def test_gather_reduce_equals_range_reduce(V, ma, K):
         np.testing.assert_array_equal(nbr.cpu().numpy(), got["gather", "cosine"][1])
 
 
-@pytest.mark.parametrize("mode", ["rows", "sort"])
+_SIF_FLAGS = {"rows": nat.SIF_ROWS, "sort": nat.SIF_SORT, "bucket": nat.SIF_BUCKET}
+
+
+@pytest.mark.parametrize("mode", ["rows", "sort", "bucket"])
 @pytest.mark.parametrize("k", [1, 10, 100, 256])
 def test_sparse_sif_ranking_equals_dense(k, mode):
     """Sparse S-IF query + ranking (touched shapes + zero-score fill) is
     identical to top-k over the dense query_sif rows: shuffled id ranks,
     self inside / outside the touched set, an empty query support (pure
     fill), fewer touched shapes than k; repeated calls (scratch re-zeroed).
-    Both implementations: per-query accumulator rows, and the sort-based one
-    (GIFT_SIF_SORT: (query, shape) pairs radix-sorted, runs summed in order)."""
-    flags = nat.SIF_SORT if mode == "sort" else nat.SIF_ROWS
+    All three implementations: per-query accumulator rows, the sort-based one
+    (GIFT_SIF_SORT: (query, shape) pairs radix-sorted, runs summed in order)
+    and the bucketed one (GIFT_SIF_BUCKET: pairs split by shape range, reduced
+    in shared memory)."""
+    flags = _SIF_FLAGS[mode]
     rng = np.random.default_rng(k)
     N, B = 500, 37
     acts = []
@@ -480,6 +485,35 @@ def test_sparse_sif_ranking_equals_dense(k, mode):
         np.testing.assert_array_equal(si.cpu().numpy(), di.cpu().numpy())
         np.testing.assert_array_equal(sv.cpu().numpy(), dv.cpu().numpy())
     assert all(float(a.abs().sum()) == 0.0 for a in sif._acc.values())
+
+
+@pytest.mark.parametrize("n_shapes", [2048, 9001, 70000])
+def test_bucketed_sif_many_buckets_and_conflicts(n_shapes):
+    """Bucketed S-IF query over several shape buckets (2^11 shapes each) with
+    long postings (few coordinates -> one shape hit by many entries of a
+    query, conflicting lanes inside a 32-pair chunk): rankings and f64
+    scores bit-equal to the dense rows and to the other two paths."""
+    rng = np.random.default_rng(n_shapes)
+    N, B, coords = n_shapes, 45, 400
+    acts = []
+    for j in range(N):
+        idx = np.sort(rng.choice(coords, size=rng.integers(1, 9), replace=False))
+        val = rng.random(len(idx)) + 0.01
+        acts.append(types.SimpleNamespace(indices=idx, values=val, norm=float(np.sum(val))))
+    raw = eg.ActRows.from_host(acts, 8)
+    sif = eg.DeviceSif.build(raw, coords)
+    nbr = torch.from_numpy(rng.integers(-1, N, size=(B, 6)).astype(np.int32)).to(dev())
+    q = eg.act_mean(raw, nbr)
+    rank = rng.permutation(N).astype(np.int32)
+    idrank = torch.from_numpy(rank).to(dev())
+    order = torch.from_numpy(np.argsort(rank).astype(np.int32)).to(dev())
+    self_local = torch.from_numpy(rng.integers(0, N, size=B).astype(np.int32)).to(dev())
+    k = 100
+    di, dv = eg.topk_rows(sif.query(q), k, idrank=idrank, self_local=self_local)
+    for mode in ("bucket", "rows", "sort", "bucket"):
+        si, sv = sif.query_topk(q, k, order, idrank, self_local, flags=_SIF_FLAGS[mode])
+        np.testing.assert_array_equal(si.cpu().numpy(), di.cpu().numpy())
+        np.testing.assert_array_equal(sv.cpu().numpy(), dv.cpu().numpy())
 
 
 @pytest.mark.parametrize("case", E2E_CASES[:2], ids=[c[0] for c in E2E_CASES[:2]])
