@@ -543,7 +543,7 @@ __global__ void sif_fill_kernel(const uint32_t* __restrict__ keys, const int64_t
 // 32-pair chunk that hit the same shape (two entries) take turns in lane
 // order, so every sum is the reference's left-to-right acc[j] += ... order
 // (rerank.py:219-230), bit-equal to the other two paths.
-constexpr int SB_WARPS = 8;
+constexpr int SB_WARPS = 16;
 constexpr int SB_MAX_R = 2048;  // buckets per query (split kernel counters)
 constexpr int SB_MAX_E = 1024;  // query support entries staged in shared memory
 constexpr int SB_MIN_RB = 11;   // 2^11 shapes (16 KB of f64) per reducing warp
@@ -580,143 +580,159 @@ __device__ int32_t block_scan_excl(int32_t* a, int n, int32_t* wsum) {
   return total;
 }
 
-__device__ __forceinline__ int entry_of(const int32_t* pre, int ne, int32_t t) {
-  int lo = 0, hi = ne;  // last e with pre[e] <= t
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (pre[mid] <= t) lo = mid; else hi = mid - 1;
-  }
-  return lo;
-}
-
-__host__ __device__ constexpr size_t sif_pre_bytes(int cap) {
-  return (sizeof(int32_t) * (cap + 1) + 15) / 16 * 16;
-}
+__host__ __device__ constexpr size_t sb_align16(size_t x) { return (x + 15) / 16 * 16; }
 
 size_t sif_split_smem(int cap, int R) {
-  return static_cast<size_t>(cap) * 16 + sif_pre_bytes(cap) +
+  return static_cast<size_t>(cap) * 16 + sb_align16(sizeof(int32_t) * (cap + 1)) * 2 +
          sizeof(int32_t) * static_cast<size_t>(SB_WARPS + 1) * R;
 }
 
-// One CTA per query b: pairs of the query support, flattened in entry order
-// (t = pre[e] + posting), warp w owning t in [w per, (w + 1) per).
+// The entry holding chunk c: the last e >= e0 with cpre[e] <= c (warp-uniform;
+// chunks of empty entries are skipped because their cpre equals the next one's).
+__device__ __forceinline__ int chunk_entry(const int32_t* cpre, int ne, int e0, int32_t c,
+                                           int lane) {
+  for (;;) {
+    const int e = e0 + lane;
+    const unsigned m = __ballot_sync(0xffffffffu, e < ne && cpre[e] <= c);
+    if (m != 0xffffffffu || e0 + 32 >= ne) return e0 + 31 - __clz(m);
+    e0 += 32;
+  }
+}
+
+// Persistent, one query per CTA at a time (queries b = blockIdx.x, + gridDim.x,
+// ...: the output regions being filled stay few enough for L2 to merge their
+// scattered writes).  The query's postings, entry by entry, form chunks of 32
+// (entry-aligned); warp w owns a contiguous range of chunks.  Pass 1 counts
+// pairs per (warp, bucket); the bucket starts plus the earlier warps' counts
+// give every warp its own cursor per bucket; pass 2 scatters through them.  A
+// chunk holds postings of one entry -- distinct shapes -- so the slot order
+// inside a chunk is immaterial (an atomic ticket), while chunks, i.e.
+// entries, stay in order (one warp's tickets in program order, a __syncwarp
+// between chunks; warps in order of their ranges): every bucket lists each
+// shape's contributions in entry order.
 __global__ void __launch_bounds__(SB_WARPS * 32)
     sif_split_kernel(const int32_t* __restrict__ q_idx, const double* __restrict__ q_val,
-                     const int32_t* __restrict__ q_cnt, int cap, const int64_t* __restrict__ e_off,
-                     const int32_t* __restrict__ e_ord, const double* __restrict__ e_val,
-                     int64_t n_global, int rb, int R, const int64_t* __restrict__ off,
-                     int32_t* __restrict__ bstart, uint16_t* __restrict__ pj,
-                     double* __restrict__ pc) {
+                     const int32_t* __restrict__ q_cnt, int cap, int B,
+                     const int64_t* __restrict__ e_off, const int32_t* __restrict__ e_ord,
+                     const double* __restrict__ e_val, int64_t n_global, int rb, int R,
+                     const int64_t* __restrict__ off, int32_t* __restrict__ bstart,
+                     uint16_t* __restrict__ pj, double* __restrict__ pc) {
   extern __shared__ __align__(16) char sb_smem[];
-  int64_t* s_p0 = reinterpret_cast<int64_t*>(sb_smem);
-  double* s_v = reinterpret_cast<double*>(sb_smem + static_cast<size_t>(cap) * 8);
-  int32_t* s_pre = reinterpret_cast<int32_t*>(sb_smem + static_cast<size_t>(cap) * 16);
-  int32_t* s_cnt =
-      reinterpret_cast<int32_t*>(sb_smem + static_cast<size_t>(cap) * 16 + sif_pre_bytes(cap));
-  int32_t* s_tot = s_cnt + SB_WARPS * R;
+  char* sp = sb_smem;
+  int64_t* s_p0 = reinterpret_cast<int64_t*>(sp);
+  sp += static_cast<size_t>(cap) * 8;
+  double* s_v = reinterpret_cast<double*>(sp);
+  sp += static_cast<size_t>(cap) * 8;
+  int32_t* s_len = reinterpret_cast<int32_t*>(sp);
+  sp += sb_align16(sizeof(int32_t) * (cap + 1));
+  int32_t* s_cpre = reinterpret_cast<int32_t*>(sp);
+  sp += sb_align16(sizeof(int32_t) * (cap + 1));
+  int32_t* s_cnt = reinterpret_cast<int32_t*>(sp);  // [SB_WARPS][R]
+  int32_t* s_tot = s_cnt + SB_WARPS * R;            // [R]
   __shared__ int32_t s_wsum[SB_WARPS];
-  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const unsigned lt = (1u << lane) - 1u;
-  const int ne = min(q_cnt[b], cap);
-  for (int e = tid; e < ne; e += blockDim.x) {
-    const int64_t i = q_idx[static_cast<int64_t>(b) * cap + e];
-    const bool ok = i >= 0 && i < n_global;
-    const int64_t a = ok ? e_off[i] : 0;
-    s_p0[e] = a;
-    s_v[e] = q_val[static_cast<int64_t>(b) * cap + e];
-    s_pre[e] = ok ? static_cast<int32_t>(e_off[i + 1] - a) : 0;
-  }
-  for (int x = tid; x < SB_WARPS * R; x += blockDim.x) s_cnt[x] = 0;
-  __syncthreads();
-  const int32_t Tb = block_scan_excl(s_pre, ne, s_wsum);
-  if (tid == 0) s_pre[ne] = Tb;
-  __syncthreads();
-  const int32_t per = (Tb + SB_WARPS - 1) / SB_WARPS;
-  const int32_t t0w = min(Tb, warp * per), t1w = min(Tb, t0w + per);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t mask = (1u << rb) - 1u;
   int32_t* my = s_cnt + warp * R;
-  // pass 1: per-(warp, bucket) counts; SB_U chunks' loads in flight per lane,
-  // one counter update per run of equal buckets in a chunk (leader lane; the
-  // counters are warp-private, leaders of one chunk hold distinct buckets)
-  {
-    int e = entry_of(s_pre, ne, t0w + lane);
-    for (int32_t c0 = t0w; c0 < t1w; c0 += 32 * SB_U) {
-      int32_t jj[SB_U];
+  for (int b = blockIdx.x; b < B; b += gridDim.x) {
+    const int ne = min(q_cnt[b], cap);
+    for (int e = tid; e < ne; e += blockDim.x) {
+      const int64_t i = q_idx[static_cast<int64_t>(b) * cap + e];
+      const bool ok = i >= 0 && i < n_global;
+      const int64_t a = ok ? e_off[i] : 0;
+      const int32_t len = ok ? static_cast<int32_t>(e_off[i + 1] - a) : 0;
+      s_p0[e] = a;
+      s_v[e] = q_val[static_cast<int64_t>(b) * cap + e];
+      s_len[e] = len;
+      s_cpre[e] = (len + 31) >> 5;
+    }
+    for (int x = tid; x < SB_WARPS * R; x += blockDim.x) s_cnt[x] = 0;
+    __syncthreads();
+    const int32_t NC = block_scan_excl(s_cpre, ne, s_wsum);
+    if (tid == 0) s_cpre[ne] = NC;
+    __syncthreads();
+    const int32_t per = (NC + SB_WARPS - 1) / SB_WARPS;
+    const int32_t cw0 = min(NC, warp * per), cw1 = min(NC, cw0 + per);
+    int e_first = 0;
+    {  // last e with cpre[e] <= cw0 (same in every lane)
+      int lo = 0, hi = max(ne - 1, 0);
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_cpre[mid] <= cw0) lo = mid; else hi = mid - 1;
+      }
+      e_first = lo;
+    }
+    // SB_U chunks' loads in flight (j = -1: no pair)
+    auto load = [&](int32_t c0, int& e, int32_t (&jj)[SB_U], double (&cc)[SB_U],
+                    double (&vq)[SB_U], bool vals) {
 #pragma unroll
       for (int u = 0; u < SB_U; ++u) {
-        const int32_t t = c0 + u * 32 + lane;
+        const int32_t c = c0 + u;
         jj[u] = -1;
-        if (t < t1w) {
-          while (s_pre[e + 1] <= t) ++e;
-          jj[u] = e_ord[s_p0[e] + (t - s_pre[e])];
+        if (c < cw1) {
+          e = chunk_entry(s_cpre, ne, e, c, lane);
+          const int32_t o = (c - s_cpre[e]) * 32 + lane;
+          if (o < s_len[e]) {
+            const int64_t p = s_p0[e] + o;
+            jj[u] = e_ord[p];
+            if (vals) {
+              cc[u] = e_val[p];
+              vq[u] = s_v[e];
+            }
+          }
         }
       }
+    };
+    {  // pass 1: per-(warp, bucket) counts
+      int e = e_first;
+      for (int32_t c0 = cw0; c0 < cw1; c0 += SB_U) {
+        int32_t jj[SB_U];
+        double cc[SB_U], vq[SB_U];
+        load(c0, e, jj, cc, vq, false);
 #pragma unroll
-      for (int u = 0; u < SB_U; ++u) {
-        const uint32_t key = jj[u] >= 0 ? static_cast<uint32_t>(jj[u]) >> rb : 0x80000000u | lane;
-        const unsigned peers = __match_any_sync(0xffffffffu, key);
-        if (jj[u] >= 0 && __ffs(peers) - 1 == lane) my[key] += __popc(peers);
-        __syncwarp();
+        for (int u = 0; u < SB_U; ++u)
+          if (jj[u] >= 0) atomicAdd(&my[static_cast<uint32_t>(jj[u]) >> rb], 1);
       }
     }
-  }
-  __syncthreads();
-  for (int r = tid; r < R; r += blockDim.x) {  // bucket totals; warp prefix within a bucket
-    int32_t run = 0;
-    for (int w = 0; w < SB_WARPS; ++w) {
-      const int32_t c = s_cnt[w * R + r];
-      s_cnt[w * R + r] = run;
-      run += c;
+    __syncthreads();
+    int32_t* bs = bstart + static_cast<int64_t>(b) * (R + 1);
+    for (int r = tid; r < R; r += blockDim.x) {  // per-warp offsets within a bucket
+      int32_t run = 0;
+      for (int w = 0; w < SB_WARPS; ++w) {
+        const int32_t c = s_cnt[w * R + r];
+        s_cnt[w * R + r] = run;
+        run += c;
+      }
+      s_tot[r] = run;
     }
-    s_tot[r] = run;
-  }
-  __syncthreads();
-  block_scan_excl(s_tot, R, s_wsum);
-  int32_t* bs = bstart + static_cast<int64_t>(b) * (R + 1);
-  for (int r = tid; r < R; r += blockDim.x) {
-    bs[r] = s_tot[r];
-    for (int w = 0; w < SB_WARPS; ++w) s_cnt[w * R + r] += s_tot[r];
-  }
-  if (tid == 0) bs[R] = Tb;
-  __syncthreads();
-  // pass 2: warp-ordered stable scatter (a lane's slot = its warp's bucket
-  // cursor + the lanes before it in the chunk with the same bucket)
-  const int64_t base = off[b];
-  const uint32_t mask = (1u << rb) - 1u;
-  int e = entry_of(s_pre, ne, t0w + lane);
-  for (int32_t c0 = t0w; c0 < t1w; c0 += 32 * SB_U) {
-    int32_t jj[SB_U];
-    double cc[SB_U], vq[SB_U];
+    __syncthreads();
+    const int32_t tb = block_scan_excl(s_tot, R, s_wsum);  // bucket starts in the query's region
+    for (int r = tid; r < R; r += blockDim.x) {
+      const int32_t st = s_tot[r];
+      bs[r] = st;
+      for (int w = 0; w < SB_WARPS; ++w) s_cnt[w * R + r] += st;
+    }
+    if (tid == 0) bs[R] = tb;
+    __syncthreads();
+    {  // pass 2: the scatter
+      const int64_t base = off[b];
+      int e = e_first;
+      for (int32_t c0 = cw0; c0 < cw1; c0 += SB_U) {
+        int32_t jj[SB_U];
+        double cc[SB_U], vq[SB_U];
+        load(c0, e, jj, cc, vq, true);
 #pragma unroll
-    for (int u = 0; u < SB_U; ++u) {  // loads only: the uses below wait for them
-      const int32_t t = c0 + u * 32 + lane;
-      jj[u] = -1;
-      cc[u] = vq[u] = 0.0;
-      if (t < t1w) {
-        while (s_pre[e + 1] <= t) ++e;
-        const int64_t p = s_p0[e] + (t - s_pre[e]);
-        jj[u] = e_ord[p];
-        cc[u] = e_val[p];
-        vq[u] = s_v[e];
+        for (int u = 0; u < SB_U; ++u) {
+          if (jj[u] >= 0) {
+            const uint32_t j = static_cast<uint32_t>(jj[u]);
+            const int32_t pos = atomicAdd(&my[j >> rb], 1);
+            pj[base + pos] = static_cast<uint16_t>(j & mask);
+            pc[base + pos] = fmin(vq[u], cc[u]);
+          }
+          __syncwarp();
+        }
       }
     }
-#pragma unroll
-    for (int u = 0; u < SB_U; ++u) {
-      const bool valid = jj[u] >= 0;
-      const uint32_t j = static_cast<uint32_t>(jj[u]);
-      const uint32_t key = valid ? j >> rb : 0x80000000u | lane;
-      const unsigned peers = __match_any_sync(0xffffffffu, key);
-      const int leader = __ffs(peers) - 1;
-      int32_t pos = 0;
-      if (valid && lane == leader) {
-        pos = my[key];
-        my[key] = pos + __popc(peers);
-      }
-      pos = __shfl_sync(0xffffffffu, pos, leader) + __popc(peers & lt);
-      if (valid) {
-        pj[base + pos] = static_cast<uint16_t>(j & mask);
-        pc[base + pos] = fmin(vq[u], cc[u]);
-      }
-    }
+    __syncthreads();
   }
 }
 
@@ -1142,7 +1158,10 @@ static int sif_bucket_rb(int64_t n_local) {
 }
 
 static bool sif_bucket_ok(int32_t cap, int64_t max_touched, int64_t n_local) {
-  return cap <= SB_MAX_E && max_touched < (1LL << 31) && sif_bucket_rb(n_local) <= SB_MAX_RB;
+  if (cap > SB_MAX_E || max_touched >= (1LL << 31)) return false;
+  const int rb = sif_bucket_rb(n_local);
+  return rb <= SB_MAX_RB &&
+         sif_split_smem(cap, static_cast<int>(cdiv(n_local, 1LL << rb))) <= 200 * 1024;
 }
 
 static bool sif_sort_ok(int64_t B, int64_t n_local) {
@@ -1222,8 +1241,8 @@ extern "C" int gift_sif_query_topk(const int64_t* e_off, const int32_t* e_ord, c
     const size_t ssm = sif_split_smem(cap, R);
     GIFT_CUDA_TRY(cudaFuncSetAttribute(sif_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(ssm)));
-    sif_split_kernel<<<static_cast<unsigned>(B), SB_WARPS * 32, ssm, st>>>(
-        q_idx, q_val, q_cnt, cap, e_off, e_ord, e_val, n_global, rb, R, off, bst, pj, pc);
+    sif_split_kernel<<<static_cast<unsigned>(min64(B, sm_count())), SB_WARPS * 32, ssm, st>>>(
+        q_idx, q_val, q_cnt, cap, B, e_off, e_ord, e_val, n_global, rb, R, off, bst, pj, pc);
     GIFT_LAUNCH_CHECK();
     const int W = 1 << rb;
     const int rw = static_cast<int>(min64(16, (208 * 1024) / (static_cast<int64_t>(W) * 8)));
