@@ -1033,6 +1033,7 @@ using namespace gift;
 #ifdef GIFT_SCAN_EXPERIMENT
 namespace gift {
 extern int g_scan_experiment;
+extern unsigned long long* g_scan_trace;
 }
 #endif
 
@@ -1286,6 +1287,7 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
     ta.dyn = (f->flags & GIFT_FIF_SCHED_STATIC) ? 0 : 1;
 #ifdef GIFT_SCAN_EXPERIMENT
     ta.exp = g_scan_experiment;
+    ta.trace = g_scan_trace;
 #endif
     {  // the truncation compensation of this launch's chunking
       const int nkb = (d + 63) / 64;

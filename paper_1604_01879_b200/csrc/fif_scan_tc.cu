@@ -31,11 +31,6 @@
 
 namespace gift {
 
-#ifdef GIFT_SCAN_EXPERIMENT
-#define GIFT_EXP(p, bit) (((p).exp & (bit)) != 0)
-#else
-#define GIFT_EXP(p, bit) false
-#endif
 
 constexpr int TC_M = 128;
 constexpr int TC_NMAX = 128;  // probes per item: N = 64 or 128 (per item)
@@ -269,6 +264,7 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&iempty[slot]);
         if (I.c < 0) break;
+        if (lane == 0) GIFT_TRACE(p, it, 1, clock64());
         const int brows = PAIR ? I.n / 2 : I.n;            // probe rows per plane half
         const uint32_t a_bytes = has_lo ? 2 * A_TILE : A_TILE;
         // this CTA's B bytes: both planes (single), one whole plane (pair, cb),
@@ -332,6 +328,7 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
             phase ^= 1;
           }
         }
+        if (lane == 0) GIFT_TRACE(p, it, 2, clock64());
       }
     }
   } else if (warp == 1) {
@@ -350,6 +347,7 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&iempty[slot]);
         if (I.c < 0) break;
+        if (lane == 0) GIFT_TRACE(p, item_ctr, 3, clock64());
         const uint32_t idesc = tc::idesc_f16_f32(PAIR ? 2 * TC_M : TC_M, I.n);
         const uint32_t idesc2 = tc::idesc_f16_f32(PAIR ? 2 * TC_M : TC_M, 2 * I.n);  // [b1 | b2]
         const uint32_t ib = item_ctr & 1, iph = (item_ctr >> 1) & 1;
@@ -440,6 +438,7 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
         }
         if (!cb && tc::elect_one()) tc::mma_commit_2sm(&dfull[ib], 0x3);
         __syncwarp();
+        if (lane == 0) GIFT_TRACE(p, item_ctr, 4, clock64());
         ++item_ctr;
       }
     }
@@ -486,6 +485,11 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
         tc::mbar_wait(&iempty[slot], iph ^ 1);
         s_item[slot] = I;
         tc::mbar_arrive(&ifull[slot]);
+        GIFT_TRACE(p, it, 0, clock64());
+        if (item < n_items) {
+          GIFT_TRACE(p, it, 8, I.n);
+          GIFT_TRACE(p, it, 9, I.c);
+        }
         if (item >= n_items) break;
       }
     }
@@ -514,6 +518,7 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
       named_bar(bar_item, TC_M);  // every thread of the group has its copy
       if (e == 0) tc::mbar_arrive(&iempty[slot]);
       if (I.c < 0) break;
+      if (et == 0) GIFT_TRACE(p, item_ctr, 5, clock64());
       const int nseg = I.seg1 - I.seg0;
       const int hn = I.n / G;     // this group's columns: [c0, c0 + hn)
       const int c0 = eg * hn;
@@ -620,6 +625,7 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
           tc::mbar_arrive(&dempty[ib]);
         ++item_ctr;
       }
+      if (et == 0) GIFT_TRACE(p, item_ctr - 1, 6, clock64());
       if (p.tcomp_scale != 0.f) {  // add back the expected truncation loss
 #pragma unroll
         for (int n = 0; n < NA; ++n) acc[n] = fmaf(acc[n], p.tcomp_scale, acc[n]);
@@ -667,6 +673,7 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
           named_bar(bar_tail, TC_M);
         }
       }
+      if (et == 0) GIFT_TRACE(p, item_ctr - 1, 7, clock64());
     }
   }
   tc::tc_fence_before();
@@ -865,4 +872,10 @@ namespace gift {
 int g_scan_experiment = 0;
 }
 extern "C" void gift_scan_experiment(int bits) { gift::g_scan_experiment = bits; }
+namespace gift {
+unsigned long long* g_scan_trace = nullptr;
+}
+extern "C" void gift_scan_trace(void* buf) {
+  gift::g_scan_trace = static_cast<unsigned long long*>(buf);
+}
 #endif

@@ -37,6 +37,7 @@ struct TcArgs {
 #ifdef GIFT_SCAN_EXPERIMENT
   int exp;  // timing experiments only (tools/scan_experiment.py): 1 = no epilogue tail,
             // 2 = no TMEM drains, 4 = no MMAs, 8 = no loads; outputs invalid
+  unsigned long long* trace;  // per-role clock64 stamps of the first CTAs' items (or null)
 #endif
 };
 
@@ -51,6 +52,21 @@ struct TcArgs {
 // dot scale with their lengths, so each item's dots are scaled once by
 //   1 + TCOMP_PER_STEP * sum_c n_c^2 / sum_c n_c.
 constexpr double TCOMP_PER_STEP = 0.5 * 0x1p-23 / (4.0 * 0.6931471805599453);
+
+#ifdef GIFT_SCAN_EXPERIMENT
+#define GIFT_EXP(p, bit) (((p).exp & (bit)) != 0)
+// per-role clock64 stamps of the first CTAs' items (tools/scan_trace.py):
+// trace[((cta * TR_ITEMS) + item) * TR_F + field]
+constexpr int TR_CTAS = 8, TR_ITEMS = 512, TR_F = 10;
+#define GIFT_TRACE(p, it, f, v)                                                       \
+  do {                                                                                \
+    if ((p).trace != nullptr && blockIdx.x < TR_CTAS && (it) < TR_ITEMS)              \
+      (p).trace[((blockIdx.x * TR_ITEMS) + (it)) * TR_F + (f)] = (v);                 \
+  } while (0)
+#else
+#define GIFT_EXP(p, bit) false
+#define GIFT_TRACE(p, it, f, v) do {} while (0)
+#endif
 
 bool tc_supported(const gift_fif_view* f);
 // The scan on CTA pairs (cta_group::2, M = 256): a work item is two
