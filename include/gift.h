@@ -77,6 +77,9 @@ extern "C" {
                                         /* 4, the 1e-5 contract at d = 4096)   */
 #define GIFT_FIF_RAW_ACCUM (1 << 29)    /* no truncation compensation of the   */
                                         /* tensor-core accumulators (tests)    */
+#define GIFT_FIF_DENSE_OFF (1 << 30)    /* fp16 storage: no probe-major pair   */
+                                        /* scan of the cells with >= 192       */
+                                        /* probes (fif_scan_dense.cu)          */
 
 typedef struct gift_fif_view {
   int32_t K;                 /* codebook size                                 */

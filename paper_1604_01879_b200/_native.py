@@ -28,8 +28,9 @@ FIF_REDUCE = {"auto": 0, "range": 1 << 18, "gather": 2 << 18, "owner": 3 << 18}
 FIF_SCHED_STATIC = 1 << 20
 FIF_PAIR = {"auto": 0, "off": 1 << 21, "on": 2 << 21}
 FIF_RAW_ACCUM = 1 << 29
+FIF_DENSE_OFF = 1 << 30
 FIF_VARIANT_MASK = ((1 << 16) | (1 << 17) | (3 << 18) | (1 << 20) | (3 << 21) | (31 << 24)
-                    | FIF_RAW_ACCUM)
+                    | FIF_RAW_ACCUM | FIF_DENSE_OFF)
 QUANT_SIMT = 1        # gift_quantize_ex flags
 SIF_ROWS, SIF_SORT, SIF_BUCKET = 1, 2, 4  # gift_sif_query_topk flags
 

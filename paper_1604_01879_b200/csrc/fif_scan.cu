@@ -42,45 +42,80 @@ __global__ void __launch_bounds__(PLAN_THREADS)
                       const int64_t* __restrict__ tile_off, int32_t* __restrict__ probe_off,
                       int64_t* __restrict__ outbase, int64_t* __restrict__ item_off,
                       int32_t* __restrict__ cursor, int64_t* __restrict__ meta, int64_t capacity,
-                      int ptile, int tile_div) {
+                      int ptile, int tile_div, int dense_min, int64_t* __restrict__ item_off2) {
   __shared__ int64_t sbuf[32];
   const int per = (K + PLAN_THREADS - 1) / PLAN_THREADS;
   const int c0 = threadIdx.x * per;
-  int64_t s_cnt = 0, s_out = 0, s_items = 0;
+  // dense cells (>= dense_min probes, fp16-exact batch: meta[M_QLO] from
+  // query_lo_kernel) go to the probe-major scan's list (fif_scan_dense.cu):
+  // ceil(T / 2) posting tile pairs x ceil(n / 256) probe tiles
+  const bool split = dense_min > 0 && meta[M_QLO] == 0;
+  auto items = [&](int64_t n, int64_t T, int64_t& i1, int64_t& i2) {
+    const bool dn = split && n >= dense_min;
+    i1 = dn ? 0 : (T + tile_div - 1) / tile_div * ((n + ptile - 1) / ptile);
+    i2 = dn ? (T + 1) / 2 * ((n + 255) / 256) : 0;
+  };
+  int64_t s_cnt = 0, s_out = 0, s_items = 0, s_items2 = 0;
   for (int c = c0; c < min(c0 + per, K); ++c) {
     int64_t n = counts[c];
     int64_t S = seg_off[c + 1] - seg_off[c];
     int64_t T = tile_off[c + 1] - tile_off[c];
+    int64_t i1, i2;
+    items(n, T, i1, i2);
     s_cnt += n;
     s_out += n * S;
-    s_items += (T + tile_div - 1) / tile_div * ((n + ptile - 1) / ptile);
+    s_items += i1;
+    s_items2 += i2;
   }
-  int64_t tot_cnt, tot_out, tot_items;
+  int64_t tot_cnt, tot_out, tot_items, tot_items2;
   int64_t p_cnt = block_exclusive_scan<int64_t>(s_cnt, &tot_cnt, sbuf);
   int64_t p_out = block_exclusive_scan<int64_t>(s_out, &tot_out, sbuf);
   int64_t p_items = block_exclusive_scan<int64_t>(s_items, &tot_items, sbuf);
+  int64_t p_items2 = block_exclusive_scan<int64_t>(s_items2, &tot_items2, sbuf);
   for (int c = c0; c < min(c0 + per, K); ++c) {
     int64_t n = counts[c];
     int64_t S = seg_off[c + 1] - seg_off[c];
     int64_t T = tile_off[c + 1] - tile_off[c];
+    int64_t i1, i2;
+    items(n, T, i1, i2);
     probe_off[c] = static_cast<int32_t>(p_cnt);
     outbase[c] = p_out;
     item_off[c] = p_items;
+    if (item_off2) item_off2[c] = p_items2;
     cursor[c] = 0;
     p_cnt += n;
     p_out += n * S;
-    p_items += (T + tile_div - 1) / tile_div * ((n + ptile - 1) / ptile);
+    p_items += i1;
+    p_items2 += i2;
   }
   if (threadIdx.x == 0) {
     probe_off[K] = static_cast<int32_t>(tot_cnt);
     outbase[K] = tot_out;
     item_off[K] = tot_items;
+    if (item_off2) item_off2[K] = tot_items2;
     meta[M_ITEMS] = tot_items;
+    meta[M_ITEMS2] = tot_items2;
     meta[M_OUT_TOTAL] = tot_out;
     meta[M_OVERFLOW] = tot_out > capacity ? 1 : 0;
     meta[M_WORK] = 0;
-    meta[M_QLO] = 0;  // set by the probe gather when a query lo plane is non-zero
+    meta[M_WORK2] = 0;
+    // M_QLO: zeroed before the plan, set by query_lo_kernel / the probe gather
   }
+}
+
+// meta[M_QLO] = 1 when some query value is not exactly an fp16 (its lo plane
+// is non-zero): the plan's dense split needs it before the probe gather
+__global__ void query_lo_kernel(const float* __restrict__ Q, int64_t n4, int64_t* __restrict__ meta) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  bool lo = false;
+  for (; i < n4; i += stride) {
+    const float4 v = reinterpret_cast<const float4*>(Q)[i];
+    lo |= __half2float(__float2half_rn(v.x)) != v.x || __half2float(__float2half_rn(v.y)) != v.y ||
+          __half2float(__float2half_rn(v.z)) != v.z || __half2float(__float2half_rn(v.w)) != v.w;
+  }
+  if (__syncthreads_or(lo) && threadIdx.x == 0)
+    atomicOr(reinterpret_cast<unsigned long long*>(meta + M_QLO), 1ull);
 }
 
 __global__ void probe_scatter_kernel(const int32_t* __restrict__ cells, int64_t nprobes,
@@ -1048,6 +1083,7 @@ struct ScoreWs {
   int32_t* probe_off;
   int64_t* outbase;
   int64_t* item_off;
+  int64_t* item_off2;
   int32_t* probe_list;
   int32_t* probe_rank;
   void* qws;
@@ -1124,6 +1160,7 @@ bool carve(Arena& ar, const gift_fif_view* f, int64_t nviews, int V, int ma, Sco
   w.probe_off = ar.take<int32_t>(K + 1);
   w.outbase = ar.take<int64_t>(K + 1);
   w.item_off = ar.take<int64_t>(K + 1);
+  w.item_off2 = ar.take<int64_t>(K + 1);
   w.probe_list = ar.take<int32_t>(nprobes);
   w.probe_rank = ar.take<int32_t>(nprobes);
   w.qws_bytes = gift_quantize_ws_bytes(nviews, f->d, K, GIFT_F32);
@@ -1242,10 +1279,19 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
   probe_count_kernel<<<static_cast<unsigned>(cdiv(nprobes, 256)), 256, 0, st>>>(w.cells, nprobes,
                                                                                w.counts);
   GIFT_LAUNCH_CHECK();
+  GIFT_CUDA_TRY(cudaMemsetAsync(w.meta + M_QLO, 0, sizeof(int64_t), st));
+  const bool dense = use_tc(f) && tc_dense_enabled(f);
+  if (dense) {
+    const int64_t n4 = nviews * d / 4;  // d % 8 == 0 on the tensor-core path
+    query_lo_kernel<<<static_cast<unsigned>(min64(max64(cdiv(n4, 256), 1), sm_count() * 8)), 256, 0,
+                      st>>>(Q, n4, w.meta);
+    GIFT_LAUNCH_CHECK();
+  }
   probe_plan_kernel<<<1, PLAN_THREADS, 0, st>>>(w.counts, K, f->seg_off, f->tile_off, w.probe_off,
                                                 w.outbase, w.item_off, w.cursor, w.meta, w.capacity,
                                                 use_tc(f) ? 128 : simt::TB,
-                                                use_tc(f) && tc_pair_enabled(f) ? 2 : 1);
+                                                use_tc(f) && tc_pair_enabled(f) ? 2 : 1,
+                                                dense ? DENSE_MIN_PROBES : 0, w.item_off2);
   GIFT_LAUNCH_CHECK();
   probe_scatter_kernel<<<static_cast<unsigned>(cdiv(nprobes, 256)), 256, 0, st>>>(
       w.cells, nprobes, w.probe_off, w.cursor, w.probe_list, w.probe_rank);
@@ -1258,6 +1304,7 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
   if (use_tc(f)) {
     TcArgs ta;
     ta.item_off = w.item_off;
+    ta.item_off2 = w.item_off2;
     ta.counts = w.counts;
     ta.probe_off = w.probe_off;
     ta.probe_list = w.probe_list;

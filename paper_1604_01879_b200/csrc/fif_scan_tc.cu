@@ -592,9 +592,9 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
         }
         tc::tc_fence_before();
         if (PAIR)
-          tc::mbar_arrive_cluster(tc::mapa(&tempty[buf], 0));  // the leader's barrier
+          tc::mbar_arrive_cluster_relaxed(tc::mapa(&tempty[buf], 0));  // the leader's barrier
         else
-          tc::mbar_arrive(&tempty[buf]);
+          tc::mbar_arrive_relaxed(&tempty[buf]);
         ++chunk_ctr;
       }
       if (cb) {
@@ -620,9 +620,9 @@ __global__ void __launch_bounds__(Epi<G>::THREADS, 1)
         }
         tc::tc_fence_before();
         if (PAIR)
-          tc::mbar_arrive_cluster(ib ? rel_d1 : rel_d0);
+          tc::mbar_arrive_cluster_relaxed(ib ? rel_d1 : rel_d0);
         else
-          tc::mbar_arrive(&dempty[ib]);
+          tc::mbar_arrive_relaxed(&dempty[ib]);
         ++item_ctr;
       }
       if (et == 0) GIFT_TRACE(p, item_ctr - 1, 6, clock64());
@@ -770,8 +770,9 @@ bool tc_supported(const gift_fif_view* f) {
 }
 
 // CTA pairs by default with the f32 lo plane (configs 2/3: half the L2 -> smem
-// traffic per SM; config 3 scan 16.3 -> 15.1 ms, config 2 unchanged), single
-// CTAs for fp16 storage (config 4: the pair is ~7% slower there)
+// traffic per SM; config 3 scan 16.3 -> 15.1 ms, config 2 unchanged); fp16
+// storage: the dense cells on the probe-major pair kernel (fif_scan_dense.cu),
+// the others on single CTAs (the posting-major pair is ~7% slower there)
 // persistent scan CTAs: one per SM minus the view's GIFT_FIF_RESERVE_SMS
 // (left to the kernels of other batches in flight)
 static int scan_ctas(const gift_fif_view* f) {
@@ -784,6 +785,14 @@ bool tc_pair_enabled(const gift_fif_view* f) {
   if (m == GIFT_FIF_PAIR_OFF) return false;
   if (m == GIFT_FIF_PAIR_ON) return sm_count() >= 2;
   return f->feat_lo != nullptr && sm_count() >= 2;
+}
+
+// fp16 storage, default pairing, segments within tiles: the dense cells run
+// on the probe-major pair kernel, the rest on the single-CTA kernel
+bool tc_dense_enabled(const gift_fif_view* f) {
+  return f->feat_lo == nullptr && !(f->flags & GIFT_FIF_DENSE_OFF) &&
+         (f->flags & GIFT_FIF_TILED_SEGMENTS) &&
+         ((f->flags >> GIFT_FIF_PAIR_SHIFT) & 3) == GIFT_FIF_PAIR_AUTO && sm_count() >= 2;
 }
 
 template <int G, bool LO>
@@ -832,6 +841,12 @@ int launch_scan_tc(const gift_fif_view* f, const float* Q, int64_t nprobes_max, 
   if (rc) return rc;
   a.has_lo = f->feat_lo != nullptr ? 1 : 0;
   if (ev0) GIFT_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(ev0), st));
+  if (tc_dense_enabled(f)) {  // dense cells first (exits at once without dense items)
+    CUtensorMap mQ;
+    rc = make_map(&mQ, g1, max64(nprobes_max, 1), d, 128);
+    if (rc) return rc;
+    GIFT_CUDA_TRY(launch_scan_dense(scan_ctas(f), st, mQ, mA1, a, a.item_off2));
+  }
   if (pair && a.has_lo) {
     GIFT_CUDA_TRY((launch_pair<1, true>(scan_ctas(f), st, mA1, mA2, mB1, mB2, mB1h, mB2h, a)));
   } else if (pair) {  // fp16 storage: tensor-bound, two epilogue groups

@@ -1,6 +1,8 @@
 // Shared declarations of the two F-IF scan implementations (fif_scan.cu,
 // fif_scan_tc.cu).
 #pragma once
+#include <cuda.h>
+
 #include "gift_common.cuh"
 
 namespace gift {
@@ -8,10 +10,13 @@ namespace gift {
 // meta[M_QLO] != 0: some probe's query lo plane (b2) is non-zero.  Queries
 // whose values are exactly fp16 (config 4's fp16-rounded views) leave it 0 and
 // the single-CTA scan then skips the b2 operand (half the MMA work, bit-identical).
-enum Meta { M_ITEMS = 0, M_OUT_TOTAL = 1, M_OVERFLOW = 2, M_WORK = 3, M_QLO = 4 };
+// M_ITEMS2 / M_WORK2: the dense-cell scan's item list (fif_scan_dense.cu).
+enum Meta { M_ITEMS = 0, M_OUT_TOTAL = 1, M_OVERFLOW = 2, M_WORK = 3, M_QLO = 4, M_ITEMS2 = 5,
+            M_WORK2 = 6 };
 
 struct TcArgs {
   const int64_t* item_off;
+  const int64_t* item_off2;  // dense-cell items (fif_scan_dense.cu)
   const int32_t* counts;
   const int32_t* probe_off;
   const int32_t* probe_list;
@@ -57,7 +62,7 @@ constexpr double TCOMP_PER_STEP = 0.5 * 0x1p-23 / (4.0 * 0.6931471805599453);
 #define GIFT_EXP(p, bit) (((p).exp & (bit)) != 0)
 // per-role clock64 stamps of the first CTAs' items (tools/scan_trace.py):
 // trace[((cta * TR_ITEMS) + item) * TR_F + field]
-constexpr int TR_CTAS = 8, TR_ITEMS = 512, TR_F = 10;
+constexpr int TR_CTAS = 8, TR_ITEMS = 512, TR_F = 16;
 #define GIFT_TRACE(p, it, f, v)                                                       \
   do {                                                                                \
     if ((p).trace != nullptr && blockIdx.x < TR_CTAS && (it) < TR_ITEMS)              \
@@ -82,6 +87,12 @@ int quantize_impl(const void* X, int32_t xdtype, int64_t n, int32_t d, const flo
                   size_t ws_bytes, void* stream, bool need_order, const float* xnorm2,
                   bool allow_tc);
 size_t tc_probe_plane_bytes(int64_t nprobes, int d);
+// Dense cells of an fp16-storage index (>= DENSE_MIN_PROBES probes in the
+// batch, fp16-exact queries): probe-major CTA-pair scan (fif_scan_dense.cu).
+constexpr int DENSE_MIN_PROBES = 192;
+bool tc_dense_enabled(const gift_fif_view* f);
+cudaError_t launch_scan_dense(int ctas, cudaStream_t st, const CUtensorMap& mQ,
+                              const CUtensorMap& mP, const TcArgs& a, const int64_t* item_off2);
 int launch_scan_tc(const gift_fif_view* f, const float* Q, int64_t nprobes_max, TcArgs a,
                    __half* g1, __half* g2, cudaStream_t st, void* ev0, void* ev1);
 

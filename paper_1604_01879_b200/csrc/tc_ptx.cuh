@@ -216,6 +216,19 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_bar) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_bar)
                : "memory");
 }
+// Arrive without release semantics (no MEMBAR: a release at cluster scope
+// waits for every outstanding global store of the warp).  For the TMEM
+// accumulator hand-back, whose ordering is the tcgen05.wait::ld +
+// tcgen05.fence::before_thread_sync issued before it.
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_bar) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_bar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_relaxed(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_addr(bar))
+               : "memory");
+}
+
 // TMA into this CTA's smem, completion bytes counted on the (leader's) barrier
 __device__ __forceinline__ void tma_load_2d_2sm(void* smem_dst, const CUtensorMap* m,
                                                 uint32_t cluster_bar, int32_t x, int32_t y) {

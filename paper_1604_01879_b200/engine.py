@@ -126,16 +126,19 @@ class DeviceFif:
 
     def set_variant(self, scan: str = "tc", quant: str = "tc", reduce: str = "auto",
                     pair: str = "auto", sched: str = "dynamic", drain_kb: int = 0,
-                    raw_accum: bool = False):
+                    raw_accum: bool = False, dense: str = "auto"):
         """Select kernel variants through the view flags (include/gift.h):
         scan/quant "tc" | "simt", reduce "auto" | "range" | "gather" | "owner",
         pair "auto" | "on" | "off", sched "dynamic" | "static", drain_kb 0..16
         (0 = default), raw_accum (no truncation compensation; measurement
-        only).  Defaults reproduce the measured-fastest choice."""
+        only), dense "auto" | "off" (fp16 storage: the probe-major pair scan
+        of the cells with >= 192 probes per batch).  Defaults reproduce the
+        measured-fastest choice."""
         v = (nat.FIF_SCAN_SIMT if scan == "simt" else 0) | \
             (nat.FIF_QUANT_SIMT if quant == "simt" else 0) | nat.FIF_REDUCE[reduce] | \
             nat.FIF_PAIR[pair] | (nat.FIF_SCHED_STATIC if sched == "static" else 0) | \
-            nat.fif_drain_kb(drain_kb) | (nat.FIF_RAW_ACCUM if raw_accum else 0)
+            nat.fif_drain_kb(drain_kb) | (nat.FIF_RAW_ACCUM if raw_accum else 0) | \
+            (nat.FIF_DENSE_OFF if dense == "off" else 0)
         self.variant = v
         self.bind()
         return self

@@ -23,19 +23,21 @@ def dev():
     return torch.device("cuda", 0)
 
 
+@pytest.mark.parametrize("pair", ["off", "on"])
 @pytest.mark.parametrize("storage", ["float16", "float32"])
-def test_fp16_exact_queries_skip_lo_plane_bit_identical(storage):
+def test_fp16_exact_queries_skip_lo_plane_bit_identical(storage, pair):
     """Queries whose values are exactly fp16 have an all-zero lo plane: the
-    single-CTA scan then issues one N = n MMA per k-step (no b2 operand).  A
-    batch with one non-fp16 value elsewhere takes the full [b1 | b2] path; the
-    fp16-exact queries must score bit-identically in both batches, and match
-    the widened oracle."""
+    scan then drops the b2 operand (single CTA: one N = n MMA per k-step;
+    fp16-storage CTA pairs: N = 256 probe columns per item instead of
+    [b1 | b2] over 128).  A batch with one non-fp16 value elsewhere takes the
+    full [b1 | b2] path; the fp16-exact queries must score bit-identically in
+    both batches, and match the widened oracle."""
     views, _ = mixture_views(31, 240, 20, 256, 12, n_queries=5)
     db = views[:240].astype(np.float16 if storage == "float16" else np.float32)
     q16 = views[240:].astype(np.float16).astype(np.float32)  # fp16-exact
     C = sampled_codebook(db.astype(np.float32), 24, 2)
     fif = mt.build_fif_from_tensor(torch.from_numpy(db).to(dev()), Codebook(C), shape_ids(240))
-    fif.dev.set_variant(pair="off")  # the single-CTA kernel (default for fp16 storage)
+    fif.dev.set_variant(pair=pair)
     other = views[240:241].copy()
     other[0, 0, 7] += np.float32(1e-6)  # not representable in fp16: lo plane non-zero
     for sim in ("gaussian", "cosine"):
@@ -126,3 +128,37 @@ def test_scan_variants_many_probes_per_cell(storage):
                                            err_msg=f"{storage} {qname} pair={pair} drain={kb}")
     fif.dev.set_variant()
     del rng
+
+
+@pytest.mark.parametrize("sim", ["gaussian", "cosine"])
+def test_dense_cells_probe_major_scan(sim):
+    """fp16 storage with cells probed by >= 192 query views in one batch: the
+    dense cells run on the probe-major CTA-pair scan (fif_scan_dense.cu; odd
+    posting-tile counts, probe counts not a multiple of 256, CTAs without
+    valid probes), the others on the single-CTA scan.  Scores match the
+    widened f64 oracle, and the posting-major scan of every cell
+    (dense="off") within the same contract; a batch with a non-fp16 query
+    value takes no dense split and scores the fp16-exact queries the same."""
+    views, _ = mixture_views(83, 1600, 8, 256, 5, n_queries=150)
+    db = views[:1600].astype(np.float16)
+    qs = views[1600:].astype(np.float16).astype(np.float32)
+    C = sampled_codebook(db.astype(np.float32), 6, 4)
+    fif = mt.build_fif_from_tensor(torch.from_numpy(db).to(dev()), Codebook(C), shape_ids(1600))
+    dbw = db.astype(np.float32)
+    assign = oracle.quantize_many(C, dbw.reshape(-1, 256), 1).reshape(1600, 8)
+    ref_fif = oracle.build_fif(list(dbw), C, assign=assign)
+    qcells = oracle.quantize_many(C, qs.reshape(-1, 256).astype(np.float64), 1).reshape(150, 8, 1)
+    counts = np.bincount(qcells.ravel(), minlength=6)
+    assert counts.max() >= 192, counts  # some cells take the dense scan
+    ref = np.stack([oracle.query_fif(ref_fif, q, 1, sim, cells=c) for q, c in zip(qs, qcells)])
+    got = mt.query_fif_batch(fif, qs, 1, sim).cpu().numpy()
+    np.testing.assert_allclose(got, ref, rtol=RTOL, atol=1e-12, err_msg="dense")
+    fif.dev.set_variant(dense="off")
+    off = mt.query_fif_batch(fif, qs, 1, sim).cpu().numpy()
+    np.testing.assert_allclose(off, ref, rtol=RTOL, atol=1e-12, err_msg="dense off")
+    np.testing.assert_allclose(got, off, rtol=4e-6, atol=1e-12)
+    fif.dev.set_variant()
+    other = views[1600:1601].copy()
+    other[0, 0, 3] += np.float32(1e-6)  # lo plane non-zero: no dense split
+    mixed = mt.query_fif_batch(fif, np.concatenate([qs, other]), 1, sim).cpu().numpy()[:150]
+    np.testing.assert_allclose(mixed, ref, rtol=RTOL, atol=1e-12, err_msg="mixed batch")

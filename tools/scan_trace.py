@@ -37,11 +37,18 @@ fif = mt.build_fif_from_tensor(db, Codebook(C), synth.shape_ids(w.n_shapes))
 del db
 fif.dev.set_variant(drain_kb=drain)
 q = qs[:w.batch].contiguous()
+so = fif.dev.seg_off.cpu().numpy()
+co = fif.dev.cell_off.cpu().numpy()
+big = np.argsort(-(co[1:] - co[:-1]))[:6]
+print("largest cells (postings, segments):",
+      [(int(co[c + 1] - co[c]), int(so[c + 1] - so[c])) for c in big], flush=True)
+print(f"{name} postings {fif.dev.P} segments {fif.dev.S} tiles {fif.dev.T} "
+      f"avg segment length {fif.dev.P / max(fif.dev.S, 1):.2f}", flush=True)
 run = eg.ScoreRunner()
 ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
 for e in ev:
     e.record()
-TR = torch.zeros(8 * 512 * 10, dtype=torch.int64, device=dev)
+TR = torch.zeros(8 * 512 * 16, dtype=torch.int64, device=dev)
 lib.gift_scan_experiment(expbits)
 for i in range(3):
     run.score(fif.dev, q, w.ma, nat.SIM_GAUSSIAN, 0.5, cand_k=4, dense=False, scan_events=ev)
@@ -52,7 +59,7 @@ run.score(fif.dev, q, w.ma, nat.SIM_GAUSSIAN, 0.5, cand_k=4, dense=False, scan_e
 torch.cuda.synchronize()
 lib.gift_scan_trace(ctypes.c_void_p(0))
 print(f"{name} scan {ev[0].elapsed_time(ev[1]):.3f} ms (traced)")
-t = TR.view(8, 512, 10).cpu().numpy()
+t = TR.view(8, 512, 16).cpu().numpy()
 os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
 np.save(os.path.join(ROOT, "gpurun_out", f"trace_{name}_{drain}_{expbits}.npy"), t)
 names = ["sched", "prod_take", "prod_end", "mma_take", "mma_end", "epi_take", "epi_drained",
@@ -73,3 +80,8 @@ for b in range(2):
               " epi drain (drained-take)", np.median(tb[:n, 6] - tb[:n, 5]),
               " tail (tail-drained)", np.median(tb[:n, 7] - tb[:n, 6]),
               " prod (end-take)", np.median(tb[:n, 2] - tb[:n, 1]))
+        if tb[:n, 12].any():
+            print("  tail parts: stage+bar", np.median(tb[:n, 10] - tb[:n, 6]),
+                  " masks+bar", np.median(tb[:n, 11] - tb[:n, 10]),
+                  " row loop", np.median(tb[:n, 12] - tb[:n, 11]),
+                  " final bar", np.median(tb[:n, 7] - tb[:n, 12]))
