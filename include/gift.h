@@ -74,7 +74,7 @@ extern "C" {
 #define GIFT_FIF_DRAIN_SHIFT 24         /* bits 24-28: D1 drain interval in    */
 #define GIFT_FIF_DRAIN_KB(n) (((n) & 31) << GIFT_FIF_DRAIN_SHIFT) /* 64-wide */
                                         /* k-blocks, 1..16 (0 = the default:   */
-                                        /* 4, the 1e-5 contract at d = 4096)   */
+                                        /* 8: max 2.1e-6 vs the 1e-5 contract) */
 #define GIFT_FIF_RAW_ACCUM (1 << 29)    /* no truncation compensation of the   */
                                         /* tensor-core accumulators (tests)    */
 #define GIFT_FIF_DENSE_OFF (1 << 30)    /* fp16 storage: no probe-major pair   */

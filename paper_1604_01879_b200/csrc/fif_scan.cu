@@ -1328,9 +1328,11 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
     ta.inv_sigma2 = mode == GIFT_SIM_GAUSSIAN ? static_cast<float>(1.0 / (sigma * sigma)) : 0.f;
     ta.has_lo = 0;
     // D1 drain interval (k-blocks): short tensor-core accumulation chains
-    // hold the 1e-5 contract; at most 4
+    // hold the 1e-5 contract; default 8 (with the calibrated truncation
+    // compensation: max 2.1e-6 on c4s, 0.65e-6 on c2s against the f64
+    // oracle, profiles/r02/drain_interval_error_study_calibrated.jsonl)
     const int dkb = (f->flags >> GIFT_FIF_DRAIN_SHIFT) & 31;
-    ta.chunk_kb = dkb == 0 ? 4 : dkb;
+    ta.chunk_kb = dkb == 0 ? 8 : dkb;
     ta.dyn = (f->flags & GIFT_FIF_SCHED_STATIC) ? 0 : 1;
 #ifdef GIFT_SCAN_EXPERIMENT
     ta.exp = g_scan_experiment;
@@ -1342,7 +1344,7 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
       for (int kb0 = 0; kb0 < nkb; kb0 += ta.chunk_kb) {
         const double n = 4.0 * min(ta.chunk_kb, nkb - kb0);  // K = 16 steps per 64-wide block
         s1 += n;
-        s2 += n * n;
+        s2 += n * n * tcomp_ratio(n);
       }
       ta.tcomp_scale = (f->flags & GIFT_FIF_RAW_ACCUM) ? 0.f
                                                        : static_cast<float>(TCOMP_PER_STEP * s2 / s1);

@@ -116,11 +116,16 @@ __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
 }
 
-// 2^x on the SFU (relative error ~2^-22)
-__device__ __forceinline__ float ex2(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
+// predicated shared store (one @P STS, no branch around it)
+__device__ __forceinline__ void sts_pred(uint32_t a, float v, uint32_t pred) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.u32 p, %2, 0;\n"
+      "@p st.shared.f32 [%0], %1;\n"
+      "}\n" ::"r"(a),
+      "f"(v), "r"(pred)
+      : "memory");
 }
 
 // predicated global store (one @P STG, no branch around it)
@@ -142,6 +147,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(16) float s_pn[2][NP];  // per group: |p|^2 of the tile's postings
   __shared__ uint32_t s_end[2][NP / 32];       // per group: segment-end columns
+  __shared__ float s_emit[2][16][MP];          // per thread: segment maxima of 16 columns
   __shared__ Item s_item[IRING];
   __shared__ __align__(8) uint64_t ifull[IRING], iempty[IRING];
   __shared__ __align__(8) int64_t s_next[IRING];
@@ -200,7 +206,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&iempty[slot]);
       if (I.c < 0) break;
-      if (lane == 0) GIFT_TRACE(p, it, 1, clock64());
+      if (lane == 0) GIFT_TRACE_K(p, 1, it, 1, clock64());
       for (int kb = 0; kb < nkb; ++kb) {
         tc::mbar_wait(&empty[stage], phase ^ 1);
         if (tc::elect_one()) {
@@ -216,7 +222,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           phase ^= 1;
         }
       }
-      if (lane == 0) GIFT_TRACE(p, it, 2, clock64());
+      if (lane == 0) GIFT_TRACE_K(p, 1, it, 2, clock64());
     }
   } else if (warp == 1) {
     // ------------------------------------------------------ MMA issuer (leader)
@@ -232,7 +238,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&iempty[slot]);
         if (I.c < 0) break;
-        if (lane == 0) GIFT_TRACE(p, it, 3, clock64());
+        if (lane == 0) GIFT_TRACE_K(p, 1, it, 3, clock64());
         for (int kb0 = 0; kb0 < nkb; kb0 += chunk_kb) {
           const uint32_t buf = chunk_ctr & 1, aph = (chunk_ctr >> 1) & 1;
           tc::mbar_wait(&tempty[buf], aph ^ 1);
@@ -263,7 +269,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           __syncwarp();
           ++chunk_ctr;
         }
-        if (lane == 0) GIFT_TRACE(p, it, 4, clock64());
+        if (lane == 0) GIFT_TRACE_K(p, 1, it, 4, clock64());
       }
     }
   } else if (warp == 2) {
@@ -300,10 +306,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc::mbar_wait(&iempty[slot], iph ^ 1);
         s_item[slot] = I;
         tc::mbar_arrive(&ifull[slot]);
-        GIFT_TRACE(p, it, 0, clock64());
+        GIFT_TRACE_K(p, 1, it, 0, clock64());
         if (item < n_items) {
-          GIFT_TRACE(p, it, 8, I.npv);
-          GIFT_TRACE(p, it, 9, I.c);
+          GIFT_TRACE_K(p, 1, it, 8, I.npv);
+          GIFT_TRACE_K(p, 1, it, 9, I.c);
         }
         if (item >= n_items) break;
       }
@@ -320,8 +326,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int row = 32 * wq + lane;    // probe row of this CTA's tile
     const int bar_tail = 1 + g, bar_item = 3 + g;
     const bool gauss = p.mode == GIFT_SIM_GAUSSIAN;
-    const float L = p.inv_sigma2 * 1.4426950408889634f;  // exp(-x / s^2) = 2^(-x L)
-    const float K2 = (gauss ? 2.0f : 1.0f) * (1.0f + p.tcomp_scale);
+    const float tc = p.tcomp_scale, K2 = gauss ? 2.0f : 1.0f;
     const uint32_t tempty_lead = tc::mapa(&tempty[0], 0);
     const uint32_t tm_row = tmem_base + (static_cast<uint32_t>(32 * wq) << 16) + g * NP;
     float* pn_s = s_pn[g];
@@ -334,7 +339,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       named_bar(bar_item, 128);
       if (e == 0) tc::mbar_arrive(&iempty[slot]);
       if (I.c < 0) break;
-      if (et == 0) GIFT_TRACE(p, it, 5, clock64());
+      if (et == 0) GIFT_TRACE_K(p, 1, it, 5, clock64());
       const int p0 = I.p0[g], ncol = I.p1[g] - p0;
       const int seg0 = I.seg0[g], nseg = I.seg1[g] - seg0;
       // tail inputs, loaded now (their latency overlaps the drains)
@@ -371,55 +376,62 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (lane == 0) tc::mbar_arrive_cluster_relaxed(tempty_lead + buf * 8);
         ++chunk_ctr;
       }
-      if (et == 0) GIFT_TRACE(p, it, 6, clock64());
+      if (et == 0) GIFT_TRACE_K(p, 1, it, 6, clock64());
       if (ncol <= 0 || I.npv == 0) continue;  // absent tile / no probes: nothing to write
       // segment-end columns of the tile (tiled segments: segment 0 starts at
       // column 0, segment e >= 1 at st_e, the last one ends at ncol - 1)
       pn_s[e] = pn_e;
       named_bar(bar_tail, 128);
-      if (et == 0) GIFT_TRACE(p, it, 10, clock64());
+      if (et == 0) GIFT_TRACE_K(p, 1, it, 10, clock64());
       if (st_e > 0) atomicOr(&end_s[(st_e - 1) >> 5], 1u << ((st_e - 1) & 31));
       if (e == 0) atomicOr(&end_s[(ncol - 1) >> 5], 1u << ((ncol - 1) & 31));
       named_bar(bar_tail, 128);
       uint32_t em[NP / 32];
 #pragma unroll
       for (int w = 0; w < NP / 32; ++w) em[w] = end_s[w];
-      if (et == 0) GIFT_TRACE(p, it, 11, clock64());
+      if (et == 0) GIFT_TRACE_K(p, 1, it, 11, clock64());
       // one probe's row: v = K2 s - |p|^2 (2 q.p - |p|^2 or q.p), running max
       // over each segment's columns, similarity stored at the segment's end
       float* o = p.out + obase + static_cast<int64_t>(I.rk0 + row) * S_c + (seg0 - seg_base);
-      // 4-column blocks: one (uniform) branch per block; only the blocks that
-      // hold a segment end (about 6 of 32 for config 4's 20-view segments)
-      // take the per-column path
+      // Straight-line code over the row (no branches: branchy per-block code
+      // thrashed the instruction cache): v = K2 s - |p|^2, running max m; at
+      // a segment end (predicated) m goes to this thread's slot of the emit
+      // buffer and restarts.  Every 16 columns a short loop turns the
+      // buffered maxima into similarities and stores them.
+      float* eb = s_emit[g][0] + row;  // entry j at eb[j * MP]
+      const uint32_t eb_s = tc::smem_addr(eb);
       float m = -INFINITY;
-      auto emit = [&]() {
-        const float sim = gauss ? ex2(fminf(m - qn, 0.f) * L) : fminf(fmaxf(m, 0.f), 1.f);
-        st_pred(o, sim, pvalid && !GIFT_EXP(p, 16));
-        ++o;
-        m = -INFINITY;
-      };
 #pragma unroll
-      for (int b = 0; b < NP / 4; ++b) {
-        const float4 pv = *reinterpret_cast<const float4*>(pn_s + 4 * b);
-        const float v0 = fmaf(acc[4 * b], K2, -pv.x), v1 = fmaf(acc[4 * b + 1], K2, -pv.y);
-        const float v2 = fmaf(acc[4 * b + 2], K2, -pv.z), v3 = fmaf(acc[4 * b + 3], K2, -pv.w);
-        const uint32_t nib = (em[b >> 3] >> ((b & 7) * 4)) & 15u;
-        if (nib == 0) {
-          m = fmaxf(m, fmaxf(fmaxf(v0, v1), fmaxf(v2, v3)));
-        } else {
-          m = fmaxf(m, v0);
-          if (nib & 1u) emit();
-          m = fmaxf(m, v1);
-          if (nib & 2u) emit();
-          m = fmaxf(m, v2);
-          if (nib & 4u) emit();
-          m = fmaxf(m, v3);
-          if (nib & 8u) emit();
+      for (int h = 0; h < NP / 16; ++h) {
+        const uint32_t bits = (em[h >> 1] >> ((h & 1) * 16)) & 0xffffu;
+        uint32_t koff = 0;  // emitted entries x MP x 4 bytes
+#pragma unroll
+        for (int i4 = 0; i4 < 16; i4 += 4) {
+          const float4 pv = *reinterpret_cast<const float4*>(pn_s + 16 * h + i4);
+          const float pc[4] = {pv.x, pv.y, pv.z, pv.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            // the posting-major kernel's arithmetic, operation for operation
+            // (scores independent of which kernel a batch's cell ran on)
+            m = fmaxf(m, fmaf(K2, fmaf(acc[16 * h + i4 + i], tc, acc[16 * h + i4 + i]), -pc[i]));
+            const uint32_t end = (bits >> (i4 + i)) & 1u;
+            sts_pred(eb_s + koff, m, end);
+            koff += end << 9;  // MP * 4 bytes
+            m = end ? -INFINITY : m;
+          }
         }
+        const int k = static_cast<int>(koff >> 9);
+        for (int j = 0; j < k; ++j) {
+          const float x = eb[j * MP];
+          const float sim =
+              gauss ? expf(-fmaxf(qn - x, 0.f) * p.inv_sigma2) : fminf(fmaxf(x, 0.f), 1.f);
+          st_pred(o + j, sim, pvalid && !GIFT_EXP(p, 16));
+        }
+        o += k;
       }
-      if (et == 0) GIFT_TRACE(p, it, 12, clock64());
+      if (et == 0) GIFT_TRACE_K(p, 1, it, 12, clock64());
       named_bar(bar_tail, 128);  // s_pn / s_end are reused by the next item
-      if (et == 0) GIFT_TRACE(p, it, 7, clock64());
+      if (et == 0) GIFT_TRACE_K(p, 1, it, 7, clock64());
     }
   }
   tc::tc_fence_before();

@@ -55,22 +55,37 @@ struct TcArgs {
 // i.e. a fraction 0.5 n 2^-23 (1/m)(1 - 2/(3m)) of v, whose mean over
 // log-uniform mantissas is 0.5 n 2^-23 / (4 ln 2).  The chunks' shares of a
 // dot scale with their lengths, so each item's dots are scaled once by
-//   1 + TCOMP_PER_STEP * sum_c n_c^2 / sum_c n_c.
+//   1 + TCOMP_PER_STEP * sum_c n_c^2 r(n_c) / sum_c n_c.
+// r(n) is the measured excess of the loss over that model (the loss per
+// step grows with the chain: 1.2x at 4 steps .. 1.8x at 64), calibrated
+// against the f64 oracle on fp16 storage (c4s) and f32 planes (c2s) alike
+// (tools/drain_error.py, profiles/r02/drain_interval_error_study.jsonl:
+// uncompensated gaussian-score bias -0.72/-0.80, -1.55/-1.67, -3.44/-3.64,
+// -8.05/-8.06, -17.7/-17.4 e-6 at 4, 8, 16, 32, 64 steps per chunk).
 constexpr double TCOMP_PER_STEP = 0.5 * 0x1p-23 / (4.0 * 0.6931471805599453);
+inline double tcomp_ratio(double n) {
+  constexpr double R[5] = {1.22, 1.30, 1.43, 1.63, 1.77};  // n = 4, 8, 16, 32, 64
+  const double x = log2(n < 4 ? 4.0 : n > 64 ? 64.0 : n) - 2.0;  // 0 .. 4
+  const int i = x >= 4.0 ? 3 : static_cast<int>(x);
+  return R[i] + (R[i + 1] - R[i]) * (x - i);
+}
 
 #ifdef GIFT_SCAN_EXPERIMENT
 #define GIFT_EXP(p, bit) (((p).exp & (bit)) != 0)
 // per-role clock64 stamps of the first CTAs' items (tools/scan_trace.py):
 // trace[((cta * TR_ITEMS) + item) * TR_F + field]
 constexpr int TR_CTAS = 8, TR_ITEMS = 512, TR_F = 16;
-#define GIFT_TRACE(p, it, f, v)                                                       \
+// (the dense-cell kernel stamps the second half: GIFT_TRACE_K(p, 1, ...))
+#define GIFT_TRACE_K(p, k, it, f, v)                                                  \
   do {                                                                                \
     if ((p).trace != nullptr && blockIdx.x < TR_CTAS && (it) < TR_ITEMS)              \
-      (p).trace[((blockIdx.x * TR_ITEMS) + (it)) * TR_F + (f)] = (v);                 \
+      (p).trace[(((k) * TR_CTAS + blockIdx.x) * TR_ITEMS + (it)) * TR_F + (f)] = (v); \
   } while (0)
+#define GIFT_TRACE(p, it, f, v) GIFT_TRACE_K(p, 0, it, f, v)
 #else
 #define GIFT_EXP(p, bit) false
 #define GIFT_TRACE(p, it, f, v) do {} while (0)
+#define GIFT_TRACE_K(p, k, it, f, v) do {} while (0)
 #endif
 
 bool tc_supported(const gift_fif_view* f);

@@ -26,6 +26,7 @@ dev = torch.device("cuda", 0)
 name = sys.argv[1] if len(sys.argv) > 1 else "c4s"
 drain = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 expbits = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+kern = int(sys.argv[4]) if len(sys.argv) > 4 else 0  # 0: posting-major scan, 1: dense cells
 w = synth.WORKLOADS[name]
 if w.storage == "float16":
     db, qs, Ct = synth.zipf_mixture(w, 20160407, dev)
@@ -48,7 +49,7 @@ run = eg.ScoreRunner()
 ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
 for e in ev:
     e.record()
-TR = torch.zeros(8 * 512 * 16, dtype=torch.int64, device=dev)
+TR = torch.zeros(2 * 8 * 512 * 16, dtype=torch.int64, device=dev)
 lib.gift_scan_experiment(expbits)
 for i in range(3):
     run.score(fif.dev, q, w.ma, nat.SIM_GAUSSIAN, 0.5, cand_k=4, dense=False, scan_events=ev)
@@ -59,9 +60,10 @@ run.score(fif.dev, q, w.ma, nat.SIM_GAUSSIAN, 0.5, cand_k=4, dense=False, scan_e
 torch.cuda.synchronize()
 lib.gift_scan_trace(ctypes.c_void_p(0))
 print(f"{name} scan {ev[0].elapsed_time(ev[1]):.3f} ms (traced)")
-t = TR.view(8, 512, 16).cpu().numpy()
+t2 = TR.view(2, 8, 512, 16).cpu().numpy()
+t = t2[kern]
 os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-np.save(os.path.join(ROOT, "gpurun_out", f"trace_{name}_{drain}_{expbits}.npy"), t)
+np.save(os.path.join(ROOT, "gpurun_out", f"trace_{name}_{drain}_{expbits}.npy"), t2)
 names = ["sched", "prod_take", "prod_end", "mma_take", "mma_end", "epi_take", "epi_drained",
          "epi_tail"]
 for b in range(2):
@@ -84,4 +86,5 @@ for b in range(2):
             print("  tail parts: stage+bar", np.median(tb[:n, 10] - tb[:n, 6]),
                   " masks+bar", np.median(tb[:n, 11] - tb[:n, 10]),
                   " row loop", np.median(tb[:n, 12] - tb[:n, 11]),
+                  " (pass 1", np.median(tb[:n, 13] - tb[:n, 11]), ")",
                   " final bar", np.median(tb[:n, 7] - tb[:n, 12]))
