@@ -308,10 +308,26 @@ def load_traffic(config):
     return n["scan_dram_read_bytes"] + n.get("scan_dram_write_bytes", 0)
 
 
-def roofline_of(nbytes, flops, scan_ms, w, kernel, measured):
+def scan_kernel_name(w, what=""):
+    """The scan's kernels: fp16 storage runs the dense cells (>= 192 probes
+    per batch) on fif_scan_dense_kernel and the others on fif_scan_tc_kernel,
+    one after the other on the stream, both inside the scan events."""
+    k = ("fif_scan_dense_kernel + fif_scan_tc_kernel (dense / other cells)"
+         if w.storage == "float16" else "fif_scan_tc_kernel")
+    return k + what
+
+
+def fp16_exact(batches):
+    """Every query value exactly an fp16 (config 4's fp16-rounded views): the
+    scan then drops the query lo plane (one fp16 MMA product per product)."""
+    return all(bool((b.to(torch.float16).to(b.dtype) == b).all()) for b in batches)
+
+
+def roofline_of(nbytes, flops, scan_ms, w, kernel, measured, q16=False):
     """The slower of the HBM time and the tensor time of the algorithmic
-    work; the fp32 split runs 2 (fp16 storage) or 3 (f32)
-    fp16 MMA products per algorithmic product on the tensor cores."""
+    work; the fp32 split runs 3 (f32 planes), 2 (fp16
+    storage) or 1 (fp16 storage, fp16-exact queries) fp16 MMA products per
+    algorithmic product on the tensor cores."""
     peak, peak_kind = measured_peaks()
     tpeak = measured_tensor_peak()
     scan_s = scan_ms / 1000.0
@@ -319,7 +335,7 @@ def roofline_of(nbytes, flops, scan_ms, w, kernel, measured):
     achieved_tf = flops / scan_s / 1e12
     t_hbm = nbytes / (peak * 1e9)
     t_tc = flops / (tpeak * 1e12)
-    split = 2 if w.storage == "float16" else 3
+    split = (1 if q16 else 2) if w.storage == "float16" else 3
     if t_tc > t_hbm:
         r = {"bound": "tensor", "achieved": achieved_tf, "peak": tpeak, "unit": "TFLOP/s",
              "frac": achieved_tf / tpeak}
@@ -565,11 +581,12 @@ def run_gift(args, w):
     nbytes = sum(x[0] for x in work) / len(work)
     flops = sum(x[1] for x in work) / len(work)
     scan_avg = sum(scan_ms) / len(scan_ms)
-    roof = roofline_of(nbytes, flops, scan_avg, w, "fif_scan_tc_kernel",
+    roof = roofline_of(nbytes, flops, scan_avg, w, scan_kernel_name(w),
                        ("CUDA events around each scan launch, the timed batches re-run one "
                         f"at a time with the timed configuration ({eng.reserve_sms} SMs left "
                         "to other lanes)") if L > 1 else
-                       "CUDA events around each scan launch inside the timed region")
+                       "CUDA events around each scan launch inside the timed region",
+                       q16=fp16_exact(batches[:4]))
     roof["scan_ms_in_flight_avg"] = sum(scan_in_flight) / len(scan_in_flight)
     roof["scan_share_of_step"] = scan_avg * args.steps / ms
     # lower bound independent of overlap: the scan's algorithmic bytes per
@@ -756,8 +773,9 @@ def run_sharded(args, w):
         sms.append(ev[0].elapsed_time(ev[1]))
     work = [scan_work(fif, batches[i % nb], w, w.top_k) for i in range(min(args.steps, 4))]
     roof = roofline_of(sum(x[0] for x in work) / len(work), sum(x[1] for x in work) / len(work),
-                       sum(sms) / len(sms), w, "fif_scan_tc_kernel (this rank's shard)",
-                       "CUDA events around the shard's scan, batches run one at a time")
+                       sum(sms) / len(sms), w, scan_kernel_name(w, " (this rank's shard)"),
+                       "CUDA events around the shard's scan, batches run one at a time",
+                       q16=fp16_exact(batches[:4]))
     if rank == 0:
         total_q = B * args.steps
         line = _gpu_line(args, workload_config(w, f"shard{ws}"), total_q / (ms / 1000.0),

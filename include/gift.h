@@ -117,6 +117,10 @@ typedef struct gift_fif_view {
   const int32_t* shape_seg;     /* [S] global segment index, ascending cell   */
   const int32_t* shape_seg_cell;/* [S] cell of segment shape_seg[g]           */
   int64_t max_cell_segments;    /* max over cells of its segment count         */
+  const uint8_t* seg_single;    /* [S] 1: the segment's shape has no other    */
+                                /* segment (all its views in one cell; the    */
+                                /* owner reduce skips its shape lookups);     */
+                                /* optional (NULL)                            */
 } gift_fif_view;
 
 /* ---- library ---- */

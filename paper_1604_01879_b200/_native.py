@@ -64,7 +64,7 @@ class FifView(ctypes.Structure):
         ("centroids", _c_p), ("cnorm2", _c_p), ("cmax_norm", _c_dbl),
         ("feat_hi", _c_p), ("feat_lo", _c_p),
         ("shape_seg_off", _c_p), ("shape_seg", _c_p), ("shape_seg_cell", _c_p),
-        ("max_cell_segments", _c_i64),
+        ("max_cell_segments", _c_i64), ("seg_single", _c_p),
     ]
 
 

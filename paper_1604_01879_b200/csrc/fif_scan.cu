@@ -633,6 +633,7 @@ struct GatherArgs {
   const int64_t* shape_seg_off;  // [n_local + 1]
   const int32_t* shape_seg;      // [S] global segment index, ascending cell
   const int32_t* shape_seg_cell; // [S] its cell
+  const uint8_t* seg_single;     // [S] the segment's shape has no other segment (or null)
   const int64_t* seg_off;        // [K + 1]
   const int32_t* seg_ord;        // [S] global shape ordinal of each segment
   const float* out;              // compact (probe x segment) best similarities
@@ -760,6 +761,12 @@ __device__ __forceinline__ bool probed(const GrTabs& t, int g, int c) {
 // f64 sum over the views (ascending) of the best similarity over the view's
 // ma slots whose cell holds a segment of the shape: the reference's
 // `total += view_best` (matching.py:153-161) for one (query g, shape).
+#ifndef OWN_FAST
+#define OWN_FAST 4
+#endif
+#ifndef OWN_CTAS1
+#define OWN_CTAS1 4
+#endif
 template <int W>
 __device__ __forceinline__ double pair_acc(const GatherArgs& a, const GrTabs& t, int g,
                                            const ShapeSegs& h) {
@@ -810,13 +817,15 @@ __device__ __forceinline__ double pair_acc(const GatherArgs& a, const GrTabs& t,
   // Fast path: ma == 1 and a single segment (every bit is its own view in the
   // shape's only cell) -> acc += compact[base_j + seg], j ascending.
   if (a.ma == 1 && h.nseg == 1) {
+    // OWN_FAST independent loads per round (config 4: the 20 views of a
+    // query probing one cell; the reduce is bound by load latency)
     const int32_t sg0 = h.seg[0];
     while (true) {
-      int jj[4];
-      bool ok[4];
-      float val[4];
+      int jj[OWN_FAST];
+      bool ok[OWN_FAST];
+      float val[OWN_FAST];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < OWN_FAST; ++q) {
         ok[q] = false;
         jj[q] = 0;
 #pragma unroll
@@ -830,11 +839,11 @@ __device__ __forceinline__ double pair_acc(const GatherArgs& a, const GrTabs& t,
       }
       if (!ok[0]) break;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) val[q] = ok[q] ? a.out[sb[jj[q]] + sg0] : 0.f;
+      for (int q = 0; q < OWN_FAST; ++q) val[q] = ok[q] ? a.out[sb[jj[q]] + sg0] : 0.f;
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < OWN_FAST; ++q)
         if (ok[q]) acc += static_cast<double>(val[q]);
-      if (!ok[3]) break;
+      if (!ok[OWN_FAST - 1]) break;
     }
   }
   while (true) {
@@ -982,7 +991,7 @@ constexpr int OWN_WARPS = GR_THREADS / 32;
 // more (80 registers for the larger probed-cell cache; config 3: 0.69 ->
 // 0.59 ms).
 template <int W>
-__global__ void __launch_bounds__(GR_THREADS, W >= 2 ? 3 : 4) fif_owner_reduce_kernel(GatherArgs a) {
+__global__ void __launch_bounds__(GR_THREADS, W >= 2 ? 3 : OWN_CTAS1) fif_owner_reduce_kernel(GatherArgs a) {
   extern __shared__ __align__(16) double s_tab[];
   if (a.meta[M_OVERFLOW]) return;
   const int slots = a.V * a.ma;
@@ -1030,7 +1039,19 @@ __global__ void __launch_bounds__(GR_THREADS, W >= 2 ? 3 : 4) fif_owner_reduce_k
   for (int64_t k = k0 + threadIdx.x; k < k1; k += GR_THREADS) {
     const int32_t ord = a.seg_ord[so + k];
     const int64_t s = ord - a.ord_base;
-    const ShapeSegs h = load_segs(a, s);
+    ShapeSegs h;
+    if (a.seg_single != nullptr && a.seg_single[so + k]) {
+      // the shape's only segment is this one (coalesced flag, no lookups)
+      h.g0 = 0;
+      h.nseg = 1;
+#pragma unroll
+      for (int r = 0; r < GR_SEGC; ++r) {
+        h.seg[r] = r == 0 ? static_cast<int32_t>(so + k) : 0;
+        h.cell[r] = r == 0 ? c : -1;
+      }
+    } else {
+      h = load_segs(a, s);
+    }
     // owner test: the first of the shape's cells (ascending) the query probed
     int first = -1;
 #pragma unroll
@@ -1396,6 +1417,7 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
     ga.shape_seg_off = f->shape_seg_off;
     ga.shape_seg = f->shape_seg;
     ga.shape_seg_cell = f->shape_seg_cell;
+    ga.seg_single = f->seg_single;
     ga.seg_off = f->seg_off;
     ga.seg_ord = f->seg_ord;
     ga.out = w.compact;

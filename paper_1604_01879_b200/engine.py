@@ -178,6 +178,7 @@ class DeviceFif:
         v.shape_seg = self.shape_seg.data_ptr()
         v.shape_seg_cell = self.shape_seg_cell.data_ptr()
         v.max_cell_segments = self.smax
+        v.seg_single = self.seg_single.data_ptr()
         v.flags = (nat.FIF_TILED_SEGMENTS if self.seg_len_max <= nat.lib().gift_fif_tile_n()
                    else 0) | self.variant
         self.view = v
@@ -365,9 +366,16 @@ class DeviceFif:
         if S:
             self.shape_seg = v3
             self.shape_seg_cell = seg_cell[v3.long()].contiguous()
+            # segments whose shape has no other segment (config 4: every
+            # shape's views share one cell): the owner reduce skips the
+            # shape's segment lookups (three scattered loads per pair)
+            nseg = self.shape_seg_off[1:] - self.shape_seg_off[:-1]
+            self.seg_single = (nseg[(self.seg_ord[:S] - self.ord_base).long()] == 1).to(
+                torch.uint8).contiguous()
         else:
             self.shape_seg = torch.zeros(1, dtype=torch.int32, device=dev)
             self.shape_seg_cell = torch.zeros(1, dtype=torch.int32, device=dev)
+            self.seg_single = torch.zeros(1, dtype=torch.uint8, device=dev)
         self.bind()
 
     # -- host views (reference container attributes) ---------------------
