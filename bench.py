@@ -882,6 +882,9 @@ def run_c5(args):
         t = torch.tensor([e2e_s], dtype=torch.float64, device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
+    roof = None
+    if bundle is not None:
+        roof = c5_roofline(bundle, idx, val, rows[args.warmup:args.warmup + min(args.steps, 4)], c)
     cpu = None
     if rank == 0 and bundle is not None and not args.no_cpu_baseline:
         cpu = c5_cpu_baseline(bundle, idx, val, rows[args.warmup], c)
@@ -893,12 +896,51 @@ def run_c5(args):
                          {"value": B * args.steps / e2e_s, "unit": UNIT,
                           "h2d_bytes_per_step": B * (L * 12 + 8),
                           "d2h_bytes_per_step": B * c["top_k"] * 12},
-                         launches * args.steps, None, cpu, clk,
+                         launches * args.steps, roof, cpu, clk,
                          {"build_s": build_s, "sif_postings": postings,
                           "host_blocking_cuda_calls_per_step": syncs}, dtype="f64")
         print(json.dumps(line), flush=True)
     if sharded:
         dist.destroy_process_group()
+
+
+def c5_roofline(bundle, idx, val, rows, c):
+    """Roofline of config 5's dominant step, the S-IF query + ranking of a
+    batch (gift_sif_query_topk: bucket split of the touched postings by shape
+    range, shared-memory sums, top-100): algorithmic bytes = the postings of
+    the query activations' coordinates, 12 B each (i32 owner + f64 value:
+    one read of every touched posting, rerank.py:187-230); time = CUDA events
+    around the call, the timed batches re-run one at a time."""
+    from paper_1604_01879_b200 import engine as eg
+
+    eng = bundle.engine
+    e_off = bundle.sif.dev.e_off
+    lens = e_off[1:] - e_off[:-1]
+    ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    nbytes, ms = [], []
+    for r in rows:
+        qi, qv = idx[r], val[r]
+        k2 = min(eng.cfg.k2, qi.shape[1])
+        nbr = torch.where(qv[:, :k2] > 0, qi[:, :k2], torch.full_like(qi[:, :k2], -1))
+        fa = eg.act_mean(eng.raw_a, nbr.to(torch.int32).contiguous())
+        live = torch.arange(fa.cap, device=fa.idx.device)[None, :] < fa.cnt[:, None].long()
+        nbytes.append(float(lens[fa.idx[live].long()].sum().item()) * 12.0)
+        torch.cuda.synchronize()
+        ev[0].record()
+        eng._sif_rank(fa, c["top_k"], r.to(torch.int32))
+        ev[1].record()
+        torch.cuda.synchronize()
+        ms.append(ev[0].elapsed_time(ev[1]))
+    peak, peak_kind = measured_peaks()
+    b = sum(nbytes) / len(nbytes)
+    t = sum(ms) / len(ms)
+    achieved = b / (t / 1000.0) / 1e9
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "kernel": "gift_sif_query_topk (sif_split_* + bucket sums + "
+            "ranking kernels)", "peak_source": peak_kind, "traffic": None,
+            "alg_bytes_per_launch": b, "sif_ms_avg": t,
+            "measured": "CUDA events around the S-IF query + ranking of each timed batch, "
+                        "re-run one at a time"}
 
 
 _C5 = None

@@ -19,6 +19,13 @@ pytestmark = pytest.mark.gpu
 
 
 def _case(i):
+    if i == "fp16":  # fp16 storage, cells probed >= 192 times: the dense-cell scan
+        views, _ = mixture_views(83, 600, 8, 64, 5, n_queries=100)
+        db = views[:600].astype(np.float16)
+        qs = views[600:].astype(np.float16).astype(np.float32)
+        C = sampled_codebook(db.astype(np.float32), 3, 4)
+        return db, qs, C, dict(n_views=8, codebook_size=3, ma=1, k1=6, k2=3, imported=True,
+                               storage_dtype="float16", similarity="gaussian"), 20
     name, seed, N, V, d, classes, K, ma, k1, k2, nq, top_k, zv = E2E_CASES[i]
     views, _ = mixture_views(seed, N, V, d, classes, zero_views=zv, n_queries=nq)
     C = sampled_codebook(views[:N], K, seed + 1)
@@ -84,7 +91,7 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("case", [1, 2])
+@pytest.mark.parametrize("case", [1, 2, "fp16"])
 def test_sharded_world1_equals_single(case):
     db, qs, C, cfgkw, top_k = _case(case)
     ref_i, ref_v = _single(db, qs, C, cfgkw, top_k)
@@ -99,7 +106,7 @@ def test_sharded_world1_equals_single(case):
     np.testing.assert_array_equal(v, ref_v)
 
 
-@pytest.mark.parametrize("case", [1, 2])
+@pytest.mark.parametrize("case", [1, 2, "fp16"])
 def test_sharded_world2_equals_single(case):
     db, qs, C, cfgkw, top_k = _case(case)
     ref_i, ref_v = _single(db, qs, C, cfgkw, top_k)

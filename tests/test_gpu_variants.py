@@ -153,6 +153,10 @@ def test_dense_cells_probe_major_scan(sim):
     ref = np.stack([oracle.query_fif(ref_fif, q, 1, sim, cells=c) for q, c in zip(qs, qcells)])
     got = mt.query_fif_batch(fif, qs, 1, sim).cpu().numpy()
     np.testing.assert_allclose(got, ref, rtol=RTOL, atol=1e-12, err_msg="dense")
+    for kw in ({"sched": "static"}, {"drain_kb": 4}, {"drain_kb": 16}):
+        fif.dev.set_variant(**kw)  # static item stride; drain intervals
+        np.testing.assert_allclose(mt.query_fif_batch(fif, qs, 1, sim).cpu().numpy(), ref,
+                                   rtol=RTOL, atol=1e-12, err_msg=str(kw))
     fif.dev.set_variant(dense="off")
     off = mt.query_fif_batch(fif, qs, 1, sim).cpu().numpy()
     np.testing.assert_allclose(off, ref, rtol=RTOL, atol=1e-12, err_msg="dense off")
