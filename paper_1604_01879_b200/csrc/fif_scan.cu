@@ -641,6 +641,8 @@ struct GatherArgs {
   const int32_t* vq;
   int B, V, ma, K, rs, n_ranges, G;
   int chunk, nchunk;             // owner reduce: segments per item, max items per cell
+  int split;                     // owner reduce: single-segment shapes (ma == 1) go to
+                                 // fif_owner_fast_kernel (candidate rows in two halves)
   const int64_t* work_off;       // owner reduce: [B * slots + 1] work-list offsets per probe
   int64_t n_local, ord_base;
   double* scores;                // [B][n_local] or null (candidates only)
@@ -1016,8 +1018,8 @@ __global__ void __launch_bounds__(GR_THREADS, W >= 2 ? 3 : OWN_CTAS1) fif_owner_
   const int b = static_cast<int>(pr / slots), j = static_cast<int>(pr - static_cast<int64_t>(b) * slots);
   const int chunk_id = static_cast<int>(w - a.work_off[pr]);
   const int64_t cand_at =
-      (((static_cast<int64_t>(b) * slots + j) * a.nchunk + chunk_id) * OWN_WARPS +
-       (threadIdx.x >> 5)) * static_cast<int64_t>(ck);
+      ((((static_cast<int64_t>(b) * slots + j) * a.nchunk + chunk_id) * (a.split ? 2 : 1)) *
+           OWN_WARPS + (threadIdx.x >> 5)) * static_cast<int64_t>(ck);
   const int c = a.cells[pr];
   const int64_t S_c = a.seg_off[c + 1] - a.seg_off[c];
   const int64_t k0 = static_cast<int64_t>(chunk_id) * a.chunk;
@@ -1037,6 +1039,7 @@ __global__ void __launch_bounds__(GR_THREADS, W >= 2 ? 3 : OWN_CTAS1) fif_owner_
   }
   const int64_t so = a.seg_off[c];
   for (int64_t k = k0 + threadIdx.x; k < k1; k += GR_THREADS) {
+    if (a.split && a.seg_single[so + k]) continue;  // fif_owner_fast_kernel's
     const int32_t ord = a.seg_ord[so + k];
     const int64_t s = ord - a.ord_base;
     ShapeSegs h;
@@ -1079,6 +1082,99 @@ __global__ void __launch_bounds__(GR_THREADS, W >= 2 ? 3 : OWN_CTAS1) fif_owner_
           a.cand_i[cand_at + r] = oo[r];
         }
   }
+  }
+}
+
+// The owner reduce's single-segment shapes when ma == 1 (config 4: every
+// shape's views share one cell): a shape's score is the f64 sum, in slot
+// order, of its column over the compact rows of the query's slots probing
+// the item's cell -- pair_acc's fast path, the same additions in the same
+// order -- with that row list built once per work item instead of per shape,
+// in a kernel light enough to keep its candidate lists in registers (the
+// general kernel spills them).  Same work list; candidates in the second
+// half of each item's candidate row.
+__global__ void __launch_bounds__(GR_THREADS) fif_owner_fast_kernel(GatherArgs a) {
+  __shared__ int64_t s_ul[128];
+  __shared__ int s_nu;
+  if (a.meta[M_OVERFLOW]) return;
+  const int slots = a.V;  // ma == 1
+  const int64_t nprobes = static_cast<int64_t>(a.B) * slots;
+  const int64_t n_work = a.work_off[nprobes];
+  const int ck = a.cand_k;
+  const int lane = threadIdx.x & 31;
+  const int64_t per = (n_work + gridDim.x - 1) / gridDim.x;
+  const int64_t w0 = static_cast<int64_t>(blockIdx.x) * per;
+  const int64_t w1 = min64(n_work, w0 + per);
+  for (int64_t w = w0; w < w1; ++w) {
+    int64_t lo = 0, hi = nprobes - 1;  // probe of work item w
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (a.work_off[mid] <= w) lo = mid; else hi = mid - 1;
+    }
+    const int64_t pr = lo;
+    const int b = static_cast<int>(pr / slots), j = static_cast<int>(pr - static_cast<int64_t>(b) * slots);
+    const int chunk_id = static_cast<int>(w - a.work_off[pr]);
+    const int c = a.cells[pr];
+    __syncthreads();  // the previous item's readers of s_ul are done
+    if (threadIdx.x < 32) {  // the query's slots probing c, ascending
+      int nu = 0;
+      const int64_t q0 = static_cast<int64_t>(b) * slots;
+      for (int j0 = 0; j0 < slots; j0 += 32) {
+        const int jj = j0 + lane;
+        const bool hit = jj < slots && a.cells[q0 + jj] == c;
+        const unsigned bal = __ballot_sync(0xffffffffu, hit);
+        if (hit) s_ul[nu + __popc(bal & ((1u << lane) - 1u))] = a.slot_base[q0 + jj];
+        nu += __popc(bal);
+      }
+      if (lane == 0) s_nu = nu;
+    }
+    __syncthreads();
+    const int nu = s_nu;
+    const int64_t so = a.seg_off[c];
+    const int64_t S_c = a.seg_off[c + 1] - so;
+    const int64_t k0 = static_cast<int64_t>(chunk_id) * a.chunk;
+    const int64_t k1 = min64(S_c, k0 + a.chunk);
+    const double denom = static_cast<double>(a.vq ? a.vq[b] : a.V);
+    double ls[RED_MAXK];
+    int32_t lo_[RED_MAXK];
+#pragma unroll
+    for (int q = 0; q < RED_MAXK; ++q) {
+      ls[q] = -INFINITY;
+      lo_[q] = -1;
+    }
+    for (int64_t k = k0 + threadIdx.x; k < k1; k += GR_THREADS) {
+      if (!a.seg_single[so + k]) continue;  // the general kernel's
+      const int64_t sg = so + k;
+      double acc = 0.0;
+      int u = 0;
+      for (; u + 4 <= nu; u += 4) {
+        float v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = a.out[s_ul[u + q] + sg];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc += static_cast<double>(v[q]);
+      }
+      for (; u < nu; ++u) acc += static_cast<double>(a.out[s_ul[u] + sg]);
+      const int32_t ord = a.seg_ord[sg];
+      const double score = acc == 0.0 ? 0.0 : acc / denom;
+      if (a.scores) a.scores[static_cast<int64_t>(b) * a.n_local + (ord - a.ord_base)] = score;
+      if (ck > 0) cand_insert(ls, lo_, ck, score, ord);
+    }
+    if (ck > 0) {  // this warp's best ck, second half of the item's row
+      double os[RED_MAXK];
+      int32_t oo[RED_MAXK];
+      warp_select(ls, lo_, ck, os, oo);
+      const int64_t at =
+          ((((static_cast<int64_t>(b) * slots + j) * a.nchunk + chunk_id) * 2 + 1) * OWN_WARPS +
+           (threadIdx.x >> 5)) * static_cast<int64_t>(ck);
+      if (lane == 0)
+#pragma unroll
+        for (int r = 0; r < RED_MAXK; ++r)
+          if (r < ck) {
+            a.cand_s[at + r] = oo[r] >= 0 ? os[r] : 0.0;
+            a.cand_i[at + r] = oo[r];
+          }
+    }
   }
 }
 
@@ -1165,6 +1261,11 @@ int reduce_mode(const gift_fif_view* f, int V, int ma) {
   return f->n_local >= OWNER_MIN_SHAPES ? RM_OWNER : RM_RANGE;
 }
 
+// single-segment shapes of an ma == 1 query batch on fif_owner_fast_kernel
+bool owner_split(const gift_fif_view* f, int V, int ma) {
+  return ma == 1 && f->seg_single != nullptr && V <= 128;
+}
+
 int owner_nchunk(const gift_fif_view* f) {
   return static_cast<int>(max64(1, cdiv(max64(f->max_cell_segments, 1), OWN_CHUNK)));
 }
@@ -1249,7 +1350,7 @@ extern "C" int gift_fif_reduce_mode(const gift_fif_view* f, int32_t V, int32_t m
 extern "C" int gift_fif_score_ranges2(const gift_fif_view* f, int32_t V, int32_t ma) {
   const int mode = reduce_mode(f, V, ma);
   if (mode == RM_GATHER) return static_cast<int>(cdiv(max64(f->n_local, 1), gather_rs(f->n_local)));
-  if (mode == RM_OWNER) return V * ma * owner_nchunk(f) * OWN_WARPS;
+  if (mode == RM_OWNER) return V * ma * owner_nchunk(f) * OWN_WARPS * (owner_split(f, V, ma) ? 2 : 1);
   return gift_fif_score_ranges(f, V);
 }
 
@@ -1441,7 +1542,8 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
       ga.rs = 0;
       ga.chunk = OWN_CHUNK;
       ga.nchunk = owner_nchunk(f);
-      ga.n_ranges = V * ma * ga.nchunk * OWN_WARPS;
+      ga.split = owner_split(f, V, ma) ? 1 : 0;
+      ga.n_ranges = V * ma * ga.nchunk * OWN_WARPS * (ga.split ? 2 : 1);
       if (out_scores)
         GIFT_CUDA_TRY(cudaMemsetAsync(out_scores, 0, sizeof(double) * B * f->n_local, st));
       if (ga.cand_k > 0) {  // slots without work keep "no candidate"
@@ -1472,11 +1574,16 @@ extern "C" int gift_fif_score_ex2(const gift_fif_view* f, const float* Q, int32_
         fif_owner_reduce_kernel<4><<<grid, GR_THREADS, smem, st>>>(ga);
       }
       GIFT_LAUNCH_CHECK();
+      if (ga.split) {
+        fif_owner_fast_kernel<<<grid, GR_THREADS, 0, st>>>(ga);
+        GIFT_LAUNCH_CHECK();
+      }
       return GIFT_OK;
     }
     ga.rs = gather_rs(f->n_local);
     ga.n_ranges = static_cast<int>(cdiv(f->n_local, ga.rs));
     ga.chunk = ga.nchunk = 0;
+    ga.split = 0;
     // queries per CTA: GR_G, fewer when that leaves the GPU under-filled
     ga.G = GR_G;
     while (ga.G > 1 && ga.n_ranges * cdiv(B, ga.G) < 8LL * sm_count()) ga.G >>= 1;
