@@ -801,6 +801,9 @@ def _set_sif_mode(sif, args):
                        "bucket": nat.SIF_BUCKET}[args.sif]
 
 
+C5_LANES = 3  # config 5: S-IF query batches in flight (latency-bound kernels; 1..4: 401k, 468k, 488k, 478k q/s)
+
+
 def run_c5(args):
     """Config 5 (re-rank dominated): given top-50 lists for 1M shapes, S-IF
     over all shapes, queries re-ranked with k = 50 neighbour-set Jaccard.
@@ -850,12 +853,28 @@ def run_c5(args):
     if sharded:
         ms, clk = _timed_sharded(args, device, step, nsteps, local)
     else:
+        # batches in flight: batch i on lane stream i % L (each lane keeps its
+        # own S-IF workspace and accumulator rows), as query_many does
+        from paper_1604_01879_b200.index import lane_streams
+
+        n_lanes = max(1, args.lanes if args.lanes is not None else C5_LANES)
+        lanes = lane_streams(n_lanes)
+        main = torch.cuda.current_stream()
+
+        def run_lanes(indices):
+            for s in lanes:
+                s.wait_stream(main)
+            for n_, i in enumerate(indices):
+                with torch.cuda.stream(lanes[n_ % n_lanes]):
+                    step(i)
+            for s in lanes:
+                main.wait_stream(s)
+
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         with ClockSampler(local) as clk_s:
-            warm(lambda i: step(i % args.warmup), args.warmup)
+            warm(lambda i: run_lanes([i % args.warmup] * n_lanes), args.warmup)
             ev[0].record()
-            for i in range(args.warmup, nsteps):
-                step(i)
+            run_lanes(range(args.warmup, nsteps))
             ev[1].record()
             torch.cuda.synchronize()
         ms, clk = ev[0].elapsed_time(ev[1]), clk_s.summary()
@@ -870,12 +889,14 @@ def run_c5(args):
     k_out = c["top_k"]
     res = [(torch.empty((B, k_out), dtype=torch.int32, pin_memory=True),
             torch.empty((B, k_out), dtype=torch.float64, pin_memory=True)) for _ in host]
+    e_lanes = lanes if not sharded else [torch.cuda.current_stream()]
     t0 = time.perf_counter()
-    for (hi_, hv, hr), (ri, rv) in zip(host, res):
-        oi, ov = run_q(hi_.to(device, non_blocking=True), hv.to(device, non_blocking=True),
-                       hr.to(device, non_blocking=True))
-        ri.copy_(oi, non_blocking=True)
-        rv.copy_(ov, non_blocking=True)
+    for n_, ((hi_, hv, hr), (ri, rv)) in enumerate(zip(host, res)):
+        with torch.cuda.stream(e_lanes[n_ % len(e_lanes)]):  # copies and compute per lane
+            oi, ov = run_q(hi_.to(device, non_blocking=True), hv.to(device, non_blocking=True),
+                           hr.to(device, non_blocking=True))
+            ri.copy_(oi, non_blocking=True)
+            rv.copy_(ov, non_blocking=True)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     if sharded:
@@ -898,6 +919,7 @@ def run_c5(args):
                           "d2h_bytes_per_step": B * c["top_k"] * 12},
                          launches * args.steps, roof, cpu, clk,
                          {"build_s": build_s, "sif_postings": postings,
+                          "lanes": 1 if sharded else n_lanes,
                           "host_blocking_cuda_calls_per_step": syncs}, dtype="f64")
         print(json.dumps(line), flush=True)
     if sharded:
