@@ -8,6 +8,7 @@ Drop-in for the reference package `shapesearch` on that path: the public API
 
 from .features import FeatureFile, import_features, write_features
 from .index import (
+    GraphedQuery,
     IndexBundle,
     IndexConfig,
     build_index,
@@ -27,6 +28,7 @@ from .index import (
 )
 
 __all__ = [
+    "GraphedQuery",
     "FeatureFile",
     "import_features",
     "write_features",

@@ -166,3 +166,30 @@ def test_dense_cells_probe_major_scan(sim):
     other[0, 0, 3] += np.float32(1e-6)  # lo plane non-zero: no dense split
     mixed = mt.query_fif_batch(fif, np.concatenate([qs, other]), 1, sim).cpu().numpy()[:150]
     np.testing.assert_allclose(mixed, ref, rtol=RTOL, atol=1e-12, err_msg="mixed batch")
+
+
+@pytest.mark.parametrize("storage", ["float32", "float16"])
+def test_graphed_query_equals_eager(storage):
+    """The whole query pipeline captured in a CUDA graph (GraphedQuery) and
+    replayed on new batches returns exactly eng.run's rankings and scores
+    (every kernel graph-safe: no host synchronisation, device-side plan
+    sizes); fp16 storage includes dense cells (the probe-major scan)."""
+    N, V, d, K = 600, 8, 64, 3
+    views, _ = mixture_views(91, N, V, d, 5, n_queries=150)
+    db = views[:N].astype(np.float16 if storage == "float16" else np.float32)
+    qs = views[N:].astype(np.float16).astype(np.float32)
+    C = sampled_codebook(db.astype(np.float32), K, 2)
+    cfg = gift.IndexConfig(n_views=V, codebook_size=K, ma=1, k1=6, k2=3, imported=True,
+                           storage_dtype=storage, similarity="gaussian")
+    bundle = gift.build_index_from_views(db, shape_ids(N), cfg,
+                                         codebooks={"A": Codebook(C, "A"),
+                                                    "B": Codebook(C, "B")})
+    eng = bundle.engine
+    Q = torch.from_numpy(qs).to(dev())
+    batches = [Q[i:i + 50].contiguous() for i in (0, 50, 100)]
+    gq = gift.GraphedQuery(eng, batches[0], top_k=20)
+    for b in batches + batches[::-1]:
+        ei, ev = eng.run(b, top_k=20, rerank=True)
+        gi, gv = gq(b)
+        torch.cuda.synchronize()
+        assert torch.equal(ei, gi) and torch.equal(ev, gv)
