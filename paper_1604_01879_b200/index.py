@@ -12,8 +12,9 @@ pipelined queries, D6), and IndexConfig fields `similarity`, `sigma`,
 from __future__ import annotations
 
 import json
-import os
 import logging
+import os
+import threading
 import time
 from dataclasses import asdict, dataclass, field, fields, replace
 from pathlib import Path
@@ -662,6 +663,19 @@ _LANES: dict = {}
 LANE_RESERVE_SMS = 44  # config 2, 4 lanes, 3 runs each: 0 SMs ~40.6k, 20 41.2k, 28 41.9k, 36-64 42.2-42.5k q/s
 
 
+_PINNED: dict = {}
+
+
+def _pinned(tag: str, n: int, dtype) -> torch.Tensor:
+    """A grow-only pinned host buffer of at least n elements, kept per (tag,
+    calling thread)."""
+    key = (tag, threading.get_ident())
+    buf = _PINNED.get(key)
+    if buf is None or buf.numel() < n or buf.dtype != dtype:
+        buf = _PINNED[key] = torch.empty(max(n, 1), dtype=dtype, pin_memory=True)
+    return buf[:n]
+
+
 def lane_streams(n: int) -> list:
     """The first n persistent side streams of the current device (scratch
     buffers are kept per stream, so reusing the streams reuses them)."""
@@ -734,8 +748,11 @@ def query_many(bundle: IndexBundle, views_host: torch.Tensor, top_k: int = 10,
     bufs = [torch.empty((bs, V, d), dtype=torch.float32, device=dev) for _ in range(NB)]
     ready = [torch.cuda.Event() for _ in range(NB)]
     free = [torch.cuda.Event() for _ in range(NB)]
-    out_idx = torch.empty((Qn, k), dtype=torch.int32, pin_memory=True)
-    out_val = torch.empty((Qn, k), dtype=torch.float64, pin_memory=True)
+    # pinned result buffers are kept between calls (a pinned allocation is a
+    # host-blocking driver call of ~0.1-1 ms: config 1's whole batch time);
+    # the caller gets copies
+    out_idx = _pinned("idx", Qn * k, torch.int32).view(Qn, k)
+    out_val = _pinned("val", Qn * k, torch.float64).view(Qn, k)
     nb = (Qn + bs - 1) // bs
 
     def issue(i):
@@ -772,7 +789,7 @@ def query_many(bundle: IndexBundle, views_host: torch.Tensor, top_k: int = 10,
         main.wait_stream(c)
     eng.reserve_sms = prev_reserve
     main.synchronize()
-    return out_idx.numpy(), out_val.numpy()
+    return out_idx.numpy().copy(), out_val.numpy().copy()
 
 
 # ------------------------------------------------------------------ evaluation

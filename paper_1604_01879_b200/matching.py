@@ -31,6 +31,13 @@ def runner() -> eg.ScoreRunner:
     return r
 
 
+def release_workspaces() -> None:
+    """Drop the calling thread's scan launcher and its grow-only workspaces
+    (up to the compact buffer's pre-sized worst case per stream): call it
+    between large indexes so their HBM goes back to the allocator."""
+    _TLS.runner = None
+
+
 def sim_mode(similarity: str) -> int:
     if similarity == "cosine":
         return nat.SIM_COSINE

@@ -14,6 +14,8 @@
 Relative score errors (max, p99.99) are recorded through
 helpers.record_parity ($GIFT_PARITY_OUT; committed under profiles/)."""
 
+import gc
+
 import numpy as np
 import pytest
 import torch
@@ -34,6 +36,19 @@ from paper_1604_01879_b200 import synth  # noqa: E402
 from paper_1604_01879_b200.codebook import Codebook, quantize_batch  # noqa: E402
 
 SEED = 20160407  # bench.py's workload seed
+
+
+@pytest.fixture(autouse=True)
+def _free_hbm():
+    """Config-scale indexes take up to ~130 GB: release the previous test's
+    (reference cycles, the thread's scan workspaces, cached blocks) first."""
+    gc.collect()
+    mt.release_workspaces()
+    torch.cuda.empty_cache()
+    yield
+    gc.collect()
+    mt.release_workspaces()
+    torch.cuda.empty_cache()
 
 
 def dev():
@@ -150,7 +165,7 @@ def test_c1_exact_config_gaussian_against_oracle():
 
 
 # ------------------------------------------------------------------ C2
-@pytest.fixture(scope="module")
+@pytest.fixture(scope="class")
 def c2():
     w = synth.WORKLOADS["c2"]
     db, qs, _ = synth.mixture(w, SEED, dev())  # the bench's own workload (device generator)
@@ -167,55 +182,58 @@ def c2():
     torch.cuda.empty_cache()
 
 
-def test_c2_lists_bit_exact(c2):
-    orc, b = c2["orc"], c2["b"]
-    cell_off, post_ord = _gpu_lists(b)
-    np.testing.assert_array_equal(cell_off, orc.cell_off)
-    np.testing.assert_array_equal(post_ord, orc.post_ord)
-    d = c2["w"].dim
-    rows = torch.from_numpy(orc.rows).to(dev())
-    assert torch.equal(b.fifs["A"].dev.feat, c2["db"].reshape(-1, d)[rows])
-    # the 64 queries' multiple assignment (ma = 2), bit-exact
-    got = quantize_batch(Codebook(c2["C"]), c2["q"].reshape(-1, d), 2)
-    ref = scale.quantize_many_mt(c2["C"], c2["q_h"].reshape(-1, d), 2)
-    np.testing.assert_array_equal(got, ref)
+class TestC2:
+    """The C2 index lives for these three tests only (class-scoped fixture)."""
+
+    def test_c2_lists_bit_exact(self, c2):
+        orc, b = c2["orc"], c2["b"]
+        cell_off, post_ord = _gpu_lists(b)
+        np.testing.assert_array_equal(cell_off, orc.cell_off)
+        np.testing.assert_array_equal(post_ord, orc.post_ord)
+        d = c2["w"].dim
+        rows = torch.from_numpy(orc.rows).to(dev())
+        assert torch.equal(b.fifs["A"].dev.feat, c2["db"].reshape(-1, d)[rows])
+        # the 64 queries' multiple assignment (ma = 2), bit-exact
+        got = quantize_batch(Codebook(c2["C"]), c2["q"].reshape(-1, d), 2)
+        ref = scale.quantize_many_mt(c2["C"], c2["q_h"].reshape(-1, d), 2)
+        np.testing.assert_array_equal(got, ref)
 
 
-def test_c2_scores_64_queries_vs_oracle(c2):
-    w, orc = c2["w"], c2["orc"]
-    got = mt.query_fif_batch(c2["b"].fifs["A"], c2["q"], w.ma, "gaussian", w.sigma).cpu().numpy()
-    ref = orc.scores(c2["q_h"])
-    st = rel_err_stats(got, ref)
-    record_parity("c2", "fif_scores_gaussian_vs_oracle_64q_x_10k", st)
-    assert st["max"] <= RTOL and st["zero_mismatch"] == 0
+    def test_c2_scores_64_queries_vs_oracle(self, c2):
+        w, orc = c2["w"], c2["orc"]
+        got = mt.query_fif_batch(c2["b"].fifs["A"], c2["q"], w.ma, "gaussian", w.sigma).cpu().numpy()
+        ref = orc.scores(c2["q_h"])
+        st = rel_err_stats(got, ref)
+        record_parity("c2", "fif_scores_gaussian_vs_oracle_64q_x_10k", st)
+        assert st["max"] <= RTOL and st["zero_mismatch"] == 0
 
 
-def test_c2_self_join_sif_and_rankings(c2):
-    w, orc, b, ids = c2["w"], c2["orc"], c2["b"], c2["ids"]
-    raw_gpu = _raw_rows(b)
-    swaps = assert_topk_rows_close(raw_gpu, [(a.idx, a.val) for a in orc.raw])
-    vals = np.concatenate([v for _i, v in raw_gpu])
-    ref_vals = np.concatenate([a.val for a in orc.raw])
-    st = rel_err_stats(vals, ref_vals) if swaps == 0 else {"n": int(len(vals))}
-    record_parity("c2", "self_join_raw_activations_vs_oracle", {**st, "raw_swaps": swaps,
-                                                                 "rows": len(raw_gpu)})
-    raw_acts = _oracle_acts(raw_gpu)
-    final, sif = scale.build_context(raw_acts, _nbrs_from_raw(raw_gpu, w.k2))
-    _check_sif_against(b, final, sif)
-    ref_sc = orc.scores(c2["q_h"])
-    got = gift.query_batch(b, c2["q"], top_k=w.top_k)
-    pos = {s: i for i, s in enumerate(ids)}
-    agree = 0
-    for qi in range(ref_sc.shape[0]):
-        fin = scale.rerank_query(raw_acts, sif, ref_sc[qi], w.k2)
-        order = scale.rank_final(fin, ids, "query", w.top_k)
-        gi, gs = _rank_ids(got[qi], pos)
-        assert_ranking_close(gi, gs, order, fin[order])
-        # fully independent: the oracle's own raw activations and S-IF
-        fin2 = scale.rerank_query(orc.raw, orc.sif, ref_sc[qi], w.k2)
-        agree += int(list(scale.rank_final(fin2, ids, "query", w.top_k)) == gi)
-    record_parity("c2", "rankings_top100_64q", {"queries": int(ref_sc.shape[0]),
-                                                "identical_to_independent_oracle": agree})
+    def test_c2_self_join_sif_and_rankings(self, c2):
+        w, orc, b, ids = c2["w"], c2["orc"], c2["b"], c2["ids"]
+        raw_gpu = _raw_rows(b)
+        swaps = assert_topk_rows_close(raw_gpu, [(a.idx, a.val) for a in orc.raw])
+        vals = np.concatenate([v for _i, v in raw_gpu])
+        ref_vals = np.concatenate([a.val for a in orc.raw])
+        st = rel_err_stats(vals, ref_vals) if swaps == 0 else {"n": int(len(vals))}
+        record_parity("c2", "self_join_raw_activations_vs_oracle", {**st, "raw_swaps": swaps,
+                                                                     "rows": len(raw_gpu)})
+        raw_acts = _oracle_acts(raw_gpu)
+        final, sif = scale.build_context(raw_acts, _nbrs_from_raw(raw_gpu, w.k2))
+        _check_sif_against(b, final, sif)
+        ref_sc = orc.scores(c2["q_h"])
+        got = gift.query_batch(b, c2["q"], top_k=w.top_k)
+        pos = {s: i for i, s in enumerate(ids)}
+        agree = 0
+        for qi in range(ref_sc.shape[0]):
+            fin = scale.rerank_query(raw_acts, sif, ref_sc[qi], w.k2)
+            order = scale.rank_final(fin, ids, "query", w.top_k)
+            gi, gs = _rank_ids(got[qi], pos)
+            assert_ranking_close(gi, gs, order, fin[order])
+            # fully independent: the oracle's own raw activations and S-IF
+            fin2 = scale.rerank_query(orc.raw, orc.sif, ref_sc[qi], w.k2)
+            agree += int(list(scale.rank_final(fin2, ids, "query", w.top_k)) == gi)
+        record_parity("c2", "rankings_top100_64q", {"queries": int(ref_sc.shape[0]),
+                                                    "identical_to_independent_oracle": agree})
 
 
 # ------------------------------------------------------------------ C5

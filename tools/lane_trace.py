@@ -66,7 +66,11 @@ for a, b in zip(pts, pts[1:]):
             alone[n.split("(")[0][-40:]] += d / len(act)
     else:
         idle += d
+per_kernel = collections.Counter()
+for s_, e_, n in iv:
+    per_kernel[n.split("(")[0][-48:]] += (e_ - s_) / args.steps
 print(json.dumps({"config": w.name, "lanes": L, "steps": args.steps,
+                  "kernel_us_per_step": [[k, round(v, 1)] for k, v in per_kernel.most_common(16)],
                   "wall_us_per_step": (t1 - t0) / args.steps,
                   "scan_active_us_per_step": scan_t / args.steps,
                   "no_scan_busy_us_per_step": other_only / args.steps,
