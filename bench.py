@@ -258,6 +258,9 @@ def c5_config(c, n, parallelism):
 
 
 # ------------------------------------------------------------------ GPU arm
+GRAPH_CONFIGS = ("c1",)  # configs whose timed batches replay CUDA graphs by default
+
+
 def default_lanes(name):
     """(batches in flight, SMs the scan leaves to the other lanes) per config:
     config 2's non-scan kernels are ~20% of a step and overlap the next
@@ -471,7 +474,7 @@ def run_gift(args, w):
     """One index per rank: configs 1-2 at any N (replicas: disjoint query
     streams, no collective), other configs at N = 1."""
     from paper_1604_01879_b200 import query_many
-    from paper_1604_01879_b200.index import lane_streams
+    from paper_1604_01879_b200.index import GraphedQuery, lane_streams
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -493,7 +496,11 @@ def run_gift(args, w):
     # quantize / reduce / re-rank kernels overlap the other batch's scan
     lanes_default, reserve_default = default_lanes(w.name)
     L = max(1, args.lanes if args.lanes is not None else lanes_default)
-    lanes = [stream] if L == 1 else lane_streams(L)
+    # CUDA graphs: one replay per batch instead of ~34 launches from Python
+    # (config 1's L2-resident batches issue faster than Python launches them)
+    use_graph = args.graph == "on" or (args.graph == "auto" and w.name in GRAPH_CONFIGS)
+    # (graph capture needs a side stream, also with one lane)
+    lanes = [stream] if L == 1 and not use_graph else lane_streams(L)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     scan_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(args.steps)]
@@ -504,8 +511,14 @@ def run_gift(args, w):
     eng.reserve_sms = (args.reserve_sms if args.reserve_sms is not None
                        else (reserve_default if L > 1 else 0))
 
+    graphs = ([GraphedQuery(eng, batches[0], w.top_k, stream=s) for s in lanes]
+              if use_graph else None)
+
     def step(i, bi, sev=None):
         s = lanes[i % L]
+        if graphs is not None:
+            graphs[i % L](batches[bi])
+            return
         with torch.cuda.stream(s):
             eng.run(batches[bi], top_k=w.top_k, rerank=True, scan_events=sev)
 
@@ -537,8 +550,8 @@ def run_gift(args, w):
     # lane's scan: the kernel's own duration comes from the same batches run
     # one at a time right after, with the timed run's configuration (the same
     # SMs left to other lanes), inside the clock sampler's run
-    scan_in_flight = [a.elapsed_time(b) for a, b in scan_ev]
-    if L > 1:
+    scan_in_flight = [a.elapsed_time(b) for a, b in scan_ev] if graphs is None else None
+    if L > 1 or graphs is not None:
         serial_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                      for _ in range(args.steps)]
         for a, b in serial_ev:
@@ -563,12 +576,14 @@ def run_gift(args, w):
     host = torch.empty((args.steps * B, w.n_views, w.dim), dtype=torch.float32, pin_memory=True)
     for i in range(args.steps):
         host[i * B:(i + 1) * B].copy_(batches[order[args.warmup + i]])
-    query_many(bundle, host[:L * B], top_k=w.top_k, lanes=L, reserve_sms=eng.reserve_sms)  # warm
+    query_many(bundle, host[:L * B], top_k=w.top_k, lanes=L, reserve_sms=eng.reserve_sms,
+               graph=use_graph)  # warm
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    query_many(bundle, host, top_k=w.top_k, lanes=L, reserve_sms=eng.reserve_sms)
+    query_many(bundle, host, top_k=w.top_k, lanes=L, reserve_sms=eng.reserve_sms,
+               graph=use_graph)
     e2e_s = time.perf_counter() - t0
     t = torch.tensor([e2e_s], dtype=torch.float64, device=device)
     if ws > 1:
@@ -587,7 +602,8 @@ def run_gift(args, w):
                         "to other lanes)") if L > 1 else
                        "CUDA events around each scan launch inside the timed region",
                        q16=fp16_exact(batches[:4]))
-    roof["scan_ms_in_flight_avg"] = sum(scan_in_flight) / len(scan_in_flight)
+    roof["scan_ms_in_flight_avg"] = (sum(scan_in_flight) / len(scan_in_flight)
+                                     if scan_in_flight else None)
     roof["scan_share_of_step"] = scan_avg * args.steps / ms
     # lower bound independent of overlap: the scan's algorithmic bytes per
     # timed step (every step runs one scan) over the whole step time
@@ -609,6 +625,7 @@ def run_gift(args, w):
                          f"single channel, over the GPU-built lists)", "host": host_info()}
     if rank == 0:
         run = {"lanes": L, "scan_reserved_sms": eng.reserve_sms, "build_s": build_s,
+               "cuda_graph": bool(use_graph),
                "drain_kb": args.drain_kb or "default", "pair": args.pair,
                "host_blocking_cuda_calls_per_step": syncs,
                "features": ("planes only (streamed build)" if eng.fa.feat is None
@@ -1110,6 +1127,8 @@ def main():
                     help="F-IF scan on CTA pairs (cta_group::2): default per storage")
     ap.add_argument("--sif", default="auto", choices=["auto", "rows", "sort", "bucket"],
                     help="S-IF query implementation (default: by batch size)")
+    ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
+                    help="replay each lane's query pipeline as a CUDA graph (default: config 1)")
     ap.add_argument("--shard", action="store_true",
                     help="shard the database by shape over the ranks (default for configs "
                          "3-5 at N > 1)")

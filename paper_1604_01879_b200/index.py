@@ -209,6 +209,7 @@ class QueryEngine:
         # it while several batches are in flight)
         self.reserve_sms = 0
         self.mode = mt.sim_mode(cfg.similarity)
+        self._graphs = {}  # graph_for: captured pipelines per (stream, shape, ...)
 
     def scores(self, Qa, Qb=None, vq=None, vqb=None, stream=None, scan_events=None, ma=None):
         ma = self.cfg.ma if ma is None else ma
@@ -221,6 +222,16 @@ class QueryEngine:
                                self.cfg.sigma, vq=vq if vqb is None else vqb, stream=stream,
                                reserve_sms=self.reserve_sms)
         return sa, sb
+
+    def graph_for(self, stream, Q_example, top_k, rerank=True) -> "GraphedQuery":
+        """The CUDA graph of this engine's pipeline on `stream` for batches
+        shaped like Q_example (captured on first use, kept)."""
+        key = (stream.cuda_stream, tuple(Q_example.shape), int(top_k), bool(rerank),
+               int(self.reserve_sms))
+        g = self._graphs.get(key)
+        if g is None:
+            g = self._graphs[key] = GraphedQuery(self, Q_example, top_k, rerank, stream)
+        return g
 
     def rerank(self, sa, sb, stream=None):
         """index.py:249-258 for a batch of channel scores -> dense f64."""
@@ -721,14 +732,16 @@ class GraphedQuery:
 
 def query_many(bundle: IndexBundle, views_host: torch.Tensor, top_k: int = 10,
                rerank: bool = True, batch_size: int | None = None, lanes: int = 2,
-               reserve_sms: int | None = None):
+               reserve_sms: int | None = None, graph: bool = False):
     """Throughput API (new): queries from pinned host memory [Q, V, d] f32,
     processed in device batches on `lanes` compute streams, the host->device
     copy of the next batches overlapped with the compute on a copy stream.
     With lanes > 1 the scan leaves `reserve_sms` SMs (default
     LANE_RESERVE_SMS) to the other batches' kernels, which cannot share an SM
-    with a scan CTA (shared memory / TMEM).  Returns host (idx [Q, k] int32
-    global ordinals, val [Q, k] f64)."""
+    with a scan CTA (shared memory / TMEM).  graph: full batches replay a
+    CUDA graph of the pipeline per lane (`GraphedQuery`, captured on first
+    use and kept on the engine).  Returns host (idx [Q, k] int32 global
+    ordinals, val [Q, k] f64)."""
     eng = bundle.engine
     bs = batch_size or bundle.config.batch_size
     Qn, V, d = views_host.shape
@@ -779,7 +792,11 @@ def query_many(bundle: IndexBundle, views_host: torch.Tensor, top_k: int = 10,
         cs = comp[i % L]
         with torch.cuda.stream(cs):
             cs.wait_event(ready[s])
-            idx, val = eng.run(bufs[s][: b1 - b0], top_k=k, rerank=rerank)
+            if graph and b1 - b0 == bs:
+                gq = eng.graph_for(cs, bufs[s], k, rerank)
+                idx, val = gq(bufs[s])  # copies the batch into the graph's input
+            else:
+                idx, val = eng.run(bufs[s][: b1 - b0], top_k=k, rerank=rerank)
             free[s].record(cs)
             out_idx[b0:b1].copy_(idx, non_blocking=True)
             out_val[b0:b1].copy_(val, non_blocking=True)

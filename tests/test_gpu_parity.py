@@ -338,15 +338,19 @@ def test_sif_self_score_exactly_one_at_scale():
         assert sc[j, j] == 1.0
 
 
-@pytest.mark.parametrize("lanes,reserve", [(1, 0), (2, 0), (3, 20)])
-def test_query_many_pipelined_equals_batch(lanes, reserve):
+@pytest.mark.parametrize("lanes,reserve,graph", [(1, 0, False), (2, 0, False), (3, 20, False),
+                                                 (1, 0, True), (3, 20, True)])
+def test_query_many_pipelined_equals_batch(lanes, reserve, graph):
     """Batches in flight on 1-3 compute streams (own scratch each; the scan
-    optionally leaving SMs to the other lanes) return the serial results, bit
-    for bit."""
+    optionally leaving SMs to the other lanes; full batches optionally
+    replaying each lane's CUDA graph, the ragged last one eager) return the
+    serial results, bit for bit -- twice, so the second call replays the
+    graphs the first captured."""
     bundle, db, qs, ids, C = _e2e_bundle(E2E_CASES[2])
-    host = torch.from_numpy(np.concatenate([qs, db[:20]])).pin_memory()
-    idx, val = gift.query_many(bundle, host, top_k=30, batch_size=5, lanes=lanes,
-                               reserve_sms=reserve)
+    host = torch.from_numpy(np.concatenate([qs, db[:21]])).pin_memory()
+    for _ in range(2 if graph else 1):
+        idx, val = gift.query_many(bundle, host, top_k=30, batch_size=5, lanes=lanes,
+                                   reserve_sms=reserve, graph=graph)
     ref = gift.query_batch(bundle, host.numpy(), top_k=30)
     for r in range(len(ref)):
         assert [ids[i] for i in idx[r]] == [x[0] for x in ref[r]]
