@@ -266,10 +266,12 @@ def default_lanes(name):
     config 2's non-scan kernels are ~20% of a step and overlap the next
     batches' scans (profiles/r02/c2_lanes_reserve_sweep.json); configs 3 and 4
     (no host synchronisation left in the query path) gain 3% / 2% from two
-    lanes with 20 SMs left to the other lane."""
+    lanes with 20 SMs left to the other lane; config 1 replays CUDA graphs and
+    saturates at 6-8 lanes (profiles/r02/c1_graph_lanes_s4/: 4 lanes 890k,
+    8 lanes 1.01M q/s)."""
     from paper_1604_01879_b200.index import LANE_RESERVE_SMS
 
-    return {"c1": (4, LANE_RESERVE_SMS), "c2": (4, LANE_RESERVE_SMS),
+    return {"c1": (8, LANE_RESERVE_SMS), "c2": (4, LANE_RESERVE_SMS),
             "c3": (2, 20), "c4": (2, 20)}.get(name, (1, 0))
 
 
