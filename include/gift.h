@@ -411,6 +411,19 @@ int gift_exact_sets(const void* Q, int32_t qdtype, const int32_t* q_cnt, int32_t
                     int32_t Vq, const void* P, int32_t pdtype, const int32_t* p_cnt,
                     int32_t N, int32_t Vp, int32_t d, double* out, void* stream);
 
+/* ---- query_fif in f64 (matching.py:136-161), the opt-in exact-precision
+ * scan: Q [B, V, d] f32 query views, cells [B * V, ma] their probed cells
+ * (gift_quantize; < 0 or >= K: none), the F-IF's cell_off [K+1], post_ord [P]
+ * (global ordinals), f32 features [P, d]; out [B, n_local] f64 = per shape
+ * the mean over the V views of the best f64 similarity in the probed cells
+ * (all-zero views contribute 0).  ws: gift_fif_score_f64_ws_bytes(B, V,
+ * n_local) bytes (per-(view, shape) maxima). */
+size_t gift_fif_score_f64_ws_bytes(int32_t B, int32_t V, int64_t n_local);
+int gift_fif_score_f64(const float* Q, int32_t B, int32_t V, int32_t d, const int32_t* cells,
+                       int32_t ma, int32_t K, const int64_t* cell_off, const int32_t* post_ord,
+                       const float* feat, int64_t ord_base, int64_t n_local, int32_t mode,
+                       double sigma, void* ws, size_t ws_bytes, double* out, void* stream);
+
 /* ---- evaluation ranks: the 1-based positions evaluate_index /
  * exact_baseline_report give each relevant shape (index.py:317-357): for
  * each query row b of scores [B, N] and each rel[b, r] >= 0,

@@ -137,6 +137,10 @@ _SIGS = {
     "gift_exact_sets": (_c_i32, [_c_p, _c_i32, _c_p, _c_i32, _c_i32, _c_p, _c_i32, _c_p, _c_i32,
                                  _c_i32, _c_i32, _c_p, _c_p]),
     "gift_eval_ranks": (_c_i32, [_c_p, _c_i32, _c_i64, _c_p, _c_p, _c_p, _c_i32, _c_p, _c_p]),
+    "gift_fif_score_f64_ws_bytes": (_c_sz, [_c_i32, _c_i32, _c_i64]),
+    "gift_fif_score_f64": (_c_i32, [_c_p, _c_i32, _c_i32, _c_i32, _c_p, _c_i32, _c_i32, _c_p,
+                                    _c_p, _c_p, _c_i64, _c_i64, _c_i32, _c_dbl, _c_p, _c_sz,
+                                    _c_p, _c_p]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -11,6 +11,16 @@
 // (1 - x is monotone, so min_u (1 - x_u) = 1 - max_u x_u bit for bit.)  One
 // CTA per pair, a warp per query view, f64 FMA over d in lane-strided order.
 //
+// gift_fif_score_f64 is query_fif (matching.py:136-161) in f64 on CUDA cores:
+// for every query view that has a non-zero entry, every posting of its ma
+// probed cells, the f64 similarity of the f32 posting and the f32 query
+// (cosine: clip(q . p, 0, 1); gaussian: exp(-|q - p|^2 / sigma^2)), the
+// per-(view, shape) running max (np.maximum.at from zeros: an atomic max on
+// the bits of non-negative doubles), then per shape the view-order f64 sum
+// over the views divided by V (`total += view_best; total / V`).  A warp per
+// posting, f64 FMA over d.  The opt-in exact-precision path (the tensor-core
+// scan's contract is 1e-5 relative; this one is f64 rounding).
+//
 // gift_eval_ranks replaces the per-query lexsort of evaluate_index /
 // exact_baseline_report (index.py:317-357): for each query row of scores and
 // each of its relevant shapes j, rank(j) = 1 + #{i != self : key_i < key_j}
@@ -152,9 +162,94 @@ __global__ void __launch_bounds__(ER_THREADS)
     if (rb[s] < 0) out_rank[static_cast<int64_t>(b) * R + s] = -1;
 }
 
+constexpr int F64_THREADS = 256;
+
+__global__ void __launch_bounds__(F64_THREADS)
+    fif_f64_best_kernel(const float* __restrict__ Q, int d, const int32_t* __restrict__ cells,
+                        int ma, int K, const int64_t* __restrict__ cell_off,
+                        const int32_t* __restrict__ post_ord, const float* __restrict__ feat,
+                        int64_t ord_base, int64_t n_local, int mode, double inv_s2,
+                        unsigned long long* __restrict__ vb) {
+  const int64_t bv = blockIdx.x;
+  const float* q = Q + bv * d;
+  int any = 0;
+  for (int k = threadIdx.x; k < d; k += F64_THREADS) any |= q[k] != 0.0f;
+  if (!__syncthreads_or(any)) return;  // an all-zero view contributes 0 (matching.py:152)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned long long* row = vb + bv * n_local;
+  for (int a = 0; a < ma; ++a) {
+    const int c = cells[bv * ma + a];
+    if (c < 0 || c >= K) continue;
+    for (int64_t p = cell_off[c] + warp; p < cell_off[c + 1]; p += F64_THREADS / 32) {
+      const float* f = feat + p * d;
+      double acc = 0.0;
+      if (mode == GIFT_SIM_COSINE) {
+        for (int k = lane; k < d; k += 32)
+          acc = fma(static_cast<double>(q[k]), static_cast<double>(f[k]), acc);
+      } else {
+        for (int k = lane; k < d; k += 32) {
+          const double df = static_cast<double>(q[k]) - static_cast<double>(f[k]);
+          acc = fma(df, df, acc);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) {
+        const double sim = mode == GIFT_SIM_COSINE ? fmin(fmax(acc, 0.0), 1.0) : exp(-acc * inv_s2);
+        atomicMax(row + (post_ord[p] - ord_base),
+                  static_cast<unsigned long long>(__double_as_longlong(sim)));
+      }
+    }
+  }
+}
+
+__global__ void fif_f64_sum_kernel(const unsigned long long* __restrict__ vb, int B, int V,
+                                   int64_t n_local, double* __restrict__ out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= static_cast<int64_t>(B) * n_local) return;
+  const int64_t b = i / n_local, j = i - b * n_local;
+  double t = 0.0;
+  for (int v = 0; v < V; ++v)
+    t += __longlong_as_double(static_cast<long long>(vb[(b * V + v) * n_local + j]));
+  out[i] = t / static_cast<double>(V);
+}
+
 }  // namespace gift
 
 using namespace gift;
+
+extern "C" size_t gift_fif_score_f64_ws_bytes(int32_t B, int32_t V, int64_t n_local) {
+  if (B <= 0 || V <= 0 || n_local <= 0) return 0;
+  return static_cast<size_t>(B) * static_cast<size_t>(V) * static_cast<size_t>(n_local) *
+         sizeof(unsigned long long);
+}
+
+extern "C" int gift_fif_score_f64(const float* Q, int32_t B, int32_t V, int32_t d,
+                                  const int32_t* cells, int32_t ma, int32_t K,
+                                  const int64_t* cell_off, const int32_t* post_ord,
+                                  const float* feat, int64_t ord_base, int64_t n_local,
+                                  int32_t mode, double sigma, void* ws, size_t ws_bytes,
+                                  double* out, void* stream) {
+  GIFT_REQUIRE(mode == GIFT_SIM_COSINE || mode == GIFT_SIM_GAUSSIAN, GIFT_ERR_INVALID,
+               "unknown similarity mode %d", mode);
+  GIFT_REQUIRE(mode == GIFT_SIM_COSINE || sigma > 0.0, GIFT_ERR_INVALID, "sigma must be > 0");
+  GIFT_REQUIRE(d >= 1 && ma >= 1 && K >= 1, GIFT_ERR_INVALID, "bad f64 F-IF score shape");
+  if (B <= 0 || n_local <= 0) return GIFT_OK;
+  GIFT_REQUIRE(V >= 1, GIFT_ERR_EMPTY, "view set is empty");
+  GIFT_REQUIRE(ws_bytes >= gift_fif_score_f64_ws_bytes(B, V, n_local), GIFT_ERR_CAPACITY,
+               "f64 F-IF score workspace too small");
+  cudaStream_t st = as_stream(stream);
+  auto* vb = static_cast<unsigned long long*>(ws);
+  GIFT_CUDA_TRY(cudaMemsetAsync(vb, 0, gift_fif_score_f64_ws_bytes(B, V, n_local), st));
+  fif_f64_best_kernel<<<static_cast<unsigned>(static_cast<int64_t>(B) * V), F64_THREADS, 0, st>>>(
+      Q, d, cells, ma, K, cell_off, post_ord, feat, ord_base, n_local, mode,
+      mode == GIFT_SIM_GAUSSIAN ? 1.0 / (sigma * sigma) : 0.0, vb);
+  GIFT_LAUNCH_CHECK();
+  const int64_t n = static_cast<int64_t>(B) * n_local;
+  fif_f64_sum_kernel<<<static_cast<unsigned>(cdiv(n, 256)), 256, 0, st>>>(vb, B, V, n_local, out);
+  GIFT_LAUNCH_CHECK();
+  return GIFT_OK;
+}
 
 extern "C" int gift_exact_sets(const void* Q, int32_t qdtype, const int32_t* q_cnt, int32_t B,
                                int32_t Vq, const void* P, int32_t pdtype, const int32_t* p_cnt,

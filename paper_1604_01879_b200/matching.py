@@ -215,23 +215,60 @@ def _as_query_tensor(query_views, dim):
     return q.to(nat.device(), dtype=torch.float32)
 
 
+PRECISIONS = ("tc", "f64")
+
+
 def query_fif(fif: FirstInvertedFile, query_views, ma: int = DEFAULT_MA,
-              similarity: str = "cosine", sigma: float = 0.5) -> np.ndarray:
+              similarity: str = "cosine", sigma: float = 0.5,
+              precision: str = "tc") -> np.ndarray:
     """Approximate similarity of one query view set against every shape
     (matching.py:136-161).  Query views are scored as f32 (stored features
-    are f32); scores are f64."""
+    are f32); scores are f64.  precision "tc": the tensor-core scan (1e-5
+    relative, the throughput path); "f64": f64 similarities on CUDA cores
+    (f64 rounding: the reference's own arithmetic, for small indexes)."""
     q = _as_query_tensor(query_views, fif.dim)
-    s = runner().score(fif.dev, q[None], ma, sim_mode(similarity), sigma)
-    return s[0].cpu().numpy()
+    return query_fif_batch(fif, q[None], ma, similarity, sigma, precision=precision)[0].cpu().numpy()
 
 
 def query_fif_batch(fif: FirstInvertedFile, Q, ma: int = DEFAULT_MA, similarity: str = "cosine",
-                    sigma: float = 0.5, vq=None) -> torch.Tensor:
+                    sigma: float = 0.5, vq=None, precision: str = "tc") -> torch.Tensor:
     """Batched scores: Q [B, V, d] -> device f64 [B, n_local] (new API)."""
+    if precision not in PRECISIONS:
+        raise ValueError(f"precision must be one of {PRECISIONS}")
     if not torch.is_tensor(Q):
         Q = torch.from_numpy(np.ascontiguousarray(Q, dtype=np.float32))
     Q = Q.to(nat.device(), dtype=torch.float32)
+    if precision == "f64":
+        return score_f64(fif.dev, Q, ma, sim_mode(similarity), sigma)
     return runner().score(fif.dev, Q, ma, sim_mode(similarity), sigma, vq=vq)
+
+
+def score_f64(dev: eg.DeviceFif, Q: torch.Tensor, ma: int, mode: int, sigma: float,
+              stream=None) -> torch.Tensor:
+    """query_fif's arithmetic in f64 (libgift gift_fif_score_f64): the query
+    views' ma cells from the bit-exact quantizer, every probed posting's f64
+    similarity, per-(view, shape) max, view-order f64 sums / V."""
+    if Q.dim() != 3 or Q.shape[1] == 0:
+        raise EmptySet("view set is empty")
+    B, V, d = Q.shape
+    if d != dev.d:
+        raise DimensionMismatch(f"query dim {d} != index dim {dev.d}")
+    if not 1 <= ma <= dev.cb.K:
+        raise ValueError(f"ma must be in [1, {dev.cb.K}]")
+    if dev.feat is None or dev.feat.dtype != torch.float32:
+        raise ValueError("the f64 scan needs the index's f32 feature copy")
+    Q = Q.contiguous()
+    out = torch.empty((B, dev.n_local), dtype=torch.float64, device=Q.device)
+    if B == 0 or dev.n_local == 0:
+        return out.zero_()
+    cells = eg.quantize_rows(dev.cb, Q.view(-1, d), ma, stream=stream)
+    wsb = nat.lib().gift_fif_score_f64_ws_bytes(B, V, dev.n_local)
+    ws = torch.empty(wsb // 8, dtype=torch.int64, device=Q.device)
+    nat.call("gift_fif_score_f64", nat.ptr(Q), B, V, d, nat.ptr(cells), ma, dev.cb.K,
+             nat.ptr(dev.cell_off), nat.ptr(dev.post_ord), nat.ptr(dev.feat), dev.ord_base,
+             dev.n_local, mode, float(sigma), nat.ptr(ws), wsb, nat.ptr(out),
+             eg._sp(stream))
+    return out
 
 
 def save_fif(fif: FirstInvertedFile, path) -> None:

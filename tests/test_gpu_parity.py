@@ -157,6 +157,59 @@ def test_query_fif_degeneracy_and_bounds():
         assert (prev.argmax(axis=1) == np.arange(12)).all()  # self-retrieval
 
 
+@pytest.mark.parametrize("tag", ["k5", "k1"])
+def test_query_fif_f64_matches_reference_goldens(tag):
+    """precision="f64" (gift_fif_score_f64): the reference's own query_fif
+    scores to f64 rounding (1e-12 absolute, the reference's criterion-3
+    tolerance), at every ma including the ma = K degeneracy."""
+    g = load_golden("fif.npz")
+    db = g["db"]
+    ids = shape_ids(len(db))
+    fif = mt.build_fif(_viewsets(db, ids, ("A",)), Codebook(g[f"{tag}_C"], "A"), "A")
+    K = len(g[f"{tag}_entry_len"])
+    queries = list(g["queries"]) + list(db[:3])
+    for ma in sorted({1, min(2, K), K}):
+        got = np.stack([mt.query_fif(fif, q, ma, precision="f64") for q in queries])
+        np.testing.assert_allclose(got, g[f"{tag}_scores_ma{ma}"], rtol=0, atol=1e-12)
+        assert ((got == 0) == (g[f"{tag}_scores_ma{ma}"] == 0)).all()
+
+
+@pytest.mark.parametrize("similarity", ["cosine", "gaussian"])
+def test_query_fif_f64_vs_oracle(similarity):
+    """The f64 path against the oracle's f64 loops (zero query views, ma = 2,
+    config-1 dims): 1e-12 relative."""
+    views, _ = mixture_views(17, 120, 16, 256, 12, n_queries=4)
+    db, qs = views[:120], views[120:].copy()
+    qs[1, 3] = 0.0
+    C = sampled_codebook(db, 16, 3)
+    assign = oracle.quantize_many(C, db.reshape(-1, 256), 1).reshape(120, 16)
+    ref = oracle.build_fif(list(db), C, assign=assign)
+    fif = mt.build_fif_from_tensor(torch.from_numpy(db).to(dev()), Codebook(C), shape_ids(120))
+    got = mt.query_fif_batch(fif, qs, 2, similarity, precision="f64").cpu().numpy()
+    for q, gq in zip(qs, got):
+        cells = oracle.quantize_many(C, q.astype(np.float64), 2)
+        e = oracle.query_fif(ref, q, 2, similarity, cells=cells)
+        np.testing.assert_allclose(gq, e, rtol=1e-12, atol=1e-15)
+        assert ((gq == 0) == (e == 0)).all()
+    with pytest.raises(ValueError):
+        mt.query_fif_batch(fif, qs, 2, similarity, precision="bf16")
+
+
+def test_query_fif_f64_degeneracy_is_exact():
+    """K = 1 and ma = K: the f64 path equals the exact set similarity to
+    1e-12 (the reference's acceptance criterion 1 asks 1e-9)."""
+    rng = np.random.default_rng(5)
+    mats = np.stack([unit_nonneg_rows(rng, 6, 24) for _ in range(12)])
+    exact = np.array([[np.clip(q.astype(np.float64) @ p.astype(np.float64).T, 0, 1).max(1).mean()
+                       for p in mats] for q in mats])
+    C = sampled_codebook(mats, 5, 0)
+    for K in (1, 5):
+        fif = mt.build_fif_from_tensor(torch.from_numpy(mats).to(dev()), Codebook(C[:K]),
+                                       shape_ids(12))
+        s = mt.query_fif_batch(fif, mats, K, precision="f64").cpu().numpy()
+        np.testing.assert_allclose(s, exact, rtol=0, atol=1e-12)
+
+
 def test_zero_views_skipped_and_counted():
     rng = np.random.default_rng(8)
     mats = np.stack([unit_nonneg_rows(rng, 4, 16) for _ in range(5)])
