@@ -41,7 +41,7 @@ def fif_reserve_sms(n: int) -> int:
 
 
 def fif_drain_kb(n: int) -> int:
-    """GIFT_FIF_DRAIN_KB(n): flags bits 24-28 (1..16; 0 = the default 4)."""
+    """GIFT_FIF_DRAIN_KB(n): flags bits 24-28 (1..16; 0 = the library default, 8)."""
     return (int(n) & 31) << 24
 
 _c_i32 = ctypes.c_int32
@@ -214,10 +214,16 @@ class Workspace:
 
     def __init__(self):
         self._buf = None
+        self._captured = False  # a CUDA graph (GraphedQuery) addresses the buffer
+        self._retired = []
 
     def get(self, nbytes: int) -> torch.Tensor:
         nbytes = max(int(nbytes), 256)
+        if torch.cuda.is_current_stream_capturing():
+            self._captured = True
         if self._buf is None or self._buf.numel() < nbytes:
+            if self._buf is not None and self._captured:
+                self._retired.append(self._buf)  # the graph's kernels still use it
             self._buf = None
             self._buf = torch.empty(nbytes, dtype=torch.uint8, device=device())
         return self._buf

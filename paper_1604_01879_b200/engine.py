@@ -669,7 +669,12 @@ class DeviceSif:
         pool = self.__dict__.setdefault("_acc", {})
         key = _sp(stream)
         acc = pool.get(key)
+        if torch.cuda.is_current_stream_capturing():
+            self.__dict__["_acc_captured"] = True
         if acc is None or acc.shape[0] < want:
+            if acc is not None and self.__dict__.get("_acc_captured"):
+                # a captured CUDA graph still addresses the old rows
+                self.__dict__.setdefault("_acc_retired", []).append(acc)
             acc = torch.zeros((want, stride), dtype=torch.float64, device=self.norms.device)
             if stream is not None:
                 torch.cuda.current_stream().synchronize()  # zeroed before `stream` uses it
