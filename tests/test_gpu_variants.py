@@ -193,3 +193,28 @@ def test_graphed_query_equals_eager(storage):
         gi, gv = gq(b)
         torch.cuda.synchronize()
         assert torch.equal(ei, gi) and torch.equal(ev, gv)
+
+
+def test_graph_survives_scratch_regrowth_on_its_stream():
+    """A bigger eager batch on the graph's own stream regrows that stream's
+    scratch (grow-only caches); the buffers the graph captured stay alive, so
+    later replays still equal eager runs."""
+    N, V, d, K = 400, 8, 64, 3
+    views, _ = mixture_views(92, N, V, d, 5, n_queries=160)
+    db, qs = views[:N], views[N:]
+    C = sampled_codebook(db, K, 2)
+    cfg = gift.IndexConfig(n_views=V, codebook_size=K, ma=1, k1=6, k2=3, imported=True)
+    bundle = gift.build_index_from_views(db, shape_ids(N), cfg,
+                                         codebooks={"A": Codebook(C, "A"),
+                                                    "B": Codebook(C, "B")})
+    eng = bundle.engine
+    Q = torch.from_numpy(qs).to(dev())
+    small, big = Q[:20].contiguous(), Q[20:160].contiguous()
+    gq = gift.GraphedQuery(eng, small, top_k=15)
+    with torch.cuda.stream(gq.stream):
+        eng.run(big, top_k=15, rerank=True)  # regrows the stream's scratch
+    for b in (Q[40:60].contiguous(), small):
+        ei, ev = eng.run(b, top_k=15, rerank=True)
+        gi, gv = gq(b)
+        torch.cuda.synchronize()
+        assert torch.equal(ei, gi) and torch.equal(ev, gv)
