@@ -548,7 +548,10 @@ constexpr int SB_MAX_R = 2048;  // buckets per query (split kernel counters)
 constexpr int SB_MAX_E = 1024;  // query support entries staged in shared memory
 constexpr int SB_MIN_RB = 11;   // 2^11 shapes (16 KB of f64) per reducing warp
 constexpr int SB_MAX_RB = 13;
-constexpr int SB_U = 4;        // chunks of 32 pairs in flight per lane
+#ifndef GIFT_SB_U
+#define GIFT_SB_U 4
+#endif
+constexpr int SB_U = GIFT_SB_U;  // chunks of 32 pairs in flight per lane
 
 // exclusive scan of a[0, n) in place (all threads of the CTA); returns the total
 __device__ int32_t block_scan_excl(int32_t* a, int n, int32_t* wsum) {
