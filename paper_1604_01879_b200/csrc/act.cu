@@ -546,7 +546,22 @@ __global__ void sif_fill_kernel(const uint32_t* __restrict__ keys, const int64_t
 constexpr int SB_WARPS = 16;
 constexpr int SB_MAX_R = 2048;  // buckets per query (split kernel counters)
 constexpr int SB_MAX_E = 1024;  // query support entries staged in shared memory
-constexpr int SB_MIN_RB = 11;   // 2^11 shapes (16 KB of f64) per reducing warp
+// Bucket width and the reduce's occupancy (config 5, 1M shapes, 3 lanes;
+// profiles/r02/c5_bucket_sweep_s4.txt): 2^11-shape buckets with one 13-warp
+// CTA per SM 484k q/s; 2^10 with 2 / 3 / 4 CTAs per SM 516k / 517k / 524k;
+// 2^9 (the split's per-bucket counters grow) 447-454k.
+#ifndef GIFT_SB_MIN_RB
+#define GIFT_SB_MIN_RB 10
+#endif
+#ifndef GIFT_SB_RED_KB
+#define GIFT_SB_RED_KB 69
+#endif
+#ifndef GIFT_SB_RED_CTAS
+#define GIFT_SB_RED_CTAS 3
+#endif
+constexpr int SB_MIN_RB = GIFT_SB_MIN_RB;  // 2^10 shapes (8 KB of f64) per reducing warp
+constexpr int SB_RED_KB = GIFT_SB_RED_KB;      // shared accumulators per reducing CTA
+constexpr int SB_RED_CTAS = GIFT_SB_RED_CTAS;  // reducing CTAs per SM
 constexpr int SB_MAX_RB = 13;
 #ifndef GIFT_SB_U
 #define GIFT_SB_U 4
@@ -1248,12 +1263,14 @@ extern "C" int gift_sif_query_topk(const int64_t* e_off, const int32_t* e_ord, c
         q_idx, q_val, q_cnt, cap, B, e_off, e_ord, e_val, n_global, rb, R, off, bst, pj, pc);
     GIFT_LAUNCH_CHECK();
     const int W = 1 << rb;
-    const int rw = static_cast<int>(min64(16, (208 * 1024) / (static_cast<int64_t>(W) * 8)));
+    const int rw =
+        static_cast<int>(min64(16, (SB_RED_KB * 1024) / (static_cast<int64_t>(W) * 8)));
     const size_t rsm = static_cast<size_t>(rw) * W * 8;
     GIFT_CUDA_TRY(cudaFuncSetAttribute(sif_bucket_reduce_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(rsm)));
-    const int64_t grid = min64(sm_count(), cdiv(static_cast<int64_t>(B) * R, rw * 4));
+    const int64_t grid =
+        min64(static_cast<int64_t>(sm_count()) * SB_RED_CTAS, cdiv(static_cast<int64_t>(B) * R, rw * 4));
     sif_bucket_reduce_kernel<<<static_cast<unsigned>(grid), rw * 32, rsm, st>>>(pj, pc, off, bst, B,
                                                                                R, rb, ntb);
     GIFT_LAUNCH_CHECK();
