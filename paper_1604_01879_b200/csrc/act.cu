@@ -1010,6 +1010,13 @@ __global__ void __launch_bounds__(RK_THREADS)
     __syncthreads();
     bitonic_sort_desc_n(xs, xt, xj, N);
   };
+  // the best-so-far plus survivors, sorted over the next power of two only
+  // (the sorts are most of this kernel's instructions)
+  auto pow2_at_least = [](int x) {
+    int N = 2;
+    while (N < x) N <<= 1;
+    return N;
+  };
   if (ntot <= RK_BUF) {
     int N = 2;
     while (N < ntot || N < k) N <<= 1;
@@ -1032,7 +1039,7 @@ __global__ void __launch_bounds__(RK_THREADS)
       const int free = RK_BUF - RK_BEST - cnt;
       if (free < 4 * RK_THREADS) {  // make room: keep the best RK_BEST
         __syncthreads();
-        pad_sort(RK_BEST + cnt, RK_BUF);
+        pad_sort(RK_BEST + cnt, pow2_at_least(RK_BEST + cnt));
         if (key_better(xs[k - 1], xt[k - 1], th_s, th_t)) {
           th_s = xs[k - 1];
           th_t = xt[k - 1];
@@ -1070,7 +1077,7 @@ __global__ void __launch_bounds__(RK_THREADS)
       t0 += span;
       __syncthreads();
     }
-    pad_sort(RK_BEST + s_cnt, RK_BUF);
+    pad_sort(RK_BEST + s_cnt, pow2_at_least(RK_BEST + s_cnt));
   }
   for (int i = tid; i < k; i += RK_THREADS) {
     const bool ok = xj[i] >= 0;
