@@ -988,6 +988,24 @@ __global__ void owner_count_kernel(const int32_t* __restrict__ cells,
 // the top-k2 merge downstream takes OWN_WARPS times more candidates)
 constexpr int OWN_WARPS = GR_THREADS / 32;
 
+// The probe of work item w: the largest p with work_off[p] <= w, given the
+// answer `from` for an earlier item (a few steps forward, else a binary
+// search over the rest) -- a CTA's items ascend.
+__device__ __forceinline__ int64_t work_probe(const int64_t* __restrict__ work_off,
+                                              int64_t nprobes, int64_t w, int64_t from) {
+#pragma unroll 1
+  for (int step = 0; step < 4; ++step) {
+    if (from + 1 >= nprobes || work_off[from + 1] > w) return from;
+    ++from;
+  }
+  int64_t lo = from, hi = nprobes - 1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) >> 1;
+    if (work_off[mid] <= w) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
 // Latency-bound (dependent gathers per pair): 4 CTAs per SM with one slot
 // word (64 registers, some spills; config 4: 3.3 -> 2.1 ms per batch), 3 with
 // more (80 registers for the larger probed-cell cache; config 3: 0.69 ->
@@ -1007,14 +1025,11 @@ __global__ void __launch_bounds__(GR_THREADS, W >= 2 ? 3 : OWN_CTAS1) fif_owner_
   const int64_t per = (n_work + gridDim.x - 1) / gridDim.x;
   const int64_t w0 = static_cast<int64_t>(blockIdx.x) * per;
   const int64_t w1 = min64(n_work, w0 + per);
+  int64_t pr = 0;
   for (int64_t w = w0; w < w1; ++w) {
-  // probe of work item w: largest p with work_off[p] <= w
-  int64_t lo = 0, hi = nprobes - 1;
-  while (lo < hi) {
-    const int64_t mid = (lo + hi + 1) >> 1;
-    if (a.work_off[mid] <= w) lo = mid; else hi = mid - 1;
-  }
-  const int64_t pr = lo;
+  // probe of work item w: largest p with work_off[p] <= w (items ascend, so
+  // it is at or after the previous item's)
+  pr = work_probe(a.work_off, nprobes, w, pr);
   const int b = static_cast<int>(pr / slots), j = static_cast<int>(pr - static_cast<int64_t>(b) * slots);
   const int chunk_id = static_cast<int>(w - a.work_off[pr]);
   const int64_t cand_at =
@@ -1105,13 +1120,9 @@ __global__ void __launch_bounds__(GR_THREADS) fif_owner_fast_kernel(GatherArgs a
   const int64_t per = (n_work + gridDim.x - 1) / gridDim.x;
   const int64_t w0 = static_cast<int64_t>(blockIdx.x) * per;
   const int64_t w1 = min64(n_work, w0 + per);
+  int64_t pr = 0;
   for (int64_t w = w0; w < w1; ++w) {
-    int64_t lo = 0, hi = nprobes - 1;  // probe of work item w
-    while (lo < hi) {
-      const int64_t mid = (lo + hi + 1) >> 1;
-      if (a.work_off[mid] <= w) lo = mid; else hi = mid - 1;
-    }
-    const int64_t pr = lo;
+    pr = work_probe(a.work_off, nprobes, w, pr);  // probe of work item w
     const int b = static_cast<int>(pr / slots), j = static_cast<int>(pr - static_cast<int64_t>(b) * slots);
     const int chunk_id = static_cast<int>(w - a.work_off[pr]);
     const int c = a.cells[pr];
