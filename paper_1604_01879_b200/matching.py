@@ -216,6 +216,7 @@ def _as_query_tensor(query_views, dim):
 
 
 PRECISIONS = ("tc", "f64")
+F64_WS_BYTES = 1 << 30  # score_f64: workspace per chunk of queries
 
 
 def query_fif(fif: FirstInvertedFile, query_views, ma: int = DEFAULT_MA,
@@ -262,12 +263,20 @@ def score_f64(dev: eg.DeviceFif, Q: torch.Tensor, ma: int, mode: int, sigma: flo
     if B == 0 or dev.n_local == 0:
         return out.zero_()
     cells = eg.quantize_rows(dev.cb, Q.view(-1, d), ma, stream=stream)
-    wsb = nat.lib().gift_fif_score_f64_ws_bytes(B, V, dev.n_local)
-    ws = torch.empty(wsb // 8, dtype=torch.int64, device=Q.device)
-    nat.call("gift_fif_score_f64", nat.ptr(Q), B, V, d, nat.ptr(cells), ma, dev.cb.K,
-             nat.ptr(dev.cell_off), nat.ptr(dev.post_ord), nat.ptr(dev.feat), dev.ord_base,
-             dev.n_local, mode, float(sigma), nat.ptr(ws), wsb, nat.ptr(out),
-             eg._sp(stream))
+    # the per-(view, shape) maxima take V n_local 8 bytes per query: queries
+    # go in chunks of at most F64_WS_BYTES of them
+    lib = nat.lib()
+    per_q = max(1, lib.gift_fif_score_f64_ws_bytes(1, V, dev.n_local))
+    bc = max(1, min(B, F64_WS_BYTES // per_q))
+    ws = torch.empty(-(-lib.gift_fif_score_f64_ws_bytes(bc, V, dev.n_local) // 8),
+                     dtype=torch.int64, device=Q.device)
+    for b0 in range(0, B, bc):
+        nb = min(bc, B - b0)
+        wsb = lib.gift_fif_score_f64_ws_bytes(nb, V, dev.n_local)
+        nat.call("gift_fif_score_f64", nat.ptr(Q[b0:b0 + nb]), nb, V, d,
+                 nat.ptr(cells[b0 * V:(b0 + nb) * V]), ma, dev.cb.K, nat.ptr(dev.cell_off),
+                 nat.ptr(dev.post_ord), nat.ptr(dev.feat), dev.ord_base, dev.n_local, mode,
+                 float(sigma), nat.ptr(ws), wsb, nat.ptr(out[b0:b0 + nb]), eg._sp(stream))
     return out
 
 

@@ -193,6 +193,14 @@ def test_query_fif_f64_vs_oracle(similarity):
         assert ((gq == 0) == (e == 0)).all()
     with pytest.raises(ValueError):
         mt.query_fif_batch(fif, qs, 2, similarity, precision="bf16")
+    # queries in workspace-bounded chunks (one query per chunk here): the same
+    old_ws = mt.F64_WS_BYTES
+    try:
+        mt.F64_WS_BYTES = 1
+        chunked = mt.query_fif_batch(fif, qs, 2, similarity, precision="f64").cpu().numpy()
+    finally:
+        mt.F64_WS_BYTES = old_ws
+    np.testing.assert_array_equal(chunked, got)
 
 
 def test_query_fif_f64_degeneracy_is_exact():
