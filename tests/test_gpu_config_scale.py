@@ -208,6 +208,26 @@ class TestC2:
         assert st["max"] <= RTOL and st["zero_mismatch"] == 0
 
 
+    def test_c2_scores_64_queries_cosine_and_f64_vs_oracle(self, c2):
+        """The same index and 64 queries through the cosine kernel (the
+        reference's own similarity, matching.py:158) and through the f64 path
+        (precision="f64", 8 queries), against the oracle's f64 scores."""
+        w, orc = c2["w"], c2["orc"]
+        B, V, d = c2["q_h"].shape
+        qc = scale.quantize_many_mt(c2["C"], c2["q_h"].reshape(B * V, d), w.ma).reshape(B, V, w.ma)
+        qc = np.where(c2["q_h"].any(axis=2)[:, :, None], qc, -1)
+        ref = scale.fif_scores_many(orc.cell_off, orc.post_ord, orc.feat_rows, c2["q_h"], qc,
+                                    w.n_shapes, "cosine")
+        got = mt.query_fif_batch(c2["b"].fifs["A"], c2["q"], w.ma, "cosine").cpu().numpy()
+        st = rel_err_stats(got, ref)
+        record_parity("c2", "fif_scores_cosine_vs_oracle_64q_x_10k", st)
+        assert st["max"] <= RTOL and st["zero_mismatch"] == 0
+        got64 = mt.query_fif_batch(c2["b"].fifs["A"], c2["q"][:8], w.ma, "cosine",
+                                   precision="f64").cpu().numpy()
+        np.testing.assert_allclose(got64, ref[:8], rtol=1e-12, atol=1e-15)
+        record_parity("c2", "fif_scores_cosine_f64_path_vs_oracle_8q_x_10k",
+                      rel_err_stats(got64, ref[:8]))
+
     def test_c2_self_join_sif_and_rankings(self, c2):
         w, orc, b, ids = c2["w"], c2["orc"], c2["b"], c2["ids"]
         raw_gpu = _raw_rows(b)
