@@ -674,16 +674,18 @@ _LANES: dict = {}
 LANE_RESERVE_SMS = 44  # config 2, 4 lanes, 3 runs each: 0 SMs ~40.6k, 20 41.2k, 28 41.9k, 36-64 42.2-42.5k q/s
 
 
-_PINNED: dict = {}
+_PINNED = threading.local()
 
 
 def _pinned(tag: str, n: int, dtype) -> torch.Tensor:
-    """A grow-only pinned host buffer of at least n elements, kept per (tag,
-    calling thread)."""
-    key = (tag, threading.get_ident())
-    buf = _PINNED.get(key)
+    """A grow-only pinned host buffer of at least n elements, kept per tag in
+    the calling thread (released with the thread)."""
+    bufs = getattr(_PINNED, "bufs", None)
+    if bufs is None:
+        bufs = _PINNED.bufs = {}
+    buf = bufs.get(tag)
     if buf is None or buf.numel() < n or buf.dtype != dtype:
-        buf = _PINNED[key] = torch.empty(max(n, 1), dtype=dtype, pin_memory=True)
+        buf = bufs[tag] = torch.empty(max(n, 1), dtype=dtype, pin_memory=True)
     return buf[:n]
 
 
