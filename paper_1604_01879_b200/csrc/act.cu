@@ -1189,6 +1189,12 @@ static bool sif_bucket_ok(int32_t cap, int64_t max_touched, int64_t n_local) {
          sif_split_smem(cap, static_cast<int>(cdiv(n_local, 1LL << rb))) <= 200 * 1024;
 }
 
+// The sort-based path sizes its pair buffers for B x max_touched (44 B per
+// pair plus radix scratch); past 2^26 pairs (~3 GB) a hub-skewed bound would
+// reserve far more than the real touch count needs, so those batches take the
+// accumulator-row kernel instead (by default; GIFT_SIF_SORT still forces it).
+constexpr int64_t SORT_MAX_PAIRS = 1LL << 26;
+
 static bool sif_sort_ok(int64_t B, int64_t n_local) {
   int bbits = 1, jbits = 1;
   while ((1LL << bbits) < B) ++bbits;
@@ -1205,7 +1211,8 @@ static SifMode sif_mode(int64_t B, int32_t cap, int64_t max_touched, int64_t n_l
   if (flags) return SIF_MODE_ROWS;  // a forced mode outside its limits
   if (B * max_touched < (1LL << 24)) return SIF_MODE_ROWS;
   if (sif_bucket_ok(cap, max_touched, n_local)) return SIF_MODE_BUCKET;
-  return sif_sort_ok(B, n_local) ? SIF_MODE_SORT : SIF_MODE_ROWS;
+  return (sif_sort_ok(B, n_local) && B * max_touched <= SORT_MAX_PAIRS) ? SIF_MODE_SORT
+                                                                     : SIF_MODE_ROWS;
 }
 
 extern "C" int gift_sif_query_topk(const int64_t* e_off, const int32_t* e_ord, const double* e_val,
